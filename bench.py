@@ -1,0 +1,359 @@
+"""Benchmark of the nuGPR training hot path on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3]
+
+A "step" is one pass of the whole hot path (every row of SURVEY §8(a) except the one-off
+clustering A0): one epoch of Algorithm 1 at config C3 (n=100,000, d=8,
+n_c=500 clusters of 200, RBF, m=8 probes): build the preconditioner at theta (A1), the 2p+1 = 7
+perturbed MLL evaluations of the central-difference gradient (A2-A8), Adam (A9).
+value = MLL+num-grad evaluations per second (7 per step) over all ranks; PAR-1 shards the 7
+evaluations of a step across ranks (strong scaling: the work per step is fixed).
+
+--impl reference times the FP64 CPU oracle (oracle/, the only other place this script runs it)
+on the same config and metric, each step a bounded sample (one of the 7 evaluations in turn,
+plus the build every 7th step).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "MLL+num-grad evals/sec (n=100k, C3)"
+UNIT = "evals/s"
+CONFIG_DESC = {
+    "C1": "n=1000 d=2 n_c=10 b=100 RBF m=8",
+    "C2": "n=20000 d=8 n_c=100 b=200 RBF m=8",
+    "C3": "n=100000 d=8 n_c=500 b=200 RBF m=8",
+    "C5": "n=1000000 d=4 n_c=2000 b=500 RBF m=8",
+}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, copy)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except (FileNotFoundError, OSError):
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                smax.append(float(f[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def init_dist(backend):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1:
+        return 0, 1, 0
+    import torch.distributed as dist
+    rank = int(os.environ["RANK"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    dist.init_process_group(backend=backend)
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------- oracle timing
+def oracle_sample(ds, probe_seed, evals_sel):
+    """Time the oracle (as it stands) on the chosen evaluations of one epoch."""
+    from oracle.mll import central_perturbations, mll as omll
+    from oracle.structured import build_blocks as obuild
+    Z = synth.probes(probe_seed, 8, ds.n)
+    pts, _ = central_perturbations(ds.theta0, (1e-3,) * 3)
+    t0 = time.perf_counter()
+    bo = obuild(ds.X, ds.offsets, ds.reps, ds.theta0)
+    t_build = time.perf_counter() - t0
+    times = {}
+    for k in evals_sel:
+        t0 = time.perf_counter()
+        omll(bo, ds.y, pts[k], Z)
+        times[k] = time.perf_counter() - t0
+    return t_build, times
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        return max([i.get("num_threads", 1) for i in info] or [1])
+    except Exception:  # noqa: BLE001
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(ds, probe_seed):
+    """Oracle epoch rate estimated from a bounded sample: the build plus one evaluation of each
+    operator mode (baseline, noise, scale, generic), extrapolated to the 7 evaluations."""
+    t_build, t = oracle_sample(ds, probe_seed, [0, 3, 5, 1])
+    epoch = t_build + t[0] + 2 * t[3] + 2 * t[5] + 2 * t[1]
+    return {"value": 7.0 / epoch, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+            "sample": (f"1 build + 4 of the 7 evaluations (one per mode: baseline, noise, scale, "
+                       f"lengthscale) at {ds.meta.get('config')}, extrapolated to one epoch of 7; "
+                       f"measured {t_build + sum(t.values()):.1f} s, est. epoch {epoch:.1f} s"),
+            "host_cores": os.cpu_count()}
+
+
+def run_reference(args):
+    rank, world, _ = init_dist("gloo")
+    if rank != 0:
+        return
+    ds = synth.make_config(args.config)
+    seed = ds.meta["probe_seed"]
+    from oracle.mll import central_perturbations, mll as omll
+    from oracle.structured import build_blocks as obuild
+    Z = synth.probes(seed, 8, ds.n)
+    pts, _ = central_perturbations(ds.theta0, (1e-3,) * 3)
+    state = {"bo": None}
+
+    def step(k):
+        if k % 7 == 0 or state["bo"] is None:
+            state["bo"] = obuild(ds.X, ds.offsets, ds.reps, ds.theta0)
+        omll(state["bo"], ds.y, pts[k % 7], Z)
+
+    for k in range(args.warmup):
+        step(k)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        step(k)
+    dt = time.perf_counter() - t0
+    value = args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": f"{args.config}: {CONFIG_DESC[args.config]}; reference step = one of "
+                               "the 7 central-difference MLL evaluations in turn (+ build every 7th)",
+                   "parallelism": "cpu-oracle"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": blas_threads(), "kind": "oracle",
+                         "sample": f"{args.steps} timed evaluations after {args.warmup} warm-up"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    rank, world, local = init_dist("nccl")
+    torch.cuda.set_device(local)
+    import paper_2510_12128_b200 as P
+    P._native.lib()
+    ds = synth.make_config(args.config)
+    seed = ds.meta["probe_seed"]
+    dev = torch.device("cuda", local)
+    Xd = torch.tensor(ds.X, device=dev)
+    yd = torch.tensor(ds.y, device=dev)
+    rd = torch.tensor(ds.reps, device=dev)
+    group = True if world > 1 else None
+    ctx = P.Context(local, group=group)
+    ws = torch.empty(P.workspace_size(ds.offsets, ds.n_c, ds.d, args.eval_slots), dtype=torch.uint8,
+                     device=dev)
+    stream = torch.cuda.current_stream(local)
+    state = np.zeros(10)
+    state[:3] = ds.theta0
+
+    def step(st, X, y, reps):
+        st2, rec = P.train(ctx, X, ds.offsets, reps, y, None, epochs=1, adam_state=st, workspace=ws,
+                           probe_seed=seed, num_probes=8)
+        return st2, rec
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up
+    st = state.copy()
+    for _ in range(args.warmup):
+        st, _ = step(st, Xd, yd, rd)
+    torch.cuda.synchronize()
+    barrier()
+    # timed region (device-resident inputs)
+    clocks = ClockSampler(local)
+    clocks.start()
+    ctx.set_profiling(True)
+    n0 = P.launch_count()
+    st = state.copy()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    barrier()
+    ev0.record(stream)
+    recs = []
+    for _ in range(args.steps):
+        st, rec = step(st, Xd, yd, rd)
+        recs.append(rec[0])
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms = ev0.elapsed_time(ev1)
+    launches = P.launch_count() - n0
+    prof = ctx.profile()
+    ctx.set_profiling(False)
+    clk = clocks.stop()
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = 7.0 * args.steps / (ms * 1e-3)
+    # e2e: the same public call with HOST buffers (inputs staged H2D inside, records read back)
+    Xh, yh, rh = ds.X, ds.y, ds.reps
+    st = state.copy()
+    step(st, Xh, yh, rh)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        st, _ = step(st, Xh, yh, rh)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    ms_e2e = max(e0.elapsed_time(e1), 1e3 * (time.perf_counter() - t0))
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+    h2d = ds.X.nbytes + ds.y.nbytes + ds.reps.nbytes
+    d2h = 7 * 128 + 4 * ds.n_c + 16 + 8 * 10
+    # roofline of the dominant kernel: the fused apply with a block term
+    peak, peak_src = peaks()
+    a_ms, a_bytes, a_n = prof["apply_B"]
+    achieved = (a_bytes / (a_ms * 1e-3)) / 1e9 if a_ms > 0 else None
+    traffic = None
+    tp = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tp):
+        try:
+            traffic = json.load(open(tp)).get(args.config, {}).get("apply_B_dram_bytes_per_launch")
+        except Exception:  # noqa: BLE001
+            traffic = None
+    total_prof_ms = sum(v[0] for v in prof.values())
+    shares = {k: round(v[0] / total_prof_ms, 4) for k, v in prof.items() if total_prof_ms > 0}
+    if rank != 0:
+        return
+    kys = [int(r[7]) for r in recs]
+    kqs = [int(r[8]) for r in recs]
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {
+            "workload": f"{args.config}: {CONFIG_DESC[args.config]}; step = one Algorithm-1 epoch "
+                        "(build preconditioner + 7-point central-difference gradient + Adam)",
+            "n": ds.n, "n_c": ds.n_c, "b": int(ds.offsets[1]), "d": ds.d, "m": 8,
+            "parallelism": f"perturbation-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs larger than L2: per step the preconditioner Linv + H + G(lambda+-) stream "
+                  f"{3 * 8 * ds.n * int(ds.offsets[1]) / 1e6:.0f} MB (> 126 MB L2)",
+            "train_time_50_epochs_s": 50 * ms / args.steps / 1e3,
+            "peak_hbm_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+            "dense_n2_f64_gb": 8.0 * ds.n * ds.n / 1e9,
+            "cg_iters_y_max": max(kys), "cg_iters_q_max": max(kqs),
+            "eval_slots": args.eval_slots,
+        },
+        "clocks": clk,
+        "gpu_launches": int(launches),
+        "roofline": {
+            "kernel": "apply_kernel (fused multi-RHS block matvec + low-rank correction, mode with B)",
+            "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+            "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+            "launches": int(a_n), "avg_launch_us": 1e3 * a_ms / a_n if a_n else None,
+            "bytes_per_launch": a_bytes / a_n if a_n else None, "peak_source": peak_src,
+            "step_share": shares,
+        },
+        "e2e": {"value": 7.0 * args.steps / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h)},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(ds, seed)
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--eval-slots", type=int, default=1)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

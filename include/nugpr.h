@@ -1,0 +1,217 @@
+/*
+ * nugpr.h — C-ABI of the B200-native nuGPR training hot path (arXiv 2510.12128).
+ *
+ * The library (libnugpr.so, hand-written sm_100a CUDA) evaluates the negative marginal
+ * log-likelihood of a GP on clustered inputs (Eq. 3, lines 59-62) with the
+ * paper's structured covariance K'' (Eq. 28), the block-Cholesky
+ * preconditioner R (Eq. 12-13), batched multi-RHS PCG (PAPER.md:107-108,
+ * 124), the Hutchinson / 2-2 Pade log-determinant (Eq. 9-10, 16)
+ * plus an SLQ estimate from the same CG coefficients, the 2p+1 finite-difference gradient
+ * (Eq. 11) and Algorithm 1.
+ *
+ * Conventions (apply to every call unless stated otherwise)
+ *  - Pointers are DEVICE pointers on the context's device unless marked [host].  Inputs
+ *    marked [host|device] may be either; host buffers are staged through the workspace
+ *    (that copy is part of the call).  Arrays are contiguous, FP64, row-major, 8-byte
+ *    aligned; clusters are contiguous: rows [offsets[i], offsets[i+1]) belong to cluster i
+ *    ("partitioned into n_c clusters"; uneven sizes allowed, reading X4/P19).
+ *  - Ownership: the caller owns every array and the single workspace buffer (allocate
+ *    nugpr_workspace_size() bytes, e.g. a torch uint8 tensor).  Handles (nugpr_ctx,
+ *    nugpr_blocks) are small host objects; a blocks handle points into the workspace and
+ *    must be destroyed before the workspace is freed.  The library never calls cudaMalloc.
+ *  - Streams: all device work is enqueued on the context stream.  Calls with [host]
+ *    outputs synchronise that stream before returning; nugpr_build_blocks does too (it
+ *    reads back the per-block factorisation status for the jitter ladder).
+ *  - Errors: every call returns nugpr_status; nugpr_last_error() gives a thread-local
+ *    message for the last failing call.  No call aborts the process.
+ *  - Determinism: identical inputs give bit-identical outputs (fixed-order reductions,
+ *    no floating-point atomics).
+ */
+#ifndef NUGPR_H
+#define NUGPR_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Exported symbols keep default visibility even when the library is built with
+ * -fvisibility=hidden. */
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define NUGPR_MAX_PROBES 15   /* columns per apply = 1 (y) + m probes <= 16 */
+#define NUGPR_NUM_EVALS 7     /* 2p+1 with p = 3 hyperparameters */
+
+typedef enum {
+  NUGPR_OK = 0,
+  NUGPR_ERR_INVALID_ARG = 1,      /* theta <= 0, d < 1, bad enum, NULL pointer, misalignment */
+  NUGPR_ERR_SHAPE = 2,            /* offsets not strictly increasing / offsets[0]!=0 / offsets[n_c]!=n, block too large */
+  NUGPR_ERR_NOT_SPD = 3,          /* a diagonal block failed Cholesky after the jitter ladder */
+  NUGPR_ERR_DEGENERATE_REPS = 4,  /* lambda_0 = lambda_min(K_rep) <= 0 (Eq. 26 needs lambda_0 > 0) */
+  NUGPR_ERR_CG_NOT_CONVERGED = 5, /* cg_max_iter reached ("flag any instances"); outputs hold the last iterate */
+  NUGPR_ERR_WORKSPACE = 6,        /* workspace too small */
+  NUGPR_ERR_CUDA = 7,
+  NUGPR_ERR_COMM = 8,             /* the allgather callback failed */
+  NUGPR_ERR_INTERNAL = 9,
+  NUGPR_ERR_UNSUPPORTED = 10
+} nugpr_status;
+
+typedef enum {
+  NUGPR_RBF = 0,            /* alpha*exp(-||x-x'||^2/(2 lambda^2)) — Eq. 2 with the square (reading X3/P1) */
+  NUGPR_MATERN52 = 1,       /* alpha*(1+sqrt5 r/l+5r^2/(3l^2))exp(-sqrt5 r/l) (config C4) */
+  NUGPR_RBF_AS_PRINTED = 2  /* Eq. 2 literally: alpha*exp(-||x-x'||_2/(2 lambda^2)) */
+} nugpr_kernel;
+
+typedef enum { NUGPR_LOGDET_PADE = 0, NUGPR_LOGDET_SLQ = 1 } nugpr_logdet_mode;
+typedef enum { NUGPR_GRAD_CENTRAL = 0, NUGPR_GRAD_FORWARD_HALVING = 1 } nugpr_grad_mode;
+typedef enum { NUGPR_REP_GIVEN = 0, NUGPR_REP_CENTROID = 1, NUGPR_REP_MEDOID = 2 } nugpr_rep_mode;
+
+/* Operator mode chosen by comparing theta with the theta_0 the blocks were built at
+ * (Eq. 23-25). */
+typedef enum { NUGPR_MODE_BASELINE = 0, NUGPR_MODE_NOISE = 1, NUGPR_MODE_SCALE = 2,
+               NUGPR_MODE_GENERIC = 3 } nugpr_mode;
+
+/* theta = (lambda, sigma^2, alpha); all > 0. */
+typedef struct { double lengthscale, noise, outputscale; } nugpr_theta;
+
+typedef struct {
+  double cg_tol;               /* residual threshold on the split system, absolute (0.01) */
+  int32_t cg_max_iter;         /* 2000 */
+  int32_t num_probes;          /* m, Hutchinson vectors (8); 1..NUGPR_MAX_PROBES */
+  uint64_t probe_seed;         /* splitmix64 counter stream (see synth.probes) when probes == NULL */
+  const double* probes;        /* NULL, or device m x n matrix of +-1 in cluster-sorted order */
+  const int32_t* replay_iters; /* [host] NULL, or 1+m iteration counts to run exactly (parity replay) */
+  int32_t logdet_mode;         /* nugpr_logdet_mode used for L */
+  int32_t reserved;
+} nugpr_solve_cfg;
+
+typedef struct {
+  int32_t mode;                /* nugpr_grad_mode */
+  int32_t max_halvings;        /* FORWARD_HALVING cap (20) */
+  double step[3];              /* CENTRAL: relative h_i = step_i*theta_i (1e-3); HALVING: relative Delta_0 (0.1) */
+  double threshold;            /* FORWARD_HALVING threshold (1e-3) */
+  int32_t threshold_relative;  /* 1: |g-g_prev| < thr*max(1,|g|) (reading P13); 0: absolute (paper literal) */
+  int32_t reserved;
+} nugpr_grad_cfg;
+
+/* One MLL evaluation record (Alg. 1 ComputeLoss). */
+typedef struct {
+  double L;            /* 1/2 (quad + logdet + n log 2pi), Eq. 3 */
+  double quad;         /* y^T K''^{-1} y = c^T A^{-1} c, c = R^{-T} y */
+  double logdet;       /* logdet_pade or logdet_slq per logdet_mode */
+  double logdet_pade;  /* Eq. 16 with the Pade trace */
+  double logdet_slq;   /* Eq. 16 with the SLQ trace from the Q(A)-CG coefficients */
+  double logdet_R;     /* 2 sum log|R_i| */
+  double lambda0;      /* lambda_min(K_rep(theta)) */
+  double resid_y;      /* final ||r|| of the y column */
+  double resid_q_max;  /* max final ||r|| over probe columns */
+  int32_t iters_y;
+  int32_t iters_q_max;
+  int32_t iters_q[16];
+  int32_t converged;   /* 1 if every column met cg_tol (or replay ran) */
+  int32_t mode;        /* nugpr_mode */
+} nugpr_mll_out;
+
+typedef struct nugpr_ctx nugpr_ctx;
+typedef struct nugpr_blocks nugpr_blocks;
+
+/* Allgather used for perturbation sharding across ranks: gathers `bytes` from every rank
+ * into recv (world*bytes, rank order).  Returns 0 on success.  Supplied by the caller
+ * (the Python binding routes it through torch.distributed, NCCL on GPU boxes). */
+typedef int (*nugpr_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
+
+const char* nugpr_version(void);
+const char* nugpr_last_error(void);
+
+/* Context on `device`, enqueuing on `cuda_stream` (cudaStream_t; NULL = legacy default). */
+nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world, nugpr_ctx** out);
+nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void* user);
+nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
+
+/* Kernel-class profiler (bench.py's live roofline): when enabled, CUDA events are recorded on
+ * the context stream around every launch of a class; accumulators reset on (re-)enable.
+ * cls: 0 apply with a block term (noise/scale/generic), 1 apply without (baseline), 2 CG update,
+ *      3 rhs/init, 4 block GEMMs (H, G), 5 Cholesky+inverse, 6 Lanczos lambda_0, 7 other.
+ * ms: summed event time; bytes: summed ALGORITHMIC bytes (apply classes only: 8*(sum b_i^2 +
+ * 2 n c + n + n_c^2) per launch with a block term, 8*(2 n c + n + n_c^2) without);
+ * launches: number of timed launches. */
+nugpr_status nugpr_ctx_set_profiling(nugpr_ctx* ctx, int32_t enable);
+nugpr_status nugpr_ctx_profile(nugpr_ctx* ctx, int32_t cls, double* ms, double* bytes, int64_t* launches);
+/* Total kernel launches issued by the library in this process. */
+int64_t nugpr_launch_count(void);
+
+/* Workspace bytes for blocks built on `offsets` ([host], n_c+1) plus `eval_slots` (1..7)
+ * evaluation scratch sets (up to NUGPR_MAX_PROBES probes, cg_max_iter < 4096).  More slots
+ * let nugpr_numgrad keep several evaluations in flight; nugpr_build_blocks uses as many as
+ * fit in the bytes it is given. */
+nugpr_status nugpr_workspace_size(const int64_t* offsets, int32_t n_c, int32_t d,
+                                  int32_t eval_slots, size_t* bytes);
+
+/* A1 — Alg. 1 line 264 at theta0: K_i assembled on the fly from X_sorted, R_i = chol(K_i)
+ * with the jitter ladder, logdet_R, u_i = R_i^{-T} 1, H_i = R_i^{-T} R_i^{-1}, K_rep,
+ * lambda_0, M = K_rep - lambda_0 I.
+ *  X_sorted [host|device] n x d, offsets [host] n_c+1, reps [host|device] n_c x d.
+ *  failed_block [host]: -1, or the block index on NUGPR_ERR_NOT_SPD.
+ *  max_jitter [host]: largest jitter added (0 if none). */
+nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets,
+                                int32_t n_c, int32_t d, const double* reps, int32_t kernel,
+                                nugpr_theta theta0, void* workspace, size_t ws_bytes,
+                                nugpr_blocks** out, int32_t* failed_block, double* max_jitter);
+nugpr_status nugpr_blocks_destroy(nugpr_blocks* blocks);
+
+/* Debug read-back of block data into a [host] buffer of `bytes` (tests only).
+ *  what: 0 Linv (packed per block as ld_i x ld_i col-major, padded), 1 H (same layout),
+ *        2 u (n, cluster-sorted order), 3 jitter (n_c), 4 scalars {logdet_R, lambda0},
+ *        5 M (n_c x n_c), 6 ld (int32 n_c), 7 the probe matrix generated for seed/num_probes
+ *        of the last nugpr_mll call (m x n). */
+nugpr_status nugpr_blocks_export(const nugpr_blocks* blocks, int32_t what, void* dst, size_t bytes);
+
+/* A2-A7 — one MLL evaluation (Alg. 1 ComputeLoss) at theta with the blocks built at theta0.
+ *  y_sorted [host|device] n.  out [host]. */
+nugpr_status nugpr_mll(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y_sorted,
+                       nugpr_theta theta, const nugpr_solve_cfg* cfg, nugpr_mll_out* out);
+
+/* A8 — numerical gradient at theta (= the blocks' theta0).  CENTRAL: 7 evaluations
+ * theta, theta +- h_i e_i, g_i = (L+ - L-)/(2 h_i), sharded over the context's ranks
+ * (perturbation parallel; results exchanged with the allgather callback).
+ * FORWARD_HALVING: Alg. 1 lines 266-278 (rank-local).  evals [host]: NULL or room for
+ * max(7, 1+3*(max_halvings+1)) records; n_evals [host]: number written. */
+nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y_sorted,
+                           nugpr_theta theta, const nugpr_grad_cfg* gcfg,
+                           const nugpr_solve_cfg* scfg, double* L0, double grad[3],
+                           nugpr_mll_out* evals, int32_t* n_evals);
+
+/* A9 — Algorithm 1: for each epoch build blocks at theta, numgrad, Adam (gamma = lr,
+ * beta = (0.9, 0.999), eps = 1e-8, theta clamped >= 1e-8).
+ *  adam_state [host] in/out: theta[3], m[3], v[3], t (10 doubles); resumable.
+ *  records [host] epochs x NUGPR_TRAIN_RECORD doubles:
+ *    {L0, g[3], theta[3] (before the step), iters_y_max, iters_q_max, jitter, n_evals, reserved} */
+#define NUGPR_TRAIN_RECORD 12
+nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets,
+                         int32_t n_c, int32_t d, const double* reps, const double* y_sorted,
+                         int32_t kernel, int32_t epochs, double lr, const nugpr_grad_cfg* gcfg,
+                         const nugpr_solve_cfg* scfg, double adam_state[10], double* records,
+                         void* workspace, size_t ws_bytes);
+
+/* Host-only helpers (no device work; usable without a GPU). */
+/* One Adam step on state {theta[3], m[3], v[3], t}. */
+nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr);
+/* Longest-processing-time assignment of n tasks with costs to `world` ranks: owner[n]. */
+nugpr_status nugpr_shard_plan(int32_t world, const double* costs, int32_t n, int32_t* owner);
+/* Symmetric tridiagonal eigen-decomposition (implicit QL) returning eigenvalues and first
+ * eigenvector components; the SLQ kernel's routine, exported for host-side tests. */
+nugpr_status nugpr_tridiag_eig(int32_t k, const double* diag, const double* off,
+                               double* evals, double* first);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NUGPR_H */

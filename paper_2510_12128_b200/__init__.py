@@ -1,0 +1,336 @@
+"""paper_2510_12128_b200 — B200-native nuGPR MLL hot path (arXiv 2510.12128).
+
+Thin Python binding over the C-ABI of libnugpr.so (include/nugpr.h): argument marshalling
+only.  Every step of the MLL evaluation runs in the library's sm_100a CUDA kernels; PyTorch
+provides device memory (the workspace tensor), the stream and the process group.
+
+    ctx = Context(device=0)
+    blocks = build_blocks(ctx, X_sorted, offsets, reps, theta0, kernel="rbf")   # row A1
+    rec = mll(ctx, blocks, y_sorted, theta)                                      # rows A2-A7
+    L0, g, evals = numgrad(ctx, blocks, y_sorted, theta)                         # row A8
+    state, records = train(ctx, X_sorted, offsets, reps, y_sorted, theta0)      # row A9
+"""
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as N
+from ._native import NugprError
+
+__all__ = ["Context", "Blocks", "build_blocks", "mll", "numgrad", "train", "adam_step",
+           "shard_plan", "tridiag_eig", "workspace_size", "NugprError", "version"]
+
+
+def version() -> str:
+    return N.lib().nugpr_version().decode()
+
+
+def launch_count() -> int:
+    """Kernel launches issued by libnugpr.so in this process."""
+    return int(N.lib().nugpr_launch_count())
+
+
+def _ptr(x, keep):
+    """Pointer to a float64/int64 C-contiguous torch tensor (any device) or numpy array."""
+    if x is None:
+        return None
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if not x.is_contiguous():
+                raise ValueError("tensor must be contiguous")
+            keep.append(x)
+            return x.data_ptr()
+    except ImportError:  # pragma: no cover
+        pass
+    a = np.ascontiguousarray(x)
+    keep.append(a)
+    return a.ctypes.data
+
+
+def _f64(x):
+    try:
+        import torch
+        if isinstance(x, torch.Tensor):
+            if x.dtype != torch.float64:
+                raise TypeError("expected float64 tensor")
+            return x.contiguous()
+    except ImportError:  # pragma: no cover
+        pass
+    return np.ascontiguousarray(x, dtype=np.float64)
+
+
+def _theta(t):
+    return N.Theta(float(t[0]), float(t[1]), float(t[2]))
+
+
+class Context:
+    """nugpr_ctx on one device, enqueuing on torch's current stream of that device.
+
+    group: an initialised torch.distributed process group (or True for the default group)
+    enables perturbation sharding in numgrad/train via the allgather callback."""
+
+    def __init__(self, device: int = 0, stream=None, group=None):
+        import torch
+        self.device = int(device)
+        if stream is None:
+            stream = torch.cuda.current_stream(self.device)
+        self.stream = stream
+        self.rank, self.world = 0, 1
+        self.group = None
+        if group is not None:
+            import torch.distributed as dist
+            self.group = None if group is True else group
+            self.rank = dist.get_rank(self.group)
+            self.world = dist.get_world_size(self.group)
+        h = C.c_void_p()
+        N.check(N.lib().nugpr_ctx_create(self.device, C.c_void_p(stream.cuda_stream), self.rank,
+                                         self.world, C.byref(h)))
+        self.handle = h
+        self._cb = None
+        if self.world > 1:
+            self._cb = N.ALLGATHER_FN(self._allgather)
+            N.check(N.lib().nugpr_ctx_set_allgather(self.handle, self._cb, None))
+
+    def _allgather(self, send, nbytes, recv, user):
+        try:
+            import torch
+            import torch.distributed as dist
+            backend = dist.get_backend(self.group)
+            dev = torch.device("cuda", self.device) if backend == "nccl" else torch.device("cpu")
+            src = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8).to(dev)
+            out = torch.empty(self.world * nbytes, dtype=torch.uint8, device=dev)
+            dist.all_gather_into_tensor(out, src, group=self.group)
+            data = out.cpu().numpy().tobytes()
+            C.memmove(recv, data, len(data))
+            return 0
+        except Exception:  # noqa: BLE001 — reported to C as a status
+            return 1
+
+    def set_profiling(self, enable: bool = True):
+        N.check(N.lib().nugpr_ctx_set_profiling(self.handle, int(bool(enable))))
+
+    def profile(self) -> dict:
+        """{class: (ms, algorithmic_bytes, launches)} accumulated since set_profiling(True)."""
+        out = {}
+        for name, cls in N.PROF_CLASSES.items():
+            ms, by, n = C.c_double(), C.c_double(), C.c_int64()
+            N.check(N.lib().nugpr_ctx_profile(self.handle, cls, C.byref(ms), C.byref(by), C.byref(n)))
+            out[name] = (ms.value, by.value, n.value)
+        return out
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.lib().nugpr_ctx_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+def workspace_size(offsets, n_c: int, d: int, eval_slots: int = 1) -> int:
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    out = C.c_size_t()
+    N.check(N.lib().nugpr_workspace_size(off.ctypes.data, int(n_c), int(d), int(eval_slots), C.byref(out)))
+    return int(out.value)
+
+
+class Blocks:
+    """nugpr_blocks handle + the torch workspace it lives in."""
+
+    def __init__(self, ctx, handle, ws, offsets, d, theta0, kernel, jitter, failed):
+        self.ctx, self.handle, self.workspace = ctx, handle, ws
+        self.offsets = offsets
+        self.n = int(offsets[-1])
+        self.n_c = int(offsets.shape[0] - 1)
+        self.d = d
+        self.theta0 = tuple(float(t) for t in theta0)
+        self.kernel = kernel
+        self.max_jitter = jitter
+
+    def export(self, what: str):
+        """Debug read-back (tests): 'linv', 'H', 'u', 'jitter', 'scalars', 'M', 'ld', 'probes'."""
+        codes = {"linv": 0, "H": 1, "u": 2, "jitter": 3, "scalars": 4, "M": 5, "ld": 6, "probes": 7}
+        ld = np.zeros(self.n_c, dtype=np.int32)
+        N.check(N.lib().nugpr_blocks_export(self.handle, 6, ld.ctypes.data, ld.nbytes))
+        if what == "ld":
+            return ld
+        if what in ("linv", "H"):
+            tot = int(np.sum(ld.astype(np.int64) ** 2))
+            buf = np.empty(tot)
+            N.check(N.lib().nugpr_blocks_export(self.handle, codes[what], buf.ctypes.data, buf.nbytes))
+            out, pos = [], 0
+            for i in range(self.n_c):
+                l = int(ld[i])
+                b = int(self.offsets[i + 1] - self.offsets[i])
+                blk = buf[pos:pos + l * l].reshape(l, l).T          # col-major -> [row, col]
+                out.append(blk[:b, :b].copy())
+                pos += l * l
+            return out
+        sizes = {"u": self.n, "jitter": self.n_c, "scalars": 2, "M": self.n_c * self.n_c}
+        if what == "probes":
+            raise ValueError("use export_probes(m)")
+        buf = np.empty(sizes[what])
+        N.check(N.lib().nugpr_blocks_export(self.handle, codes[what], buf.ctypes.data, buf.nbytes))
+        return buf.reshape(self.n_c, self.n_c) if what == "M" else buf
+
+    def export_probes(self, m: int):
+        buf = np.empty((m, self.n))
+        N.check(N.lib().nugpr_blocks_export(self.handle, 7, buf.ctypes.data, buf.nbytes))
+        return buf
+
+    def close(self):
+        if getattr(self, "handle", None):
+            N.lib().nugpr_blocks_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # pragma: no cover
+            pass
+
+
+def build_blocks(ctx: Context, X_sorted, offsets, reps, theta0, kernel: str = "rbf",
+                 eval_slots: int = 1, workspace=None) -> Blocks:
+    """Row A1 (Alg. 1): preconditioner, u_i, H_i, K_rep, lambda_0 at theta0."""
+    import torch
+    keep = []
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    X = _f64(X_sorted)
+    n_c, d = off.shape[0] - 1, int(X.shape[1])
+    nbytes = workspace_size(off, n_c, d, eval_slots)
+    if workspace is None:
+        workspace = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", ctx.device))
+    h = C.c_void_p()
+    fb = C.c_int32(-1)
+    jit = C.c_double(0.0)
+    st = N.lib().nugpr_build_blocks(ctx.handle, _ptr(X, keep), off.ctypes.data, n_c, d,
+                                    _ptr(_f64(reps), keep), N.KERNELS[kernel], _theta(theta0),
+                                    C.c_void_p(workspace.data_ptr()), workspace.numel(), C.byref(h),
+                                    C.byref(fb), C.byref(jit))
+    N.check(st)
+    return Blocks(ctx, h, workspace, off, d, theta0, kernel, jit.value, fb.value)
+
+
+def _solve_cfg(num_probes=8, tol=0.01, max_iter=2000, probe_seed=0, probes=None, replay=None,
+               logdet="pade", keep=None):
+    cfg = N.SolveCfg()
+    cfg.cg_tol = float(tol)
+    cfg.cg_max_iter = int(max_iter)
+    cfg.num_probes = int(num_probes)
+    cfg.probe_seed = int(probe_seed) & 0xFFFFFFFFFFFFFFFF
+    cfg.probes = _ptr(_f64(probes), keep) if probes is not None else None
+    if replay is not None:
+        r = np.ascontiguousarray(replay, dtype=np.int32)
+        keep.append(r)
+        cfg.replay_iters = r.ctypes.data
+    cfg.logdet_mode = {"pade": 0, "slq": 1}[logdet]
+    return cfg
+
+
+def _rec(o: N.MllOut, m: int) -> dict:
+    return dict(L=o.L, quad=o.quad, logdet=o.logdet, logdet_pade=o.logdet_pade,
+                logdet_slq=o.logdet_slq, logdet_R=o.logdet_R, lambda0=o.lambda0,
+                resid_y=o.resid_y, resid_q_max=o.resid_q_max, iters_y=o.iters_y,
+                iters_q=[o.iters_q[j] for j in range(m)], iters_q_max=o.iters_q_max,
+                converged=bool(o.converged), mode=N.MODES.get(o.mode, o.mode))
+
+
+def mll(ctx: Context, blocks: Blocks, y_sorted, theta, **solve) -> dict:
+    """Rows A2-A7: one MLL evaluation (Alg. 1 ComputeLoss) at theta."""
+    keep = []
+    cfg = _solve_cfg(keep=keep, **solve)
+    out = N.MllOut()
+    N.check(N.lib().nugpr_mll(ctx.handle, blocks.handle, _ptr(_f64(y_sorted), keep), _theta(theta),
+                              C.byref(cfg), C.byref(out)))
+    return _rec(out, cfg.num_probes)
+
+
+def _grad_cfg(mode="central", step=None, threshold=1e-3, threshold_relative=True, max_halvings=20):
+    g = N.GradCfg()
+    g.mode = {"central": 0, "forward_halving": 1}[mode]
+    if step is None:
+        step = (1e-3, 1e-3, 1e-3) if mode == "central" else (0.1, 0.1, 0.1)
+    for i in range(3):
+        g.step[i] = float(step[i])
+    g.threshold = float(threshold)
+    g.threshold_relative = int(bool(threshold_relative))
+    g.max_halvings = int(max_halvings)
+    return g
+
+
+def numgrad(ctx: Context, blocks: Blocks, y_sorted, theta, mode="central", step=None,
+            threshold=1e-3, threshold_relative=True, max_halvings=20, **solve):
+    """Row A8: numerical gradient (CENTRAL 2p+1 = 7 evaluations, or FORWARD_HALVING)."""
+    keep = []
+    scfg = _solve_cfg(keep=keep, **solve)
+    gcfg = _grad_cfg(mode, step, threshold, threshold_relative, max_halvings)
+    L0 = C.c_double()
+    g = (C.c_double * 3)()
+    cap = 1 + 3 * 21
+    evals = (N.MllOut * cap)()
+    ne = C.c_int32(0)
+    N.check(N.lib().nugpr_numgrad(ctx.handle, blocks.handle, _ptr(_f64(y_sorted), keep), _theta(theta),
+                                  C.byref(gcfg), C.byref(scfg), C.byref(L0), g, evals, C.byref(ne)))
+    return L0.value, np.array(list(g)), [_rec(evals[k], scfg.num_probes) for k in range(ne.value)]
+
+
+def train(ctx: Context, X_sorted, offsets, reps, y_sorted, theta0, epochs=50, lr=0.05,
+          kernel="rbf", adam_state=None, mode="central", step=None, threshold=1e-3,
+          threshold_relative=True, max_halvings=20, eval_slots=1, workspace=None, **solve):
+    """Row A9: Algorithm 1 (build blocks, numerical gradient, Adam) for `epochs` epochs."""
+    import torch
+    keep = []
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    X = _f64(X_sorted)
+    n_c, d = off.shape[0] - 1, int(X.shape[1])
+    if workspace is None:
+        workspace = torch.empty(workspace_size(off, n_c, d, eval_slots), dtype=torch.uint8,
+                                device=torch.device("cuda", ctx.device))
+    scfg = _solve_cfg(keep=keep, **solve)
+    gcfg = _grad_cfg(mode, step, threshold, threshold_relative, max_halvings)
+    st = np.zeros(10)
+    if adam_state is None:
+        st[:3] = theta0
+    else:
+        st[:] = adam_state
+    rec = np.zeros((max(epochs, 1), N.NUGPR_TRAIN_RECORD))
+    N.check(N.lib().nugpr_train(ctx.handle, _ptr(X, keep), off.ctypes.data, n_c, d, _ptr(_f64(reps), keep),
+                                _ptr(_f64(y_sorted), keep), N.KERNELS[kernel], int(epochs), float(lr),
+                                C.byref(gcfg), C.byref(scfg), st.ctypes.data_as(C.POINTER(C.c_double)),
+                                C.c_void_p(rec.ctypes.data), C.c_void_p(workspace.data_ptr()),
+                                workspace.numel()))
+    return st, rec[:epochs]
+
+
+def adam_step(state, grad, lr=0.05):
+    s = np.ascontiguousarray(state, dtype=np.float64).copy()
+    g = np.ascontiguousarray(grad, dtype=np.float64)
+    N.check(N.lib().nugpr_adam_step(s.ctypes.data_as(C.POINTER(C.c_double)),
+                                    g.ctypes.data_as(C.POINTER(C.c_double)), float(lr)))
+    return s
+
+
+def shard_plan(world: int, costs):
+    c = np.ascontiguousarray(costs, dtype=np.float64)
+    owner = np.zeros(c.shape[0], dtype=np.int32)
+    N.check(N.lib().nugpr_shard_plan(int(world), c.ctypes.data_as(C.POINTER(C.c_double)), c.shape[0],
+                                     owner.ctypes.data_as(C.POINTER(C.c_int32))))
+    return owner
+
+
+def tridiag_eig(diag, off):
+    d = np.ascontiguousarray(diag, dtype=np.float64)
+    e = np.ascontiguousarray(off, dtype=np.float64) if len(off) else np.zeros(1)
+    k = d.shape[0]
+    ev, first = np.zeros(k), np.zeros(k)
+    P = C.POINTER(C.c_double)
+    N.check(N.lib().nugpr_tridiag_eig(k, d.ctypes.data_as(P), e.ctypes.data_as(P), ev.ctypes.data_as(P),
+                                      first.ctypes.data_as(P)))
+    return ev, first

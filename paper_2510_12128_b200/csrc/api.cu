@@ -1,0 +1,942 @@
+// api.cu — C-ABI entry points and host orchestration of the nuGPR hot path.
+//
+// Host code here only marshals arguments, carves the caller's workspace, enqueues kernels on
+// the context stream and runs the tiny host-side steps the paper keeps on the host (the
+// halving decisions of Alg. 1 and the Adam update).  Every step of the MLL
+// evaluation runs in the CUDA kernels of build_kernels.cu / eval_kernels.cu.
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/nugpr.h"
+#include "common.cuh"
+#include "kernels_decl.h"
+#include "tridiag.h"
+
+using namespace nugpr;
+
+namespace {
+
+thread_local std::string g_err;
+
+nugpr_status fail(nugpr_status st, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return st;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return fail(NUGPR_ERR_CUDA, "%s: %s (%s:%d)", #call,       \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__);   \
+  } while (0)
+
+#define CKL()                                                                         \
+  do {                                                                                \
+    cudaError_t e_ = cudaGetLastError();                                              \
+    if (e_ != cudaSuccess) return fail(NUGPR_ERR_CUDA, "kernel launch: %s (%s:%d)",   \
+                                       cudaGetErrorString(e_), __FILE__, __LINE__);   \
+  } while (0)
+
+#define RET(expr)                                  \
+  do {                                             \
+    nugpr_status s_ = (expr);                      \
+    if (s_ != NUGPR_OK) return s_;                 \
+  } while (0)
+
+constexpr int HIST = 4096;          // max recorded CG iterations (cg_max_iter cap)
+constexpr int LD_MAX_SUPPORTED = 768;
+constexpr int LANCZOS_KMAX_CAP = 400;
+
+struct HostLayout {
+  int n_c = 0, d = 0;
+  int64_t n = 0, n_pad = 0, blk_total = 0;
+  int ld_max = 0;
+  std::vector<int64_t> off, poff, boff;
+  std::vector<int32_t> ld, tile0;
+  std::vector<TileDesc> tiles;
+};
+
+nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) {
+  if (!offsets) return fail(NUGPR_ERR_INVALID_ARG, "offsets is NULL");
+  if (n_c < 1) return fail(NUGPR_ERR_INVALID_ARG, "n_c must be >= 1");
+  if (d < 1 || d > 32) return fail(NUGPR_ERR_INVALID_ARG, "d must be in [1, 32]");
+  if (offsets[0] != 0) return fail(NUGPR_ERR_SHAPE, "offsets[0] must be 0");
+  L = HostLayout();
+  L.n_c = n_c;
+  L.d = d;
+  L.off.assign(offsets, offsets + n_c + 1);
+  L.poff.resize(n_c + 1);
+  L.boff.resize(n_c);
+  L.ld.resize(n_c);
+  L.tile0.resize(n_c + 1);
+  int64_t pp = 0, bb = 0;
+  for (int i = 0; i < n_c; ++i) {
+    int64_t b = offsets[i + 1] - offsets[i];
+    if (b <= 0) return fail(NUGPR_ERR_SHAPE, "offsets must be strictly increasing (cluster %d empty)", i);
+    int64_t ld = (b + PAD - 1) / PAD * PAD;
+    if (ld > LD_MAX_SUPPORTED)
+      return fail(NUGPR_ERR_SHAPE, "cluster %d has %lld points; this build supports <= %d per cluster",
+                  i, (long long)b, LD_MAX_SUPPORTED);
+    L.ld[i] = static_cast<int32_t>(ld);
+    L.ld_max = std::max<int>(L.ld_max, static_cast<int>(ld));
+    L.poff[i] = pp;
+    L.boff[i] = bb;
+    L.tile0[i] = static_cast<int32_t>(L.tiles.size());
+    for (int r0 = 0; r0 < ld; r0 += TILE_ROWS) {
+      TileDesc t;
+      t.blk = i;
+      t.row0 = r0;
+      t.nrows = static_cast<int32_t>(std::min<int64_t>(TILE_ROWS, ld - r0));
+      t.pad_ = 0;
+      L.tiles.push_back(t);
+    }
+    pp += ld;
+    bb += ld * ld;
+  }
+  L.poff[n_c] = pp;
+  L.tile0[n_c] = static_cast<int32_t>(L.tiles.size());
+  L.n = offsets[n_c];
+  L.n_pad = pp;
+  L.blk_total = bb;
+  return NUGPR_OK;
+}
+
+struct Carver {
+  char* base;
+  size_t pos = 0;
+  explicit Carver(void* b) : base(static_cast<char*>(b)) {}
+  template <class T>
+  T* take(size_t count) {
+    pos = (pos + 255) / 256 * 256;
+    T* p = base ? reinterpret_cast<T*>(base + pos) : nullptr;
+    pos += count * sizeof(T);
+    return p;
+  }
+};
+
+// One evaluation's scratch (a "slot").
+struct EvalDev {
+  double* G = nullptr;        // blk_total (generic mode: K(theta') then G)
+  double* T = nullptr;        // blk_total (generic mode: K Linv^T)
+  double* Krep = nullptr;     // n_c^2
+  double* M = nullptr;        // n_c^2
+  double* v0 = nullptr;       // n_c
+  double* lz = nullptr;       // lanczos scratch
+  int32_t* linfo = nullptr;
+  double* scal = nullptr;     // [0] lam0
+  double* RHS = nullptr, *R = nullptr, *X = nullptr, *V = nullptr, *Q = nullptr, *U = nullptr;
+  double* Pb[2] = {nullptr, nullptr};
+  double* SR = nullptr, *SPb[2] = {nullptr, nullptr}, *SV = nullptr, *SX = nullptr, *dots = nullptr,
+         *rrp = nullptr;
+  EvalParams* prm = nullptr;
+  CGState* st = nullptr;
+  nugpr_mll_out* out = nullptr;
+  double* ah = nullptr, *bh = nullptr, *slqw = nullptr;
+  double* ystage = nullptr;   // n
+};
+
+struct BlocksDev {
+  int64_t* off = nullptr, *poff = nullptr, *boff = nullptr;
+  int32_t* ld = nullptr, *tile0 = nullptr, *list = nullptr, *status = nullptr;
+  TileDesc* tiles = nullptr;
+  double* X = nullptr, *reps = nullptr;
+  double* Linv = nullptr, *H = nullptr;
+  double* u = nullptr, *jitter = nullptr, *logdet_blk = nullptr;
+  double* scal = nullptr;     // [0] logdet_R, [1] lam0
+  double* Krep = nullptr, *M = nullptr, *v0 = nullptr, *lz = nullptr;
+  int32_t* linfo = nullptr;
+  double* Zexport = nullptr;  // m x n (debug probe export)
+};
+
+void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
+  const int n_c = L.n_c;
+  const int64_t nt = static_cast<int64_t>(L.tiles.size());
+  const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
+  const size_t lzs = lanczos_scratch_doubles(n_c, kmax);
+  B.off = c.take<int64_t>(n_c + 1);
+  B.poff = c.take<int64_t>(n_c + 1);
+  B.boff = c.take<int64_t>(n_c);
+  B.ld = c.take<int32_t>(n_c);
+  B.tile0 = c.take<int32_t>(n_c + 1);
+  B.list = c.take<int32_t>(n_c);
+  B.status = c.take<int32_t>(n_c);
+  B.tiles = c.take<TileDesc>(nt);
+  B.X = c.take<double>(static_cast<size_t>(L.n) * L.d);
+  B.reps = c.take<double>(static_cast<size_t>(n_c) * L.d);
+  B.Linv = c.take<double>(L.blk_total);
+  B.H = c.take<double>(L.blk_total);
+  B.u = c.take<double>(L.n_pad);
+  B.jitter = c.take<double>(n_c);
+  B.logdet_blk = c.take<double>(n_c);
+  B.scal = c.take<double>(8);
+  B.Krep = c.take<double>(static_cast<size_t>(n_c) * n_c);
+  B.M = c.take<double>(static_cast<size_t>(n_c) * n_c);
+  B.v0 = c.take<double>(n_c);
+  B.lz = c.take<double>(lzs);
+  B.linfo = c.take<int32_t>(4);
+  B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
+  E.assign(slots, EvalDev());
+  const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
+  for (int s = 0; s < slots; ++s) {
+    EvalDev& e = E[s];
+    e.G = c.take<double>(L.blk_total);
+    e.T = c.take<double>(L.blk_total);
+    e.Krep = c.take<double>(static_cast<size_t>(n_c) * n_c);
+    e.M = c.take<double>(static_cast<size_t>(n_c) * n_c);
+    e.v0 = c.take<double>(n_c);
+    e.lz = c.take<double>(lzs);
+    e.linfo = c.take<int32_t>(4);
+    e.scal = c.take<double>(8);
+    e.RHS = c.take<double>(vec);
+    e.R = c.take<double>(vec);
+    e.X = c.take<double>(vec);
+    e.V = c.take<double>(vec);
+    e.Q = c.take<double>(vec);
+    e.U = c.take<double>(vec);
+    e.Pb[0] = c.take<double>(vec);
+    e.Pb[1] = c.take<double>(vec);
+    e.SR = c.take<double>(nt * MAXC);
+    e.SPb[0] = c.take<double>(nt * MAXC);
+    e.SPb[1] = c.take<double>(nt * MAXC);
+    e.SV = c.take<double>(nt * MAXC);
+    e.SX = c.take<double>(nt * MAXC);
+    e.dots = c.take<double>(nt * MAXC);
+    e.rrp = c.take<double>(nt * MAXC);
+    e.prm = c.take<EvalParams>(1);
+    e.st = c.take<CGState>(1);
+    e.out = c.take<nugpr_mll_out>(1);
+    e.ah = c.take<double>(static_cast<size_t>(MAXC) * HIST);
+    e.bh = c.take<double>(static_cast<size_t>(MAXC) * HIST);
+    e.slqw = c.take<double>(static_cast<size_t>(MAXC) * 3 * HIST);
+    e.ystage = c.take<double>(L.n);
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
+}
+
+}  // namespace
+
+// Event-based per-kernel-class profiler (bench.py's live roofline): CUDA events recorded on the
+// launching stream around each launch of a class, harvested at the next host sync.
+enum ProfClass { PC_APPLY_B = 0, PC_APPLY_LR = 1, PC_UPDATE = 2, PC_RHS = 3, PC_GEMM = 4, PC_CHOL = 5,
+                 PC_LANCZOS = 6, PC_OTHER = 7, PC_N = 8 };
+struct ProfPending { int cls; double bytes; cudaEvent_t a, b; };
+
+struct nugpr_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  int rank = 0, world = 1;
+  nugpr_allgather_fn ag = nullptr;
+  void* ag_user = nullptr;
+  int32_t* h_flag = nullptr;             // pinned
+  nugpr_mll_out* h_out = nullptr;        // pinned
+  bool prof = false;
+  std::vector<cudaEvent_t> pool;
+  std::vector<ProfPending> pend;
+  double acc_ms[PC_N] = {0}, acc_bytes[PC_N] = {0};
+  long long acc_n[PC_N] = {0};
+};
+
+static int prof_begin(nugpr_ctx* c, cudaStream_t s) {
+  if (!c || !c->prof) return -1;
+  ProfPending p;
+  for (cudaEvent_t* ev : {&p.a, &p.b}) {
+    if (!c->pool.empty()) { *ev = c->pool.back(); c->pool.pop_back(); }
+    else cudaEventCreate(ev);
+  }
+  p.cls = PC_OTHER;
+  p.bytes = 0.0;
+  cudaEventRecord(p.a, s);
+  c->pend.push_back(p);
+  return static_cast<int>(c->pend.size()) - 1;
+}
+static void prof_end(nugpr_ctx* c, int idx, int cls, double bytes, cudaStream_t s) {
+  if (idx < 0) return;
+  ProfPending& p = c->pend[idx];
+  p.cls = cls;
+  p.bytes = bytes;
+  cudaEventRecord(p.b, s);
+}
+static void prof_harvest(nugpr_ctx* c) {
+  if (!c) return;
+  for (ProfPending& p : c->pend) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, p.a, p.b) == cudaSuccess) {
+      c->acc_ms[p.cls] += ms;
+      c->acc_bytes[p.cls] += p.bytes;
+      c->acc_n[p.cls] += 1;
+    }
+    c->pool.push_back(p.a);
+    c->pool.push_back(p.b);
+  }
+  c->pend.clear();
+}
+#define PROF(ctx_, cls_, bytes_, stream_, launch_)        \
+  do {                                                    \
+    int pi_ = prof_begin((ctx_), (stream_));              \
+    launch_;                                              \
+    prof_end((ctx_), pi_, (cls_), (bytes_), (stream_));   \
+  } while (0)
+
+struct nugpr_blocks {
+  nugpr_ctx* ctx = nullptr;
+  HostLayout L;
+  LayoutDev Ld;
+  BlocksDev B;
+  std::vector<EvalDev> E;
+  int kind = 0;
+  nugpr_theta theta0{};
+  double logdet_R = 0.0, lam0 = 0.0, max_jitter = 0.0;
+  std::vector<double> h_jitter;
+  std::vector<int32_t> h_list;
+  int last_m = 0;
+  uint64_t last_seed = 0;
+  const double* last_probes = nullptr;
+};
+
+extern "C" {
+
+const char* nugpr_version(void) { return "nugpr-b200 0.1 (sm_100a, FP64)"; }
+const char* nugpr_last_error(void) { return g_err.c_str(); }
+
+nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world, nugpr_ctx** out) {
+  if (!out) return fail(NUGPR_ERR_INVALID_ARG, "out is NULL");
+  if (world < 1 || rank < 0 || rank >= world) return fail(NUGPR_ERR_INVALID_ARG, "bad rank/world");
+  CK(cudaSetDevice(device));
+  nugpr_ctx* c = new nugpr_ctx();
+  c->device = device;
+  c->stream = static_cast<cudaStream_t>(cuda_stream);
+  c->rank = rank;
+  c->world = world;
+  cudaError_t e1 = cudaMallocHost(&c->h_flag, 64);
+  cudaError_t e2 = cudaMallocHost(&c->h_out, sizeof(nugpr_mll_out));
+  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+    delete c;
+    return fail(NUGPR_ERR_CUDA, "pinned host allocation failed");
+  }
+  *out = c;
+  return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void* user) {
+  if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->ag = fn;
+  ctx->ag_user = user;
+  return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_set_profiling(nugpr_ctx* ctx, int32_t enable) {
+  if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->prof = enable != 0;
+  for (int k = 0; k < PC_N; ++k) { ctx->acc_ms[k] = 0; ctx->acc_bytes[k] = 0; ctx->acc_n[k] = 0; }
+  return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_profile(nugpr_ctx* ctx, int32_t cls, double* ms, double* bytes, int64_t* launches) {
+  if (!ctx || cls < 0 || cls >= PC_N) return fail(NUGPR_ERR_INVALID_ARG, "bad profile query");
+  cudaStreamSynchronize(ctx->stream);
+  prof_harvest(ctx);
+  if (ms) *ms = ctx->acc_ms[cls];
+  if (bytes) *bytes = ctx->acc_bytes[cls];
+  if (launches) *launches = ctx->acc_n[cls];
+  return NUGPR_OK;
+}
+
+int64_t nugpr_launch_count(void) { return launch_count(); }
+
+nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
+  if (!ctx) return NUGPR_OK;
+  for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
+  if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
+  if (ctx->h_out) cudaFreeHost(ctx->h_out);
+  delete ctx;
+  return NUGPR_OK;
+}
+
+}  // extern "C"
+
+static nugpr_status ws_size_slots(const int64_t* offsets, int32_t n_c, int32_t d, int slots, size_t* bytes) {
+  HostLayout L;
+  RET(make_layout(offsets, n_c, d, L));
+  if (L.off[n_c] <= 0) return fail(NUGPR_ERR_SHAPE, "n must be > 0");
+  Carver c(nullptr);
+  BlocksDev B;
+  std::vector<EvalDev> E;
+  carve_all(c, L, slots, B, E);
+  *bytes = c.pos + 256;
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_workspace_size(const int64_t* offsets, int32_t n_c, int32_t d,
+                                             int32_t eval_slots, size_t* bytes) {
+  if (!bytes) return fail(NUGPR_ERR_INVALID_ARG, "bytes is NULL");
+  if (eval_slots < 1 || eval_slots > NUGPR_NUM_EVALS) return fail(NUGPR_ERR_INVALID_ARG, "eval_slots must be in [1, 7]");
+  return ws_size_slots(offsets, n_c, d, eval_slots, bytes);
+}
+
+static bool theta_ok(const nugpr_theta& t) {
+  return t.lengthscale > 0 && t.noise > 0 && t.outputscale > 0 && std::isfinite(t.lengthscale) &&
+         std::isfinite(t.noise) && std::isfinite(t.outputscale);
+}
+
+// Lanczos lambda_0 of K (device n_c x n_c), warm start vinit (or NULL), writes lam0/v0/M.
+static nugpr_status enqueue_lambda0(nugpr_blocks* bl, const double* K, const double* vinit, double* lz,
+                                    double* lam0, double* v0, double* M, int32_t* info, cudaStream_t s) {
+  const int n_c = bl->L.n_c;
+  const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
+  launch_lanczos(K, n_c, vinit, lz, kmax, 1e-13, lam0, v0, M, info, s);
+  CKL();
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets,
+                                           int32_t n_c, int32_t d, const double* reps, int32_t kernel,
+                                           nugpr_theta theta0, void* workspace, size_t ws_bytes,
+                                           nugpr_blocks** out, int32_t* failed_block, double* max_jitter) {
+  if (failed_block) *failed_block = -1;
+  if (max_jitter) *max_jitter = 0.0;
+  if (!ctx || !X_sorted || !reps || !workspace || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (kernel < 0 || kernel > 2) return fail(NUGPR_ERR_INVALID_ARG, "bad kernel id %d", kernel);
+  if (!theta_ok(theta0)) return fail(NUGPR_ERR_INVALID_ARG, "theta0 must be positive and finite");
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(NUGPR_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  CK(cudaSetDevice(ctx->device));
+  nugpr_blocks* bl = new nugpr_blocks();
+  nugpr_status st = make_layout(offsets, n_c, d, bl->L);
+  if (st != NUGPR_OK) { delete bl; return st; }
+  // number of eval slots that fit
+  int slots = 0;
+  for (int s = NUGPR_NUM_EVALS; s >= 1; --s) {
+    size_t need = 0;
+    ws_size_slots(offsets, n_c, d, s, &need);
+    if (need <= ws_bytes) { slots = s; break; }
+  }
+  if (slots == 0) {
+    size_t need = 0;
+    ws_size_slots(offsets, n_c, d, 1, &need);
+    delete bl;
+    return fail(NUGPR_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  }
+  Carver c(workspace);
+  carve_all(c, bl->L, slots, bl->B, bl->E);
+  bl->ctx = ctx;
+  bl->kind = kernel;
+  bl->theta0 = theta0;
+  HostLayout& L = bl->L;
+  BlocksDev& B = bl->B;
+  cudaStream_t s = ctx->stream;
+  LayoutDev& Ld = bl->Ld;
+  Ld.off = B.off; Ld.poff = B.poff; Ld.boff = B.boff; Ld.ld = B.ld; Ld.tiles = B.tiles;
+  Ld.tile0 = B.tile0; Ld.n_c = n_c; Ld.n_tiles = static_cast<int32_t>(L.tiles.size());
+  Ld.n = L.n; Ld.n_pad = L.n_pad;
+#define CKB(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { delete bl; \
+    return fail(NUGPR_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
+  CKB(cudaMemcpyAsync(B.off, L.off.data(), sizeof(int64_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.poff, L.poff.data(), sizeof(int64_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.boff, L.boff.data(), sizeof(int64_t) * n_c, cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * n_c, cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.X, X_sorted, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
+  CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
+  CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * n_c, s));
+  CKB(cudaMemsetAsync(B.u, 0, sizeof(double) * L.n_pad, s));
+  // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
+  PROF(ctx, PC_OTHER, 0.0, s,
+       launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
+                       theta0.noise, theta0.outputscale, s));
+  PROF(ctx, PC_CHOL, 0.0, s, launch_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, s));
+  CKB(cudaGetLastError());
+  std::vector<int32_t> hstat(n_c);
+  CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
+  CKB(cudaStreamSynchronize(s));
+  bl->h_jitter.assign(n_c, 0.0);
+  const double base = 1e-8 * (theta0.outputscale + theta0.noise);   // 1e-8 * mean(diag K_i)
+  for (int t = 0; t <= 5; ++t) {
+    bl->h_list.clear();
+    for (int i = 0; i < n_c; ++i) if (hstat[i]) bl->h_list.push_back(i);
+    if (bl->h_list.empty()) break;
+    if (t == 5) {
+      int fb = bl->h_list[0];
+      if (failed_block) *failed_block = fb;
+      delete bl;
+      return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
+    }
+    for (int i : bl->h_list) bl->h_jitter[i] = base * std::pow(10.0, t);
+    CKB(cudaMemcpyAsync(B.jitter, bl->h_jitter.data(), sizeof(double) * n_c, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.list, bl->h_list.data(), sizeof(int32_t) * bl->h_list.size(), cudaMemcpyHostToDevice, s));
+    launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
+                    kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
+    launch_chol_trtri(B.Linv, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.status,
+                      B.logdet_blk, B.u, s);
+    CKB(cudaGetLastError());
+    CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
+    CKB(cudaStreamSynchronize(s));
+  }
+  for (double j : bl->h_jitter) bl->max_jitter = std::max(bl->max_jitter, j);
+  // H_i = Linv_i Linv_i^T ; logdet_R ; K_rep, lambda_0, M
+  PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
+  launch_sum(B.logdet_blk, n_c, B.scal + 0, s);
+  launch_krep(B.reps, n_c, d, kernel, theta0.lengthscale, theta0.outputscale, B.Krep, s);
+  CKB(cudaGetLastError());
+  nugpr_status ls;
+  PROF(ctx, PC_LANCZOS, 0.0, s, ls = enqueue_lambda0(bl, B.Krep, nullptr, B.lz, B.scal + 1, B.v0, B.M, B.linfo, s));
+  if (ls != NUGPR_OK) { delete bl; return ls; }
+  double hs[2];
+  CKB(cudaMemcpyAsync(hs, B.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+  CKB(cudaStreamSynchronize(s));
+#undef CKB
+  prof_harvest(ctx);
+  bl->logdet_R = hs[0];
+  bl->lam0 = hs[1];
+  if (max_jitter) *max_jitter = bl->max_jitter;
+  if (!(bl->lam0 > 0.0)) {
+    delete bl;
+    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0 = %g <= 0 (degenerate representatives)", hs[1]);
+  }
+  *out = bl;
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_blocks_destroy(nugpr_blocks* blocks) {
+  delete blocks;
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_blocks_export(const nugpr_blocks* bl, int32_t what, void* dst, size_t bytes) {
+  if (!bl || !dst) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  const HostLayout& L = bl->L;
+  cudaStream_t s = bl->ctx->stream;
+  CK(cudaSetDevice(bl->ctx->device));
+  auto need = [&](size_t n) -> bool { return bytes >= n; };
+  switch (what) {
+    case 0:
+    case 1: {
+      size_t n = sizeof(double) * L.blk_total;
+      if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
+      CK(cudaMemcpyAsync(dst, what == 0 ? bl->B.Linv : bl->B.H, n, cudaMemcpyDeviceToHost, s));
+      break;
+    }
+    case 2: {
+      size_t n = sizeof(double) * L.n;
+      if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
+      std::vector<double> up(L.n_pad);
+      CK(cudaMemcpyAsync(up.data(), bl->B.u, sizeof(double) * L.n_pad, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double* o = static_cast<double*>(dst);
+      for (int i = 0; i < L.n_c; ++i)
+        for (int64_t r = 0; r < L.off[i + 1] - L.off[i]; ++r) o[L.off[i] + r] = up[L.poff[i] + r];
+      return NUGPR_OK;
+    }
+    case 3: {
+      size_t n = sizeof(double) * L.n_c;
+      if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
+      CK(cudaMemcpyAsync(dst, bl->B.jitter, n, cudaMemcpyDeviceToHost, s));
+      break;
+    }
+    case 4: {
+      if (!need(2 * sizeof(double))) return fail(NUGPR_ERR_INVALID_ARG, "need 16 bytes");
+      CK(cudaMemcpyAsync(dst, bl->B.scal, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+      break;
+    }
+    case 5: {
+      size_t n = sizeof(double) * L.n_c * L.n_c;
+      if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
+      CK(cudaMemcpyAsync(dst, bl->B.M, n, cudaMemcpyDeviceToHost, s));
+      break;
+    }
+    case 6: {
+      size_t n = sizeof(int32_t) * L.n_c;
+      if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
+      memcpy(dst, L.ld.data(), n);
+      return NUGPR_OK;
+    }
+    case 7: {
+      size_t n = sizeof(double) * bl->last_m * L.n;
+      if (bl->last_m == 0 || !need(n)) return fail(NUGPR_ERR_INVALID_ARG, "no probes / need %zu bytes", n);
+      launch_probe_gen(bl->last_seed, bl->last_m, L.n, bl->B.Zexport, s);
+      CKL();
+      CK(cudaMemcpyAsync(dst, bl->B.Zexport, n, cudaMemcpyDeviceToHost, s));
+      break;
+    }
+    default:
+      return fail(NUGPR_ERR_INVALID_ARG, "unknown export %d", what);
+  }
+  CK(cudaStreamSynchronize(s));
+  return NUGPR_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// One evaluation, fully enqueued on stream s using slot e; the record lands in e.out (device).
+static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, const double* y_dev,
+                                 nugpr_theta th, const nugpr_solve_cfg* cfg, cudaStream_t s, int* mode_out,
+                                 int32_t* h_flag) {
+  const HostLayout& L = bl->L;
+  const LayoutDev& Ld = bl->Ld;
+  const BlocksDev& B = bl->B;
+  const nugpr_theta t0 = bl->theta0;
+  const int m = cfg->num_probes;
+  const int ncol = 1 + m;
+  const int ncp = (ncol + 1) & ~1;
+  const int max_iter = cfg->cg_max_iter;
+  EvalParams P;
+  memset(&P, 0, sizeof(P));
+  P.tol = cfg->cg_tol;
+  P.max_iter = max_iter;
+  P.ncol = ncol;
+  P.mscale = 1.0;
+  P.Mp = B.M;
+  if (cfg->replay_iters) {
+    P.replay = 1;
+    for (int c = 0; c < ncol; ++c) P.replay_iters[c] = std::min(cfg->replay_iters[c], max_iter);
+  }
+  const double* lam0_ptr = B.scal + 1;
+  int mode;
+  const bool same_l = th.lengthscale == t0.lengthscale, same_s = th.noise == t0.noise,
+             same_a = th.outputscale == t0.outputscale;
+  if (same_l && same_s && same_a) {                       // Eq. (23)
+    mode = NUGPR_MODE_BASELINE;
+    P.a = 1.0; P.B = nullptr;
+  } else if (same_l && same_a) {                          // Eq. (24)
+    mode = NUGPR_MODE_NOISE;
+    P.a = 1.0; P.b0 = th.noise - t0.noise; P.b1 = 0.0; P.B = B.H;
+  } else if (same_l && same_s) {                          // Eq. (25)
+    mode = NUGPR_MODE_SCALE;
+    const double r = (th.outputscale - t0.outputscale) / t0.outputscale;
+    P.a = 1.0 + r; P.b0 = -t0.noise * r; P.b1 = -r; P.B = B.H; P.mscale = 1.0 + r;
+  } else {                                                // generic (lengthscale step)
+    mode = NUGPR_MODE_GENERIC;
+    P.a = 0.0; P.b0 = 1.0; P.b1 = 0.0; P.B = e.G; P.Mp = e.M;
+    PROF(ctx, PC_OTHER, 0.0, s,
+         launch_assemble(B.X, L.d, Ld, nullptr, 0, L.ld_max, B.jitter, e.G, bl->kind, th.lengthscale,
+                         th.noise, th.outputscale, s));
+    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_KLt(e.G, B.Linv, e.T, Ld, L.ld_max, s));
+    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_LT(B.Linv, e.T, e.G, Ld, L.ld_max, s));
+    launch_krep(B.reps, L.n_c, L.d, bl->kind, th.lengthscale, th.outputscale, e.Krep, s);
+    CKL();
+    nugpr_status ls;
+    PROF(ctx, PC_LANCZOS, 0.0, s, ls = enqueue_lambda0(bl, e.Krep, B.v0, e.lz, e.scal, e.v0, e.M, e.linfo, s));
+    RET(ls);
+    lam0_ptr = e.scal;
+  }
+  P.mode = mode;
+  if (mode_out) *mode_out = mode;
+  CK(cudaMemcpyAsync(e.prm, &P, sizeof(P), cudaMemcpyHostToDevice, s));
+  if (mode == NUGPR_MODE_SCALE) {
+    // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
+    // build read back, written to the slot scalar (reported in the record only).
+    double l0 = bl->lam0 * P.mscale;
+    CK(cudaMemcpyAsync(e.scal + 1, &l0, sizeof(double), cudaMemcpyHostToDevice, s));
+    lam0_ptr = e.scal + 1;
+  }
+  // rhs + init
+  RhsArgs ra;
+  ra.L = Ld; ra.prm = e.prm; ra.st = e.st; ra.Linv = B.Linv; ra.y = y_dev;
+  ra.probes = cfg->probes; ra.seed = cfg->probe_seed; ra.u = B.u; ra.RHS = e.RHS; ra.R = e.R;
+  ra.X = e.X; ra.P0 = e.Pb[0]; ra.SP0 = e.SPb[0]; ra.SR_part = e.SR; ra.rr_part = e.rrp; ra.ncol = ncol;
+  PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
+  CKL();
+  // algorithmic bytes of one apply: w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
+  double sum_b2 = 0.0;
+  for (int i = 0; i < L.n_c; ++i) { double b = static_cast<double>(L.off[i + 1] - L.off[i]); sum_b2 += b * b; }
+  const double vec_bytes = 8.0 * (2.0 * L.n * ncol + L.n + static_cast<double>(L.n_c) * L.n_c);
+  const double apply_bytes = (P.B ? 8.0 * sum_b2 : 0.0) + vec_bytes;
+  const int apply_cls = P.B ? PC_APPLY_B : PC_APPLY_LR;
+  // CG iteration building blocks
+  ApplyArgs a1;
+  memset(&a1, 0, sizeof(a1));
+  a1.L = Ld; a1.prm = e.prm; a1.st = e.st; a1.u = B.u; a1.jitter = B.jitter; a1.ncol = ncol;
+  a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
+  a1.alpha_hist = e.ah; a1.hist_stride = HIST;
+  ApplyArgs a2 = a1;
+  // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
+  a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;
+  a1.fin = FIN_NONE; a1.gate = 1;
+  for (int c = 0; c < MAXC; ++c) { a1.cA[c] = 1.0; a1.cV[c] = 0.0; a1.cP[c] = 0.0; }
+  // apply 2: q = A V + 4 V + p (probe columns), q = V (y column); p^T q partials -> alpha
+  a2.D = e.V; a2.S_D = e.SV; a2.fuse_p = 0; a2.out = e.Q; a2.use_par_p2 = 1; a2.epi = EPI_DOT;
+  a2.dots = e.dots; a2.fin = FIN_ALPHA; a2.gate = 1;
+  for (int c = 0; c < MAXC; ++c) {
+    if (c == 0) { a2.cA[c] = 0.0; a2.cV[c] = 1.0; a2.cP[c] = 0.0; }
+    else { a2.cA[c] = 1.0; a2.cV[c] = 4.0; a2.cP[c] = 1.0; }
+  }
+  // (with use_par_p2 the kernel takes both the combine term P2 and the dot partner Y2 from
+  //  the parity-resolved current direction P[par^1])
+  UpdateArgs ua;
+  ua.L = Ld; ua.prm = e.prm; ua.st = e.st; ua.u = B.u; ua.X = e.X; ua.R = e.R; ua.Q = e.Q;
+  ua.Pbuf[0] = e.Pb[0]; ua.Pbuf[1] = e.Pb[1]; ua.rr_part = e.rrp; ua.SR_part = e.SR;
+  ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol;
+
+  const int limit = cfg->replay_iters ? [&] { int mx = 0; for (int c = 0; c < ncol; ++c) mx = std::max(mx, P.replay_iters[c]); return mx; }()
+                                      : max_iter;
+  const int CH = 4;
+  int done = 0;
+  while (done < limit) {
+    for (int q = 0; q < CH && done < limit; ++q, ++done) {
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a1, ncp, L.ld_max, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a2, ncp, L.ld_max, s));
+      PROF(ctx, PC_UPDATE, 0.0, s, launch_update(ua, ncp, s));
+    }
+    CKL();
+    CK(cudaMemcpyAsync(h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!*h_flag) break;
+  }
+  // trace: V = A X, U = 3 A V - 3 X (probe cols) / X (y col), dotted with RHS
+  launch_spart(Ld, B.u, e.X, ncol, e.SX, s);
+  ApplyArgs a3 = a1;
+  a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
+  a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a3, ncp, L.ld_max, s));
+  ApplyArgs a4 = a3;
+  a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
+  a4.fin = FIN_TRACE;
+  for (int c = 0; c < MAXC; ++c) {
+    if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
+    else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
+  }
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a4, ncp, L.ld_max, s));
+  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, lam0_ptr, static_cast<double>(L.n),
+               ncol, cfg->logdet_mode, e.out, s);
+  CKL();
+  return NUGPR_OK;
+}
+
+static nugpr_status check_cfg(const nugpr_solve_cfg* cfg) {
+  if (!cfg) return fail(NUGPR_ERR_INVALID_ARG, "cfg is NULL");
+  if (cfg->num_probes < 1 || cfg->num_probes > NUGPR_MAX_PROBES)
+    return fail(NUGPR_ERR_INVALID_ARG, "num_probes must be in [1, %d]", NUGPR_MAX_PROBES);
+  if (cfg->cg_max_iter < 1 || cfg->cg_max_iter >= HIST)
+    return fail(NUGPR_ERR_INVALID_ARG, "cg_max_iter must be in [1, %d)", HIST);
+  if (!(cfg->cg_tol >= 0.0)) return fail(NUGPR_ERR_INVALID_ARG, "cg_tol must be >= 0");
+  if (cfg->logdet_mode != 0 && cfg->logdet_mode != 1) return fail(NUGPR_ERR_INVALID_ARG, "bad logdet_mode");
+  return NUGPR_OK;
+}
+
+static nugpr_status stage_y(nugpr_blocks* bl, const double* y, EvalDev& e, cudaStream_t s, const double** y_dev) {
+  if (is_device_ptr(y)) { *y_dev = y; return NUGPR_OK; }
+  CK(cudaMemcpyAsync(e.ystage, y, sizeof(double) * bl->L.n, cudaMemcpyHostToDevice, s));
+  *y_dev = e.ystage;
+  return NUGPR_OK;
+}
+
+static nugpr_status run_eval(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_dev, nugpr_theta th,
+                             const nugpr_solve_cfg* cfg, nugpr_mll_out* out) {
+  cudaStream_t s = ctx->stream;
+  EvalDev& e = bl->E[0];
+  int mode = 0;
+  RET(enqueue_eval(ctx, bl, e, y_dev, th, cfg, s, &mode, ctx->h_flag));
+  CK(cudaMemcpyAsync(ctx->h_out, e.out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  prof_harvest(ctx);
+  *out = *ctx->h_out;
+  bl->last_m = cfg->num_probes;
+  bl->last_seed = cfg->probe_seed;
+  if (!(out->lambda0 > 0.0))
+    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", out->lambda0);
+  if (!out->converged) return fail(NUGPR_ERR_CG_NOT_CONVERGED, "CG reached cg_max_iter = %d", cfg->cg_max_iter);
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_mll(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
+                                  const nugpr_solve_cfg* cfg, nugpr_mll_out* out) {
+  if (!ctx || !bl || !y_sorted || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (!theta_ok(theta)) return fail(NUGPR_ERR_INVALID_ARG, "theta must be positive and finite");
+  RET(check_cfg(cfg));
+  CK(cudaSetDevice(ctx->device));
+  const double* y_dev = nullptr;
+  RET(stage_y(bl, y_sorted, bl->E[0], ctx->stream, &y_dev));
+  return run_eval(ctx, bl, y_dev, theta, cfg, out);
+}
+
+// ------------------------------------------------------------------------------------------
+// Numerical gradient (row A8).
+extern "C" nugpr_status nugpr_shard_plan(int32_t world, const double* costs, int32_t n, int32_t* owner) {
+  if (world < 1 || n < 0 || (n > 0 && (!costs || !owner))) return fail(NUGPR_ERR_INVALID_ARG, "bad shard plan args");
+  std::vector<int> idx(n);
+  for (int k = 0; k < n; ++k) idx[k] = k;
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return costs[a] > costs[b]; });
+  std::vector<double> load(world, 0.0);
+  for (int k : idx) {
+    int best = 0;
+    for (int r = 1; r < world; ++r) if (load[r] < load[best]) best = r;
+    owner[k] = best;
+    load[best] += costs[k];
+  }
+  return NUGPR_OK;
+}
+
+struct EvalRecord {
+  nugpr_mll_out o;
+  int32_t status;
+  int32_t valid;
+};
+
+extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
+                                      const nugpr_grad_cfg* gcfg, const nugpr_solve_cfg* scfg, double* L0,
+                                      double grad[3], nugpr_mll_out* evals, int32_t* n_evals) {
+  if (!ctx || !bl || !y_sorted || !gcfg || !L0 || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (!theta_ok(theta)) return fail(NUGPR_ERR_INVALID_ARG, "theta must be positive and finite");
+  RET(check_cfg(scfg));
+  CK(cudaSetDevice(ctx->device));
+  const double th[3] = {theta.lengthscale, theta.noise, theta.outputscale};
+  const double* y_dev = nullptr;
+  RET(stage_y(bl, y_sorted, bl->E[0], ctx->stream, &y_dev));
+  auto mk = [](const double* p) { nugpr_theta t{p[0], p[1], p[2]}; return t; };
+  int ne = 0;
+  if (gcfg->mode == NUGPR_GRAD_CENTRAL) {
+    double pts[NUGPR_NUM_EVALS][3];
+    double h[3];
+    for (int i = 0; i < 3; ++i) h[i] = gcfg->step[i] * th[i];
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) for (int i = 0; i < 3; ++i) pts[k][i] = th[i];
+    for (int i = 0; i < 3; ++i) {
+      pts[1 + 2 * i][i] = th[i] + h[i];
+      pts[2 + 2 * i][i] = th[i] - h[i];
+      if (!(pts[2 + 2 * i][i] > 0.0)) return fail(NUGPR_ERR_INVALID_ARG, "step too large for parameter %d", i);
+    }
+    // perturbation sharding (PAR-1): LPT over a cost model (baseline: no block reads)
+    const double cost[NUGPR_NUM_EVALS] = {1.0, 3.0, 3.0, 2.0, 2.0, 2.0, 2.0};
+    int32_t owner[NUGPR_NUM_EVALS];
+    RET(nugpr_shard_plan(ctx->world, cost, NUGPR_NUM_EVALS, owner));
+    EvalRecord mine[NUGPR_NUM_EVALS];
+    memset(mine, 0, sizeof(mine));
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
+      if (owner[k] != ctx->rank) continue;
+      nugpr_status st = run_eval(ctx, bl, y_dev, mk(pts[k]), scfg, &mine[k].o);
+      mine[k].status = st;
+      mine[k].valid = 1;
+      if (st != NUGPR_OK && st != NUGPR_ERR_CG_NOT_CONVERGED) return st;
+    }
+    EvalRecord all[NUGPR_NUM_EVALS];
+    if (ctx->world > 1) {
+      if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");
+      std::vector<EvalRecord> recv(static_cast<size_t>(ctx->world) * NUGPR_NUM_EVALS);
+      if (ctx->ag(mine, sizeof(mine), recv.data(), ctx->ag_user) != 0) return fail(NUGPR_ERR_COMM, "allgather failed");
+      for (int k = 0; k < NUGPR_NUM_EVALS; ++k) all[k] = recv[static_cast<size_t>(owner[k]) * NUGPR_NUM_EVALS + k];
+    } else {
+      memcpy(all, mine, sizeof(mine));
+    }
+    nugpr_status worst = NUGPR_OK;
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
+      if (!all[k].valid) return fail(NUGPR_ERR_COMM, "evaluation %d missing after exchange", k);
+      if (all[k].status != NUGPR_OK) worst = static_cast<nugpr_status>(all[k].status);
+      if (evals) evals[k] = all[k].o;
+    }
+    ne = NUGPR_NUM_EVALS;
+    *L0 = all[0].o.L;
+    for (int i = 0; i < 3; ++i) grad[i] = (all[1 + 2 * i].o.L - all[2 + 2 * i].o.L) / (2.0 * h[i]);
+    if (n_evals) *n_evals = ne;
+    if (worst != NUGPR_OK) return fail(worst, "an evaluation did not converge");
+    return NUGPR_OK;
+  } else if (gcfg->mode == NUGPR_GRAD_FORWARD_HALVING) {
+    if (gcfg->max_halvings < 0 || gcfg->max_halvings > 20) return fail(NUGPR_ERR_INVALID_ARG, "max_halvings must be in [0, 20]");
+    // Alg. 1 lines 265-278 (readings P12-P14)
+    nugpr_mll_out o;
+    nugpr_status st = run_eval(ctx, bl, y_dev, theta, scfg, &o);
+    if (st != NUGPR_OK) return st;
+    if (evals) evals[ne] = o;
+    ++ne;
+    *L0 = o.L;
+    for (int i = 0; i < 3; ++i) {
+      double delta = gcfg->step[i] * th[i];
+      double gprev = INFINITY, g = 0.0;
+      int nh = 0;
+      while (true) {
+        double p[3] = {th[0], th[1], th[2]};
+        p[i] += delta;
+        nugpr_mll_out o1;
+        st = run_eval(ctx, bl, y_dev, mk(p), scfg, &o1);
+        if (st != NUGPR_OK) return st;
+        if (evals) evals[ne] = o1;
+        ++ne;
+        g = (o1.L - o.L) / delta;
+        const double scale = gcfg->threshold_relative ? std::max(1.0, std::fabs(g)) : 1.0;
+        if (std::fabs(g - gprev) < gcfg->threshold * scale || nh >= gcfg->max_halvings) break;
+        gprev = g;
+        delta *= 0.5;
+        ++nh;
+      }
+      grad[i] = g;
+    }
+    if (n_evals) *n_evals = ne;
+    return NUGPR_OK;
+  }
+  return fail(NUGPR_ERR_INVALID_ARG, "bad gradient mode");
+}
+
+// ------------------------------------------------------------------------------------------
+extern "C" nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr) {
+  if (!state || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  double t = state[9] + 1.0;
+  for (int i = 0; i < 3; ++i) {
+    double m = b1 * state[3 + i] + (1.0 - b1) * grad[i];
+    double v = b2 * state[6 + i] + (1.0 - b2) * grad[i] * grad[i];
+    double mh = m / (1.0 - std::pow(b1, t));
+    double vh = v / (1.0 - std::pow(b2, t));
+    double th = state[i] - lr * mh / (std::sqrt(vh) + eps);
+    state[i] = th > 1e-8 ? th : 1e-8;
+    state[3 + i] = m;
+    state[6 + i] = v;
+  }
+  state[9] = t;
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
+                                    int32_t d, const double* reps, const double* y_sorted, int32_t kernel,
+                                    int32_t epochs, double lr, const nugpr_grad_cfg* gcfg,
+                                    const nugpr_solve_cfg* scfg, double adam_state[10], double* records,
+                                    void* workspace, size_t ws_bytes) {
+  if (!ctx || !adam_state || !gcfg || !scfg) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (epochs < 0) return fail(NUGPR_ERR_INVALID_ARG, "epochs < 0");
+  for (int ep = 0; ep < epochs; ++ep) {
+    nugpr_theta th{adam_state[0], adam_state[1], adam_state[2]};
+    nugpr_blocks* bl = nullptr;
+    int32_t fb = -1;
+    double jit = 0.0;
+    RET(nugpr_build_blocks(ctx, X_sorted, offsets, n_c, d, reps, kernel, th, workspace, ws_bytes, &bl, &fb, &jit));
+    double L0 = 0.0, g[3] = {0, 0, 0};
+    nugpr_mll_out ev[1 + 3 * 21];
+    int32_t ne = 0;
+    nugpr_status st = nugpr_numgrad(ctx, bl, y_sorted, th, gcfg, scfg, &L0, g, ev, &ne);
+    nugpr_blocks_destroy(bl);
+    if (st != NUGPR_OK) return st;
+    if (records) {
+      double* r = records + static_cast<size_t>(ep) * NUGPR_TRAIN_RECORD;
+      int ky = 0, kq = 0;
+      for (int k = 0; k < ne; ++k) { ky = std::max(ky, ev[k].iters_y); kq = std::max(kq, ev[k].iters_q_max); }
+      r[0] = L0; r[1] = g[0]; r[2] = g[1]; r[3] = g[2];
+      r[4] = th.lengthscale; r[5] = th.noise; r[6] = th.outputscale;
+      r[7] = ky; r[8] = kq; r[9] = jit; r[10] = ne; r[11] = 0.0;
+    }
+    RET(nugpr_adam_step(adam_state, g, lr));
+  }
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_tridiag_eig(int32_t k, const double* diag, const double* off, double* evals,
+                                          double* first) {
+  if (k < 1 || !diag || !evals || !first || (k > 1 && !off)) return fail(NUGPR_ERR_INVALID_ARG, "bad args");
+  std::vector<double> e(k, 0.0);
+  for (int i = 0; i + 1 < k; ++i) e[i] = off[i];
+  for (int i = 0; i < k; ++i) evals[i] = diag[i];
+  if (tql_first(k, evals, e.data(), first) != 0) return fail(NUGPR_ERR_INTERNAL, "QL did not converge");
+  return NUGPR_OK;
+}

@@ -1,0 +1,652 @@
+// build_kernels.cu — rows A1/A2 of SURVEY §8(a): on-the-fly kernel-block assembly,
+// batched per-cluster Cholesky + triangular inverse, batched FP64 GEMMs for
+// H_i = R_i^{-T} R_i^{-1} and G_i(theta') = R_i^{-T} K_i(theta') R_i^{-1}, K_rep and the
+// Lanczos lambda_0 = lambda_min(K_rep).
+//
+// Notation: L_i = R_i^T is the lower Cholesky factor of K_i, Linv_i = L_i^{-1} = R_i^{-T}.
+// Then u_i = Linv_i 1 (Eq. 21), c_i = Linv_i y_i, H_i = Linv_i Linv_i^T,
+// G_i = Linv_i K_i(theta') Linv_i^T.
+#include "common.cuh"
+#include "kernels_decl.h"
+#include "tridiag.h"
+
+#include <atomic>
+
+namespace nugpr {
+
+static std::atomic<long long> g_launches{0};
+void note_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
+
+// ---------------------------------------------------------------------------------------
+// Kernel value.  Squared distance as sum_d (x_d - x'_d)^2 with explicitly non-fused ops
+// (bitwise-symmetric blocks with an exact diagonal).
+__device__ __forceinline__ double kval(int kind, double sq, double lam, double alpha) {
+  if (kind == 0) {                       // RBF (reading X3)
+    return alpha * exp(-__ddiv_rn(sq, 2.0 * lam * lam));
+  } else if (kind == 2) {                // Eq. (2) as printed
+    return alpha * exp(-__ddiv_rn(sqrt(sq), 2.0 * lam * lam));
+  } else {                               // Matern-5/2
+    double rho = sqrt(sq);
+    double s = sqrt(5.0) * rho / lam;
+    return alpha * (1.0 + s + 5.0 * sq / (3.0 * lam * lam)) * exp(-s);
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Assemble K_i(theta) = k(X_i, X_i) + (noise + jitter_i) I into dst (ld x ld col-major),
+// padding = identity.  grid = (tiles32 x tiles32 of the largest block, #blocks in list).
+struct AsmArgs {
+  const double* X;       // n x d, cluster-sorted
+  int d;
+  const int64_t* off;
+  const int64_t* boff;
+  const int32_t* ld;
+  const int32_t* list;   // NULL => blockIdx.y is the cluster
+  const double* jitter;  // [n_c] or NULL
+  double* dst;
+  int kind;
+  double lam, noise, alpha;
+};
+
+__global__ void __launch_bounds__(256) assemble_kernel(AsmArgs a) {
+  const int i = a.list ? a.list[blockIdx.y] : blockIdx.y;
+  const int ld = a.ld[i];
+  const int nt = (ld + 31) / 32;
+  const int tr = blockIdx.x % nt, tc = blockIdx.x / nt;
+  if (tc >= nt) return;
+  const int64_t o = a.off[i];
+  const int b = static_cast<int>(a.off[i + 1] - o);
+  __shared__ double xr[32 * 33], xc[32 * 33];
+  const int d = a.d;
+  for (int idx = threadIdx.x; idx < 32 * d; idx += blockDim.x) {
+    int rr = idx / d, dd = idx % d;
+    int r = tr * 32 + rr, c = tc * 32 + rr;
+    xr[rr * 33 + dd] = (r < b) ? a.X[(o + r) * d + dd] : 0.0;
+    xc[rr * 33 + dd] = (c < b) ? a.X[(o + c) * d + dd] : 0.0;
+  }
+  __syncthreads();
+  const double diag_add = a.noise + (a.jitter ? a.jitter[i] : 0.0);
+  double* K = a.dst + a.boff[i];
+  const int rr = threadIdx.x & 31;
+  for (int cc = threadIdx.x >> 5; cc < 32; cc += 8) {
+    const int r = tr * 32 + rr, c = tc * 32 + cc;
+    if (r >= ld || c >= ld) continue;
+    double v;
+    if (r < b && c < b) {
+      double sq = 0.0;
+      for (int dd = 0; dd < d; ++dd) {
+        double df = __dsub_rn(xr[rr * 33 + dd], xc[cc * 33 + dd]);
+        sq = __dadd_rn(sq, __dmul_rn(df, df));
+      }
+      v = kval(a.kind, sq, a.lam, a.alpha);
+      if (r == c) v += diag_add;
+    } else {
+      v = (r == c) ? 1.0 : 0.0;
+    }
+    K[static_cast<int64_t>(c) * ld + r] = v;
+  }
+}
+
+void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist,
+                     int ld_max, const double* jitter, double* dst, int kind, double lam,
+                     double noise, double alpha, cudaStream_t s) {
+  AsmArgs a{X, d, L.off, L.boff, L.ld, list, jitter, dst, kind, lam, noise, alpha};
+  int nt = (ld_max + 31) / 32;
+  dim3 grid(nt * nt, list ? nlist : L.n_c);
+  assemble_kernel<<<grid, 256, 0, s>>>(a);
+  note_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// Batched Cholesky + triangular inverse, one CTA per cluster, in place.
+// Right-looking blocked Cholesky with 32-column panels staged in shared memory:
+//   for each panel: load A[k0:ld, k0:k0+nb] -> smem, unblocked factorisation of the tall
+//   panel (column scale + in-panel rank-1 updates), write back, then trailing update
+//   A[k0+nb:, k0+nb:] -= P P^T (lower triangle) from smem.
+// Then Linv = L^{-1} by tile rows:  X_II = L_II^{-1};  X_I,0:I0 = -X_II (L_I,0:I0 X_0:I0,0:I0).
+// Also: status (0 ok / 1 not SPD), logdet partial 2 sum log L_jj, u = Linv 1_b.
+constexpr int NB = 32;
+
+struct CholArgs {
+  double* A;             // block storage (in: K, out: Linv)
+  const int64_t* off;
+  const int64_t* poff;
+  const int64_t* boff;
+  const int32_t* ld;
+  const int32_t* list;
+  int32_t* status;       // [n_c]
+  double* logdet_blk;    // [n_c]
+  double* u;             // [n_pad]
+};
+
+__global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
+  const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
+  const int ld = a.ld[i];
+  const int b = static_cast<int>(a.off[i + 1] - a.off[i]);
+  double* A = a.A + a.boff[i];
+  extern __shared__ double sm[];
+  double* Pn = sm;                 // panel: (ld) x NB, col-major with leading dim ld
+  __shared__ int fail;
+  __shared__ double red[8];
+  const int tid = threadIdx.x;
+  if (tid == 0) fail = 0;
+  __syncthreads();
+
+  // ---------------- Cholesky ----------------
+  for (int k0 = 0; k0 < ld; k0 += NB) {
+    const int nb = min(NB, ld - k0);
+    const int pr = ld - k0;          // panel rows
+    for (int idx = tid; idx < pr * nb; idx += NT) {
+      int c = idx / pr, r = idx % pr;
+      Pn[c * pr + r] = A[static_cast<int64_t>(k0 + c) * ld + k0 + r];
+    }
+    __syncthreads();
+    for (int j = 0; j < nb; ++j) {
+      if (tid == 0) {
+        double piv = Pn[j * pr + j];
+        if (!(piv > 0.0)) { fail = 1; piv = 1.0; }
+        Pn[j * pr + j] = sqrt(piv);
+      }
+      __syncthreads();
+      const double ljj = Pn[j * pr + j];
+      for (int r = j + 1 + tid; r < pr; r += NT) Pn[j * pr + r] /= ljj;
+      __syncthreads();
+      // rank-1 update of panel columns c in (j, nb), rows r >= c
+      const int ncols = nb - j - 1;
+      for (int idx = tid; idx < ncols * pr; idx += NT) {
+        int c = j + 1 + idx / pr, r = idx % pr;
+        if (r >= c) Pn[c * pr + r] -= Pn[j * pr + r] * Pn[j * pr + c];
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < pr * nb; idx += NT) {
+      int c = idx / pr, r = idx % pr;
+      A[static_cast<int64_t>(k0 + c) * ld + k0 + r] = (r >= c) ? Pn[c * pr + r] : 0.0;
+    }
+    // trailing update: A[k0+nb+r][k0+nb+c] -= sum_j P[nb+r][j] P[nb+c][j], r >= c
+    const int tr = pr - nb;
+    if (tr > 0) {
+      // 4x4 register tiles over the lower triangle of the tr x tr trailing matrix
+      const int nt4 = (tr + 3) / 4;
+      const int ntiles = nt4 * (nt4 + 1) / 2;
+      for (int t = tid; t < ntiles; t += NT) {
+        // map t -> (ti >= tj)
+        int ti = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+        while (ti * (ti + 1) / 2 > t) --ti;
+        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+        int tj = t - ti * (ti + 1) / 2;
+        double acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        for (int j = 0; j < nb; ++j) {
+          double pa[4], pb[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            int r = ti * 4 + x, c = tj * 4 + x;
+            pa[x] = (r < tr) ? Pn[j * pr + nb + r] : 0.0;
+            pb[x] = (c < tr) ? Pn[j * pr + nb + c] : 0.0;
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] += pa[x] * pb[y];
+        }
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) {
+            int r = ti * 4 + x, c = tj * 4 + y;
+            if (r < tr && c < tr && r >= c)
+              A[static_cast<int64_t>(k0 + nb + c) * ld + k0 + nb + r] -= acc[x][y];
+          }
+      }
+    }
+    __syncthreads();
+  }
+  // logdet partial (real rows only; padding diagonal is 1)
+  double ls = 0.0;
+  for (int r = tid; r < b; r += NT) ls += log(A[static_cast<int64_t>(r) * ld + r]);
+  ls = warp_sum(ls);
+  if ((tid & 31) == 0) red[tid >> 5] = ls;
+  __syncthreads();
+  if (tid == 0) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += red[w];
+    a.logdet_blk[i] = 2.0 * s;
+    a.status[i] = fail;
+  }
+  __syncthreads();
+  if (fail) return;
+
+  // ---------------- triangular inverse (in place, by tile rows) ----------------
+  // Row panel I = rows [I0, I0+nb).  smem: Lrow = L[I, 0:I0+nb] (nb x (I0+nb), row-major),
+  // Xd = (L_II)^{-1} (nb x nb), Yc = (L[I,0:I0] * Xinv[0:I0, cc0:cc0+YC]) column chunk.
+  constexpr int YC = 64;
+  double* Lrow = sm;
+  for (int I0 = 0; I0 < ld; I0 += NB) {
+    const int nb = min(NB, ld - I0);
+    const int ldr = I0 + nb;
+    double* Xd = Lrow + nb * ldr;             // NB x NB (row-major)
+    double* Yc = Xd + NB * NB;                // nb x YC (row-major)
+    for (int idx = tid; idx < nb * ldr; idx += NT) {
+      int c = idx / nb, r = idx % nb;         // coalesced over r in global
+      Lrow[r * ldr + c] = A[static_cast<int64_t>(c) * ld + I0 + r];
+    }
+    __syncthreads();
+    // diagonal tile inverse: thread j < nb solves L_II x = e_j (forward substitution)
+    if (tid < nb) {
+      const int j = tid;
+      for (int r = 0; r < nb; ++r) {
+        double v = 0.0;
+        if (r >= j) {
+          v = (r == j) ? 1.0 : 0.0;
+          for (int k = j; k < r; ++k) v -= Lrow[r * ldr + I0 + k] * Xd[k * NB + j];
+          v /= Lrow[r * ldr + I0 + r];
+        }
+        Xd[r * NB + j] = v;
+      }
+    }
+    __syncthreads();
+    for (int cc0 = 0; cc0 < I0; cc0 += YC) {
+      const int ncc = min(YC, I0 - cc0);
+      // Yc[r][c] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]  (Xinv rows < I0 are final in A)
+      for (int idx = tid; idx < nb * ncc; idx += NT) {
+        int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        const double* xc = A + static_cast<int64_t>(c) * ld;
+        double acc = 0.0;
+        for (int k = c; k < I0; ++k) acc += Lrow[r * ldr + k] * xc[k];
+        Yc[r * YC + cl] = acc;
+      }
+      __syncthreads();
+      // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
+      for (int idx = tid; idx < nb * ncc; idx += NT) {
+        int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        double acc = 0.0;
+        for (int k = 0; k <= r; ++k) acc += Xd[r * NB + k] * Yc[k * YC + cl];
+        A[static_cast<int64_t>(c) * ld + I0 + r] = -acc;
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < nb * nb; idx += NT) {
+      int r = idx % nb, c = idx / nb;
+      A[static_cast<int64_t>(I0 + c) * ld + I0 + r] = (r >= c) ? Xd[r * NB + c] : 0.0;
+    }
+    // strict upper triangle right of the diagonal tile := 0
+    for (int idx = tid; idx < nb * (ld - I0 - nb); idx += NT) {
+      int r = idx % nb, c = I0 + nb + idx / nb;
+      A[static_cast<int64_t>(c) * ld + I0 + r] = 0.0;
+    }
+    __syncthreads();
+  }
+  // u = Linv * 1_b  (row sums over the real columns); rows >= b are padding => 0
+  const int64_t p0 = a.poff[i];
+  for (int r = tid; r < ld; r += NT) {
+    double acc = 0.0;
+    if (r < b)
+      for (int k = 0; k <= r; ++k) acc += A[static_cast<int64_t>(k) * ld + r];
+    a.u[p0 + r] = acc;
+  }
+}
+
+size_t chol_smem_bytes(int ld_max) {
+  size_t panel = static_cast<size_t>(ld_max) * NB;                         // Cholesky panel
+  size_t inv = static_cast<size_t>(NB) * ld_max + NB * NB + static_cast<size_t>(NB) * 64;
+  return sizeof(double) * (panel > inv ? panel : inv);
+}
+
+void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
+                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s) {
+  CholArgs a{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
+  size_t smem = chol_smem_bytes(ld_max);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(chol_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
+  note_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// Batched FP64 GEMM on cluster blocks: C_i = A_i * op(B_i), all ld_i x ld_i col-major.
+//   op(B)(k,c) = TRANSB ? B[k*ld + c] (= B^T) : B[c*ld + k]
+//   A_LOWER: A(r,k) = 0 for k > r;  B_LOWERT: op(B)(k,c) = 0 for k > c (B^T of a lower matrix)
+//   SYM: C symmetric — only tiles with tile_r >= tile_c are computed and mirrored.
+// 64x64 tiles, 256 threads, 4x4 register tile per thread, K step 16 in shared memory.
+struct GemmArgs {
+  const double* A;
+  const double* B;
+  double* C;
+  const int64_t* boff;
+  const int32_t* ld;
+  int ntile_max;         // tiles per dimension of the largest block
+};
+
+template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM>
+__global__ void __launch_bounds__(256) gemm_blocks_kernel(GemmArgs g) {
+  const int i = blockIdx.y;
+  const int ld = g.ld[i];
+  const int nt = (ld + 63) / 64;
+  int tr, tc;
+  if (SYM) {
+    int t = blockIdx.x;
+    if (t >= nt * (nt + 1) / 2) return;
+    tr = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (tr * (tr + 1) / 2 > t) --tr;
+    while ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
+    tc = t - tr * (tr + 1) / 2;
+  } else {
+    if (static_cast<int>(blockIdx.x) >= nt * nt) return;
+    tr = blockIdx.x % nt;
+    tc = blockIdx.x / nt;
+  }
+  const int64_t bo = g.boff[i];
+  const double* A = g.A + bo;
+  const double* B = g.B + bo;
+  double* C = g.C + bo;
+  const int r0 = tr * 64, c0 = tc * 64;
+  int kend = ld;
+  if (A_LOWER) kend = min(kend, r0 + 64);
+  if (B_LOWERT) kend = min(kend, c0 + 64);
+  __shared__ double As[16][64 + 2];
+  __shared__ double Bs[16][64 + 2];
+  const int tid = threadIdx.x;
+  const int tx = tid & 15, ty = tid >> 4;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+  for (int k0 = 0; k0 < kend; k0 += 16) {
+    // A tile: rows r0..r0+63, k0..k0+15 ; load coalesced over rows
+    for (int idx = tid; idx < 16 * 64; idx += 256) {
+      int kk = idx / 64, rr = idx % 64;
+      int r = r0 + rr, k = k0 + kk;
+      As[kk][rr] = (r < ld && k < ld) ? A[static_cast<int64_t>(k) * ld + r] : 0.0;
+    }
+    for (int idx = tid; idx < 16 * 64; idx += 256) {
+      int kk, cc;
+      if (TRANSB) { kk = idx / 64; cc = idx % 64; }
+      else        { cc = idx / 16; kk = idx % 16; }
+      int c = c0 + cc, k = k0 + kk;
+      double v = 0.0;
+      if (c < ld && k < ld) v = TRANSB ? B[static_cast<int64_t>(k) * ld + c] : B[static_cast<int64_t>(c) * ld + k];
+      Bs[kk][cc] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      double a4[4], b4[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) a4[x] = As[kk][ty + 16 * x];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) b4[y] = Bs[kk][tx + 16 * y];
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a4[x], b4[y], acc[x][y]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      int r = r0 + ty + 16 * x, c = c0 + tx + 16 * y;
+      if (r < ld && c < ld) {
+        if (SYM) {
+          if (r >= c) {
+            C[static_cast<int64_t>(c) * ld + r] = acc[x][y];
+            C[static_cast<int64_t>(r) * ld + c] = acc[x][y];
+          }
+        } else {
+          C[static_cast<int64_t>(c) * ld + r] = acc[x][y];
+        }
+      }
+    }
+}
+
+// H = Linv * Linv^T (symmetric)
+void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s) {
+  int nt = (ld_max + 63) / 64;
+  GemmArgs g{Linv, Linv, H, L.boff, L.ld, nt};
+  gemm_blocks_kernel<true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  note_launch();
+}
+// T = K * Linv^T
+void launch_gemm_KLt(const double* K, const double* Linv, double* T, const LayoutDev& L, int ld_max,
+                     cudaStream_t s) {
+  int nt = (ld_max + 63) / 64;
+  GemmArgs g{K, Linv, T, L.boff, L.ld, nt};
+  gemm_blocks_kernel<true, false, true, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
+  note_launch();
+}
+// G = Linv * T (symmetric)
+void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max,
+                    cudaStream_t s) {
+  int nt = (ld_max + 63) / 64;
+  GemmArgs g{Linv, T, G, L.boff, L.ld, nt};
+  gemm_blocks_kernel<false, true, false, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  note_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// Fixed-order sum of n doubles (single CTA) -> out[0].
+__global__ void sum_kernel(const double* v, int n, double* out) {
+  __shared__ double red[NT];
+  double s = 0.0;
+  const int per = (n + NT - 1) / NT;
+  const int lo = threadIdx.x * per, hi = min(n, lo + per);
+  for (int k = lo; k < hi; ++k) s += v[k];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int k = 0; k < NT; ++k) t += red[k];
+    out[0] = t;
+  }
+}
+void launch_sum(const double* v, int n, double* out, cudaStream_t s) {
+  sum_kernel<<<1, NT, 0, s>>>(v, n, out);
+  note_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// K_rep(theta) = k(r_i, r_j) (no noise, Eq. 22 / SPEC.md:74), n_c x n_c row-major.
+__global__ void krep_kernel(const double* reps, int n_c, int d, int kind, double lam, double alpha,
+                            double* K) {
+  int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(n_c) * n_c) return;
+  int r = static_cast<int>(idx / n_c), c = static_cast<int>(idx % n_c);
+  double sq = 0.0;
+  for (int dd = 0; dd < d; ++dd) {
+    double df = __dsub_rn(reps[r * d + dd], reps[c * d + dd]);
+    sq = __dadd_rn(sq, __dmul_rn(df, df));
+  }
+  K[idx] = kval(kind, sq, lam, alpha);
+}
+void launch_krep(const double* reps, int n_c, int d, int kind, double lam, double alpha, double* K,
+                 cudaStream_t s) {
+  int64_t tot = static_cast<int64_t>(n_c) * n_c;
+  krep_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(reps, n_c, d, kind, lam, alpha, K);
+  note_launch();
+}
+
+// ---------------------------------------------------------------------------------------
+// lambda_0 = lambda_min(K_rep) by Lanczos with full (twice classical Gram-Schmidt)
+// reorthogonalisation, single CTA of 1024 threads.  Converged when the Ritz residual
+// beta_{k+1} |s_k| <= tol_rel * ||K||_inf.  Writes lam0, the Ritz vector v0 (warm start for
+// the next solve) and M = K - lam0 I.  ws: (kmax+1) x n_c doubles of Lanczos vectors.
+struct LanczosArgs {
+  const double* K;       // n_c x n_c
+  int n_c;
+  const double* vinit;   // NULL or n_c
+  double* V;             // (kmax+1) x n_c
+  int kmax;
+  double tol_rel;
+  double* lam0;          // [1]
+  double* v0;            // [n_c] out
+  double* M;             // n_c x n_c out (K - lam0 I)
+  int32_t* info;         // [2] {iterations, converged}
+  double* tri;           // scratch 6*kmax
+};
+
+__global__ void __launch_bounds__(1024) lanczos_kernel(LanczosArgs a) {
+  const int n = a.n_c;
+  const int tid = threadIdx.x;
+  const int nthr = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
+  extern __shared__ double sm[];
+  double* w = sm;                  // n
+  double* h = w + n;               // kmax+1
+  __shared__ double red[32];
+  __shared__ double s_alpha, s_beta, s_norm;
+  __shared__ int s_done;
+  double* alph = a.tri;            // kmax
+  double* bet = a.tri + a.kmax;    // kmax  (bet[k] couples k and k+1)
+  double* ta = a.tri + 2 * a.kmax; // copies for the tridiagonal solve
+  double* tb = a.tri + 3 * a.kmax;
+  double* sv = a.tri + 4 * a.kmax; // eigenvector (kmax) + scratch beyond
+  // ||K||_inf
+  double rmax = 0.0;
+  for (int r = wid; r < n; r += nw) {
+    double s = 0.0;
+    for (int c = lane; c < n; c += 32) s += fabs(a.K[static_cast<int64_t>(r) * n + c]);
+    s = warp_sum(s);
+    rmax = fmax(rmax, s);
+  }
+  if (lane == 0) red[wid] = rmax;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int k = 0; k < nw; ++k) m = fmax(m, red[k]);
+    s_norm = m;
+    s_done = 0;
+  }
+  __syncthreads();
+  // v_0
+  for (int r = tid; r < n; r += nthr) {
+    double v = a.vinit ? a.vinit[r] : (probe_value(0x5eed1a2c5ull, 0, r) * (1.0 + 0.01 * (r % 7)));
+    w[r] = v;
+  }
+  __syncthreads();
+  auto block_sum = [&](double v) -> double {
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[wid] = v;
+    __syncthreads();
+    double t = 0.0;
+    for (int k = 0; k < nw; ++k) t += red[k];
+    return t;
+  };
+  {
+    double s = 0.0;
+    for (int r = tid; r < n; r += nthr) s += w[r] * w[r];
+    double nrm = sqrt(block_sum(s));
+    for (int r = tid; r < n; r += nthr) a.V[r] = w[r] / nrm;
+  }
+  __syncthreads();
+  int k_final = 0;
+  int converged = 0;
+  double theta = 0.0;
+  for (int k = 0; k < a.kmax; ++k) {
+    const double* vk = a.V + static_cast<int64_t>(k) * n;
+    // w = K v_k (warp per row)
+    for (int r = wid; r < n; r += nw) {
+      const double* Kr = a.K + static_cast<int64_t>(r) * n;
+      double s = 0.0;
+      for (int c = lane; c < n; c += 32) s += Kr[c] * vk[c];
+      s = warp_sum(s);
+      if (lane == 0) w[r] = s;
+    }
+    __syncthreads();
+    // two passes of classical Gram-Schmidt against v_0..v_k (includes alpha_k = v_k^T w)
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = wid; j <= k; j += nw) {
+        const double* vj = a.V + static_cast<int64_t>(j) * n;
+        double s = 0.0;
+        for (int c = lane; c < n; c += 32) s += vj[c] * w[c];
+        s = warp_sum(s);
+        if (lane == 0) h[j] = s;
+      }
+      __syncthreads();
+      if (pass == 0 && tid == 0) s_alpha = h[k];
+      if (pass == 1 && tid == 0) s_alpha += h[k];
+      for (int r = tid; r < n; r += nthr) {
+        double s = w[r];
+        for (int j = 0; j <= k; ++j) s -= h[j] * a.V[static_cast<int64_t>(j) * n + r];
+        w[r] = s;
+      }
+      __syncthreads();
+    }
+    double s = 0.0;
+    for (int r = tid; r < n; r += nthr) s += w[r] * w[r];
+    double beta = sqrt(block_sum(s));
+    if (tid == 0) {
+      alph[k] = s_alpha;
+      bet[k] = beta;
+      s_beta = beta;
+    }
+    __syncthreads();
+    const int kk = k + 1;
+    const bool last = (kk == a.kmax) || (kk == n) || !(beta > 1e-300);
+    if (tid == 0 && (last || (kk % 4 == 0))) {
+      for (int t = 0; t < kk; ++t) { ta[t] = alph[t]; tb[t] = bet[t]; }
+      theta = tridiag_min_eig(kk, ta, tb);
+      tridiag_eigvec(kk, ta, tb, theta, sv, sv + a.kmax);
+      double res = fabs(bet[k] * sv[kk - 1]);
+      if (res <= a.tol_rel * s_norm || last) {
+        s_done = 1;
+        converged = (res <= a.tol_rel * s_norm) || !(beta > 1e-300) || (kk == n);
+      }
+    }
+    __syncthreads();
+    if (s_done) { k_final = kk; break; }
+    for (int r = tid; r < n; r += nthr) a.V[static_cast<int64_t>(k + 1) * n + r] = w[r] / s_beta;
+    __syncthreads();
+  }
+  // Ritz vector v0 = V s, normalised; lam0; M = K - lam0 I
+  __shared__ double s_theta;
+  if (tid == 0) { s_theta = theta; a.lam0[0] = theta; a.info[0] = k_final; a.info[1] = converged; }
+  __syncthreads();
+  double ss = 0.0;
+  for (int r = tid; r < n; r += nthr) {
+    double v = 0.0;
+    for (int j = 0; j < k_final; ++j) v += a.V[static_cast<int64_t>(j) * n + r] * sv[j];
+    w[r] = v;
+    ss += v * v;
+  }
+  double nrm = sqrt(block_sum(ss));
+  for (int r = tid; r < n; r += nthr) a.v0[r] = w[r] / nrm;
+  const double l0 = s_theta;
+  for (int64_t idx = tid; idx < static_cast<int64_t>(n) * n; idx += nthr) {
+    int r = static_cast<int>(idx / n), c = static_cast<int>(idx % n);
+    a.M[idx] = a.K[idx] - (r == c ? l0 : 0.0);
+  }
+}
+
+size_t lanczos_scratch_doubles(int n_c, int kmax) {
+  return static_cast<size_t>(kmax + 1) * n_c + 8 * static_cast<size_t>(kmax) + 64;
+}
+
+void launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
+                    double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
+                    cudaStream_t s) {
+  LanczosArgs a;
+  a.K = K; a.n_c = n_c; a.vinit = vinit; a.V = scratch; a.kmax = kmax; a.tol_rel = tol_rel;
+  a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info;
+  a.tri = scratch + static_cast<size_t>(kmax + 1) * n_c;
+  size_t smem = sizeof(double) * (static_cast<size_t>(n_c) + kmax + 1);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  lanczos_kernel<<<1, 1024, smem, s>>>(a);
+  note_launch();
+}
+
+}  // namespace nugpr

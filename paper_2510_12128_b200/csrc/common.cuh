@@ -1,0 +1,162 @@
+// common.cuh — device-side layout and state shared by the nuGPR kernels.
+//
+// Internal data layout in HBM:
+//  * Clusters are padded to ld_i = round_up(b_i, 8) rows ("padded rows", reading P19); the
+//    padding rows are identity rows in every block matrix and zero in every vector, so they
+//    are exactly invisible to the method.
+//  * Vectors: column-major [NC][n_pad] FP64 (one contiguous length-n_pad column per RHS;
+//    column 0 = the y-solve, columns 1..m = the Hutchinson probes).
+//  * Block matrices (Linv_i, H_i, G_i): dense ld_i x ld_i column-major at boff[i];
+//    H and G are stored full (both triangles) so the apply streams them coalesced.
+//  * Row tiles: a cluster is split into tiles of <= TILE_ROWS padded rows; each apply /
+//    update CTA owns one tile; per-tile partial sums (S = W^T D partials, dots) live in
+//    [n_tiles][16] arrays and are reduced in fixed tile order (deterministic).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace nugpr {
+
+constexpr int MAXC = 16;        // max columns per apply (1 + m)
+constexpr int NT = 256;         // threads per CTA for the tile kernels
+constexpr int TILE_ROWS = 256;  // max padded rows per tile
+constexpr int PAD = 8;          // cluster padding granularity (rows)
+
+struct TileDesc {
+  int32_t blk;    // cluster index
+  int32_t row0;   // first padded row within the cluster
+  int32_t nrows;  // rows in this tile (even)
+  int32_t pad_;
+};
+
+struct LayoutDev {
+  const int64_t* off;    // [n_c+1] original (unpadded) row offsets
+  const int64_t* poff;   // [n_c+1] padded row offsets
+  const int64_t* boff;   // [n_c] element offset of block i in block storage
+  const int32_t* ld;     // [n_c] padded cluster size
+  const TileDesc* tiles; // [n_tiles]
+  const int32_t* tile0;  // [n_c+1] tile range of each cluster
+  int32_t n_c;
+  int32_t n_tiles;
+  int64_t n;             // unpadded rows
+  int64_t n_pad;         // padded rows (vector column stride)
+};
+
+// Per-evaluation operator parameters (device resident so one captured graph serves all
+// evaluation modes).  A D = a*D + b_i*B_i*D + u_i*(mscale * Mp S)_i with b_i = b0 + b1*jitter_i.
+struct EvalParams {
+  double a;
+  double b0, b1;
+  const double* B;       // H or G (block storage layout), NULL => no block term
+  const double* Mp;      // n_c x n_c row-major
+  double mscale;
+  double tol;
+  int32_t max_iter;
+  int32_t replay;        // 1 => active_j = iters_j < replay_iters[j]
+  int32_t replay_iters[MAXC];
+  int32_t ncol;
+  int32_t mode;
+};
+
+// CG state for up to MAXC columns, updated only by "last CTA" finalisers.
+struct CGState {
+  double rr[MAXC];        // r^T r (current)
+  double rr0[MAXC];       // ||rhs||^2
+  double alpha[MAXC];
+  double beta[MAXC];
+  int32_t active[MAXC];
+  int32_t iters[MAXC];
+  int32_t any_active;
+  int32_t par;            // ping-pong parity of the P / S(P) buffers
+  int32_t hit_max;        // some column stopped at max_iter unconverged
+  int32_t pad_;
+  double quad;
+  double t[MAXC];         // Pade trace terms
+  unsigned int ticket[8]; // last-CTA counters (self-resetting)
+};
+
+enum FinKind { FIN_NONE = 0, FIN_INIT = 1, FIN_ALPHA = 2, FIN_UPDATE = 3, FIN_TRACE = 4 };
+enum EpiKind { EPI_S = 0, EPI_DOT = 1 };
+
+struct ApplyArgs {
+  LayoutDev L;
+  const EvalParams* prm;
+  CGState* st;
+  const double* u;         // [n_pad]
+  const double* jitter;    // [n_c]
+  // input D
+  const double* D;         // [NC][n_pad]; with fuse_p this is R
+  const double* S_D;       // [n_tiles][16] partials of S(D) (fuse_p: S(R))
+  int fuse_p;              // D := R + beta o P_old (active columns), P_new written
+  double* Pbuf[2];         // P ping-pong
+  double* SPbuf[2];        // S(P) ping-pong partials
+  int use_par_p2;          // P2 := Pbuf[par^1] (current search direction)
+  // output
+  double* out;
+  const double* P2;        // combine term (or NULL)
+  double cA[MAXC], cV[MAXC], cP[MAXC];
+  int epi;                 // EpiKind
+  double* Sout;            // EPI_S: partials of u^T out
+  const double* Y2;        // EPI_DOT: partner of the dot
+  double* dots;            // EPI_DOT: partials of out . Y2
+  int fin;                 // FinKind (FIN_ALPHA or FIN_TRACE)
+  int gate;                // return immediately when !st->any_active
+  int ncol;
+  double* alpha_hist;      // [MAXC][hist_stride]
+  int hist_stride;
+};
+
+struct UpdateArgs {
+  LayoutDev L;
+  const EvalParams* prm;
+  CGState* st;
+  const double* u;
+  double* X;
+  double* R;
+  const double* Q;
+  double* Pbuf[2];
+  double* rr_part;         // [n_tiles][16]
+  double* SR_part;         // [n_tiles][16]
+  double* beta_hist;       // [MAXC][hist_stride]
+  int hist_stride;
+  int ncol;
+};
+
+struct RhsArgs {
+  LayoutDev L;
+  const EvalParams* prm;
+  CGState* st;
+  const double* Linv;
+  const double* y;         // [n] cluster-sorted (unpadded)
+  const double* probes;    // NULL or [m][n]
+  uint64_t seed;
+  const double* u;
+  double* RHS;             // [NC][n_pad]
+  double* R;
+  double* X;
+  double* P0;              // Pbuf[0]
+  double* SP0;             // SPbuf[0]
+  double* SR_part;
+  double* rr_part;
+  int ncol;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// splitmix64 counter generator (identical definition in synth/__init__.py `probes`).
+__host__ __device__ __forceinline__ uint64_t splitmix64_at(uint64_t seed, uint64_t ctr) {
+  uint64_t x = seed + (ctr + 1ull) * 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ double probe_value(uint64_t seed, int j, int64_t p) {
+  uint64_t ctr = (static_cast<uint64_t>(j) << 40) | static_cast<uint64_t>(p);
+  return (splitmix64_at(seed, ctr) >> 63) ? -1.0 : 1.0;
+}
+
+}  // namespace nugpr

@@ -1,0 +1,608 @@
+// eval_kernels.cu — rows A3-A7 of SURVEY §8(a): the fused multi-RHS apply of
+// A = R^{-T} K''(theta) R^{-1} (Eq. 18-21, 23-25), the fused PCG update
+// (PAPER.md:107-108, 124), the Pade trace (Eq. 9-10, 16), the SLQ
+// log-det from the CG coefficients and the MLL assembly (Eq. 3).
+//
+// One evaluation = rhs_init -> { apply(A p) -> apply(Q(A) p) -> update }* -> spart(X) ->
+// apply(A X) -> apply(3 A^2 X - 3 X, dotted with Z) -> final.  Every global reduction
+// (S = W^T D, p^T q, r^T r, the trace dots) is written as per-tile partials and summed by
+// the last CTA to finish, in fixed tile order: results are bit-reproducible.
+#include "common.cuh"
+#include "kernels_decl.h"
+#include "tridiag.h"
+
+namespace nugpr {
+
+// Block-wide fixed-order reduction of NCP per-thread values -> out[0..NCP) (smem).
+template <int NCP>
+__device__ __forceinline__ void block_reduce_cols(double (&v)[NCP], double* sred, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) v[c] = warp_sum(v[c]);
+  __syncthreads();
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) sred[wid * NCP + c] = v[c];
+  }
+  __syncthreads();
+  if (threadIdx.x < NCP) {
+    double s = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s += sred[w * NCP + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  __syncthreads();
+}
+
+// Last-CTA election (threadfence reduction pattern): true in every thread of the last CTA.
+__device__ __forceinline__ bool last_cta(unsigned int* ticket) {
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned int t = atomicAdd(ticket, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last) __threadfence();
+  return s_last != 0;
+}
+
+// Fixed-order sum of column c of per-tile partials [n_tiles][MAXC]; result in thread 0.
+__device__ double sum_tiles(const double* part, int n_tiles, int c, double* sred) {
+  const int per = (n_tiles + NT - 1) / NT;
+  const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
+  double s = 0.0;
+  for (int t = lo; t < hi; ++t) s += part[t * MAXC + c];
+  __syncthreads();
+  sred[threadIdx.x] = s;
+  __syncthreads();
+  double tot = 0.0;
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NT; ++k) tot += sred[k];
+  __syncthreads();
+  return tot;
+}
+
+// Column activity rule (PAPER.md:406 tol/max_iter, readings P3, P5; replay for parity).
+__device__ __forceinline__ int is_active(const EvalParams* P, int c, int iters, double rr) {
+  if (P->replay) return iters < P->replay_iters[c];
+  if (iters >= P->max_iter) return 0;
+  if (sqrt(rr) < P->tol) return 0;
+  if (!(rr > 0.0)) return 0;
+  return 1;
+}
+
+// ---------------------------------------------------------------------------------------
+// rhs_init: RHS col 0 = c = Linv y (per-cluster lower trmv), cols 1..m = probes z_j;
+// R = P_0 = RHS, X = 0; partials of r^T r and S(R); the last CTA initialises the CG state.
+__global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
+  extern __shared__ double sm[];
+  const int t = blockIdx.x;
+  const TileDesc td = a.L.tiles[t];
+  const int i = td.blk;
+  const int ld = a.L.ld[i];
+  const int64_t p0 = a.L.poff[i];
+  const int64_t o = a.L.off[i];
+  const int b = static_cast<int>(a.L.off[i + 1] - o);
+  const int64_t n_pad = a.L.n_pad;
+  const int64_t n = a.L.n;
+  const int ncol = a.ncol;
+  double* ys = sm;                      // ld
+  double* sred = ys + ld;               // NT * MAXC
+  double* outv = sred + NT * MAXC;      // MAXC
+  for (int k = threadIdx.x; k < ld; k += NT) ys[k] = (k < b) ? a.y[o + k] : 0.0;
+  __syncthreads();
+  const double* Li = a.Linv + a.L.boff[i];
+  double rr[MAXC], sr[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) { rr[c] = 0.0; sr[c] = 0.0; }
+  for (int rl = threadIdx.x; rl < td.nrows; rl += NT) {
+    const int r = td.row0 + rl;
+    const int64_t g = p0 + r;
+    const double uu = a.u[g];
+    double cval = 0.0;
+    if (r < b)
+      for (int k = 0; k <= r; ++k) cval += Li[static_cast<int64_t>(k) * ld + r] * ys[k];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c) {
+      if (c >= ncol) break;
+      double v;
+      if (c == 0) v = cval;
+      else if (r >= b) v = 0.0;
+      else v = a.probes ? a.probes[static_cast<int64_t>(c - 1) * n + o + r] : probe_value(a.seed, c - 1, o + r);
+      const int64_t gi = c * n_pad + g;
+      a.RHS[gi] = v;
+      a.R[gi] = v;
+      a.P0[gi] = v;
+      a.X[gi] = 0.0;
+      rr[c] += v * v;
+      sr[c] += uu * v;
+    }
+  }
+  block_reduce_cols<MAXC>(rr, sred, outv);
+  if (threadIdx.x < MAXC) a.rr_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+  __syncthreads();
+  block_reduce_cols<MAXC>(sr, sred, outv);
+  if (threadIdx.x < MAXC) {
+    a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+    a.SP0[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+  }
+  if (last_cta(&a.st->ticket[FIN_INIT])) {
+    CGState* st = a.st;
+    int any = 0;
+    for (int c = 0; c < ncol; ++c) {
+      double tot = sum_tiles(a.rr_part, a.L.n_tiles, c, sred);
+      if (threadIdx.x == 0) {
+        st->rr[c] = tot;
+        st->rr0[c] = tot;
+        st->alpha[c] = 0.0;
+        st->beta[c] = 0.0;
+        st->iters[c] = 0;
+        st->active[c] = is_active(a.prm, c, 0, tot);
+        any |= st->active[c];
+        st->t[c] = 0.0;
+      }
+    }
+    if (threadIdx.x == 0) {
+      for (int c = ncol; c < MAXC; ++c) { st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0; }
+      st->any_active = any;
+      st->par = 0;
+      st->hit_max = 0;
+      st->quad = 0.0;
+      st->ticket[FIN_INIT] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused apply on one row tile of cluster i:
+//   D_i    = (fuse_p ? R + beta o P_old : D) staged in smem (all ld_i rows)
+//   T_i    = mscale * sum_j Mp[i][j] S_j(D)                       (low-rank, Eq. 19-21)
+//   BD     = B_i D_i (rows of this tile; B = H or G streamed from HBM, 16-byte loads)
+//   val    = a D + b_i BD + u_i T_i                                (Eq. 23-25 modes)
+//   out    = cA val + cV D + cP P2                                 (Q(A) / trace combines)
+// Epilogue: per-tile partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
+template <int NCP>
+__global__ void __launch_bounds__(NT) apply_kernel(ApplyArgs a) {
+  if (a.gate && !a.st->any_active) return;
+  extern __shared__ double sm[];
+  const int t = blockIdx.x;
+  const int tid = threadIdx.x;
+  const TileDesc td = a.L.tiles[t];
+  const int i = td.blk, ld = a.L.ld[i], row0 = td.row0, nrows = td.nrows;
+  const int64_t p0 = a.L.poff[i], n_pad = a.L.n_pad;
+  const int n_c = a.L.n_c;
+  const int ncol = a.ncol;
+  const EvalParams* P = a.prm;
+  const int par = a.st->par;
+  double* Dsm = sm;                        // ld * NCP   (row-major: Dsm[k*NCP + c])
+  double* red = Dsm + ld * NCP;            // NT * 2 * NCP
+  double* sred = red + NT * 2 * NCP;       // NT * NCP (>= NT)
+  double* Tsm = sred + NT * NCP;           // NCP
+  double* Esm = Tsm + NCP;                 // NCP
+  double* cb = Esm + NCP;                  // NCP: beta ; NCP: active
+  if (tid < NCP) {
+    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
+    cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
+  }
+  __syncthreads();
+  const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
+  double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+  // 1. stage D_i
+  for (int idx = tid; idx < ld * NCP; idx += NT) {
+    const int c = idx / ld, k = idx % ld;
+    double v = 0.0;
+    if (c < ncol) {
+      const int64_t g = c * n_pad + p0 + k;
+      if (a.fuse_p) {
+        const double po = Pold[g];
+        v = (cb[NCP + c] != 0.0) ? a.D[g] + cb[c] * po : po;
+        if (k >= row0 && k < row0 + nrows) Pnew[g] = v;
+      } else {
+        v = a.D[g];
+      }
+    }
+    Dsm[k * NCP + c] = v;
+  }
+  if (a.fuse_p && tid < ncol) {
+    const double sr = a.S_D[t * MAXC + tid], sp = a.SPbuf[par][t * MAXC + tid];
+    a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
+  }
+  // 2. low-rank coefficient T_i = sum_j Mp[i][j] S_j
+  {
+    double tacc[NCP];
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+    const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
+    const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
+    for (int j = tid; j < n_c; j += NT) {
+      const double m = Mrow[j];
+      const int tb = a.L.tile0[j], te = a.L.tile0[j + 1];
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) {
+        double s = 0.0;
+        for (int tt = tb; tt < te; ++tt) {
+          double v = a.S_D[tt * MAXC + c];
+          if (a.fuse_p) v = (cb[NCP + c] != 0.0) ? v + cb[c] * SPo[tt * MAXC + c] : SPo[tt * MAXC + c];
+          s += v;
+        }
+        tacc[c] += m * s;
+      }
+    }
+    block_reduce_cols<NCP>(tacc, sred, Tsm);   // includes __syncthreads (Dsm ready too)
+  }
+  // 3. block term BD = B_i D_i for rows [row0, row0+nrows), k split over KS groups
+  const double* B = P->B;
+  const bool useB = (B != nullptr);
+  const int RP = nrows >> 1;
+  int KS = NT / RP;
+  if (KS < 1) KS = 1;
+  const int grp = tid / RP, rp = tid % RP;
+  double acc0[NCP], acc1[NCP];
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
+  if (useB) {
+    if (grp < KS) {
+      const double* Bi = B + a.L.boff[i];
+      const int r = row0 + 2 * rp;
+      const int kchunk = (((ld + KS - 1) / KS) + 3) & ~3;
+      const int kb = grp * kchunk;
+      const int ke = min(ld, kb + kchunk);
+      const double* bp = Bi + static_cast<int64_t>(kb) * ld + r;
+      int k = kb;
+      for (; k + 4 <= ke; k += 4) {
+        double2 bb[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bb[q] = __ldg(reinterpret_cast<const double2*>(bp + static_cast<int64_t>(q) * ld));
+        bp += static_cast<int64_t>(4) * ld;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const double2* dk = reinterpret_cast<const double2*>(Dsm + (k + q) * NCP);
+#pragma unroll
+          for (int c2 = 0; c2 < NCP / 2; ++c2) {
+            const double2 dv = dk[c2];
+            acc0[2 * c2] = fma(bb[q].x, dv.x, acc0[2 * c2]);
+            acc0[2 * c2 + 1] = fma(bb[q].x, dv.y, acc0[2 * c2 + 1]);
+            acc1[2 * c2] = fma(bb[q].y, dv.x, acc1[2 * c2]);
+            acc1[2 * c2 + 1] = fma(bb[q].y, dv.y, acc1[2 * c2 + 1]);
+          }
+        }
+      }
+      for (; k < ke; ++k, bp += ld) {
+        const double2 b2 = __ldg(reinterpret_cast<const double2*>(bp));
+        const double2* dk = reinterpret_cast<const double2*>(Dsm + k * NCP);
+#pragma unroll
+        for (int c2 = 0; c2 < NCP / 2; ++c2) {
+          const double2 dv = dk[c2];
+          acc0[2 * c2] = fma(b2.x, dv.x, acc0[2 * c2]);
+          acc0[2 * c2 + 1] = fma(b2.x, dv.y, acc0[2 * c2 + 1]);
+          acc1[2 * c2] = fma(b2.y, dv.x, acc1[2 * c2]);
+          acc1[2 * c2 + 1] = fma(b2.y, dv.y, acc1[2 * c2 + 1]);
+        }
+      }
+      if (grp > 0) {
+        double* dst = red + ((grp - 1) * RP + rp) * 2 * NCP;
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) { dst[c] = acc0[c]; dst[NCP + c] = acc1[c]; }
+      }
+    }
+    __syncthreads();
+    if (grp == 0) {
+      for (int gg = 1; gg < KS; ++gg) {
+        const double* src = red + ((gg - 1) * RP + rp) * 2 * NCP;
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) { acc0[c] += src[c]; acc1[c] += src[NCP + c]; }
+      }
+    }
+  }
+  // 4. epilogue (group 0 owns row pairs)
+  double ep[NCP];
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
+  if (grp == 0) {
+    const double bi = P->b0 + P->b1 * a.jitter[i];
+    const double pa = P->a, ms = P->mscale;
+    const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+    const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int r = row0 + 2 * rp + h;
+      const int64_t gl = p0 + r;
+      const double uu = a.u[gl];
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) {
+        if (c < ncol) {
+          const double d = Dsm[r * NCP + c];
+          const double bd = (h == 0) ? acc0[c] : acc1[c];
+          double val = pa * d;
+          if (useB) val += bi * bd;
+          val += uu * (ms * Tsm[c]);
+          double o = a.cA[c] * val + a.cV[c] * d;
+          if (P2) o += a.cP[c] * P2[c * n_pad + gl];
+          a.out[c * n_pad + gl] = o;
+          ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
+        }
+      }
+    }
+  }
+  block_reduce_cols<NCP>(ep, sred, Esm);
+  if (tid < ncol) {
+    if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = Esm[tid];
+    else a.dots[t * MAXC + tid] = Esm[tid];
+  }
+  // 5. finaliser
+  if (a.fin != FIN_NONE) {
+    if (last_cta(&a.st->ticket[a.fin])) {
+      CGState* st = a.st;
+      for (int c = 0; c < ncol; ++c) {
+        const double tot = sum_tiles(a.dots, a.L.n_tiles, c, sred);
+        if (tid == 0) {
+          if (a.fin == FIN_ALPHA) {
+            if (st->active[c]) {
+              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
+              st->alpha[c] = al;
+              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
+            }
+          } else {  // FIN_TRACE
+            if (c == 0) st->quad = tot; else st->t[c] = tot;
+          }
+        }
+      }
+      if (tid == 0) st->ticket[a.fin] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// CG update: x += alpha p, r -= alpha q (active columns); partials of r^T r and S(r);
+// the last CTA forms beta = r'^T r' / r^T r, records it, advances counters and freezes.
+template <int NCP>
+__global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
+  CGState* st = a.st;
+  if (!st->any_active) return;
+  __shared__ double sred[NT * MAXC];
+  __shared__ double outv[MAXC];
+  __shared__ double cal[NCP], cact[NCP];
+  const int t = blockIdx.x;
+  const TileDesc td = a.L.tiles[t];
+  const int i = td.blk;
+  const int64_t p0 = a.L.poff[i] + td.row0, n_pad = a.L.n_pad;
+  const int ncol = a.ncol;
+  const int par = st->par;
+  const double* Pc = a.Pbuf[par ^ 1];
+  if (threadIdx.x < NCP) {
+    cal[threadIdx.x] = (threadIdx.x < ncol) ? st->alpha[threadIdx.x] : 0.0;
+    cact[threadIdx.x] = (threadIdx.x < ncol) ? static_cast<double>(st->active[threadIdx.x]) : 0.0;
+  }
+  __syncthreads();
+  double rr[NCP], sr[NCP];
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) { rr[c] = 0.0; sr[c] = 0.0; }
+  for (int rl = threadIdx.x; rl < td.nrows; rl += NT) {
+    const int64_t g = p0 + rl;
+    const double uu = a.u[g];
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) {
+      if (c < ncol && cact[c] != 0.0) {
+        const int64_t gi = c * n_pad + g;
+        const double al = cal[c];
+        a.X[gi] = a.X[gi] + al * Pc[gi];
+        const double rv = a.R[gi] - al * a.Q[gi];
+        a.R[gi] = rv;
+        rr[c] += rv * rv;
+        sr[c] += uu * rv;
+      }
+    }
+  }
+  block_reduce_cols<NCP>(rr, sred, outv);
+  if (threadIdx.x < ncol) a.rr_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+  __syncthreads();
+  block_reduce_cols<NCP>(sr, sred, outv);
+  if (threadIdx.x < ncol) a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+  if (last_cta(&st->ticket[FIN_UPDATE])) {
+    const EvalParams* P = a.prm;
+    int any = 0;
+    for (int c = 0; c < ncol; ++c) {
+      const bool act = st->active[c] != 0;     // uniform across the CTA
+      double tot = 0.0;
+      if (act) tot = sum_tiles(a.rr_part, a.L.n_tiles, c, sred);
+      if (threadIdx.x == 0 && act) {
+        const double be = tot / st->rr[c];
+        st->beta[c] = be;
+        a.beta_hist[c * a.hist_stride + st->iters[c]] = be;
+        st->rr[c] = tot;
+        st->iters[c] += 1;
+        const int na = is_active(P, c, st->iters[c], tot);
+        if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
+          st->hit_max = 1;
+        st->active[c] = na;
+      }
+      if (threadIdx.x == 0) any |= st->active[c];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      st->any_active = any;
+      st->par = par ^ 1;
+      st->ticket[FIN_UPDATE] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// S partials of a vector block: part[t][c] = sum_rows u * V[c]  (used before the trace applies)
+__global__ void __launch_bounds__(NT) spart_kernel(LayoutDev L, const double* u, const double* V,
+                                                   int ncol, double* part) {
+  __shared__ double sred[NT * MAXC];
+  __shared__ double outv[MAXC];
+  const TileDesc td = L.tiles[blockIdx.x];
+  const int64_t p0 = L.poff[td.blk] + td.row0;
+  double s[MAXC];
+#pragma unroll
+  for (int c = 0; c < MAXC; ++c) s[c] = 0.0;
+  for (int rl = threadIdx.x; rl < td.nrows; rl += NT) {
+    const double uu = u[p0 + rl];
+#pragma unroll
+    for (int c = 0; c < MAXC; ++c)
+      if (c < ncol) s[c] += uu * V[c * L.n_pad + p0 + rl];
+  }
+  block_reduce_cols<MAXC>(s, sred, outv);
+  if (threadIdx.x < MAXC) part[blockIdx.x * MAXC + threadIdx.x] = outv[threadIdx.x];
+}
+
+// ---------------------------------------------------------------------------------------
+// final: SLQ per probe (thread j), Pade log-det, MLL assembly into a nugpr_mll_out record.
+struct FinalArgs {
+  const CGState* st;
+  const EvalParams* prm;
+  const double* alpha_hist;
+  const double* beta_hist;
+  int hist_stride;
+  double* slq_work;          // [MAXC][3*hist_stride]
+  const double* logdet_R;    // device scalar
+  const double* lam0;        // device scalar
+  double n;
+  int ncol;
+  int logdet_mode;
+  nugpr_mll_out* out;
+};
+
+__global__ void final_kernel(FinalArgs a) {
+  __shared__ double s_slq[MAXC];
+  const CGState* st = a.st;
+  const int j = threadIdx.x;
+  if (j >= 1 && j < a.ncol) {
+    const int k = st->iters[j];
+    double val = 0.0;
+    if (k > 0) {
+      double* d = a.slq_work + static_cast<int64_t>(j) * 3 * a.hist_stride;
+      double* e = d + a.hist_stride;
+      double* z = e + a.hist_stride;
+      const double* al = a.alpha_hist + j * a.hist_stride;
+      const double* be = a.beta_hist + j * a.hist_stride;
+      d[0] = 1.0 / al[0];
+      for (int q = 1; q < k; ++q) d[q] = 1.0 / al[q] + be[q - 1] / al[q - 1];
+      for (int q = 0; q + 1 < k; ++q) e[q] = sqrt(be[q]) / al[q];
+      tql_first(k, d, e, z);
+      for (int l = 0; l < k; ++l) val += z[l] * z[l] * log(-2.0 + sqrt(3.0 + d[l]));
+      val *= st->rr0[j];
+    }
+    s_slq[j] = val;
+  }
+  __syncthreads();
+  if (j == 0) {
+    const int m = a.ncol - 1;
+    double tsum = 0.0, ssum = 0.0, rq = 0.0;
+    int kq = 0;
+    nugpr_mll_out o;
+    for (int q = 0; q < 16; ++q) o.iters_q[q] = 0;
+    for (int c = 1; c < a.ncol; ++c) {
+      tsum += st->t[c];
+      ssum += s_slq[c];
+      rq = fmax(rq, sqrt(st->rr[c]));
+      kq = max(kq, st->iters[c]);
+      o.iters_q[c - 1] = st->iters[c];
+    }
+    const double ldR = a.logdet_R[0];
+    o.quad = st->quad;
+    o.logdet_R = ldR;
+    o.logdet_pade = ldR + tsum / m;
+    o.logdet_slq = ldR + ssum / m;
+    o.logdet = (a.logdet_mode == 1) ? o.logdet_slq : o.logdet_pade;
+    o.L = 0.5 * (o.quad + o.logdet + a.n * 1.8378770664093453);   // n log(2 pi)
+    o.lambda0 = a.lam0[0];
+    o.resid_y = sqrt(st->rr[0]);
+    o.resid_q_max = rq;
+    o.iters_y = st->iters[0];
+    o.iters_q_max = kq;
+    o.converged = st->hit_max ? 0 : 1;
+    o.mode = a.prm->mode;
+    *a.out = o;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// probe export (debug): Z[j][p] for the seed, cluster-sorted order
+__global__ void probe_gen_kernel(uint64_t seed, int m, int64_t n, double* Z) {
+  int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(m) * n) return;
+  int j = static_cast<int>(idx / n);
+  int64_t p = idx % n;
+  Z[idx] = probe_value(seed, j, p);
+}
+
+// ======================================================================================
+// launchers
+template <int NCP>
+static void apply_launch_t(const ApplyArgs& a, int ld_max, cudaStream_t s) {
+  size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) * NCP + NT * 2 * NCP + NT * NCP + 4 * NCP);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(apply_kernel<NCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  apply_kernel<NCP><<<a.L.n_tiles, NT, smem, s>>>(a);
+  note_launch();
+}
+
+size_t apply_smem_bytes(int ncp, int ld_max) {
+  return sizeof(double) * (static_cast<size_t>(ld_max) * ncp + NT * 2 * ncp + NT * ncp + 4 * ncp);
+}
+
+void launch_apply(const ApplyArgs& a, int ncp, int ld_max, cudaStream_t s) {
+  switch (ncp) {
+    case 2: apply_launch_t<2>(a, ld_max, s); break;
+    case 4: apply_launch_t<4>(a, ld_max, s); break;
+    case 6: apply_launch_t<6>(a, ld_max, s); break;
+    case 8: apply_launch_t<8>(a, ld_max, s); break;
+    case 10: apply_launch_t<10>(a, ld_max, s); break;
+    case 12: apply_launch_t<12>(a, ld_max, s); break;
+    case 14: apply_launch_t<14>(a, ld_max, s); break;
+    default: apply_launch_t<16>(a, ld_max, s); break;
+  }
+}
+
+void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s) {
+  switch (ncp) {
+    case 2: update_kernel<2><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 4: update_kernel<4><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 6: update_kernel<6><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 8: update_kernel<8><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 10: update_kernel<10><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 12: update_kernel<12><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 14: update_kernel<14><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    default: update_kernel<16><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+  }
+}
+
+void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
+  size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) + NT * MAXC + MAXC);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rhs_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    attr = true;
+  }
+  rhs_init_kernel<<<a.L.n_tiles, NT, smem, s>>>(a);
+  note_launch();
+}
+
+void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
+                  cudaStream_t s) {
+  spart_kernel<<<L.n_tiles, NT, 0, s>>>(L, u, V, ncol, part);
+  note_launch();
+}
+
+void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
+                  int stride, double* slq_work, const double* logdet_R, const double* lam0, double n,
+                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s) {
+  FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, lam0, n, ncol, logdet_mode, out};
+  final_kernel<<<1, 32, 0, s>>>(a);
+  note_launch();
+}
+
+void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s) {
+  int64_t tot = static_cast<int64_t>(m) * n;
+  probe_gen_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(seed, m, n, Z);
+  note_launch();
+}
+
+}  // namespace nugpr

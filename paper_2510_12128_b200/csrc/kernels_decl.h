@@ -1,0 +1,48 @@
+// kernels_decl.h — host-side launchers of the nuGPR kernels (internal).
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "../../include/nugpr.h"
+#include "common.cuh"
+
+namespace nugpr {
+
+// Count of kernel launches issued by this library (bench.py reports it as gpu_launches).
+void note_launch(long long n = 1);
+long long launch_count();
+
+// build_kernels.cu
+void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist,
+                     int ld_max, const double* jitter, double* dst, int kind, double lam,
+                     double noise, double alpha, cudaStream_t s);
+size_t chol_smem_bytes(int ld_max);
+void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
+                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
+void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s);
+void launch_gemm_KLt(const double* K, const double* Linv, double* T, const LayoutDev& L, int ld_max,
+                     cudaStream_t s);
+void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max,
+                    cudaStream_t s);
+void launch_sum(const double* v, int n, double* out, cudaStream_t s);
+void launch_krep(const double* reps, int n_c, int d, int kind, double lam, double alpha, double* K,
+                 cudaStream_t s);
+size_t lanczos_scratch_doubles(int n_c, int kmax);
+void launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
+                    double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
+                    cudaStream_t s);
+
+// eval_kernels.cu
+size_t apply_smem_bytes(int ncp, int ld_max);
+void launch_apply(const ApplyArgs& a, int ncp, int ld_max, cudaStream_t s);
+void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
+void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
+void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
+                  cudaStream_t s);
+void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
+                  int stride, double* slq_work, const double* logdet_R, const double* lam0, double n,
+                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s);
+void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
+
+}  // namespace nugpr
