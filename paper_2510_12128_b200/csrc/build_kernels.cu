@@ -18,6 +18,26 @@ static std::atomic<long long> g_launches{0};
 void note_launch(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 long long launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+void smem_optin(const void* func) {
+  static std::atomic<const void*> done[64];
+  for (auto& d : done) {
+    const void* v = d.load();
+    if (v == func) return;
+    if (v == nullptr) {
+      int dev = 0, optin = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaFuncAttributes at;
+      cudaFuncGetAttributes(&at, func);
+      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           optin - static_cast<int>(at.sharedSizeBytes));
+      const void* expect = nullptr;
+      d.compare_exchange_strong(expect, func);
+      return;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // Kernel value.  Squared distance as sum_d (x_d - x'_d)^2 with explicitly non-fused ops
 // (bitwise-symmetric blocks with an exact diagonal).
@@ -301,11 +321,7 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
                        int32_t* status, double* logdet_blk, double* u, cudaStream_t s) {
   CholArgs a{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
   size_t smem = chol_smem_bytes(ld_max);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(chol_trtri_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel));
   chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
   note_launch();
 }
@@ -640,11 +656,7 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
   a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info;
   a.tri = scratch + static_cast<size_t>(kmax + 1) * n_c;
   size_t smem = sizeof(double) * (static_cast<size_t>(n_c) + kmax + 1);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(lanczos_kernel));
   lanczos_kernel<<<1, 1024, smem, s>>>(a);
   note_launch();
 }

@@ -535,11 +535,7 @@ __global__ void probe_gen_kernel(uint64_t seed, int m, int64_t n, double* Z) {
 template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, int ld_max, cudaStream_t s) {
   size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) * NCP + NT * 2 * NCP + NT * NCP + 4 * NCP);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(apply_kernel<NCP>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
   apply_kernel<NCP><<<a.L.n_tiles, NT, smem, s>>>(a);
   note_launch();
 }
@@ -576,11 +572,7 @@ void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s) {
 
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
   size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) + NT * MAXC + MAXC);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rhs_init_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr = true;
-  }
+  smem_optin(reinterpret_cast<const void*>(rhs_init_kernel));
   rhs_init_kernel<<<a.L.n_tiles, NT, smem, s>>>(a);
   note_launch();
 }

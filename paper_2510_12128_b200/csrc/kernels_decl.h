@@ -12,6 +12,9 @@ namespace nugpr {
 // Count of kernel launches issued by this library (bench.py reports it as gpu_launches).
 void note_launch(long long n = 1);
 long long launch_count();
+// Opt a kernel into the largest dynamic shared memory the device allows (optin limit minus the
+// kernel's static shared memory); cached per function.
+void smem_optin(const void* func);
 
 // build_kernels.cu
 void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist,
