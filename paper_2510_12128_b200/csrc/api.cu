@@ -224,10 +224,9 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
 
 bool is_device_ptr(const void* p) {
   cudaPointerAttributes at;
-  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
-    cudaGetLastError();
-    return false;
-  }
+  cudaError_t e = cudaPointerGetAttributes(&at, p);
+  cudaGetLastError();
+  if (e != cudaSuccess) return false;
   return at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged;
 }
 
@@ -417,6 +416,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   if (!theta_ok(theta0)) return fail(NUGPR_ERR_INVALID_ARG, "theta0 must be positive and finite");
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(NUGPR_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   CK(cudaSetDevice(ctx->device));
+  cudaGetLastError();   // drop stale errors left by unrelated runtime calls
   nugpr_blocks* bl = new nugpr_blocks();
   nugpr_status st = make_layout(offsets, n_c, d, bl->L);
   if (st != NUGPR_OK) { delete bl; return st; }
@@ -739,6 +739,7 @@ static nugpr_status stage_y(nugpr_blocks* bl, const double* y, EvalDev& e, cudaS
 static nugpr_status run_eval(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_dev, nugpr_theta th,
                              const nugpr_solve_cfg* cfg, nugpr_mll_out* out) {
   cudaStream_t s = ctx->stream;
+  cudaGetLastError();
   EvalDev& e = bl->E[0];
   int mode = 0;
   RET(enqueue_eval(ctx, bl, e, y_dev, th, cfg, s, &mode, ctx->h_flag));

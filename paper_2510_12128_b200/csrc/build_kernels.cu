@@ -11,6 +11,9 @@
 #include "tridiag.h"
 
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 namespace nugpr {
 
@@ -26,16 +29,38 @@ void smem_optin(const void* func) {
     if (v == nullptr) {
       int dev = 0, optin = 0;
       cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      cudaError_t e1 = cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
       cudaFuncAttributes at;
-      cudaFuncGetAttributes(&at, func);
-      cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           optin - static_cast<int>(at.sharedSizeBytes));
+      memset(&at, 0, sizeof(at));
+      cudaError_t e2 = cudaFuncGetAttributes(&at, func);
+      cudaError_t e3 = cudaSuccess;
+      if (e1 == cudaSuccess && e2 == cudaSuccess)
+        e3 = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  optin - static_cast<int>(at.sharedSizeBytes));
+      if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
+        fprintf(stderr, "[nugpr] smem opt-in failed: optin=%d static=%zu (%s / %s / %s)\n", optin,
+                static_cast<size_t>(at.sharedSizeBytes), cudaGetErrorString(e1), cudaGetErrorString(e2),
+                cudaGetErrorString(e3));
+        return;
+      }
       const void* expect = nullptr;
       d.compare_exchange_strong(expect, func);
       return;
     }
   }
+}
+
+bool debug_sync() {
+  static int v = -1;
+  if (v < 0) { const char* e = getenv("NUGPR_DEBUG_SYNC"); v = (e && e[0] == '1') ? 1 : 0; }
+  return v == 1;
+}
+
+void post_launch(const char* name) {
+  if (!debug_sync()) return;
+  cudaError_t e = cudaDeviceSynchronize();
+  cudaError_t l = cudaPeekAtLastError();
+  fprintf(stderr, "[nugpr] %-22s sync=%s last=%s\n", name, cudaGetErrorString(e), cudaGetErrorString(l));
 }
 
 // ---------------------------------------------------------------------------------------
@@ -115,7 +140,7 @@ void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* 
   int nt = (ld_max + 31) / 32;
   dim3 grid(nt * nt, list ? nlist : L.n_c);
   assemble_kernel<<<grid, 256, 0, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("assemble_kernel");
 }
 
 // ---------------------------------------------------------------------------------------
@@ -323,7 +348,7 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
   size_t smem = chol_smem_bytes(ld_max);
   smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel));
   chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("chol_trtri_kernel");
 }
 
 // ---------------------------------------------------------------------------------------
@@ -430,7 +455,7 @@ void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max
   int nt = (ld_max + 63) / 64;
   GemmArgs g{Linv, Linv, H, L.boff, L.ld, nt};
   gemm_blocks_kernel<true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
-  note_launch();
+  note_launch(); post_launch("gemm_H");
 }
 // T = K * Linv^T
 void launch_gemm_KLt(const double* K, const double* Linv, double* T, const LayoutDev& L, int ld_max,
@@ -438,7 +463,7 @@ void launch_gemm_KLt(const double* K, const double* Linv, double* T, const Layou
   int nt = (ld_max + 63) / 64;
   GemmArgs g{K, Linv, T, L.boff, L.ld, nt};
   gemm_blocks_kernel<true, false, true, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
-  note_launch();
+  note_launch(); post_launch("gemm_KLt");
 }
 // G = Linv * T (symmetric)
 void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max,
@@ -446,7 +471,7 @@ void launch_gemm_LT(const double* Linv, const double* T, double* G, const Layout
   int nt = (ld_max + 63) / 64;
   GemmArgs g{Linv, T, G, L.boff, L.ld, nt};
   gemm_blocks_kernel<false, true, false, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
-  note_launch();
+  note_launch(); post_launch("gemm_LT");
 }
 
 // ---------------------------------------------------------------------------------------
@@ -467,7 +492,7 @@ __global__ void sum_kernel(const double* v, int n, double* out) {
 }
 void launch_sum(const double* v, int n, double* out, cudaStream_t s) {
   sum_kernel<<<1, NT, 0, s>>>(v, n, out);
-  note_launch();
+  note_launch(); post_launch("sum_kernel");
 }
 
 // ---------------------------------------------------------------------------------------
@@ -488,7 +513,7 @@ void launch_krep(const double* reps, int n_c, int d, int kind, double lam, doubl
                  cudaStream_t s) {
   int64_t tot = static_cast<int64_t>(n_c) * n_c;
   krep_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(reps, n_c, d, kind, lam, alpha, K);
-  note_launch();
+  note_launch(); post_launch("krep_kernel");
 }
 
 // ---------------------------------------------------------------------------------------
@@ -658,7 +683,7 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
   size_t smem = sizeof(double) * (static_cast<size_t>(n_c) + kmax + 1);
   smem_optin(reinterpret_cast<const void*>(lanczos_kernel));
   lanczos_kernel<<<1, 1024, smem, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("lanczos_kernel");
 }
 
 }  // namespace nugpr

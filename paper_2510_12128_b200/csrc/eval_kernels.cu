@@ -537,7 +537,7 @@ static void apply_launch_t(const ApplyArgs& a, int ld_max, cudaStream_t s) {
   size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) * NCP + NT * 2 * NCP + NT * NCP + 4 * NCP);
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
   apply_kernel<NCP><<<a.L.n_tiles, NT, smem, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("apply_kernel");
 }
 
 size_t apply_smem_bytes(int ncp, int ld_max) {
@@ -559,14 +559,14 @@ void launch_apply(const ApplyArgs& a, int ncp, int ld_max, cudaStream_t s) {
 
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s) {
   switch (ncp) {
-    case 2: update_kernel<2><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 4: update_kernel<4><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 6: update_kernel<6><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 8: update_kernel<8><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 10: update_kernel<10><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 12: update_kernel<12><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    case 14: update_kernel<14><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
-    default: update_kernel<16><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); break;
+    case 2: update_kernel<2><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 4: update_kernel<4><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 6: update_kernel<6><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 8: update_kernel<8><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 10: update_kernel<10><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 12: update_kernel<12><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    case 14: update_kernel<14><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
+    default: update_kernel<16><<<a.L.n_tiles, NT, 0, s>>>(a); note_launch(); post_launch("update_kernel"); break;
   }
 }
 
@@ -574,13 +574,13 @@ void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
   size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) + NT * MAXC + MAXC);
   smem_optin(reinterpret_cast<const void*>(rhs_init_kernel));
   rhs_init_kernel<<<a.L.n_tiles, NT, smem, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("rhs_init_kernel");
 }
 
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s) {
   spart_kernel<<<L.n_tiles, NT, 0, s>>>(L, u, V, ncol, part);
-  note_launch();
+  note_launch(); post_launch("spart_kernel");
 }
 
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
@@ -588,13 +588,13 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
                   int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s) {
   FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, lam0, n, ncol, logdet_mode, out};
   final_kernel<<<1, 32, 0, s>>>(a);
-  note_launch();
+  note_launch(); post_launch("final_kernel");
 }
 
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s) {
   int64_t tot = static_cast<int64_t>(m) * n;
   probe_gen_kernel<<<static_cast<unsigned>((tot + 255) / 256), 256, 0, s>>>(seed, m, n, Z);
-  note_launch();
+  note_launch(); post_launch("probe_gen_kernel");
 }
 
 }  // namespace nugpr

@@ -15,6 +15,8 @@ long long launch_count();
 // Opt a kernel into the largest dynamic shared memory the device allows (optin limit minus the
 // kernel's static shared memory); cached per function.
 void smem_optin(const void* func);
+// NUGPR_DEBUG_SYNC=1: synchronise and report after every launch (debugging only).
+void post_launch(const char* name);
 
 // build_kernels.cu
 void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist,

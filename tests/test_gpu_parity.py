@@ -45,7 +45,7 @@ def perturbed(theta0, h=1e-3):
             "lam+": (l * (1 + h), s, a), "lam-": (l * (1 - h), s, a)}
 
 
-def compare(rec, ds, bo, theta, Z, rtol=TIGHT, free_check=True, logdet_mode="pade"):
+def compare(rec, ds, bo, theta, Z, rtol=TIGHT, free_check=True, logdet_mode="pade", tol=0.01):
     replay = [rec["iters_y"]] + list(rec["iters_q"])
     ro = oracle_mll(bo, ds.y, theta, Z, replay=replay, logdet_mode=logdet_mode)
     assert rec["mode"] == ro.mode
@@ -55,10 +55,10 @@ def compare(rec, ds, bo, theta, Z, rtol=TIGHT, free_check=True, logdet_mode="pad
     assert rel(rec["logdet_slq"], ro.logdet_slq) < rtol
     assert rel(rec["lambda0"], ro.lambda0) < 1e-11
     if free_check:
-        rf = oracle_mll(bo, ds.y, theta, Z)
+        rf = oracle_mll(bo, ds.y, theta, Z, tol=tol)
         if [rf.iters_y] + rf.iters_q != replay:
             # a count may only differ when a residual sits on the threshold (parity protocol 3)
-            assert abs(rf.resid_y - 0.01) < 1e-6 or abs(rf.resid_q_max - 0.01) < 1e-6, (replay, rf)
+            assert abs(rf.resid_y - tol) < 1e-6 * tol or abs(rf.resid_q_max - tol) < 1e-6 * tol, (replay, rf)
         else:
             assert rel(rec["L"], rf.L) < RTOL_L
     return ro
@@ -148,7 +148,7 @@ def test_tight_tolerance_and_replay(P, ctx):
     Z = synth.probes(1, 4, ds.n)
     rec = P.mll(ctx, bg, ds.y, ds.theta0, tol=1e-10, num_probes=4, probe_seed=1)
     assert rec["iters_y"] <= ds.n_c + 2           # PAPER.md:244, +1 for rounding
-    compare(rec, ds, bo, ds.theta0, Z)
+    compare(rec, ds, bo, ds.theta0, Z, tol=1e-10)
     rep = P.mll(ctx, bg, ds.y, ds.theta0, num_probes=4, probe_seed=1, replay=[2, 1, 3, 2, 4])
     assert rep["iters_y"] == 2 and rep["iters_q"] == [1, 3, 2, 4]
     compare(rep, ds, bo, ds.theta0, Z, free_check=False)
