@@ -179,6 +179,13 @@ class Blocks:
         N.check(N.lib().nugpr_blocks_export(self.handle, codes[what], buf.ctypes.data, buf.nbytes))
         return buf.reshape(self.n_c, self.n_c) if what == "M" else buf
 
+    def lanczos_info(self, which: str = "build"):
+        """(iterations, converged) of the build's lambda_0 solve or of the last generic eval's."""
+        buf = np.zeros(2, dtype=np.int32)
+        N.check(N.lib().nugpr_blocks_export(self.handle, 8 if which == "build" else 9, buf.ctypes.data,
+                                            buf.nbytes))
+        return int(buf[0]), bool(buf[1])
+
     def export_probes(self, m: int):
         buf = np.empty((m, self.n))
         N.check(N.lib().nugpr_blocks_export(self.handle, 7, buf.ctypes.data, buf.nbytes))

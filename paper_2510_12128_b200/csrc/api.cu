@@ -54,7 +54,7 @@ nugpr_status fail(nugpr_status st, const char* fmt, ...) {
   } while (0)
 
 constexpr int HIST = 4096;          // max recorded CG iterations (cg_max_iter cap)
-constexpr int LD_MAX_SUPPORTED = 768;
+constexpr int LD_MAX_SUPPORTED = 512;
 constexpr int LANCZOS_KMAX_CAP = 400;
 
 struct HostLayout {
@@ -400,7 +400,7 @@ static nugpr_status enqueue_lambda0(nugpr_blocks* bl, const double* K, const dou
                                     double* lam0, double* v0, double* M, int32_t* info, cudaStream_t s) {
   const int n_c = bl->L.n_c;
   const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
-  launch_lanczos(K, n_c, vinit, lz, kmax, 1e-13, lam0, v0, M, info, s);
+  launch_lanczos(K, n_c, vinit, lz, kmax, 1e-11, lam0, v0, M, info, s);
   CKL();
   return NUGPR_OK;
 }
@@ -456,6 +456,11 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   CKB(cudaMemcpyAsync(B.X, X_sorted, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
   CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
   CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * n_c, s));
+  for (EvalDev& ev : bl->E) {
+    const size_t np = static_cast<size_t>(L.tiles.size()) * MAXC * sizeof(double);
+    for (double* p : {ev.SR, ev.SPb[0], ev.SPb[1], ev.SV, ev.SX, ev.dots, ev.rrp}) CKB(cudaMemsetAsync(p, 0, np, s));
+    CKB(cudaMemsetAsync(ev.st, 0, sizeof(CGState), s));
+  }
   CKB(cudaMemsetAsync(B.u, 0, sizeof(double) * L.n_pad, s));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
   PROF(ctx, PC_OTHER, 0.0, s,
@@ -575,6 +580,13 @@ extern "C" nugpr_status nugpr_blocks_export(const nugpr_blocks* bl, int32_t what
       CK(cudaMemcpyAsync(dst, bl->B.Zexport, n, cudaMemcpyDeviceToHost, s));
       break;
     }
+    case 8:
+    case 9: {   // Lanczos {iterations, converged}: 8 = the build's, 9 = slot 0's last generic eval
+      if (!need(2 * sizeof(int32_t))) return fail(NUGPR_ERR_INVALID_ARG, "need 8 bytes");
+      CK(cudaMemcpyAsync(dst, what == 8 ? bl->B.linfo : bl->E[0].linfo, 2 * sizeof(int32_t),
+                         cudaMemcpyDeviceToHost, s));
+      break;
+    }
     default:
       return fail(NUGPR_ERR_INVALID_ARG, "unknown export %d", what);
   }
@@ -638,6 +650,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   P.mode = mode;
   if (mode_out) *mode_out = mode;
   CK(cudaMemcpyAsync(e.prm, &P, sizeof(P), cudaMemcpyHostToDevice, s));
+  // the workspace is caller memory with arbitrary contents: the CG state (incl. the
+  // self-resetting last-CTA tickets) and the S partials start from zero every evaluation
+  CK(cudaMemsetAsync(e.st, 0, sizeof(CGState), s));
   if (mode == NUGPR_MODE_SCALE) {
     // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
     // build read back, written to the slot scalar (reported in the record only).
@@ -664,6 +679,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   a1.L = Ld; a1.prm = e.prm; a1.st = e.st; a1.u = B.u; a1.jitter = B.jitter; a1.ncol = ncol;
   a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
   a1.alpha_hist = e.ah; a1.hist_stride = HIST;
+  a1.ld_max = L.ld_max;
+  a1.slot_doubles = std::max(SLOT_TARGET_DOUBLES, L.ld_max);
+  a1.red_doubles = 2 * ncp * NT;
   ApplyArgs a2 = a1;
   // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
   a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;
@@ -689,8 +707,8 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   int done = 0;
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a1, ncp, L.ld_max, s));
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a2, ncp, L.ld_max, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a1, ncp, P.B != nullptr, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a2, ncp, P.B != nullptr, s));
       PROF(ctx, PC_UPDATE, 0.0, s, launch_update(ua, ncp, s));
     }
     CKL();
@@ -703,7 +721,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   ApplyArgs a3 = a1;
   a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
   a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a3, ncp, L.ld_max, s));
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a3, ncp, P.B != nullptr, s));
   ApplyArgs a4 = a3;
   a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
   a4.fin = FIN_TRACE;
@@ -711,7 +729,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
     if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
     else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
   }
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a4, ncp, L.ld_max, s));
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a4, ncp, P.B != nullptr, s));
   launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, lam0_ptr, static_cast<double>(L.n),
                ncol, cfg->logdet_mode, e.out, s);
   CKL();

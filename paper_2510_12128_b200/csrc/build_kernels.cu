@@ -11,6 +11,7 @@
 #include "tridiag.h"
 
 #include <atomic>
+#include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -517,12 +518,16 @@ void launch_krep(const double* reps, int n_c, int d, int kind, double lam, doubl
 }
 
 // ---------------------------------------------------------------------------------------
-// lambda_0 = lambda_min(K_rep) by Lanczos with full (twice classical Gram-Schmidt)
-// reorthogonalisation, single CTA of 1024 threads.  Converged when the Ritz residual
-// beta_{k+1} |s_k| <= tol_rel * ||K||_inf.  Writes lam0, the Ritz vector v0 (warm start for
-// the next solve) and M = K - lam0 I.  ws: (kmax+1) x n_c doubles of Lanczos vectors.
+// lambda_0 = lambda_min(K_rep) (Eq. 26) by Lanczos with full reorthogonalisation (two passes
+// of classical Gram-Schmidt), run by ONE thread-block cluster of CS CTAs: CTA q owns rows
+// [q*R, (q+1)*R) of K_rep (cached in its shared memory when they fit) and of every Lanczos
+// vector; the per-iteration dot products are reduced across the cluster through distributed
+// shared memory in fixed rank order, so every CTA holds bit-identical alpha/beta and takes
+// the same convergence decision.  Converged when the Ritz residual beta_{k+1}|s_k| <=
+// tol_rel*||K||_inf (then |theta - lambda| <= that bound).  Writes lam0, the normalised Ritz
+// vector v0 (warm start of the next solve) and M = K - lam0 I.
 struct LanczosArgs {
-  const double* K;       // n_c x n_c
+  const double* K;       // n_c x n_c row-major
   int n_c;
   const double* vinit;   // NULL or n_c
   double* V;             // (kmax+1) x n_c
@@ -532,145 +537,235 @@ struct LanczosArgs {
   double* v0;            // [n_c] out
   double* M;             // n_c x n_c out (K - lam0 I)
   int32_t* info;         // [2] {iterations, converged}
-  double* tri;           // scratch 6*kmax
+  int cacheK;
 };
 
-__global__ void __launch_bounds__(1024) lanczos_kernel(LanczosArgs a) {
+constexpr int LZ_NT = 512;
+
+// smallest eigenvalue of the k x k tridiagonal (a, b) by 32-way multisection in one warp
+__device__ double warp_tridiag_min_eig(int k, const double* a, const double* b, double hi_hint) {
+  const int lane = threadIdx.x & 31;
+  double lo = a[0], hi = a[0];
+  for (int i = 0; i < k; ++i) {
+    double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
+    lo = fmin(lo, a[i] - r);
+    hi = fmax(hi, a[i] + r);
+  }
+  hi = fmin(hi, hi_hint);
+  for (int it = 0; it < 14; ++it) {
+    const double x = lo + (hi - lo) * (lane + 1) / 33.0;
+    const int cnt = sturm_count(k, a, b, x);
+    const unsigned m = __ballot_sync(0xffffffffu, cnt >= 1);
+    // first lane whose point has >= 1 eigenvalue below it
+    const int f = m ? (__ffs(m) - 1) : 32;
+    const double nlo = lo + (hi - lo) * f / 33.0;
+    const double nhi = (f < 32) ? lo + (hi - lo) * (f + 1) / 33.0 : hi;
+    lo = nlo;
+    hi = nhi;
+    if (!(hi > lo)) break;
+  }
+  return 0.5 * (lo + hi);
+}
+
+template <int CS>
+__global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a) {
+  namespace cgs = cooperative_groups;
+  cgs::cluster_group cl = cgs::this_cluster();
+  const int q = static_cast<int>(cl.block_rank());
   const int n = a.n_c;
-  const int tid = threadIdx.x;
-  const int nthr = blockDim.x;
-  const int lane = tid & 31, wid = tid >> 5, nw = nthr >> 5;
-  extern __shared__ double sm[];
-  double* w = sm;                  // n
-  double* h = w + n;               // kmax+1
+  const int kmax = a.kmax;
+  const int R = (n + CS - 1) / CS;
+  const int r0 = min(n, q * R), r1 = min(n, r0 + R), nr = r1 - r0;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = LZ_NT / 32;
+  extern __shared__ __align__(16) double sm[];
+  double* vfull = sm;                 // n
+  double* wl = vfull + n;             // R
+  double* hp = wl + R;                // 2 * (kmax+1)   (partial dots, double-buffered)
+  double* hs = hp + 2 * (kmax + 1);   // kmax+1         (cluster-summed dots)
+  double* nb = hs + (kmax + 1);       // 4              (partial norms / scalars)
+  double* al = nb + 4;                // kmax
+  double* be = al + kmax;             // kmax
+  double* ta = be + kmax;             // kmax
+  double* tb = ta + kmax;             // kmax
+  double* sv = tb + kmax;             // kmax
+  double* sw = sv + kmax;             // 2 kmax
+  double* Kc = sw + 2 * kmax;         // R * n (if cached)
   __shared__ double red[32];
-  __shared__ double s_alpha, s_beta, s_norm;
-  __shared__ int s_done;
-  double* alph = a.tri;            // kmax
-  double* bet = a.tri + a.kmax;    // kmax  (bet[k] couples k and k+1)
-  double* ta = a.tri + 2 * a.kmax; // copies for the tridiagonal solve
-  double* tb = a.tri + 3 * a.kmax;
-  double* sv = a.tri + 4 * a.kmax; // eigenvector (kmax) + scratch beyond
-  // ||K||_inf
-  double rmax = 0.0;
-  for (int r = wid; r < n; r += nw) {
-    double s = 0.0;
-    for (int c = lane; c < n; c += 32) s += fabs(a.K[static_cast<int64_t>(r) * n + c]);
-    s = warp_sum(s);
-    rmax = fmax(rmax, s);
-  }
-  if (lane == 0) red[wid] = rmax;
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0.0;
-    for (int k = 0; k < nw; ++k) m = fmax(m, red[k]);
-    s_norm = m;
-    s_done = 0;
-  }
-  __syncthreads();
-  // v_0
-  for (int r = tid; r < n; r += nthr) {
-    double v = a.vinit ? a.vinit[r] : (probe_value(0x5eed1a2c5ull, 0, r) * (1.0 + 0.01 * (r % 7)));
-    w[r] = v;
-  }
-  __syncthreads();
+  __shared__ int s_done, s_conv;
+  __shared__ double s_theta;
+  const double* Kg = a.K;
+  auto Krow = [&](int r) -> const double* {   // r local
+    return a.cacheK ? Kc + static_cast<int64_t>(r) * n : Kg + static_cast<int64_t>(r0 + r) * n;
+  };
   auto block_sum = [&](double v) -> double {
     v = warp_sum(v);
     __syncthreads();
     if (lane == 0) red[wid] = v;
     __syncthreads();
     double t = 0.0;
-    for (int k = 0; k < nw; ++k) t += red[k];
+    for (int w = 0; w < nw; ++w) t += red[w];
     return t;
   };
-  {
-    double s = 0.0;
-    for (int r = tid; r < n; r += nthr) s += w[r] * w[r];
-    double nrm = sqrt(block_sum(s));
-    for (int r = tid; r < n; r += nthr) a.V[r] = w[r] / nrm;
-  }
+  // cluster-wide fixed-order sum of one scalar per CTA (slot in nb)
+  auto cluster_sum = [&](int slot, double v) -> double {
+    if (tid == 0) nb[slot] = v;
+    cl.sync();
+    double t = 0.0;
+    for (int p = 0; p < CS; ++p) t += *cl.map_shared_rank(nb + slot, p);
+    return t;
+  };
+  if (a.cacheK)
+    for (int64_t idx = tid; idx < static_cast<int64_t>(nr) * n; idx += LZ_NT)
+      Kc[idx] = Kg[static_cast<int64_t>(r0) * n + idx];
   __syncthreads();
-  int k_final = 0;
-  int converged = 0;
-  double theta = 0.0;
-  for (int k = 0; k < a.kmax; ++k) {
-    const double* vk = a.V + static_cast<int64_t>(k) * n;
-    // w = K v_k (warp per row)
-    for (int r = wid; r < n; r += nw) {
-      const double* Kr = a.K + static_cast<int64_t>(r) * n;
-      double s = 0.0;
-      for (int c = lane; c < n; c += 32) s += Kr[c] * vk[c];
-      s = warp_sum(s);
-      if (lane == 0) w[r] = s;
-    }
-    __syncthreads();
-    // two passes of classical Gram-Schmidt against v_0..v_k (includes alpha_k = v_k^T w)
-    for (int pass = 0; pass < 2; ++pass) {
-      for (int j = wid; j <= k; j += nw) {
-        const double* vj = a.V + static_cast<int64_t>(j) * n;
-        double s = 0.0;
-        for (int c = lane; c < n; c += 32) s += vj[c] * w[c];
-        s = warp_sum(s);
-        if (lane == 0) h[j] = s;
-      }
-      __syncthreads();
-      if (pass == 0 && tid == 0) s_alpha = h[k];
-      if (pass == 1 && tid == 0) s_alpha += h[k];
-      for (int r = tid; r < n; r += nthr) {
-        double s = w[r];
-        for (int j = 0; j <= k; ++j) s -= h[j] * a.V[static_cast<int64_t>(j) * n + r];
-        w[r] = s;
-      }
-      __syncthreads();
-    }
+  // ||K||_inf (max row sum) over the cluster
+  double rmax = 0.0;
+  for (int r = wid; r < nr; r += nw) {
+    const double* kr = Krow(r);
     double s = 0.0;
-    for (int r = tid; r < n; r += nthr) s += w[r] * w[r];
-    double beta = sqrt(block_sum(s));
-    if (tid == 0) {
-      alph[k] = s_alpha;
-      bet[k] = beta;
-      s_beta = beta;
-    }
-    __syncthreads();
-    const int kk = k + 1;
-    const bool last = (kk == a.kmax) || (kk == n) || !(beta > 1e-300);
-    if (tid == 0 && (last || (kk % 4 == 0))) {
-      for (int t = 0; t < kk; ++t) { ta[t] = alph[t]; tb[t] = bet[t]; }
-      theta = tridiag_min_eig(kk, ta, tb);
-      tridiag_eigvec(kk, ta, tb, theta, sv, sv + a.kmax);
-      double res = fabs(bet[k] * sv[kk - 1]);
-      if (res <= a.tol_rel * s_norm || last) {
-        s_done = 1;
-        converged = (res <= a.tol_rel * s_norm) || !(beta > 1e-300) || (kk == n);
-      }
-    }
-    __syncthreads();
-    if (s_done) { k_final = kk; break; }
-    for (int r = tid; r < n; r += nthr) a.V[static_cast<int64_t>(k + 1) * n + r] = w[r] / s_beta;
-    __syncthreads();
+    for (int c = lane; c < n; c += 32) s += fabs(kr[c]);
+    rmax = fmax(rmax, warp_sum(s));
   }
-  // Ritz vector v0 = V s, normalised; lam0; M = K - lam0 I
-  __shared__ double s_theta;
-  if (tid == 0) { s_theta = theta; a.lam0[0] = theta; a.info[0] = k_final; a.info[1] = converged; }
+  if (lane == 0) red[wid] = rmax;
   __syncthreads();
+  if (tid == 0) { double m = 0.0; for (int w = 0; w < nw; ++w) m = fmax(m, red[w]); nb[2] = m; s_done = 0; s_conv = 0; }
+  cl.sync();
+  double knorm = 0.0;
+  for (int p = 0; p < CS; ++p) knorm = fmax(knorm, *cl.map_shared_rank(nb + 2, p));
+  // v_0 (rows of this CTA), normalised over the cluster
   double ss = 0.0;
-  for (int r = tid; r < n; r += nthr) {
-    double v = 0.0;
-    for (int j = 0; j < k_final; ++j) v += a.V[static_cast<int64_t>(j) * n + r] * sv[j];
-    w[r] = v;
+  for (int r = tid; r < nr; r += LZ_NT) {
+    const int g = r0 + r;
+    double v = a.vinit ? a.vinit[g] : probe_value(0x5eed1a2c5ull, 0, g) * (1.0 + 0.01 * (g % 7));
+    wl[r] = v;
     ss += v * v;
   }
-  double nrm = sqrt(block_sum(ss));
-  for (int r = tid; r < n; r += nthr) a.v0[r] = w[r] / nrm;
-  const double l0 = s_theta;
-  for (int64_t idx = tid; idx < static_cast<int64_t>(n) * n; idx += nthr) {
-    int r = static_cast<int>(idx / n), c = static_cast<int>(idx % n);
-    a.M[idx] = a.K[idx] - (r == c ? l0 : 0.0);
+  double nrm = sqrt(cluster_sum(0, block_sum(ss)));
+  for (int r = tid; r < nr; r += LZ_NT) a.V[r0 + r] = wl[r] / nrm;
+  cl.sync();
+  int k_final = 0;
+  double theta = 0.0, theta_prev = INFINITY;
+  for (int k = 0; k < kmax; ++k) {
+    const double* vk = a.V + static_cast<int64_t>(k) * n;
+    for (int c = tid; c < n; c += LZ_NT) vfull[c] = vk[c];
+    __syncthreads();
+    // w = K v_k on this CTA's rows (warp per row)
+    for (int r = wid; r < nr; r += nw) {
+      const double* kr = Krow(r);
+      double s = 0.0;
+      for (int c = lane; c < n; c += 32) s += kr[c] * vfull[c];
+      s = warp_sum(s);
+      if (lane == 0) wl[r] = s;
+    }
+    __syncthreads();
+    double alpha = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      double* hpp = hp + pass * (kmax + 1);
+      for (int j = wid; j <= k; j += nw) {
+        const double* vj = a.V + static_cast<int64_t>(j) * n + r0;
+        double s = 0.0;
+        for (int r = lane; r < nr; r += 32) s += vj[r] * wl[r];
+        s = warp_sum(s);
+        if (lane == 0) hpp[j] = s;
+      }
+      cl.sync();
+      for (int j = tid; j <= k; j += LZ_NT) {
+        double t = 0.0;
+        for (int p = 0; p < CS; ++p) t += cl.map_shared_rank(hpp, p)[j];
+        hs[j] = t;
+      }
+      __syncthreads();
+      alpha += hs[k];
+      for (int r = tid; r < nr; r += LZ_NT) {
+        double s = wl[r];
+        for (int j = 0; j <= k; ++j) s -= hs[j] * a.V[static_cast<int64_t>(j) * n + r0 + r];
+        wl[r] = s;
+      }
+      __syncthreads();
+    }
+    double s2 = 0.0;
+    for (int r = tid; r < nr; r += LZ_NT) s2 += wl[r] * wl[r];
+    const double beta = sqrt(cluster_sum(k & 1, block_sum(s2)));
+    if (tid == 0) { al[k] = alpha; be[k] = beta; }
+    __syncthreads();
+    const int kk = k + 1;
+    const bool last = (kk == kmax) || (kk == n) || !(beta > 1e-300);
+    if (last || (kk % 4 == 0)) {
+      if (wid == 0) {
+        for (int t = lane; t < kk; t += 32) { ta[t] = al[t]; tb[t] = be[t]; }
+        __syncwarp();
+        const double th = warp_tridiag_min_eig(kk, ta, tb, theta_prev);
+        if (lane == 0) {
+          tridiag_eigvec(kk, ta, tb, th, sv, sw);
+          const double res = fabs(be[k] * sv[kk - 1]);
+          s_theta = th;
+          const bool ok = res <= a.tol_rel * knorm;
+          if (ok || last) {
+            s_done = 1;
+            s_conv = ok || !(beta > 1e-300) || (kk == n);
+          }
+        }
+      }
+      __syncthreads();
+      theta = s_theta;
+      theta_prev = theta;
+    }
+    if (s_done) { k_final = kk; break; }
+    for (int r = tid; r < nr; r += LZ_NT) a.V[static_cast<int64_t>(k + 1) * n + r0 + r] = wl[r] / beta;
+    cl.sync();
   }
+  // Ritz vector (rows of this CTA), normalised over the cluster; M = K - theta I
+  double s3 = 0.0;
+  for (int r = tid; r < nr; r += LZ_NT) {
+    double v = 0.0;
+    for (int j = 0; j < k_final; ++j) v += a.V[static_cast<int64_t>(j) * n + r0 + r] * sv[j];
+    wl[r] = v;
+    s3 += v * v;
+  }
+  const double vn = sqrt(cluster_sum(2, block_sum(s3)));
+  for (int r = tid; r < nr; r += LZ_NT) a.v0[r0 + r] = wl[r] / vn;
+  for (int64_t idx = tid; idx < static_cast<int64_t>(nr) * n; idx += LZ_NT) {
+    const int r = static_cast<int>(idx / n), c = static_cast<int>(idx % n);
+    const int64_t g = static_cast<int64_t>(r0) * n + idx;
+    a.M[g] = Krow(r)[c] - ((r0 + r) == c ? theta : 0.0);
+  }
+  if (q == 0 && tid == 0) { a.lam0[0] = theta; a.info[0] = k_final; a.info[1] = s_conv; }
+  cl.sync();   // keep shared memory alive until every CTA is done reading remote slots
 }
 
 size_t lanczos_scratch_doubles(int n_c, int kmax) {
-  return static_cast<size_t>(kmax + 1) * n_c + 8 * static_cast<size_t>(kmax) + 64;
+  return static_cast<size_t>(kmax + 1) * n_c + 64;
+}
+
+template <int CS>
+static cudaError_t lanczos_launch_cs(const LanczosArgs& a0, cudaStream_t s) {
+  LanczosArgs a = a0;
+  const int n = a.n_c, kmax = a.kmax, R = (n + CS - 1) / CS;
+  size_t base = static_cast<size_t>(n) + R + 3 * (kmax + 1) + 4 + 7 * static_cast<size_t>(kmax);
+  size_t withK = base + static_cast<size_t>(R) * n;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t limit = static_cast<size_t>(optin) - 1024;
+  a.cacheK = (withK * sizeof(double) <= limit) ? 1 : 0;
+  const size_t smem = (a.cacheK ? withK : base) * sizeof(double);
+  if (smem > limit) return cudaErrorInvalidValue;
+  auto kern = lanczos_cluster_kernel<CS>;
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(limit));
+  if (CS > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(CS, 1, 1);
+  cfg.blockDim = dim3(LZ_NT, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
 void launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
@@ -678,12 +773,16 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
                     cudaStream_t s) {
   LanczosArgs a;
   a.K = K; a.n_c = n_c; a.vinit = vinit; a.V = scratch; a.kmax = kmax; a.tol_rel = tol_rel;
-  a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info;
-  a.tri = scratch + static_cast<size_t>(kmax + 1) * n_c;
-  size_t smem = sizeof(double) * (static_cast<size_t>(n_c) + kmax + 1);
-  smem_optin(reinterpret_cast<const void*>(lanczos_kernel));
-  lanczos_kernel<<<1, 1024, smem, s>>>(a);
-  note_launch(); post_launch("lanczos_kernel");
+  a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info; a.cacheK = 0;
+  cudaError_t e;
+  if (n_c >= 128) {
+    e = lanczos_launch_cs<16>(a, s);
+    if (e != cudaSuccess) { cudaGetLastError(); e = lanczos_launch_cs<8>(a, s); }
+  } else {
+    e = lanczos_launch_cs<4>(a, s);
+  }
+  (void)e;
+  note_launch(); post_launch("lanczos_cluster_kernel");
 }
 
 }  // namespace nugpr

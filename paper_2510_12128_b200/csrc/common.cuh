@@ -19,7 +19,9 @@ namespace nugpr {
 
 constexpr int MAXC = 16;        // max columns per apply (1 + m)
 constexpr int NT = 256;         // threads per CTA for the tile kernels
-constexpr int TILE_ROWS = 256;  // max padded rows per tile
+constexpr int TILE_ROWS = 512;  // max padded rows per tile (= whole clusters in this build)
+constexpr int NSTAGE = 3;       // TMA ring depth of the apply kernel
+constexpr int SLOT_TARGET_DOUBLES = 3072;  // ~24 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
 
 struct TileDesc {
@@ -104,6 +106,9 @@ struct ApplyArgs {
   int ncol;
   double* alpha_hist;      // [MAXC][hist_stride]
   int hist_stride;
+  int ld_max;
+  int slot_doubles;        // TMA ring slot size (>= ld_max)
+  int red_doubles;         // cross-k-group reduction scratch
 };
 
 struct UpdateArgs {

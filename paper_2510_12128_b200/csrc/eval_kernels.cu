@@ -7,8 +7,11 @@
 // apply(A X) -> apply(3 A^2 X - 3 X, dotted with Z) -> final.  Every global reduction
 // (S = W^T D, p^T q, r^T r, the trace dots) is written as per-tile partials and summed by
 // the last CTA to finish, in fixed tile order: results are bit-reproducible.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels_decl.h"
+#include "tma.cuh"
 #include "tridiag.h"
 
 namespace nugpr {
@@ -47,20 +50,13 @@ __device__ __forceinline__ bool last_cta(unsigned int* ticket) {
   return s_last != 0;
 }
 
-// Fixed-order sum of column c of per-tile partials [n_tiles][MAXC]; result in thread 0.
-__device__ double sum_tiles(const double* part, int n_tiles, int c, double* sred) {
-  const int per = (n_tiles + NT - 1) / NT;
-  const int lo = threadIdx.x * per, hi = min(n_tiles, lo + per);
+// Deterministic total of column c of per-tile partials [n_tiles][MAXC]: called by a whole
+// warp; lanes stride over tiles, then an xor-butterfly (every lane ends with the same bits).
+__device__ __forceinline__ double col_total(const double* part, int n_tiles, int c) {
+  const int lane = threadIdx.x & 31;
   double s = 0.0;
-  for (int t = lo; t < hi; ++t) s += part[t * MAXC + c];
-  __syncthreads();
-  sred[threadIdx.x] = s;
-  __syncthreads();
-  double tot = 0.0;
-  if (threadIdx.x == 0)
-    for (int k = 0; k < NT; ++k) tot += sred[k];
-  __syncthreads();
-  return tot;
+  for (int t = lane; t < n_tiles; t += 32) s += part[t * MAXC + c];
+  return warp_sum(s);
 }
 
 // Column activity rule (PAPER.md:406 tol/max_iter, readings P3, P5; replay for parity).
@@ -129,22 +125,29 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
   }
   if (last_cta(&a.st->ticket[FIN_INIT])) {
     CGState* st = a.st;
-    int any = 0;
-    for (int c = 0; c < ncol; ++c) {
-      double tot = sum_tiles(a.rr_part, a.L.n_tiles, c, sred);
-      if (threadIdx.x == 0) {
-        st->rr[c] = tot;
-        st->rr0[c] = tot;
-        st->alpha[c] = 0.0;
-        st->beta[c] = 0.0;
-        st->iters[c] = 0;
-        st->active[c] = is_active(a.prm, c, 0, tot);
-        any |= st->active[c];
-        st->t[c] = 0.0;
+    __shared__ int act[MAXC];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int c = wid; c < MAXC; c += NT / 32) {
+      if (c < ncol) {
+        const double tot = col_total(a.rr_part, a.L.n_tiles, c);
+        if (lane == 0) {
+          st->rr[c] = tot;
+          st->rr0[c] = tot;
+          st->alpha[c] = 0.0;
+          st->beta[c] = 0.0;
+          st->iters[c] = 0;
+          st->t[c] = 0.0;
+          act[c] = st->active[c] = is_active(a.prm, c, 0, tot);
+        }
+      } else if (lane == 0) {
+        st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0;
+        act[c] = 0;
       }
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
-      for (int c = ncol; c < MAXC; ++c) { st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0; }
+      int any = 0;
+      for (int c = 0; c < ncol; ++c) any |= act[c];
       st->any_active = any;
       st->par = 0;
       st->hit_max = 0;
@@ -155,188 +158,206 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused apply on one row tile of cluster i:
-//   D_i    = (fuse_p ? R + beta o P_old : D) staged in smem (all ld_i rows)
+// Fused apply, persistent: CTA c owns clusters c, c+G, c+2G, ... (tiles are whole clusters).
+// For cluster i:
+//   D_i    = (fuse_p ? R + beta o P_old : D) staged in smem
 //   T_i    = mscale * sum_j Mp[i][j] S_j(D)                       (low-rank, Eq. 19-21)
-//   BD     = B_i D_i (rows of this tile; B = H or G streamed from HBM, 16-byte loads)
+//   BD     = B_i D_i, B_i (H or G, ld_i x ld_i column-major, contiguous) streamed through a
+//            NSTAGE-deep shared-memory ring by 1-D TMA bulk copies of KC-column chunks
 //   val    = a D + b_i BD + u_i T_i                                (Eq. 23-25 modes)
 //   out    = cA val + cV D + cP P2                                 (Q(A) / trace combines)
-// Epilogue: per-tile partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
+// Epilogue: per-cluster partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
+// The TMA producer (thread 0) runs ahead across clusters, so a cluster's prologue overlaps
+// the previous cluster's stream.
 template <int NCP>
-__global__ void __launch_bounds__(NT) apply_kernel(ApplyArgs a) {
+__global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
   if (a.gate && !a.st->any_active) return;
-  extern __shared__ double sm[];
-  const int t = blockIdx.x;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[NSTAGE];
   const int tid = threadIdx.x;
-  const TileDesc td = a.L.tiles[t];
-  const int i = td.blk, ld = a.L.ld[i], row0 = td.row0, nrows = td.nrows;
-  const int64_t p0 = a.L.poff[i], n_pad = a.L.n_pad;
-  const int n_c = a.L.n_c;
+  const int n_c = a.L.n_c, n_tiles = a.L.n_tiles;
+  const int64_t n_pad = a.L.n_pad;
   const int ncol = a.ncol;
   const EvalParams* P = a.prm;
   const int par = a.st->par;
-  double* Dsm = sm;                        // ld * NCP   (row-major: Dsm[k*NCP + c])
-  double* red = Dsm + ld * NCP;            // NT * 2 * NCP
-  double* sred = red + NT * 2 * NCP;       // NT * NCP (>= NT)
-  double* Tsm = sred + NT * NCP;           // NCP
-  double* Esm = Tsm + NCP;                 // NCP
-  double* cb = Esm + NCP;                  // NCP: beta ; NCP: active
+  const double* B = P->B;
+  const bool useB = (B != nullptr);
+  const int slot = a.slot_doubles;
+  double* ring = sm;                                   // NSTAGE * slot
+  double* Dsm = ring + (useB ? NSTAGE * slot : 0);     // ld_max * NCP (row-major Dsm[k*NCP+c])
+  double* red = Dsm + a.ld_max * NCP;                  // red_doubles (aliased by sred)
+  double* sred = red;
+  double* Tsm = red + a.red_doubles;                   // NCP
+  double* Esm = Tsm + NCP;                             // NCP
+  double* cb = Esm + NCP;                              // NCP beta ; NCP active
   if (tid < NCP) {
     cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
     cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
+  // producer cursor (thread 0): tile pt, chunk pc
+  int pt = blockIdx.x, pc = 0;
+  const int G = gridDim.x;
+  auto issue = [&](int s_) {
+    if (pt >= n_tiles) return;
+    const int i = a.L.tiles[pt].blk;
+    const int ld = a.L.ld[i];
+    const int KC = max(1, slot / ld);
+    const int k0 = pc * KC;
+    const int kc = min(KC, ld - k0);
+    const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&full[s_], bytes);
+    tma_load_1d(ring + s_ * slot, B + a.L.boff[i] + static_cast<int64_t>(k0) * ld, bytes, &full[s_]);
+    if ((pc + 1) * KC >= ld) { pc = 0; pt += G; } else { ++pc; }
+  };
+  if (tid == 0) {
+    for (int s_ = 0; s_ < NSTAGE; ++s_) mbar_init(&full[s_], 1);
+    fence_mbar_init();
+  }
   __syncthreads();
+  if (useB && tid == 0)
+    for (int s_ = 0; s_ < NSTAGE; ++s_) issue(s_);
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
-  // 1. stage D_i
-  for (int idx = tid; idx < ld * NCP; idx += NT) {
-    const int c = idx / ld, k = idx % ld;
-    double v = 0.0;
-    if (c < ncol) {
-      const int64_t g = c * n_pad + p0 + k;
-      if (a.fuse_p) {
-        const double po = Pold[g];
-        v = (cb[NCP + c] != 0.0) ? a.D[g] + cb[c] * po : po;
-        if (k >= row0 && k < row0 + nrows) Pnew[g] = v;
-      } else {
-        v = a.D[g];
-      }
-    }
-    Dsm[k * NCP + c] = v;
-  }
-  if (a.fuse_p && tid < ncol) {
-    const double sr = a.S_D[t * MAXC + tid], sp = a.SPbuf[par][t * MAXC + tid];
-    a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
-  }
-  // 2. low-rank coefficient T_i = sum_j Mp[i][j] S_j
-  {
-    double tacc[NCP];
-#pragma unroll
-    for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
-    const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
-    const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-    for (int j = tid; j < n_c; j += NT) {
-      const double m = Mrow[j];
-      const int tb = a.L.tile0[j], te = a.L.tile0[j + 1];
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) {
-        double s = 0.0;
-        for (int tt = tb; tt < te; ++tt) {
-          double v = a.S_D[tt * MAXC + c];
-          if (a.fuse_p) v = (cb[NCP + c] != 0.0) ? v + cb[c] * SPo[tt * MAXC + c] : SPo[tt * MAXC + c];
-          s += v;
+  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
+  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+  uint32_t seq = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += G) {
+    const TileDesc td = a.L.tiles[t];
+    const int i = td.blk, ld = a.L.ld[i];
+    const int64_t p0 = a.L.poff[i];
+    // 1. stage D_i
+    for (int idx = tid; idx < ld * NCP; idx += NT) {
+      const int c = idx / ld, k = idx % ld;
+      double v = 0.0;
+      if (c < ncol) {
+        const int64_t g = c * n_pad + p0 + k;
+        if (a.fuse_p) {
+          const double po = Pold[g];
+          v = (cb[NCP + c] != 0.0) ? a.D[g] + cb[c] * po : po;
+          Pnew[g] = v;
+        } else {
+          v = a.D[g];
         }
-        tacc[c] += m * s;
       }
+      Dsm[k * NCP + c] = v;
     }
-    block_reduce_cols<NCP>(tacc, sred, Tsm);   // includes __syncthreads (Dsm ready too)
-  }
-  // 3. block term BD = B_i D_i for rows [row0, row0+nrows), k split over KS groups
-  const double* B = P->B;
-  const bool useB = (B != nullptr);
-  const int RP = nrows >> 1;
-  int KS = NT / RP;
-  if (KS < 1) KS = 1;
-  const int grp = tid / RP, rp = tid % RP;
-  double acc0[NCP], acc1[NCP];
+    if (a.fuse_p && tid < ncol) {
+      const double sr = a.S_D[t * MAXC + tid], sp = SPo[t * MAXC + tid];
+      a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
+    }
+    // 2. low-rank coefficient T_i = sum_j Mp[i][j] S_j
+    {
+      double tacc[NCP];
 #pragma unroll
-  for (int c = 0; c < NCP; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
-  if (useB) {
-    if (grp < KS) {
-      const double* Bi = B + a.L.boff[i];
-      const int r = row0 + 2 * rp;
-      const int kchunk = (((ld + KS - 1) / KS) + 3) & ~3;
-      const int kb = grp * kchunk;
-      const int ke = min(ld, kb + kchunk);
-      const double* bp = Bi + static_cast<int64_t>(kb) * ld + r;
-      int k = kb;
-      for (; k + 4 <= ke; k += 4) {
-        double2 bb[4];
+      for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+      const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
+      for (int j = tid; j < n_c; j += NT) {
+        const double m = Mrow[j];
+        const double* sj = a.S_D + a.L.tile0[j] * MAXC;
+        const double* spj = a.fuse_p ? SPo + a.L.tile0[j] * MAXC : nullptr;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) bb[q] = __ldg(reinterpret_cast<const double2*>(bp + static_cast<int64_t>(q) * ld));
-        bp += static_cast<int64_t>(4) * ld;
+        for (int c = 0; c < NCP; ++c) {
+          double v = sj[c];
+          if (a.fuse_p) v = (cb[NCP + c] != 0.0) ? v + cb[c] * spj[c] : spj[c];
+          tacc[c] += m * v;
+        }
+      }
+      block_reduce_cols<NCP>(tacc, sred, Tsm);   // ends with __syncthreads (Dsm ready too)
+    }
+    // 3. block term, streamed through the TMA ring
+    const int RP = ld >> 1;
+    int KS = NT / RP;
+    if (KS < 1) KS = 1;
+    const int grp = tid / RP, rp = tid % RP;
+    const int r = 2 * rp;
+    double acc0[NCP], acc1[NCP];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const double2* dk = reinterpret_cast<const double2*>(Dsm + (k + q) * NCP);
+    for (int c = 0; c < NCP; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
+    if (useB) {
+      const int KC = max(1, slot / ld);
+      for (int k0 = 0; k0 < ld; k0 += KC) {
+        const int kc = min(KC, ld - k0);
+        const int s_ = seq % NSTAGE;
+        mbar_wait(&full[s_], (seq / NSTAGE) & 1u);
+        const double* cbuf = ring + s_ * slot;
+        if (grp < KS) {
+          for (int kk = grp; kk < kc; kk += KS) {
+            const double2 b2 = *reinterpret_cast<const double2*>(cbuf + kk * ld + r);
+            const double2* dk = reinterpret_cast<const double2*>(Dsm + (k0 + kk) * NCP);
 #pragma unroll
-          for (int c2 = 0; c2 < NCP / 2; ++c2) {
-            const double2 dv = dk[c2];
-            acc0[2 * c2] = fma(bb[q].x, dv.x, acc0[2 * c2]);
-            acc0[2 * c2 + 1] = fma(bb[q].x, dv.y, acc0[2 * c2 + 1]);
-            acc1[2 * c2] = fma(bb[q].y, dv.x, acc1[2 * c2]);
-            acc1[2 * c2 + 1] = fma(bb[q].y, dv.y, acc1[2 * c2 + 1]);
+            for (int c2 = 0; c2 < NCP / 2; ++c2) {
+              const double2 dv = dk[c2];
+              acc0[2 * c2] = fma(b2.x, dv.x, acc0[2 * c2]);
+              acc0[2 * c2 + 1] = fma(b2.x, dv.y, acc0[2 * c2 + 1]);
+              acc1[2 * c2] = fma(b2.y, dv.x, acc1[2 * c2]);
+              acc1[2 * c2 + 1] = fma(b2.y, dv.y, acc1[2 * c2 + 1]);
+            }
+          }
+        }
+        __syncthreads();                      // slot s_ fully consumed
+        if (tid == 0) issue(s_);
+        ++seq;
+      }
+      if (KS > 1) {
+        if (grp > 0 && grp < KS) {
+          double* dst = red + ((grp - 1) * RP + rp) * 2 * NCP;
+#pragma unroll
+          for (int c = 0; c < NCP; ++c) { dst[c] = acc0[c]; dst[NCP + c] = acc1[c]; }
+        }
+        __syncthreads();
+        if (grp == 0) {
+          for (int gg = 1; gg < KS; ++gg) {
+            const double* src = red + ((gg - 1) * RP + rp) * 2 * NCP;
+#pragma unroll
+            for (int c = 0; c < NCP; ++c) { acc0[c] += src[c]; acc1[c] += src[NCP + c]; }
           }
         }
       }
-      for (; k < ke; ++k, bp += ld) {
-        const double2 b2 = __ldg(reinterpret_cast<const double2*>(bp));
-        const double2* dk = reinterpret_cast<const double2*>(Dsm + k * NCP);
-#pragma unroll
-        for (int c2 = 0; c2 < NCP / 2; ++c2) {
-          const double2 dv = dk[c2];
-          acc0[2 * c2] = fma(b2.x, dv.x, acc0[2 * c2]);
-          acc0[2 * c2 + 1] = fma(b2.x, dv.y, acc0[2 * c2 + 1]);
-          acc1[2 * c2] = fma(b2.y, dv.x, acc1[2 * c2]);
-          acc1[2 * c2 + 1] = fma(b2.y, dv.y, acc1[2 * c2 + 1]);
-        }
-      }
-      if (grp > 0) {
-        double* dst = red + ((grp - 1) * RP + rp) * 2 * NCP;
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) { dst[c] = acc0[c]; dst[NCP + c] = acc1[c]; }
-      }
     }
-    __syncthreads();
+    // 4. epilogue (group 0 owns the row pairs)
+    double ep[NCP];
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
     if (grp == 0) {
-      for (int gg = 1; gg < KS; ++gg) {
-        const double* src = red + ((gg - 1) * RP + rp) * 2 * NCP;
+      const double bi = P->b0 + P->b1 * a.jitter[i];
+      const double pa = P->a, ms = P->mscale;
 #pragma unroll
-        for (int c = 0; c < NCP; ++c) { acc0[c] += src[c]; acc1[c] += src[NCP + c]; }
-      }
-    }
-  }
-  // 4. epilogue (group 0 owns row pairs)
-  double ep[NCP];
+      for (int h = 0; h < 2; ++h) {
+        const int rr = r + h;
+        const int64_t gl = p0 + rr;
+        const double uu = a.u[gl];
 #pragma unroll
-  for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
-  if (grp == 0) {
-    const double bi = P->b0 + P->b1 * a.jitter[i];
-    const double pa = P->a, ms = P->mscale;
-    const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
-    const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
-#pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      const int r = row0 + 2 * rp + h;
-      const int64_t gl = p0 + r;
-      const double uu = a.u[gl];
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) {
-        if (c < ncol) {
-          const double d = Dsm[r * NCP + c];
-          const double bd = (h == 0) ? acc0[c] : acc1[c];
-          double val = pa * d;
-          if (useB) val += bi * bd;
-          val += uu * (ms * Tsm[c]);
-          double o = a.cA[c] * val + a.cV[c] * d;
-          if (P2) o += a.cP[c] * P2[c * n_pad + gl];
-          a.out[c * n_pad + gl] = o;
-          ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
+        for (int c = 0; c < NCP; ++c) {
+          if (c < ncol) {
+            const double d = Dsm[rr * NCP + c];
+            const double bd = (h == 0) ? acc0[c] : acc1[c];
+            double val = pa * d;
+            if (useB) val += bi * bd;
+            val += uu * (ms * Tsm[c]);
+            double o = a.cA[c] * val + a.cV[c] * d;
+            if (P2) o += a.cP[c] * P2[c * n_pad + gl];
+            a.out[c * n_pad + gl] = o;
+            ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
+          }
         }
       }
     }
+    block_reduce_cols<NCP>(ep, sred, Esm);
+    if (tid < ncol) {
+      if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = Esm[tid];
+      else a.dots[t * MAXC + tid] = Esm[tid];
+    }
   }
-  block_reduce_cols<NCP>(ep, sred, Esm);
-  if (tid < ncol) {
-    if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = Esm[tid];
-    else a.dots[t * MAXC + tid] = Esm[tid];
-  }
-  // 5. finaliser
+  // 5. finaliser (last CTA; one warp per column)
   if (a.fin != FIN_NONE) {
     if (last_cta(&a.st->ticket[a.fin])) {
       CGState* st = a.st;
-      for (int c = 0; c < ncol; ++c) {
-        const double tot = sum_tiles(a.dots, a.L.n_tiles, c, sred);
-        if (tid == 0) {
+      const int lane = tid & 31, wid = tid >> 5;
+      for (int c = wid; c < ncol; c += NT / 32) {
+        const double tot = col_total(a.dots, n_tiles, c);
+        if (lane == 0) {
           if (a.fin == FIN_ALPHA) {
             if (st->active[c]) {
               const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
@@ -348,6 +369,7 @@ __global__ void __launch_bounds__(NT) apply_kernel(ApplyArgs a) {
           }
         }
       }
+      __syncthreads();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
   }
@@ -401,26 +423,31 @@ __global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
   if (threadIdx.x < ncol) a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
   if (last_cta(&st->ticket[FIN_UPDATE])) {
     const EvalParams* P = a.prm;
-    int any = 0;
-    for (int c = 0; c < ncol; ++c) {
-      const bool act = st->active[c] != 0;     // uniform across the CTA
+    __shared__ int act[MAXC];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int c = wid; c < ncol; c += NT / 32) {
+      const bool was = st->active[c] != 0;
       double tot = 0.0;
-      if (act) tot = sum_tiles(a.rr_part, a.L.n_tiles, c, sred);
-      if (threadIdx.x == 0 && act) {
-        const double be = tot / st->rr[c];
-        st->beta[c] = be;
-        a.beta_hist[c * a.hist_stride + st->iters[c]] = be;
-        st->rr[c] = tot;
-        st->iters[c] += 1;
-        const int na = is_active(P, c, st->iters[c], tot);
-        if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
-          st->hit_max = 1;
-        st->active[c] = na;
+      if (was) tot = col_total(a.rr_part, a.L.n_tiles, c);
+      if (lane == 0) {
+        if (was) {
+          const double be = tot / st->rr[c];
+          st->beta[c] = be;
+          a.beta_hist[c * a.hist_stride + st->iters[c]] = be;
+          st->rr[c] = tot;
+          st->iters[c] += 1;
+          const int na = is_active(P, c, st->iters[c], tot);
+          if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
+            st->hit_max = 1;
+          st->active[c] = na;
+        }
+        act[c] = st->active[c];
       }
-      if (threadIdx.x == 0) any |= st->active[c];
-      __syncthreads();
     }
+    __syncthreads();
     if (threadIdx.x == 0) {
+      int any = 0;
+      for (int c = 0; c < ncol; ++c) any |= act[c];
       st->any_active = any;
       st->par = par ^ 1;
       st->ticket[FIN_UPDATE] = 0;
@@ -532,28 +559,41 @@ __global__ void probe_gen_kernel(uint64_t seed, int m, int64_t n, double* Z) {
 
 // ======================================================================================
 // launchers
+static int num_sms() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    if (v <= 0) v = 148;
+  }
+  return v;
+}
+
+size_t apply_smem_bytes(int ncp, int ld_max, bool useB, int slot_doubles, int red_doubles) {
+  return sizeof(double) * ((useB ? static_cast<size_t>(NSTAGE) * slot_doubles : 0) +
+                           static_cast<size_t>(ld_max) * ncp + red_doubles + 4 * ncp);
+}
+
 template <int NCP>
-static void apply_launch_t(const ApplyArgs& a, int ld_max, cudaStream_t s) {
-  size_t smem = sizeof(double) * (static_cast<size_t>(ld_max) * NCP + NT * 2 * NCP + NT * NCP + 4 * NCP);
+static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
+  size_t smem = apply_smem_bytes(NCP, a.ld_max, useB, a.slot_doubles, a.red_doubles);
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  apply_kernel<NCP><<<a.L.n_tiles, NT, smem, s>>>(a);
+  const int grid = std::min(a.L.n_tiles, num_sms());
+  apply_kernel<NCP><<<grid, NT, smem, s>>>(a);
   note_launch(); post_launch("apply_kernel");
 }
 
-size_t apply_smem_bytes(int ncp, int ld_max) {
-  return sizeof(double) * (static_cast<size_t>(ld_max) * ncp + NT * 2 * ncp + NT * ncp + 4 * ncp);
-}
-
-void launch_apply(const ApplyArgs& a, int ncp, int ld_max, cudaStream_t s) {
+void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
   switch (ncp) {
-    case 2: apply_launch_t<2>(a, ld_max, s); break;
-    case 4: apply_launch_t<4>(a, ld_max, s); break;
-    case 6: apply_launch_t<6>(a, ld_max, s); break;
-    case 8: apply_launch_t<8>(a, ld_max, s); break;
-    case 10: apply_launch_t<10>(a, ld_max, s); break;
-    case 12: apply_launch_t<12>(a, ld_max, s); break;
-    case 14: apply_launch_t<14>(a, ld_max, s); break;
-    default: apply_launch_t<16>(a, ld_max, s); break;
+    case 2: apply_launch_t<2>(a, useB, s); break;
+    case 4: apply_launch_t<4>(a, useB, s); break;
+    case 6: apply_launch_t<6>(a, useB, s); break;
+    case 8: apply_launch_t<8>(a, useB, s); break;
+    case 10: apply_launch_t<10>(a, useB, s); break;
+    case 12: apply_launch_t<12>(a, useB, s); break;
+    case 14: apply_launch_t<14>(a, useB, s); break;
+    default: apply_launch_t<16>(a, useB, s); break;
   }
 }
 
