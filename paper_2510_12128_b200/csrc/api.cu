@@ -680,8 +680,16 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
   a1.alpha_hist = e.ah; a1.hist_stride = HIST;
   a1.ld_max = L.ld_max;
-  a1.slot_doubles = std::max(SLOT_TARGET_DOUBLES, L.ld_max);
-  a1.red_doubles = 2 * ncp * NT;
+  {
+    const ApplyPlan pl = plan_apply(ncp, ncol, L.ld_max, Ld.n_tiles, apply_grid(Ld.n_tiles));
+    if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, m=%d)", L.ld_max, m);
+    a1.slot_doubles = pl.slot_doubles;
+    a1.red_doubles = pl.red_doubles;
+    a1.nstage = pl.nstage;
+    a1.nmine_max = pl.nmine_max;
+    a1.smem_b = pl.smem_b;
+    a1.smem_nob = pl.smem_nob;
+  }
   ApplyArgs a2 = a1;
   // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
   a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;

@@ -20,7 +20,7 @@ namespace nugpr {
 constexpr int MAXC = 16;        // max columns per apply (1 + m)
 constexpr int NT = 256;         // threads per CTA for the tile kernels
 constexpr int TILE_ROWS = 512;  // max padded rows per tile (= whole clusters in this build)
-constexpr int NSTAGE = 3;       // TMA ring depth of the apply kernel
+constexpr int MAX_NSTAGE = 6;   // max TMA ring depth of the apply kernel
 constexpr int SLOT_TARGET_DOUBLES = 3072;  // ~24 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
 
@@ -109,6 +109,15 @@ struct ApplyArgs {
   int ld_max;
   int slot_doubles;        // TMA ring slot size (>= ld_max)
   int red_doubles;         // cross-k-group reduction scratch
+  int nstage;              // TMA ring depth
+  int nmine_max;           // max clusters per persistent CTA
+  size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
+};
+
+struct ApplyPlan {
+  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0;
+  size_t smem_b = 0, smem_nob = 0;
+  bool ok = false;
 };
 
 struct UpdateArgs {

@@ -160,20 +160,22 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
 // ---------------------------------------------------------------------------------------
 // Fused apply, persistent: CTA c owns clusters c, c+G, c+2G, ... (tiles are whole clusters).
 // For cluster i:
-//   D_i    = (fuse_p ? R + beta o P_old : D) staged in smem
-//   T_i    = mscale * sum_j Mp[i][j] S_j(D)                       (low-rank, Eq. 19-21)
-//   BD     = B_i D_i, B_i (H or G, ld_i x ld_i column-major, contiguous) streamed through a
-//            NSTAGE-deep shared-memory ring by 1-D TMA bulk copies of KC-column chunks
-//   val    = a D + b_i BD + u_i T_i                                (Eq. 23-25 modes)
-//   out    = cA val + cV D + cP P2                                 (Q(A) / trace combines)
+//   D_i    = (fuse_p ? R + beta o P_old : D)      inputs TMA-prefetched one cluster ahead
+//   T_i    = mscale * sum_j Mp[i][j] S_j(D)       (low-rank, Eq. 19-21; all of this CTA's
+//                                                   clusters computed once at kernel start)
+//   BD     = B_i D_i, B_i (H or G, ld_i x ld_i column-major, contiguous) streamed through an
+//            nstage-deep shared-memory ring by 1-D TMA bulk copies of KC-column chunks
+//   val    = a D + b_i BD + u_i T_i                (Eq. 23-25 modes)
+//   out    = cA val + cV D + cP P2                 (Q(A) / trace combines)
 // Epilogue: per-cluster partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
-// The TMA producer (thread 0) runs ahead across clusters, so a cluster's prologue overlaps
-// the previous cluster's stream.
+// The TMA producer (thread 0) runs ahead across clusters, so a cluster's prologue and
+// epilogue overlap the B stream of the next one.
 template <int NCP>
 __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
   if (a.gate && !a.st->any_active) return;
   extern __shared__ __align__(128) double sm[];
-  __shared__ __align__(8) uint64_t full[NSTAGE];
+  __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t dbar;
   const int tid = threadIdx.x;
   const int n_c = a.L.n_c, n_tiles = a.L.n_tiles;
   const int64_t n_pad = a.L.n_pad;
@@ -183,20 +185,29 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
   const double* B = P->B;
   const bool useB = (B != nullptr);
   const int slot = a.slot_doubles;
-  double* ring = sm;                                   // NSTAGE * slot
-  double* Dsm = ring + (useB ? NSTAGE * slot : 0);     // ld_max * NCP (row-major Dsm[k*NCP+c])
-  double* red = Dsm + a.ld_max * NCP;                  // red_doubles (aliased by sred)
+  const int nstage = a.nstage;
+  const int G = gridDim.x;
+  const int nmine = (n_tiles - static_cast<int>(blockIdx.x) + G - 1) / G;
+  const int nsrc = a.fuse_p ? 2 : 1;
+  double* ring = sm;                                         // nstage * slot (useB only)
+  double* stg = ring + (useB ? nstage * slot : 0);           // nsrc * ncol * ld_max (staged D inputs)
+  double* Dsm = stg + 2 * ncol * a.ld_max;                   // ld_max * NCP (row-major Dsm[k*NCP+c])
+  double* red = Dsm + a.ld_max * NCP;                        // red_doubles (aliased by sred)
   double* sred = red;
-  double* Tsm = red + a.red_doubles;                   // NCP
-  double* Esm = Tsm + NCP;                             // NCP
-  double* cb = Esm + NCP;                              // NCP beta ; NCP active
+  double* Tall = red + a.red_doubles;                        // nmine_max * NCP
+  double* Esm = Tall + a.nmine_max * NCP;                    // NCP
+  double* cb = Esm + NCP;                                    // NCP beta ; NCP active
   if (tid < NCP) {
     cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
     cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
+  const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
+  double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
+  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   // producer cursor (thread 0): tile pt, chunk pc
   int pt = blockIdx.x, pc = 0;
-  const int G = gridDim.x;
   auto issue = [&](int s_) {
     if (pt >= n_tiles) return;
     const int i = a.L.tiles[pt].blk;
@@ -210,35 +221,89 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
     tma_load_1d(ring + s_ * slot, B + a.L.boff[i] + static_cast<int64_t>(k0) * ld, bytes, &full[s_]);
     if ((pc + 1) * KC >= ld) { pc = 0; pt += G; } else { ++pc; }
   };
+  // D-input prefetch of tile t (thread 0): ncol columns of D (and of P_old when fused)
+  auto issue_stage = [&](int t) {
+    const int i = a.L.tiles[t].blk;
+    const int ld = a.L.ld[i];
+    const int64_t p0 = a.L.poff[i];
+    const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&dbar, cbytes * ncol * nsrc);
+    for (int c = 0; c < ncol; ++c) {
+      tma_load_1d(stg + c * ld, a.D + c * n_pad + p0, cbytes, &dbar);
+      if (nsrc == 2) tma_load_1d(stg + (ncol + c) * ld, Pold + c * n_pad + p0, cbytes, &dbar);
+    }
+  };
   if (tid == 0) {
-    for (int s_ = 0; s_ < NSTAGE; ++s_) mbar_init(&full[s_], 1);
+    for (int s_ = 0; s_ < nstage; ++s_) mbar_init(&full[s_], 1);
+    mbar_init(&dbar, 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (useB && tid == 0)
-    for (int s_ = 0; s_ < NSTAGE; ++s_) issue(s_);
-  const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
-  double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
-  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
-  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+  if (tid == 0) {
+    issue_stage(blockIdx.x);
+    if (useB)
+      for (int s_ = 0; s_ < nstage; ++s_) issue(s_);
+  }
+  // low-rank coefficients of all my clusters: T[q][c] = sum_j Mp[i_q][j] S_j[c]
+  {
+    constexpr int JPT = 4;                      // j values held per thread per sweep
+    for (int j0 = 0; j0 < n_c; j0 += NT * JPT) {
+      double sv[JPT][NCP];
+#pragma unroll
+      for (int u_ = 0; u_ < JPT; ++u_) {
+        const int j = j0 + u_ * NT + tid;
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) sv[u_][c] = 0.0;
+        if (j < n_c) {
+          const double* sj = a.S_D + a.L.tile0[j] * MAXC;
+          if (a.fuse_p) {
+            const double* spj = SPo + a.L.tile0[j] * MAXC;
+#pragma unroll
+            for (int c = 0; c < NCP; ++c)
+              sv[u_][c] = (cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c];
+          } else {
+#pragma unroll
+            for (int c = 0; c < NCP; ++c) sv[u_][c] = sj[c];
+          }
+        }
+      }
+      for (int q = 0; q < nmine; ++q) {
+        const int i = a.L.tiles[blockIdx.x + q * G].blk;
+        const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
+        double tacc[NCP];
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+#pragma unroll
+        for (int u_ = 0; u_ < JPT; ++u_) {
+          const int j = j0 + u_ * NT + tid;
+          const double m = (j < n_c) ? Mrow[j] : 0.0;
+#pragma unroll
+          for (int c = 0; c < NCP; ++c) tacc[c] += m * sv[u_][c];
+        }
+        block_reduce_cols<NCP>(tacc, sred, Esm);
+        if (tid < NCP) Tall[q * NCP + tid] = (j0 == 0 ? 0.0 : Tall[q * NCP + tid]) + Esm[tid];
+        __syncthreads();
+      }
+    }
+  }
   uint32_t seq = 0;
-  for (int t = blockIdx.x; t < n_tiles; t += G) {
+  int q = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
     const TileDesc td = a.L.tiles[t];
     const int i = td.blk, ld = a.L.ld[i];
     const int64_t p0 = a.L.poff[i];
-    // 1. stage D_i
+    // 1. D_i from the staged inputs (fused: D = R + beta o P_old, P_new written back)
+    mbar_wait(&dbar, static_cast<uint32_t>(q & 1));
     for (int idx = tid; idx < ld * NCP; idx += NT) {
       const int c = idx / ld, k = idx % ld;
       double v = 0.0;
       if (c < ncol) {
-        const int64_t g = c * n_pad + p0 + k;
+        v = stg[c * ld + k];
         if (a.fuse_p) {
-          const double po = Pold[g];
-          v = (cb[NCP + c] != 0.0) ? a.D[g] + cb[c] * po : po;
-          Pnew[g] = v;
-        } else {
-          v = a.D[g];
+          const double po = stg[(ncol + c) * ld + k];
+          v = (cb[NCP + c] != 0.0) ? v + cb[c] * po : po;
+          Pnew[c * n_pad + p0 + k] = v;
         }
       }
       Dsm[k * NCP + c] = v;
@@ -247,26 +312,9 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
       const double sr = a.S_D[t * MAXC + tid], sp = SPo[t * MAXC + tid];
       a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
     }
-    // 2. low-rank coefficient T_i = sum_j Mp[i][j] S_j
-    {
-      double tacc[NCP];
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
-      const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
-      for (int j = tid; j < n_c; j += NT) {
-        const double m = Mrow[j];
-        const double* sj = a.S_D + a.L.tile0[j] * MAXC;
-        const double* spj = a.fuse_p ? SPo + a.L.tile0[j] * MAXC : nullptr;
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) {
-          double v = sj[c];
-          if (a.fuse_p) v = (cb[NCP + c] != 0.0) ? v + cb[c] * spj[c] : spj[c];
-          tacc[c] += m * v;
-        }
-      }
-      block_reduce_cols<NCP>(tacc, sred, Tsm);   // ends with __syncthreads (Dsm ready too)
-    }
-    // 3. block term, streamed through the TMA ring
+    __syncthreads();                                  // stg consumed, Dsm ready
+    if (tid == 0 && t + G < n_tiles) issue_stage(t + G);
+    // 2. block term, streamed through the TMA ring
     const int RP = ld >> 1;
     int KS = NT / RP;
     if (KS < 1) KS = 1;
@@ -279,8 +327,8 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
       const int KC = max(1, slot / ld);
       for (int k0 = 0; k0 < ld; k0 += KC) {
         const int kc = min(KC, ld - k0);
-        const int s_ = seq % NSTAGE;
-        mbar_wait(&full[s_], (seq / NSTAGE) & 1u);
+        const int s_ = static_cast<int>(seq % nstage);
+        mbar_wait(&full[s_], (seq / nstage) & 1u);
         const double* cbuf = ring + s_ * slot;
         if (grp < KS) {
           for (int kk = grp; kk < kc; kk += KS) {
@@ -316,32 +364,44 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
         }
       }
     }
-    // 4. epilogue (group 0 owns the row pairs)
+    // 3. epilogue (group 0 owns the row pairs)
     double ep[NCP];
 #pragma unroll
     for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
     if (grp == 0) {
       const double bi = P->b0 + P->b1 * a.jitter[i];
       const double pa = P->a, ms = P->mscale;
+      const double* Tq = Tall + q * NCP;
+      const double2 u2 = *reinterpret_cast<const double2*>(a.u + p0 + r);
+      double p2v[2][NCP], y2v[2][NCP];
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) {
+        const bool on = c < ncol;
+        const int64_t g = c * n_pad + p0 + r;
+        double2 pp = make_double2(0.0, 0.0), yy = make_double2(0.0, 0.0);
+        if (on && P2) pp = *reinterpret_cast<const double2*>(P2 + g);
+        if (on && a.epi != EPI_S) yy = *reinterpret_cast<const double2*>(Y2 + g);
+        p2v[0][c] = pp.x; p2v[1][c] = pp.y; y2v[0][c] = yy.x; y2v[1][c] = yy.y;
+      }
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int rr = r + h;
-        const int64_t gl = p0 + rr;
-        const double uu = a.u[gl];
+        const double uu = (h == 0) ? u2.x : u2.y;
+        double o[NCP];
 #pragma unroll
         for (int c = 0; c < NCP; ++c) {
-          if (c < ncol) {
-            const double d = Dsm[rr * NCP + c];
-            const double bd = (h == 0) ? acc0[c] : acc1[c];
-            double val = pa * d;
-            if (useB) val += bi * bd;
-            val += uu * (ms * Tsm[c]);
-            double o = a.cA[c] * val + a.cV[c] * d;
-            if (P2) o += a.cP[c] * P2[c * n_pad + gl];
-            a.out[c * n_pad + gl] = o;
-            ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
-          }
+          const double d = Dsm[rr * NCP + c];
+          const double bd = (h == 0) ? acc0[c] : acc1[c];
+          double val = pa * d;
+          if (useB) val += bi * bd;
+          val += uu * (ms * Tq[c]);
+          o[c] = a.cA[c] * val + a.cV[c] * d;
+          if (P2) o[c] += a.cP[c] * p2v[h][c];
+          ep[c] += (a.epi == EPI_S) ? uu * o[c] : o[c] * y2v[h][c];
         }
+#pragma unroll
+        for (int c = 0; c < NCP; ++c)
+          if (c < ncol) a.out[c * n_pad + p0 + rr] = o[c];
       }
     }
     block_reduce_cols<NCP>(ep, sred, Esm);
@@ -350,7 +410,7 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
       else a.dots[t * MAXC + tid] = Esm[tid];
     }
   }
-  // 5. finaliser (last CTA; one warp per column)
+  // 4. finaliser (last CTA; one warp per column)
   if (a.fin != FIN_NONE) {
     if (last_cta(&a.st->ticket[a.fin])) {
       CGState* st = a.st;
@@ -382,7 +442,7 @@ template <int NCP>
 __global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
   CGState* st = a.st;
   if (!st->any_active) return;
-  __shared__ double sred[NT * MAXC];
+  __shared__ double sred[(NT / 32) * MAXC];
   __shared__ double outv[MAXC];
   __shared__ double cal[NCP], cact[NCP];
   const int t = blockIdx.x;
@@ -459,7 +519,7 @@ __global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
 // S partials of a vector block: part[t][c] = sum_rows u * V[c]  (used before the trace applies)
 __global__ void __launch_bounds__(NT) spart_kernel(LayoutDev L, const double* u, const double* V,
                                                    int ncol, double* part) {
-  __shared__ double sred[NT * MAXC];
+  __shared__ double sred[(NT / 32) * MAXC];
   __shared__ double outv[MAXC];
   const TileDesc td = L.tiles[blockIdx.x];
   const int64_t p0 = L.poff[td.blk] + td.row0;
@@ -570,17 +630,39 @@ static int num_sms() {
   return v;
 }
 
-size_t apply_smem_bytes(int ncp, int ld_max, bool useB, int slot_doubles, int red_doubles) {
-  return sizeof(double) * ((useB ? static_cast<size_t>(NSTAGE) * slot_doubles : 0) +
-                           static_cast<size_t>(ld_max) * ncp + red_doubles + 4 * ncp);
+// Shared-memory plan of the apply kernel (host side): ring depth chosen to fit.
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int n_tiles, int grid) {
+  ApplyPlan p;
+  int dev = 0, optin = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  const size_t budget = static_cast<size_t>(optin) - 2048;
+  const int rp = ld_max / 2;
+  const int ks = std::max(1, NT / std::max(1, rp));
+  p.red_doubles = std::max((ks - 1) * rp * 2 * ncp, (NT / 32) * ncp);
+  p.nmine_max = (n_tiles + grid - 1) / grid;
+  p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
+  const size_t fixed = static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
+                       p.red_doubles + static_cast<size_t>(p.nmine_max) * ncp + 3 * ncp;
+  long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
+  p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+  if (p.nstage < 2) {
+    p.slot_doubles = ld_max;
+    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+  }
+  p.smem_nob = fixed * sizeof(double);
+  p.smem_b = (fixed + static_cast<size_t>(p.nstage) * p.slot_doubles) * sizeof(double);
+  p.ok = p.nstage >= 2;
+  return p;
 }
+
+int apply_grid(int n_tiles) { return std::min(n_tiles, num_sms()); }
 
 template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
-  size_t smem = apply_smem_bytes(NCP, a.ld_max, useB, a.slot_doubles, a.red_doubles);
+  size_t smem = useB ? a.smem_b : a.smem_nob;
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  const int grid = std::min(a.L.n_tiles, num_sms());
-  apply_kernel<NCP><<<grid, NT, smem, s>>>(a);
+  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NT, smem, s>>>(a);
   note_launch(); post_launch("apply_kernel");
 }
 
