@@ -681,7 +681,8 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   a1.alpha_hist = e.ah; a1.hist_stride = HIST;
   a1.ld_max = L.ld_max;
   {
-    const ApplyPlan pl = plan_apply(ncp, ncol, L.ld_max, Ld.n_tiles, apply_grid(Ld.n_tiles));
+    const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
+    const ApplyPlan pl = plan_apply(ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles));
     if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, m=%d)", L.ld_max, m);
     a1.slot_doubles = pl.slot_doubles;
     a1.red_doubles = pl.red_doubles;

@@ -21,7 +21,7 @@ constexpr int MAXC = 16;        // max columns per apply (1 + m)
 constexpr int NT = 256;         // threads per CTA for the tile kernels
 constexpr int TILE_ROWS = 512;  // max padded rows per tile (= whole clusters in this build)
 constexpr int MAX_NSTAGE = 6;   // max TMA ring depth of the apply kernel
-constexpr int SLOT_TARGET_DOUBLES = 3072;  // ~24 KB per TMA chunk
+constexpr int SLOT_TARGET_DOUBLES = 4096;  // ~32 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
 
 struct TileDesc {

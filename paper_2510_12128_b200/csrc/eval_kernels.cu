@@ -158,25 +158,71 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Fused apply, persistent: CTA c owns clusters c, c+G, c+2G, ... (tiles are whole clusters).
+// Fused apply, persistent and warp-specialised.  CTA c owns clusters c, c+G, ... (tiles are
+// whole clusters).  Warp NWC (the last) is the TMA producer; warps 0..NWC-1 consume.
 // For cluster i:
-//   D_i    = (fuse_p ? R + beta o P_old : D)      inputs TMA-prefetched one cluster ahead
+//   D_i    = (fuse_p ? R + beta o P_old : D)      inputs TMA-staged by the producer
 //   T_i    = mscale * sum_j Mp[i][j] S_j(D)       (low-rank, Eq. 19-21; all of this CTA's
 //                                                   clusters computed once at kernel start)
-//   BD     = B_i D_i, B_i (H or G, ld_i x ld_i column-major, contiguous) streamed through an
-//            nstage-deep shared-memory ring by 1-D TMA bulk copies of KC-column chunks
+//   BD     = B_i D_i: B_i (H or G, ld_i x ld_i column-major, contiguous) streams through an
+//            nstage-deep shared-memory ring of KC-column chunks (1-D TMA bulk copies,
+//            full/empty mbarriers per slot; no CTA-wide barrier in the stream)
 //   val    = a D + b_i BD + u_i T_i                (Eq. 23-25 modes)
 //   out    = cA val + cV D + cP P2                 (Q(A) / trace combines)
+// Consumer mapping: thread -> (row quad rq, k-group g), g in the low lane bits (KG lanes per
+// row quad, KG a power of two): each thread accumulates 4 rows x NCP columns over the chunk
+// columns kk = g (mod KG); the KG partial sums are combined with xor shuffles.
 // Epilogue: per-cluster partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
-// The TMA producer (thread 0) runs ahead across clusters, so a cluster's prologue and
-// epilogue overlap the B stream of the next one.
+constexpr int NTA = 512;              // threads per apply CTA
+constexpr int NWC = NTA / 32 - 1;     // consumer warps
+constexpr int NTC = NWC * 32;         // consumer threads
+
+__device__ __forceinline__ void cons_sync() {
+  asm volatile("bar.sync 1, %0;" ::"r"(NTC) : "memory");
+}
+
 template <int NCP>
-__global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
+__device__ __forceinline__ void cons_reduce_cols(double (&v)[NCP], double* sred, double* out) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) v[c] = warp_sum(v[c]);
+  cons_sync();
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) sred[wid * NCP + c] = v[c];
+  }
+  cons_sync();
+  if (threadIdx.x < NCP) {
+    double s = 0.0;
+    for (int w = 0; w < NWC; ++w) s += sred[w * NCP + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+  cons_sync();
+}
+
+template <int RPT>
+__device__ __forceinline__ int apply_kg(int ld) {
+  const int rq = ld / RPT;
+  int kg = 1;
+  while (kg < 32 && rq * kg * 2 <= NTC) kg <<= 1;
+  return kg;
+}
+__device__ __forceinline__ int apply_kc(int ld, int slot, int kg) {
+  int kc = max(1, slot / ld);
+  if (kc >= kg) kc = (kc / kg) * kg;
+  return kc;
+}
+
+template <int NCP>
+__global__ void __launch_bounds__(NTA, 1) apply_kernel(ApplyArgs a) {
+  constexpr int RPT = (NCP <= 10) ? 4 : 2;   // rows per consumer thread (register budget)
   if (a.gate && !a.st->any_active) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
-  __shared__ __align__(8) uint64_t dbar;
+  __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t dbar, dfree;
   const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
   const int n_c = a.L.n_c, n_tiles = a.L.n_tiles;
   const int64_t n_pad = a.L.n_pad;
   const int ncol = a.ncol;
@@ -190,232 +236,223 @@ __global__ void __launch_bounds__(NT, 1) apply_kernel(ApplyArgs a) {
   const int nmine = (n_tiles - static_cast<int>(blockIdx.x) + G - 1) / G;
   const int nsrc = a.fuse_p ? 2 : 1;
   double* ring = sm;                                         // nstage * slot (useB only)
-  double* stg = ring + (useB ? nstage * slot : 0);           // nsrc * ncol * ld_max (staged D inputs)
+  double* stg = ring + (useB ? nstage * slot : 0);           // 2 * ncol * ld_max (staged D inputs)
   double* Dsm = stg + 2 * ncol * a.ld_max;                   // ld_max * NCP (row-major Dsm[k*NCP+c])
-  double* red = Dsm + a.ld_max * NCP;                        // red_doubles (aliased by sred)
-  double* sred = red;
-  double* Tall = red + a.red_doubles;                        // nmine_max * NCP
+  double* sred = Dsm + a.ld_max * NCP;                       // NWC * NCP
+  double* Tall = sred + NWC * NCP;                           // nmine_max * NCP
   double* Esm = Tall + a.nmine_max * NCP;                    // NCP
   double* cb = Esm + NCP;                                    // NCP beta ; NCP active
-  if (tid < NCP) {
-    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
-    cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
-  }
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
   const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
   const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
-  // producer cursor (thread 0): tile pt, chunk pc
-  int pt = blockIdx.x, pc = 0;
-  auto issue = [&](int s_) {
-    if (pt >= n_tiles) return;
-    const int i = a.L.tiles[pt].blk;
-    const int ld = a.L.ld[i];
-    const int KC = max(1, slot / ld);
-    const int k0 = pc * KC;
-    const int kc = min(KC, ld - k0);
-    const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&full[s_], bytes);
-    tma_load_1d(ring + s_ * slot, B + a.L.boff[i] + static_cast<int64_t>(k0) * ld, bytes, &full[s_]);
-    if ((pc + 1) * KC >= ld) { pc = 0; pt += G; } else { ++pc; }
-  };
-  // D-input prefetch of tile t (thread 0): ncol columns of D (and of P_old when fused)
-  auto issue_stage = [&](int t) {
-    const int i = a.L.tiles[t].blk;
-    const int ld = a.L.ld[i];
-    const int64_t p0 = a.L.poff[i];
-    const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
-    fence_proxy_async_smem();
-    mbar_arrive_expect_tx(&dbar, cbytes * ncol * nsrc);
-    for (int c = 0; c < ncol; ++c) {
-      tma_load_1d(stg + c * ld, a.D + c * n_pad + p0, cbytes, &dbar);
-      if (nsrc == 2) tma_load_1d(stg + (ncol + c) * ld, Pold + c * n_pad + p0, cbytes, &dbar);
-    }
-  };
   if (tid == 0) {
-    for (int s_ = 0; s_ < nstage; ++s_) mbar_init(&full[s_], 1);
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWC); }
     mbar_init(&dbar, 1);
+    mbar_init(&dfree, 1);
     fence_mbar_init();
   }
-  __syncthreads();
-  if (tid == 0) {
-    issue_stage(blockIdx.x);
-    if (useB)
-      for (int s_ = 0; s_ < nstage; ++s_) issue(s_);
+  if (tid < NCP) {
+    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
+    cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
-  // low-rank coefficients of all my clusters: T[q][c] = sum_j Mp[i_q][j] S_j[c]
-  {
-    constexpr int JPT = 4;                      // j values held per thread per sweep
-    for (int j0 = 0; j0 < n_c; j0 += NT * JPT) {
-      double sv[JPT][NCP];
-#pragma unroll
-      for (int u_ = 0; u_ < JPT; ++u_) {
-        const int j = j0 + u_ * NT + tid;
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) sv[u_][c] = 0.0;
-        if (j < n_c) {
-          const double* sj = a.S_D + a.L.tile0[j] * MAXC;
-          if (a.fuse_p) {
-            const double* spj = SPo + a.L.tile0[j] * MAXC;
-#pragma unroll
-            for (int c = 0; c < NCP; ++c)
-              sv[u_][c] = (cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c];
-          } else {
-#pragma unroll
-            for (int c = 0; c < NCP; ++c) sv[u_][c] = sj[c];
+  __syncthreads();
+
+  if (wid == NWC) {
+    // ============================ producer warp ============================
+    if (lane == 0) {
+      uint32_t pseq = 0;
+      int q = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
+        const int i = a.L.tiles[t].blk;
+        const int ld = a.L.ld[i];
+        const int64_t p0 = a.L.poff[i];
+        // staged D inputs of tile t (after the consumers released the stage buffer)
+        if (q > 0) mbar_wait(&dfree, static_cast<uint32_t>((q - 1) & 1));
+        const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&dbar, cbytes * ncol * nsrc);
+        for (int c = 0; c < ncol; ++c) {
+          tma_load_1d(stg + c * ld, a.D + c * n_pad + p0, cbytes, &dbar);
+          if (nsrc == 2) tma_load_1d(stg + (ncol + c) * ld, Pold + c * n_pad + p0, cbytes, &dbar);
+        }
+        if (useB) {
+          const int KC = apply_kc(ld, slot, apply_kg<RPT>(ld));
+          const double* Bi = B + a.L.boff[i];
+          for (int k0 = 0; k0 < ld; k0 += KC, ++pseq) {
+            const int s_ = static_cast<int>(pseq % nstage);
+            const uint32_t use = pseq / nstage;
+            if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
+            const int kc = min(KC, ld - k0);
+            const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+            fence_proxy_async_smem();
+            mbar_arrive_expect_tx(&full[s_], bytes);
+            tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(k0) * ld, bytes, &full[s_]);
           }
         }
       }
-      for (int q = 0; q < nmine; ++q) {
-        const int i = a.L.tiles[blockIdx.x + q * G].blk;
-        const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
-        double tacc[NCP];
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+    }
+  } else {
+    // ============================ consumer warps ============================
+    // low-rank coefficients of all my clusters: T[q][c] = sum_j Mp[i_q][j] S_j[c]
+    {
+      constexpr int JPT = 1;
+      for (int j0 = 0; j0 < n_c; j0 += NTC * JPT) {
+        double sv[JPT][NCP];
 #pragma unroll
         for (int u_ = 0; u_ < JPT; ++u_) {
-          const int j = j0 + u_ * NT + tid;
-          const double m = (j < n_c) ? Mrow[j] : 0.0;
+          const int j = j0 + u_ * NTC + tid;
 #pragma unroll
-          for (int c = 0; c < NCP; ++c) tacc[c] += m * sv[u_][c];
-        }
-        block_reduce_cols<NCP>(tacc, sred, Esm);
-        if (tid < NCP) Tall[q * NCP + tid] = (j0 == 0 ? 0.0 : Tall[q * NCP + tid]) + Esm[tid];
-        __syncthreads();
-      }
-    }
-  }
-  uint32_t seq = 0;
-  int q = 0;
-  for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
-    const TileDesc td = a.L.tiles[t];
-    const int i = td.blk, ld = a.L.ld[i];
-    const int64_t p0 = a.L.poff[i];
-    // 1. D_i from the staged inputs (fused: D = R + beta o P_old, P_new written back)
-    mbar_wait(&dbar, static_cast<uint32_t>(q & 1));
-    for (int idx = tid; idx < ld * NCP; idx += NT) {
-      const int c = idx / ld, k = idx % ld;
-      double v = 0.0;
-      if (c < ncol) {
-        v = stg[c * ld + k];
-        if (a.fuse_p) {
-          const double po = stg[(ncol + c) * ld + k];
-          v = (cb[NCP + c] != 0.0) ? v + cb[c] * po : po;
-          Pnew[c * n_pad + p0 + k] = v;
-        }
-      }
-      Dsm[k * NCP + c] = v;
-    }
-    if (a.fuse_p && tid < ncol) {
-      const double sr = a.S_D[t * MAXC + tid], sp = SPo[t * MAXC + tid];
-      a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
-    }
-    __syncthreads();                                  // stg consumed, Dsm ready
-    if (tid == 0 && t + G < n_tiles) issue_stage(t + G);
-    // 2. block term, streamed through the TMA ring
-    const int RP = ld >> 1;
-    int KS = NT / RP;
-    if (KS < 1) KS = 1;
-    const int grp = tid / RP, rp = tid % RP;
-    const int r = 2 * rp;
-    double acc0[NCP], acc1[NCP];
+          for (int c = 0; c < NCP; ++c) sv[u_][c] = 0.0;
+          if (j < n_c) {
+            const double* sj = a.S_D + a.L.tile0[j] * MAXC;
+            if (a.fuse_p) {
+              const double* spj = SPo + a.L.tile0[j] * MAXC;
 #pragma unroll
-    for (int c = 0; c < NCP; ++c) { acc0[c] = 0.0; acc1[c] = 0.0; }
-    if (useB) {
-      const int KC = max(1, slot / ld);
-      for (int k0 = 0; k0 < ld; k0 += KC) {
-        const int kc = min(KC, ld - k0);
-        const int s_ = static_cast<int>(seq % nstage);
-        mbar_wait(&full[s_], (seq / nstage) & 1u);
-        const double* cbuf = ring + s_ * slot;
-        if (grp < KS) {
-          for (int kk = grp; kk < kc; kk += KS) {
-            const double2 b2 = *reinterpret_cast<const double2*>(cbuf + kk * ld + r);
-            const double2* dk = reinterpret_cast<const double2*>(Dsm + (k0 + kk) * NCP);
+              for (int c = 0; c < NCP; ++c)
+                sv[u_][c] = (cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c];
+            } else {
 #pragma unroll
-            for (int c2 = 0; c2 < NCP / 2; ++c2) {
-              const double2 dv = dk[c2];
-              acc0[2 * c2] = fma(b2.x, dv.x, acc0[2 * c2]);
-              acc0[2 * c2 + 1] = fma(b2.x, dv.y, acc0[2 * c2 + 1]);
-              acc1[2 * c2] = fma(b2.y, dv.x, acc1[2 * c2]);
-              acc1[2 * c2 + 1] = fma(b2.y, dv.y, acc1[2 * c2 + 1]);
+              for (int c = 0; c < NCP; ++c) sv[u_][c] = sj[c];
             }
           }
         }
-        __syncthreads();                      // slot s_ fully consumed
-        if (tid == 0) issue(s_);
-        ++seq;
-      }
-      if (KS > 1) {
-        if (grp > 0 && grp < KS) {
-          double* dst = red + ((grp - 1) * RP + rp) * 2 * NCP;
+        for (int q = 0; q < nmine; ++q) {
+          const int i = a.L.tiles[blockIdx.x + q * G].blk;
+          const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
+          double tacc[NCP];
 #pragma unroll
-          for (int c = 0; c < NCP; ++c) { dst[c] = acc0[c]; dst[NCP + c] = acc1[c]; }
+          for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+#pragma unroll
+          for (int u_ = 0; u_ < JPT; ++u_) {
+            const int j = j0 + u_ * NTC + tid;
+            const double m = (j < n_c) ? Mrow[j] : 0.0;
+#pragma unroll
+            for (int c = 0; c < NCP; ++c) tacc[c] += m * sv[u_][c];
+          }
+          cons_reduce_cols<NCP>(tacc, sred, Esm);
+          if (tid < NCP) Tall[q * NCP + tid] = (j0 == 0 ? 0.0 : Tall[q * NCP + tid]) + Esm[tid];
         }
-        __syncthreads();
-        if (grp == 0) {
-          for (int gg = 1; gg < KS; ++gg) {
-            const double* src = red + ((gg - 1) * RP + rp) * 2 * NCP;
+      }
+    }
+    uint32_t seq = 0;
+    int q = 0;
+    for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
+      const TileDesc td = a.L.tiles[t];
+      const int i = td.blk, ld = a.L.ld[i];
+      const int64_t p0 = a.L.poff[i];
+      // 1. D_i from the staged inputs (fused: D = R + beta o P_old, P_new written back)
+      mbar_wait(&dbar, static_cast<uint32_t>(q & 1));
+      for (int idx = tid; idx < ld * NCP; idx += NTC) {
+        const int c = idx / ld, k = idx % ld;
+        double v = 0.0;
+        if (c < ncol) {
+          v = stg[c * ld + k];
+          if (a.fuse_p) {
+            const double po = stg[(ncol + c) * ld + k];
+            v = (cb[NCP + c] != 0.0) ? v + cb[c] * po : po;
+            Pnew[c * n_pad + p0 + k] = v;
+          }
+        }
+        Dsm[k * NCP + c] = v;
+      }
+      if (a.fuse_p && tid < ncol) {
+        const double sr = a.S_D[t * MAXC + tid], sp = SPo[t * MAXC + tid];
+        a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
+      }
+      cons_sync();                                           // stg consumed, Dsm ready
+      if (tid == 0) mbar_arrive(&dfree);
+      // 2. block term from the TMA ring
+      const int KG = apply_kg<RPT>(ld);
+      const int RQ = ld / RPT;
+      const int rq = tid / KG, g = tid % KG;
+      const bool act = rq < RQ;
+      const int r = RPT * rq;
+      double acc[RPT][NCP];
 #pragma unroll
-            for (int c = 0; c < NCP; ++c) { acc0[c] += src[c]; acc1[c] += src[NCP + c]; }
+      for (int h = 0; h < RPT; ++h)
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) acc[h][c] = 0.0;
+      if (useB) {
+        const int KC = apply_kc(ld, slot, KG);
+        for (int k0 = 0; k0 < ld; k0 += KC, ++seq) {
+          const int kc = min(KC, ld - k0);
+          const int s_ = static_cast<int>(seq % nstage);
+          mbar_wait(&full[s_], (seq / nstage) & 1u);
+          const double* cbuf = ring + s_ * slot;
+          if (act) {
+            for (int kk = g; kk < kc; kk += KG) {
+              double bv[RPT];
+#pragma unroll
+              for (int h2 = 0; h2 < RPT / 2; ++h2) {
+                const double2 b2 = *reinterpret_cast<const double2*>(cbuf + kk * ld + r + 2 * h2);
+                bv[2 * h2] = b2.x;
+                bv[2 * h2 + 1] = b2.y;
+              }
+              const double2* dk = reinterpret_cast<const double2*>(Dsm + (k0 + kk) * NCP);
+#pragma unroll
+              for (int c2 = 0; c2 < NCP / 2; ++c2) {
+                const double2 dv = dk[c2];
+#pragma unroll
+                for (int h = 0; h < RPT; ++h) {
+                  acc[h][2 * c2] = fma(bv[h], dv.x, acc[h][2 * c2]);
+                  acc[h][2 * c2 + 1] = fma(bv[h], dv.y, acc[h][2 * c2 + 1]);
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[s_]);
+        }
+        // combine the KG k-group partials (adjacent lanes) with xor shuffles
+        for (int o = 1; o < KG; o <<= 1) {
+#pragma unroll
+          for (int h = 0; h < RPT; ++h)
+#pragma unroll
+            for (int c = 0; c < NCP; ++c) acc[h][c] += __shfl_xor_sync(0xffffffffu, acc[h][c], o);
+        }
+      }
+      // 3. epilogue (k-group 0 lanes own the row quads)
+      double ep[NCP];
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
+      if (act && g == 0) {
+        const double bi = P->b0 + P->b1 * a.jitter[i];
+        const double pa = P->a, ms = P->mscale;
+        const double* Tq = Tall + q * NCP;
+#pragma unroll
+        for (int h = 0; h < RPT; ++h) {
+          const int rr = r + h;
+          const int64_t gl = p0 + rr;
+          const double uu = a.u[gl];
+#pragma unroll
+          for (int c = 0; c < NCP; ++c) {
+            if (c < ncol) {
+              const double d = Dsm[rr * NCP + c];
+              double val = pa * d;
+              if (useB) val += bi * acc[h][c];
+              val += uu * (ms * Tq[c]);
+              double o = a.cA[c] * val + a.cV[c] * d;
+              if (P2) o += a.cP[c] * P2[c * n_pad + gl];
+              a.out[c * n_pad + gl] = o;
+              ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
+            }
           }
         }
       }
-    }
-    // 3. epilogue (group 0 owns the row pairs)
-    double ep[NCP];
-#pragma unroll
-    for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
-    if (grp == 0) {
-      const double bi = P->b0 + P->b1 * a.jitter[i];
-      const double pa = P->a, ms = P->mscale;
-      const double* Tq = Tall + q * NCP;
-      const double2 u2 = *reinterpret_cast<const double2*>(a.u + p0 + r);
-      double p2v[2][NCP], y2v[2][NCP];
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) {
-        const bool on = c < ncol;
-        const int64_t g = c * n_pad + p0 + r;
-        double2 pp = make_double2(0.0, 0.0), yy = make_double2(0.0, 0.0);
-        if (on && P2) pp = *reinterpret_cast<const double2*>(P2 + g);
-        if (on && a.epi != EPI_S) yy = *reinterpret_cast<const double2*>(Y2 + g);
-        p2v[0][c] = pp.x; p2v[1][c] = pp.y; y2v[0][c] = yy.x; y2v[1][c] = yy.y;
+      cons_reduce_cols<NCP>(ep, sred, Esm);
+      if (tid < ncol) {
+        if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = Esm[tid];
+        else a.dots[t * MAXC + tid] = Esm[tid];
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int rr = r + h;
-        const double uu = (h == 0) ? u2.x : u2.y;
-        double o[NCP];
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) {
-          const double d = Dsm[rr * NCP + c];
-          const double bd = (h == 0) ? acc0[c] : acc1[c];
-          double val = pa * d;
-          if (useB) val += bi * bd;
-          val += uu * (ms * Tq[c]);
-          o[c] = a.cA[c] * val + a.cV[c] * d;
-          if (P2) o[c] += a.cP[c] * p2v[h][c];
-          ep[c] += (a.epi == EPI_S) ? uu * o[c] : o[c] * y2v[h][c];
-        }
-#pragma unroll
-        for (int c = 0; c < NCP; ++c)
-          if (c < ncol) a.out[c * n_pad + p0 + rr] = o[c];
-      }
-    }
-    block_reduce_cols<NCP>(ep, sred, Esm);
-    if (tid < ncol) {
-      if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = Esm[tid];
-      else a.dots[t * MAXC + tid] = Esm[tid];
     }
   }
   // 4. finaliser (last CTA; one warp per column)
   if (a.fin != FIN_NONE) {
     if (last_cta(&a.st->ticket[a.fin])) {
       CGState* st = a.st;
-      const int lane = tid & 31, wid = tid >> 5;
-      for (int c = wid; c < ncol; c += NT / 32) {
+      for (int c = wid; c < ncol; c += NTA / 32) {
         const double tot = col_total(a.dots, n_tiles, c);
         if (lane == 0) {
           if (a.fin == FIN_ALPHA) {
@@ -631,19 +668,18 @@ static int num_sms() {
 }
 
 // Shared-memory plan of the apply kernel (host side): ring depth chosen to fit.
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int n_tiles, int grid) {
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid) {
   ApplyPlan p;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t budget = static_cast<size_t>(optin) - 2048;
-  const int rp = ld_max / 2;
-  const int ks = std::max(1, NT / std::max(1, rp));
-  p.red_doubles = std::max((ks - 1) * rp * 2 * ncp, (NT / 32) * ncp);
+  (void)ld_min;
+  p.red_doubles = 0;
   p.nmine_max = (n_tiles + grid - 1) / grid;
   p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
   const size_t fixed = static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
-                       p.red_doubles + static_cast<size_t>(p.nmine_max) * ncp + 3 * ncp;
+                       static_cast<size_t>(NWC) * ncp + static_cast<size_t>(p.nmine_max) * ncp + 3 * ncp;
   long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
   p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
   if (p.nstage < 2) {
@@ -662,7 +698,7 @@ template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
   size_t smem = useB ? a.smem_b : a.smem_nob;
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NT, smem, s>>>(a);
+  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NTA, smem, s>>>(a);
   note_launch(); post_launch("apply_kernel");
 }
 

@@ -39,7 +39,7 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
                     cudaStream_t s);
 
 // eval_kernels.cu
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int n_tiles, int grid);
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid);
 int apply_grid(int n_tiles);
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s);
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
