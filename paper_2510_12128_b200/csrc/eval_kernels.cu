@@ -173,7 +173,7 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
 // row quad, KG a power of two): each thread accumulates 4 rows x NCP columns over the chunk
 // columns kk = g (mod KG); the KG partial sums are combined with xor shuffles.
 // Epilogue: per-cluster partials of u^T out (next apply's S) or of out . Y2 (CG / trace dots).
-constexpr int NTA = 512;              // threads per apply CTA
+constexpr int NTA = 256;              // threads per apply CTA (2 CTAs per SM)
 constexpr int NWC = NTA / 32 - 1;     // consumer warps
 constexpr int NTC = NWC * 32;         // consumer threads
 
@@ -204,7 +204,7 @@ template <int RPT>
 __device__ __forceinline__ int apply_kg(int ld) {
   const int rq = ld / RPT;
   int kg = 1;
-  while (kg < 32 && rq * kg * 2 <= NTC) kg <<= 1;
+  while (kg < 8 && rq * kg * 2 <= NTC) kg <<= 1;
   return kg;
 }
 __device__ __forceinline__ int apply_kc(int ld, int slot, int kg) {
@@ -214,7 +214,7 @@ __device__ __forceinline__ int apply_kc(int ld, int slot, int kg) {
 }
 
 template <int NCP>
-__global__ void __launch_bounds__(NTA, 1) apply_kernel(ApplyArgs a) {
+__global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
   constexpr int RPT = (NCP <= 10) ? 4 : 2;   // rows per consumer thread (register budget)
   if (a.gate && !a.st->any_active) return;
   extern __shared__ __align__(128) double sm[];
@@ -413,30 +413,38 @@ __global__ void __launch_bounds__(NTA, 1) apply_kernel(ApplyArgs a) {
             for (int c = 0; c < NCP; ++c) acc[h][c] += __shfl_xor_sync(0xffffffffu, acc[h][c], o);
         }
       }
-      // 3. epilogue (k-group 0 lanes own the row quads)
+      // 3. epilogue: after the xor all-reduce every k-group lane holds the row-quad sums;
+      //    lane g writes the columns c with c % KG == g
       double ep[NCP];
 #pragma unroll
       for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
-      if (act && g == 0) {
+      if (act) {
         const double bi = P->b0 + P->b1 * a.jitter[i];
         const double pa = P->a, ms = P->mscale;
         const double* Tq = Tall + q * NCP;
+        double uu[RPT];
 #pragma unroll
-        for (int h = 0; h < RPT; ++h) {
-          const int rr = r + h;
-          const int64_t gl = p0 + rr;
-          const double uu = a.u[gl];
+        for (int h = 0; h < RPT; ++h) uu[h] = a.u[p0 + r + h];
 #pragma unroll
-          for (int c = 0; c < NCP; ++c) {
-            if (c < ncol) {
-              const double d = Dsm[rr * NCP + c];
+        for (int c = 0; c < NCP; ++c) {
+          if (c < ncol && (c % KG) == g) {
+            const int64_t gb = c * n_pad + p0 + r;
+            double p2v[RPT], y2v[RPT];
+#pragma unroll
+            for (int h = 0; h < RPT; ++h) {
+              p2v[h] = P2 ? P2[gb + h] : 0.0;
+              y2v[h] = (a.epi == EPI_S) ? uu[h] : Y2[gb + h];
+            }
+#pragma unroll
+            for (int h = 0; h < RPT; ++h) {
+              const double d = Dsm[(r + h) * NCP + c];
               double val = pa * d;
               if (useB) val += bi * acc[h][c];
-              val += uu * (ms * Tq[c]);
+              val += uu[h] * (ms * Tq[c]);
               double o = a.cA[c] * val + a.cV[c] * d;
-              if (P2) o += a.cP[c] * P2[c * n_pad + gl];
-              a.out[c * n_pad + gl] = o;
-              ep[c] += (a.epi == EPI_S) ? uu * o : o * Y2[c * n_pad + gl];
+              if (P2) o += a.cP[c] * p2v[h];
+              a.out[gb + h] = o;
+              ep[c] += o * y2v[h];
             }
           }
         }
@@ -670,10 +678,12 @@ static int num_sms() {
 // Shared-memory plan of the apply kernel (host side): ring depth chosen to fit.
 ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid) {
   ApplyPlan p;
-  int dev = 0, optin = 0;
+  int dev = 0, optin = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t budget = static_cast<size_t>(optin) - 2048;
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  // two CTAs per SM: each gets half of the SM's shared memory (minus the per-CTA reserve)
+  const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / 2) - 2048;
   (void)ld_min;
   p.red_doubles = 0;
   p.nmine_max = (n_tiles + grid - 1) / grid;
@@ -692,7 +702,7 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
   return p;
 }
 
-int apply_grid(int n_tiles) { return std::min(n_tiles, num_sms()); }
+int apply_grid(int n_tiles) { return std::min(n_tiles, 2 * num_sms()); }
 
 template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
