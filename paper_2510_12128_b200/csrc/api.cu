@@ -143,6 +143,7 @@ struct EvalDev {
   nugpr_mll_out* out = nullptr;
   double* ah = nullptr, *bh = nullptr, *slqw = nullptr;
   double* ystage = nullptr;   // n
+  double* Tbuf = nullptr;     // n_c x MAXC
 };
 
 struct BlocksDev {
@@ -219,6 +220,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.bh = c.take<double>(static_cast<size_t>(MAXC) * HIST);
     e.slqw = c.take<double>(static_cast<size_t>(MAXC) * 3 * HIST);
     e.ystage = c.take<double>(L.n);
+    e.Tbuf = c.take<double>(static_cast<size_t>(n_c) * MAXC);
   }
 }
 
@@ -688,6 +690,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
     a1.red_doubles = pl.red_doubles;
     a1.nstage = pl.nstage;
     a1.nmine_max = pl.nmine_max;
+    a1.Tbuf = e.Tbuf;
     a1.smem_b = pl.smem_b;
     a1.smem_nob = pl.smem_nob;
   }

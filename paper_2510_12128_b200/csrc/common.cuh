@@ -110,6 +110,7 @@ struct ApplyArgs {
   int slot_doubles;        // TMA ring slot size (>= ld_max)
   int red_doubles;         // cross-k-group reduction scratch
   int nstage;              // TMA ring depth
+  double* Tbuf;            // [n_c][MAXC] low-rank coefficients M' S (phase 1 of the apply)
   int nmine_max;           // max clusters per persistent CTA
   size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
 };

@@ -9,6 +9,8 @@
 // the last CTA to finish, in fixed tile order: results are bit-reproducible.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels_decl.h"
 #include "tma.cuh"
@@ -239,8 +241,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
   double* stg = ring + (useB ? nstage * slot : 0);           // 2 * ncol * ld_max (staged D inputs)
   double* Dsm = stg + 2 * ncol * a.ld_max;                   // ld_max * NCP (row-major Dsm[k*NCP+c])
   double* sred = Dsm + a.ld_max * NCP;                       // NWC * NCP
-  double* Tall = sred + NWC * NCP;                           // nmine_max * NCP
-  double* Esm = Tall + a.nmine_max * NCP;                    // NCP
+  double* Esm = sred + NWC * NCP;                            // NCP
   double* cb = Esm + NCP;                                    // NCP beta ; NCP active
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
@@ -258,18 +259,21 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
     cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
   __syncthreads();
-
-  if (wid == NWC) {
-    // ============================ producer warp ============================
-    if (lane == 0) {
-      uint32_t pseq = 0;
-      int q = 0;
-      for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
-        const int i = a.L.tiles[t].blk;
-        const int ld = a.L.ld[i];
+  // TMA producer (lane 0 of warp NWC): work items in order: per tile q, the staged D inputs,
+  // then the KC-column chunks of B_i.  prefill=true stops at the first item that would wait.
+  int ct = blockIdx.x, cq = 0, ck0 = 0;
+  bool cstaged = false;
+  uint32_t pseq = 0;
+  auto produce = [&](bool prefill) {
+    while (ct < n_tiles) {
+      const int i = a.L.tiles[ct].blk;
+      const int ld = a.L.ld[i];
+      if (!cstaged) {
+        if (cq > 0) {
+          if (prefill) return;
+          mbar_wait(&dfree, static_cast<uint32_t>((cq - 1) & 1));
+        }
         const int64_t p0 = a.L.poff[i];
-        // staged D inputs of tile t (after the consumers released the stage buffer)
-        if (q > 0) mbar_wait(&dfree, static_cast<uint32_t>((q - 1) & 1));
         const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
         fence_proxy_async_smem();
         mbar_arrive_expect_tx(&dbar, cbytes * ncol * nsrc);
@@ -277,65 +281,73 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
           tma_load_1d(stg + c * ld, a.D + c * n_pad + p0, cbytes, &dbar);
           if (nsrc == 2) tma_load_1d(stg + (ncol + c) * ld, Pold + c * n_pad + p0, cbytes, &dbar);
         }
-        if (useB) {
-          const int KC = apply_kc(ld, slot, apply_kg<RPT>(ld));
-          const double* Bi = B + a.L.boff[i];
-          for (int k0 = 0; k0 < ld; k0 += KC, ++pseq) {
-            const int s_ = static_cast<int>(pseq % nstage);
-            const uint32_t use = pseq / nstage;
-            if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
-            const int kc = min(KC, ld - k0);
-            const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
-            fence_proxy_async_smem();
-            mbar_arrive_expect_tx(&full[s_], bytes);
-            tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(k0) * ld, bytes, &full[s_]);
+        cstaged = true;
+        ck0 = 0;
+      }
+      if (useB) {
+        const int KC = apply_kc(ld, slot, apply_kg<RPT>(ld));
+        const double* Bi = B + a.L.boff[i];
+        while (ck0 < ld) {
+          const int s_ = static_cast<int>(pseq % nstage);
+          const uint32_t use = pseq / nstage;
+          if (use > 0) {
+            if (prefill) return;
+            mbar_wait(&empty[s_], (use - 1) & 1u);
           }
+          const int kc = min(KC, ld - ck0);
+          const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[s_], bytes);
+          tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
+          ck0 += KC;
+          ++pseq;
         }
       }
+      ct += G;
+      ++cq;
+      cstaged = false;
     }
+  };
+  if (wid == NWC && lane == 0) produce(true);
+  // ---- phase 1 (cooperative): T = M' S for this CTA's slice of clusters (B stream in flight) ----
+  {
+    const int R = (n_c + G - 1) / G;
+    const int i0 = blockIdx.x * R, i1 = min(n_c, i0 + R);
+    for (int i = i0 + wid; i < i1; i += NTA / 32) {
+      const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
+      double tacc[NCP];
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
+      for (int j = lane; j < n_c; j += 32) {
+        const double m = Mrow[j];
+        const double* sj = a.S_D + a.L.tile0[j] * MAXC;
+        if (a.fuse_p) {
+          const double* spj = SPo + a.L.tile0[j] * MAXC;
+#pragma unroll
+          for (int c = 0; c < NCP; ++c)
+            tacc[c] += m * ((cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c]);
+        } else {
+#pragma unroll
+          for (int c = 0; c < NCP; ++c) tacc[c] += m * sj[c];
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) tacc[c] = warp_sum(tacc[c]);
+      if (lane < NCP) {
+        double v = 0.0;
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) if (c == lane) v = tacc[c];
+        a.Tbuf[i * MAXC + lane] = v;
+      }
+    }
+  }
+  cooperative_groups::this_grid().sync();
+
+  if (wid == NWC) {
+    // ============================ producer warp ============================
+    if (lane == 0) produce(false);
   } else {
     // ============================ consumer warps ============================
-    // low-rank coefficients of all my clusters: T[q][c] = sum_j Mp[i_q][j] S_j[c]
-    {
-      constexpr int JPT = 1;
-      for (int j0 = 0; j0 < n_c; j0 += NTC * JPT) {
-        double sv[JPT][NCP];
-#pragma unroll
-        for (int u_ = 0; u_ < JPT; ++u_) {
-          const int j = j0 + u_ * NTC + tid;
-#pragma unroll
-          for (int c = 0; c < NCP; ++c) sv[u_][c] = 0.0;
-          if (j < n_c) {
-            const double* sj = a.S_D + a.L.tile0[j] * MAXC;
-            if (a.fuse_p) {
-              const double* spj = SPo + a.L.tile0[j] * MAXC;
-#pragma unroll
-              for (int c = 0; c < NCP; ++c)
-                sv[u_][c] = (cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c];
-            } else {
-#pragma unroll
-              for (int c = 0; c < NCP; ++c) sv[u_][c] = sj[c];
-            }
-          }
-        }
-        for (int q = 0; q < nmine; ++q) {
-          const int i = a.L.tiles[blockIdx.x + q * G].blk;
-          const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
-          double tacc[NCP];
-#pragma unroll
-          for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
-#pragma unroll
-          for (int u_ = 0; u_ < JPT; ++u_) {
-            const int j = j0 + u_ * NTC + tid;
-            const double m = (j < n_c) ? Mrow[j] : 0.0;
-#pragma unroll
-            for (int c = 0; c < NCP; ++c) tacc[c] += m * sv[u_][c];
-          }
-          cons_reduce_cols<NCP>(tacc, sred, Esm);
-          if (tid < NCP) Tall[q * NCP + tid] = (j0 == 0 ? 0.0 : Tall[q * NCP + tid]) + Esm[tid];
-        }
-      }
-    }
     uint32_t seq = 0;
     int q = 0;
     for (int t = blockIdx.x; t < n_tiles; t += G, ++q) {
@@ -421,7 +433,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
       if (act) {
         const double bi = P->b0 + P->b1 * a.jitter[i];
         const double pa = P->a, ms = P->mscale;
-        const double* Tq = Tall + q * NCP;
+        const double* Tq = a.Tbuf + static_cast<int64_t>(i) * MAXC;
         double uu[RPT];
 #pragma unroll
         for (int h = 0; h < RPT; ++h) uu[h] = a.u[p0 + r + h];
@@ -689,7 +701,7 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
   p.nmine_max = (n_tiles + grid - 1) / grid;
   p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
   const size_t fixed = static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
-                       static_cast<size_t>(NWC) * ncp + static_cast<size_t>(p.nmine_max) * ncp + 3 * ncp;
+                       static_cast<size_t>(NWC) * ncp + 3 * ncp;
   long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
   p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
   if (p.nstage < 2) {
@@ -708,7 +720,17 @@ template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
   size_t smem = useB ? a.smem_b : a.smem_nob;
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NTA, smem, s>>>(a);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(apply_grid(a.L.n_tiles), 1, 1);
+  cfg.blockDim = dim3(NTA, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, apply_kernel<NCP>, a);
   note_launch(); post_launch("apply_kernel");
 }
 
