@@ -311,18 +311,20 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
   if (wid == NWC && lane == 0) produce(true);
   // ---- phase 1 (cooperative): T = M' S for this CTA's slice of clusters (B stream in flight) ----
   {
+    // rows [i0, i1) of T, each reduced by the whole CTA (tiles are whole clusters: S row j = tile j)
     const int R = (n_c + G - 1) / G;
     const int i0 = blockIdx.x * R, i1 = min(n_c, i0 + R);
-    for (int i = i0 + wid; i < i1; i += NTA / 32) {
+    for (int i = i0; i < i1; ++i) {
       const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
       double tacc[NCP];
 #pragma unroll
       for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
-      for (int j = lane; j < n_c; j += 32) {
+#pragma unroll 2
+      for (int j = tid; j < n_c; j += NTA) {
         const double m = Mrow[j];
-        const double* sj = a.S_D + a.L.tile0[j] * MAXC;
+        const double* sj = a.S_D + j * MAXC;
         if (a.fuse_p) {
-          const double* spj = SPo + a.L.tile0[j] * MAXC;
+          const double* spj = SPo + j * MAXC;
 #pragma unroll
           for (int c = 0; c < NCP; ++c)
             tacc[c] += m * ((cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c]);
@@ -331,14 +333,8 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
           for (int c = 0; c < NCP; ++c) tacc[c] += m * sj[c];
         }
       }
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) tacc[c] = warp_sum(tacc[c]);
-      if (lane < NCP) {
-        double v = 0.0;
-#pragma unroll
-        for (int c = 0; c < NCP; ++c) if (c == lane) v = tacc[c];
-        a.Tbuf[i * MAXC + lane] = v;
-      }
+      block_reduce_cols<NCP>(tacc, sred, Esm);
+      if (tid < NCP) a.Tbuf[i * MAXC + tid] = Esm[tid];
     }
   }
   cooperative_groups::this_grid().sync();
