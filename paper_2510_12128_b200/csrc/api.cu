@@ -715,11 +715,18 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
 
   const int limit = cfg->replay_iters ? [&] { int mx = 0; for (int c = 0; c < ncol; ++c) mx = std::max(mx, P.replay_iters[c]); return mx; }()
                                       : max_iter;
+  LowrankArgs t1;
+  t1.st = e.st; t1.Mp = P.Mp; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
+  t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
+  LowrankArgs t2 = t1;
+  t2.S = e.SV; t2.fuse_p = 0;
   const int CH = 4;
   int done = 0;
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
+      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t1, ncp, s));
       PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a1, ncp, P.B != nullptr, s));
+      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t2, ncp, s));
       PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a2, ncp, P.B != nullptr, s));
       PROF(ctx, PC_UPDATE, 0.0, s, launch_update(ua, ncp, s));
     }
@@ -733,6 +740,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   ApplyArgs a3 = a1;
   a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
   a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
+  LowrankArgs t3 = t2;
+  t3.S = e.SX; t3.gate = 0;
+  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t3, ncp, s));
   PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a3, ncp, P.B != nullptr, s));
   ApplyArgs a4 = a3;
   a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
@@ -741,6 +751,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
     if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
     else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
   }
+  LowrankArgs t4 = t2;
+  t4.S = e.SV; t4.gate = 0;
+  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t4, ncp, s));
   PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a4, ncp, P.B != nullptr, s));
   launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, lam0_ptr, static_cast<double>(L.n),
                ncol, cfg->logdet_mode, e.out, s);

@@ -121,6 +121,18 @@ struct ApplyPlan {
   bool ok = false;
 };
 
+struct LowrankArgs {
+  const CGState* st;
+  const double* Mp;        // n_c x n_c row-major
+  const double* S;         // [n_tiles][16] S partials (tiles == clusters); fuse_p: S(R)
+  double* SPbuf[2];        // fuse_p: S(P) ping-pong
+  int fuse_p;
+  double* T;               // [n_c][16] out
+  int n_c;
+  int ncol;
+  int gate;
+};
+
 struct UpdateArgs {
   LayoutDev L;
   const EvalParams* prm;

@@ -308,36 +308,6 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
       cstaged = false;
     }
   };
-  if (wid == NWC && lane == 0) produce(true);
-  // ---- phase 1 (cooperative): T = M' S for this CTA's slice of clusters (B stream in flight) ----
-  {
-    // rows [i0, i1) of T, each reduced by the whole CTA (tiles are whole clusters: S row j = tile j)
-    const int R = (n_c + G - 1) / G;
-    const int i0 = blockIdx.x * R, i1 = min(n_c, i0 + R);
-    for (int i = i0; i < i1; ++i) {
-      const double* Mrow = P->Mp + static_cast<int64_t>(i) * n_c;
-      double tacc[NCP];
-#pragma unroll
-      for (int c = 0; c < NCP; ++c) tacc[c] = 0.0;
-#pragma unroll 2
-      for (int j = tid; j < n_c; j += NTA) {
-        const double m = Mrow[j];
-        const double* sj = a.S_D + j * MAXC;
-        if (a.fuse_p) {
-          const double* spj = SPo + j * MAXC;
-#pragma unroll
-          for (int c = 0; c < NCP; ++c)
-            tacc[c] += m * ((cb[NCP + c] != 0.0) ? sj[c] + cb[c] * spj[c] : spj[c]);
-        } else {
-#pragma unroll
-          for (int c = 0; c < NCP; ++c) tacc[c] += m * sj[c];
-        }
-      }
-      block_reduce_cols<NCP>(tacc, sred, Esm);
-      if (tid < NCP) a.Tbuf[i * MAXC + tid] = Esm[tid];
-    }
-  }
-  cooperative_groups::this_grid().sync();
 
   if (wid == NWC) {
     // ============================ producer warp ============================
@@ -364,10 +334,6 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
           }
         }
         Dsm[k * NCP + c] = v;
-      }
-      if (a.fuse_p && tid < ncol) {
-        const double sr = a.S_D[t * MAXC + tid], sp = SPo[t * MAXC + tid];
-        a.SPbuf[par ^ 1][t * MAXC + tid] = (cb[NCP + tid] != 0.0) ? sr + cb[tid] * sp : sp;
       }
       cons_sync();                                           // stg consumed, Dsm ready
       if (tid == 0) mbar_arrive(&dfree);
@@ -485,6 +451,62 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
       __syncthreads();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Low-rank coefficients T = M' S(D) (Eq. 19-21: block i of W M' W^T D is u_i T_i), one warp per
+// row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new) = S(R) +
+// beta o S(P_old) for the active columns (S is linear), and CTA 0 also stores S(P_new).
+constexpr int TROWS = 8;   // rows of T per CTA (one per warp)
+
+template <int NCP>
+__global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
+  if (a.gate && !a.st->any_active) return;
+  extern __shared__ double Ss[];          // n_c * NCP
+  __shared__ double cb[2 * NCP];
+  const int n_c = a.n_c;
+  const int ncol = a.ncol;
+  const int par = a.st->par;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  if (tid < NCP) {
+    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
+    cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
+  }
+  __syncthreads();
+  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
+  for (int idx = tid; idx < n_c * NCP; idx += NT) {
+    const int j = idx / NCP, c = idx % NCP;
+    double v = a.S[j * MAXC + c];
+    if (a.fuse_p) {
+      const double sp = SPo[j * MAXC + c];
+      v = (cb[NCP + c] != 0.0) ? v + cb[c] * sp : sp;
+      if (blockIdx.x == 0 && c < ncol) a.SPbuf[par ^ 1][j * MAXC + c] = v;
+    }
+    Ss[idx] = v;
+  }
+  __syncthreads();
+  const int i = blockIdx.x * TROWS + wid;
+  if (i >= n_c) return;
+  const double* Mrow = a.Mp + static_cast<int64_t>(i) * n_c;
+  double t[NCP];
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) t[c] = 0.0;
+  for (int j = lane; j < n_c; j += 32) {
+    const double m = Mrow[j];
+    const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
+#pragma unroll
+    for (int c2 = 0; c2 < NCP / 2; ++c2) {
+      const double2 v = sj[c2];
+      t[2 * c2] = fma(m, v.x, t[2 * c2]);
+      t[2 * c2 + 1] = fma(m, v.y, t[2 * c2 + 1]);
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < NCP; ++c) t[c] = warp_sum(t[c]);
+  if (lane == 0) {
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) a.T[i * MAXC + c] = t[c];
   }
 }
 
@@ -716,17 +738,7 @@ template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
   size_t smem = useB ? a.smem_b : a.smem_nob;
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(apply_grid(a.L.n_tiles), 1, 1);
-  cfg.blockDim = dim3(NTA, 1, 1);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeCooperative;
-  attr[0].val.cooperative = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  cudaLaunchKernelEx(&cfg, apply_kernel<NCP>, a);
+  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NTA, smem, s>>>(a);
   note_launch(); post_launch("apply_kernel");
 }
 
@@ -740,6 +752,27 @@ void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
     case 12: apply_launch_t<12>(a, useB, s); break;
     case 14: apply_launch_t<14>(a, useB, s); break;
     default: apply_launch_t<16>(a, useB, s); break;
+  }
+}
+
+template <int NCP>
+static void lowrank_launch_t(const LowrankArgs& a, cudaStream_t s) {
+  const size_t smem = sizeof(double) * static_cast<size_t>(a.n_c) * NCP;
+  smem_optin(reinterpret_cast<const void*>(lowrank_kernel<NCP>));
+  lowrank_kernel<NCP><<<(a.n_c + TROWS - 1) / TROWS, NT, smem, s>>>(a);
+  note_launch(); post_launch("lowrank_kernel");
+}
+
+void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s) {
+  switch (ncp) {
+    case 2: lowrank_launch_t<2>(a, s); break;
+    case 4: lowrank_launch_t<4>(a, s); break;
+    case 6: lowrank_launch_t<6>(a, s); break;
+    case 8: lowrank_launch_t<8>(a, s); break;
+    case 10: lowrank_launch_t<10>(a, s); break;
+    case 12: lowrank_launch_t<12>(a, s); break;
+    case 14: lowrank_launch_t<14>(a, s); break;
+    default: lowrank_launch_t<16>(a, s); break;
   }
 }
 

@@ -43,6 +43,7 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
 int apply_grid(int n_tiles);
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s);
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
+void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s);
