@@ -475,15 +475,39 @@ __global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
   }
   __syncthreads();
   const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-  for (int idx = tid; idx < n_c * NCP; idx += NT) {
-    const int j = idx / NCP, c = idx % NCP;
-    double v = a.S[j * MAXC + c];
-    if (a.fuse_p) {
-      const double sp = SPo[j * MAXC + c];
-      v = (cb[NCP + c] != 0.0) ? v + cb[c] * sp : sp;
-      if (blockIdx.x == 0 && c < ncol) a.SPbuf[par ^ 1][j * MAXC + c] = v;
+  // stage S (n_c rows of NCP) with all loads of a thread in flight: thread -> rows j = tid + k*NT
+  for (int j0 = 0; j0 < n_c; j0 += NT * 4) {
+    double v[4][NCP];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * NT + tid;
+#pragma unroll
+      for (int c2 = 0; c2 < NCP / 2; ++c2) {
+        double2 x = make_double2(0.0, 0.0);
+        if (j < n_c) {
+          x = *reinterpret_cast<const double2*>(a.S + j * MAXC + 2 * c2);
+          if (a.fuse_p) {
+            const double2 y = *reinterpret_cast<const double2*>(SPo + j * MAXC + 2 * c2);
+            x.x = (cb[NCP + 2 * c2] != 0.0) ? x.x + cb[2 * c2] * y.x : y.x;
+            x.y = (cb[NCP + 2 * c2 + 1] != 0.0) ? x.y + cb[2 * c2 + 1] * y.y : y.y;
+          }
+        }
+        v[u][2 * c2] = x.x;
+        v[u][2 * c2 + 1] = x.y;
+      }
     }
-    Ss[idx] = v;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int j = j0 + u * NT + tid;
+      if (j < n_c) {
+#pragma unroll
+        for (int c = 0; c < NCP; ++c) Ss[j * NCP + c] = v[u][c];
+        if (a.fuse_p && blockIdx.x == 0)
+#pragma unroll
+          for (int c = 0; c < NCP; ++c)
+            if (c < ncol) a.SPbuf[par ^ 1][j * MAXC + c] = v[u][c];
+      }
+    }
   }
   __syncthreads();
   const int i = blockIdx.x * TROWS + wid;
@@ -492,6 +516,7 @@ __global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
   double t[NCP];
 #pragma unroll
   for (int c = 0; c < NCP; ++c) t[c] = 0.0;
+#pragma unroll 4
   for (int j = lane; j < n_c; j += 32) {
     const double m = Mrow[j];
     const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
@@ -538,16 +563,26 @@ __global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
   for (int rl = threadIdx.x; rl < td.nrows; rl += NT) {
     const int64_t g = p0 + rl;
     const double uu = a.u[g];
+    double xv[NCP], pv[NCP], rv[NCP], qv[NCP];
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) {
+      const bool on = c < ncol && cact[c] != 0.0;
+      const int64_t gi = c * n_pad + g;
+      xv[c] = on ? a.X[gi] : 0.0;
+      pv[c] = on ? Pc[gi] : 0.0;
+      rv[c] = on ? a.R[gi] : 0.0;
+      qv[c] = on ? a.Q[gi] : 0.0;
+    }
 #pragma unroll
     for (int c = 0; c < NCP; ++c) {
       if (c < ncol && cact[c] != 0.0) {
         const int64_t gi = c * n_pad + g;
         const double al = cal[c];
-        a.X[gi] = a.X[gi] + al * Pc[gi];
-        const double rv = a.R[gi] - al * a.Q[gi];
-        a.R[gi] = rv;
-        rr[c] += rv * rv;
-        sr[c] += uu * rv;
+        a.X[gi] = xv[c] + al * pv[c];
+        const double r2 = rv[c] - al * qv[c];
+        a.R[gi] = r2;
+        rr[c] += r2 * r2;
+        sr[c] += uu * r2;
       }
     }
   }
