@@ -10,6 +10,7 @@
 #include "kernels_decl.h"
 #include "tridiag.h"
 
+#include <algorithm>
 #include <atomic>
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -172,19 +173,21 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   const int b = static_cast<int>(a.off[i + 1] - a.off[i]);
   double* A = a.A + a.boff[i];
   extern __shared__ double sm[];
-  double* Pn = sm;                 // panel: (ld) x NB, col-major with leading dim ld
   __shared__ int fail;
   __shared__ double red[8];
   const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
   __syncthreads();
 
-  // ---------------- Cholesky ----------------
+  // ---------------- Cholesky (right-looking, NB-column panels) ----------------
+  // Panel Pn is column-major in smem with leading dimension pr (rows contiguous): every
+  // per-row sweep is unit-stride across lanes (no bank conflicts).
+  double* Pn = sm;
   for (int k0 = 0; k0 < ld; k0 += NB) {
     const int nb = min(NB, ld - k0);
     const int pr = ld - k0;          // panel rows
     for (int idx = tid; idx < pr * nb; idx += NT) {
-      int c = idx / pr, r = idx % pr;
+      const int c = idx / pr, r = idx % pr;
       Pn[c * pr + r] = A[static_cast<int64_t>(k0 + c) * ld + k0 + r];
     }
     __syncthreads();
@@ -195,59 +198,65 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
         Pn[j * pr + j] = sqrt(piv);
       }
       __syncthreads();
-      const double ljj = Pn[j * pr + j];
-      for (int r = j + 1 + tid; r < pr; r += NT) Pn[j * pr + r] /= ljj;
+      const double inv = 1.0 / Pn[j * pr + j];
+      for (int r = j + 1 + tid; r < pr; r += NT) Pn[j * pr + r] *= inv;
       __syncthreads();
-      // rank-1 update of panel columns c in (j, nb), rows r >= c
       const int ncols = nb - j - 1;
-      for (int idx = tid; idx < ncols * pr; idx += NT) {
-        int c = j + 1 + idx / pr, r = idx % pr;
+      const int nrow = pr - j - 1;      // rows j+1.. of the panel
+      for (int idx = tid; idx < ncols * nrow; idx += NT) {
+        const int c = j + 1 + idx / nrow, r = j + 1 + idx % nrow;
         if (r >= c) Pn[c * pr + r] -= Pn[j * pr + r] * Pn[j * pr + c];
       }
       __syncthreads();
     }
     for (int idx = tid; idx < pr * nb; idx += NT) {
-      int c = idx / pr, r = idx % pr;
+      const int c = idx / pr, r = idx % pr;
       A[static_cast<int64_t>(k0 + c) * ld + k0 + r] = (r >= c) ? Pn[c * pr + r] : 0.0;
     }
-    // trailing update: A[k0+nb+r][k0+nb+c] -= sum_j P[nb+r][j] P[nb+c][j], r >= c
+    // trailing update of the lower triangle: A[t+r][t+c] -= sum_j P[nb+r][j] P[nb+c][j], r >= c,
+    // in 64x64 output tiles, 4x4 register tile per thread, coalesced read-modify-write of A.
     const int tr = pr - nb;
     if (tr > 0) {
-      // 4x4 register tiles over the lower triangle of the tr x tr trailing matrix
-      const int nt4 = (tr + 3) / 4;
-      const int ntiles = nt4 * (nt4 + 1) / 2;
-      for (int t = tid; t < ntiles; t += NT) {
-        // map t -> (ti >= tj)
-        int ti = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-        while (ti * (ti + 1) / 2 > t) --ti;
-        while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
-        int tj = t - ti * (ti + 1) / 2;
+      const int t0 = k0 + nb;
+      const int nt = (tr + 63) / 64;
+      const int ntl = nt * (nt + 1) / 2;
+      const int tx = tid & 15, ty = tid >> 4;    // rows tx*4.., cols ty*4..
+      for (int tt = 0; tt < ntl; ++tt) {
+        int bi = static_cast<int>((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
+        while (bi * (bi + 1) / 2 > tt) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= tt) ++bi;
+        const int bj = tt - bi * (bi + 1) / 2;
+        const int rb = bi * 64 + tx * 4, cb = bj * 64 + ty * 4;   // offsets in the trailing block
+        if (rb >= tr || cb >= tr || rb + 3 < cb) continue;
         double acc[4][4];
 #pragma unroll
         for (int x = 0; x < 4; ++x)
 #pragma unroll
           for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
         for (int j = 0; j < nb; ++j) {
-          double pa[4], pb[4];
+          const double* pc = Pn + j * pr + nb;
+          double av[4], bv[4];
 #pragma unroll
           for (int x = 0; x < 4; ++x) {
-            int r = ti * 4 + x, c = tj * 4 + x;
-            pa[x] = (r < tr) ? Pn[j * pr + nb + r] : 0.0;
-            pb[x] = (c < tr) ? Pn[j * pr + nb + c] : 0.0;
+            av[x] = (rb + x < tr) ? pc[rb + x] : 0.0;
+            bv[x] = (cb + x < tr) ? pc[cb + x] : 0.0;
           }
 #pragma unroll
           for (int x = 0; x < 4; ++x)
 #pragma unroll
-            for (int y = 0; y < 4; ++y) acc[x][y] += pa[x] * pb[y];
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
         }
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int y = 0; y < 4; ++y) {
+          const int c = cb + y;
+          if (c >= tr) continue;
+          double* col = A + static_cast<int64_t>(t0 + c) * ld + t0;
 #pragma unroll
-          for (int y = 0; y < 4; ++y) {
-            int r = ti * 4 + x, c = tj * 4 + y;
-            if (r < tr && c < tr && r >= c)
-              A[static_cast<int64_t>(k0 + nb + c) * ld + k0 + nb + r] -= acc[x][y];
+          for (int x = 0; x < 4; ++x) {
+            const int r = rb + x;
+            if (r < tr && r >= c) col[r] -= acc[x][y];
           }
+        }
       }
     }
     __syncthreads();
@@ -259,70 +268,72 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   if ((tid & 31) == 0) red[tid >> 5] = ls;
   __syncthreads();
   if (tid == 0) {
-    double s = 0.0;
-    for (int w = 0; w < NT / 32; ++w) s += red[w];
-    a.logdet_blk[i] = 2.0 * s;
+    double s_ = 0.0;
+    for (int w = 0; w < NT / 32; ++w) s_ += red[w];
+    a.logdet_blk[i] = 2.0 * s_;
     a.status[i] = fail;
   }
   __syncthreads();
   if (fail) return;
 
-  // ---------------- triangular inverse (in place, by tile rows) ----------------
-  // Row panel I = rows [I0, I0+nb).  smem: Lrow = L[I, 0:I0+nb] (nb x (I0+nb), row-major),
-  // Xd = (L_II)^{-1} (nb x nb), Yc = (L[I,0:I0] * Xinv[0:I0, cc0:cc0+YC]) column chunk.
+  // ---------------- triangular inverse (in place, by row panels) ----------------
+  // Row panel I = rows [I0, I0+nb).  smem (all column-major: rows contiguous):
+  //   LrT[k*NB + r] = L[I0+r][k] (k < I0+nb),  XdT[k*NB + r] = (L_II^{-1})[r][k],
+  //   Yc[cl*NB + r] = (L[I,0:I0] * Xinv[0:I0, cc0+cl])[r].
   constexpr int YC = 64;
-  double* Lrow = sm;
+  constexpr int NBP = NB + 1;                 // padded stride: conflict-free column sweeps
+  double* LrT = sm;
   for (int I0 = 0; I0 < ld; I0 += NB) {
     const int nb = min(NB, ld - I0);
     const int ldr = I0 + nb;
-    double* Xd = Lrow + nb * ldr;             // NB x NB (row-major)
-    double* Yc = Xd + NB * NB;                // nb x YC (row-major)
+    double* XdT = LrT + NBP * ldr;            // NB x NB (stride NBP)
+    double* Yc = XdT + NBP * NB;              // NB x YC
     for (int idx = tid; idx < nb * ldr; idx += NT) {
-      int c = idx / nb, r = idx % nb;         // coalesced over r in global
-      Lrow[r * ldr + c] = A[static_cast<int64_t>(c) * ld + I0 + r];
+      const int k = idx / nb, r = idx % nb;   // coalesced over r in global and smem
+      LrT[k * NBP + r] = A[static_cast<int64_t>(k) * ld + I0 + r];
     }
     __syncthreads();
-    // diagonal tile inverse: thread j < nb solves L_II x = e_j (forward substitution)
+    // diagonal tile inverse: thread j < nb solves L_II x = e_j by forward substitution
     if (tid < nb) {
       const int j = tid;
       for (int r = 0; r < nb; ++r) {
         double v = 0.0;
         if (r >= j) {
           v = (r == j) ? 1.0 : 0.0;
-          for (int k = j; k < r; ++k) v -= Lrow[r * ldr + I0 + k] * Xd[k * NB + j];
-          v /= Lrow[r * ldr + I0 + r];
+          for (int k = j; k < r; ++k) v -= LrT[(I0 + k) * NBP + r] * XdT[j * NBP + k];
+          v /= LrT[(I0 + r) * NBP + r];
         }
-        Xd[r * NB + j] = v;
+        XdT[j * NBP + r] = v;                  // column j of the inverse
       }
     }
     __syncthreads();
     for (int cc0 = 0; cc0 < I0; cc0 += YC) {
       const int ncc = min(YC, I0 - cc0);
-      // Yc[r][c] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]  (Xinv rows < I0 are final in A)
+      // Yc[cl][r] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]   (Xinv rows < I0 final in A)
       for (int idx = tid; idx < nb * ncc; idx += NT) {
-        int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
         const double* xc = A + static_cast<int64_t>(c) * ld;
         double acc = 0.0;
-        for (int k = c; k < I0; ++k) acc += Lrow[r * ldr + k] * xc[k];
-        Yc[r * YC + cl] = acc;
+        for (int k = c; k < I0; ++k) acc = fma(LrT[k * NBP + r], xc[k], acc);
+        Yc[cl * NB + r] = acc;
       }
       __syncthreads();
       // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
       for (int idx = tid; idx < nb * ncc; idx += NT) {
-        int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
         double acc = 0.0;
-        for (int k = 0; k <= r; ++k) acc += Xd[r * NB + k] * Yc[k * YC + cl];
+        for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yc[cl * NB + k], acc);
         A[static_cast<int64_t>(c) * ld + I0 + r] = -acc;
       }
       __syncthreads();
     }
     for (int idx = tid; idx < nb * nb; idx += NT) {
-      int r = idx % nb, c = idx / nb;
-      A[static_cast<int64_t>(I0 + c) * ld + I0 + r] = (r >= c) ? Xd[r * NB + c] : 0.0;
+      const int r = idx % nb, c = idx / nb;
+      A[static_cast<int64_t>(I0 + c) * ld + I0 + r] = (r >= c) ? XdT[c * NBP + r] : 0.0;
     }
     // strict upper triangle right of the diagonal tile := 0
     for (int idx = tid; idx < nb * (ld - I0 - nb); idx += NT) {
-      int r = idx % nb, c = I0 + nb + idx / nb;
+      const int r = idx % nb, c = I0 + nb + idx / nb;
       A[static_cast<int64_t>(c) * ld + I0 + r] = 0.0;
     }
     __syncthreads();
@@ -339,7 +350,7 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 
 size_t chol_smem_bytes(int ld_max) {
   size_t panel = static_cast<size_t>(ld_max) * NB;                         // Cholesky panel
-  size_t inv = static_cast<size_t>(NB) * ld_max + NB * NB + static_cast<size_t>(NB) * 64;
+  size_t inv = static_cast<size_t>(NB + 1) * ld_max + (NB + 1) * NB + static_cast<size_t>(NB) * 64 + 64;
   return sizeof(double) * (panel > inv ? panel : inv);
 }
 
@@ -538,9 +549,34 @@ struct LanczosArgs {
   double* M;             // n_c x n_c out (K - lam0 I)
   int32_t* info;         // [2] {iterations, converged}
   int cacheK;
+  int kcache;            // Lanczos vectors cached in shared memory
 };
 
 constexpr int LZ_NT = 512;
+
+// Number of eigenvalues of T (diag a, off b) below x, division-free: signs of the leading
+// principal minors p_i = (a_i - x) p_{i-1} - b_{i-1}^2 p_{i-2}, rescaled by powers of two.
+__device__ __forceinline__ int sturm_count_nodiv(int k, const double* a, const double* b, double x) {
+  // p_0 = 1, p_1 = a_0 - x, p_{i+1} = (a_i - x) p_i - b_{i-1}^2 p_{i-1}; #sign changes = #eig < x.
+  // A zero minor is replaced by a tiny value of the opposite sign of its predecessor.
+  double pm2 = 1.0, pm1 = a[0] - x;
+  if (pm1 == 0.0) pm1 = -1e-300;
+  int cnt = (pm1 < 0.0) ? 1 : 0;
+  for (int i = 1; i < k; ++i) {
+    double p = (a[i] - x) * pm1 - b[i - 1] * b[i - 1] * pm2;
+    if (p == 0.0) p = (pm1 > 0.0) ? -1e-300 : 1e-300;
+    if ((p < 0.0) != (pm1 < 0.0)) ++cnt;
+    const double ap = fabs(p);
+    if (ap > 1e150 || ap < 1e-150) {
+      const int e = ilogb(ap);
+      pm1 = scalbn(pm1, -e);
+      p = scalbn(p, -e);
+    }
+    pm2 = pm1;
+    pm1 = p;
+  }
+  return cnt;
+}
 
 // smallest eigenvalue of the k x k tridiagonal (a, b) by 32-way multisection in one warp
 __device__ double warp_tridiag_min_eig(int k, const double* a, const double* b, double hi_hint) {
@@ -551,18 +587,17 @@ __device__ double warp_tridiag_min_eig(int k, const double* a, const double* b, 
     lo = fmin(lo, a[i] - r);
     hi = fmax(hi, a[i] + r);
   }
-  hi = fmin(hi, hi_hint);
-  for (int it = 0; it < 14; ++it) {
+  if (hi_hint < hi && sturm_count_nodiv(k, a, b, hi_hint) >= 1) hi = hi_hint;
+  for (int it = 0; it < 16; ++it) {
     const double x = lo + (hi - lo) * (lane + 1) / 33.0;
-    const int cnt = sturm_count(k, a, b, x);
+    const int cnt = sturm_count_nodiv(k, a, b, x);
     const unsigned m = __ballot_sync(0xffffffffu, cnt >= 1);
-    // first lane whose point has >= 1 eigenvalue below it
     const int f = m ? (__ffs(m) - 1) : 32;
     const double nlo = lo + (hi - lo) * f / 33.0;
     const double nhi = (f < 32) ? lo + (hi - lo) * (f + 1) / 33.0 : hi;
     lo = nlo;
     hi = nhi;
-    if (!(hi > lo)) break;
+    if (!(hi - lo > 1e-16 * fabs(hi))) break;
   }
   return 0.5 * (lo + hi);
 }
@@ -589,13 +624,19 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
   double* tb = ta + kmax;             // kmax
   double* sv = tb + kmax;             // kmax
   double* sw = sv + kmax;             // 2 kmax
-  double* Kc = sw + 2 * kmax;         // R * n (if cached)
+  double* part = sw + 2 * kmax;       // nw * R       (per-warp partial updates)
+  double* Kc = part + nw * R;         // R * n (if cached)
+  double* Vc = Kc + (a.cacheK ? static_cast<size_t>(R) * n : 0);   // kcache * R (Lanczos vectors, rows of this CTA)
+  const int kcache = a.kcache;
   __shared__ double red[32];
   __shared__ int s_done, s_conv;
   __shared__ double s_theta;
   const double* Kg = a.K;
   auto Krow = [&](int r) -> const double* {   // r local
     return a.cacheK ? Kc + static_cast<int64_t>(r) * n : Kg + static_cast<int64_t>(r0 + r) * n;
+  };
+  auto Vrow = [&](int j) -> const double* {   // rows of this CTA of Lanczos vector j
+    return (j < kcache) ? Vc + static_cast<int64_t>(j) * R : a.V + static_cast<int64_t>(j) * n + r0;
   };
   auto block_sum = [&](double v) -> double {
     v = warp_sum(v);
@@ -606,7 +647,6 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     for (int w = 0; w < nw; ++w) t += red[w];
     return t;
   };
-  // cluster-wide fixed-order sum of one scalar per CTA (slot in nb)
   auto cluster_sum = [&](int slot, double v) -> double {
     if (tid == 0) nb[slot] = v;
     cl.sync();
@@ -614,11 +654,14 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     for (int p = 0; p < CS; ++p) t += *cl.map_shared_rank(nb + slot, p);
     return t;
   };
+  auto store_v = [&](int j, int r, double v) {   // V[j][r0+r]
+    a.V[static_cast<int64_t>(j) * n + r0 + r] = v;
+    if (j < kcache) Vc[static_cast<int64_t>(j) * R + r] = v;
+  };
   if (a.cacheK)
     for (int64_t idx = tid; idx < static_cast<int64_t>(nr) * n; idx += LZ_NT)
       Kc[idx] = Kg[static_cast<int64_t>(r0) * n + idx];
   __syncthreads();
-  // ||K||_inf (max row sum) over the cluster
   double rmax = 0.0;
   for (int r = wid; r < nr; r += nw) {
     const double* kr = Krow(r);
@@ -632,7 +675,6 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
   cl.sync();
   double knorm = 0.0;
   for (int p = 0; p < CS; ++p) knorm = fmax(knorm, *cl.map_shared_rank(nb + 2, p));
-  // v_0 (rows of this CTA), normalised over the cluster
   double ss = 0.0;
   for (int r = tid; r < nr; r += LZ_NT) {
     const int g = r0 + r;
@@ -641,7 +683,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     ss += v * v;
   }
   double nrm = sqrt(cluster_sum(0, block_sum(ss)));
-  for (int r = tid; r < nr; r += LZ_NT) a.V[r0 + r] = wl[r] / nrm;
+  for (int r = tid; r < nr; r += LZ_NT) store_v(0, r, wl[r] / nrm);
   cl.sync();
   int k_final = 0;
   double theta = 0.0, theta_prev = INFINITY;
@@ -649,7 +691,6 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     const double* vk = a.V + static_cast<int64_t>(k) * n;
     for (int c = tid; c < n; c += LZ_NT) vfull[c] = vk[c];
     __syncthreads();
-    // w = K v_k on this CTA's rows (warp per row)
     for (int r = wid; r < nr; r += nw) {
       const double* kr = Krow(r);
       double s = 0.0;
@@ -662,7 +703,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     for (int pass = 0; pass < 2; ++pass) {
       double* hpp = hp + pass * (kmax + 1);
       for (int j = wid; j <= k; j += nw) {
-        const double* vj = a.V + static_cast<int64_t>(j) * n + r0;
+        const double* vj = Vrow(j);
         double s = 0.0;
         for (int r = lane; r < nr; r += 32) s += vj[r] * wl[r];
         s = warp_sum(s);
@@ -676,10 +717,17 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
       }
       __syncthreads();
       alpha += hs[k];
+      // w -= sum_j hs[j] V_j : warp w sums j = w (mod nw) for its rows, then fixed-order combine
+      for (int r = lane; r < nr; r += 32) {
+        double t = 0.0;
+        for (int j = wid; j <= k; j += nw) t = fma(hs[j], Vrow(j)[r], t);
+        part[wid * R + r] = t;
+      }
+      __syncthreads();
       for (int r = tid; r < nr; r += LZ_NT) {
-        double s = wl[r];
-        for (int j = 0; j <= k; ++j) s -= hs[j] * a.V[static_cast<int64_t>(j) * n + r0 + r];
-        wl[r] = s;
+        double t = 0.0;
+        for (int w = 0; w < nw; ++w) t += part[w * R + r];
+        wl[r] -= t;
       }
       __syncthreads();
     }
@@ -690,7 +738,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     __syncthreads();
     const int kk = k + 1;
     const bool last = (kk == kmax) || (kk == n) || !(beta > 1e-300);
-    if (last || (kk % 4 == 0)) {
+    if (last || (kk % 4 == 0 && kk >= 8)) {
       if (wid == 0) {
         for (int t = lane; t < kk; t += 32) { ta[t] = al[t]; tb[t] = be[t]; }
         __syncwarp();
@@ -711,14 +759,14 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
       theta_prev = theta;
     }
     if (s_done) { k_final = kk; break; }
-    for (int r = tid; r < nr; r += LZ_NT) a.V[static_cast<int64_t>(k + 1) * n + r0 + r] = wl[r] / beta;
+    for (int r = tid; r < nr; r += LZ_NT) store_v(k + 1, r, wl[r] / beta);
     cl.sync();
   }
   // Ritz vector (rows of this CTA), normalised over the cluster; M = K - theta I
   double s3 = 0.0;
   for (int r = tid; r < nr; r += LZ_NT) {
     double v = 0.0;
-    for (int j = 0; j < k_final; ++j) v += a.V[static_cast<int64_t>(j) * n + r0 + r] * sv[j];
+    for (int j = 0; j < k_final; ++j) v += Vrow(j)[r] * sv[j];
     wl[r] = v;
     s3 += v * v;
   }
@@ -741,14 +789,19 @@ template <int CS>
 static cudaError_t lanczos_launch_cs(const LanczosArgs& a0, cudaStream_t s) {
   LanczosArgs a = a0;
   const int n = a.n_c, kmax = a.kmax, R = (n + CS - 1) / CS;
-  size_t base = static_cast<size_t>(n) + R + 3 * (kmax + 1) + 4 + 7 * static_cast<size_t>(kmax);
+  size_t base = static_cast<size_t>(n) + R + 3 * (kmax + 1) + 4 + 7 * static_cast<size_t>(kmax) +
+                static_cast<size_t>(LZ_NT / 32) * R;
   size_t withK = base + static_cast<size_t>(R) * n;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   const size_t limit = static_cast<size_t>(optin) - 1024;
   a.cacheK = (withK * sizeof(double) <= limit) ? 1 : 0;
-  const size_t smem = (a.cacheK ? withK : base) * sizeof(double);
+  size_t used = a.cacheK ? withK : base;
+  long room = static_cast<long>(limit / sizeof(double)) - static_cast<long>(used);
+  a.kcache = static_cast<int>(std::max<long>(0, std::min<long>(kmax + 1, room / std::max(1, R))));
+  used += static_cast<size_t>(a.kcache) * R;
+  const size_t smem = used * sizeof(double);
   if (smem > limit) return cudaErrorInvalidValue;
   auto kern = lanczos_cluster_kernel<CS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(limit));
@@ -773,7 +826,7 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
                     cudaStream_t s) {
   LanczosArgs a;
   a.K = K; a.n_c = n_c; a.vinit = vinit; a.V = scratch; a.kmax = kmax; a.tol_rel = tol_rel;
-  a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info; a.cacheK = 0;
+  a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info; a.cacheK = 0; a.kcache = 0;
   cudaError_t e;
   if (n_c >= 128) {
     e = lanczos_launch_cs<16>(a, s);
