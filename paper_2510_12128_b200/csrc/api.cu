@@ -693,6 +693,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
     a1.Tbuf = e.Tbuf;
     a1.smem_b = pl.smem_b;
     a1.smem_nob = pl.smem_nob;
+    a1.grid = pl.grid;
   }
   ApplyArgs a2 = a1;
   // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)

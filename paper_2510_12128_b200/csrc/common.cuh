@@ -113,10 +113,11 @@ struct ApplyArgs {
   double* Tbuf;            // [n_c][MAXC] low-rank coefficients M' S (phase 1 of the apply)
   int nmine_max;           // max clusters per persistent CTA
   size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
+  int grid;                // persistent grid size
 };
 
 struct ApplyPlan {
-  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0;
+  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0;
   size_t smem_b = 0, smem_nob = 0;
   bool ok = false;
 };

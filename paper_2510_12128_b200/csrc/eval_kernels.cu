@@ -741,30 +741,36 @@ static int num_sms() {
 }
 
 // Shared-memory plan of the apply kernel (host side): ring depth chosen to fit.
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid) {
-  ApplyPlan p;
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid_unused) {
+  (void)ld_min;
+  (void)grid_unused;
   int dev = 0, optin = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  // two CTAs per SM: each gets half of the SM's shared memory (minus the per-CTA reserve)
-  const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / 2) - 2048;
-  (void)ld_min;
-  p.red_doubles = 0;
-  p.nmine_max = (n_tiles + grid - 1) / grid;
-  p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
   const size_t fixed = static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
                        static_cast<size_t>(NWC) * ncp + 3 * ncp;
-  long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
-  p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
-  if (p.nstage < 2) {
-    p.slot_doubles = ld_max;
+  // prefer two CTAs per SM (one streams while the other runs its epilogue); fall back to one
+  for (int per = 2; per >= 1; --per) {
+    ApplyPlan p;
+    const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - 2048;
+    p.red_doubles = 0;
+    p.ctas_per_sm = per;
+    p.grid = std::min(n_tiles, per * num_sms());
+    p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
+    p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
+    long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
     p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+    if (p.nstage < 2) {
+      p.slot_doubles = ld_max;
+      p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+    }
+    p.smem_nob = fixed * sizeof(double);
+    p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
+    p.ok = p.nstage >= 2;
+    if (p.ok) return p;
   }
-  p.smem_nob = fixed * sizeof(double);
-  p.smem_b = (fixed + static_cast<size_t>(p.nstage) * p.slot_doubles) * sizeof(double);
-  p.ok = p.nstage >= 2;
-  return p;
+  return ApplyPlan();
 }
 
 int apply_grid(int n_tiles) { return std::min(n_tiles, 2 * num_sms()); }
@@ -773,7 +779,7 @@ template <int NCP>
 static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
   size_t smem = useB ? a.smem_b : a.smem_nob;
   smem_optin(reinterpret_cast<const void*>(apply_kernel<NCP>));
-  apply_kernel<NCP><<<apply_grid(a.L.n_tiles), NTA, smem, s>>>(a);
+  apply_kernel<NCP><<<a.grid, NTA, smem, s>>>(a);
   note_launch(); post_launch("apply_kernel");
 }
 
