@@ -157,6 +157,7 @@ struct BlocksDev {
   double* Krep = nullptr, *M = nullptr, *v0 = nullptr, *lz = nullptr;
   int32_t* linfo = nullptr;
   double* Zexport = nullptr;  // m x n (debug probe export)
+  double* cy = nullptr;       // n_pad: c = R^{-T} y cached across the evaluations of one numgrad
 };
 
 void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
@@ -186,6 +187,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.lz = c.take<double>(lzs);
   B.linfo = c.take<int32_t>(4);
   B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
+  B.cy = c.take<double>(L.n_pad);
   E.assign(slots, EvalDev());
   const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
   for (int s = 0; s < slots; ++s) {
@@ -310,6 +312,7 @@ struct nugpr_blocks {
   int last_m = 0;
   uint64_t last_seed = 0;
   const double* last_probes = nullptr;
+  int cy_mode = 0;            // 0: compute c per evaluation; 1: compute and store; 2: reuse B.cy
 };
 
 extern "C" {
@@ -667,6 +670,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
   ra.L = Ld; ra.prm = e.prm; ra.st = e.st; ra.Linv = B.Linv; ra.y = y_dev;
   ra.probes = cfg->probes; ra.seed = cfg->probe_seed; ra.u = B.u; ra.RHS = e.RHS; ra.R = e.R;
   ra.X = e.X; ra.P0 = e.Pb[0]; ra.SP0 = e.SPb[0]; ra.SR_part = e.SR; ra.rr_part = e.rrp; ra.ncol = ncol;
+  ra.cy = (bl->cy_mode == 2) ? B.cy : nullptr;
+  ra.cy_out = (bl->cy_mode == 1) ? B.cy : nullptr;
+  if (bl->cy_mode == 1) bl->cy_mode = 2;
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
   // algorithmic bytes of one apply: w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
@@ -845,6 +851,9 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   RET(stage_y(bl, y_sorted, bl->E[0], ctx->stream, &y_dev));
   auto mk = [](const double* p) { nugpr_theta t{p[0], p[1], p[2]}; return t; };
   int ne = 0;
+  // every evaluation of this call shares y and R: c = R^{-T} y is computed once and reused
+  struct CyGuard { nugpr_blocks* b; ~CyGuard() { b->cy_mode = 0; } } cyg{bl};
+  bl->cy_mode = 1;
   if (gcfg->mode == NUGPR_GRAD_CENTRAL) {
     double pts[NUGPR_NUM_EVALS][3];
     double h[3];

@@ -578,28 +578,71 @@ __device__ __forceinline__ int sturm_count_nodiv(int k, const double* a, const d
   return cnt;
 }
 
-// smallest eigenvalue of the k x k tridiagonal (a, b) by 32-way multisection in one warp
-__device__ double warp_tridiag_min_eig(int k, const double* a, const double* b, double hi_hint) {
-  const int lane = threadIdx.x & 31;
-  double lo = a[0], hi = a[0];
-  for (int i = 0; i < k; ++i) {
-    double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
-    lo = fmin(lo, a[i] - r);
-    hi = fmax(hi, a[i] + r);
+// smallest eigenvalue of the k x k tridiagonal (a, b) by LZ_NT-way multisection over the whole
+// CTA (9+ bits per round); every thread returns the same value.
+__device__ double block_tridiag_min_eig(int k, const double* a, const double* b, double hi_hint,
+                                        int* cnt_sm, double* lohi) {
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    double lo = a[0], hi = a[0];
+    for (int i = 0; i < k; ++i) {
+      double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < k - 1 ? fabs(b[i]) : 0.0);
+      lo = fmin(lo, a[i] - r);
+      hi = fmax(hi, a[i] + r);
+    }
+    if (hi_hint < hi && sturm_count_nodiv(k, a, b, hi_hint) >= 1) hi = hi_hint;
+    lohi[0] = lo;
+    lohi[1] = hi;
   }
-  if (hi_hint < hi && sturm_count_nodiv(k, a, b, hi_hint) >= 1) hi = hi_hint;
-  for (int it = 0; it < 16; ++it) {
-    const double x = lo + (hi - lo) * (lane + 1) / 33.0;
-    const int cnt = sturm_count_nodiv(k, a, b, x);
-    const unsigned m = __ballot_sync(0xffffffffu, cnt >= 1);
-    const int f = m ? (__ffs(m) - 1) : 32;
-    const double nlo = lo + (hi - lo) * f / 33.0;
-    const double nhi = (f < 32) ? lo + (hi - lo) * (f + 1) / 33.0 : hi;
-    lo = nlo;
-    hi = nhi;
-    if (!(hi - lo > 1e-16 * fabs(hi))) break;
+  __syncthreads();
+  for (int it = 0; it < 8; ++it) {
+    const double lo = lohi[0], hi = lohi[1];
+    if (!(hi - lo > 1e-16 * fabs(hi))) break;       // uniform: all threads read the same values
+    const double x = lo + (hi - lo) * (tid + 1) / (LZ_NT + 1.0);
+    cnt_sm[tid] = (sturm_count_nodiv(k, a, b, x) >= 1) ? 1 : 0;
+    __syncthreads();
+    if (tid == 0) {
+      int f = LZ_NT;
+      for (int t = 0; t < LZ_NT; ++t) if (cnt_sm[t]) { f = t; break; }
+      lohi[0] = lo + (hi - lo) * f / (LZ_NT + 1.0);
+      lohi[1] = (f < LZ_NT) ? lo + (hi - lo) * (f + 1) / (LZ_NT + 1.0) : hi;
+    }
+    __syncthreads();
   }
-  return 0.5 * (lo + hi);
+  const double r = 0.5 * (lohi[0] + lohi[1]);
+  __syncthreads();
+  return r;
+}
+
+// eigenvector of T for eigenvalue th: two inverse-iteration steps (Thomas, one division per row)
+__device__ void tridiag_eigvec_fast(int k, const double* a, const double* b, double th, double* s,
+                                    double* w) {
+  double scale = 0.0;
+  for (int i = 0; i < k; ++i) scale = fmax(scale, fabs(a[i]) + (i < k - 1 ? fabs(b[i]) : 0.0));
+  const double tiny = 1e-300 + 1e-15 * scale;
+  for (int i = 0; i < k; ++i) s[i] = 1.0;
+  double* cp = w;
+  double* dp = w + k;
+  for (int step = 0; step < 2; ++step) {
+    double den = a[0] - th;
+    if (fabs(den) < tiny) den = (den >= 0 ? tiny : -tiny);
+    double inv = 1.0 / den;
+    cp[0] = (k > 1 ? b[0] : 0.0) * inv;
+    dp[0] = s[0] * inv;
+    for (int i = 1; i < k; ++i) {
+      den = (a[i] - th) - b[i - 1] * cp[i - 1];
+      if (fabs(den) < tiny) den = (den >= 0 ? tiny : -tiny);
+      inv = 1.0 / den;
+      cp[i] = (i < k - 1 ? b[i] : 0.0) * inv;
+      dp[i] = (s[i] - b[i - 1] * dp[i - 1]) * inv;
+    }
+    s[k - 1] = dp[k - 1];
+    for (int i = k - 2; i >= 0; --i) s[i] = dp[i] - cp[i] * s[i + 1];
+    double nrm = 0.0;
+    for (int i = 0; i < k; ++i) nrm += s[i] * s[i];
+    nrm = 1.0 / sqrt(nrm);
+    for (int i = 0; i < k; ++i) s[i] *= nrm;
+  }
 }
 
 template <int CS>
@@ -675,6 +718,9 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
   cl.sync();
   double knorm = 0.0;
   for (int p = 0; p < CS; ++p) knorm = fmax(knorm, *cl.map_shared_rank(nb + 2, p));
+  __shared__ int cnt_sm[LZ_NT];
+  __shared__ double lohi[2];
+  // v_0: unnormalised start slice in wl, its squared norm partial in nb[3]
   double ss = 0.0;
   for (int r = tid; r < nr; r += LZ_NT) {
     const int g = r0 + r;
@@ -682,21 +728,31 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     wl[r] = v;
     ss += v * v;
   }
-  double nrm = sqrt(cluster_sum(0, block_sum(ss)));
-  for (int r = tid; r < nr; r += LZ_NT) store_v(0, r, wl[r] / nrm);
+  ss = block_sum(ss);
+  if (tid == 0) nb[3] = ss;
   cl.sync();
   int k_final = 0;
   double theta = 0.0, theta_prev = INFINITY;
+  double bprev = 0.0;
   for (int k = 0; k < kmax; ++k) {
-    const double* vk = a.V + static_cast<int64_t>(k) * n;
-    for (int c = tid; c < n; c += LZ_NT) vfull[c] = vk[c];
+    // exchange: v_k = w_{k} / ||w_k|| assembled from every CTA's wl slice (DSMEM), norm from nb[3]
+    double nn = 0.0;
+    for (int p = 0; p < CS; ++p) nn += *cl.map_shared_rank(nb + 3, p);
+    const double inv = 1.0 / sqrt(nn);
+    for (int c = tid; c < n; c += LZ_NT) {
+      const int p = c / R, rr = c - p * R;
+      vfull[c] = cl.map_shared_rank(wl, p)[rr] * inv;
+    }
+    if (k > 0 && tid == 0) be[k - 1] = sqrt(nn);
+    cl.sync();                                    // everyone done reading remote wl / nb[3]
+    for (int r = tid; r < nr; r += LZ_NT) store_v(k, r, vfull[r0 + r]);
     __syncthreads();
     for (int r = wid; r < nr; r += nw) {
       const double* kr = Krow(r);
-      double s = 0.0;
-      for (int c = lane; c < n; c += 32) s += kr[c] * vfull[c];
-      s = warp_sum(s);
-      if (lane == 0) wl[r] = s;
+      double s_ = 0.0;
+      for (int c = lane; c < n; c += 32) s_ += kr[c] * vfull[c];
+      s_ = warp_sum(s_);
+      if (lane == 0) wl[r] = s_;
     }
     __syncthreads();
     double alpha = 0.0;
@@ -704,10 +760,10 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
       double* hpp = hp + pass * (kmax + 1);
       for (int j = wid; j <= k; j += nw) {
         const double* vj = Vrow(j);
-        double s = 0.0;
-        for (int r = lane; r < nr; r += 32) s += vj[r] * wl[r];
-        s = warp_sum(s);
-        if (lane == 0) hpp[j] = s;
+        double s_ = 0.0;
+        for (int r = lane; r < nr; r += 32) s_ += vj[r] * wl[r];
+        s_ = warp_sum(s_);
+        if (lane == 0) hpp[j] = s_;
       }
       cl.sync();
       for (int j = tid; j <= k; j += LZ_NT) {
@@ -717,7 +773,6 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
       }
       __syncthreads();
       alpha += hs[k];
-      // w -= sum_j hs[j] V_j : warp w sums j = w (mod nw) for its rows, then fixed-order combine
       for (int r = lane; r < nr; r += 32) {
         double t = 0.0;
         for (int j = wid; j <= k; j += nw) t = fma(hs[j], Vrow(j)[r], t);
@@ -733,34 +788,35 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     }
     double s2 = 0.0;
     for (int r = tid; r < nr; r += LZ_NT) s2 += wl[r] * wl[r];
-    const double beta = sqrt(cluster_sum(k & 1, block_sum(s2)));
-    if (tid == 0) { al[k] = alpha; be[k] = beta; }
-    __syncthreads();
+    s2 = block_sum(s2);
+    if (tid == 0) { al[k] = alpha; nb[3] = s2; }
+    cl.sync();                                    // partial norms + new wl visible cluster-wide
+    double nn2 = 0.0;
+    for (int p = 0; p < CS; ++p) nn2 += *cl.map_shared_rank(nb + 3, p);
+    const double beta = sqrt(nn2);
+    if (tid == 0) be[k] = beta;
+    (void)bprev;
     const int kk = k + 1;
     const bool last = (kk == kmax) || (kk == n) || !(beta > 1e-300);
-    if (last || (kk % 4 == 0 && kk >= 8)) {
-      if (wid == 0) {
-        for (int t = lane; t < kk; t += 32) { ta[t] = al[t]; tb[t] = be[t]; }
-        __syncwarp();
-        const double th = warp_tridiag_min_eig(kk, ta, tb, theta_prev);
-        if (lane == 0) {
-          tridiag_eigvec(kk, ta, tb, th, sv, sw);
-          const double res = fabs(be[k] * sv[kk - 1]);
-          s_theta = th;
-          const bool ok = res <= a.tol_rel * knorm;
-          if (ok || last) {
-            s_done = 1;
-            s_conv = ok || !(beta > 1e-300) || (kk == n);
-          }
+    if (last || (kk >= 16 && kk % 8 == 0)) {
+      for (int t = tid; t < kk; t += LZ_NT) { ta[t] = al[t]; tb[t] = (t < k) ? be[t] : beta; }
+      __syncthreads();
+      const double th = block_tridiag_min_eig(kk, ta, tb, theta_prev, cnt_sm, lohi);
+      if (tid == 0) {
+        tridiag_eigvec_fast(kk, ta, tb, th, sv, sw);
+        const double res = fabs(beta * sv[kk - 1]);
+        s_theta = th;
+        const bool ok = res <= a.tol_rel * knorm;
+        if (ok || last) {
+          s_done = 1;
+          s_conv = ok || !(beta > 1e-300) || (kk == n);
         }
       }
       __syncthreads();
       theta = s_theta;
       theta_prev = theta;
     }
-    if (s_done) { k_final = kk; break; }
-    for (int r = tid; r < nr; r += LZ_NT) store_v(k + 1, r, wl[r] / beta);
-    cl.sync();
+    if (s_done) { k_final = kk; cl.sync(); break; }
   }
   // Ritz vector (rows of this CTA), normalised over the cluster; M = K - theta I
   double s3 = 0.0;

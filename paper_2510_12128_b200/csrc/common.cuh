@@ -167,6 +167,8 @@ struct RhsArgs {
   double* SR_part;
   double* rr_part;
   int ncol;
+  const double* cy;        // NULL, or the precomputed transformed RHS c = R^{-T} y (padded layout)
+  double* cy_out;          // NULL, or where to store c (first evaluation of a numgrad)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

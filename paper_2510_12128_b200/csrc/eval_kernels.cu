@@ -99,8 +99,21 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
     const int64_t g = p0 + r;
     const double uu = a.u[g];
     double cval = 0.0;
-    if (r < b)
-      for (int k = 0; k <= r; ++k) cval += Li[static_cast<int64_t>(k) * ld + r] * ys[k];
+    if (a.cy) {
+      cval = a.cy[g];
+    } else if (r < b) {
+      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+      int k = 0;
+      for (; k + 3 <= r; k += 4) {
+        c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
+        c1 = fma(Li[static_cast<int64_t>(k + 1) * ld + r], ys[k + 1], c1);
+        c2 = fma(Li[static_cast<int64_t>(k + 2) * ld + r], ys[k + 2], c2);
+        c3 = fma(Li[static_cast<int64_t>(k + 3) * ld + r], ys[k + 3], c3);
+      }
+      for (; k <= r; ++k) c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
+      cval = (c0 + c1) + (c2 + c3);
+    }
+    if (a.cy_out) a.cy_out[g] = cval;
 #pragma unroll
     for (int c = 0; c < MAXC; ++c) {
       if (c >= ncol) break;
@@ -461,7 +474,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
 constexpr int TROWS = 8;   // rows of T per CTA (one per warp)
 
 template <int NCP>
-__global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
+__global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
   if (a.gate && !a.st->any_active) return;
   extern __shared__ double Ss[];          // n_c * NCP
   __shared__ double cb[2 * NCP];
@@ -476,10 +489,10 @@ __global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
   __syncthreads();
   const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
   // stage S (n_c rows of NCP) with all loads of a thread in flight: thread -> rows j = tid + k*NT
-  for (int j0 = 0; j0 < n_c; j0 += NT * 4) {
-    double v[4][NCP];
+  for (int j0 = 0; j0 < n_c; j0 += NT * 2) {
+    double v[2][NCP];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 2; ++u) {
       const int j = j0 + u * NT + tid;
 #pragma unroll
       for (int c2 = 0; c2 < NCP / 2; ++c2) {
@@ -497,7 +510,7 @@ __global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
       }
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < 2; ++u) {
       const int j = j0 + u * NT + tid;
       if (j < n_c) {
 #pragma unroll
@@ -539,7 +552,7 @@ __global__ void __launch_bounds__(NT) lowrank_kernel(LowrankArgs a) {
 // CG update: x += alpha p, r -= alpha q (active columns); partials of r^T r and S(r);
 // the last CTA forms beta = r'^T r' / r^T r, records it, advances counters and freezes.
 template <int NCP>
-__global__ void __launch_bounds__(NT) update_kernel(UpdateArgs a) {
+__global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
   CGState* st = a.st;
   if (!st->any_active) return;
   __shared__ double sred[(NT / 32) * MAXC];
