@@ -851,7 +851,11 @@ static cudaError_t lanczos_launch_cs(const LanczosArgs& a0, cudaStream_t s) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  const size_t limit = static_cast<size_t>(optin) - 1024;
+  auto kern = lanczos_cluster_kernel<CS>;
+  cudaFuncAttributes fa;
+  memset(&fa, 0, sizeof(fa));
+  cudaFuncGetAttributes(&fa, kern);
+  const size_t limit = static_cast<size_t>(optin) - fa.sharedSizeBytes - 256;
   a.cacheK = (withK * sizeof(double) <= limit) ? 1 : 0;
   size_t used = a.cacheK ? withK : base;
   long room = static_cast<long>(limit / sizeof(double)) - static_cast<long>(used);
@@ -859,7 +863,6 @@ static cudaError_t lanczos_launch_cs(const LanczosArgs& a0, cudaStream_t s) {
   used += static_cast<size_t>(a.kcache) * R;
   const size_t smem = used * sizeof(double);
   if (smem > limit) return cudaErrorInvalidValue;
-  auto kern = lanczos_cluster_kernel<CS>;
   cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(limit));
   if (CS > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
   cudaLaunchConfig_t cfg = {};
