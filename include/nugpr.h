@@ -144,6 +144,29 @@ nugpr_status nugpr_ctx_profile(nugpr_ctx* ctx, int32_t cls, double* ms, double* 
 /* Total kernel launches issued by the library in this process. */
 int64_t nugpr_launch_count(void);
 
+/* A0 — clustering ("k-means to find n_c clusters", cluster centres become the
+ * representatives; PAPER.md:43, 290 cluster-contiguous storage; Eq. (32)
+ * medoids).  Lloyd k-means per reading P18: squared distances summed in dimension order
+ * without FMA, ties to the lowest centre, centroid sums exact in int64 fixed point at scale
+ * 2^s with s = 62 - ceil(log2(max|x| n)), empty clusters keep their centre; stop when no
+ * assignment changes or after max_iter update steps.  Then a stable sort by (cluster,
+ * original index).  The assignment, perm and offsets are bit-exact functions of the inputs.
+ *  X [host|device] n x d original order (d <= 32).  init_centers [host|device] n_c x d, or NULL
+ *  for Forgy rows x_{i_j}: candidate t of centre j is splitmix64_seed((j<<32)|t) mod n, the first
+ *  not yet taken.  rep_mode nugpr_rep_mode: GIVEN = the initial centres, CENTROID = the final
+ *  centres, MEDOID = argmax_{x in C_j} sum_{x' in C_j} k(x, x'; theta) (reading P17; `kernel`,
+ *  theta.lengthscale/outputscale used only here), lowest original index on ties.
+ *  y [host|device] n or NULL.  Outputs (each [host|device], NULL to skip except offsets):
+ *  perm n (perm[k] = original row of sorted row k), offsets [host] n_c+1, reps n_c x d,
+ *  X_sorted n x d, y_sorted n, iters [host] (update steps made).  An empty final cluster
+ *  returns NUGPR_ERR_SHAPE (outputs are still written).  workspace: nugpr_cluster_workspace_size. */
+nugpr_status nugpr_cluster_workspace_size(int64_t n, int32_t d, int32_t n_c, size_t* bytes);
+nugpr_status nugpr_cluster(nugpr_ctx* ctx, const double* X, int64_t n, int32_t d, int32_t n_c,
+                           const double* init_centers, uint64_t seed, int32_t max_iter,
+                           int32_t rep_mode, int32_t kernel, nugpr_theta theta, const double* y,
+                           void* workspace, size_t ws_bytes, int64_t* perm, int64_t* offsets,
+                           double* reps, double* X_sorted, double* y_sorted, int32_t* iters);
+
 /* Workspace bytes for blocks built on `offsets` ([host], n_c+1) plus `eval_slots` (1..7)
  * evaluation scratch sets (up to NUGPR_MAX_PROBES probes, cg_max_iter < 4096).  More slots
  * let nugpr_numgrad keep several evaluations in flight; nugpr_build_blocks uses as many as

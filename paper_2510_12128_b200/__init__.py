@@ -5,6 +5,7 @@ only.  Every step of the MLL evaluation runs in the library's sm_100a CUDA kerne
 provides device memory (the workspace tensor), the stream and the process group.
 
     ctx = Context(device=0)
+    cl = cluster(ctx, X, n_c, y=y)                                               # row A0
     blocks = build_blocks(ctx, X_sorted, offsets, reps, theta0, kernel="rbf")   # row A1
     rec = mll(ctx, blocks, y_sorted, theta)                                      # rows A2-A7
     L0, g, evals = numgrad(ctx, blocks, y_sorted, theta)                         # row A8
@@ -19,7 +20,7 @@ import numpy as np
 from . import _native as N
 from ._native import NugprError
 
-__all__ = ["Context", "Blocks", "build_blocks", "mll", "numgrad", "train", "adam_step",
+__all__ = ["Context", "Blocks", "cluster", "build_blocks", "mll", "numgrad", "train", "adam_step",
            "shard_plan", "tridiag_eig", "workspace_size", "NugprError", "version"]
 
 
@@ -131,6 +132,35 @@ class Context:
             self.close()
         except Exception:  # pragma: no cover
             pass
+
+
+def cluster(ctx: Context, X, n_c: int, y=None, init_centers=None, seed: int = 0, max_iter: int = 100,
+            rep_mode: str = "centroid", kernel: str = "rbf", theta=(1.0, 0.1, 1.0)) -> dict:
+    """Row A0: k-means + stable cluster sort.  Returns device tensors
+    perm, reps, X_sorted, y_sorted (if y given), host offsets and the iteration count."""
+    import torch
+    keep = []
+    Xf = _f64(X)
+    n, d = int(Xf.shape[0]), int(Xf.shape[1])
+    dev = torch.device("cuda", ctx.device)
+    nb = C.c_size_t()
+    N.check(N.lib().nugpr_cluster_workspace_size(n, d, int(n_c), C.byref(nb)))
+    ws = torch.empty(nb.value, dtype=torch.uint8, device=dev)
+    perm = torch.empty(n, dtype=torch.int64, device=dev)
+    reps = torch.empty((n_c, d), dtype=torch.float64, device=dev)
+    Xs = torch.empty((n, d), dtype=torch.float64, device=dev)
+    ys = torch.empty(n, dtype=torch.float64, device=dev) if y is not None else None
+    off = np.zeros(n_c + 1, dtype=np.int64)
+    it = C.c_int32(0)
+    N.check(N.lib().nugpr_cluster(ctx.handle, _ptr(Xf, keep), n, d, int(n_c),
+                                  _ptr(_f64(init_centers), keep) if init_centers is not None else None,
+                                  int(seed) & 0xFFFFFFFFFFFFFFFF, int(max_iter), N.REP_MODES[rep_mode],
+                                  N.KERNELS[kernel], _theta(theta),
+                                  _ptr(_f64(y), keep) if y is not None else None,
+                                  C.c_void_p(ws.data_ptr()), ws.numel(), C.c_void_p(perm.data_ptr()),
+                                  off.ctypes.data, C.c_void_p(reps.data_ptr()), C.c_void_p(Xs.data_ptr()),
+                                  C.c_void_p(ys.data_ptr()) if ys is not None else None, C.byref(it)))
+    return dict(perm=perm, offsets=off, reps=reps, X_sorted=Xs, y_sorted=ys, iters=int(it.value))
 
 
 def workspace_size(offsets, n_c: int, d: int, eval_slots: int = 1) -> int:

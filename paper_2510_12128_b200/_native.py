@@ -19,6 +19,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "DEGENERATE_RE
           5: "CG_NOT_CONVERGED", 6: "WORKSPACE", 7: "CUDA", 8: "COMM", 9: "INTERNAL",
           10: "UNSUPPORTED"}
 KERNELS = {"rbf": 0, "matern52": 1, "rbf_as_printed": 2}
+REP_MODES = {"given": 0, "centroid": 1, "medoid": 2}
 MODES = {0: "baseline", 1: "noise", 2: "scale", 3: "generic"}
 PROF_CLASSES = {"apply_B": 0, "apply_lowrank": 1, "update": 2, "rhs": 3, "gemm": 4, "chol": 5,
                 "lanczos": 6, "other": 7}
@@ -92,6 +93,10 @@ def lib():
         "nugpr_train": (C.c_int, [P, P, P, C.c_int32, C.c_int32, P, P, C.c_int32, C.c_int32,
                                   C.c_double, C.POINTER(GradCfg), C.POINTER(SolveCfg),
                                   C.POINTER(C.c_double), P, P, C.c_size_t]),
+        "nugpr_cluster_workspace_size": (C.c_int, [C.c_int64, C.c_int32, C.c_int32, C.POINTER(C.c_size_t)]),
+        "nugpr_cluster": (C.c_int, [P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_uint64, C.c_int32,
+                                    C.c_int32, C.c_int32, Theta, P, P, C.c_size_t, P, P, P, P, P,
+                                    C.POINTER(C.c_int32)]),
         "nugpr_adam_step": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double]),
         "nugpr_shard_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
         "nugpr_tridiag_eig": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -114,4 +119,4 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_ctx_destroy", "nugpr_ctx_set_profiling", "nugpr_ctx_profile",
             "nugpr_launch_count", "nugpr_workspace_size", "nugpr_build_blocks", "nugpr_blocks_destroy",
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
-            "nugpr_shard_plan", "nugpr_tridiag_eig"]
+            "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster"]

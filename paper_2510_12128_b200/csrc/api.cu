@@ -600,6 +600,157 @@ extern "C" nugpr_status nugpr_blocks_export(const nugpr_blocks* bl, int32_t what
 }
 
 // ------------------------------------------------------------------------------------------
+// Row A0: clustering (cluster_kernels.cu).  Host code only sequences the Lloyd iterations
+// (one 4-byte "changed" read-back per iteration) and draws the Forgy row indices.
+namespace {
+struct KmWs {
+  double *X, *C, *C0, *Xs, *yin, *ys, *score;
+  unsigned long long *S, *cnt, *amax;
+  int32_t *a0, *a1, *changed;
+  long long* hist;
+  int64_t *perm, *off, *med, *idx;
+};
+size_t km_carve(Carver& c, int64_t n, int d, int n_c, KmWs& w) {
+  const int64_t nch = km_chunks(n);
+  w.X = c.take<double>(static_cast<size_t>(n) * d);
+  w.Xs = c.take<double>(static_cast<size_t>(n) * d);
+  w.yin = c.take<double>(n);
+  w.ys = c.take<double>(n);
+  w.score = c.take<double>(n);
+  w.C = c.take<double>(static_cast<size_t>(n_c) * d);
+  w.C0 = c.take<double>(static_cast<size_t>(n_c) * d);
+  w.S = c.take<unsigned long long>(static_cast<size_t>(n_c) * d);
+  w.cnt = c.take<unsigned long long>(n_c);
+  w.amax = c.take<unsigned long long>(1);
+  w.a0 = c.take<int32_t>(n);
+  w.a1 = c.take<int32_t>(n);
+  w.changed = c.take<int32_t>(1);
+  w.hist = c.take<long long>(static_cast<size_t>(nch) * n_c);
+  w.perm = c.take<int64_t>(n);
+  w.off = c.take<int64_t>(n_c + 1);
+  w.med = c.take<int64_t>(n_c);
+  w.idx = c.take<int64_t>(n_c);
+  return c.pos + 256;
+}
+}  // namespace
+
+extern "C" nugpr_status nugpr_cluster_workspace_size(int64_t n, int32_t d, int32_t n_c, size_t* bytes) {
+  if (!bytes) return fail(NUGPR_ERR_INVALID_ARG, "bytes is NULL");
+  if (n < 1 || d < 1 || d > 32 || n_c < 1 || n_c > n) return fail(NUGPR_ERR_INVALID_ARG, "need n >= n_c >= 1, 1 <= d <= 32");
+  Carver c(nullptr);
+  KmWs w;
+  *bytes = km_carve(c, n, d, n_c, w);
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_cluster(nugpr_ctx* ctx, const double* X, int64_t n, int32_t d, int32_t n_c,
+                                      const double* init_centers, uint64_t seed, int32_t max_iter,
+                                      int32_t rep_mode, int32_t kernel, nugpr_theta theta, const double* y,
+                                      void* workspace, size_t ws_bytes, int64_t* perm, int64_t* offsets,
+                                      double* reps, double* X_sorted, double* y_sorted, int32_t* iters) {
+  if (!ctx || !X || !workspace || !offsets) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  size_t need = 0;
+  RET(nugpr_cluster_workspace_size(n, d, n_c, &need));
+  if (ws_bytes < need) return fail(NUGPR_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
+  if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(NUGPR_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  if (max_iter < 0) return fail(NUGPR_ERR_INVALID_ARG, "max_iter < 0");
+  if (rep_mode < NUGPR_REP_GIVEN || rep_mode > NUGPR_REP_MEDOID) return fail(NUGPR_ERR_INVALID_ARG, "bad rep_mode");
+  if (rep_mode == NUGPR_REP_MEDOID && (kernel < 0 || kernel > 2 || !theta_ok(theta)))
+    return fail(NUGPR_ERR_INVALID_ARG, "MEDOID needs a valid kernel and theta");
+  CK(cudaSetDevice(ctx->device));
+  cudaGetLastError();
+  cudaStream_t s = ctx->stream;
+  Carver c(workspace);
+  KmWs w;
+  km_carve(c, n, d, n_c, w);
+  const size_t xb = sizeof(double) * static_cast<size_t>(n) * d, cb = sizeof(double) * static_cast<size_t>(n_c) * d;
+  CK(cudaMemcpyAsync(w.X, X, xb, cudaMemcpyDefault, s));
+  if (init_centers) {
+    CK(cudaMemcpyAsync(w.C0, init_centers, cb, cudaMemcpyDefault, s));
+  } else {
+    // Forgy: candidate t of centre j = splitmix64_seed((j << 32) | t) mod n, first one not taken
+    std::vector<int64_t> idx(n_c);
+    std::vector<char> taken(static_cast<size_t>(n), 0);
+    for (int j = 0; j < n_c; ++j) {
+      for (uint64_t t = 0;; ++t) {
+        const int64_t i = static_cast<int64_t>(splitmix64_at(seed, (static_cast<uint64_t>(j) << 32) | t) %
+                                               static_cast<uint64_t>(n));
+        if (!taken[i]) { taken[i] = 1; idx[j] = i; break; }
+      }
+    }
+    CK(cudaMemcpyAsync(w.idx, idx.data(), sizeof(int64_t) * n_c, cudaMemcpyHostToDevice, s));
+    launch_km_gather(w.X, d, w.idx, nullptr, n_c, w.C0, s);
+  }
+  CK(cudaMemcpyAsync(w.C, w.C0, cb, cudaMemcpyDeviceToDevice, s));
+  // fixed-point scale 2^s, s = 62 - ceil(log2(max|x| n))
+  CK(cudaMemsetAsync(w.amax, 0, sizeof(unsigned long long), s));
+  launch_km_absmax(w.X, static_cast<int64_t>(n) * d, w.amax, s);
+  unsigned long long amax_bits = 0;
+  CK(cudaMemcpyAsync(&amax_bits, w.amax, sizeof(amax_bits), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  double amax;
+  memcpy(&amax, &amax_bits, sizeof(double));
+  const int shift = (amax == 0.0) ? 62 : static_cast<int>(62 - std::ceil(std::log2(amax * static_cast<double>(n))));
+  const double scale = std::ldexp(1.0, shift), inv_scale = std::ldexp(1.0, -shift);
+  CK(cudaMemsetAsync(w.S, 0, sizeof(unsigned long long) * static_cast<size_t>(n_c) * d, s));
+  CK(cudaMemsetAsync(w.cnt, 0, sizeof(unsigned long long) * n_c, s));
+  // Lloyd: assign; repeat {update; assign} until no change or max_iter updates
+  int32_t* a_cur = w.a0;
+  int32_t* a_nxt = w.a1;
+  launch_km_assign(w.X, n, d, n_c, w.C, nullptr, a_cur, scale, w.S, w.cnt, w.changed, s);
+  CKL();
+  int it = 0;
+  while (it < max_iter) {
+    launch_km_update(n_c, d, inv_scale, w.S, w.cnt, w.C, s);
+    ++it;
+    CK(cudaMemsetAsync(w.changed, 0, sizeof(int32_t), s));
+    launch_km_assign(w.X, n, d, n_c, w.C, a_cur, a_nxt, scale, w.S, w.cnt, w.changed, s);
+    CKL();
+    std::swap(a_cur, a_nxt);
+    CK(cudaMemcpyAsync(ctx->h_flag, w.changed, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (!*ctx->h_flag) break;
+  }
+  if (iters) *iters = it;
+  // stable counting sort by (cluster, original index)
+  launch_km_sort(a_cur, n, n_c, w.hist, w.perm, w.off, s);
+  CKL();
+  CK(cudaMemcpyAsync(offsets, w.off, sizeof(int64_t) * (n_c + 1), cudaMemcpyDeviceToHost, s));
+  launch_km_gather(w.X, d, w.perm, nullptr, n, w.Xs, s);
+  if (y) {
+    CK(cudaMemcpyAsync(w.yin, y, sizeof(double) * n, cudaMemcpyDefault, s));
+    launch_km_gather(w.yin, 1, w.perm, nullptr, n, w.ys, s);
+  }
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  int64_t bmax = 0;
+  bool empty = false;
+  for (int j = 0; j < n_c; ++j) {
+    bmax = std::max<int64_t>(bmax, offsets[j + 1] - offsets[j]);
+    if (offsets[j + 1] == offsets[j]) empty = true;
+  }
+  if (reps) {
+    if (rep_mode == NUGPR_REP_GIVEN) {
+      CK(cudaMemcpyAsync(reps, w.C0, cb, cudaMemcpyDefault, s));
+    } else if (rep_mode == NUGPR_REP_CENTROID) {
+      CK(cudaMemcpyAsync(reps, w.C, cb, cudaMemcpyDefault, s));
+    } else {
+      if (empty) return fail(NUGPR_ERR_SHAPE, "MEDOID representatives need non-empty clusters");
+      launch_km_medoids(w.Xs, d, w.off, n_c, bmax, kernel, theta.lengthscale, theta.outputscale, w.score, w.med, s);
+      launch_km_gather(w.Xs, d, w.med, nullptr, n_c, w.C0, s);
+      CKL();
+      CK(cudaMemcpyAsync(reps, w.C0, cb, cudaMemcpyDefault, s));
+    }
+  }
+  if (perm) CK(cudaMemcpyAsync(perm, w.perm, sizeof(int64_t) * n, cudaMemcpyDefault, s));
+  if (X_sorted) CK(cudaMemcpyAsync(X_sorted, w.Xs, xb, cudaMemcpyDefault, s));
+  if (y_sorted && y) CK(cudaMemcpyAsync(y_sorted, w.ys, sizeof(double) * n, cudaMemcpyDefault, s));
+  CK(cudaStreamSynchronize(s));
+  if (empty) return fail(NUGPR_ERR_SHAPE, "a cluster is empty after k-means");
+  return NUGPR_OK;
+}
+
+// ------------------------------------------------------------------------------------------
 // One evaluation, fully enqueued on stream s using slot e; the record lands in e.out (device).
 static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, const double* y_dev,
                                  nugpr_theta th, const nugpr_solve_cfg* cfg, cudaStream_t s, int* mode_out,

@@ -66,20 +66,6 @@ void post_launch(const char* name) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Kernel value.  Squared distance as sum_d (x_d - x'_d)^2 with explicitly non-fused ops
-// (bitwise-symmetric blocks with an exact diagonal).
-__device__ __forceinline__ double kval(int kind, double sq, double lam, double alpha) {
-  if (kind == 0) {                       // RBF (reading X3)
-    return alpha * exp(-__ddiv_rn(sq, 2.0 * lam * lam));
-  } else if (kind == 2) {                // Eq. (2) as printed
-    return alpha * exp(-__ddiv_rn(sqrt(sq), 2.0 * lam * lam));
-  } else {                               // Matern-5/2
-    double rho = sqrt(sq);
-    double s = sqrt(5.0) * rho / lam;
-    return alpha * (1.0 + s + 5.0 * sq / (3.0 * lam * lam)) * exp(-s);
-  }
-}
-
 // ---------------------------------------------------------------------------------------
 // Assemble K_i(theta) = k(X_i, X_i) + (noise + jitter_i) I into dst (ld x ld col-major),
 // padding = identity.  grid = (tiles32 x tiles32 of the largest block, #blocks in list).

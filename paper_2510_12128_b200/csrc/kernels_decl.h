@@ -52,4 +52,20 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
                   int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
 
+// cluster_kernels.cu (row A0)
+void launch_km_absmax(const double* X, int64_t cnt, unsigned long long* out, cudaStream_t s);
+size_t km_assign_smem();
+void launch_km_assign(const double* X, int64_t n, int d, int n_c, const double* C, const int32_t* a_old,
+                      int32_t* a_new, double scale, unsigned long long* S, unsigned long long* cnt,
+                      int32_t* changed, cudaStream_t s);
+void launch_km_update(int n_c, int d, double inv_scale, unsigned long long* S, unsigned long long* cnt,
+                      double* C, cudaStream_t s);
+int64_t km_chunks(int64_t n);
+void launch_km_sort(const int32_t* a, int64_t n, int n_c, long long* hist, int64_t* perm, int64_t* off,
+                    cudaStream_t s);
+void launch_km_gather(const double* src, int width, const int64_t* idx64, const int32_t* idx32, int64_t rows,
+                      double* dst, cudaStream_t s);
+void launch_km_medoids(const double* Xs, int d, const int64_t* off, int n_c, int64_t b_max, int kind, double lam,
+                       double alpha, double* score, int64_t* out, cudaStream_t s);
+
 }  // namespace nugpr

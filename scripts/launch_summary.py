@@ -16,7 +16,7 @@ for r in rows:
     unit = d["Metric Unit"]
     m = d["Metric Name"]
     if m == "gpu__time_duration.sum":
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(unit, 1.0)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}.get(unit, 1.0)
         agg[key][1] += val * scale
     elif m.startswith("dram__bytes"):
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
