@@ -10,6 +10,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/nugpr.h"
@@ -142,7 +143,6 @@ struct EvalDev {
   CGState* st = nullptr;
   nugpr_mll_out* out = nullptr;
   double* ah = nullptr, *bh = nullptr, *slqw = nullptr;
-  double* ystage = nullptr;   // n
   double* Tbuf = nullptr;     // n_c x MAXC
 };
 
@@ -158,6 +158,7 @@ struct BlocksDev {
   int32_t* linfo = nullptr;
   double* Zexport = nullptr;  // m x n (debug probe export)
   double* cy = nullptr;       // n_pad: c = R^{-T} y cached across the evaluations of one numgrad
+  double* ystage = nullptr;   // n: host y staged to the device
 };
 
 void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
@@ -188,6 +189,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.linfo = c.take<int32_t>(4);
   B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
   B.cy = c.take<double>(L.n_pad);
+  B.ystage = c.take<double>(L.n);
   E.assign(slots, EvalDev());
   const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
   for (int s = 0; s < slots; ++s) {
@@ -221,7 +223,6 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.ah = c.take<double>(static_cast<size_t>(MAXC) * HIST);
     e.bh = c.take<double>(static_cast<size_t>(MAXC) * HIST);
     e.slqw = c.take<double>(static_cast<size_t>(MAXC) * 3 * HIST);
-    e.ystage = c.take<double>(L.n);
     e.Tbuf = c.take<double>(static_cast<size_t>(n_c) * MAXC);
   }
 }
@@ -255,7 +256,25 @@ struct nugpr_ctx {
   std::vector<ProfPending> pend;
   double acc_ms[PC_N] = {0}, acc_bytes[PC_N] = {0};
   long long acc_n[PC_N] = {0};
+  // concurrent evaluations: one stream per eval slot, fork/join events, pinned staging
+  cudaStream_t capture_stream = nullptr;
+  cudaStream_t slot_stream[NUGPR_NUM_EVALS] = {nullptr};
+  cudaEvent_t ev_fork = nullptr, ev_join[NUGPR_NUM_EVALS] = {nullptr};
+  EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
+  // instantiated CG graphs keyed by (workspace, layout, slot, ncol, logdet mode)
+  std::unordered_map<std::string, cudaGraphExec_t> graphs;
+  std::vector<cudaGraph_t> graph_defs;
 };
+constexpr int MAX_STAGE = 64;
+
+static nugpr_status ensure_slot_streams(nugpr_ctx* c, int slots) {
+  for (int k = 0; k < slots && k < NUGPR_NUM_EVALS; ++k) {
+    if (!c->slot_stream[k]) CK(cudaStreamCreateWithFlags(&c->slot_stream[k], cudaStreamNonBlocking));
+    if (!c->ev_join[k]) CK(cudaEventCreateWithFlags(&c->ev_join[k], cudaEventDisableTiming));
+  }
+  if (!c->ev_fork) CK(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  return NUGPR_OK;
+}
 
 static int prof_begin(nugpr_ctx* c, cudaStream_t s) {
   if (!c || !c->prof) return -1;
@@ -312,7 +331,9 @@ struct nugpr_blocks {
   int last_m = 0;
   uint64_t last_seed = 0;
   const double* last_probes = nullptr;
-  int cy_mode = 0;            // 0: compute c per evaluation; 1: compute and store; 2: reuse B.cy
+  bool cy_ready = false;      // B.cy holds c = R^{-T} y for the current numgrad call
+  bool no_graph = false;      // NUGPR_NO_GRAPH=1: direct launches with host polling
+  const void* ws_base = nullptr;
 };
 
 extern "C" {
@@ -330,8 +351,10 @@ nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world
   c->rank = rank;
   c->world = world;
   cudaError_t e1 = cudaMallocHost(&c->h_flag, 64);
-  cudaError_t e2 = cudaMallocHost(&c->h_out, sizeof(nugpr_mll_out));
-  if (e1 != cudaSuccess || e2 != cudaSuccess) {
+  cudaError_t e2 = cudaMallocHost(&c->h_out, sizeof(nugpr_mll_out) * MAX_STAGE);
+  cudaError_t e3 = cudaMallocHost(&c->h_prm, sizeof(EvalParams) * MAX_STAGE);
+  cudaError_t e4 = cudaStreamCreateWithFlags(&c->capture_stream, cudaStreamNonBlocking);
+  if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess || e4 != cudaSuccess) {
     delete c;
     return fail(NUGPR_ERR_CUDA, "pinned host allocation failed");
   }
@@ -368,8 +391,17 @@ int64_t nugpr_launch_count(void) { return launch_count(); }
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
   if (!ctx) return NUGPR_OK;
   for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
+  for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+  for (cudaGraph_t g : ctx->graph_defs) cudaGraphDestroy(g);
+  for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
+    if (ctx->slot_stream[k]) cudaStreamDestroy(ctx->slot_stream[k]);
+    if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
+  }
+  if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
+  if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
   delete ctx;
   return NUGPR_OK;
 }
@@ -441,6 +473,11 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   Carver c(workspace);
   carve_all(c, bl->L, slots, bl->B, bl->E);
   bl->ctx = ctx;
+  bl->ws_base = workspace;
+  {
+    const char* ng = getenv("NUGPR_NO_GRAPH");
+    bl->no_graph = ng && ng[0] == '1';
+  }
   bl->kind = kernel;
   bl->theta0 = theta0;
   HostLayout& L = bl->L;
@@ -751,19 +788,143 @@ extern "C" nugpr_status nugpr_cluster(nugpr_ctx* ctx, const double* X, int64_t n
 }
 
 // ------------------------------------------------------------------------------------------
-// One evaluation, fully enqueued on stream s using slot e; the record lands in e.out (device).
-static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, const double* y_dev,
+// One evaluation = host-side parameter setup and mode-specific pre-work (Eq. 23-28), the CG
+// solves (rows A4-A5) and the trace / final kernels (A5-A7).  In graph mode the CG loop and the
+// tail are ONE CUDA graph per (workspace, slot): a conditional WHILE node whose condition the
+// update kernel's last CTA sets on the device, so an evaluation needs no host round trip and
+// every operator mode shares the graph (mode data live in the device EvalParams).  With
+// profiling on (bench.py's roofline pass) the same kernels are launched directly, serialised,
+// with CUDA events around each one.
+
+struct IterArgs {
+  ApplyArgs a1, a2, a3, a4;
+  LowrankArgs t1, t2, t3, t4;
+  UpdateArgs ua;
+  int ncp = 0;
+};
+
+static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterArgs& A) {
+  const HostLayout& L = bl->L;
+  const LayoutDev& Ld = bl->Ld;
+  const BlocksDev& B = bl->B;
+  A.ncp = (ncol + 1) & ~1;
+  ApplyArgs& a1 = A.a1;
+  memset(&a1, 0, sizeof(a1));
+  a1.L = Ld; a1.prm = e.prm; a1.st = e.st; a1.u = B.u; a1.jitter = B.jitter; a1.ncol = ncol;
+  a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
+  a1.alpha_hist = e.ah; a1.hist_stride = HIST;
+  a1.ld_max = L.ld_max;
+  {
+    const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
+    const ApplyPlan pl = plan_apply(A.ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles));
+    if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, ncol=%d)", L.ld_max, ncol);
+    a1.slot_doubles = pl.slot_doubles;
+    a1.red_doubles = pl.red_doubles;
+    a1.nstage = pl.nstage;
+    a1.nmine_max = pl.nmine_max;
+    a1.Tbuf = e.Tbuf;
+    a1.smem_b = pl.smem_b;
+    a1.smem_nob = pl.smem_nob;
+    a1.grid = pl.grid;
+  }
+  ApplyArgs& a2 = A.a2;
+  a2 = a1;
+  // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
+  a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;
+  a1.fin = FIN_NONE; a1.gate = 1;
+  for (int c = 0; c < MAXC; ++c) { a1.cA[c] = 1.0; a1.cV[c] = 0.0; a1.cP[c] = 0.0; }
+  // apply 2: q = A V + 4 V + p (probe columns), q = V (y column); p^T q partials -> alpha
+  a2.D = e.V; a2.S_D = e.SV; a2.fuse_p = 0; a2.out = e.Q; a2.use_par_p2 = 1; a2.epi = EPI_DOT;
+  a2.dots = e.dots; a2.fin = FIN_ALPHA; a2.gate = 1;
+  for (int c = 0; c < MAXC; ++c) {
+    if (c == 0) { a2.cA[c] = 0.0; a2.cV[c] = 1.0; a2.cP[c] = 0.0; }
+    else { a2.cA[c] = 1.0; a2.cV[c] = 4.0; a2.cP[c] = 1.0; }
+  }
+  // (with use_par_p2 the kernel takes both the combine term P2 and the dot partner Y2 from
+  //  the parity-resolved current direction P[par^1])
+  UpdateArgs& ua = A.ua;
+  memset(&ua, 0, sizeof(ua));
+  ua.L = Ld; ua.prm = e.prm; ua.st = e.st; ua.u = B.u; ua.X = e.X; ua.R = e.R; ua.Q = e.Q;
+  ua.Pbuf[0] = e.Pb[0]; ua.Pbuf[1] = e.Pb[1]; ua.rr_part = e.rrp; ua.SR_part = e.SR;
+  ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol; ua.cond = 0;
+  LowrankArgs& t1 = A.t1;
+  memset(&t1, 0, sizeof(t1));
+  t1.st = e.st; t1.prm = e.prm; t1.Mp = nullptr; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
+  t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
+  LowrankArgs& t2 = A.t2;
+  t2 = t1;
+  t2.S = e.SV; t2.fuse_p = 0;
+  // trace: V = A X, U = 3 A V - 3 X (probe cols) / X (y col), dotted with RHS
+  ApplyArgs& a3 = A.a3;
+  a3 = a1;
+  a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
+  a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
+  LowrankArgs& t3 = A.t3;
+  t3 = t2;
+  t3.S = e.SX; t3.gate = 0;
+  ApplyArgs& a4 = A.a4;
+  a4 = a3;
+  a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
+  a4.fin = FIN_TRACE;
+  for (int c = 0; c < MAXC; ++c) {
+    if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
+    else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
+  }
+  LowrankArgs& t4 = A.t4;
+  t4 = t2;
+  t4.S = e.SV; t4.gate = 0;
+  return NUGPR_OK;
+}
+
+// Direct launches of one CG iteration / the tail (useB selects the apply's smem variant).
+static void launch_iteration(const IterArgs& A, bool useB, cudaStream_t s) {
+  launch_lowrank(A.t1, A.ncp, s);
+  launch_apply(A.a1, A.ncp, useB, s);
+  launch_lowrank(A.t2, A.ncp, s);
+  launch_apply(A.a2, A.ncp, useB, s);
+  launch_update(A.ua, A.ncp, s);
+}
+static void launch_tail(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol, cudaStream_t s) {
+  launch_spart(bl->Ld, bl->B.u, e.X, ncol, e.SX, s);
+  launch_lowrank(A.t3, A.ncp, s);
+  launch_apply(A.a3, A.ncp, useB, s);
+  launch_lowrank(A.t4, A.ncp, s);
+  launch_apply(A.a4, A.ncp, useB, s);
+}
+
+// Graph of one slot: while (any column active) { CG iteration }; spart; trace applies; final.
+struct EvalGraph {
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t exec = nullptr;
+};
+
+static std::string graph_key(const nugpr_blocks* bl, int slot, int ncol, int logdet_mode) {
+  char buf[160];
+  const HostLayout& L = bl->L;
+  uint64_t h = 1469598103934665603ull;    // FNV-1a over the offsets (pointers follow from them)
+  for (int64_t v : L.off) { h ^= static_cast<uint64_t>(v); h *= 1099511628211ull; }
+  snprintf(buf, sizeof(buf), "%p|%zu|%d|%d|%d|%d|%llx|%d", static_cast<const void*>(bl->ws_base), bl->E.size(),
+           slot, ncol, logdet_mode, L.d, static_cast<unsigned long long>(h), L.n_c);
+  return std::string(buf);
+}
+
+static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int ncol, int logdet_mode,
+                              cudaGraphExec_t* out);
+
+// Enqueue one evaluation on stream s with slot e; the record lands in e.out (device).  `limit`
+// receives the host-known iteration bound (replay) for the launch accounting.
+static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, const double* y_dev,
                                  nugpr_theta th, const nugpr_solve_cfg* cfg, cudaStream_t s, int* mode_out,
-                                 int32_t* h_flag) {
+                                 EvalParams* hstage) {
+  EvalDev& e = bl->E[slot];
   const HostLayout& L = bl->L;
   const LayoutDev& Ld = bl->Ld;
   const BlocksDev& B = bl->B;
   const nugpr_theta t0 = bl->theta0;
   const int m = cfg->num_probes;
   const int ncol = 1 + m;
-  const int ncp = (ncol + 1) & ~1;
   const int max_iter = cfg->cg_max_iter;
-  EvalParams P;
+  EvalParams& P = *hstage;                  // pinned host staging (async upload below)
   memset(&P, 0, sizeof(P));
   P.tol = cfg->cg_tol;
   P.max_iter = max_iter;
@@ -804,118 +965,111 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, c
     lam0_ptr = e.scal;
   }
   P.mode = mode;
+  P.lam0_src = lam0_ptr;
   if (mode_out) *mode_out = mode;
+  if (mode == NUGPR_MODE_SCALE) {
+    // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
+    // build read back (reported in the record only)
+    P.lam0_val = bl->lam0 * P.mscale;
+    P.lam0_src = nullptr;
+  }
   CK(cudaMemcpyAsync(e.prm, &P, sizeof(P), cudaMemcpyHostToDevice, s));
   // the workspace is caller memory with arbitrary contents: the CG state (incl. the
   // self-resetting last-CTA tickets) and the S partials start from zero every evaluation
   CK(cudaMemsetAsync(e.st, 0, sizeof(CGState), s));
-  if (mode == NUGPR_MODE_SCALE) {
-    // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
-    // build read back, written to the slot scalar (reported in the record only).
-    double l0 = bl->lam0 * P.mscale;
-    CK(cudaMemcpyAsync(e.scal + 1, &l0, sizeof(double), cudaMemcpyHostToDevice, s));
-    lam0_ptr = e.scal + 1;
-  }
   // rhs + init
   RhsArgs ra;
   ra.L = Ld; ra.prm = e.prm; ra.st = e.st; ra.Linv = B.Linv; ra.y = y_dev;
   ra.probes = cfg->probes; ra.seed = cfg->probe_seed; ra.u = B.u; ra.RHS = e.RHS; ra.R = e.R;
   ra.X = e.X; ra.P0 = e.Pb[0]; ra.SP0 = e.SPb[0]; ra.SR_part = e.SR; ra.rr_part = e.rrp; ra.ncol = ncol;
-  ra.cy = (bl->cy_mode == 2) ? B.cy : nullptr;
-  ra.cy_out = (bl->cy_mode == 1) ? B.cy : nullptr;
-  if (bl->cy_mode == 1) bl->cy_mode = 2;
+  ra.cy = bl->cy_ready ? B.cy : nullptr;
+  ra.cy_out = nullptr;
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
-  // algorithmic bytes of one apply (SURVEY §8(d)): w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
+  const bool useB = P.B != nullptr;
+  if (!ctx->prof && !bl->no_graph) {
+    cudaGraphExec_t ex = nullptr;
+    RET(get_graph(ctx, bl, slot, ncol, cfg->logdet_mode, &ex));
+    CK(cudaGraphLaunch(ex, s));
+    return NUGPR_OK;
+  }
+  // direct launches (profiling / NUGPR_NO_GRAPH): host polls the activity flag every CH iterations
+  IterArgs A;
+  RET(make_iter_args(bl, e, ncol, A));
   double sum_b2 = 0.0;
   for (int i = 0; i < L.n_c; ++i) { double b = static_cast<double>(L.off[i + 1] - L.off[i]); sum_b2 += b * b; }
+  // algorithmic bytes of one apply (SURVEY §8(d)): w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
   const double vec_bytes = 8.0 * (2.0 * L.n * ncol + L.n + static_cast<double>(L.n_c) * L.n_c);
-  const double apply_bytes = (P.B ? 8.0 * sum_b2 : 0.0) + vec_bytes;
-  const int apply_cls = P.B ? PC_APPLY_B : PC_APPLY_LR;
-  // CG iteration building blocks
-  ApplyArgs a1;
-  memset(&a1, 0, sizeof(a1));
-  a1.L = Ld; a1.prm = e.prm; a1.st = e.st; a1.u = B.u; a1.jitter = B.jitter; a1.ncol = ncol;
-  a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
-  a1.alpha_hist = e.ah; a1.hist_stride = HIST;
-  a1.ld_max = L.ld_max;
-  {
-    const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
-    const ApplyPlan pl = plan_apply(ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles));
-    if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, m=%d)", L.ld_max, m);
-    a1.slot_doubles = pl.slot_doubles;
-    a1.red_doubles = pl.red_doubles;
-    a1.nstage = pl.nstage;
-    a1.nmine_max = pl.nmine_max;
-    a1.Tbuf = e.Tbuf;
-    a1.smem_b = pl.smem_b;
-    a1.smem_nob = pl.smem_nob;
-    a1.grid = pl.grid;
-  }
-  ApplyArgs a2 = a1;
-  // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
-  a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;
-  a1.fin = FIN_NONE; a1.gate = 1;
-  for (int c = 0; c < MAXC; ++c) { a1.cA[c] = 1.0; a1.cV[c] = 0.0; a1.cP[c] = 0.0; }
-  // apply 2: q = A V + 4 V + p (probe columns), q = V (y column); p^T q partials -> alpha
-  a2.D = e.V; a2.S_D = e.SV; a2.fuse_p = 0; a2.out = e.Q; a2.use_par_p2 = 1; a2.epi = EPI_DOT;
-  a2.dots = e.dots; a2.fin = FIN_ALPHA; a2.gate = 1;
-  for (int c = 0; c < MAXC; ++c) {
-    if (c == 0) { a2.cA[c] = 0.0; a2.cV[c] = 1.0; a2.cP[c] = 0.0; }
-    else { a2.cA[c] = 1.0; a2.cV[c] = 4.0; a2.cP[c] = 1.0; }
-  }
-  // (with use_par_p2 the kernel takes both the combine term P2 and the dot partner Y2 from
-  //  the parity-resolved current direction P[par^1])
-  UpdateArgs ua;
-  ua.L = Ld; ua.prm = e.prm; ua.st = e.st; ua.u = B.u; ua.X = e.X; ua.R = e.R; ua.Q = e.Q;
-  ua.Pbuf[0] = e.Pb[0]; ua.Pbuf[1] = e.Pb[1]; ua.rr_part = e.rrp; ua.SR_part = e.SR;
-  ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol;
-
+  const double apply_bytes = (useB ? 8.0 * sum_b2 : 0.0) + vec_bytes;
+  const int apply_cls = useB ? PC_APPLY_B : PC_APPLY_LR;
   const int limit = cfg->replay_iters ? [&] { int mx = 0; for (int c = 0; c < ncol; ++c) mx = std::max(mx, P.replay_iters[c]); return mx; }()
                                       : max_iter;
-  LowrankArgs t1;
-  t1.st = e.st; t1.Mp = P.Mp; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
-  t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
-  LowrankArgs t2 = t1;
-  t2.S = e.SV; t2.fuse_p = 0;
   const int CH = 4;
   int done = 0;
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
-      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t1, ncp, s));
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a1, ncp, P.B != nullptr, s));
-      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t2, ncp, s));
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a2, ncp, P.B != nullptr, s));
-      PROF(ctx, PC_UPDATE, 0.0, s, launch_update(ua, ncp, s));
+      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
+      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+      PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
     }
     CKL();
-    CK(cudaMemcpyAsync(h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(ctx->h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
-    if (!*h_flag) break;
+    if (!*ctx->h_flag) break;
   }
-  // trace: V = A X, U = 3 A V - 3 X (probe cols) / X (y col), dotted with RHS
   launch_spart(Ld, B.u, e.X, ncol, e.SX, s);
-  ApplyArgs a3 = a1;
-  a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
-  a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
-  LowrankArgs t3 = t2;
-  t3.S = e.SX; t3.gate = 0;
-  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t3, ncp, s));
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a3, ncp, P.B != nullptr, s));
-  ApplyArgs a4 = a3;
-  a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
-  a4.fin = FIN_TRACE;
-  for (int c = 0; c < MAXC; ++c) {
-    if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
-    else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
-  }
-  LowrankArgs t4 = t2;
-  t4.S = e.SV; t4.gate = 0;
-  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(t4, ncp, s));
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(a4, ncp, P.B != nullptr, s));
-  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, lam0_ptr, static_cast<double>(L.n),
+  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
+  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
+  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
+  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(L.n),
                ncol, cfg->logdet_mode, e.out, s);
   CKL();
+  return NUGPR_OK;
+}
+
+static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int ncol, int logdet_mode,
+                              cudaGraphExec_t* out) {
+  const std::string key = graph_key(bl, slot, ncol, logdet_mode);
+  auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end()) { *out = it->second; return NUGPR_OK; }
+  EvalDev& e = bl->E[slot];
+  IterArgs A;
+  RET(make_iter_args(bl, e, ncol, A));
+  // every kernel of the graph opts into its shared memory before capture
+  cudaStream_t cs = ctx->capture_stream;
+  cudaGraph_t g = nullptr;
+  CK(cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  CK(cudaGraphAddNode(&wnode, g, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  A.ua.cond = h;
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  launch_iteration(A, true, cs);
+  cudaGraph_t body_out = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(cs, &body_out);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph body capture: %s", cudaGetErrorString(ce)); }
+  CK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
+  launch_tail(bl, e, A, true, ncol, cs);
+  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n),
+               ncol, logdet_mode, e.out, cs);
+  cudaGraph_t g_out = nullptr;
+  ce = cudaStreamEndCapture(cs, &g_out);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph tail capture: %s", cudaGetErrorString(ce)); }
+  cudaGraphExec_t ex = nullptr;
+  ce = cudaGraphInstantiate(&ex, g, 0);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
+  ctx->graphs[key] = ex;
+  ctx->graph_defs.push_back(g);
+  *out = ex;
   return NUGPR_OK;
 }
 
@@ -930,30 +1084,42 @@ static nugpr_status check_cfg(const nugpr_solve_cfg* cfg) {
   return NUGPR_OK;
 }
 
-static nugpr_status stage_y(nugpr_blocks* bl, const double* y, EvalDev& e, cudaStream_t s, const double** y_dev) {
+static nugpr_status stage_y(nugpr_blocks* bl, const double* y, cudaStream_t s, const double** y_dev) {
   if (is_device_ptr(y)) { *y_dev = y; return NUGPR_OK; }
-  CK(cudaMemcpyAsync(e.ystage, y, sizeof(double) * bl->L.n, cudaMemcpyHostToDevice, s));
-  *y_dev = e.ystage;
+  CK(cudaMemcpyAsync(bl->B.ystage, y, sizeof(double) * bl->L.n, cudaMemcpyHostToDevice, s));
+  *y_dev = bl->B.ystage;
   return NUGPR_OK;
 }
 
+// Kernel launches a finished graph-mode evaluation made (host counter for gpu_launches).
+static void account_graph_launches(const nugpr_mll_out& o) {
+  int k = o.iters_y;
+  for (int j = 0; j < 16; ++j) k = std::max(k, o.iters_q[j]);
+  note_launch(5LL * std::max(1, k) + 6);
+}
+
+static nugpr_status finish_record(nugpr_blocks* bl, const nugpr_solve_cfg* cfg, const nugpr_mll_out& o,
+                                  bool graph) {
+  if (graph) account_graph_launches(o);
+  bl->last_m = cfg->num_probes;
+  bl->last_seed = cfg->probe_seed;
+  if (!(o.lambda0 > 0.0)) return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", o.lambda0);
+  if (!o.converged) return fail(NUGPR_ERR_CG_NOT_CONVERGED, "CG reached cg_max_iter = %d", cfg->cg_max_iter);
+  return NUGPR_OK;
+}
+
+// One evaluation on the context stream with slot 0, record read back.
 static nugpr_status run_eval(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_dev, nugpr_theta th,
                              const nugpr_solve_cfg* cfg, nugpr_mll_out* out) {
   cudaStream_t s = ctx->stream;
   cudaGetLastError();
-  EvalDev& e = bl->E[0];
   int mode = 0;
-  RET(enqueue_eval(ctx, bl, e, y_dev, th, cfg, s, &mode, ctx->h_flag));
-  CK(cudaMemcpyAsync(ctx->h_out, e.out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, s));
+  RET(enqueue_eval(ctx, bl, 0, y_dev, th, cfg, s, &mode, &ctx->h_prm[0]));
+  CK(cudaMemcpyAsync(&ctx->h_out[0], bl->E[0].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   prof_harvest(ctx);
-  *out = *ctx->h_out;
-  bl->last_m = cfg->num_probes;
-  bl->last_seed = cfg->probe_seed;
-  if (!(out->lambda0 > 0.0))
-    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", out->lambda0);
-  if (!out->converged) return fail(NUGPR_ERR_CG_NOT_CONVERGED, "CG reached cg_max_iter = %d", cfg->cg_max_iter);
-  return NUGPR_OK;
+  *out = ctx->h_out[0];
+  return finish_record(bl, cfg, *out, !ctx->prof && !bl->no_graph);
 }
 
 extern "C" nugpr_status nugpr_mll(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
@@ -963,7 +1129,8 @@ extern "C" nugpr_status nugpr_mll(nugpr_ctx* ctx, nugpr_blocks* bl, const double
   RET(check_cfg(cfg));
   CK(cudaSetDevice(ctx->device));
   const double* y_dev = nullptr;
-  RET(stage_y(bl, y_sorted, bl->E[0], ctx->stream, &y_dev));
+  RET(stage_y(bl, y_sorted, ctx->stream, &y_dev));
+  bl->cy_ready = false;
   return run_eval(ctx, bl, y_dev, theta, cfg, out);
 }
 
@@ -990,6 +1157,49 @@ struct EvalRecord {
   int32_t valid;
 };
 
+// Evaluate the points `ks` (indices into pts) concurrently: evaluation j runs on slot j % slots,
+// each slot on its own stream forked from the context stream; one host sync at the end.
+static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_dev,
+                                         const std::vector<int>& ks, const nugpr_theta* pts,
+                                         const nugpr_solve_cfg* cfg, EvalRecord* recs) {
+  cudaStream_t s0 = ctx->stream;
+  const int slots = static_cast<int>(bl->E.size());
+  const bool graph = !ctx->prof && !bl->no_graph;
+  if (slots <= 1 || ctx->prof || ks.size() <= 1) {
+    for (int k : ks) {
+      nugpr_status st = run_eval(ctx, bl, y_dev, pts[k], cfg, &recs[k].o);
+      recs[k].status = st;
+      recs[k].valid = 1;
+      if (st != NUGPR_OK && st != NUGPR_ERR_CG_NOT_CONVERGED) return st;
+    }
+    return NUGPR_OK;
+  }
+  RET(ensure_slot_streams(ctx, slots));
+  CK(cudaEventRecord(ctx->ev_fork, s0));
+  const int nk = static_cast<int>(ks.size());
+  for (int j = 0; j < nk; ++j) {
+    const int slot = j % slots;
+    cudaStream_t ss = ctx->slot_stream[slot];
+    if (j < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    int mode = 0;
+    RET(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &mode, &ctx->h_prm[j]));
+    CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
+  }
+  for (int slot = 0; slot < std::min(slots, nk); ++slot) {
+    CK(cudaEventRecord(ctx->ev_join[slot], ctx->slot_stream[slot]));
+    CK(cudaStreamWaitEvent(s0, ctx->ev_join[slot], 0));
+  }
+  CK(cudaStreamSynchronize(s0));
+  for (int j = 0; j < nk; ++j) {
+    EvalRecord& r = recs[ks[j]];
+    r.o = ctx->h_out[j];
+    r.valid = 1;
+    r.status = finish_record(bl, cfg, r.o, graph);
+    if (r.status != NUGPR_OK && r.status != NUGPR_ERR_CG_NOT_CONVERGED) return static_cast<nugpr_status>(r.status);
+  }
+  return NUGPR_OK;
+}
+
 extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
                                       const nugpr_grad_cfg* gcfg, const nugpr_solve_cfg* scfg, double* L0,
                                       double grad[3], nugpr_mll_out* evals, int32_t* n_evals) {
@@ -997,14 +1207,17 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   if (!theta_ok(theta)) return fail(NUGPR_ERR_INVALID_ARG, "theta must be positive and finite");
   RET(check_cfg(scfg));
   CK(cudaSetDevice(ctx->device));
+  cudaGetLastError();
   const double th[3] = {theta.lengthscale, theta.noise, theta.outputscale};
   const double* y_dev = nullptr;
-  RET(stage_y(bl, y_sorted, bl->E[0], ctx->stream, &y_dev));
+  RET(stage_y(bl, y_sorted, ctx->stream, &y_dev));
   auto mk = [](const double* p) { nugpr_theta t{p[0], p[1], p[2]}; return t; };
   int ne = 0;
   // every evaluation of this call shares y and R: c = R^{-T} y is computed once and reused
-  struct CyGuard { nugpr_blocks* b; ~CyGuard() { b->cy_mode = 0; } } cyg{bl};
-  bl->cy_mode = 1;
+  struct CyGuard { nugpr_blocks* b; ~CyGuard() { b->cy_ready = false; } } cyg{bl};
+  launch_cy(bl->Ld, bl->B.Linv, y_dev, bl->L.ld_max, bl->B.cy, ctx->stream);
+  CKL();
+  bl->cy_ready = true;
   if (gcfg->mode == NUGPR_GRAD_CENTRAL) {
     double pts[NUGPR_NUM_EVALS][3];
     double h[3];
@@ -1015,19 +1228,18 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
       pts[2 + 2 * i][i] = th[i] - h[i];
       if (!(pts[2 + 2 * i][i] > 0.0)) return fail(NUGPR_ERR_INVALID_ARG, "step too large for parameter %d", i);
     }
-    // perturbation sharding (PAR-1): LPT over a cost model (baseline: no block reads)
+    nugpr_theta tp[NUGPR_NUM_EVALS];
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) tp[k] = mk(pts[k]);
+    // perturbation sharding (PAR-1): LPT over a cost model (baseline: no block reads; lambda:
+    // G precompute + Lanczos)
     const double cost[NUGPR_NUM_EVALS] = {1.0, 3.0, 3.0, 2.0, 2.0, 2.0, 2.0};
     int32_t owner[NUGPR_NUM_EVALS];
     RET(nugpr_shard_plan(ctx->world, cost, NUGPR_NUM_EVALS, owner));
     EvalRecord mine[NUGPR_NUM_EVALS];
     memset(mine, 0, sizeof(mine));
-    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
-      if (owner[k] != ctx->rank) continue;
-      nugpr_status st = run_eval(ctx, bl, y_dev, mk(pts[k]), scfg, &mine[k].o);
-      mine[k].status = st;
-      mine[k].valid = 1;
-      if (st != NUGPR_OK && st != NUGPR_ERR_CG_NOT_CONVERGED) return st;
-    }
+    std::vector<int> ks;                       // this rank's evaluations, most expensive first
+    for (int k : {1, 2, 3, 4, 5, 6, 0}) if (owner[k] == ctx->rank) ks.push_back(k);
+    RET(run_evals_concurrent(ctx, bl, y_dev, ks, tp, scfg, mine));
     EvalRecord all[NUGPR_NUM_EVALS];
     if (ctx->world > 1) {
       if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");

@@ -58,6 +58,8 @@ struct EvalParams {
   int32_t replay_iters[MAXC];
   int32_t ncol;
   int32_t mode;
+  const double* lam0_src;  // lambda_0(theta) for the record: device scalar, or NULL => lam0_val
+  double lam0_val;
 };
 
 // CG state for up to MAXC columns, updated only by "last CTA" finalisers.
@@ -124,7 +126,8 @@ struct ApplyPlan {
 
 struct LowrankArgs {
   const CGState* st;
-  const double* Mp;        // n_c x n_c row-major
+  const EvalParams* prm;   // if set, M' is read from prm->Mp (mode-independent graphs)
+  const double* Mp;        // n_c x n_c row-major (used when prm is NULL)
   const double* S;         // [n_tiles][16] S partials (tiles == clusters); fuse_p: S(R)
   double* SPbuf[2];        // fuse_p: S(P) ping-pong
   int fuse_p;
@@ -148,6 +151,7 @@ struct UpdateArgs {
   double* beta_hist;       // [MAXC][hist_stride]
   int hist_stride;
   int ncol;
+  unsigned long long cond; // cudaGraphConditionalHandle of the CG while-loop (0 = not in a graph)
 };
 
 struct RhsArgs {

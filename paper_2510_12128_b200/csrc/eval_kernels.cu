@@ -70,6 +70,39 @@ __device__ __forceinline__ int is_active(const EvalParams* P, int c, int iters, 
   return 1;
 }
 
+// Row r of the per-cluster lower triangular product c_i = Linv_i y_i (c = R^{-T} y):
+// one fixed summation order, shared by rhs_init and cy_kernel so both give the same bits.
+__device__ __forceinline__ double trmv_row(const double* Li, const double* ys, int ld, int r) {
+  double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
+  int k = 0;
+  for (; k + 3 <= r; k += 4) {
+    c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
+    c1 = fma(Li[static_cast<int64_t>(k + 1) * ld + r], ys[k + 1], c1);
+    c2 = fma(Li[static_cast<int64_t>(k + 2) * ld + r], ys[k + 2], c2);
+    c3 = fma(Li[static_cast<int64_t>(k + 3) * ld + r], ys[k + 3], c3);
+  }
+  for (; k <= r; ++k) c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
+  return (c0 + c1) + (c2 + c3);
+}
+
+// c = R^{-T} y for all clusters (padded layout, zero on padding rows), computed once per
+// numerical gradient and shared by its concurrent evaluations.
+__global__ void __launch_bounds__(NT) cy_kernel(LayoutDev L, const double* Linv, const double* y, double* cy) {
+  extern __shared__ double ys[];
+  const TileDesc td = L.tiles[blockIdx.x];
+  const int i = td.blk;
+  const int ld = L.ld[i];
+  const int64_t o = L.off[i], p0 = L.poff[i];
+  const int b = static_cast<int>(L.off[i + 1] - o);
+  for (int k = threadIdx.x; k < ld; k += NT) ys[k] = (k < b) ? y[o + k] : 0.0;
+  __syncthreads();
+  const double* Li = Linv + L.boff[i];
+  for (int rl = threadIdx.x; rl < td.nrows; rl += NT) {
+    const int r = td.row0 + rl;
+    cy[p0 + r] = (r < b) ? trmv_row(Li, ys, ld, r) : 0.0;
+  }
+}
+
 // ---------------------------------------------------------------------------------------
 // rhs_init: RHS col 0 = c = Linv y (per-cluster lower trmv), cols 1..m = probes z_j;
 // R = P_0 = RHS, X = 0; partials of r^T r and S(R); the last CTA initialises the CG state.
@@ -102,16 +135,7 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
     if (a.cy) {
       cval = a.cy[g];
     } else if (r < b) {
-      double c0 = 0.0, c1 = 0.0, c2 = 0.0, c3 = 0.0;
-      int k = 0;
-      for (; k + 3 <= r; k += 4) {
-        c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
-        c1 = fma(Li[static_cast<int64_t>(k + 1) * ld + r], ys[k + 1], c1);
-        c2 = fma(Li[static_cast<int64_t>(k + 2) * ld + r], ys[k + 2], c2);
-        c3 = fma(Li[static_cast<int64_t>(k + 3) * ld + r], ys[k + 3], c3);
-      }
-      for (; k <= r; ++k) c0 = fma(Li[static_cast<int64_t>(k) * ld + r], ys[k], c0);
-      cval = (c0 + c1) + (c2 + c3);
+      cval = trmv_row(Li, ys, ld, r);
     }
     if (a.cy_out) a.cy_out[g] = cval;
 #pragma unroll
@@ -525,7 +549,7 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
   __syncthreads();
   const int i = blockIdx.x * TROWS + wid;
   if (i >= n_c) return;
-  const double* Mrow = a.Mp + static_cast<int64_t>(i) * n_c;
+  const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
   double t[NCP];
 #pragma unroll
   for (int c = 0; c < NCP; ++c) t[c] = 0.0;
@@ -554,7 +578,11 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
 template <int NCP>
 __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
   CGState* st = a.st;
-  if (!st->any_active) return;
+  if (!st->any_active) {
+    // nothing left to do: end the graph's CG while-loop (no-op outside a graph)
+    if (a.cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0u);
+    return;
+  }
   __shared__ double sred[(NT / 32) * MAXC];
   __shared__ double outv[MAXC];
   __shared__ double cal[NCP], cact[NCP];
@@ -634,6 +662,7 @@ __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
       st->any_active = any;
       st->par = par ^ 1;
       st->ticket[FIN_UPDATE] = 0;
+      if (a.cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
     }
   }
 }
@@ -669,7 +698,6 @@ struct FinalArgs {
   int hist_stride;
   double* slq_work;          // [MAXC][3*hist_stride]
   const double* logdet_R;    // device scalar
-  const double* lam0;        // device scalar
   double n;
   int ncol;
   int logdet_mode;
@@ -719,7 +747,7 @@ __global__ void final_kernel(FinalArgs a) {
     o.logdet_slq = ldR + ssum / m;
     o.logdet = (a.logdet_mode == 1) ? o.logdet_slq : o.logdet_pade;
     o.L = 0.5 * (o.quad + o.logdet + a.n * 1.8378770664093453);   // n log(2 pi)
-    o.lambda0 = a.lam0[0];
+    o.lambda0 = a.prm->lam0_src ? a.prm->lam0_src[0] : a.prm->lam0_val;
     o.resid_y = sqrt(st->rr[0]);
     o.resid_q_max = rq;
     o.iters_y = st->iters[0];
@@ -850,6 +878,11 @@ void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
   note_launch(); post_launch("rhs_init_kernel");
 }
 
+void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s) {
+  cy_kernel<<<L.n_tiles, NT, sizeof(double) * ld_max, s>>>(L, Linv, y, cy);
+  note_launch(); post_launch("cy_kernel");
+}
+
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s) {
   spart_kernel<<<L.n_tiles, NT, 0, s>>>(L, u, V, ncol, part);
@@ -857,9 +890,9 @@ void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol
 }
 
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
-                  int stride, double* slq_work, const double* logdet_R, const double* lam0, double n,
+                  int stride, double* slq_work, const double* logdet_R, double n,
                   int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s) {
-  FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, lam0, n, ncol, logdet_mode, out};
+  FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, n, ncol, logdet_mode, out};
   final_kernel<<<1, 32, 0, s>>>(a);
   note_launch(); post_launch("final_kernel");
 }

@@ -45,10 +45,11 @@ void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s);
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
 void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
+void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s);
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s);
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
-                  int stride, double* slq_work, const double* logdet_R, const double* lam0, double n,
+                  int stride, double* slq_work, const double* logdet_R, double n,
                   int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
 

@@ -266,3 +266,47 @@ def test_jitter_ladder_matches_oracle(P, ctx):
     bo = OS.build_blocks(X, off, reps, th0)
     np.testing.assert_allclose(bg.export("jitter"), bo.jitter, rtol=1e-12)
     assert bo.jitter[0] > 0
+
+
+# ----------------------------------------------------------------------------- execution modes
+def test_graph_mode_equals_direct_launches_bitwise(P, ctx, monkeypatch):
+    """The CUDA-graph CG loop (conditional while node) runs the same kernels in the same order
+    as the direct-launch path: records are bit-identical in every operator mode."""
+    ds = synth.make_config("C2")
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
+    monkeypatch.setenv("NUGPR_NO_GRAPH", "1")
+    bd = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
+    monkeypatch.delenv("NUGPR_NO_GRAPH")
+    for which, th in perturbed(ds.theta0).items():
+        r1 = P.mll(ctx, bg, ds.y, th, probe_seed=202)
+        r2 = P.mll(ctx, bd, ds.y, th, probe_seed=202)
+        assert r1 == r2, which
+    rr = P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=202, replay=[3] * 9)
+    assert rr["iters_y"] == 3 and rr["iters_q"] == [3] * 8
+
+
+def test_concurrent_slots_equal_serial_bitwise_and_oracle(P, ctx):
+    """numgrad with 7 evaluation slots (7 concurrent streams) = 1 slot, bit for bit; and the
+    concurrent records match the oracle (C2)."""
+    ds = synth.make_config("C2")
+    b7 = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=7)
+    b1 = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=1)
+    L7, g7, e7 = P.numgrad(ctx, b7, ds.y, ds.theta0, probe_seed=202)
+    L1, g1, e1 = P.numgrad(ctx, b1, ds.y, ds.theta0, probe_seed=202)
+    assert e7 == e1 and L7 == L1 and np.array_equal(g7, g1)
+    bo = OS.build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    Z = synth.probes(202, 8, ds.n)
+    from oracle.mll import central_perturbations
+    for rec, th in zip(e7, central_perturbations(ds.theta0)[0]):
+        compare(rec, ds, bo, th, Z, free_check=False)
+
+
+def test_train_concurrent_C2_matches_oracle(P, ctx):
+    ds = synth.make_config("C2")
+    Z = synth.probes(202, 8, ds.n)
+    E = 2
+    st, rec = P.train(ctx, ds.X, ds.offsets, ds.reps, ds.y, ds.theta0, epochs=E, probe_seed=202, eval_slots=7)
+    sto, reco = oracle_train(ds.X, ds.offsets, ds.reps, ds.y, ds.theta0, Z, epochs=E)
+    np.testing.assert_allclose(st[:3], sto.theta, rtol=1e-6)
+    for e in range(E):
+        assert rel(rec[e, 0], reco[e]["L0"]) < 1e-9
