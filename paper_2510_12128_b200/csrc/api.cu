@@ -826,6 +826,9 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     a1.smem_b = pl.smem_b;
     a1.smem_nob = pl.smem_nob;
     a1.grid = pl.grid;
+    const char* dbg = getenv("NUGPR_APPLY_DBG");
+    a1.dbg = dbg ? atoi(dbg) : 0;
+    a1.mma = pl.mma;
   }
   ApplyArgs& a2 = A.a2;
   a2 = a1;

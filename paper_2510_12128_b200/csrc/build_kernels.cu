@@ -39,6 +39,11 @@ void smem_optin(const void* func) {
       if (e1 == cudaSuccess && e2 == cudaSuccess)
         e3 = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   optin - static_cast<int>(at.sharedSizeBytes));
+      // full shared-memory carveout: otherwise the driver may pick a smaller L1/smem split
+      // that admits fewer CTAs per SM than the launch plan assumes
+      if (e3 == cudaSuccess)
+        e3 = cudaFuncSetAttribute(func, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                  static_cast<int>(cudaSharedmemCarveoutMaxShared));
       if (e1 != cudaSuccess || e2 != cudaSuccess || e3 != cudaSuccess) {
         fprintf(stderr, "[nugpr] smem opt-in failed: optin=%d static=%zu (%s / %s / %s)\n", optin,
                 static_cast<size_t>(at.sharedSizeBytes), cudaGetErrorString(e1), cudaGetErrorString(e2),

@@ -20,7 +20,7 @@ namespace nugpr {
 constexpr int MAXC = 16;        // max columns per apply (1 + m)
 constexpr int NT = 256;         // threads per CTA for the tile kernels
 constexpr int TILE_ROWS = 512;  // max padded rows per tile (= whole clusters in this build)
-constexpr int MAX_NSTAGE = 6;   // max TMA ring depth of the apply kernel
+constexpr int MAX_NSTAGE = 16;  // max TMA ring depth of the apply kernel
 constexpr int SLOT_TARGET_DOUBLES = 4096;  // ~32 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
 
@@ -116,10 +116,12 @@ struct ApplyArgs {
   int nmine_max;           // max clusters per persistent CTA
   size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
   int grid;                // persistent grid size
+  int dbg;                 // timing experiments (NUGPR_APPLY_DBG); 0 in production
+  int mma;                 // 1: DMMA kernel (ncol == 9), 0: DFMA kernel
 };
 
 struct ApplyPlan {
-  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0;
+  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0;
   size_t smem_b = 0, smem_nob = 0;
   bool ok = false;
 };

@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
           const int s_ = static_cast<int>(seq % nstage);
           mbar_wait(&full[s_], (seq / nstage) & 1u);
           const double* cbuf = ring + s_ * slot;
-          if (act) {
+          if (act && !(a.dbg & 1)) {
             for (int kk = g; kk < kc; kk += KG) {
               double bv[RPT];
 #pragma unroll
@@ -429,7 +429,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
       double ep[NCP];
 #pragma unroll
       for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
-      if (act) {
+      if (act && !(a.dbg & 2)) {
         const double bi = P->b0 + P->b1 * a.jitter[i];
         const double pa = P->a, ms = P->mscale;
         const double* Tq = a.Tbuf + static_cast<int64_t>(i) * MAXC;
@@ -486,6 +486,292 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
         }
       }
       __syncthreads();
+      if (tid == 0) st->ticket[a.fin] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Fused apply on the FP64 tensor pipe (DMMA mma.sync m8n8k4) for the paper's batch shape
+// c = 1 + m = 9 columns (m = 8 probes).  Same contract as apply_kernel; the block
+// product B_i D_i is split as
+//   probe columns (8):  out_p[r, 0:8] += B_i[r, k:k+4] D_p[k:k+4, 0:8]   one m8n8k4 per 8 rows x 4 k
+//   y column (1):       out_y[r]      += B_i[r, k] y_k                     one DFMA per A fragment
+// so every issued FMA is useful (no column padding) and one DMMA replaces 8 DFMA instructions.
+// Persistent CTAs (clusters c, c+G, ...), warp NWM (the last) drives the TMA ring of B_i chunks;
+// the NWM consumer warps own the 8-row m-tiles mt = w, w + NWM, ... of the cluster and run over
+// every chunk column.  D_i (and P_new = R + beta o P_old for the fused first apply) is read from
+// L2/HBM once per cluster into shared memory: D_p as [k][LDP] with LDP = 12 (conflict-free
+// B-fragment loads), y as [k].
+constexpr int NWM = 7;                    // consumer warps of the DMMA apply (2 CTAs x 8 warps / SM)
+constexpr int NTM = (NWM + 1) * 32;       // + 1 TMA producer warp
+constexpr int LDP = 12;                   // row stride of the probe block in shared memory
+
+__device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void mma_sync_consumers() {
+  asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
+}
+
+template <int MTMAX>   // m-tiles per warp: 4 (ld <= 224), 8 (ld <= 448), 10 (ld <= 560)
+__global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
+  constexpr int EG = 2;                      // m-tiles per epilogue load group
+  constexpr int NCPE = 10;                 // epilogue column slots (9 used)
+  if (a.gate && !a.st->any_active) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
+  __shared__ double sred[NWM * NCPE];
+  __shared__ double Esm[NCPE];
+  __shared__ double cb[2 * NCPE];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int n_tiles = a.L.n_tiles;
+  const int64_t n_pad = a.L.n_pad;
+  const int ncol = a.ncol;                 // == 9
+  const EvalParams* P = a.prm;
+  const int par = a.st->par;
+  const double* B = P->B;
+  const bool useB = (B != nullptr);
+  const int slot = a.slot_doubles;
+  const int nstage = a.nstage;
+  const int G = gridDim.x;
+  double* ring = sm;                                         // nstage * slot (useB only)
+  double* Dp = ring + (useB ? nstage * slot : 0);            // ld_max * LDP
+  double* ys = Dp + a.ld_max * LDP;                          // ld_max
+  const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
+  double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+  if (tid == 0) {
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWM); }
+    fence_mbar_init();
+  }
+  if (tid < NCPE) {
+    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
+    cb[NCPE + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
+  }
+  __syncthreads();
+  if (wid == NWM) {
+    // ============================ TMA producer ============================
+    if (lane == 0 && useB) {
+      uint32_t pseq = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += G) {
+        const int i = a.L.tiles[t].blk;
+        const int ld = a.L.ld[i];
+        const int KC = max(4, (slot / ld) & ~3);
+        const double* Bi = B + a.L.boff[i];
+        for (int ck0 = 0; ck0 < ld; ck0 += KC, ++pseq) {
+          const int s_ = static_cast<int>(pseq % nstage);
+          const uint32_t use = pseq / nstage;
+          if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
+          const int kc = min(KC, ld - ck0);
+          const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[s_], bytes);
+          tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
+        }
+      }
+    }
+    return;
+  }
+  // ============================ consumers ============================
+  const int qr = lane >> 2, qc = lane & 3;   // fragment row / k (A), k / n (B) coordinates
+  uint32_t seq = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += G) {
+    const TileDesc td = a.L.tiles[t];
+    const int i = td.blk, ld = a.L.ld[i];
+    const int64_t p0 = a.L.poff[i];
+    const int mtt = ld >> 3;                               // m-tiles of the cluster
+    // 1. D_i -> shared (fused: D = R + beta o P_old for active columns, P_new written back);
+    //    loads batched 4 deep per thread so one cluster costs ~one memory round trip
+    if (a.dbg & 4) {
+      for (int idx = tid; idx < ld * 9; idx += NWM * 32) {
+        const int c = idx / ld, k = idx - c * ld;
+        const int64_t gi = c * n_pad + p0 + k;
+        double v = a.D[gi];
+        if (a.fuse_p) {
+          const double po = Pold[gi];
+          v = (cb[NCPE + c] != 0.0) ? v + cb[c] * po : po;
+          Pnew[gi] = v;
+        }
+        if (c == 0) ys[k] = v; else Dp[k * LDP + (c - 1)] = v;
+      }
+    } else {
+      const int tot = ld * 9;
+      constexpr int CU = 4;
+      for (int base = 0; base < tot; base += CU * NWM * 32) {
+        double v[CU], po[CU];
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int idx = base + u * NWM * 32 + tid;
+          v[u] = 0.0; po[u] = 0.0;
+          if (idx < tot) {
+            const int c = idx / ld, k = idx - c * ld;
+            const int64_t gi = c * n_pad + p0 + k;
+            v[u] = __ldg(a.D + gi);
+            if (a.fuse_p) po[u] = __ldg(Pold + gi);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < CU; ++u) {
+          const int idx = base + u * NWM * 32 + tid;
+          if (idx < tot) {
+            const int c = idx / ld, k = idx - c * ld;
+            double x = v[u];
+            if (a.fuse_p) {
+              x = (cb[NCPE + c] != 0.0) ? x + cb[c] * po[u] : po[u];
+              Pnew[c * n_pad + p0 + k] = x;
+            }
+            if (c == 0) ys[k] = x; else Dp[k * LDP + (c - 1)] = x;
+          }
+        }
+      }
+    }
+    mma_sync_consumers();
+    // 2. block term: DMMA over the ring chunks
+    double acc0[MTMAX], acc1[MTMAX], accy[MTMAX];
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; accy[j] = 0.0; }
+    if (useB) {
+      const int KC = max(4, (slot / ld) & ~3);
+      for (int k0 = 0; k0 < ld; k0 += KC, ++seq) {
+        const int kc = min(KC, ld - k0);
+        const int s_ = static_cast<int>(seq % nstage);
+        mbar_wait(&full[s_], (seq / nstage) & 1u);
+        const double* cbuf = ring + s_ * slot;
+        if (!(a.dbg & 1)) {
+          for (int kq = 0; kq < kc; kq += 4) {
+            const int k = k0 + kq + qc;                      // this lane's k in the cluster
+            const double bfr = Dp[k * LDP + qr];             // B fragment: D_p[k][n = qr]
+            const double yv = ys[k];
+            const double* acol = cbuf + (kq + qc) * ld + qr; // A fragment base: B_i[r][k]
+#pragma unroll
+            for (int j = 0; j < MTMAX; ++j) {
+              const int mt = wid + j * NWM;
+              if (mt < mtt) {
+                const double afr = acol[mt * 8];
+                dmma884(acc0[j], acc1[j], afr, bfr);
+                accy[j] = fma(afr, yv, accy[j]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s_]);
+      }
+    }
+    // y column: reduce the 4 k-lanes of each row quad
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j) {
+      accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 1);
+      accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 2);
+    }
+    // 3. epilogue: lane owns row r = 8 mt + qr, probe columns c = 1 + 2 qc + {0, 1}, and the y
+    //    column when qc == 0
+    double ep[NCPE];
+#pragma unroll
+    for (int c = 0; c < NCPE; ++c) ep[c] = 0.0;
+    if (!(a.dbg & 2)) {
+      const double bi = P->b0 + P->b1 * a.jitter[i];
+      const double pa = P->a, ms = P->mscale;
+      const double* Tq = a.Tbuf + static_cast<int64_t>(i) * MAXC;
+      const int c0 = 1 + 2 * qc;
+#pragma unroll
+      for (int jg = 0; jg < MTMAX; jg += EG) {
+        // load phase (all global reads of EG m-tiles in flight together), then compute
+        double uu[EG], p2v[EG][3], y2v[EG][3];
+#pragma unroll
+        for (int jj = 0; jj < EG; ++jj) {
+          const int mt = wid + (jg + jj) * NWM;
+          const bool on = mt < mtt;
+          const int r = mt * 8 + qr;
+          uu[jj] = on ? __ldg(a.u + p0 + r) : 0.0;
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            const int c = (e < 2) ? c0 + e : 0;
+            const int64_t gi = c * n_pad + p0 + r;
+            const bool le = on && (e < 2 || qc == 0);
+            p2v[jj][e] = (le && P2) ? P2[gi] : 0.0;
+            y2v[jj][e] = (le && a.epi != EPI_S) ? Y2[gi] : 0.0;
+          }
+        }
+#pragma unroll
+        for (int jj = 0; jj < EG; ++jj) {
+          const int j = jg + jj;
+          const int mt = wid + j * NWM;
+          if (mt < mtt) {
+            const int r = mt * 8 + qr;
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+              if (e == 2 && qc != 0) continue;
+              const int c = (e < 2) ? c0 + e : 0;
+              const double bd = (e == 0) ? acc0[j] : (e == 1) ? acc1[j] : accy[j];
+              const double d = (e < 2) ? Dp[r * LDP + c - 1] : ys[r];
+              const int64_t gi = c * n_pad + p0 + r;
+              double val = pa * d;
+              if (useB) val += bi * bd;
+              val += uu[jj] * (ms * Tq[c]);
+              double o = a.cA[c] * val + a.cV[c] * d;
+              if (P2) o += a.cP[c] * p2v[jj][e];
+              a.out[gi] = o;
+              const double y2 = (a.epi == EPI_S) ? uu[jj] : y2v[jj][e];
+              // ep[c] += o * y2 with a compile-time column index
+#pragma unroll
+              for (int cc = 0; cc < 9; ++cc)
+                if (cc == c) ep[cc] += o * y2;
+            }
+          }
+        }
+      }
+    }
+    // CTA-wide fixed-order column sums of ep over the consumer warps
+#pragma unroll
+    for (int c = 0; c < NCPE; ++c) ep[c] = warp_sum(ep[c]);
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < NCPE; ++c) sred[wid * NCPE + c] = ep[c];
+    }
+    mma_sync_consumers();
+    if (tid < ncol) {
+      double s = 0.0;
+      for (int w = 0; w < NWM; ++w) s += sred[w * NCPE + tid];
+      if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = s;
+      else a.dots[t * MAXC + tid] = s;
+    }
+    mma_sync_consumers();                                   // sred / Dp / ys reuse
+  }
+  // 4. finaliser (last CTA among the consumers; one warp per column)
+  if (a.fin != FIN_NONE) {
+    __shared__ int s_last;
+    __threadfence();
+    mma_sync_consumers();
+    if (tid == 0) {
+      const unsigned int tk = atomicAdd(&a.st->ticket[a.fin], 1u);
+      s_last = (tk == gridDim.x - 1);
+    }
+    mma_sync_consumers();
+    if (s_last) {
+      __threadfence();
+      CGState* st = a.st;
+      for (int c = wid; c < ncol; c += NWM) {
+        const double tot = col_total(a.dots, n_tiles, c);
+        if (lane == 0) {
+          if (a.fin == FIN_ALPHA) {
+            if (st->active[c]) {
+              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
+              st->alpha[c] = al;
+              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
+            }
+          } else {  // FIN_TRACE
+            if (c == 0) st->quad = tot; else st->t[c] = tot;
+          }
+        }
+      }
+      mma_sync_consumers();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
   }
@@ -782,6 +1068,14 @@ static int num_sms() {
 }
 
 // Shared-memory plan of the apply kernel (host side): ring depth chosen to fit.
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return (v && *v) ? atoi(v) : dflt;
+}
+
+// Shared-memory / grid plan of the apply (host side).  ncol == 9 (the paper's m = 8) uses the DMMA
+// kernel unless NUGPR_APPLY_MMA=0; the ring depth is chosen to fit; NUGPR_APPLY_{SLOT,PER,BAL}
+// are tuning knobs (slot doubles, max CTAs per SM, equal clusters per CTA).
 ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid_unused) {
   (void)ld_min;
   (void)grid_unused;
@@ -789,21 +1083,28 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
   cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t fixed = static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
-                       static_cast<size_t>(NWC) * ncp + 3 * ncp;
-  // prefer two CTAs per SM (one streams while the other runs its epilogue); fall back to one
-  for (int per = 2; per >= 1; --per) {
+  const bool mma = (ncol == 9) && env_int("NUGPR_APPLY_MMA", 1) != 0;
+  const size_t fixed = mma ? static_cast<size_t>(ld_max) * (LDP + 1)
+                           : static_cast<size_t>(2) * ncol * ld_max + static_cast<size_t>(ld_max) * ncp +
+                                 static_cast<size_t>(NWC) * ncp + 3 * ncp;
+  const size_t static_smem = 4096;   // static shared memory + the 1 KB per-CTA system reservation, with margin
+  const int slot_target = env_int("NUGPR_APPLY_SLOT", SLOT_TARGET_DOUBLES);
+  const int per_max = std::max(1, std::min(3, env_int("NUGPR_APPLY_PER", 2)));
+  const bool balance = env_int("NUGPR_APPLY_BAL", 1) != 0;
+  for (int per = per_max; per >= 1; --per) {
     ApplyPlan p;
-    const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - 2048;
+    p.mma = mma ? 1 : 0;
+    const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - static_smem;
     p.red_doubles = 0;
     p.ctas_per_sm = per;
     p.grid = std::min(n_tiles, per * num_sms());
     p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
-    p.slot_doubles = std::max(SLOT_TARGET_DOUBLES, ld_max);
+    if (balance) p.grid = (n_tiles + p.nmine_max - 1) / p.nmine_max;
+    p.slot_doubles = std::max(slot_target, mma ? 4 * ld_max : ld_max);
     long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
     p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
     if (p.nstage < 2) {
-      p.slot_doubles = ld_max;
+      p.slot_doubles = mma ? 4 * ld_max : ld_max;
       p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
     }
     p.smem_nob = fixed * sizeof(double);
@@ -825,6 +1126,21 @@ static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
 }
 
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
+  if (a.mma) {
+    size_t smem = useB ? a.smem_b : a.smem_nob;
+    if (a.ld_max <= 4 * NWM * 8) {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<4>));
+      apply_mma_kernel<4><<<a.grid, NTM, smem, s>>>(a);
+    } else if (a.ld_max <= 8 * NWM * 8) {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<8>));
+      apply_mma_kernel<8><<<a.grid, NTM, smem, s>>>(a);
+    } else {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<10>));
+      apply_mma_kernel<10><<<a.grid, NTM, smem, s>>>(a);
+    }
+    note_launch(); post_launch("apply_mma_kernel");
+    return;
+  }
   switch (ncp) {
     case 2: apply_launch_t<2>(a, useB, s); break;
     case 4: apply_launch_t<4>(a, useB, s); break;
