@@ -63,8 +63,8 @@ struct HostLayout {
   int64_t n = 0, n_pad = 0, blk_total = 0;
   int ld_max = 0;
   std::vector<int64_t> off, poff, boff;
-  std::vector<int32_t> ld, tile0;
-  std::vector<TileDesc> tiles;
+  std::vector<int32_t> ld, tile0, ctask0;
+  std::vector<TileDesc> tiles, ctasks;
 };
 
 nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) {
@@ -106,6 +106,20 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
   }
   L.poff[n_c] = pp;
   L.tile0[n_c] = static_cast<int32_t>(L.tiles.size());
+  // column tasks of the DMMA column apply: CTW columns (= rows of the symmetric block)
+  L.ctask0.resize(n_c + 1);
+  for (int i = 0; i < n_c; ++i) {
+    L.ctask0[i] = static_cast<int32_t>(L.ctasks.size());
+    for (int c0 = 0; c0 < L.ld[i]; c0 += CTW) {
+      TileDesc t;
+      t.blk = i;
+      t.row0 = c0;
+      t.nrows = std::min(CTW, L.ld[i] - c0);
+      t.pad_ = 0;
+      L.ctasks.push_back(t);
+    }
+  }
+  L.ctask0[n_c] = static_cast<int32_t>(L.ctasks.size());
   L.n = offsets[n_c];
   L.n_pad = pp;
   L.blk_total = bb;
@@ -148,8 +162,8 @@ struct EvalDev {
 
 struct BlocksDev {
   int64_t* off = nullptr, *poff = nullptr, *boff = nullptr;
-  int32_t* ld = nullptr, *tile0 = nullptr, *list = nullptr, *status = nullptr;
-  TileDesc* tiles = nullptr;
+  int32_t* ld = nullptr, *tile0 = nullptr, *list = nullptr, *status = nullptr, *ctask0 = nullptr;
+  TileDesc* tiles = nullptr, *ctasks = nullptr;
   double* X = nullptr, *reps = nullptr;
   double* Linv = nullptr, *H = nullptr;
   double* u = nullptr, *jitter = nullptr, *logdet_blk = nullptr;
@@ -174,6 +188,8 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.list = c.take<int32_t>(n_c);
   B.status = c.take<int32_t>(n_c);
   B.tiles = c.take<TileDesc>(nt);
+  B.ctasks = c.take<TileDesc>(L.ctasks.size());
+  B.ctask0 = c.take<int32_t>(n_c + 1);
   B.X = c.take<double>(static_cast<size_t>(L.n) * L.d);
   B.reps = c.take<double>(static_cast<size_t>(n_c) * L.d);
   B.Linv = c.take<double>(L.blk_total);
@@ -213,9 +229,10 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.SR = c.take<double>(nt * MAXC);
     e.SPb[0] = c.take<double>(nt * MAXC);
     e.SPb[1] = c.take<double>(nt * MAXC);
-    e.SV = c.take<double>(nt * MAXC);
+    const int64_t npart = std::max<int64_t>(nt, static_cast<int64_t>(L.ctasks.size()));   // per tile or per column task
+    e.SV = c.take<double>(npart * MAXC);
     e.SX = c.take<double>(nt * MAXC);
-    e.dots = c.take<double>(nt * MAXC);
+    e.dots = c.take<double>(npart * MAXC);
     e.rrp = c.take<double>(nt * MAXC);
     e.prm = c.take<EvalParams>(1);
     e.st = c.take<CGState>(1);
@@ -334,6 +351,7 @@ struct nugpr_blocks {
   bool cy_ready = false;      // B.cy holds c = R^{-T} y for the current numgrad call
   bool no_graph = false;      // NUGPR_NO_GRAPH=1: direct launches with host polling
   const void* ws_base = nullptr;
+  int iter_kernels = 5;       // kernels per CG iteration in the graph (launch accounting)
 };
 
 extern "C" {
@@ -486,6 +504,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   LayoutDev& Ld = bl->Ld;
   Ld.off = B.off; Ld.poff = B.poff; Ld.boff = B.boff; Ld.ld = B.ld; Ld.tiles = B.tiles;
   Ld.tile0 = B.tile0; Ld.n_c = n_c; Ld.n_tiles = static_cast<int32_t>(L.tiles.size());
+  Ld.ctasks = B.ctasks; Ld.ctask0 = B.ctask0; Ld.n_ctasks = static_cast<int32_t>(L.ctasks.size());
   Ld.n = L.n; Ld.n_pad = L.n_pad;
 #define CKB(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { delete bl; \
     return fail(NUGPR_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
@@ -495,6 +514,8 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * n_c, cudaMemcpyHostToDevice, s));
   CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
   CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.ctasks, L.ctasks.data(), sizeof(TileDesc) * L.ctasks.size(), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
   CKB(cudaMemcpyAsync(B.X, X_sorted, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
   CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
   CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * n_c, s));
@@ -801,6 +822,12 @@ struct IterArgs {
   LowrankArgs t1, t2, t3, t4;
   UpdateArgs ua;
   int ncp = 0;
+  bool pnew = false;       // launch pnew_kernel before apply 1
+  const CGState* st = nullptr;
+  const double* R = nullptr;
+  double* Pb[2] = {nullptr, nullptr};
+  int64_t n_pad = 0;
+  int ncol = 0;
 };
 
 static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterArgs& A) {
@@ -816,7 +843,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   a1.ld_max = L.ld_max;
   {
     const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
-    const ApplyPlan pl = plan_apply(A.ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles));
+    const ApplyPlan pl = plan_apply(A.ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles), Ld.n_ctasks);
     if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, ncol=%d)", L.ld_max, ncol);
     a1.slot_doubles = pl.slot_doubles;
     a1.red_doubles = pl.red_doubles;
@@ -829,6 +856,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     const char* dbg = getenv("NUGPR_APPLY_DBG");
     a1.dbg = dbg ? atoi(dbg) : 0;
     a1.mma = pl.mma;
+    a1.lds = pl.lds;
   }
   ApplyArgs& a2 = A.a2;
   a2 = a1;
@@ -852,6 +880,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol; ua.cond = 0;
   LowrankArgs& t1 = A.t1;
   memset(&t1, 0, sizeof(t1));
+  t1.task0 = nullptr;
   t1.st = e.st; t1.prm = e.prm; t1.Mp = nullptr; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
   t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
   LowrankArgs& t2 = A.t2;
@@ -876,12 +905,24 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   LowrankArgs& t4 = A.t4;
   t4 = t2;
   t4.S = e.SV; t4.gate = 0;
+  if (a1.mma == 3) {
+    // column-task apply: P_new is formed by pnew_kernel before apply 1; the apply outputs'
+    // S / dot partials are per column task
+    A.pnew = true;
+    A.a1.fuse_p = 0;
+    A.a1.d_is_pnew = 1;
+    A.t2.task0 = bl->B.ctask0;
+    A.t4.task0 = bl->B.ctask0;
+  }
+  bl->iter_kernels = A.pnew ? 6 : 5;
+  A.st = e.st; A.R = e.R; A.Pb[0] = e.Pb[0]; A.Pb[1] = e.Pb[1]; A.n_pad = L.n_pad; A.ncol = ncol;
   return NUGPR_OK;
 }
 
 // Direct launches of one CG iteration / the tail (useB selects the apply's smem variant).
 static void launch_iteration(const IterArgs& A, bool useB, cudaStream_t s) {
   launch_lowrank(A.t1, A.ncp, s);
+  if (A.pnew) launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s);
   launch_apply(A.a1, A.ncp, useB, s);
   launch_lowrank(A.t2, A.ncp, s);
   launch_apply(A.a2, A.ncp, useB, s);
@@ -1012,6 +1053,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
       PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
+      if (A.pnew) PROF(ctx, PC_UPDATE, 0.0, s, launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s));
       PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
       PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
       PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
@@ -1095,15 +1137,15 @@ static nugpr_status stage_y(nugpr_blocks* bl, const double* y, cudaStream_t s, c
 }
 
 // Kernel launches a finished graph-mode evaluation made (host counter for gpu_launches).
-static void account_graph_launches(const nugpr_mll_out& o) {
+static void account_graph_launches(const nugpr_blocks* bl, const nugpr_mll_out& o) {
   int k = o.iters_y;
   for (int j = 0; j < 16; ++j) k = std::max(k, o.iters_q[j]);
-  note_launch(5LL * std::max(1, k) + 6);
+  note_launch(static_cast<long long>(bl->iter_kernels) * std::max(1, k) + 6);
 }
 
 static nugpr_status finish_record(nugpr_blocks* bl, const nugpr_solve_cfg* cfg, const nugpr_mll_out& o,
                                   bool graph) {
-  if (graph) account_graph_launches(o);
+  if (graph) account_graph_launches(bl, o);
   bl->last_m = cfg->num_probes;
   bl->last_seed = cfg->probe_seed;
   if (!(o.lambda0 > 0.0)) return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", o.lambda0);

@@ -23,6 +23,7 @@ constexpr int TILE_ROWS = 512;  // max padded rows per tile (= whole clusters in
 constexpr int MAX_NSTAGE = 16;  // max TMA ring depth of the apply kernel
 constexpr int SLOT_TARGET_DOUBLES = 4096;  // ~32 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
+constexpr int CTW = 16;         // columns per task of the DMMA column apply
 
 struct TileDesc {
   int32_t blk;    // cluster index
@@ -38,8 +39,11 @@ struct LayoutDev {
   const int32_t* ld;     // [n_c] padded cluster size
   const TileDesc* tiles; // [n_tiles]
   const int32_t* tile0;  // [n_c+1] tile range of each cluster
+  const TileDesc* ctasks; // [n_ctasks] column tasks of the DMMA column apply: (cluster, col0, ncols)
+  const int32_t* ctask0; // [n_c+1] column-task range of each cluster
   int32_t n_c;
   int32_t n_tiles;
+  int32_t n_ctasks;
   int64_t n;             // unpadded rows
   int64_t n_pad;         // padded rows (vector column stride)
 };
@@ -117,16 +121,19 @@ struct ApplyArgs {
   size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
   int grid;                // persistent grid size
   int dbg;                 // timing experiments (NUGPR_APPLY_DBG); 0 in production
-  int mma;                 // 1: DMMA kernel (ncol == 9), 0: DFMA kernel
+  int mma;                 // 3: DMMA column-task kernel, 2: staged DMMA, 1: DMMA, 0: DFMA
+  int lds;                 // column-task kernel: padded column stride in shared memory
+  int d_is_pnew;           // column-task kernel: D := P_new = Pbuf[par^1] (formed by pnew_kernel)
 };
 
 struct ApplyPlan {
-  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0;
+  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0, lds = 0;
   size_t smem_b = 0, smem_nob = 0;
   bool ok = false;
 };
 
 struct LowrankArgs {
+  const int32_t* task0;    // NULL: S partials per cluster; else per column task, cluster j = [task0[j], task0[j+1])
   const CGState* st;
   const EvalParams* prm;   // if set, M' is read from prm->Mp (mode-independent graphs)
   const double* Mp;        // n_c x n_c row-major (used when prm is NULL)

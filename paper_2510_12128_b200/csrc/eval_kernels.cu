@@ -8,6 +8,7 @@
 // (S = W^T D, p^T q, r^T r, the trace dots) is written as per-tile partials and summed by
 // the last CTA to finish, in fixed tile order: results are bit-reproducible.
 #include <algorithm>
+#include <cstdio>
 
 #include <cooperative_groups.h>
 
@@ -564,6 +565,27 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         const int ld = a.L.ld[i];
         const int KC = max(4, (slot / ld) & ~3);
         const double* Bi = B + a.L.boff[i];
+        if (!(a.dbg & 32)) {
+          // warm L2 with this cluster's epilogue inputs and the next cluster's D inputs, so the
+          // consumers' plain loads there do not queue behind the B stream in DRAM
+          const int64_t p0 = a.L.poff[i];
+          const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
+          tma_prefetch_l2(a.u + p0, cb8);
+          for (int c = 0; c < ncol; ++c) {
+            if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cb8);
+            if (a.epi != EPI_S && Y2 != P2) tma_prefetch_l2(Y2 + c * n_pad + p0, cb8);
+          }
+          const int tn = t + G;
+          if (tn < n_tiles) {
+            const int in = a.L.tiles[tn].blk;
+            const int64_t pn = a.L.poff[in];
+            const uint32_t cbn = static_cast<uint32_t>(a.L.ld[in]) * 8u;
+            for (int c = 0; c < ncol; ++c) {
+              tma_prefetch_l2(a.D + c * n_pad + pn, cbn);
+              if (a.fuse_p) tma_prefetch_l2(Pold + c * n_pad + pn, cbn);
+            }
+          }
+        }
         for (int ck0 = 0; ck0 < ld; ck0 += KC, ++pseq) {
           const int s_ = static_cast<int>(pseq % nstage);
           const uint32_t use = pseq / nstage;
@@ -581,6 +603,17 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   // ============================ consumers ============================
   const int qr = lane >> 2, qc = lane & 3;   // fragment row / k (A), k / n (B) coordinates
   uint32_t seq = 0;
+  // (a.dbg & 16: per-CTA phase timestamps via printf, timing experiments only)
+  unsigned long long tsm[1 + 3 * 16];
+  int nts = 0;
+  auto stamp = [&]() {
+    if ((a.dbg & 16) && tid == 0 && nts < 1 + 3 * 16) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      tsm[nts++] = tt;
+    }
+  };
+  stamp();
   for (int t = blockIdx.x; t < n_tiles; t += G) {
     const TileDesc td = a.L.tiles[t];
     const int i = td.blk, ld = a.L.ld[i];
@@ -601,6 +634,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         if (c == 0) ys[k] = v; else Dp[k * LDP + (c - 1)] = v;
       }
     } else {
+      /* batched conversion below */
       const int tot = ld * 9;
       constexpr int CU = 4;
       for (int base = 0; base < tot; base += CU * NWM * 32) {
@@ -632,6 +666,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
       }
     }
     mma_sync_consumers();
+    stamp();
     // 2. block term: DMMA over the ring chunks
     double acc0[MTMAX], acc1[MTMAX], accy[MTMAX];
 #pragma unroll
@@ -664,6 +699,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         if (lane == 0) mbar_arrive(&empty[s_]);
       }
     }
+    stamp();
     // y column: reduce the 4 k-lanes of each row quad
 #pragma unroll
     for (int j = 0; j < MTMAX; ++j) {
@@ -743,6 +779,13 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
       else a.dots[t * MAXC + tid] = s;
     }
     mma_sync_consumers();                                   // sred / Dp / ys reuse
+    stamp();
+  }
+  if ((a.dbg & 16) && tid == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int k = 0; k < nts; ++k)
+      printf("T %d %u %d %llu\n", blockIdx.x, smid, k, tsm[k]);
   }
   // 4. finaliser (last CTA among the consumers; one warp per column)
   if (a.fin != FIN_NONE) {
@@ -778,6 +821,575 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Staged variant of the DMMA apply (1 CTA per SM): every per-cluster input is TMA-staged into
+// shared memory by the producer warp ahead of use, so the consumers' cluster prologue (forming
+// D_i) and epilogue run from shared memory instead of paying global-memory round trips that
+// queue behind the B stream.  Producer work per owned cluster q (polled, non-blocking):
+//   D(q): the 9 columns of D_i (+ the 9 of P_old when fused) -> stgD, after the consumers
+//         released stgD from cluster q-1 (dfree);
+//   E(q): u_i, the P2 and Y2 columns and the low-rank row T_i -> stgE, after the epilogue of
+//         cluster q-1 released stgE (efree);
+//   B(q): the KC-column chunks of B_i through the ring (full/empty barriers).
+// Tile metadata of the CTA's clusters is loaded once into shared memory.
+constexpr int MAXQ = 32;                  // clusters per CTA held in the metadata cache
+
+template <int MTMAX>
+__global__ void __launch_bounds__(NTM, 1) apply_mma_staged_kernel(ApplyArgs a) {
+  constexpr int NCPE = 10;
+  if (a.gate && !a.st->any_active) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t dbar, dfree, ebar, efree;
+  __shared__ double sred[NWM * NCPE];
+  __shared__ double cb[2 * NCPE];
+  __shared__ int q_ld[MAXQ];
+  __shared__ int64_t q_p0[MAXQ], q_boff[MAXQ];
+  __shared__ double q_bi[MAXQ];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int n_tiles = a.L.n_tiles;
+  const int64_t n_pad = a.L.n_pad;
+  const int ncol = a.ncol;                 // == 9
+  const EvalParams* P = a.prm;
+  const int par = a.st->par;
+  const double* B = P->B;
+  const bool useB = (B != nullptr);
+  const int slot = a.slot_doubles;
+  const int nstage = a.nstage;
+  const int G = gridDim.x;
+  const int ldm = a.ld_max;
+  const int nmine = (n_tiles - static_cast<int>(blockIdx.x) + G - 1) / G;
+  const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
+  double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+  const bool eY2 = (a.epi != EPI_S) && (Y2 != P2);          // Y2 needs its own staging
+  double* ring = sm;                                         // nstage * slot
+  double* stgD = ring + (useB ? nstage * slot : 0);          // 18 * ldm
+  double* stgE = stgD + 18 * ldm;                            // u | P2 (9) | Y2 (9) | T (16)
+  double* sT = stgE + 19 * ldm;
+  double* Dp = sT + 16;                                      // ldm * LDP
+  double* ys = Dp + ldm * LDP;                               // ldm
+  if (tid == 0) {
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWM); }
+    mbar_init(&dbar, 1); mbar_init(&dfree, 1); mbar_init(&ebar, 1); mbar_init(&efree, 1);
+    fence_mbar_init();
+  }
+  if (tid < NCPE) {
+    cb[tid] = (tid < ncol) ? a.st->beta[tid] : 0.0;
+    cb[NCPE + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
+  }
+  for (int q = tid; q < nmine; q += NTM) {
+    const int i = a.L.tiles[blockIdx.x + q * G].blk;
+    q_ld[q] = a.L.ld[i];
+    q_p0[q] = a.L.poff[i];
+    q_boff[q] = a.L.boff[i];
+    q_bi[q] = P->b0 + P->b1 * a.jitter[i];
+  }
+  __syncthreads();
+  if (wid == NWM) {
+    // ============================ TMA producer ============================
+    if (lane == 0) {
+      int qD = 0, qE = 0, qB = 0, ck0 = 0;
+      uint32_t pseq = 0;
+      while (qD < nmine || qE < nmine || qB < nmine) {
+        if (qD < nmine && qD <= qB + 1 && (qD == 0 || mbar_try_wait(&dfree, (qD - 1) & 1))) {
+          const int ld = q_ld[qD];
+          const int64_t p0 = q_p0[qD];
+          const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&dbar, cb8 * ncol * (a.fuse_p ? 2 : 1));
+          for (int c = 0; c < ncol; ++c) {
+            tma_load_1d(stgD + c * ld, a.D + c * n_pad + p0, cb8, &dbar);
+            if (a.fuse_p) tma_load_1d(stgD + (9 + c) * ld, Pold + c * n_pad + p0, cb8, &dbar);
+          }
+          ++qD;
+        }
+        if (qE < nmine && qE <= qB && (qE == 0 || mbar_try_wait(&efree, (qE - 1) & 1))) {
+          const int ld = q_ld[qE];
+          const int64_t p0 = q_p0[qE];
+          const int i = a.L.tiles[blockIdx.x + qE * G].blk;
+          const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
+          const uint32_t tot = cb8 * (1 + (P2 ? ncol : 0) + (eY2 ? ncol : 0)) + 16u * 8u;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&ebar, tot);
+          tma_load_1d(stgE, a.u + p0, cb8, &ebar);
+          for (int c = 0; c < ncol; ++c) {
+            if (P2) tma_load_1d(stgE + (1 + c) * ld, P2 + c * n_pad + p0, cb8, &ebar);
+            if (eY2) tma_load_1d(stgE + (10 + c) * ld, Y2 + c * n_pad + p0, cb8, &ebar);
+          }
+          tma_load_1d(sT, a.Tbuf + static_cast<int64_t>(i) * MAXC, 16u * 8u, &ebar);
+          ++qE;
+        }
+        if (qB < nmine && qB < qD) {
+          if (!useB) {
+            ++qB;
+          } else {
+            const int s_ = static_cast<int>(pseq % nstage);
+            const uint32_t use = pseq / nstage;
+            if (use == 0 || mbar_try_wait(&empty[s_], (use - 1) & 1u)) {
+              const int ld = q_ld[qB];
+              const int KC = max(4, (slot / ld) & ~3);
+              const int kc = min(KC, ld - ck0);
+              const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+              fence_proxy_async_smem();
+              mbar_arrive_expect_tx(&full[s_], bytes);
+              tma_load_1d(ring + s_ * slot, B + q_boff[qB] + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
+              ++pseq;
+              ck0 += KC;
+              if (ck0 >= ld) { ck0 = 0; ++qB; }
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+  // ============================ consumers ============================
+  const int qr = lane >> 2, qc = lane & 3;
+  uint32_t seq = 0;
+  unsigned long long tsm[1 + 3 * MAXQ];
+  int nts = 0;
+  auto stamp = [&]() {
+    if ((a.dbg & 16) && tid == 0 && nts < 1 + 3 * MAXQ) {
+      unsigned long long tt;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+      tsm[nts++] = tt;
+    }
+  };
+  stamp();
+  for (int q = 0; q < nmine; ++q) {
+    const int t = blockIdx.x + q * G;
+    const int ld = q_ld[q];
+    const int64_t p0 = q_p0[q];
+    const int mtt = ld >> 3;
+    // 1. D_i from stgD (fused: D = R + beta o P_old for active columns, P_new written back)
+    mbar_wait(&dbar, static_cast<uint32_t>(q & 1));
+    for (int idx = tid; idx < ld * 9; idx += NWM * 32) {
+      const int c = idx / ld, k = idx - c * ld;
+      double v = stgD[c * ld + k];
+      if (a.fuse_p) {
+        const double po = stgD[(9 + c) * ld + k];
+        v = (cb[NCPE + c] != 0.0) ? v + cb[c] * po : po;
+        Pnew[c * n_pad + p0 + k] = v;
+      }
+      if (c == 0) ys[k] = v; else Dp[k * LDP + (c - 1)] = v;
+    }
+    mma_sync_consumers();
+    stamp();
+    if (tid == 0) mbar_arrive(&dfree);
+    // 2. block term: DMMA over the ring chunks
+    double acc0[MTMAX], acc1[MTMAX], accy[MTMAX];
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; accy[j] = 0.0; }
+    if (useB) {
+      const int KC = max(4, (slot / ld) & ~3);
+      for (int k0 = 0; k0 < ld; k0 += KC, ++seq) {
+        const int kc = min(KC, ld - k0);
+        const int s_ = static_cast<int>(seq % nstage);
+        mbar_wait(&full[s_], (seq / nstage) & 1u);
+        const double* cbuf = ring + s_ * slot;
+        if (!(a.dbg & 1)) {
+          for (int kq = 0; kq < kc; kq += 4) {
+            const int k = k0 + kq + qc;
+            const double bfr = Dp[k * LDP + qr];
+            const double yv = ys[k];
+            const double* acol = cbuf + (kq + qc) * ld + qr;
+#pragma unroll
+            for (int j = 0; j < MTMAX; ++j) {
+              const int mt = wid + j * NWM;
+              if (mt < mtt) {
+                const double afr = acol[mt * 8];
+                dmma884(acc0[j], acc1[j], afr, bfr);
+                accy[j] = fma(afr, yv, accy[j]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s_]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j) {
+      accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 1);
+      accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 2);
+    }
+    stamp();
+    // 3. epilogue from shared memory
+    mbar_wait(&ebar, static_cast<uint32_t>(q & 1));
+    double ep[NCPE];
+#pragma unroll
+    for (int c = 0; c < NCPE; ++c) ep[c] = 0.0;
+    {
+      const double bi = q_bi[q];
+      const double pa = P->a, ms = P->mscale;
+      const double* su = stgE;
+      const double* sP2 = stgE + ld;                    // column c at sP2[c*ld]
+      const double* sY2 = eY2 ? stgE + 10 * ld : sP2;
+#pragma unroll
+      for (int j = 0; j < MTMAX; ++j) {
+        const int mt = wid + j * NWM;
+        if (mt < mtt) {
+          const int r = mt * 8 + qr;
+          const double uu = su[r];
+#pragma unroll
+          for (int e = 0; e < 3; ++e) {
+            if (e == 2 && qc != 0) continue;
+            const int c = (e < 2) ? 1 + 2 * qc + e : 0;
+            const double bd = (e == 0) ? acc0[j] : (e == 1) ? acc1[j] : accy[j];
+            const double d = (e < 2) ? Dp[r * LDP + c - 1] : ys[r];
+            double val = pa * d;
+            if (useB) val += bi * bd;
+            val += uu * (ms * sT[c]);
+            double o = a.cA[c] * val + a.cV[c] * d;
+            if (P2) o += a.cP[c] * sP2[c * ld + r];
+            a.out[c * n_pad + p0 + r] = o;
+            const double y2 = (a.epi == EPI_S) ? uu : sY2[c * ld + r];
+#pragma unroll
+            for (int cc = 0; cc < 9; ++cc)
+              if (cc == c) ep[cc] += o * y2;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NCPE; ++c) ep[c] = warp_sum(ep[c]);
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < NCPE; ++c) sred[wid * NCPE + c] = ep[c];
+    }
+    mma_sync_consumers();
+    if (tid < ncol) {
+      double s = 0.0;
+      for (int w = 0; w < NWM; ++w) s += sred[w * NCPE + tid];
+      if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = s;
+      else a.dots[t * MAXC + tid] = s;
+    }
+    mma_sync_consumers();                                   // sred / Dp / ys / stgE reuse
+    if (tid == 0) mbar_arrive(&efree);
+    stamp();
+  }
+  if ((a.dbg & 16) && tid == 0) {
+    unsigned int smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    for (int k = 0; k < nts; ++k)
+      printf("T %d %u %d %llu\n", blockIdx.x, smid, k, tsm[k]);
+  }
+  // 4. finaliser (last CTA among the consumers; one warp per column)
+  if (a.fin != FIN_NONE) {
+    __shared__ int s_last;
+    __threadfence();
+    mma_sync_consumers();
+    if (tid == 0) {
+      const unsigned int tk = atomicAdd(&a.st->ticket[a.fin], 1u);
+      s_last = (tk == gridDim.x - 1);
+    }
+    mma_sync_consumers();
+    if (s_last) {
+      __threadfence();
+      CGState* st = a.st;
+      for (int c = wid; c < ncol; c += NWM) {
+        const double tot = col_total(a.dots, n_tiles, c);
+        if (lane == 0) {
+          if (a.fin == FIN_ALPHA) {
+            if (st->active[c]) {
+              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
+              st->alpha[c] = al;
+              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
+            }
+          } else {  // FIN_TRACE
+            if (c == 0) st->quad = tot; else st->t[c] = tot;
+          }
+        }
+      }
+      mma_sync_consumers();
+      if (tid == 0) st->ticket[a.fin] = 0;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// DMMA apply over column tasks (c = 9, ld_max <= 256; the default for C1-C3).  B_i is symmetric
+// (H or G), so its columns [c0, c0+16) are also rows [c0, c0+16) and are CONTIGUOUS in the
+// column-major storage: a task = (cluster i, 16 output rows) streams 16 whole columns of B_i and
+// produces those rows of out completely.  Tasks (~13 per C3 cluster) are split evenly over one
+// persistent CTA per SM, so all SMs stream until the end (whole-cluster work units leave 15% of
+// the SMs idle at C3).  Warp NWM is the producer: per task it lands the 16 B columns (one bulk
+// copy each, padded row stride lds = ld (mod 16) + 4 so the A-fragment loads are bank-conflict
+// free) plus the task's epilogue inputs (u, P2, Y2 rows) in one ring slot; per cluster it lands
+// the 9 D columns, the low-rank row T_i and b_i in a D slot (3-deep ring).  Consumer warp w owns
+// the CTA's tasks w, w+NWM, ...; there is no CTA-wide barrier: each warp waits on its slot's
+// full barrier, runs the DMMAs, writes its rows and per-task partial sums, and releases the slot.
+constexpr int NDB = 3;                    // D-slot ring depth
+constexpr int MAXT = 96;                  // column tasks per CTA (metadata cache)
+
+template <int MT>   // m-tiles per task (CTW / 8)
+__global__ void __launch_bounds__(NTM, 1) apply_col_kernel(ApplyArgs a) {
+  constexpr int NCPE = 10;
+  if (a.gate && !a.st->any_active) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[MAX_NSTAGE], empty[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t dfull[NDB], dempty[NDB];
+  __shared__ int s_task[MAX_NSTAGE], s_qseq[MAX_NSTAGE];
+  __shared__ int d_ntask[NDB], d_cnt[NDB], d_ld[NDB], d_q[NDB];
+  __shared__ int64_t d_p0[NDB];
+  __shared__ double d_bi[NDB];
+  __shared__ int tk_blk[MAXT], tk_row0[MAXT], tk_nc[MAXT], tk_ld[MAXT];
+  __shared__ int64_t tk_p0[MAXT], tk_boff[MAXT];
+  __shared__ double tk_bi[MAXT];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int64_t n_pad = a.L.n_pad;
+  const int ncol = a.ncol;                 // == 9
+  const EvalParams* P = a.prm;
+  const int par = a.st->par;
+  const double* B = P->B;
+  const bool useB = (B != nullptr);
+  const int nstage = a.nstage;
+  const int lds = a.lds;
+  const int T = a.L.n_ctasks;
+  const int G = gridDim.x;
+  const int t0 = static_cast<int>((static_cast<int64_t>(T) * blockIdx.x) / G);
+  const int t1 = static_cast<int>((static_cast<int64_t>(T) * (blockIdx.x + 1)) / G);
+  const int nt = t1 - t0;
+  const double* D = a.d_is_pnew ? a.Pbuf[par ^ 1] : a.D;
+  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+  // slot layout (doubles): task slot = CTW columns of B_i at their natural stride ld (one bulk copy)
+  const int tslot = CTW * a.ld_max;
+  const int dslot = 9 * lds + 16;                              // 9 D columns | T_i (16)
+  double* ring = sm;
+  double* dring = ring + nstage * tslot;
+  if (tid == 0) {
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], 1); s_task[s_] = -1; }
+    for (int s_ = 0; s_ < NDB; ++s_) { mbar_init(&dfull[s_], 1); mbar_init(&dempty[s_], 1); d_cnt[s_] = 0; d_q[s_] = -1; }
+    fence_mbar_init();
+  }
+  // task metadata of this CTA, loaded once (the plan guarantees nt <= MAXT)
+  for (int j = tid; j < nt; j += NTM) {
+    const TileDesc td = a.L.ctasks[t0 + j];
+    tk_blk[j] = td.blk;
+    tk_row0[j] = td.row0;
+    tk_nc[j] = td.nrows;
+    tk_ld[j] = a.L.ld[td.blk];
+    tk_p0[j] = a.L.poff[td.blk];
+    tk_boff[j] = a.L.boff[td.blk];
+    tk_bi[j] = P->b0 + P->b1 * a.jitter[td.blk];
+  }
+  __syncthreads();
+  if (wid == NWM) {
+    // ============================ producer warp ============================
+    int qseq = -1, cur = -1;
+    for (int j = 0; j < nt; ++j) {
+      const int i = tk_blk[j];
+      const int ld = tk_ld[j];
+      const int64_t p0 = tk_p0[j];
+      const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
+      if (i != cur) {                                          // new cluster: D slot
+        cur = i;
+        ++qseq;
+        const int ds = qseq % NDB;
+        if (qseq >= NDB) mbar_wait(&dempty[ds], static_cast<uint32_t>((qseq / NDB - 1) & 1));
+        double* dst = dring + ds * dslot;
+        if (lane == 0) {
+          int cnt = 0;
+          for (int jj = j; jj < nt && tk_blk[jj] == i; ++jj) ++cnt;
+          d_ntask[ds] = cnt;
+          d_ld[ds] = ld;
+          d_p0[ds] = p0;
+          d_bi[ds] = tk_bi[j];
+          *reinterpret_cast<volatile int*>(&d_q[ds]) = qseq;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&dfull[ds], cb8 * 9u + 16u * 8u);
+        }
+        __syncwarp();
+        if (lane < 9) tma_load_1d(dst + lane * lds, D + lane * n_pad + p0, cb8, &dfull[ds]);
+        else if (lane == 9) tma_load_1d(dst + 9 * lds, a.Tbuf + static_cast<int64_t>(i) * MAXC, 16u * 8u, &dfull[ds]);
+      }
+      const int s_ = j % nstage;
+      if (j >= nstage) mbar_wait(&empty[s_], static_cast<uint32_t>((j / nstage - 1) & 1));
+      const int nc = tk_nc[j];
+      if (lane == 0) {
+        s_qseq[s_] = qseq;
+        *reinterpret_cast<volatile int*>(&s_task[s_]) = t0 + j;
+        if (useB) {
+          const uint32_t bytes = cb8 * static_cast<uint32_t>(nc);
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[s_], bytes);
+          tma_load_1d(ring + s_ * tslot, B + tk_boff[j] + static_cast<int64_t>(tk_row0[j]) * ld, bytes, &full[s_]);
+        } else {
+          mbar_arrive(&full[s_]);
+        }
+      }
+      __syncwarp();
+    }
+    return;
+  }
+  // ============================ consumer warps ============================
+  const int qr = lane >> 2, qc = lane & 3;
+  const double pa = P->a, ms = P->mscale;
+  for (int j = wid; j < nt; j += NWM) {
+    const int s_ = j % nstage;
+    // A warp's first use of a slot may be the slot's k-th: a parity wait is only meaningful once
+    // the producer has started that use (it publishes the task id first), else the "previous
+    // phase" of a fresh barrier would satisfy it.  Same for the D slots.
+    while (*reinterpret_cast<volatile int*>(&s_task[s_]) != t0 + j) __nanosleep(64);
+    mbar_wait(&full[s_], static_cast<uint32_t>((j / nstage) & 1));
+    const int gt = t0 + j;
+    const int qs = s_qseq[s_];
+    const int ds = qs % NDB;
+    while (*reinterpret_cast<volatile int*>(&d_q[ds]) != qs) __nanosleep(64);
+    mbar_wait(&dfull[ds], static_cast<uint32_t>((qs / NDB) & 1));
+    const double* tsl = ring + s_ * tslot;
+    const double* dsl = dring + ds * dslot;
+    const int ld = d_ld[ds];
+    const int64_t p0 = d_p0[ds];
+    TileDesc td;
+    td.blk = tk_blk[j]; td.row0 = tk_row0[j]; td.nrows = tk_nc[j];
+    const int nmt = td.nrows >> 3;
+    // epilogue inputs (global, issued now so their latency hides behind the DMMA loop)
+    double uu[MT], p2v[MT][3], y2v[MT][3];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const bool on = m < nmt;
+      const int r = td.row0 + m * 8 + qr;
+      uu[m] = on ? __ldg(a.u + p0 + r) : 0.0;
+#pragma unroll
+      for (int e = 0; e < 3; ++e) {
+        const int c = (e < 2) ? 1 + 2 * qc + e : 0;
+        const int64_t gi = c * n_pad + p0 + r;
+        const bool le = on && (e < 2 || qc == 0);
+        p2v[m][e] = (le && P2) ? P2[gi] : 0.0;
+        y2v[m][e] = (le && a.epi != EPI_S) ? Y2[gi] : 0.0;
+      }
+    }
+    double acc0[MT], acc1[MT], accy[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) { acc0[m] = 0.0; acc1[m] = 0.0; accy[m] = 0.0; }
+    if (useB && !(a.dbg & 1)) {
+      const double* bcol = dsl + (1 + qr) * lds + qc;           // B fragment: D[k][n = qr]
+      const double* ycol = dsl + qc;
+      const double* arow = tsl + qr * ld + qc;                  // A fragment: B_i[k][r = qr] (row r = column)
+#pragma unroll 4
+      for (int k0 = 0; k0 < ld; k0 += 4) {
+        const double bfr = bcol[k0];
+        const double yv = ycol[k0];
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+          if (m < nmt) {
+            const double afr = arow[m * 8 * ld + k0];
+            dmma884(acc0[m], acc1[m], afr, bfr);
+            accy[m] = fma(afr, yv, accy[m]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s_]);                     // B columns consumed: slot free
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      accy[m] += __shfl_xor_sync(0xffffffffu, accy[m], 1);
+      accy[m] += __shfl_xor_sync(0xffffffffu, accy[m], 2);
+    }
+    // epilogue: lane owns row m*8 + qr of the task, probe columns 1 + 2qc + {0,1}, y if qc == 0
+    double ep[NCPE];
+#pragma unroll
+    for (int c = 0; c < NCPE; ++c) ep[c] = 0.0;
+    const double bi = d_bi[ds];
+    const double* sT = dsl + 9 * lds;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      if (m < nmt) {
+        const int r = td.row0 + m * 8 + qr;                     // row within the cluster
+#pragma unroll
+        for (int e = 0; e < 3; ++e) {
+          if (e == 2 && qc != 0) continue;
+          const int c = (e < 2) ? 1 + 2 * qc + e : 0;
+          const double bd = (e == 0) ? acc0[m] : (e == 1) ? acc1[m] : accy[m];
+          const double d = dsl[c * lds + r];
+          double val = pa * d;
+          if (useB) val += bi * bd;
+          val += uu[m] * (ms * sT[c]);
+          double o = a.cA[c] * val + a.cV[c] * d;
+          if (P2) o += a.cP[c] * p2v[m][e];
+          a.out[c * n_pad + p0 + r] = o;
+          const double y2 = (a.epi == EPI_S) ? uu[m] : y2v[m][e];
+#pragma unroll
+          for (int cc = 0; cc < 9; ++cc)
+            if (cc == c) ep[cc] += o * y2;
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 9; ++c) ep[c] = warp_sum(ep[c]);
+    double* part = (a.epi == EPI_S) ? a.Sout : a.dots;
+    if (lane < 9) {
+      double v = 0.0;
+#pragma unroll
+      for (int c = 0; c < 9; ++c) if (c == lane) v = ep[c];
+      part[static_cast<int64_t>(gt) * MAXC + lane] = v;
+    }
+    __syncwarp();
+    if (lane == 0) {
+      if (atomicAdd(&d_cnt[ds], 1) + 1 == d_ntask[ds]) {        // last task of this cluster's D slot
+        d_cnt[ds] = 0;
+        mbar_arrive(&dempty[ds]);
+      }
+    }
+  }
+  // finaliser (last CTA; one warp per column)
+  if (a.fin != FIN_NONE) {
+    __shared__ int s_last;
+    __threadfence();
+    mma_sync_consumers();
+    if (tid == 0) {
+      const unsigned int tk = atomicAdd(&a.st->ticket[a.fin], 1u);
+      s_last = (tk == gridDim.x - 1);
+    }
+    mma_sync_consumers();
+    if (s_last) {
+      __threadfence();
+      CGState* st = a.st;
+      for (int c = wid; c < ncol; c += NWM) {
+        const double tot = col_total(a.dots, T, c);
+        if (lane == 0) {
+          if (a.fin == FIN_ALPHA) {
+            if (st->active[c]) {
+              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
+              st->alpha[c] = al;
+              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
+            }
+          } else {  // FIN_TRACE
+            if (c == 0) st->quad = tot; else st->t[c] = tot;
+          }
+        }
+      }
+      mma_sync_consumers();
+      if (tid == 0) st->ticket[a.fin] = 0;
+    }
+  }
+}
+
+// P_new = R + beta o P_old for the active columns (P_old kept for frozen ones): the fused
+// search-direction update of the first apply, run as its own pass for the column-task apply.
+__global__ void __launch_bounds__(NT) pnew_kernel(const CGState* st, const double* R, double* const* Pbuf_unused,
+                                                  const double* P0, const double* P1, double* Q0, double* Q1,
+                                                  int64_t n_pad, int ncol) {
+  (void)Pbuf_unused;
+  const int par = st->par;
+  const double* Pold = par ? P1 : P0;
+  double* Pnew = par ? Q0 : Q1;
+  const int64_t tot = n_pad * ncol;
+  for (int64_t g = blockIdx.x * static_cast<int64_t>(NT) + threadIdx.x; g < tot; g += static_cast<int64_t>(gridDim.x) * NT) {
+    const int c = static_cast<int>(g / n_pad);
+    const double po = Pold[g];
+    Pnew[g] = st->active[c] ? R[g] + st->beta[c] * po : po;
+  }
+}
+
+// ---------------------------------------------------------------------------------------
 // Low-rank coefficients T = M' S(D) (Eq. 19-21: block i of W M' W^T D is u_i T_i), one warp per
 // row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new) = S(R) +
 // beta o S(P_old) for the active columns (S is linear), and CTA 0 also stores S(P_new).
@@ -808,7 +1420,15 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
       for (int c2 = 0; c2 < NCP / 2; ++c2) {
         double2 x = make_double2(0.0, 0.0);
         if (j < n_c) {
-          x = *reinterpret_cast<const double2*>(a.S + j * MAXC + 2 * c2);
+          if (a.task0) {         // per-column-task partials of the cluster, summed in task order
+            for (int tk = a.task0[j]; tk < a.task0[j + 1]; ++tk) {
+              const double2 w = *reinterpret_cast<const double2*>(a.S + tk * MAXC + 2 * c2);
+              x.x += w.x;
+              x.y += w.y;
+            }
+          } else {
+            x = *reinterpret_cast<const double2*>(a.S + j * MAXC + 2 * c2);
+          }
           if (a.fuse_p) {
             const double2 y = *reinterpret_cast<const double2*>(SPo + j * MAXC + 2 * c2);
             x.x = (cb[NCP + 2 * c2] != 0.0) ? x.x + cb[2 * c2] * y.x : y.x;
@@ -1076,7 +1696,7 @@ static int env_int(const char* name, int dflt) {
 // Shared-memory / grid plan of the apply (host side).  ncol == 9 (the paper's m = 8) uses the DMMA
 // kernel unless NUGPR_APPLY_MMA=0; the ring depth is chosen to fit; NUGPR_APPLY_{SLOT,PER,BAL}
 // are tuning knobs (slot doubles, max CTAs per SM, equal clusters per CTA).
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid_unused) {
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid_unused, int n_ctasks) {
   (void)ld_min;
   (void)grid_unused;
   int dev = 0, optin = 0, per_sm = 0;
@@ -1091,6 +1711,41 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
   const int slot_target = env_int("NUGPR_APPLY_SLOT", SLOT_TARGET_DOUBLES);
   const int per_max = std::max(1, std::min(3, env_int("NUGPR_APPLY_PER", 2)));
   const bool balance = env_int("NUGPR_APPLY_BAL", 1) != 0;
+  const int col_mode = env_int("NUGPR_APPLY_COL", 0);     // experimental (slower at C3 so far)
+  if (mma && col_mode && ld_max <= 256) {
+    ApplyPlan p;
+    p.mma = 3;
+    p.lds = ld_max + ((4 - ld_max % 16) + 16) % 16;             // lds = 4 (mod 16)
+    const size_t tslot = static_cast<size_t>(CTW) * ld_max;
+    const size_t dslot = static_cast<size_t>(9) * p.lds + 16;
+    const size_t budget = static_cast<size_t>(optin) - 8192;
+    p.ctas_per_sm = 1;
+    p.grid = num_sms();
+    p.slot_doubles = static_cast<int>(tslot);
+    const long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(NDB * dslot);
+    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / static_cast<long>(tslot)));
+    p.smem_nob = p.smem_b = (NDB * dslot + static_cast<size_t>(std::max(p.nstage, 0)) * tslot) * sizeof(double);
+    p.ok = p.nstage >= 3 && (n_ctasks + p.grid - 1) / p.grid <= MAXT;
+    if (p.ok) return p;
+  }
+  const int stage_mode = env_int("NUGPR_APPLY_STAGE", 0); // experimental (no gain at C3 so far)
+  if (mma && stage_mode) {
+    ApplyPlan p;
+    p.mma = 2;
+    const size_t fixed_s = static_cast<size_t>(ld_max) * (18 + 19 + LDP + 1) + 16;
+    const size_t budget = static_cast<size_t>(optin) - 8192;
+    p.ctas_per_sm = 1;
+    p.grid = std::min(n_tiles, num_sms());
+    p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
+    if (balance) p.grid = (n_tiles + p.nmine_max - 1) / p.nmine_max;
+    p.slot_doubles = std::max(slot_target, 4 * ld_max);
+    const long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed_s);
+    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+    p.smem_nob = fixed_s * sizeof(double);
+    p.smem_b = (fixed_s + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
+    p.ok = p.nstage >= 3 && p.nmine_max <= MAXQ;
+    if (p.ok) return p;
+  }
   for (int per = per_max; per >= 1; --per) {
     ApplyPlan p;
     p.mma = mma ? 1 : 0;
@@ -1126,6 +1781,28 @@ static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
 }
 
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
+  if (a.mma == 3) {
+    size_t smem = a.smem_b;
+    smem_optin(reinterpret_cast<const void*>(apply_col_kernel<CTW / 8>));
+    apply_col_kernel<CTW / 8><<<a.grid, NTM, smem, s>>>(a);
+    note_launch(); post_launch("apply_col_kernel");
+    return;
+  }
+  if (a.mma == 2) {
+    size_t smem = useB ? a.smem_b : a.smem_nob;
+    if (a.ld_max <= 4 * NWM * 8) {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_staged_kernel<4>));
+      apply_mma_staged_kernel<4><<<a.grid, NTM, smem, s>>>(a);
+    } else if (a.ld_max <= 8 * NWM * 8) {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_staged_kernel<8>));
+      apply_mma_staged_kernel<8><<<a.grid, NTM, smem, s>>>(a);
+    } else {
+      smem_optin(reinterpret_cast<const void*>(apply_mma_staged_kernel<10>));
+      apply_mma_staged_kernel<10><<<a.grid, NTM, smem, s>>>(a);
+    }
+    note_launch(); post_launch("apply_mma_staged_kernel");
+    return;
+  }
   if (a.mma) {
     size_t smem = useB ? a.smem_b : a.smem_nob;
     if (a.ld_max <= 4 * NWM * 8) {
@@ -1197,6 +1874,13 @@ void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s) {
   cy_kernel<<<L.n_tiles, NT, sizeof(double) * ld_max, s>>>(L, Linv, y, cy);
   note_launch(); post_launch("cy_kernel");
+}
+
+void launch_pnew(const CGState* st, const double* R, double* const* Pbuf, int64_t n_pad, int ncol, cudaStream_t s) {
+  const int64_t tot = n_pad * ncol;
+  const int grid = static_cast<int>(std::min<int64_t>((tot + NT - 1) / NT, 4 * num_sms()));
+  pnew_kernel<<<grid, NT, 0, s>>>(st, R, nullptr, Pbuf[0], Pbuf[1], Pbuf[0], Pbuf[1], n_pad, ncol);
+  note_launch(); post_launch("pnew_kernel");
 }
 
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,

@@ -39,13 +39,14 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
                     cudaStream_t s);
 
 // eval_kernels.cu
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid);
+ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid, int n_ctasks);
 int apply_grid(int n_tiles);
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s);
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
 void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s);
+void launch_pnew(const CGState* st, const double* R, double* const* Pbuf, int64_t n_pad, int ncol, cudaStream_t s);
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s);
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
