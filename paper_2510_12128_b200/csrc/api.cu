@@ -277,12 +277,23 @@ struct nugpr_ctx {
   cudaStream_t capture_stream = nullptr;
   cudaStream_t slot_stream[NUGPR_NUM_EVALS] = {nullptr};
   cudaEvent_t ev_fork = nullptr, ev_join[NUGPR_NUM_EVALS] = {nullptr};
+  // side streams for independent work inside one slot / the build (lambda_0 Lanczos next to the
+  // block factorisation or the G precompute): index NUGPR_NUM_EVALS is the build's
+  cudaStream_t aux_stream[NUGPR_NUM_EVALS + 1] = {nullptr};
+  cudaEvent_t ev_aux[NUGPR_NUM_EVALS + 1][2] = {{nullptr}};
   EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
   // instantiated CG graphs keyed by (workspace, layout, slot, ncol, logdet mode)
   std::unordered_map<std::string, cudaGraphExec_t> graphs;
   std::vector<cudaGraph_t> graph_defs;
 };
 constexpr int MAX_STAGE = 64;
+
+static nugpr_status ensure_aux(nugpr_ctx* c, int k) {
+  if (!c->aux_stream[k]) CK(cudaStreamCreateWithFlags(&c->aux_stream[k], cudaStreamNonBlocking));
+  for (int e = 0; e < 2; ++e)
+    if (!c->ev_aux[k][e]) CK(cudaEventCreateWithFlags(&c->ev_aux[k][e], cudaEventDisableTiming));
+  return NUGPR_OK;
+}
 
 static nugpr_status ensure_slot_streams(nugpr_ctx* c, int slots) {
   for (int k = 0; k < slots && k < NUGPR_NUM_EVALS; ++k) {
@@ -416,6 +427,10 @@ nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
     if (ctx->ev_join[k]) cudaEventDestroy(ctx->ev_join[k]);
   }
   if (ctx->ev_fork) cudaEventDestroy(ctx->ev_fork);
+  for (int k = 0; k <= NUGPR_NUM_EVALS; ++k) {
+    if (ctx->aux_stream[k]) cudaStreamDestroy(ctx->aux_stream[k]);
+    for (int e = 0; e < 2; ++e) if (ctx->ev_aux[k][e]) cudaEventDestroy(ctx->ev_aux[k][e]);
+  }
   if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
@@ -525,6 +540,24 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     CKB(cudaMemsetAsync(ev.st, 0, sizeof(CGState), s));
   }
   CKB(cudaMemsetAsync(B.u, 0, sizeof(double) * L.n_pad, s));
+  // K_rep(theta0), lambda_0, v_0, M depend on the representatives only: side stream, overlapped
+  // with the block factorisation below
+  {
+    nugpr_status as_ = ensure_aux(ctx, NUGPR_NUM_EVALS);
+    if (as_ != NUGPR_OK) { delete bl; return as_; }
+  }
+  cudaStream_t bas = ctx->prof ? s : ctx->aux_stream[NUGPR_NUM_EVALS];
+  if (bas != s) {
+    CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][0], s));
+    CKB(cudaStreamWaitEvent(bas, ctx->ev_aux[NUGPR_NUM_EVALS][0], 0));
+  }
+  launch_krep(B.reps, n_c, d, kernel, theta0.lengthscale, theta0.outputscale, B.Krep, bas);
+  {
+    nugpr_status ls;
+    PROF(ctx, PC_LANCZOS, 0.0, bas, ls = enqueue_lambda0(bl, B.Krep, nullptr, B.lz, B.scal + 1, B.v0, B.M, B.linfo, bas));
+    if (ls != NUGPR_OK) { delete bl; return ls; }
+  }
+  if (bas != s) CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][1], bas));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
   PROF(ctx, PC_OTHER, 0.0, s,
        launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
@@ -543,6 +576,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     if (t == 5) {
       int fb = bl->h_list[0];
       if (failed_block) *failed_block = fb;
+      cudaStreamSynchronize(bas);           // the side stream still writes into the workspace
       delete bl;
       return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
     }
@@ -558,14 +592,11 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     CKB(cudaStreamSynchronize(s));
   }
   for (double j : bl->h_jitter) bl->max_jitter = std::max(bl->max_jitter, j);
-  // H_i = Linv_i Linv_i^T ; logdet_R ; K_rep, lambda_0, M
+  // H_i = Linv_i Linv_i^T ; logdet_R (K_rep, lambda_0, M were launched on the side stream)
   PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
   launch_sum(B.logdet_blk, n_c, B.scal + 0, s);
-  launch_krep(B.reps, n_c, d, kernel, theta0.lengthscale, theta0.outputscale, B.Krep, s);
   CKB(cudaGetLastError());
-  nugpr_status ls;
-  PROF(ctx, PC_LANCZOS, 0.0, s, ls = enqueue_lambda0(bl, B.Krep, nullptr, B.lz, B.scal + 1, B.v0, B.M, B.linfo, s));
-  if (ls != NUGPR_OK) { delete bl; return ls; }
+  if (bas != s) CKB(cudaStreamWaitEvent(s, ctx->ev_aux[NUGPR_NUM_EVALS][1], 0));
   double hs[2];
   CKB(cudaMemcpyAsync(hs, B.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
@@ -996,16 +1027,27 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   } else {                                                // generic (lengthscale step)
     mode = NUGPR_MODE_GENERIC;
     P.a = 0.0; P.b0 = 1.0; P.b1 = 0.0; P.B = e.G; P.Mp = e.M;
+    // K_rep(theta') and its lambda_0 (latency-bound Lanczos) run on a side stream while this
+    // stream assembles K_i(lambda') and forms G (FP64 tensor-pipe GEMMs)
+    RET(ensure_aux(ctx, slot));
+    cudaStream_t as = ctx->prof ? s : ctx->aux_stream[slot];
+    if (as != s) {
+      CK(cudaEventRecord(ctx->ev_aux[slot][0], s));
+      CK(cudaStreamWaitEvent(as, ctx->ev_aux[slot][0], 0));
+    }
+    launch_krep(B.reps, L.n_c, L.d, bl->kind, th.lengthscale, th.outputscale, e.Krep, as);
+    CKL();
+    nugpr_status ls;
+    PROF(ctx, PC_LANCZOS, 0.0, as, ls = enqueue_lambda0(bl, e.Krep, B.v0, e.lz, e.scal, e.v0, e.M, e.linfo, as));
+    RET(ls);
+    if (as != s) CK(cudaEventRecord(ctx->ev_aux[slot][1], as));
     PROF(ctx, PC_OTHER, 0.0, s,
          launch_assemble(B.X, L.d, Ld, nullptr, 0, L.ld_max, B.jitter, e.G, bl->kind, th.lengthscale,
                          th.noise, th.outputscale, s));
     PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_KLt(e.G, B.Linv, e.T, Ld, L.ld_max, s));
     PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_LT(B.Linv, e.T, e.G, Ld, L.ld_max, s));
-    launch_krep(B.reps, L.n_c, L.d, bl->kind, th.lengthscale, th.outputscale, e.Krep, s);
     CKL();
-    nugpr_status ls;
-    PROF(ctx, PC_LANCZOS, 0.0, s, ls = enqueue_lambda0(bl, e.Krep, B.v0, e.lz, e.scal, e.v0, e.M, e.linfo, s));
-    RET(ls);
+    if (as != s) CK(cudaStreamWaitEvent(s, ctx->ev_aux[slot][1], 0));
     lam0_ptr = e.scal;
   }
   P.mode = mode;

@@ -453,11 +453,148 @@ __global__ void __launch_bounds__(256) gemm_blocks_kernel(GemmArgs g) {
     }
 }
 
+// DMMA (mma.sync m8n8k4 f64) version of the batched block GEMM: same contract as
+// gemm_blocks_kernel.  64x64 CTA tile, 8 warps as 2 (rows) x 4 (cols), warp tile 32x16 =
+// 4 x 2 m8n8 tiles; K staged 16 at a time in shared memory (k-major, row stride 68 = 4 mod 16
+// so the fragment loads are bank-conflict free), register double buffering of the next stage.
+// 8x8 sub-tiles entirely outside the block (ld is a multiple of 8) are skipped.
+constexpr int GLD = 68;
+
+__device__ __forceinline__ void dmma884g(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM>
+__global__ void __launch_bounds__(256) gemm_dmma_kernel(GemmArgs g) {
+  const int i = blockIdx.y;
+  const int ld = g.ld[i];
+  const int nt = (ld + 63) / 64;
+  int tr, tc;
+  if (SYM) {
+    int t = blockIdx.x;
+    if (t >= nt * (nt + 1) / 2) return;
+    tr = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (tr * (tr + 1) / 2 > t) --tr;
+    while ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
+    tc = t - tr * (tr + 1) / 2;
+  } else {
+    if (static_cast<int>(blockIdx.x) >= nt * nt) return;
+    tr = blockIdx.x % nt;
+    tc = blockIdx.x / nt;
+  }
+  const int64_t bo = g.boff[i];
+  const double* A = g.A + bo;
+  const double* B = g.B + bo;
+  double* C = g.C + bo;
+  const int r0 = tr * 64, c0 = tc * 64;
+  int kend = ld;
+  if (A_LOWER) kend = min(kend, r0 + 64);
+  if (B_LOWERT) kend = min(kend, c0 + 64);
+  __shared__ __align__(16) double As[2][16 * GLD];
+  __shared__ __align__(16) double Bs[2][16 * GLD];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int wm = wid & 1, wn = wid >> 1;
+  const int qr = lane >> 2, qc = lane & 3;
+  // global -> register staging: 4 A and 4 B values per thread per stage
+  double ra[4], rb[4];
+  auto gload = [&](int k0) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + u * 256;
+      {
+        const int kk = idx >> 6, rr = idx & 63;
+        const int r = r0 + rr, k = k0 + kk;
+        ra[u] = (r < ld && k < ld) ? A[static_cast<int64_t>(k) * ld + r] : 0.0;
+      }
+      {
+        int kk, cc;
+        if (TRANSB) { kk = idx >> 6; cc = idx & 63; }
+        else        { cc = idx >> 4; kk = idx & 15; }
+        const int c = c0 + cc, k = k0 + kk;
+        double v = 0.0;
+        if (c < ld && k < ld) v = TRANSB ? B[static_cast<int64_t>(k) * ld + c] : B[static_cast<int64_t>(c) * ld + k];
+        rb[u] = v;
+      }
+    }
+  };
+  auto sstore = [&](int buf) {
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int idx = tid + u * 256;
+      As[buf][(idx >> 6) * GLD + (idx & 63)] = ra[u];
+      if (TRANSB) Bs[buf][(idx >> 6) * GLD + (idx & 63)] = rb[u];
+      else        Bs[buf][(idx & 15) * GLD + (idx >> 4)] = rb[u];
+    }
+  };
+  double acc[4][2][2];
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n) { acc[m][n][0] = 0.0; acc[m][n][1] = 0.0; }
+  // which 8x8 sub-tiles of this warp lie inside the block
+  const int wr = r0 + wm * 32, wc = c0 + wn * 16;
+  const int mval = max(0, min(4, (ld - wr) >> 3));
+  const int nval = max(0, min(2, (ld - wc) >> 3));
+  if (kend > 0) {
+    gload(0);
+    sstore(0);
+    __syncthreads();
+    int buf = 0;
+    for (int k0 = 0; k0 < kend; k0 += 16) {
+      const bool more = k0 + 16 < kend;
+      if (more) gload(k0 + 16);
+      const double* as = As[buf];
+      const double* bs = Bs[buf];
+#pragma unroll
+      for (int k4 = 0; k4 < 16; k4 += 4) {
+        double af[4], bf[2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) af[m] = as[(k4 + qc) * GLD + wm * 32 + m * 8 + qr];
+#pragma unroll
+        for (int n = 0; n < 2; ++n) bf[n] = bs[(k4 + qc) * GLD + wn * 16 + n * 8 + qr];
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int n = 0; n < 2; ++n)
+            if (m < mval && n < nval) dmma884g(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
+      }
+      if (more) {
+        sstore(buf ^ 1);
+        __syncthreads();
+        buf ^= 1;
+      }
+    }
+  }
+  // C fragment: row qr, columns 2qc, 2qc+1 of each 8x8 tile
+#pragma unroll
+  for (int m = 0; m < 4; ++m)
+#pragma unroll
+    for (int n = 0; n < 2; ++n) {
+      if (m >= mval || n >= nval) continue;
+      const int r = wr + m * 8 + qr;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int c = wc + n * 8 + 2 * qc + e;
+        const double v = acc[m][n][e];
+        if (SYM) {
+          if (r >= c) {
+            C[static_cast<int64_t>(c) * ld + r] = v;
+            C[static_cast<int64_t>(r) * ld + c] = v;
+          }
+        } else {
+          C[static_cast<int64_t>(c) * ld + r] = v;
+        }
+      }
+    }
+}
+
 // H = Linv * Linv^T (symmetric)
 void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
   GemmArgs g{Linv, Linv, H, L.boff, L.ld, nt};
-  gemm_blocks_kernel<true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  gemm_dmma_kernel<true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_H");
 }
 // T = K * Linv^T
@@ -465,7 +602,7 @@ void launch_gemm_KLt(const double* K, const double* Linv, double* T, const Layou
                      cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
   GemmArgs g{K, Linv, T, L.boff, L.ld, nt};
-  gemm_blocks_kernel<true, false, true, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
+  gemm_dmma_kernel<true, false, true, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_KLt");
 }
 // G = Linv * T (symmetric)
@@ -473,7 +610,7 @@ void launch_gemm_LT(const double* Linv, const double* T, double* G, const Layout
                     cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
   GemmArgs g{Linv, T, G, L.boff, L.ld, nt};
-  gemm_blocks_kernel<false, true, false, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  gemm_dmma_kernel<false, true, false, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_LT");
 }
 
