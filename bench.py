@@ -280,6 +280,27 @@ def run_ours(args):
         t = torch.tensor([ms_e2e], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_e2e = float(t.item())
+    # phase split of one epoch in production mode: the build alone, then the numerical gradient
+    phase = {}
+    try:
+        th0 = tuple(float(t) for t in ds.theta0)
+        reps_ph = 3
+        e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0p.record(stream)
+        for _ in range(reps_ph):
+            blk = P.build_blocks(ctx, Xd, ds.offsets, rd, th0, workspace=ws, eval_slots=args.eval_slots)
+        e1p.record(stream)
+        torch.cuda.synchronize()
+        phase["build_ms"] = e0p.elapsed_time(e1p) / reps_ph
+        e0p.record(stream)
+        for _ in range(reps_ph):
+            P.numgrad(ctx, blk, yd, th0, probe_seed=seed, num_probes=8)
+        e1p.record(stream)
+        torch.cuda.synchronize()
+        phase["numgrad_ms"] = e0p.elapsed_time(e1p) / reps_ph
+        blk.close()
+    except Exception as ex:  # noqa: BLE001
+        phase["error"] = str(ex)[:200]
     # roofline pass: the same steps with per-kernel CUDA events (direct, serialised launches on
     # the context stream — events cannot bracket kernels inside a graph), after the timed region
     ctx.set_profiling(True)
@@ -324,6 +345,7 @@ def run_ours(args):
             "dense_n2_f64_gb": 8.0 * ds.n * ds.n / 1e9,
             "cg_iters_y_max": max(kys), "cg_iters_q_max": max(kqs),
             "eval_slots": args.eval_slots,
+            "phase_ms": phase,
         },
         "clocks": clk,
         "gpu_launches": int(launches),

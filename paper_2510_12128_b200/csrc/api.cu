@@ -559,10 +559,17 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   }
   if (bas != s) CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][1], bas));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
-  PROF(ctx, PC_OTHER, 0.0, s,
-       launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
-                       theta0.noise, theta0.outputscale, s));
-  PROF(ctx, PC_CHOL, 0.0, s, launch_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, s));
+  const bool fused_chol = chol_fused_ok(L.ld_max);
+  if (fused_chol) {
+    PROF(ctx, PC_CHOL, 0.0, s,
+         launch_chol_fused(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
+                           theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s));
+  } else {
+    PROF(ctx, PC_OTHER, 0.0, s,
+         launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
+                         theta0.noise, theta0.outputscale, s));
+    PROF(ctx, PC_CHOL, 0.0, s, launch_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, s));
+  }
   CKB(cudaGetLastError());
   std::vector<int32_t> hstat(n_c);
   CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
@@ -583,10 +590,15 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     for (int i : bl->h_list) bl->h_jitter[i] = base * std::pow(10.0, t);
     CKB(cudaMemcpyAsync(B.jitter, bl->h_jitter.data(), sizeof(double) * n_c, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(B.list, bl->h_list.data(), sizeof(int32_t) * bl->h_list.size(), cudaMemcpyHostToDevice, s));
-    launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
-                    kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
-    launch_chol_trtri(B.Linv, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.status,
-                      B.logdet_blk, B.u, s);
+    if (fused_chol) {
+      launch_chol_fused(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
+                        kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s);
+    } else {
+      launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
+                      kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
+      launch_chol_trtri(B.Linv, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.status,
+                        B.logdet_blk, B.u, s);
+    }
     CKB(cudaGetLastError());
     CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
     CKB(cudaStreamSynchronize(s));

@@ -339,6 +339,233 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Shared-memory-resident variant for ld <= CS_LDMAX (C1-C3): the packed lower triangle of the
+// block lives in shared memory for the whole factorisation (ld = 200: 161 KB), K_i is
+// assembled straight into it from X (the same distance / kernel arithmetic as
+// assemble_kernel, so the blocks are bit-identical), then: blocked right-looking Cholesky
+// (16-column panels, column steps by all threads, 4x4 register-tiled trailing update),
+// logdet, in-place triangular inverse by 16-row panels, and one coalesced write of Linv
+// (zero upper triangle) plus u = Linv 1.  Global memory is touched once in and once out.
+constexpr int CS_NT = 512;
+constexpr int CS_NB = 16;
+constexpr int CS_YC = 32;
+constexpr int CS_LDMAX = 224;
+
+__device__ __forceinline__ int cofs(int c, int ld) { return c * ld - (c * (c - 1)) / 2; }
+
+struct CholSmemArgs {
+  CholArgs c;
+  const double* X;       // cluster-sorted inputs (fused assembly)
+  int d;
+  const double* jitter;
+  int kind;
+  double lam, noise, alpha;
+};
+
+__global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
+  const CholArgs& a = g.c;
+  const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
+  const int ld = a.ld[i];
+  const int64_t o = a.off[i];
+  const int b = static_cast<int>(a.off[i + 1] - o);
+  double* A = a.A + a.boff[i];
+  extern __shared__ double sm[];
+  const int np = ld * (ld + 1) / 2;
+  double* S = sm;                                    // packed lower: (r, c) at cofs(c) + r - c
+  double* XdT = S + ((np + 1) & ~1);                 // (NB+1) x NB
+  double* Yc = XdT + (CS_NB + 1) * CS_NB;            // NB x YC
+  __shared__ int fail;
+  __shared__ double red[CS_NT / 32];
+  __shared__ double s_inv;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  constexpr int NWP = CS_NT / 32;
+  if (tid == 0) fail = 0;
+#define SP(r, c) S[cofs((c), ld) + (r) - (c)]
+  // ---- fused assembly of K_i = k(X_i, X_i) + (noise + jitter_i) I, padding = identity ----
+  {
+    const double diag_add = g.noise + (g.jitter ? g.jitter[i] : 0.0);
+    const double* Xi = g.X + o * g.d;
+    for (int c = wid; c < ld; c += NWP) {
+      for (int r = c + lane; r < ld; r += 32) {
+        double v;
+        if (r < b && c < b) {
+          double sq = 0.0;
+          for (int dd = 0; dd < g.d; ++dd) {
+            const double df = __dsub_rn(Xi[static_cast<int64_t>(r) * g.d + dd], Xi[static_cast<int64_t>(c) * g.d + dd]);
+            sq = __dadd_rn(sq, __dmul_rn(df, df));
+          }
+          v = kval(g.kind, sq, g.lam, g.alpha);
+          if (r == c) v += diag_add;
+        } else {
+          v = (r == c) ? 1.0 : 0.0;
+        }
+        SP(r, c) = v;
+      }
+    }
+  }
+  __syncthreads();
+  // ---- Cholesky, 16-column panels ----
+  for (int k0 = 0; k0 < ld; k0 += CS_NB) {
+    const int nb = min(CS_NB, ld - k0);
+    for (int j = 0; j < nb; ++j) {
+      const int col = k0 + j;
+      if (tid == 0) {
+        double piv = SP(col, col);
+        if (!(piv > 0.0)) { fail = 1; piv = 1.0; }
+        const double dg = sqrt(piv);
+        SP(col, col) = dg;
+        s_inv = 1.0 / dg;
+      }
+      __syncthreads();
+      const double inv = s_inv;
+      for (int r = col + 1 + tid; r < ld; r += CS_NT) SP(r, col) *= inv;
+      __syncthreads();
+      const int ncols = k0 + nb - col - 1;          // remaining panel columns
+      if (ncols > 0) {
+        const int nrow = ld - col - 1;
+        for (int idx = tid; idx < ncols * nrow; idx += CS_NT) {
+          const int c2 = col + 1 + idx / nrow, r = col + 1 + idx % nrow;
+          if (r >= c2) SP(r, c2) -= SP(r, col) * SP(c2, col);
+        }
+        __syncthreads();
+      }
+    }
+    // trailing update of the lower triangle with the panel, 4x4 tiles
+    const int t0 = k0 + nb;
+    const int tr = ld - t0;
+    if (tr > 0) {
+      const int nt4 = (tr + 3) / 4;
+      const int ntl = nt4 * (nt4 + 1) / 2;
+      for (int tt = tid; tt < ntl; tt += CS_NT) {
+        int bi = static_cast<int>((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
+        while (bi * (bi + 1) / 2 > tt) --bi;
+        while ((bi + 1) * (bi + 2) / 2 <= tt) ++bi;
+        const int bj = tt - bi * (bi + 1) / 2;
+        const int rb = t0 + bi * 4, cb = t0 + bj * 4;
+        double acc[4][4];
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+        for (int jj = 0; jj < nb; ++jj) {
+          const double* pc = S + cofs(k0 + jj, ld) - (k0 + jj);   // column k0+jj, indexed by row
+          double av[4], bv[4];
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            av[x] = (rb + x < ld) ? pc[rb + x] : 0.0;
+            bv[x] = (cb + x < ld) ? pc[cb + x] : 0.0;
+          }
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+#pragma unroll
+            for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+        }
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = cb + y;
+          if (c >= ld) continue;
+#pragma unroll
+          for (int x = 0; x < 4; ++x) {
+            const int r = rb + x;
+            if (r < ld && r >= c) SP(r, c) -= acc[x][y];
+          }
+        }
+      }
+    }
+    __syncthreads();
+  }
+  // logdet partial (real rows only; padding diagonal is 1)
+  double ls = 0.0;
+  for (int r = tid; r < b; r += CS_NT) ls += log(SP(r, r));
+  ls = warp_sum(ls);
+  if (lane == 0) red[wid] = ls;
+  __syncthreads();
+  if (tid == 0) {
+    double s_ = 0.0;
+    for (int w = 0; w < NWP; ++w) s_ += red[w];
+    a.logdet_blk[i] = 2.0 * s_;
+    a.status[i] = fail;
+  }
+  __syncthreads();
+  if (fail) return;
+  // ---- triangular inverse in place, by 16-row panels ----
+  constexpr int NBP = CS_NB + 1;
+  for (int I0 = 0; I0 < ld; I0 += CS_NB) {
+    const int nb = min(CS_NB, ld - I0);
+    // diagonal tile inverse: thread j < nb solves L_II x = e_j (column j of the inverse)
+    if (tid < nb) {
+      const int j = tid;
+      for (int r = 0; r < nb; ++r) {
+        double v = 0.0;
+        if (r >= j) {
+          v = (r == j) ? 1.0 : 0.0;
+          for (int k = j; k < r; ++k) v -= SP(I0 + r, I0 + k) * XdT[j * NBP + k];
+          v /= SP(I0 + r, I0 + r);
+        }
+        XdT[j * NBP + r] = v;
+      }
+    }
+    __syncthreads();
+    for (int cc0 = 0; cc0 < I0; cc0 += CS_YC) {
+      const int ncc = min(CS_YC, I0 - cc0);
+      // Yc[cl][r] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]
+      for (int idx = tid; idx < nb * ncc; idx += CS_NT) {
+        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        double acc = 0.0;
+        for (int k = c; k < I0; ++k) acc = fma(SP(I0 + r, k), SP(k, c), acc);
+        Yc[cl * CS_NB + r] = acc;
+      }
+      __syncthreads();
+      // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
+      for (int idx = tid; idx < nb * ncc; idx += CS_NT) {
+        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
+        double acc = 0.0;
+        for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yc[cl * CS_NB + k], acc);
+        SP(I0 + r, c) = -acc;
+      }
+      __syncthreads();
+    }
+    for (int idx = tid; idx < nb * nb; idx += CS_NT) {
+      const int r = idx % nb, c = idx / nb;
+      if (r >= c) SP(I0 + r, I0 + c) = XdT[c * NBP + r];
+    }
+    __syncthreads();
+  }
+  // ---- write Linv (zero upper triangle) and u = Linv 1_b ----
+  for (int c = wid; c < ld; c += NWP)
+    for (int r = lane; r < ld; r += 32) A[static_cast<int64_t>(c) * ld + r] = (r >= c) ? SP(r, c) : 0.0;
+  const int64_t p0 = a.poff[i];
+  for (int r = tid; r < ld; r += CS_NT) {
+    double acc = 0.0;
+    if (r < b)
+      for (int k = 0; k <= r; ++k) acc += SP(r, k);
+    a.u[p0 + r] = acc;
+  }
+#undef SP
+}
+
+size_t chol_smem_bytes_fused(int ld_max) {
+  const size_t np = static_cast<size_t>(ld_max) * (ld_max + 1) / 2;
+  return sizeof(double) * (((np + 1) & ~static_cast<size_t>(1)) + (CS_NB + 1) * CS_NB + CS_NB * CS_YC);
+}
+
+bool chol_fused_ok(int ld_max) {
+  const char* v = getenv("NUGPR_CHOL_SMEM");      // experimental: slower than the global-memory kernel so far
+  return ld_max <= CS_LDMAX && v && v[0] == '1';
+}
+
+void launch_chol_fused(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
+                       const double* jitter, double* A, int kind, double lam, double noise, double alpha,
+                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s) {
+  CholSmemArgs g;
+  g.c = CholArgs{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
+  g.X = X; g.d = d; g.jitter = jitter; g.kind = kind; g.lam = lam; g.noise = noise; g.alpha = alpha;
+  smem_optin(reinterpret_cast<const void*>(chol_smem_kernel));
+  chol_smem_kernel<<<list ? nlist : L.n_c, CS_NT, chol_smem_bytes_fused(ld_max), s>>>(g);
+  note_launch(); post_launch("chol_smem_kernel");
+}
+
 size_t chol_smem_bytes(int ld_max) {
   size_t panel = static_cast<size_t>(ld_max) * NB;                         // Cholesky panel
   size_t inv = static_cast<size_t>(NB + 1) * ld_max + (NB + 1) * NB + static_cast<size_t>(NB) * 64 + 64;

@@ -23,6 +23,10 @@ void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* 
                      int ld_max, const double* jitter, double* dst, int kind, double lam,
                      double noise, double alpha, cudaStream_t s);
 size_t chol_smem_bytes(int ld_max);
+bool chol_fused_ok(int ld_max);
+void launch_chol_fused(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
+                       const double* jitter, double* A, int kind, double lam, double noise, double alpha,
+                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
 void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
                        int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
 void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s);
