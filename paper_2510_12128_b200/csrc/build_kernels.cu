@@ -350,9 +350,12 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 constexpr int CS_NT = 512;
 constexpr int CS_NB = 16;
 constexpr int CS_YC = 32;
-constexpr int CS_LDMAX = 224;
+constexpr int CS_LDMAX = 216;
 
 __device__ __forceinline__ int cofs(int c, int ld) { return c * ld - (c * (c - 1)) / 2; }
+
+__device__ int g_chol_trace = 0;
+__device__ __forceinline__ bool getenv_flag_chol_trace() { return g_chol_trace != 0; }
 
 struct CholSmemArgs {
   CholArgs c;
@@ -381,6 +384,10 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   constexpr int NWP = CS_NT / 32;
   if (tid == 0) fail = 0;
+  unsigned long long tst[6];
+  auto stamp = [&](int q) { if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[q])); };
+  const bool trace = getenv_flag_chol_trace();
+  stamp(0);
 #define SP(r, c) S[cofs((c), ld) + (r) - (c)]
   // ---- fused assembly of K_i = k(X_i, X_i) + (noise + jitter_i) I, padding = identity ----
   {
@@ -405,6 +412,7 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
     }
   }
   __syncthreads();
+  stamp(1);
   // ---- Cholesky, 16-column panels ----
   for (int k0 = 0; k0 < ld; k0 += CS_NB) {
     const int nb = min(CS_NB, ld - k0);
@@ -475,6 +483,7 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
     }
     __syncthreads();
   }
+  stamp(2);
   // logdet partial (real rows only; padding diagonal is 1)
   double ls = 0.0;
   for (int r = tid; r < b; r += CS_NT) ls += log(SP(r, r));
@@ -490,10 +499,13 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
   __syncthreads();
   if (fail) return;
   // ---- triangular inverse in place, by 16-row panels ----
+  // Row panel I = rows [I0, I0+nb): X_II = L_II^{-1} (XdT, 16 threads), Y = L[I, 0:I0] X[0:I0, 0:I0]
+  // (thread pair per column c: 8 rows each, 8 independent accumulators over k = c..I0-1, with
+  // the L row segments broadcast), then X[I, 0:I0] = -X_II Y written over L[I, 0:I0].
   constexpr int NBP = CS_NB + 1;
+  double* Yt = Yc;                                   // Y as [c][16]: 16 * I0 <= 16 * ld doubles
   for (int I0 = 0; I0 < ld; I0 += CS_NB) {
     const int nb = min(CS_NB, ld - I0);
-    // diagonal tile inverse: thread j < nb solves L_II x = e_j (column j of the inverse)
     if (tid < nb) {
       const int j = tid;
       for (int r = 0; r < nb; ++r) {
@@ -506,25 +518,27 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
         XdT[j * NBP + r] = v;
       }
     }
+    for (int t = tid; t < 2 * I0; t += CS_NT) {
+      const int c = t >> 1, rh = (t & 1) * 8;
+      double acc[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
+      const double* xc = S + cofs(c, ld) - c;          // X[k][c] = xc[k], k >= c
+      for (int k = c; k < I0; ++k) {
+        const double xv = xc[k];
+        const double* lk = S + cofs(k, ld) - k + I0 + rh;   // L[I0+rh+q][k] = lk[q]
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[q] = fma((rh + q < nb) ? lk[q] : 0.0, xv, acc[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) Yt[c * CS_NB + rh + q] = acc[q];
+    }
     __syncthreads();
-    for (int cc0 = 0; cc0 < I0; cc0 += CS_YC) {
-      const int ncc = min(CS_YC, I0 - cc0);
-      // Yc[cl][r] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]
-      for (int idx = tid; idx < nb * ncc; idx += CS_NT) {
-        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
-        double acc = 0.0;
-        for (int k = c; k < I0; ++k) acc = fma(SP(I0 + r, k), SP(k, c), acc);
-        Yc[cl * CS_NB + r] = acc;
-      }
-      __syncthreads();
-      // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
-      for (int idx = tid; idx < nb * ncc; idx += CS_NT) {
-        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
-        double acc = 0.0;
-        for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yc[cl * CS_NB + k], acc);
-        SP(I0 + r, c) = -acc;
-      }
-      __syncthreads();
+    for (int idx = tid; idx < nb * I0; idx += CS_NT) {
+      const int r = idx % nb, c = idx / nb;
+      double acc = 0.0;
+      for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yt[c * CS_NB + k], acc);
+      SP(I0 + r, c) = -acc;
     }
     for (int idx = tid; idx < nb * nb; idx += CS_NT) {
       const int r = idx % nb, c = idx / nb;
@@ -532,6 +546,7 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
     }
     __syncthreads();
   }
+  stamp(3);
   // ---- write Linv (zero upper triangle) and u = Linv 1_b ----
   for (int c = wid; c < ld; c += NWP)
     for (int r = lane; r < ld; r += 32) A[static_cast<int64_t>(c) * ld + r] = (r >= c) ? SP(r, c) : 0.0;
@@ -542,12 +557,16 @@ __global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
       for (int k = 0; k <= r; ++k) acc += SP(r, k);
     a.u[p0 + r] = acc;
   }
+  stamp(4);
+  if (trace && tid == 0 && blockIdx.x < 4)
+    printf("CHOL blk %d asm %.1f chol %.1f inv %.1f out %.1f us\n", blockIdx.x, (tst[1] - tst[0]) * 1e-3,
+           (tst[2] - tst[1]) * 1e-3, (tst[3] - tst[2]) * 1e-3, (tst[4] - tst[3]) * 1e-3);
 #undef SP
 }
 
 size_t chol_smem_bytes_fused(int ld_max) {
   const size_t np = static_cast<size_t>(ld_max) * (ld_max + 1) / 2;
-  return sizeof(double) * (((np + 1) & ~static_cast<size_t>(1)) + (CS_NB + 1) * CS_NB + CS_NB * CS_YC);
+  return sizeof(double) * (((np + 1) & ~static_cast<size_t>(1)) + (CS_NB + 1) * CS_NB + CS_NB * static_cast<size_t>(ld_max));
 }
 
 bool chol_fused_ok(int ld_max) {
@@ -562,6 +581,14 @@ void launch_chol_fused(const double* X, int d, const LayoutDev& L, const int32_t
   g.c = CholArgs{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
   g.X = X; g.d = d; g.jitter = jitter; g.kind = kind; g.lam = lam; g.noise = noise; g.alpha = alpha;
   smem_optin(reinterpret_cast<const void*>(chol_smem_kernel));
+  {
+    static int traced = -1;
+    if (traced < 0) {
+      const char* v = getenv("NUGPR_CHOL_TRACE");
+      traced = (v && v[0] == '1') ? 1 : 0;
+      if (traced) cudaMemcpyToSymbol(g_chol_trace, &traced, sizeof(int));
+    }
+  }
   chol_smem_kernel<<<list ? nlist : L.n_c, CS_NT, chol_smem_bytes_fused(ld_max), s>>>(g);
   note_launch(); post_launch("chol_smem_kernel");
 }
