@@ -127,7 +127,9 @@ typedef int (*nugpr_allgather_fn)(const void* send, size_t bytes, void* recv, vo
 const char* nugpr_version(void);
 const char* nugpr_last_error(void);
 
-/* Context on `device`, enqueuing on `cuda_stream` (cudaStream_t; NULL = legacy default). */
+/* Context on `device`, enqueuing on `cuda_stream` (cudaStream_t; NULL = legacy default).
+ * device < 0 creates a host-only context (no CUDA calls; rank/world/allgather only) usable with
+ * the host helpers below (nugpr_numgrad_exchange). */
 nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world, nugpr_ctx** out);
 nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void* user);
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
@@ -221,6 +223,13 @@ nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, const int64_t* 
                          void* workspace, size_t ws_bytes);
 
 /* Host-only helpers (no device work; usable without a GPU). */
+/* PAR-1 exchange of nugpr_numgrad CENTRAL: the 7 evaluations theta, theta +- h_i e_i
+ * (h_i = step_i theta_i) are owned per nugpr_shard_plan(world, {1,3,3,2,2,2,2}); this rank passes
+ * the losses of the evaluations it owns in L_mine[k] (others ignored); one allgather through the
+ * context callback; every rank returns the same L0 = L(theta) and g_i = (L+ - L-)/(2 h_i)
+ * (Eq. 11 as a central difference, reading X2).  nugpr_numgrad uses the same exchange. */
+nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta, const double step[3],
+                                    const double L_mine[7], double* L0, double grad[3]);
 /* One Adam step on state {theta[3], m[3], v[3], t}. */
 nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr);
 /* Longest-processing-time assignment of n tasks with costs to `world` ranks: owner[n]. */

@@ -74,11 +74,8 @@ class Context:
     enables perturbation sharding in numgrad/train via the allgather callback."""
 
     def __init__(self, device: int = 0, stream=None, group=None):
-        import torch
+        """device < 0: host-only context (rank/world/allgather for the host helpers; no CUDA)."""
         self.device = int(device)
-        if stream is None:
-            stream = torch.cuda.current_stream(self.device)
-        self.stream = stream
         self.rank, self.world = 0, 1
         self.group = None
         if group is not None:
@@ -86,9 +83,16 @@ class Context:
             self.group = None if group is True else group
             self.rank = dist.get_rank(self.group)
             self.world = dist.get_world_size(self.group)
+        if self.device >= 0:
+            import torch
+            if stream is None:
+                stream = torch.cuda.current_stream(self.device)
+            sp = C.c_void_p(stream.cuda_stream)
+        else:
+            sp = C.c_void_p(None)
+        self.stream = stream
         h = C.c_void_p()
-        N.check(N.lib().nugpr_ctx_create(self.device, C.c_void_p(stream.cuda_stream), self.rank,
-                                         self.world, C.byref(h)))
+        N.check(N.lib().nugpr_ctx_create(self.device, sp, self.rank, self.world, C.byref(h)))
         self.handle = h
         self._cb = None
         if self.world > 1:
@@ -97,14 +101,7 @@ class Context:
 
     def _allgather(self, send, nbytes, recv, user):
         try:
-            import torch
-            import torch.distributed as dist
-            backend = dist.get_backend(self.group)
-            dev = torch.device("cuda", self.device) if backend == "nccl" else torch.device("cpu")
-            src = torch.frombuffer(bytearray(C.string_at(send, nbytes)), dtype=torch.uint8).to(dev)
-            out = torch.empty(self.world * nbytes, dtype=torch.uint8, device=dev)
-            dist.all_gather_into_tensor(out, src, group=self.group)
-            data = out.cpu().numpy().tobytes()
+            data = allgather_bytes(C.string_at(send, nbytes), self.world, self.group, self.device)
             C.memmove(recv, data, len(data))
             return 0
         except Exception:  # noqa: BLE001 — reported to C as a status
@@ -161,6 +158,31 @@ def cluster(ctx: Context, X, n_c: int, y=None, init_centers=None, seed: int = 0,
                                   off.ctypes.data, C.c_void_p(reps.data_ptr()), C.c_void_p(Xs.data_ptr()),
                                   C.c_void_p(ys.data_ptr()) if ys is not None else None, C.byref(it)))
     return dict(perm=perm, offsets=off, reps=reps, X_sorted=Xs, y_sorted=ys, iters=int(it.value))
+
+
+def allgather_bytes(data: bytes, world: int, group=None, device: int = -1) -> bytes:
+    """Allgather of equal-length byte strings through torch.distributed (NCCL on GPU boxes with
+    a CUDA device, gloo on CPU): the rank-ordered concatenation."""
+    import torch
+    import torch.distributed as dist
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", device) if (backend == "nccl" and device >= 0) else torch.device("cpu")
+    src = torch.frombuffer(bytearray(data), dtype=torch.uint8).to(dev)
+    out = torch.empty(world * len(data), dtype=torch.uint8, device=dev)
+    dist.all_gather_into_tensor(out, src, group=group)
+    return out.cpu().numpy().tobytes()
+
+
+def numgrad_exchange(ctx: Context, theta, step, L_mine):
+    """Host side of the perturbation-sharded CENTRAL gradient (nugpr_numgrad_exchange)."""
+    st = np.ascontiguousarray(step, dtype=np.float64)
+    Lm = np.ascontiguousarray(L_mine, dtype=np.float64)
+    L0 = C.c_double()
+    g = np.zeros(3)
+    P_ = C.POINTER(C.c_double)
+    N.check(N.lib().nugpr_numgrad_exchange(ctx.handle, _theta(theta), st.ctypes.data_as(P_), Lm.ctypes.data_as(P_),
+                                           C.byref(L0), g.ctypes.data_as(P_)))
+    return L0.value, g
 
 
 def workspace_size(offsets, n_c: int, d: int, eval_slots: int = 1) -> int:

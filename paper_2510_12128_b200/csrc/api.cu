@@ -373,6 +373,14 @@ const char* nugpr_last_error(void) { return g_err.c_str(); }
 nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world, nugpr_ctx** out) {
   if (!out) return fail(NUGPR_ERR_INVALID_ARG, "out is NULL");
   if (world < 1 || rank < 0 || rank >= world) return fail(NUGPR_ERR_INVALID_ARG, "bad rank/world");
+  if (device < 0) {                       // host-only context: rank/world/allgather for host helpers
+    nugpr_ctx* c = new nugpr_ctx();
+    c->device = -1;
+    c->rank = rank;
+    c->world = world;
+    *out = c;
+    return NUGPR_OK;
+  }
   CK(cudaSetDevice(device));
   nugpr_ctx* c = new nugpr_ctx();
   c->device = device;
@@ -419,6 +427,7 @@ int64_t nugpr_launch_count(void) { return launch_count(); }
 
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
   if (!ctx) return NUGPR_OK;
+  if (ctx->device < 0) { delete ctx; return NUGPR_OK; }
   for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
   for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
   for (cudaGraph_t g : ctx->graph_defs) cudaGraphDestroy(g);
@@ -1256,6 +1265,53 @@ struct EvalRecord {
   int32_t valid;
 };
 
+// PAR-1 exchange of the CENTRAL gradient: every rank holds the records of the
+// evaluations it owns (owner[k] == rank); one allgather of the 7-record arrays, then each record
+// is taken from its owner's copy, and every rank forms the same L0 and g_i = (L+ - L-)/(2 h_i)
+// (Eq. 11 read as a central difference, reading X2).
+static nugpr_status central_exchange(nugpr_ctx* ctx, const int32_t* owner, const EvalRecord* mine,
+                                     const double* h, double* L0, double* grad, nugpr_mll_out* evals,
+                                     nugpr_status* worst) {
+  EvalRecord all[NUGPR_NUM_EVALS];
+  if (ctx->world > 1) {
+    if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");
+    std::vector<EvalRecord> recv(static_cast<size_t>(ctx->world) * NUGPR_NUM_EVALS);
+    if (ctx->ag(mine, sizeof(EvalRecord) * NUGPR_NUM_EVALS, recv.data(), ctx->ag_user) != 0)
+      return fail(NUGPR_ERR_COMM, "allgather failed");
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) all[k] = recv[static_cast<size_t>(owner[k]) * NUGPR_NUM_EVALS + k];
+  } else {
+    memcpy(all, mine, sizeof(all));
+  }
+  *worst = NUGPR_OK;
+  for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
+    if (!all[k].valid) return fail(NUGPR_ERR_COMM, "evaluation %d missing after exchange", k);
+    if (all[k].status != NUGPR_OK) *worst = static_cast<nugpr_status>(all[k].status);
+    if (evals) evals[k] = all[k].o;
+  }
+  *L0 = all[0].o.L;
+  for (int i = 0; i < 3; ++i) grad[i] = (all[1 + 2 * i].o.L - all[2 + 2 * i].o.L) / (2.0 * h[i]);
+  return NUGPR_OK;
+}
+
+// Host-only entry to the same exchange (tests of the sharded path without a GPU): this rank
+// passes L values for the evaluations nugpr_shard_plan gives it (others ignored).
+extern "C" nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta, const double step[3],
+                                               const double L_mine[7], double* L0, double grad[3]) {
+  if (!ctx || !step || !L_mine || !L0 || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  const double th[3] = {theta.lengthscale, theta.noise, theta.outputscale};
+  double h[3];
+  for (int i = 0; i < 3; ++i) h[i] = step[i] * th[i];
+  const double cost[NUGPR_NUM_EVALS] = {1.0, 3.0, 3.0, 2.0, 2.0, 2.0, 2.0};
+  int32_t owner[NUGPR_NUM_EVALS];
+  RET(nugpr_shard_plan(ctx->world, cost, NUGPR_NUM_EVALS, owner));
+  EvalRecord mine[NUGPR_NUM_EVALS];
+  memset(mine, 0, sizeof(mine));
+  for (int k = 0; k < NUGPR_NUM_EVALS; ++k)
+    if (owner[k] == ctx->rank) { mine[k].o.L = L_mine[k]; mine[k].valid = 1; mine[k].status = NUGPR_OK; }
+  nugpr_status worst = NUGPR_OK;
+  return central_exchange(ctx, owner, mine, h, L0, grad, nullptr, &worst);
+}
+
 // Evaluate the points `ks` (indices into pts) concurrently: evaluation j runs on slot j % slots,
 // each slot on its own stream forked from the context stream; one host sync at the end.
 static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_dev,
@@ -1339,24 +1395,9 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
     std::vector<int> ks;                       // this rank's evaluations, most expensive first
     for (int k : {1, 2, 3, 4, 5, 6, 0}) if (owner[k] == ctx->rank) ks.push_back(k);
     RET(run_evals_concurrent(ctx, bl, y_dev, ks, tp, scfg, mine));
-    EvalRecord all[NUGPR_NUM_EVALS];
-    if (ctx->world > 1) {
-      if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");
-      std::vector<EvalRecord> recv(static_cast<size_t>(ctx->world) * NUGPR_NUM_EVALS);
-      if (ctx->ag(mine, sizeof(mine), recv.data(), ctx->ag_user) != 0) return fail(NUGPR_ERR_COMM, "allgather failed");
-      for (int k = 0; k < NUGPR_NUM_EVALS; ++k) all[k] = recv[static_cast<size_t>(owner[k]) * NUGPR_NUM_EVALS + k];
-    } else {
-      memcpy(all, mine, sizeof(mine));
-    }
     nugpr_status worst = NUGPR_OK;
-    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
-      if (!all[k].valid) return fail(NUGPR_ERR_COMM, "evaluation %d missing after exchange", k);
-      if (all[k].status != NUGPR_OK) worst = static_cast<nugpr_status>(all[k].status);
-      if (evals) evals[k] = all[k].o;
-    }
+    RET(central_exchange(ctx, owner, mine, h, L0, grad, evals, &worst));
     ne = NUGPR_NUM_EVALS;
-    *L0 = all[0].o.L;
-    for (int i = 0; i < 3; ++i) grad[i] = (all[1 + 2 * i].o.L - all[2 + 2 * i].o.L) / (2.0 * h[i]);
     if (n_evals) *n_evals = ne;
     if (worst != NUGPR_OK) return fail(worst, "an evaluation did not converge");
     return NUGPR_OK;
