@@ -55,11 +55,13 @@ nugpr_status fail(nugpr_status st, const char* fmt, ...) {
   } while (0)
 
 constexpr int HIST = 4096;          // max recorded CG iterations (cg_max_iter cap)
-constexpr int LD_MAX_SUPPORTED = 512;
+constexpr int LD_MAX_SUPPORTED = 8192;
+constexpr int LD_SMALL_MAX = 512;     // above: big-block mode (blocked multi-launch factorisation, row-tiled apply)
 constexpr int LANCZOS_KMAX_CAP = 400;
 
 struct HostLayout {
   int n_c = 0, d = 0;
+  bool big = false;
   int64_t n = 0, n_pad = 0, blk_total = 0;
   int ld_max = 0;
   std::vector<int64_t> off, poff, boff;
@@ -76,6 +78,10 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
   L.n_c = n_c;
   L.d = d;
   L.off.assign(offsets, offsets + n_c + 1);
+  int64_t bmax = 0;
+  for (int i = 0; i < n_c; ++i) bmax = std::max<int64_t>(bmax, offsets[i + 1] - offsets[i]);
+  L.big = (bmax + PAD - 1) / PAD * PAD > LD_SMALL_MAX;
+  const int tile_rows = L.big ? 64 : TILE_ROWS;
   L.poff.resize(n_c + 1);
   L.boff.resize(n_c);
   L.ld.resize(n_c);
@@ -93,11 +99,11 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
     L.poff[i] = pp;
     L.boff[i] = bb;
     L.tile0[i] = static_cast<int32_t>(L.tiles.size());
-    for (int r0 = 0; r0 < ld; r0 += TILE_ROWS) {
+    for (int r0 = 0; r0 < ld; r0 += tile_rows) {
       TileDesc t;
       t.blk = i;
       t.row0 = r0;
-      t.nrows = static_cast<int32_t>(std::min<int64_t>(TILE_ROWS, ld - r0));
+      t.nrows = static_cast<int32_t>(std::min<int64_t>(tile_rows, ld - r0));
       t.pad_ = 0;
       L.tiles.push_back(t);
     }
@@ -173,6 +179,7 @@ struct BlocksDev {
   double* Zexport = nullptr;  // m x n (debug probe export)
   double* cy = nullptr;       // n_pad: c = R^{-T} y cached across the evaluations of one numgrad
   double* ystage = nullptr;   // n: host y staged to the device
+  double* bigscr = nullptr;   // big-block mode: diagonal-block inverses + inverse-step scratch
 };
 
 void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
@@ -206,6 +213,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
   B.cy = c.take<double>(L.n_pad);
   B.ystage = c.take<double>(L.n);
+  if (L.big) B.bigscr = c.take<double>(big_scratch_doubles(n_c, L.ld_max));
   E.assign(slots, EvalDev());
   const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
   for (int s = 0; s < slots; ++s) {
@@ -568,8 +576,14 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   }
   if (bas != s) CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][1], bas));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
-  const bool fused_chol = chol_fused_ok(L.ld_max);
-  if (fused_chol) {
+  const bool fused_chol = !L.big && chol_fused_ok(L.ld_max);
+  if (L.big) {
+    PROF(ctx, PC_OTHER, 0.0, s,
+         launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
+                         theta0.noise, theta0.outputscale, s));
+    PROF(ctx, PC_CHOL, 0.0, s,
+         launch_big_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, B.bigscr, s));
+  } else if (fused_chol) {
     PROF(ctx, PC_CHOL, 0.0, s,
          launch_chol_fused(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
                            theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s));
@@ -599,7 +613,12 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     for (int i : bl->h_list) bl->h_jitter[i] = base * std::pow(10.0, t);
     CKB(cudaMemcpyAsync(B.jitter, bl->h_jitter.data(), sizeof(double) * n_c, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(B.list, bl->h_list.data(), sizeof(int32_t) * bl->h_list.size(), cudaMemcpyHostToDevice, s));
-    if (fused_chol) {
+    if (L.big) {
+      launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
+                      kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
+      launch_big_chol_trtri(B.Linv, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.status,
+                            B.logdet_blk, B.u, B.bigscr, s);
+    } else if (fused_chol) {
       launch_chol_fused(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
                         kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s);
     } else {
@@ -893,7 +912,11 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
   a1.alpha_hist = e.ah; a1.hist_stride = HIST;
   a1.ld_max = L.ld_max;
-  {
+  if (L.big) {
+    a1.big = 1;
+    a1.grid = Ld.n_tiles;
+    a1.Tbuf = e.Tbuf;
+  } else {
     const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
     const ApplyPlan pl = plan_apply(A.ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles), Ld.n_ctasks);
     if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, ncol=%d)", L.ld_max, ncol);
@@ -965,6 +988,9 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     A.a1.d_is_pnew = 1;
     A.t2.task0 = bl->B.ctask0;
     A.t4.task0 = bl->B.ctask0;
+  }
+  if (L.big) {                                   // S partials are per 64-row tile
+    A.t1.task0 = bl->B.tile0; A.t2.task0 = bl->B.tile0; A.t3.task0 = bl->B.tile0; A.t4.task0 = bl->B.tile0;
   }
   bl->iter_kernels = A.pnew ? 6 : 5;
   A.st = e.st; A.R = e.R; A.Pb[0] = e.Pb[0]; A.Pb[1] = e.Pb[1]; A.n_pad = L.n_pad; A.ncol = ncol;

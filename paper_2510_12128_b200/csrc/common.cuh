@@ -124,6 +124,7 @@ struct ApplyArgs {
   int mma;                 // 3: DMMA column-task kernel, 2: staged DMMA, 1: DMMA, 0: DFMA
   int lds;                 // column-task kernel: padded column stride in shared memory
   int d_is_pnew;           // column-task kernel: D := P_new = Pbuf[par^1] (formed by pnew_kernel)
+  int big;                 // big-block mode (ld_max > 512): row-tiled apply_big_kernel
 };
 
 struct ApplyPlan {

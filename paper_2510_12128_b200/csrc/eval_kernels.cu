@@ -1781,6 +1781,7 @@ static void apply_launch_t(const ApplyArgs& a, bool useB, cudaStream_t s) {
 }
 
 void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
+  if (a.big) { launch_apply_big(a, ncp, s); return; }
   if (a.mma == 3) {
     size_t smem = a.smem_b;
     smem_optin(reinterpret_cast<const void*>(apply_col_kernel<CTW / 8>));

@@ -58,6 +58,12 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
                   int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
 
+// big_kernels.cu (ld_max > 512)
+size_t big_scratch_doubles(int n_c, int ld_max);
+void launch_big_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
+                           int32_t* status, double* logdet_blk, double* u, double* scratch, cudaStream_t s);
+void launch_apply_big(const ApplyArgs& a, int ncp, cudaStream_t s);
+
 // cluster_kernels.cu (row A0)
 void launch_km_absmax(const double* X, int64_t cnt, unsigned long long* out, cudaStream_t s);
 size_t km_assign_smem();

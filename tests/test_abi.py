@@ -57,8 +57,10 @@ def test_workspace_size_validation(lib):
         P.workspace_size(np.array([1, 5, 9]), 2, 2, 1)
     assert e.value.name == "SHAPE"
     with pytest.raises(P.NugprError) as e:
-        P.workspace_size(np.array([0, 5000]), 1, 2, 1)   # cluster larger than this build's limit
+        P.workspace_size(np.array([0, 9000]), 1, 2, 1)   # cluster larger than this build's limit (8192)
     assert e.value.name == "SHAPE"
+    big = P.workspace_size(np.array([0, 5000]), 1, 2, 1)       # big-block mode (ld > 512)
+    assert big > 2 * 5000 * 5000 * 8
 
 
 def test_adam_step_matches_oracle(lib):

@@ -1,0 +1,118 @@
+"""GPU parity of the big-block path (clusters > 512 points: blocked multi-launch factorisation
+and the row-tiled apply), against the FP64 oracle: uneven hand-made clusters, and config C4
+(G-REAL, 32,000 training points, k-means n_c = 20 uneven clusters up to ~4.3k, Matern-5/2)."""
+import numpy as np
+import pytest
+
+import synth
+from oracle import kmeans as KM
+from oracle import structured as OS
+from oracle.mll import mll as oracle_mll
+
+pytestmark = pytest.mark.gpu
+
+TIGHT = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_12128_b200 as P
+    P._native.lib()
+    return P
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    return P.Context(0)
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def uneven(sizes, d, seed, spread=1.0):
+    rng = np.random.default_rng(seed)
+    n_c = len(sizes)
+    reps = rng.uniform(-10, 10, size=(n_c, d))
+    X = np.concatenate([reps[i] + spread * rng.standard_normal((s, d)) for i, s in enumerate(sizes)])
+    y = np.sin(X).sum(axis=1) + 0.4 * rng.standard_normal(X.shape[0])
+    off = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    return X, y, off, reps
+
+
+def check_eval(P, ctx, bg, bo, y, theta, seed, rtol=TIGHT):
+    rec = P.mll(ctx, bg, y, theta, probe_seed=seed)
+    Z = synth.probes(seed, 8, y.shape[0])
+    ro = oracle_mll(bo, y, theta, Z, replay=[rec["iters_y"]] + rec["iters_q"])
+    assert rec["mode"] == ro.mode
+    for k in ("L", "quad", "logdet_pade", "logdet_slq"):
+        assert rel(rec[k], getattr(ro, k)) < rtol, (k, rec[k], getattr(ro, k))
+    return rec
+
+
+def test_big_blocks_uneven_parity(P, ctx):
+    sizes = [700, 300, 1100, 530, 90]
+    X, y, off, reps = uneven(sizes, 4, 3)
+    th0 = (1.3, 0.2, 1.1)
+    bg = P.build_blocks(ctx, X, off, reps, th0)
+    bo = OS.build_blocks(X, off, reps, th0)
+    # factor data: Linv = R^{-T}, u, logdet_R
+    Linv = bg.export("linv")
+    for i in range(len(sizes)):
+        Lo = np.linalg.inv(bo.R[i].T)
+        np.testing.assert_allclose(Linv[i], Lo, rtol=0, atol=1e-10 * np.abs(Lo).max())
+    np.testing.assert_allclose(bg.export("u"), np.concatenate(bo.u), rtol=1e-10, atol=1e-12)
+    assert rel(bg.export("scalars")[0], bo.logdet_R) < 1e-12
+    l, s, a = th0
+    for th in [th0, (l, s * 1.001, a), (l, s, a * 0.999), (l * 1.001, s, a)]:
+        check_eval(P, ctx, bg, bo, y, th, 7)
+
+
+def test_big_blocks_mixed_with_small_and_jitter(P, ctx):
+    """A singular large cluster (duplicated points, tiny noise) takes the jitter ladder on the
+    big path exactly as the oracle does."""
+    rng = np.random.default_rng(4)
+    X1 = np.repeat(rng.standard_normal((300, 2)), 2, axis=0)          # 600 points, duplicates
+    X2 = 6 + rng.standard_normal((40, 2))
+    X = np.concatenate([X1, X2])
+    y = rng.standard_normal(X.shape[0])
+    off = np.array([0, 600, 640], dtype=np.int64)
+    reps = np.array([[0.0, 0.0], [6.0, 6.0]])
+    th0 = (1.0, 1e-18, 1.0)
+    bg = P.build_blocks(ctx, X, off, reps, th0)
+    bo = OS.build_blocks(X, off, reps, th0)
+    np.testing.assert_allclose(bg.export("jitter"), bo.jitter, rtol=1e-12)
+    assert bo.jitter[0] > 0
+
+
+def c4_dataset():
+    g = synth.g_real(N=40000, d=8, seed=104)
+    km = KM.kmeans(g["X"], 20, seed=104, rep_mode=KM.CENTROID)
+    X = g["X"][km["perm"]]
+    y = g["y"][km["perm"]]
+    off = km["offsets"]
+    # theta0 = (median intra-cluster distance, 0.16, Var(y)) (SURVEY §8(d) G-REAL recipe)
+    rng = np.random.default_rng(0)
+    dists = []
+    for i in range(20):
+        Xi = X[off[i]:off[i + 1]]
+        a = rng.integers(0, Xi.shape[0], 200)
+        b = rng.integers(0, Xi.shape[0], 200)
+        dists.append(np.linalg.norm(Xi[a] - Xi[b], axis=1))
+    th0 = (float(np.median(np.concatenate(dists))), 0.16, float(np.var(y)))
+    return X, y, off, km["reps"], th0
+
+
+def test_C4_matern_build_and_mll_parity(P, ctx):
+    X, y, off, reps, th0 = c4_dataset()
+    sizes = np.diff(off)
+    assert sizes.max() > 512 and sizes.min() < 1000            # uneven, big-block mode
+    bg = P.build_blocks(ctx, X, off, reps, th0, kernel="matern52")
+    bo = OS.build_blocks(X, off, reps, th0, kind="matern52")
+    assert rel(bg.export("scalars")[0], bo.logdet_R) < 1e-11
+    l, s, a = th0
+    check_eval(P, ctx, bg, bo, y, th0, 204)
+    check_eval(P, ctx, bg, bo, y, (l * 1.001, s, a), 204)
