@@ -38,8 +38,38 @@ CONFIG_DESC = {
     "C1": "n=1000 d=2 n_c=10 b=100 RBF m=8",
     "C2": "n=20000 d=8 n_c=100 b=200 RBF m=8",
     "C3": "n=100000 d=8 n_c=500 b=200 RBF m=8",
+    "C4": "n=32000 (+8000 test) d=8 n_c=20 uneven k-means clusters, Matern-5/2, m=8",
     "C5": "n=1000000 d=4 n_c=2000 b=500 RBF m=8",
 }
+
+
+def load_config(name, P=None, ctx=None):
+    """Dataset of a BASELINE config.  C4 (G-REAL) is clustered by row A0 first: on the GPU
+    through the library (nugpr_cluster) for our arm, by the oracle's k-means for the reference
+    arm (the two are bit-identical, tests/test_gpu_cluster.py); theta0 per the G-REAL recipe
+    (median intra-cluster distance, 0.16, Var(y))."""
+    if name != "C4":
+        return synth.make_config(name)
+    g = synth.g_real(N=40000, d=8, seed=104)
+    if P is not None:
+        r = P.cluster(ctx, g["X"], 20, y=g["y"], seed=104, rep_mode="centroid")
+        X, y, off, reps = (r["X_sorted"].cpu().numpy(), r["y_sorted"].cpu().numpy(), r["offsets"],
+                           r["reps"].cpu().numpy())
+    else:
+        from oracle import kmeans as KM
+        km = KM.kmeans(g["X"], 20, seed=104, rep_mode=KM.CENTROID)
+        X, y, off, reps = g["X"][km["perm"]], g["y"][km["perm"]], km["offsets"], km["reps"]
+    rng = np.random.default_rng(0)
+    dists = []
+    for i in range(20):
+        Xi = X[off[i]:off[i + 1]]
+        a = rng.integers(0, Xi.shape[0], 200)
+        b = rng.integers(0, Xi.shape[0], 200)
+        dists.append(np.linalg.norm(Xi[a] - Xi[b], axis=1))
+    th0 = (float(np.median(np.concatenate(dists))), 0.16, float(np.var(y)))
+    return synth.Dataset(X=np.ascontiguousarray(X), y=np.ascontiguousarray(y), offsets=np.asarray(off, dtype=np.int64),
+                         reps=np.ascontiguousarray(reps), theta0=th0,
+                         meta=dict(config="C4", probe_seed=204, m=8, kernel="matern52", kind="g_real"))
 
 
 def peaks():
@@ -127,7 +157,7 @@ def oracle_sample(ds, probe_seed, evals_sel):
     Z = synth.probes(probe_seed, 8, ds.n)
     pts, _ = central_perturbations(ds.theta0, (1e-3,) * 3)
     t0 = time.perf_counter()
-    bo = obuild(ds.X, ds.offsets, ds.reps, ds.theta0)
+    bo = obuild(ds.X, ds.offsets, ds.reps, ds.theta0, ds.meta.get("kernel", "rbf"))
     t_build = time.perf_counter() - t0
     times = {}
     for k in evals_sel:
@@ -162,7 +192,7 @@ def run_reference(args):
     rank, world, _ = init_dist("gloo")
     if rank != 0:
         return
-    ds = synth.make_config(args.config)
+    ds = load_config(args.config)
     seed = ds.meta["probe_seed"]
     from oracle.mll import central_perturbations, mll as omll
     from oracle.structured import build_blocks as obuild
@@ -172,7 +202,7 @@ def run_reference(args):
 
     def step(k):
         if k % 7 == 0 or state["bo"] is None:
-            state["bo"] = obuild(ds.X, ds.offsets, ds.reps, ds.theta0)
+            state["bo"] = obuild(ds.X, ds.offsets, ds.reps, ds.theta0, ds.meta.get("kernel", "rbf"))
         omll(state["bo"], ds.y, pts[k % 7], Z)
 
     for k in range(args.warmup):
@@ -204,14 +234,15 @@ def run_ours(args):
     torch.cuda.set_device(local)
     import paper_2510_12128_b200 as P
     P._native.lib()
-    ds = synth.make_config(args.config)
+    group = True if world > 1 else None
+    ctx = P.Context(local, group=group)
+    ds = load_config(args.config, P, ctx)
+    kernel = ds.meta.get("kernel", "rbf")
     seed = ds.meta["probe_seed"]
     dev = torch.device("cuda", local)
     Xd = torch.tensor(ds.X, device=dev)
     yd = torch.tensor(ds.y, device=dev)
     rd = torch.tensor(ds.reps, device=dev)
-    group = True if world > 1 else None
-    ctx = P.Context(local, group=group)
     ws = torch.empty(P.workspace_size(ds.offsets, ds.n_c, ds.d, args.eval_slots), dtype=torch.uint8,
                      device=dev)
     stream = torch.cuda.current_stream(local)
@@ -220,7 +251,7 @@ def run_ours(args):
 
     def step(st, X, y, reps):
         st2, rec = P.train(ctx, X, ds.offsets, reps, y, None, epochs=1, adam_state=st, workspace=ws,
-                           probe_seed=seed, num_probes=8)
+                           probe_seed=seed, num_probes=8, kernel=kernel)
         return st2, rec
 
     def barrier():
@@ -288,7 +319,7 @@ def run_ours(args):
         e0p, e1p = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0p.record(stream)
         for _ in range(reps_ph):
-            blk = P.build_blocks(ctx, Xd, ds.offsets, rd, th0, workspace=ws, eval_slots=args.eval_slots)
+            blk = P.build_blocks(ctx, Xd, ds.offsets, rd, th0, kernel=kernel, workspace=ws, eval_slots=args.eval_slots)
         e1p.record(stream)
         torch.cuda.synchronize()
         phase["build_ms"] = e0p.elapsed_time(e1p) / reps_ph
@@ -336,10 +367,11 @@ def run_ours(args):
         "config": {
             "workload": f"{args.config}: {CONFIG_DESC[args.config]}; step = one Algorithm-1 epoch "
                         "(build preconditioner + 7-point central-difference gradient + Adam)",
-            "n": ds.n, "n_c": ds.n_c, "b": int(ds.offsets[1]), "d": ds.d, "m": 8,
+            "n": ds.n, "n_c": ds.n_c, "b": int(ds.offsets[1]), "b_max": int(np.diff(ds.offsets).max()), "d": ds.d, "m": 8,
+            "kernel": kernel,
             "parallelism": f"perturbation-sharded x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2: per step the preconditioner Linv + H + G(lambda+-) stream "
-                  f"{3 * 8 * ds.n * int(ds.offsets[1]) / 1e6:.0f} MB (> 126 MB L2)",
+                  f"{3 * 8 * float(np.sum(np.diff(ds.offsets).astype(np.float64) ** 2)) / 1e6:.0f} MB (> 126 MB L2)",
             "train_time_50_epochs_s": 50 * ms / args.steps / 1e3,
             "peak_hbm_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
             "dense_n2_f64_gb": 8.0 * ds.n * ds.n / 1e9,
@@ -374,7 +406,7 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C5"])
+    ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--eval-slots", type=int, default=7)
     ap.add_argument("--prof-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")

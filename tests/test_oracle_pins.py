@@ -380,3 +380,47 @@ def test_generator_shapes_and_nonoverlap():
         Xi = ds.X[ds.offsets[i]:ds.offsets[i + 1]]
         assert np.all(np.linalg.norm(Xi - ds.reps[i], axis=1) <= ds.meta["rho"] + 1e-12)
     assert ds.meta["rho"] < ds.meta["l"] / 2
+
+
+# ----------------------------------------------------------------------------- NEXT-1 predict
+def test_predict_structured_equals_dense_Kpp():
+    from oracle import predict as OP
+    ds = synth.g_hyper(n_c=6, b=40, d=2, seed=12, b_test=5)
+    bo = build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    m1, v1 = OP.posterior(bo, ds.y, ds.X_test)
+    m2, v2 = OP.dense_posterior(bo, ds.y, ds.X_test)
+    np.testing.assert_allclose(m1, m2, rtol=1e-9, atol=1e-11)
+    np.testing.assert_allclose(v1, v2, rtol=1e-8, atol=1e-11)
+    # (var may be slightly negative: K* is the exact kernel while K'' approximates the
+    #  off-diagonal blocks, so K** - K*^T K''^{-1} K* is not a Schur complement of one PSD matrix)
+
+
+def test_predict_single_cluster_is_exact_gp_and_sklearn():
+    """n_c = 1 => M = [0] => K'' = K: the textbook GP posterior; sklearn's GaussianProcessRegressor
+    with the same fixed kernel gives the same latent mean and std."""
+    from sklearn.gaussian_process import GaussianProcessRegressor
+    from sklearn.gaussian_process.kernels import RBF as SkRBF, ConstantKernel
+    from oracle import predict as OP
+    rng = np.random.default_rng(3)
+    X = rng.uniform(-2, 2, size=(60, 2))
+    y = np.sin(X[:, 0]) + 0.1 * rng.standard_normal(60)
+    Xt = rng.uniform(-2, 2, size=(7, 2))
+    th = (0.8, 0.05, 1.7)
+    bo = build_blocks(X, np.array([0, 60]), X.mean(axis=0, keepdims=True), th)
+    m, v = OP.posterior(bo, y, Xt)
+    gp = GaussianProcessRegressor(ConstantKernel(th[2], "fixed") * SkRBF(th[0], "fixed"), alpha=th[1],
+                                  optimizer=None, normalize_y=False).fit(X, y)
+    ms, ss = gp.predict(Xt, return_std=True)
+    np.testing.assert_allclose(m, ms, rtol=1e-9, atol=1e-12)
+    np.testing.assert_allclose(np.sqrt(v), ss, rtol=1e-7)
+
+
+def test_predict_one_point_closed_form_spec_365():
+    """one training point, test point at the same location: mean = alpha/(alpha+s2) y."""
+    from oracle import predict as OP
+    X = np.array([[0.3, -0.2]])
+    bo = build_blocks(X, np.array([0, 1]), X, (1.0, 0.5, 2.0))
+    m, v = OP.posterior(bo, np.array([1.7]), X)
+    assert abs(m[0] - 2.0 / 2.5 * 1.7) < 1e-14
+    assert abs(v[0] - (2.0 - 2.0 * 2.0 / 2.5)) < 1e-14
+    assert OP.rmse([1.0, 3.0], [0.0, 0.0]) == pytest.approx(np.sqrt(5.0))
