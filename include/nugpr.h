@@ -222,6 +222,16 @@ nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, const int64_t* 
                          const nugpr_solve_cfg* scfg, double adam_state[10], double* records,
                          void* workspace, size_t ws_bytes);
 
+/* NEXT-1 — posterior at the blocks' theta_0 (build the blocks at the trained theta): Eq. (4)-(5)
+ * (PAPER.md:68-73), mean = K*^T K''^{-1} y, var = alpha - diag(K*^T K''^{-1} K*) (+ sigma^2 when
+ * add_noise; reading P22), with K* = k(X_train, X_test) generated on the fly and K''^{-1} applied
+ * EXACTLY through the Woodbury form of Eq. (28) (no CG; oracle/predict.py gives the algebra).
+ *  y_sorted [host|device] n; X_test [host|device] n_test x d; mean [host|device] n_test;
+ *  var [host|device] n_test or NULL.  Uses the blocks' first evaluation slot as scratch.
+ *  n_c <= 512 in this build (NUGPR_ERR_UNSUPPORTED otherwise). */
+nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y_sorted, const double* X_test,
+                           int64_t n_test, int32_t add_noise, double* mean, double* var);
+
 /* Host-only helpers (no device work; usable without a GPU). */
 /* PAR-1 exchange of nugpr_numgrad CENTRAL: the 7 evaluations theta, theta +- h_i e_i
  * (h_i = step_i theta_i) are owned per nugpr_shard_plan(world, {1,3,3,2,2,2,2}); this rank passes

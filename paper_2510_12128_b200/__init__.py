@@ -20,7 +20,7 @@ import numpy as np
 from . import _native as N
 from ._native import NugprError
 
-__all__ = ["Context", "Blocks", "cluster", "build_blocks", "mll", "numgrad", "train", "adam_step",
+__all__ = ["Context", "Blocks", "cluster", "build_blocks", "predict", "mll", "numgrad", "train", "adam_step",
            "shard_plan", "tridiag_eig", "workspace_size", "NugprError", "version"]
 
 
@@ -309,6 +309,22 @@ def mll(ctx: Context, blocks: Blocks, y_sorted, theta, **solve) -> dict:
     N.check(N.lib().nugpr_mll(ctx.handle, blocks.handle, _ptr(_f64(y_sorted), keep), _theta(theta),
                               C.byref(cfg), C.byref(out)))
     return _rec(out, cfg.num_probes)
+
+
+def predict(ctx: Context, blocks: Blocks, y_sorted, X_test, add_noise: bool = False, variance: bool = True):
+    """NEXT-1: posterior mean (and variance) at the blocks' theta0 (Eq. 4-5, exact structured
+    K''^{-1}).  Returns device tensors (mean, var or None)."""
+    import torch
+    keep = []
+    Xt = _f64(X_test)
+    n_t = int(Xt.shape[0])
+    dev = torch.device("cuda", ctx.device)
+    mean = torch.empty(n_t, dtype=torch.float64, device=dev)
+    var = torch.empty(n_t, dtype=torch.float64, device=dev) if variance else None
+    N.check(N.lib().nugpr_predict(ctx.handle, blocks.handle, _ptr(_f64(y_sorted), keep), _ptr(Xt, keep), n_t,
+                                  int(bool(add_noise)), C.c_void_p(mean.data_ptr()),
+                                  C.c_void_p(var.data_ptr()) if var is not None else None))
+    return mean, var
 
 
 def _grad_cfg(mode="central", step=None, threshold=1e-3, threshold_relative=True, max_halvings=20):

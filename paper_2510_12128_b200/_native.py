@@ -99,6 +99,7 @@ def lib():
                                     C.POINTER(C.c_int32)]),
         "nugpr_numgrad_exchange": (C.c_int, [P, Theta, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "nugpr_predict": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, P, P]),
         "nugpr_adam_step": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double]),
         "nugpr_shard_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
         "nugpr_tridiag_eig": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -122,4 +123,4 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_launch_count", "nugpr_workspace_size", "nugpr_build_blocks", "nugpr_blocks_destroy",
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
             "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster",
-            "nugpr_numgrad_exchange"]
+            "nugpr_numgrad_exchange", "nugpr_predict"]

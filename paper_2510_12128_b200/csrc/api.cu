@@ -180,6 +180,7 @@ struct BlocksDev {
   double* cy = nullptr;       // n_pad: c = R^{-T} y cached across the evaluations of one numgrad
   double* ystage = nullptr;   // n: host y staged to the device
   double* bigscr = nullptr;   // big-block mode: diagonal-block inverses + inverse-step scratch
+  int64_t* pmeta = nullptr;   // predict: one-block layout of C = I + M~ (off, poff, boff, ld, loff, goff)
 };
 
 void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
@@ -213,6 +214,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
   B.cy = c.take<double>(L.n_pad);
   B.ystage = c.take<double>(L.n);
+  B.pmeta = c.take<int64_t>(16);
   if (L.big) B.bigscr = c.take<double>(big_scratch_doubles(n_c, L.ld_max));
   E.assign(slots, EvalDev());
   const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
@@ -1461,6 +1463,90 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
     return NUGPR_OK;
   }
   return fail(NUGPR_ERR_INVALID_ARG, "bad gradient mode");
+}
+
+// ------------------------------------------------------------------------------------------
+// NEXT-1: posterior mean / variance (Eq. 4-5) with the exact structured K''^{-1} (predict_kernels.cu).
+extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, const double* X_test,
+                                      int64_t n_test, int32_t add_noise, double* mean, double* var) {
+  if (!ctx || !bl || !y_sorted || !X_test || !mean) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (n_test < 0) return fail(NUGPR_ERR_INVALID_ARG, "n_test < 0");
+  if (n_test == 0) return NUGPR_OK;
+  const HostLayout& L = bl->L;
+  if (L.n_c > LD_SMALL_MAX) return fail(NUGPR_ERR_UNSUPPORTED, "predict supports n_c <= %d in this build", LD_SMALL_MAX);
+  CK(cudaSetDevice(ctx->device));
+  cudaGetLastError();
+  cudaStream_t s = ctx->stream;
+  const LayoutDev& Ld = bl->Ld;
+  BlocksDev& B = bl->B;
+  EvalDev& e = bl->E[0];
+  const int n_c = L.n_c, d = L.d;
+  const int ldc = (n_c + PAD - 1) / PAD * PAD;
+  const nugpr_theta th = bl->theta0;
+  // chunk of test points bounded by the slot buffers it uses
+  int64_t nt = 256;
+  nt = std::min<int64_t>(nt, L.blk_total / std::max<int64_t>(1, L.n_pad));
+  nt = std::min<int64_t>(nt, (static_cast<int64_t>(MAXC) * L.n_pad) / (3 * std::max(n_c, ldc)));
+  nt = std::min<int64_t>(nt, (static_cast<int64_t>(MAXC) * L.n_pad) / std::max(1, d));
+  if (nt < 1) return fail(NUGPR_ERR_WORKSPACE, "workspace too small for predict");
+  double* Ks = e.G;                       // n_pad x nt (per-cluster column-major)
+  double* W = e.T;                        // same layout
+  double* wc = e.RHS;                     // [n_c][nt] x 3
+  double* ww = wc + static_cast<int64_t>(n_c) * nt;
+  double* p = ww + static_cast<int64_t>(n_c) * nt;
+  double* pc = e.R;                       // ldc x nt
+  double* lp = e.X;                       // ldc x nt
+  double* Cm = e.V;                       // ldc x ldc (C, then Linv_C)
+  double* zeta = e.Tbuf, *sd = e.Tbuf + n_c, *lz = e.Tbuf + 2 * n_c;
+  double* xt = e.Q;                       // nt x d staged test inputs
+  double* ostage = e.dots;                // 2 * nt outputs when the user's buffers are host memory
+  // c = R^{-T} y
+  const double* y_dev = nullptr;
+  RET(stage_y(bl, y_sorted, s, &y_dev));
+  launch_cy(Ld, B.Linv, y_dev, L.ld_max, B.cy, s);
+  // C = I + D^{1/2} M D^{1/2}, its factor and inverse (one-block layout), lz = Linv_C zeta
+  launch_pred_setup(Ld, B.cy, B.u, B.M, ldc, zeta, sd, Cm, s);
+  int64_t hm[16] = {0, n_c, 0, ldc, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // off[2], poff[2], boff[1]
+  int32_t* ldp = reinterpret_cast<int32_t*>(B.pmeta + 8);                     // ld[1]
+  int64_t* zero64 = B.pmeta + 10;                                             // loff = goff = 0
+  int32_t ldh = ldc;
+  CK(cudaMemcpyAsync(B.pmeta, hm, sizeof(hm), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(ldp, &ldh, sizeof(int32_t), cudaMemcpyHostToDevice, s));
+  LayoutDev Lc = Ld;
+  Lc.off = B.pmeta; Lc.poff = B.pmeta + 2; Lc.boff = B.pmeta + 4; Lc.ld = ldp; Lc.n_c = 1;
+  launch_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, s);
+  CKL();
+  int32_t cst = 0;
+  CK(cudaMemcpyAsync(&cst, e.linfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  launch_pred_lz(Cm, ldc, n_c, zeta, lz, s);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  if (cst) return fail(NUGPR_ERR_NOT_SPD, "I + M~ is not SPD (degenerate low-rank term)");
+  const bool xdev = is_device_ptr(X_test), mdev = is_device_ptr(mean), vdev = var ? is_device_ptr(var) : true;
+  const double noise_add = add_noise ? th.noise : 0.0;
+  for (int64_t j0 = 0; j0 < n_test; j0 += nt) {
+    const int m = static_cast<int>(std::min<int64_t>(nt, n_test - j0));
+    const double* xtp = X_test + j0 * d;
+    if (!xdev) {
+      CK(cudaMemcpyAsync(xt, xtp, sizeof(double) * m * d, cudaMemcpyHostToDevice, s));
+      xtp = xt;
+    }
+    launch_pred_ks(B.X, xtp, d, Ld, m, L.ld_max, bl->kind, th.lengthscale, th.outputscale, Ks, s);
+    launch_pred_trmm(B.Linv, Ks, W, B.ld, B.boff, B.poff, n_c, m, L.ld_max, s);
+    launch_pred_reduce(Ld, W, B.cy, B.u, m, wc, ww, p, s);
+    launch_pred_pcol(p, n_c, m, ldc, pc, s);
+    launch_pred_trmm(Cm, pc, lp, ldp, zero64, zero64, 1, m, ldc, s);
+    double* mo = mdev ? mean : ostage;
+    double* vo = var ? (vdev ? var : ostage + nt) : nullptr;
+    launch_pred_final(n_c, m, ldc, wc, ww, pc, lp, zeta, lz, th.outputscale, noise_add, mo, vo,
+                      mdev ? j0 : 0, s);
+    CKL();
+    if (!mdev) CK(cudaMemcpyAsync(mean + j0, ostage, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (var && !vdev) CK(cudaMemcpyAsync(var + j0, ostage + nt, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
+    if (!mdev || (var && !vdev) || !xdev) CK(cudaStreamSynchronize(s));
+  }
+  CK(cudaStreamSynchronize(s));
+  return NUGPR_OK;
 }
 
 // ------------------------------------------------------------------------------------------

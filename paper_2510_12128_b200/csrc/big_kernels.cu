@@ -422,18 +422,43 @@ __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
 #pragma unroll
   for (int q = 0; q < CPT; ++q) acc[q] = 0.0;
   if (useB) {
+    // register double buffering: chunk k0+64 is loaded while chunk k0 is multiplied
+    constexpr int NBV = BNB * BNB / 256, NDV = (BNB * NCP + 255) / 256;
+    double rbv[NBV], rdv[NDV];
+    auto gload = [&](int k0) {
+      const int kc = min(BNB, ld - k0);
+#pragma unroll
+      for (int u = 0; u < NBV; ++u) {
+        const int idx = tid + u * 256;
+        const int rr = idx / BNB, k = idx % BNB;
+        rbv[u] = (rr < nr && k < kc) ? Bi[static_cast<int64_t>(r0 + rr) * ld + k0 + k] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < NDV; ++u) {
+        const int idx = tid + u * 256;
+        const int c = idx / BNB, k = idx % BNB;
+        rdv[u] = (idx < BNB * NCP && c < ncol && k < kc) ? dval(c, c * n_pad + p0 + k0 + k) : 0.0;
+      }
+    };
+    auto sstore = [&]() {
+#pragma unroll
+      for (int u = 0; u < NBV; ++u) {
+        const int idx = tid + u * 256;
+        Bs[(idx % BNB) * BLDS + idx / BNB] = rbv[u];
+      }
+#pragma unroll
+      for (int u = 0; u < NDV; ++u) {
+        const int idx = tid + u * 256;
+        if (idx < BNB * NCP) Ds[(idx % BNB) * NCP + idx / BNB] = rdv[u];
+      }
+    };
+    gload(0);
     for (int k0 = 0; k0 < ld; k0 += BNB) {
       const int kc = min(BNB, ld - k0);
       __syncthreads();
-      for (int idx = tid; idx < BNB * BNB; idx += 256) {
-        const int rr = idx / BNB, k = idx % BNB;     // column r0+rr of B, row k0+k: contiguous in k
-        Bs[k * BLDS + rr] = (rr < nr && k < kc) ? Bi[static_cast<int64_t>(r0 + rr) * ld + k0 + k] : 0.0;
-      }
-      for (int idx = tid; idx < BNB * NCP; idx += 256) {
-        const int c = idx / BNB, k = idx % BNB;
-        Ds[k * NCP + c] = (c < ncol && k < kc) ? dval(c, c * n_pad + p0 + k0 + k) : 0.0;
-      }
+      sstore();
       __syncthreads();
+      if (k0 + BNB < ld) gload(k0 + BNB);
       for (int k = 0; k < kc; ++k) {
         const double bv = Bs[k * BLDS + r];
 #pragma unroll

@@ -64,6 +64,21 @@ void launch_big_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, i
                            int32_t* status, double* logdet_blk, double* u, double* scratch, cudaStream_t s);
 void launch_apply_big(const ApplyArgs& a, int ncp, cudaStream_t s);
 
+// predict_kernels.cu (NEXT-1)
+void launch_pred_ks(const double* X, const double* Xt, int d, const LayoutDev& L, int nt, int ld_max, int kind,
+                    double lam, double alpha, double* Ks, cudaStream_t s);
+void launch_pred_trmm(const double* Lm, const double* Bm, double* Cm, const int32_t* ld, const int64_t* loff,
+                      const int64_t* goff, int groups, int nt, int ld_max, cudaStream_t s);
+void launch_pred_reduce(const LayoutDev& L, const double* W, const double* c, const double* u, int nt, double* wc,
+                        double* ww, double* p, cudaStream_t s);
+void launch_pred_setup(const LayoutDev& L, const double* c, const double* u, const double* M, int ldc, double* zeta,
+                       double* sd, double* Cm, cudaStream_t s);
+void launch_pred_lz(const double* Lc, int ldc, int n_c, const double* zeta, double* lz, cudaStream_t s);
+void launch_pred_pcol(const double* p, int n_c, int nt, int ldc, double* pc, cudaStream_t s);
+void launch_pred_final(int n_c, int nt, int ldc, const double* wc, const double* ww, const double* p, const double* lp,
+                       const double* zeta, const double* lz, double alpha, double noise_add, double* mean, double* var,
+                       int64_t out_off, cudaStream_t s);
+
 // cluster_kernels.cu (row A0)
 void launch_km_absmax(const double* X, int64_t cnt, unsigned long long* out, cudaStream_t s);
 size_t km_assign_smem();

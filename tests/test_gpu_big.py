@@ -116,3 +116,34 @@ def test_C4_matern_build_and_mll_parity(P, ctx):
     l, s, a = th0
     check_eval(P, ctx, bg, bo, y, th0, 204)
     check_eval(P, ctx, bg, bo, y, (l * 1.001, s, a), 204)
+
+
+# ----------------------------------------------------------------------------- NEXT-1 predict
+def test_predict_parity_small_and_C3_shape(P, ctx):
+    from oracle import predict as OP
+    for n_c, b, d, seed in [(6, 40, 2, 12), (50, 120, 8, 13)]:
+        ds = synth.g_hyper(n_c=n_c, b=b, d=d, seed=seed, b_test=3)
+        bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
+        bo = OS.build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+        m, v = P.predict(ctx, bg, ds.y, ds.X_test)
+        mo, vo = OP.posterior(bo, ds.y, ds.X_test)
+        np.testing.assert_allclose(m.cpu().numpy(), mo, rtol=1e-9, atol=1e-11)
+        np.testing.assert_allclose(v.cpu().numpy(), vo, rtol=1e-8, atol=1e-11)
+        m2, v2 = P.predict(ctx, bg, ds.y, ds.X_test, add_noise=True)
+        np.testing.assert_allclose(v2.cpu().numpy() - v.cpu().numpy(), ds.theta0[1], rtol=1e-12)
+
+
+def test_predict_C4_matern_with_variance(P, ctx):
+    """C4 'train + predict with variance': the posterior at theta0 on the 8,000 held-out points."""
+    from oracle import predict as OP
+    g = synth.g_real(N=40000, d=8, seed=104)
+    X, y, off, reps, th0 = c4_dataset()
+    bg = P.build_blocks(ctx, X, off, reps, th0, kernel="matern52")
+    bo = OS.build_blocks(X, off, reps, th0, kind="matern52")
+    Xt = g["X_test"][:1000]
+    m, v = P.predict(ctx, bg, y, Xt)
+    mo, vo = OP.posterior(bo, y, Xt)
+    np.testing.assert_allclose(m.cpu().numpy(), mo, rtol=1e-8, atol=1e-9)
+    np.testing.assert_allclose(v.cpu().numpy(), vo, rtol=1e-7, atol=1e-9)
+    rm = OP.rmse(m.cpu().numpy(), g["y_test"][:1000])
+    assert np.isfinite(rm)                              # (quality at the untrained theta0 is not a pin)
