@@ -1393,7 +1393,7 @@ __global__ void __launch_bounds__(NT) pnew_kernel(const CGState* st, const doubl
 // Low-rank coefficients T = M' S(D) (Eq. 19-21: block i of W M' W^T D is u_i T_i), one warp per
 // row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new) = S(R) +
 // beta o S(P_old) for the active columns (S is linear), and CTA 0 also stores S(P_new).
-constexpr int TROWS = 2;   // rows of T per CTA (NT/32/TROWS warps per row)
+constexpr int TROWS = 8;   // rows of T per CTA (one per warp)
 
 template <int NCP>
 __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
@@ -1453,38 +1453,28 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
     }
   }
   __syncthreads();
-  // TROWS rows per CTA, LRW warps per row splitting j; fixed-order combine of the warp partials
-  constexpr int LRW = (NT / 32) / TROWS;
-  const int i = blockIdx.x * TROWS + wid / LRW;
-  const int q = wid % LRW;
+  const int i = blockIdx.x * TROWS + wid;
+  if (i >= n_c) return;
+  const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
   double t[NCP];
 #pragma unroll
   for (int c = 0; c < NCP; ++c) t[c] = 0.0;
-  if (i < n_c) {
-    const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
 #pragma unroll 4
-    for (int j = q * 32 + lane; j < n_c; j += 32 * LRW) {
-      const double m = Mrow[j];
-      const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
+  for (int j = lane; j < n_c; j += 32) {
+    const double m = Mrow[j];
+    const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
 #pragma unroll
-      for (int c2 = 0; c2 < NCP / 2; ++c2) {
-        const double2 v = sj[c2];
-        t[2 * c2] = fma(m, v.x, t[2 * c2]);
-        t[2 * c2 + 1] = fma(m, v.y, t[2 * c2 + 1]);
-      }
+    for (int c2 = 0; c2 < NCP / 2; ++c2) {
+      const double2 v = sj[c2];
+      t[2 * c2] = fma(m, v.x, t[2 * c2]);
+      t[2 * c2 + 1] = fma(m, v.y, t[2 * c2 + 1]);
     }
   }
 #pragma unroll
   for (int c = 0; c < NCP; ++c) t[c] = warp_sum(t[c]);
-  __shared__ double tpart[NT / 32][NCP];
-  if (lane == 0)
+  if (lane == 0) {
 #pragma unroll
-    for (int c = 0; c < NCP; ++c) tpart[wid][c] = t[c];
-  __syncthreads();
-  if (q == 0 && lane < NCP && i < n_c) {
-    double v = 0.0;
-    for (int w = 0; w < LRW; ++w) v += tpart[wid + w][lane];
-    a.T[i * MAXC + lane] = v;
+    for (int c = 0; c < NCP; ++c) a.T[i * MAXC + c] = t[c];
   }
 }
 
