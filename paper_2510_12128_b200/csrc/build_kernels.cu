@@ -1072,12 +1072,30 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     for (int w = 0; w < nw; ++w) t += red[w];
     return t;
   };
+  // Cross-CTA reductions of one value per CTA: warp 0 reads the CS remote slots (one per lane),
+  // butterfly-sums them (the same fixed order in every CTA, so all CTAs get the same bits) and
+  // broadcasts through shared memory -- instead of every thread reading every remote slot.
+  __shared__ double s_bc[4];
+  int bc_i = 0;
+  auto remote_sum = [&](double* slot, bool is_max) -> double {
+    const int bi = bc_i;
+    bc_i = (bc_i + 1) & 3;
+    if (wid == 0) {
+      double v = (lane < CS) ? *cl.map_shared_rank(slot, lane) : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double w = __shfl_xor_sync(0xffffffffu, v, o);
+        v = is_max ? fmax(v, w) : v + w;
+      }
+      if (lane == 0) s_bc[bi] = v;
+    }
+    __syncthreads();
+    return s_bc[bi];
+  };
   auto cluster_sum = [&](int slot, double v) -> double {
     if (tid == 0) nb[slot] = v;
     cl.sync();
-    double t = 0.0;
-    for (int p = 0; p < CS; ++p) t += *cl.map_shared_rank(nb + slot, p);
-    return t;
+    return remote_sum(nb + slot, false);
   };
   auto store_v = [&](int j, int r, double v) {   // V[j][r0+r]
     a.V[static_cast<int64_t>(j) * n + r0 + r] = v;
@@ -1098,8 +1116,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
   __syncthreads();
   if (tid == 0) { double m = 0.0; for (int w = 0; w < nw; ++w) m = fmax(m, red[w]); nb[2] = m; s_done = 0; s_conv = 0; }
   cl.sync();
-  double knorm = 0.0;
-  for (int p = 0; p < CS; ++p) knorm = fmax(knorm, *cl.map_shared_rank(nb + 2, p));
+  const double knorm = remote_sum(nb + 2, true);
   __shared__ int cnt_sm[LZ_NT];
   __shared__ double lohi[2];
   // v_0: unnormalised start slice in wl, its squared norm partial in nb[3]
@@ -1118,8 +1135,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
   double bprev = 0.0;
   for (int k = 0; k < kmax; ++k) {
     // exchange: v_k = w_{k} / ||w_k|| assembled from every CTA's wl slice (DSMEM), norm from nb[3]
-    double nn = 0.0;
-    for (int p = 0; p < CS; ++p) nn += *cl.map_shared_rank(nb + 3, p);
+    const double nn = remote_sum(nb + 3, false);
     const double inv = 1.0 / sqrt(nn);
     for (int c = tid; c < n; c += LZ_NT) {
       const int p = c / R, rr = c - p * R;
@@ -1148,10 +1164,15 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
         if (lane == 0) hpp[j] = s_;
       }
       cl.sync();
-      for (int j = tid; j <= k; j += LZ_NT) {
-        double t = 0.0;
-        for (int p = 0; p < CS; ++p) t += cl.map_shared_rank(hpp, p)[j];
-        hs[j] = t;
+      // hs[j] = sum over the CTAs of hpp[j]: 16 lanes per j (lane group reads the CS slots),
+      // segmented butterfly over the group
+      for (int base = 0; base < 16 * (k + 1); base += LZ_NT) {   // warp-uniform trip count
+        const int t0 = base + tid;
+        const int j = t0 >> 4, p = t0 & 15;
+        double v = (j <= k && p < CS) ? cl.map_shared_rank(hpp, p)[j] : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (p == 0 && j <= k) hs[j] = v;
       }
       __syncthreads();
       alpha += hs[k];
@@ -1173,8 +1194,7 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     s2 = block_sum(s2);
     if (tid == 0) { al[k] = alpha; nb[3] = s2; }
     cl.sync();                                    // partial norms + new wl visible cluster-wide
-    double nn2 = 0.0;
-    for (int p = 0; p < CS; ++p) nn2 += *cl.map_shared_rank(nb + 3, p);
+    const double nn2 = remote_sum(nb + 3, false);
     const double beta = sqrt(nn2);
     if (tid == 0) be[k] = beta;
     (void)bprev;

@@ -834,7 +834,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
 constexpr int MAXQ = 32;                  // clusters per CTA held in the metadata cache
 
 template <int MTMAX>
-__global__ void __launch_bounds__(NTM, 1) apply_mma_staged_kernel(ApplyArgs a) {
+__global__ void __launch_bounds__(NTM, 2) apply_mma_staged_kernel(ApplyArgs a) {
   constexpr int NCPE = 10;
   if (a.gate && !a.st->any_active) return;
   extern __shared__ __align__(128) double sm[];
@@ -1730,21 +1730,23 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
   }
   const int stage_mode = env_int("NUGPR_APPLY_STAGE", 0); // experimental (no gain at C3 so far)
   if (mma && stage_mode) {
-    ApplyPlan p;
-    p.mma = 2;
-    const size_t fixed_s = static_cast<size_t>(ld_max) * (18 + 19 + LDP + 1) + 16;
-    const size_t budget = static_cast<size_t>(optin) - 8192;
-    p.ctas_per_sm = 1;
-    p.grid = std::min(n_tiles, num_sms());
-    p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
-    if (balance) p.grid = (n_tiles + p.nmine_max - 1) / p.nmine_max;
-    p.slot_doubles = std::max(slot_target, 4 * ld_max);
-    const long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed_s);
-    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
-    p.smem_nob = fixed_s * sizeof(double);
-    p.smem_b = (fixed_s + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
-    p.ok = p.nstage >= 3 && p.nmine_max <= MAXQ;
-    if (p.ok) return p;
+    for (int per = std::min(per_max, 2); per >= 1; --per) {
+      ApplyPlan p;
+      p.mma = 2;
+      const size_t fixed_s = static_cast<size_t>(ld_max) * (18 + 19 + LDP + 1) + 16;
+      const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - 8192;
+      p.ctas_per_sm = per;
+      p.grid = std::min(n_tiles, per * num_sms());
+      p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
+      if (balance) p.grid = (n_tiles + p.nmine_max - 1) / p.nmine_max;
+      p.slot_doubles = std::max(per == 2 ? std::min(slot_target, 2048) : slot_target, 4 * ld_max);
+      const long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed_s);
+      p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+      p.smem_nob = fixed_s * sizeof(double);
+      p.smem_b = (fixed_s + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
+      p.ok = p.nstage >= (per == 2 ? 2 : 3) && p.nmine_max <= MAXQ;
+      if (p.ok) return p;
+    }
   }
   for (int per = per_max; per >= 1; --per) {
     ApplyPlan p;
