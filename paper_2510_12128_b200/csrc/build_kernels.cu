@@ -158,6 +158,9 @@ struct CholArgs {
   double* u;             // [n_pad]
 };
 
+__device__ int g_chol_trace = 0;
+__device__ __forceinline__ bool getenv_flag_chol_trace() { return g_chol_trace != 0; }
+
 __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int ld = a.ld[i];
@@ -168,12 +171,18 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   __shared__ double red[8];
   const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
+  unsigned long long tst[3];
+  const bool trace = getenv_flag_chol_trace();
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[0]));
   __syncthreads();
 
   // ---------------- Cholesky (right-looking, NB-column panels) ----------------
   // Panel Pn is column-major in smem with leading dimension pr (rows contiguous): every
   // per-row sweep is unit-stride across lanes (no bank conflicts).
   double* Pn = sm;
+  long long tph[4] = {0, 0, 0, 0};
+  long long tc0 = clock64();
+  auto tick = [&](int q) { if (tid == 0) { long long t = clock64(); tph[q] += t - tc0; tc0 = t; } };
   for (int k0 = 0; k0 < ld; k0 += NB) {
     const int nb = min(NB, ld - k0);
     const int pr = ld - k0;          // panel rows
@@ -182,28 +191,54 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       Pn[c * pr + r] = A[static_cast<int64_t>(k0 + c) * ld + k0 + r];
     }
     __syncthreads();
+    // one barrier per column: every thread forms the pivot, the rank-1 update of the remaining
+    // panel columns uses the scaled column j formed on the fly (x*inv, the same roundings as
+    // scaling first), and the scaling of the panel's columns is applied after the loop
+    // ccol[j&1][c] mirrors the panel's column j at rows c < nb in a separate array (written by
+    // the step before), so the broadcast reads of the update do not alias its stores
+    tick(0);
+    __shared__ double pdg[NB], pinv[NB], ccol[2][NB];
+    for (int r = tid; r < nb; r += NT) ccol[0][r] = Pn[r];
+    __syncthreads();
     for (int j = 0; j < nb; ++j) {
-      if (tid == 0) {
-        double piv = Pn[j * pr + j];
-        if (!(piv > 0.0)) { fail = 1; piv = 1.0; }
-        Pn[j * pr + j] = sqrt(piv);
-      }
-      __syncthreads();
-      const double inv = 1.0 / Pn[j * pr + j];
-      for (int r = j + 1 + tid; r < pr; r += NT) Pn[j * pr + r] *= inv;
-      __syncthreads();
-      const int ncols = nb - j - 1;
-      const int nrow = pr - j - 1;      // rows j+1.. of the panel
-      for (int idx = tid; idx < ncols * nrow; idx += NT) {
-        const int c = j + 1 + idx / nrow, r = j + 1 + idx % nrow;
-        if (r >= c) Pn[c * pr + r] -= Pn[j * pr + r] * Pn[j * pr + c];
+      double piv = Pn[j * pr + j];
+      if (!(piv > 0.0)) { if (tid == 0) fail = 1; piv = 1.0; }
+      const double dgv = sqrt(piv);
+      const double inv = 1.0 / dgv;
+      if (tid == 0) { pdg[j] = dgv; pinv[j] = inv; }
+      const int cmax_p = nb - 1;
+      const double* cc = ccol[j & 1];
+      double* cn = ccol[(j + 1) & 1];
+      for (int r = j + 1 + tid; r < pr; r += NT) {
+        const double lr = Pn[j * pr + r] * inv;
+        const int cmax = min(r, cmax_p);
+        // groups of 4 columns: all loads of a group are issued before its stores (ILP 4)
+        for (int c0 = j + 1; c0 <= cmax; c0 += 4) {
+          double v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] = (c0 + q <= cmax) ? Pn[(c0 + q) * pr + r] : 0.0;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) v[q] -= lr * (cc[min(c0 + q, NB - 1)] * inv);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (c0 + q <= cmax) Pn[(c0 + q) * pr + r] = v[q];
+          if (c0 == j + 1 && r < nb) cn[r] = v[0];
+        }
       }
       __syncthreads();
     }
     for (int idx = tid; idx < pr * nb; idx += NT) {
       const int c = idx / pr, r = idx % pr;
+      if (r == c) Pn[c * pr + r] = pdg[c];
+      else if (r > c) Pn[c * pr + r] *= pinv[c];
+    }
+    __syncthreads();
+    tick(1);
+    for (int idx = tid; idx < pr * nb; idx += NT) {
+      const int c = idx / pr, r = idx % pr;
       A[static_cast<int64_t>(k0 + c) * ld + k0 + r] = (r >= c) ? Pn[c * pr + r] : 0.0;
     }
+    tick(2);
     // trailing update of the lower triangle: A[t+r][t+c] -= sum_j P[nb+r][j] P[nb+c][j], r >= c,
     // in 64x64 output tiles, 4x4 register tile per thread, coalesced read-modify-write of A.
     const int tr = pr - nb;
@@ -251,7 +286,9 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       }
     }
     __syncthreads();
+    tick(3);
   }
+  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[1]));
   // logdet partial (real rows only; padding diagonal is 1)
   double ls = 0.0;
   for (int r = tid; r < b; r += NT) ls += log(A[static_cast<int64_t>(r) * ld + r]);
@@ -286,16 +323,23 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
     __syncthreads();
     // diagonal tile inverse: thread j < nb solves L_II x = e_j by forward substitution
     if (tid < nb) {
+      // column j of L_II^{-1} by forward substitution, kept in registers (fully unrolled)
       const int j = tid;
-      for (int r = 0; r < nb; ++r) {
+      double x[NB];
+#pragma unroll
+      for (int r = 0; r < NB; ++r) {
         double v = 0.0;
-        if (r >= j) {
+        if (r < nb && r >= j) {
           v = (r == j) ? 1.0 : 0.0;
-          for (int k = j; k < r; ++k) v -= LrT[(I0 + k) * NBP + r] * XdT[j * NBP + k];
+#pragma unroll
+          for (int k = 0; k < r; ++k)
+            if (k >= j) v -= LrT[(I0 + k) * NBP + r] * x[k];
           v /= LrT[(I0 + r) * NBP + r];
         }
-        XdT[j * NBP + r] = v;                  // column j of the inverse
+        x[r] = v;
       }
+#pragma unroll
+      for (int r = 0; r < NB; ++r) XdT[j * NBP + r] = x[r];     // column j of the inverse
     }
     __syncthreads();
     for (int cc0 = 0; cc0 < I0; cc0 += YC) {
@@ -304,9 +348,16 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       for (int idx = tid; idx < nb * ncc; idx += NT) {
         const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
         const double* xc = A + static_cast<int64_t>(c) * ld;
-        double acc = 0.0;
-        for (int k = c; k < I0; ++k) acc = fma(LrT[k * NBP + r], xc[k], acc);
-        Yc[cl * NB + r] = acc;
+        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // independent chains: loads in flight
+        int k = c;
+        for (; k + 3 < I0; k += 4) {
+          a0 = fma(LrT[k * NBP + r], xc[k], a0);
+          a1 = fma(LrT[(k + 1) * NBP + r], xc[k + 1], a1);
+          a2 = fma(LrT[(k + 2) * NBP + r], xc[k + 2], a2);
+          a3 = fma(LrT[(k + 3) * NBP + r], xc[k + 3], a3);
+        }
+        for (; k < I0; ++k) a0 = fma(LrT[k * NBP + r], xc[k], a0);
+        Yc[cl * NB + r] = (a0 + a1) + (a2 + a3);
       }
       __syncthreads();
       // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
@@ -332,10 +383,24 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   // u = Linv * 1_b  (row sums over the real columns); rows >= b are padding => 0
   const int64_t p0 = a.poff[i];
   for (int r = tid; r < ld; r += NT) {
-    double acc = 0.0;
-    if (r < b)
-      for (int k = 0; k <= r; ++k) acc += A[static_cast<int64_t>(k) * ld + r];
-    a.u[p0 + r] = acc;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    if (r < b) {
+      int k = 0;
+      for (; k + 3 <= r; k += 4) {
+        a0 += A[static_cast<int64_t>(k) * ld + r];
+        a1 += A[static_cast<int64_t>(k + 1) * ld + r];
+        a2 += A[static_cast<int64_t>(k + 2) * ld + r];
+        a3 += A[static_cast<int64_t>(k + 3) * ld + r];
+      }
+      for (; k <= r; ++k) a0 += A[static_cast<int64_t>(k) * ld + r];
+    }
+    a.u[p0 + r] = (a0 + a1) + (a2 + a3);
+  }
+  if (tid == 0) {
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[2]));
+    if (trace && blockIdx.x < 4)
+      printf("CHOLG blk %d chol %.1f inv %.1f us | cycles load %lld cols %lld store %lld trail %lld\n", blockIdx.x,
+             (tst[1] - tst[0]) * 1e-3, (tst[2] - tst[1]) * 1e-3, tph[0], tph[1], tph[2], tph[3]);
   }
 }
 
@@ -354,8 +419,6 @@ constexpr int CS_LDMAX = 216;
 
 __device__ __forceinline__ int cofs(int c, int ld) { return c * ld - (c * (c - 1)) / 2; }
 
-__device__ int g_chol_trace = 0;
-__device__ __forceinline__ bool getenv_flag_chol_trace() { return g_chol_trace != 0; }
 
 struct CholSmemArgs {
   CholArgs c;
@@ -604,6 +667,14 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
   CholArgs a{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
   size_t smem = chol_smem_bytes(ld_max);
   smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel));
+  {
+    static int traced = -1;
+    if (traced < 0) {
+      const char* v = getenv("NUGPR_CHOL_TRACE");
+      traced = (v && v[0] == '1') ? 1 : 0;
+      if (traced) cudaMemcpyToSymbol(g_chol_trace, &traced, sizeof(int));
+    }
+  }
   chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
   note_launch(); post_launch("chol_trtri_kernel");
 }
