@@ -161,6 +161,11 @@ struct CholArgs {
 __device__ int g_chol_trace = 0;
 __device__ __forceinline__ bool getenv_flag_chol_trace() { return g_chol_trace != 0; }
 
+__device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int ld = a.ld[i];
@@ -246,42 +251,42 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       const int t0 = k0 + nb;
       const int nt = (tr + 63) / 64;
       const int ntl = nt * (nt + 1) / 2;
-      const int tx = tid & 15, ty = tid >> 4;    // rows tx*4.., cols ty*4..
+      // FP64 DMMA: 8 warps as 2 x 4, warp tile 32 x 16 of each 64x64 output tile, K = nb panel columns
+      const int lane = tid & 31, wid = tid >> 5, wm = wid & 1, wn = wid >> 1;
+      const int qr = lane >> 2, qc = lane & 3;
       for (int tt = 0; tt < ntl; ++tt) {
         int bi = static_cast<int>((sqrt(8.0 * tt + 1.0) - 1.0) * 0.5);
         while (bi * (bi + 1) / 2 > tt) --bi;
         while ((bi + 1) * (bi + 2) / 2 <= tt) ++bi;
         const int bj = tt - bi * (bi + 1) / 2;
-        const int rb = bi * 64 + tx * 4, cb = bj * 64 + ty * 4;   // offsets in the trailing block
-        if (rb >= tr || cb >= tr || rb + 3 < cb) continue;
-        double acc[4][4];
+        const int rw = bi * 64 + wm * 32, cw = bj * 64 + wn * 16;   // warp tile origin (trailing block)
+        double acc[4][2][2];
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
+        for (int m = 0; m < 4; ++m)
 #pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-        for (int j = 0; j < nb; ++j) {
-          const double* pc = Pn + j * pr + nb;
-          double av[4], bv[4];
+          for (int n = 0; n < 2; ++n) { acc[m][n][0] = 0.0; acc[m][n][1] = 0.0; }
+        if (rw < tr && cw < tr && rw + 31 >= cw) {
+          for (int k4 = 0; k4 < nb; k4 += 4) {
+            const double* pk = Pn + (k4 + qc) * pr + nb;            // panel column k4+qc, trailing rows
+            double af[4], bf[2];
 #pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            av[x] = (rb + x < tr) ? pc[rb + x] : 0.0;
-            bv[x] = (cb + x < tr) ? pc[cb + x] : 0.0;
+            for (int m = 0; m < 4; ++m) { const int r = rw + m * 8 + qr; af[m] = (r < tr) ? pk[r] : 0.0; }
+#pragma unroll
+            for (int n = 0; n < 2; ++n) { const int c = cw + n * 8 + qr; bf[n] = (c < tr) ? pk[c] : 0.0; }
+#pragma unroll
+            for (int m = 0; m < 4; ++m)
+#pragma unroll
+              for (int n = 0; n < 2; ++n) dmma_c(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
           }
 #pragma unroll
-          for (int x = 0; x < 4; ++x)
+          for (int m = 0; m < 4; ++m)
 #pragma unroll
-            for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
-        }
+            for (int n = 0; n < 2; ++n)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          const int c = cb + y;
-          if (c >= tr) continue;
-          double* col = A + static_cast<int64_t>(t0 + c) * ld + t0;
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int r = rb + x;
-            if (r < tr && r >= c) col[r] -= acc[x][y];
-          }
+              for (int e = 0; e < 2; ++e) {
+                const int r = rw + m * 8 + qr, c = cw + n * 8 + 2 * qc + e;
+                if (r < tr && c < tr && r >= c) A[static_cast<int64_t>(t0 + c) * ld + t0 + r] -= acc[m][n][e];
+              }
         }
       }
     }
@@ -344,30 +349,54 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
     __syncthreads();
     for (int cc0 = 0; cc0 < I0; cc0 += YC) {
       const int ncc = min(YC, I0 - cc0);
-      // Yc[cl][r] = sum_{k=c}^{I0-1} L[I0+r][k] * Xinv[k][c]   (Xinv rows < I0 final in A)
-      for (int idx = tid; idx < nb * ncc; idx += NT) {
-        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
-        const double* xc = A + static_cast<int64_t>(c) * ld;
-        double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;   // independent chains: loads in flight
-        int k = c;
-        for (; k + 3 < I0; k += 4) {
-          a0 = fma(LrT[k * NBP + r], xc[k], a0);
-          a1 = fma(LrT[(k + 1) * NBP + r], xc[k + 1], a1);
-          a2 = fma(LrT[(k + 2) * NBP + r], xc[k + 2], a2);
-          a3 = fma(LrT[(k + 3) * NBP + r], xc[k + 3], a3);
+      // Y = L[I, c..I0) X[c..I0, cc0:cc0+64) and X[I, cc0:..] = -Xd Y, both on the FP64 tensor
+      // pipe: warp w owns the 8 columns cc0 + 8w.. (one n8 tile) and the 4 m8 tiles of the 32 rows
+      {
+        const int lane = tid & 31, wid = tid >> 5;
+        const int qr = lane >> 2, qc = lane & 3;
+        const int c8 = wid * 8;                               // column offset within the block
+        double acc[4][2];
+#pragma unroll
+        for (int m = 0; m < 4; ++m) { acc[m][0] = 0.0; acc[m][1] = 0.0; }
+        if (c8 < ncc) {
+          const double* xcol = A + static_cast<int64_t>(cc0 + c8 + qr) * ld;   // X[k][cc0+c8+qr]
+          for (int k4 = cc0 + c8; k4 < I0; k4 += 4) {
+            const double bf = xcol[k4 + qc];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const int r = m * 8 + qr;
+              const double af = (r < nb) ? LrT[(k4 + qc) * NBP + r] : 0.0;
+              dmma_c(acc[m][0], acc[m][1], af, bf);
+            }
+          }
         }
-        for (; k < I0; ++k) a0 = fma(LrT[k * NBP + r], xc[k], a0);
-        Yc[cl * NB + r] = (a0 + a1) + (a2 + a3);
+#pragma unroll
+        for (int m = 0; m < 4; ++m)
+#pragma unroll
+          for (int e = 0; e < 2; ++e) Yc[(c8 + 2 * qc + e) * NB + m * 8 + qr] = acc[m][e];
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 4; ++m) { acc[m][0] = 0.0; acc[m][1] = 0.0; }
+        if (c8 < ncc) {
+          for (int k4 = 0; k4 < nb; k4 += 4) {
+            const double bf = Yc[(c8 + qr) * NB + k4 + qc];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const int r = m * 8 + qr;
+              const double af = (r < nb) ? XdT[(k4 + qc) * NBP + r] : 0.0;
+              dmma_c(acc[m][0], acc[m][1], af, bf);
+            }
+          }
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int r = m * 8 + qr, cl = c8 + 2 * qc + e;
+              if (r < nb && cl < ncc) A[static_cast<int64_t>(cc0 + cl) * ld + I0 + r] = -acc[m][e];
+            }
+        }
+        __syncthreads();
       }
-      __syncthreads();
-      // X[I0+r][c] = -sum_{k<=r} Xd[r][k] Yc[k][c]
-      for (int idx = tid; idx < nb * ncc; idx += NT) {
-        const int r = idx % nb, cl = idx / nb, c = cc0 + cl;
-        double acc = 0.0;
-        for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yc[cl * NB + k], acc);
-        A[static_cast<int64_t>(c) * ld + I0 + r] = -acc;
-      }
-      __syncthreads();
     }
     for (int idx = tid; idx < nb * nb; idx += NT) {
       const int r = idx % nb, c = idx / nb;
