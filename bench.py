@@ -27,6 +27,10 @@ import time
 
 import numpy as np
 
+# the 7 concurrent evaluation streams (+ side streams) need more hardware work queues than the
+# default 8, or unrelated streams alias onto one queue and serialise; set before CUDA starts
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 

@@ -14,6 +14,11 @@ provides device memory (the workspace tensor), the stream and the process group.
 from __future__ import annotations
 
 import ctypes as C
+import os
+
+# More hardware work queues than the default 8 for the concurrent evaluation streams (effective
+# when this package is imported before CUDA is initialised in the process).
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 import numpy as np
 

@@ -292,6 +292,7 @@ struct nugpr_ctx {
   cudaStream_t aux_stream[NUGPR_NUM_EVALS + 1] = {nullptr};
   cudaEvent_t ev_aux[NUGPR_NUM_EVALS + 1][2] = {{nullptr}};
   EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
+  cudaEvent_t tl_pre = nullptr;          // NUGPR_TIMELINE: recorded before rhs_init of the next eval
   // instantiated CG graphs keyed by (workspace, layout, slot, ncol, logdet mode)
   std::unordered_map<std::string, cudaGraphExec_t> graphs;
   std::vector<cudaGraph_t> graph_defs;
@@ -1119,6 +1120,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   ra.X = e.X; ra.P0 = e.Pb[0]; ra.SP0 = e.SPb[0]; ra.SR_part = e.SR; ra.rr_part = e.rrp; ra.ncol = ncol;
   ra.cy = bl->cy_ready ? B.cy : nullptr;
   ra.cy_out = nullptr;
+  if (ctx->tl_pre) CK(cudaEventRecord(ctx->tl_pre, s));
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
   const bool useB = P.B != nullptr;
@@ -1358,14 +1360,25 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
     return NUGPR_OK;
   }
   RET(ensure_slot_streams(ctx, slots));
-  CK(cudaEventRecord(ctx->ev_fork, s0));
+  // NUGPR_TIMELINE=1: per-evaluation start / pre-work done / end times (debugging the overlap)
+  static const bool tl_on = [] { const char* v = getenv("NUGPR_TIMELINE"); return v && v[0] == '1'; }();
+  cudaEvent_t tl0 = nullptr, tls[16], tlp[16], tle[16];
   const int nk = static_cast<int>(ks.size());
+  if (tl_on) {
+    cudaEventCreate(&tl0);
+    for (int j = 0; j < nk; ++j) { cudaEventCreate(&tls[j]); cudaEventCreate(&tlp[j]); cudaEventCreate(&tle[j]); }
+    cudaEventRecord(tl0, s0);
+  }
+  CK(cudaEventRecord(ctx->ev_fork, s0));
+  int modes[16] = {0};
   for (int j = 0; j < nk; ++j) {
     const int slot = j % slots;
     cudaStream_t ss = ctx->slot_stream[slot];
     if (j < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
-    int mode = 0;
-    RET(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &mode, &ctx->h_prm[j]));
+    if (tl_on) { cudaEventRecord(tls[j], ss); ctx->tl_pre = tlp[j]; }
+    RET(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j]));
+    ctx->tl_pre = nullptr;
+    if (tl_on) cudaEventRecord(tle[j], ss);
     CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
   }
   for (int slot = 0; slot < std::min(slots, nk); ++slot) {
@@ -1373,6 +1386,18 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
     CK(cudaStreamWaitEvent(s0, ctx->ev_join[slot], 0));
   }
   CK(cudaStreamSynchronize(s0));
+  if (tl_on) {
+    for (int j = 0; j < nk; ++j) {
+      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+      cudaEventElapsedTime(&a0, tl0, tls[j]);
+      cudaEventElapsedTime(&a1, tl0, tlp[j]);
+      cudaEventElapsedTime(&a2, tl0, tle[j]);
+      fprintf(stderr, "[nugpr timeline] eval %d mode %d start %.3f pre-done %.3f end %.3f ms (iters %d)\n", ks[j],
+              modes[j], a0, a1, a2, ctx->h_out[j].iters_q_max);
+      cudaEventDestroy(tls[j]); cudaEventDestroy(tlp[j]); cudaEventDestroy(tle[j]);
+    }
+    cudaEventDestroy(tl0);
+  }
   for (int j = 0; j < nk; ++j) {
     EvalRecord& r = recs[ks[j]];
     r.o = ctx->h_out[j];
