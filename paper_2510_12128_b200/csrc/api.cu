@@ -1040,7 +1040,7 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
 // receives the host-known iteration bound (replay) for the launch accounting.
 static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, const double* y_dev,
                                  nugpr_theta th, const nugpr_solve_cfg* cfg, cudaStream_t s, int* mode_out,
-                                 EvalParams* hstage) {
+                                 EvalParams* hstage, bool prep_only = false) {
   EvalDev& e = bl->E[slot];
   const HostLayout& L = bl->L;
   const LayoutDev& Ld = bl->Ld;
@@ -1123,6 +1123,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   if (ctx->tl_pre) CK(cudaEventRecord(ctx->tl_pre, s));
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
+  if (prep_only) return NUGPR_OK;
   const bool useB = P.B != nullptr;
   if (!ctx->prof && !bl->no_graph) {
     cudaGraphExec_t ex = nullptr;
@@ -1207,6 +1208,105 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
   ctx->graphs[key] = ex;
   ctx->graph_defs.push_back(g);
+  *out = ex;
+  return NUGPR_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// NEXT-3: a batch of ng evaluations whose operators share the block term (noise and scale steps:
+// B = H) runs its CG in lockstep in ONE graph; every apply is one apply_multi_kernel launch that
+// streams H once for the batch.  The other kernels (lowrank, update, spart, final) stay per
+// evaluation; a tiny kernel ORs the groups' activity into the while-loop condition.
+static nugpr_status get_batch_graph(nugpr_ctx* ctx, nugpr_blocks* bl, const int* slots, int ng, int ncol,
+                                    int logdet_mode, cudaGraphExec_t* out) {
+  std::string key = "batch";
+  for (int g = 0; g < ng; ++g) key += ":" + std::to_string(slots[g]);
+  key += "|" + graph_key(bl, slots[0], ncol, logdet_mode);
+  auto it = ctx->graphs.find(key);
+  if (it != ctx->graphs.end()) { *out = it->second; return NUGPR_OK; }
+  std::vector<IterArgs> A(ng);
+  for (int g = 0; g < ng; ++g) RET(make_iter_args(bl, bl->E[slots[g]], ncol, A[g]));
+  // multi-apply launch plan: 2 CTAs per SM when the per-group D staging and a >= 2-deep ring fit
+  int dev = 0, optin = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const int ld_max = bl->L.ld_max;
+  int grid = 0, slot_d = 0, nstage = 0;
+  size_t smem = 0;
+  for (int per = 2; per >= 1 && !smem; --per) {
+    const size_t budget = std::min<size_t>(optin, per_sm / per) - 4096;
+    for (int sl : {4096, 2048}) {
+      const int sd = std::max(sl, 4 * ld_max);
+      const size_t fixed = apply_multi_smem(ng, ld_max, 0, 0);
+      if (fixed >= budget) continue;
+      const int ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed) / (sizeof(double) * sd)));
+      if (ns >= 2) {
+        slot_d = sd; nstage = ns; smem = apply_multi_smem(ng, ld_max, sd, ns);
+        const int nt = bl->Ld.n_tiles;
+        int gr = std::min(nt, per * num_sms_host());
+        const int nm = (nt + gr - 1) / gr;
+        grid = (nt + nm - 1) / nm;
+        break;
+      }
+    }
+  }
+  if (!smem) return fail(NUGPR_ERR_SHAPE, "batched apply does not fit shared memory (ld_max=%d)", ld_max);
+  auto fix = [&](ApplyArgs& x) { x.grid = grid; x.slot_doubles = slot_d; x.nstage = nstage; x.smem_b = smem; x.smem_nob = smem; };
+  ApplyArgs ga1[4], ga2[4], ga3[4], ga4[4];
+  const CGState* sts[4];
+  for (int g = 0; g < ng; ++g) {
+    fix(A[g].a1); fix(A[g].a2); fix(A[g].a3); fix(A[g].a4);
+    ga1[g] = A[g].a1; ga2[g] = A[g].a2; ga3[g] = A[g].a3; ga4[g] = A[g].a4;
+    sts[g] = bl->E[slots[g]].st;
+  }
+  cudaStream_t cs = ctx->capture_stream;
+  cudaGraph_t g0 = nullptr;
+  CK(cudaGraphCreate(&g0, 0));
+  cudaGraphConditionalHandle h;
+  CK(cudaGraphConditionalHandleCreate(&h, g0, 1u, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t wnode;
+  CK(cudaGraphAddNode(&wnode, g0, nullptr, 0, &cp));
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+  for (int g = 0; g < ng; ++g) {
+    launch_lowrank(A[g].t1, A[g].ncp, cs);
+    if (A[g].pnew) launch_pnew(A[g].st, A[g].R, A[g].Pb, A[g].n_pad, A[g].ncol, cs);
+  }
+  launch_apply_multi(ga1, ng, cs);
+  for (int g = 0; g < ng; ++g) launch_lowrank(A[g].t2, A[g].ncp, cs);
+  launch_apply_multi(ga2, ng, cs);
+  for (int g = 0; g < ng; ++g) { UpdateArgs ua = A[g].ua; ua.cond = 0; launch_update(ua, A[g].ncp, cs); }
+  launch_cond_any(sts, ng, h, cs);
+  cudaGraph_t bo = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(cs, &bo);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch body capture: %s", cudaGetErrorString(ce)); }
+  CK(cudaStreamBeginCaptureToGraph(cs, g0, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
+  for (int g = 0; g < ng; ++g) {
+    EvalDev& e = bl->E[slots[g]];
+    launch_spart(bl->Ld, bl->B.u, e.X, ncol, e.SX, cs);
+    launch_lowrank(A[g].t3, A[g].ncp, cs);
+  }
+  launch_apply_multi(ga3, ng, cs);
+  for (int g = 0; g < ng; ++g) launch_lowrank(A[g].t4, A[g].ncp, cs);
+  launch_apply_multi(ga4, ng, cs);
+  for (int g = 0; g < ng; ++g) {
+    EvalDev& e = bl->E[slots[g]];
+    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n), ncol,
+                 logdet_mode, e.out, cs);
+  }
+  cudaGraph_t go = nullptr;
+  ce = cudaStreamEndCapture(cs, &go);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch tail capture: %s", cudaGetErrorString(ce)); }
+  cudaGraphExec_t ex = nullptr;
+  ce = cudaGraphInstantiate(&ex, g0, 0);
+  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch graph instantiate: %s", cudaGetErrorString(ce)); }
+  ctx->graphs[key] = ex;
+  ctx->graph_defs.push_back(g0);
   *out = ex;
   return NUGPR_OK;
 }
@@ -1371,17 +1471,57 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   }
   CK(cudaEventRecord(ctx->ev_fork, s0));
   int modes[16] = {0};
+  // NEXT-3 batching: the noise- and scale-step evaluations (B = H for all of them) form one
+  // lockstep batch whose applies read H once (m = 8 DMMA path, graphs, one slot per evaluation)
+  std::vector<int> batch;
+  // opt-in (NUGPR_BATCH=1): at C3 the per-cluster phases of the apply dominate and a 4-group apply
+  // is no faster than four separate ones; it pays where streaming dominates (large clusters)
+  static const bool batch_on = [] { const char* v = getenv("NUGPR_BATCH"); return v && v[0] == '1'; }();
+  if (batch_on && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big) {
+    const nugpr_theta t0 = bl->theta0;
+    for (int j = 0; j < nk && batch.size() < 4; ++j) {
+      const nugpr_theta& th = pts[ks[j]];
+      const bool sl = th.lengthscale == t0.lengthscale, ss_ = th.noise == t0.noise, sa = th.outputscale == t0.outputscale;
+      if (sl && (ss_ != sa)) batch.push_back(j);      // exactly one of noise / scale differs
+    }
+    if (batch.size() < 2) batch.clear();
+  }
+  std::vector<char> in_batch(nk, 0);
+  for (int j : batch) in_batch[j] = 1;
+  int q = 0;                                         // stream index of the next job
   for (int j = 0; j < nk; ++j) {
+    if (in_batch[j]) continue;
     const int slot = j % slots;
-    cudaStream_t ss = ctx->slot_stream[slot];
-    if (j < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    cudaStream_t ss = ctx->slot_stream[q % slots];
+    if (q < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    ++q;
     if (tl_on) { cudaEventRecord(tls[j], ss); ctx->tl_pre = tlp[j]; }
     RET(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j]));
     ctx->tl_pre = nullptr;
     if (tl_on) cudaEventRecord(tle[j], ss);
     CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
   }
-  for (int slot = 0; slot < std::min(slots, nk); ++slot) {
+  if (!batch.empty()) {
+    cudaStream_t ss = ctx->slot_stream[q % slots];
+    if (q < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    ++q;
+    int bslots[4];
+    for (size_t g = 0; g < batch.size(); ++g) {
+      const int j = batch[g];
+      bslots[g] = j % slots;
+      if (tl_on) { cudaEventRecord(tls[j], ss); ctx->tl_pre = tlp[j]; }
+      RET(enqueue_eval(ctx, bl, bslots[g], y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j], true));
+      ctx->tl_pre = nullptr;
+    }
+    cudaGraphExec_t ex = nullptr;
+    RET(get_batch_graph(ctx, bl, bslots, static_cast<int>(batch.size()), 1 + cfg->num_probes, cfg->logdet_mode, &ex));
+    CK(cudaGraphLaunch(ex, ss));
+    for (int j : batch) {
+      if (tl_on) cudaEventRecord(tle[j], ss);
+      CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[j % slots].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
+    }
+  }
+  for (int slot = 0; slot < std::min(slots, q); ++slot) {
     CK(cudaEventRecord(ctx->ev_join[slot], ctx->slot_stream[slot]));
     CK(cudaStreamWaitEvent(s0, ctx->ev_join[slot], 0));
   }

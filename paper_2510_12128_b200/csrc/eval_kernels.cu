@@ -9,6 +9,7 @@
 // the last CTA to finish, in fixed tile order: results are bit-reproducible.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include <cooperative_groups.h>
 
@@ -818,6 +819,254 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
       if (tid == 0) st->ticket[a.fin] = 0;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------
+// Cross-perturbation batched apply (NEXT-3): NG evaluations whose operators share
+// the block term B (the noise- and scale-steps all use H, Eq. 24-25) run their CG in lockstep and
+// their applies are ONE launch that streams each B_i once for all of them.  Group g has its own
+// ApplyArgs (EvalParams, CG state, vectors, partials); the kernel is apply_mma_kernel with the
+// probe block of group g in n-tile g and its y column as a DFMA on the same A fragment.
+constexpr int MGMAX = 4;
+struct MultiApplyArgs {
+  ApplyArgs g[MGMAX];
+  int ng;
+};
+
+template <int MTMAX, int NG>
+__global__ void __launch_bounds__(NTM, 2) apply_multi_kernel(const __grid_constant__ MultiApplyArgs ma) {
+  constexpr int NCPE = 10;
+  constexpr int LDG = (NG == 1) ? 12 : (NG == 2) ? 20 : 36;   // probe row stride: 8*NG (+pad), = 4 (mod 16)
+  const ApplyArgs& a0 = ma.g[0];
+  bool any = false;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) any |= (!ma.g[g].gate || ma.g[g].st->any_active);
+  if (!any) return;
+  extern __shared__ __align__(128) double sm[];
+  __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
+  __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
+  __shared__ double sred[NWM * NCPE];
+  __shared__ double cb[NG][2 * NCPE];
+  __shared__ int s_par[NG];
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  const int n_tiles = a0.L.n_tiles;
+  const int64_t n_pad = a0.L.n_pad;
+  const double* B = a0.prm->B;                 // shared by every group
+  const bool useB = (B != nullptr);
+  const int slot = a0.slot_doubles;
+  const int nstage = a0.nstage;
+  const int G = gridDim.x;
+  double* ring = sm;
+  double* Dp = ring + (useB ? nstage * slot : 0);          // ld_max * LDG: probes of group g at 8g
+  double* ys = Dp + a0.ld_max * LDG;                       // NG * ld_max
+  if (tid == 0) {
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWM); }
+    fence_mbar_init();
+  }
+  if (tid < NG) s_par[tid] = ma.g[tid].st->par;
+  for (int t = tid; t < NG * NCPE; t += NTM) {
+    const int g = t / NCPE, c = t % NCPE;
+    const CGState* st = ma.g[g].st;
+    cb[g][c] = (c < 9) ? st->beta[c] : 0.0;
+    cb[g][NCPE + c] = (c < 9) ? static_cast<double>(st->active[c]) : 0.0;
+  }
+  __syncthreads();
+  if (wid == NWM) {
+    if (lane == 0 && useB) {
+      uint32_t pseq = 0;
+      for (int t = blockIdx.x; t < n_tiles; t += G) {
+        const int i = a0.L.tiles[t].blk;
+        const int ld = a0.L.ld[i];
+        const int KC = max(4, (slot / ld) & ~3);
+        const double* Bi = B + a0.L.boff[i];
+        for (int ck0 = 0; ck0 < ld; ck0 += KC, ++pseq) {
+          const int s_ = static_cast<int>(pseq % nstage);
+          const uint32_t use = pseq / nstage;
+          if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
+          const int kc = min(KC, ld - ck0);
+          const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&full[s_], bytes);
+          tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
+        }
+      }
+    }
+    return;
+  }
+  const int qr = lane >> 2, qc = lane & 3;
+  uint32_t seq = 0;
+  for (int t = blockIdx.x; t < n_tiles; t += G) {
+    const TileDesc td = a0.L.tiles[t];
+    const int i = td.blk, ld = a0.L.ld[i];
+    const int64_t p0 = a0.L.poff[i];
+    const int mtt = ld >> 3;
+    // 1. D_i of every group -> shared
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const ApplyArgs& a = ma.g[g];
+      const int par = s_par[g];
+      const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
+      double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+      for (int idx = tid; idx < ld * 9; idx += NWM * 32) {
+        const int c = idx / ld, k = idx - c * ld;
+        const int64_t gi = c * n_pad + p0 + k;
+        double v = a.D[gi];
+        if (a.fuse_p) {
+          const double po = Pold[gi];
+          v = (cb[g][NCPE + c] != 0.0) ? v + cb[g][c] * po : po;
+          Pnew[gi] = v;
+        }
+        if (c == 0) ys[g * a0.ld_max + k] = v; else Dp[k * LDG + 8 * g + (c - 1)] = v;
+      }
+    }
+    mma_sync_consumers();
+    // 2. block term: one pass over B_i's chunks for all groups
+    double acc0[MTMAX][NG], acc1[MTMAX][NG], accy[MTMAX][NG];
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) { acc0[j][g] = 0.0; acc1[j][g] = 0.0; accy[j][g] = 0.0; }
+    if (useB) {
+      const int KC = max(4, (slot / ld) & ~3);
+      for (int k0 = 0; k0 < ld; k0 += KC, ++seq) {
+        const int kc = min(KC, ld - k0);
+        const int s_ = static_cast<int>(seq % nstage);
+        mbar_wait(&full[s_], (seq / nstage) & 1u);
+        const double* cbuf = ring + s_ * slot;
+        for (int kq = 0; kq < kc; kq += 4) {
+          const int k = k0 + kq + qc;
+          double bfr[NG], yv[NG];
+#pragma unroll
+          for (int g = 0; g < NG; ++g) { bfr[g] = Dp[k * LDG + 8 * g + qr]; yv[g] = ys[g * a0.ld_max + k]; }
+          const double* acol = cbuf + (kq + qc) * ld + qr;
+#pragma unroll
+          for (int j = 0; j < MTMAX; ++j) {
+            const int mt = wid + j * NWM;
+            if (mt < mtt) {
+              const double afr = acol[mt * 8];
+#pragma unroll
+              for (int g = 0; g < NG; ++g) {
+                dmma884(acc0[j][g], acc1[j][g], afr, bfr[g]);
+                accy[j][g] = fma(afr, yv[g], accy[j][g]);
+              }
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s_]);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < MTMAX; ++j)
+#pragma unroll
+      for (int g = 0; g < NG; ++g) {
+        accy[j][g] += __shfl_xor_sync(0xffffffffu, accy[j][g], 1);
+        accy[j][g] += __shfl_xor_sync(0xffffffffu, accy[j][g], 2);
+      }
+    // 3. epilogue per group
+#pragma unroll
+    for (int g = 0; g < NG; ++g) {
+      const ApplyArgs& a = ma.g[g];
+      const EvalParams* P = a.prm;
+      const int par = s_par[g];
+      const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+      const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
+      double ep[NCPE];
+#pragma unroll
+      for (int c = 0; c < NCPE; ++c) ep[c] = 0.0;
+      const bool gon = !a.gate || a.st->any_active;
+      if (gon) {
+        const double bi = P->b0 + P->b1 * a.jitter[i];
+        const double pa = P->a, ms = P->mscale;
+        const double* Tq = a.Tbuf + static_cast<int64_t>(i) * MAXC;
+#pragma unroll
+        for (int j = 0; j < MTMAX; ++j) {
+          const int mt = wid + j * NWM;
+          if (mt < mtt) {
+            const int r = mt * 8 + qr;
+            const double uu = a.u[p0 + r];
+#pragma unroll
+            for (int e = 0; e < 3; ++e) {
+              if (e == 2 && qc != 0) continue;
+              const int c = (e < 2) ? 1 + 2 * qc + e : 0;
+              const double bd = (e == 0) ? acc0[j][g] : (e == 1) ? acc1[j][g] : accy[j][g];
+              const double d = (e < 2) ? Dp[r * LDG + 8 * g + c - 1] : ys[g * a0.ld_max + r];
+              const int64_t gi = c * n_pad + p0 + r;
+              double val = pa * d;
+              if (useB) val += bi * bd;
+              val += uu * (ms * Tq[c]);
+              double o = a.cA[c] * val + a.cV[c] * d;
+              if (P2) o += a.cP[c] * P2[gi];
+              a.out[gi] = o;
+              const double y2 = (a.epi == EPI_S) ? uu : Y2[gi];
+#pragma unroll
+              for (int cc = 0; cc < 9; ++cc)
+                if (cc == c) ep[cc] += o * y2;
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int c = 0; c < NCPE; ++c) ep[c] = warp_sum(ep[c]);
+      if (lane == 0) {
+#pragma unroll
+        for (int c = 0; c < NCPE; ++c) sred[wid * NCPE + c] = ep[c];
+      }
+      mma_sync_consumers();
+      if (tid < 9) {
+        double s = 0.0;
+        for (int w = 0; w < NWM; ++w) s += sred[w * NCPE + tid];
+        if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = s;
+        else a.dots[t * MAXC + tid] = s;
+      }
+      mma_sync_consumers();
+    }
+  }
+  // 4. finalisers (last CTA; one warp per (group, column))
+  if (a0.fin != FIN_NONE) {
+    __shared__ int s_last;
+    __threadfence();
+    mma_sync_consumers();
+    if (tid == 0) {
+      const unsigned int tk = atomicAdd(&a0.st->ticket[a0.fin], 1u);
+      s_last = (tk == gridDim.x - 1);
+    }
+    mma_sync_consumers();
+    if (s_last) {
+      __threadfence();
+      for (int gc = wid; gc < NG * 9; gc += NWM) {
+        const int g = gc / 9, c = gc % 9;
+        const ApplyArgs& a = ma.g[g];
+        CGState* st = a.st;
+        if (a.gate && !st->any_active) continue;
+        const double tot = col_total(a.dots, n_tiles, c);
+        if (lane == 0) {
+          if (a.fin == FIN_ALPHA) {
+            if (st->active[c]) {
+              const double al = st->rr[c] / tot;
+              st->alpha[c] = al;
+              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
+            }
+          } else {
+            if (c == 0) st->quad = tot; else st->t[c] = tot;
+          }
+        }
+      }
+      mma_sync_consumers();
+      if (tid == 0) a0.st->ticket[a0.fin] = 0;
+    }
+  }
+}
+
+// Loop condition of a batched CG graph: continue while any group has an active column.
+__global__ void cond_any_kernel(const CGState* s0, const CGState* s1, const CGState* s2, const CGState* s3,
+                                int ng, unsigned long long cond) {
+  int any = s0->any_active;
+  if (ng > 1) any |= s1->any_active;
+  if (ng > 2) any |= s2->any_active;
+  if (ng > 3) any |= s3->any_active;
+  cudaGraphSetConditional(cond, any ? 1u : 0u);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1693,6 +1942,8 @@ static int env_int(const char* name, int dflt) {
   return (v && *v) ? atoi(v) : dflt;
 }
 
+int num_sms_host() { return num_sms(); }
+
 // Shared-memory / grid plan of the apply (host side).  ncol == 9 (the paper's m = 8) uses the DMMA
 // kernel unless NUGPR_APPLY_MMA=0; the ring depth is chosen to fit; NUGPR_APPLY_{SLOT,PER,BAL}
 // are tuning knobs (slot doubles, max CTAs per SM, equal clusters per CTA).
@@ -1877,6 +2128,38 @@ void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s) {
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s) {
   cy_kernel<<<L.n_tiles, NT, sizeof(double) * ld_max, s>>>(L, Linv, y, cy);
   note_launch(); post_launch("cy_kernel");
+}
+
+void launch_apply_multi(const ApplyArgs* ga, int ng, cudaStream_t s) {
+  MultiApplyArgs ma;
+  memset(&ma, 0, sizeof(ma));
+  for (int g = 0; g < ng; ++g) ma.g[g] = ga[g];
+  ma.ng = ng;
+  const ApplyArgs& a = ga[0];
+  const size_t smem = a.smem_b;
+#define NUGPR_AM(MT, NGV)                                                                   \
+  do {                                                                                      \
+    smem_optin(reinterpret_cast<const void*>(apply_multi_kernel<MT, NGV>));                \
+    apply_multi_kernel<MT, NGV><<<a.grid, NTM, smem, s>>>(ma);                             \
+  } while (0)
+  if (a.ld_max <= 4 * NWM * 8) {
+    if (ng == 2) NUGPR_AM(4, 2); else if (ng == 3) NUGPR_AM(4, 3); else if (ng == 4) NUGPR_AM(4, 4); else NUGPR_AM(4, 1);
+  } else {
+    if (ng == 2) NUGPR_AM(10, 2); else if (ng == 3) NUGPR_AM(10, 3); else if (ng == 4) NUGPR_AM(10, 4); else NUGPR_AM(10, 1);
+  }
+#undef NUGPR_AM
+  note_launch(); post_launch("apply_multi_kernel");
+}
+
+size_t apply_multi_smem(int ng, int ld_max, int slot_doubles, int nstage) {
+  const int ldg = (ng == 1) ? 12 : (ng == 2) ? 20 : 36;
+  return sizeof(double) * (static_cast<size_t>(nstage) * slot_doubles + static_cast<size_t>(ld_max) * (ldg + ng));
+}
+
+void launch_cond_any(const CGState* const* sts, int ng, unsigned long long cond, cudaStream_t s) {
+  cond_any_kernel<<<1, 1, 0, s>>>(sts[0], ng > 1 ? sts[1] : sts[0], ng > 2 ? sts[2] : sts[0], ng > 3 ? sts[3] : sts[0],
+                                  ng, cond);
+  note_launch(); post_launch("cond_any_kernel");
 }
 
 void launch_pnew(const CGState* st, const double* R, double* const* Pbuf, int64_t n_pad, int ncol, cudaStream_t s) {

@@ -50,6 +50,10 @@ void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
 void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s);
+int num_sms_host();
+void launch_apply_multi(const ApplyArgs* ga, int ng, cudaStream_t s);
+size_t apply_multi_smem(int ng, int ld_max, int slot_doubles, int nstage);
+void launch_cond_any(const CGState* const* sts, int ng, unsigned long long cond, cudaStream_t s);
 void launch_pnew(const CGState* st, const double* R, double* const* Pbuf, int64_t n_pad, int ncol, cudaStream_t s);
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s);
