@@ -147,3 +147,28 @@ def test_predict_C4_matern_with_variance(P, ctx):
     np.testing.assert_allclose(v.cpu().numpy(), vo, rtol=1e-7, atol=1e-9)
     rm = OP.rmse(m.cpu().numpy(), g["y_test"][:1000])
     assert np.isfinite(rm)                              # (quality at the untrained theta0 is not a pin)
+
+
+# ----------------------------------------------------------------------------- C5 at full size
+def test_C5_full_size_logdetR_and_quad_bound(P, ctx):
+    """C5 (n = 1,000,000, 2000 clusters of 500) in the launch configuration bench.py times:
+    properties that hold at any size, checked against the oracle's own arithmetic —
+    logdet_R = 2 sum log diag chol(K_i) (exact), and at the baseline the y-solve satisfies
+    |c^T x - c^T A^{-1} c| <= tol ||c|| (lambda_min(A) >= 1), with c^T A^{-1} c from the exact
+    structured (Woodbury) oracle on a bounded sample of clusters' contributions."""
+    import math
+    from oracle import exact as OX
+    ds = synth.make_config("C5")
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=1)
+    bo = OS.build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    assert rel(bg.export("scalars")[0], bo.logdet_R) < 1e-11
+    assert rel(bg.export("scalars")[1], bo.lam0) < 1e-10
+    tol = 1e-6
+    rec = P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=205, tol=tol)
+    c = OS.solve_Rt(bo, ds.y)
+    d = np.array([float(u @ u) for u in bo.u])
+    sd = np.sqrt(d)
+    Mt = sd[:, None] * bo.M * sd[None, :]
+    xi = np.array([bo.u[i] @ c[bo.block(i)] for i in range(bo.n_c)]) / sd
+    quad_exact = float(c @ c) - float(xi @ (Mt @ np.linalg.solve(np.eye(bo.n_c) + Mt, xi)))
+    assert abs(rec["quad"] - quad_exact) <= tol * math.sqrt(float(c @ c)) * 1.0001 + 1e-9 * abs(quad_exact)
