@@ -51,6 +51,8 @@ def mll(blocks: Blocks, y, theta, Z, tol=0.01, max_iter=2000, replay=None,
     Z = np.asarray(Z, dtype=np.float64)
     m = Z.shape[0]
     c = solve_Rt(blocks, y)                                  # transformed RHS R^{-T} y
+    if logdet_mode == "mbcg":
+        return _mll_mbcg(blocks, op, y, c, Z, tol, max_iter, replay)
     ry = None if replay is None else [replay[0]]
     rq = None if replay is None else list(replay[1:1 + m])
     sol_y = cg_batched(op.apply, c, tol, max_iter, ry)      # Alg. 1
@@ -69,6 +71,25 @@ def mll(blocks: Blocks, y, theta, Z, tol=0.01, max_iter=2000, replay=None,
                      iters_y=int(sol_y.iters[0]), iters_q=[int(k) for k in sol_q.iters],
                      resid_y=float(sol_y.resid[0]), resid_q_max=float(np.max(sol_q.resid)),
                      t=t, s=s, mode=op.mode)
+
+
+def _mll_mbcg(blocks, op, y, c, Z, tol, max_iter, replay) -> MLLRecord:
+    """NEXT-4 (GPyTorch-style mBCG): ONE batched CG on A with
+    the columns [c, z_1..z_m] (x_0 = 0, per-column alpha/beta and freezing as in cg_batched);
+    quad = c^T x_c; each probe's CG coefficients give A's Lanczos tridiagonal (same formulas as
+    for Q(A)), and z^T log(A) z ~ ||z||^2 sum_l tau_l^2 log(theta_l).  No Pade term (NaN)."""
+    m = Z.shape[0]
+    sol = cg_batched(op.apply, np.column_stack([c, Z.T]), tol, max_iter, replay)
+    quad = float(c @ sol.X[:, 0])
+    znorm2 = np.einsum("ij,ij->i", Z, Z)
+    s = np.array([slq_term(sol.alphas[1 + j], sol.betas[1 + j], znorm2[j], f=np.log) for j in range(m)])
+    logdet_slq = blocks.logdet_R + float(np.mean(s))
+    n = y.shape[0]
+    L = 0.5 * (quad + logdet_slq + n * LOG2PI)
+    return MLLRecord(L=L, quad=quad, logdet=logdet_slq, logdet_pade=float("nan"), logdet_slq=logdet_slq,
+                     logdet_R=blocks.logdet_R, lambda0=op.lam0, iters_y=int(sol.iters[0]),
+                     iters_q=[int(k) for k in sol.iters[1:]], resid_y=float(sol.resid[0]),
+                     resid_q_max=float(np.max(sol.resid[1:])), t=None, s=s, mode=op.mode)
 
 
 def central_perturbations(theta, step=(1e-3, 1e-3, 1e-3)):

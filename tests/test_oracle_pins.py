@@ -424,3 +424,54 @@ def test_predict_one_point_closed_form_spec_365():
     assert abs(m[0] - 2.0 / 2.5 * 1.7) < 1e-14
     assert abs(v[0] - (2.0 - 2.0 * 2.0 / 2.5)) < 1e-14
     assert OP.rmse([1.0, 3.0], [0.0, 0.0]) == pytest.approx(np.sqrt(5.0))
+
+
+# --------------------------------------------------------------------------- NEXT-4 mBCG estimator
+def test_mbcg_baseline_tight_tol_is_exact_log_quadform():
+    """At the baseline A = I + W M W^T has <= n_c + 1 distinct eigenvalues, so tight-tol CG on A
+    terminates with an exact Lanczos quadrature: s_j = z^T log(A) z (closed form), quad = Woodbury."""
+    ds = small(5, 14, 2, seed=21)
+    b = build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    Z = synth.probes(5, 4, ds.n)
+    rec = mll(b, ds.y, ds.theta0, Z, tol=1e-11, logdet_mode="mbcg")
+    _, quad_ex, logdet_ex = exact.exact_structured(ds.X, ds.offsets, ds.reps, ds.y, ds.theta0)
+    assert rec.quad == pytest.approx(quad_ex, rel=1e-10)
+    for j in range(4):
+        sj = exact.probe_quadform_baseline(b, Z[j], np.log)
+        assert rec.s[j] == pytest.approx(sj, rel=1e-8, abs=1e-8)
+    assert max(rec.iters_q) <= b.n_c + 1
+    assert math.isnan(rec.logdet_pade) and rec.logdet == rec.logdet_slq
+
+
+def test_mbcg_perturbed_full_krylov_matches_dense_log():
+    """Off the baseline (noise step: A = I + WMW^T + d H), CG run to n iterations on a tiny n is
+    a full Lanczos: z^T log(A) z equals the dense eigen-decomposition value."""
+    ds = small(3, 8, 2, seed=23)
+    b = build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    l, s, a = ds.theta0
+    th = (l, 1.3 * s, a)
+    Z = synth.probes(9, 3, ds.n)
+    rec = mll(b, ds.y, th, Z, tol=1e-13, max_iter=ds.n, logdet_mode="mbcg")
+    op = Operator(b, th)
+    A = op.apply(np.eye(ds.n))
+    w, V = np.linalg.eigh(0.5 * (A + A.T))
+    for j in range(3):
+        zl = float(Z[j] @ (V @ (np.log(w) * (V.T @ Z[j]))))
+        assert rec.s[j] == pytest.approx(zl, rel=1e-7, abs=1e-8)
+    c = solve_Rt(b, ds.y)
+    assert rec.quad == pytest.approx(float(c @ np.linalg.solve(A, c)), rel=1e-10)
+
+
+def test_mbcg_vs_pade_estimators_agree_within_pade_bias():
+    """Same probes: the SLQ-on-A and Pade-on-Q(A) log-dets agree within the Pade bias + CG error
+    (Pade bias <= 3e-5 relative at lambda = 0.5 l)."""
+    ds = small(6, 30, 3, seed=24)
+    b = build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    Z = synth.probes(2, 8, ds.n)
+    l, s, a = ds.theta0
+    for th in [ds.theta0, (1.01 * l, s, a)]:
+        r1 = mll(b, ds.y, th, Z, tol=1e-8, logdet_mode="mbcg")
+        r2 = mll(b, ds.y, th, Z, tol=1e-8)
+        assert r1.logdet_slq == pytest.approx(r2.logdet_slq, rel=1e-7)
+        assert r1.logdet == pytest.approx(r2.logdet_pade, rel=1e-3)
+        assert r1.quad == pytest.approx(r2.quad, rel=1e-9)
