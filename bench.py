@@ -255,7 +255,8 @@ def run_ours(args):
 
     def step(st, X, y, reps):
         st2, rec = P.train(ctx, X, ds.offsets, reps, y, None, epochs=1, adam_state=st, workspace=ws,
-                           probe_seed=seed, num_probes=8, kernel=kernel)
+                           probe_seed=seed, num_probes=8, kernel=kernel, block_storage=args.blocks,
+                           logdet=args.logdet)
         return st2, rec
 
     def barrier():
@@ -329,7 +330,8 @@ def run_ours(args):
         phase["build_ms"] = e0p.elapsed_time(e1p) / reps_ph
         e0p.record(stream)
         for _ in range(reps_ph):
-            P.numgrad(ctx, blk, yd, th0, probe_seed=seed, num_probes=8)
+            P.numgrad(ctx, blk, yd, th0, probe_seed=seed, num_probes=8, block_storage=args.blocks,
+                      logdet=args.logdet)
         e1p.record(stream)
         torch.cuda.synchronize()
         phase["numgrad_ms"] = e0p.elapsed_time(e1p) / reps_ph
@@ -367,12 +369,13 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None,
+        "dtype": "f64" if args.blocks == "f64" else "f64 (FP32-stored H/G blocks)", "data": "synthetic",
         "config": {
             "workload": f"{args.config}: {CONFIG_DESC[args.config]}; step = one Algorithm-1 epoch "
                         "(build preconditioner + 7-point central-difference gradient + Adam)",
             "n": ds.n, "n_c": ds.n_c, "b": int(ds.offsets[1]), "b_max": int(np.diff(ds.offsets).max()), "d": ds.d, "m": 8,
-            "kernel": kernel,
+            "kernel": kernel, "logdet": args.logdet, "block_storage": args.blocks,
             "parallelism": f"perturbation-sharded x{world}" if world > 1 else "single GPU",
             "l2": "inputs larger than L2: per step the preconditioner Linv + H + G(lambda+-) stream "
                   f"{3 * 8 * float(np.sum(np.diff(ds.offsets).astype(np.float64) ** 2)) / 1e6:.0f} MB (> 126 MB L2)",
@@ -413,6 +416,10 @@ def main():
     ap.add_argument("--config", default="C3", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--eval-slots", type=int, default=7)
     ap.add_argument("--prof-steps", type=int, default=2)
+    ap.add_argument("--blocks", default="f64", choices=["f64", "f32"],
+                    help="storage of the streamed blocks H/G (f32: reading X6 fast path, 1e-3 bar)")
+    ap.add_argument("--logdet", default="pade", choices=["pade", "slq", "mbcg"],
+                    help="log-det estimator (mbcg: NEXT-4, one CG on A, SLQ with f = log)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:

@@ -66,7 +66,15 @@ typedef enum {
   NUGPR_RBF_AS_PRINTED = 2  /* Eq. 2 literally: alpha*exp(-||x-x'||_2/(2 lambda^2)) */
 } nugpr_kernel;
 
-typedef enum { NUGPR_LOGDET_PADE = 0, NUGPR_LOGDET_SLQ = 1 } nugpr_logdet_mode;
+/* PADE: Eq. (16) (Pade on Q(A)^{-1} z, literal P(A)); SLQ: Lanczos on Q(A) from the same CG's
+ * coefficients (reading X1).  MBCG: ONE batched CG on A with [c, Z]
+ * (1 apply per iteration), log-det by SLQ with f = log on A's own Lanczos tridiagonal;
+ * logdet_pade is NaN in that mode. */
+typedef enum { NUGPR_LOGDET_PADE = 0, NUGPR_LOGDET_SLQ = 1, NUGPR_LOGDET_MBCG = 2 } nugpr_logdet_mode;
+/* Storage of the blocks the apply streams (reading X6): FP64 (the parity path, 1e-6), or an FP32
+ * copy of H / G(lambda') read by the FP64-accumulating DMMA apply (half the HBM bytes of the
+ * dominant kernel; 1e-3 bar).  FP32 needs the m = 8 DMMA path and clusters <= 512 points. */
+typedef enum { NUGPR_BLOCKS_F64 = 0, NUGPR_BLOCKS_F32 = 1 } nugpr_block_storage;
 typedef enum { NUGPR_GRAD_CENTRAL = 0, NUGPR_GRAD_FORWARD_HALVING = 1 } nugpr_grad_mode;
 typedef enum { NUGPR_REP_GIVEN = 0, NUGPR_REP_CENTROID = 1, NUGPR_REP_MEDOID = 2 } nugpr_rep_mode;
 
@@ -86,7 +94,7 @@ typedef struct {
   const double* probes;        /* NULL, or device m x n matrix of +-1 in cluster-sorted order */
   const int32_t* replay_iters; /* [host] NULL, or 1+m iteration counts to run exactly (parity replay) */
   int32_t logdet_mode;         /* nugpr_logdet_mode used for L */
-  int32_t reserved;
+  int32_t block_storage;       /* nugpr_block_storage: storage of the streamed blocks H / G in the apply */
 } nugpr_solve_cfg;
 
 typedef struct {
@@ -222,13 +230,26 @@ nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, const int64_t* 
                          const nugpr_solve_cfg* scfg, double adam_state[10], double* records,
                          void* workspace, size_t ws_bytes);
 
+/* NEXT-2 — the EXACT structured MLL at the blocks' theta_0, from the
+ * structure of Eq. (28)-(29) with no probes, Pade or CG: W = R^{-T}E has
+ * disjoint columns u_i, D = diag(u_i^T u_i), M~ = D^{1/2} M D^{1/2}, C = I + M~ = L_C L_C^T,
+ * c = R^{-T} y, zeta_i = u_i^T c_i / sqrt(d_i):
+ *     log|K''| = logdet_R + log|C|                                  (matrix determinant lemma)
+ *     y^T K''^{-1} y = c^T c - (zeta^T zeta - ||L_C^{-1} zeta||^2)  (Woodbury, M~ C^{-1} = I - C^{-1})
+ *     L = (quad + log|K''| + n log 2 pi) / 2.
+ *  y_sorted [host|device] n.  out [host] 4 doubles: {L, quad, logdet, log|C|}.
+ *  Uses the blocks' first evaluation slot as scratch (same n_c bound as nugpr_predict).
+ *  NUGPR_ERR_NOT_SPD if C is not SPD (lambda_0 did not make M PSD). */
+nugpr_status nugpr_mll_exact(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y_sorted, double out[4]);
+
 /* NEXT-1 — posterior at the blocks' theta_0 (build the blocks at the trained theta): Eq. (4)-(5)
  * (PAPER.md:68-73), mean = K*^T K''^{-1} y, var = alpha - diag(K*^T K''^{-1} K*) (+ sigma^2 when
  * add_noise; reading P22), with K* = k(X_train, X_test) generated on the fly and K''^{-1} applied
  * EXACTLY through the Woodbury form of Eq. (28) (no CG; oracle/predict.py gives the algebra).
  *  y_sorted [host|device] n; X_test [host|device] n_test x d; mean [host|device] n_test;
  *  var [host|device] n_test or NULL.  Uses the blocks' first evaluation slot as scratch.
- *  n_c <= 512 in this build (NUGPR_ERR_UNSUPPORTED otherwise). */
+ *  Any n_c whose (n_c rounded up to 8)^2 doubles fit in one slot vector (16 n_pad doubles; else
+ *  NUGPR_ERR_WORKSPACE); n_c > 512 factorises I + M~ with the blocked big-block kernels. */
 nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y_sorted, const double* X_test,
                            int64_t n_test, int32_t add_noise, double* mean, double* var);
 

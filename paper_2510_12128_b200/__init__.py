@@ -283,7 +283,7 @@ def build_blocks(ctx: Context, X_sorted, offsets, reps, theta0, kernel: str = "r
 
 
 def _solve_cfg(num_probes=8, tol=0.01, max_iter=2000, probe_seed=0, probes=None, replay=None,
-               logdet="pade", keep=None):
+               logdet="pade", block_storage="f64", keep=None):
     cfg = N.SolveCfg()
     cfg.cg_tol = float(tol)
     cfg.cg_max_iter = int(max_iter)
@@ -294,7 +294,8 @@ def _solve_cfg(num_probes=8, tol=0.01, max_iter=2000, probe_seed=0, probes=None,
         r = np.ascontiguousarray(replay, dtype=np.int32)
         keep.append(r)
         cfg.replay_iters = r.ctypes.data
-    cfg.logdet_mode = {"pade": 0, "slq": 1}[logdet]
+    cfg.logdet_mode = {"pade": 0, "slq": 1, "mbcg": 2}[logdet]
+    cfg.block_storage = {"f64": 0, "f32": 1}[block_storage]
     return cfg
 
 
@@ -330,6 +331,15 @@ def predict(ctx: Context, blocks: Blocks, y_sorted, X_test, add_noise: bool = Fa
                                   int(bool(add_noise)), C.c_void_p(mean.data_ptr()),
                                   C.c_void_p(var.data_ptr()) if var is not None else None))
     return mean, var
+
+
+def mll_exact(ctx: Context, blocks: Blocks, y_sorted) -> dict:
+    """NEXT-2: the exact structured MLL at the blocks' theta0 (determinant lemma + Woodbury on
+    Eq. (28)-(29); no probes, Pade or CG)."""
+    keep = []
+    out = (C.c_double * 4)()
+    N.check(N.lib().nugpr_mll_exact(ctx.handle, blocks.handle, _ptr(_f64(y_sorted), keep), out))
+    return {"L": out[0], "quad": out[1], "logdet": out[2], "logdet_C": out[3]}
 
 
 def _grad_cfg(mode="central", step=None, threshold=1e-3, threshold_relative=True, max_halvings=20):

@@ -39,7 +39,7 @@ class Theta(C.Structure):
 class SolveCfg(C.Structure):
     _fields_ = [("cg_tol", C.c_double), ("cg_max_iter", C.c_int32), ("num_probes", C.c_int32),
                 ("probe_seed", C.c_uint64), ("probes", C.c_void_p), ("replay_iters", C.c_void_p),
-                ("logdet_mode", C.c_int32), ("reserved", C.c_int32)]
+                ("logdet_mode", C.c_int32), ("block_storage", C.c_int32)]
 
 
 class GradCfg(C.Structure):
@@ -100,6 +100,7 @@ def lib():
         "nugpr_numgrad_exchange": (C.c_int, [P, Theta, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "nugpr_predict": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, P, P]),
+        "nugpr_mll_exact": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
         "nugpr_adam_step": (C.c_int, [C.POINTER(C.c_double), C.POINTER(C.c_double), C.c_double]),
         "nugpr_shard_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
         "nugpr_tridiag_eig": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -123,4 +124,4 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_launch_count", "nugpr_workspace_size", "nugpr_build_blocks", "nugpr_blocks_destroy",
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
             "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster",
-            "nugpr_numgrad_exchange", "nugpr_predict"]
+            "nugpr_numgrad_exchange", "nugpr_predict", "nugpr_mll_exact"]

@@ -172,6 +172,7 @@ struct BlocksDev {
   TileDesc* tiles = nullptr, *ctasks = nullptr;
   double* X = nullptr, *reps = nullptr;
   double* Linv = nullptr, *H = nullptr;
+  float* H32 = nullptr;       // FP32-stored H (NUGPR_BLOCKS_F32)
   double* u = nullptr, *jitter = nullptr, *logdet_blk = nullptr;
   double* scal = nullptr;     // [0] logdet_R, [1] lam0
   double* Krep = nullptr, *M = nullptr, *v0 = nullptr, *lz = nullptr;
@@ -202,6 +203,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.reps = c.take<double>(static_cast<size_t>(n_c) * L.d);
   B.Linv = c.take<double>(L.blk_total);
   B.H = c.take<double>(L.blk_total);
+  B.H32 = reinterpret_cast<float*>(c.take<double>((L.blk_total + 1) / 2));
   B.u = c.take<double>(L.n_pad);
   B.jitter = c.take<double>(n_c);
   B.logdet_blk = c.take<double>(n_c);
@@ -373,7 +375,9 @@ struct nugpr_blocks {
   bool cy_ready = false;      // B.cy holds c = R^{-T} y for the current numgrad call
   bool no_graph = false;      // NUGPR_NO_GRAPH=1: direct launches with host polling
   const void* ws_base = nullptr;
-  int iter_kernels = 5;       // kernels per CG iteration in the graph (launch accounting)
+  bool pnew = false;          // the CG iteration launches pnew_kernel (launch accounting)
+  bool f32 = false;           // current evaluation streams FP32-stored blocks
+  bool h32_ready = false;     // H32 holds the FP32 copy of H
 };
 
 extern "C" {
@@ -902,9 +906,10 @@ struct IterArgs {
   double* Pb[2] = {nullptr, nullptr};
   int64_t n_pad = 0;
   int ncol = 0;
+  bool mbcg = false;       // NEXT-4: one apply per iteration (CG on A for every column)
 };
 
-static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterArgs& A) {
+static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterArgs& A, bool mbcg = false) {
   const HostLayout& L = bl->L;
   const LayoutDev& Ld = bl->Ld;
   const BlocksDev& B = bl->B;
@@ -935,6 +940,10 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     a1.dbg = dbg ? atoi(dbg) : 0;
     a1.mma = pl.mma;
     a1.lds = pl.lds;
+    if (bl->f32) {
+      if (pl.mma != 1) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs the m = 8 DMMA apply");
+      a1.f32 = 1;
+    }
   }
   ApplyArgs& a2 = A.a2;
   a2 = a1;
@@ -995,7 +1004,16 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   if (L.big) {                                   // S partials are per 64-row tile
     A.t1.task0 = bl->B.tile0; A.t2.task0 = bl->B.tile0; A.t3.task0 = bl->B.tile0; A.t4.task0 = bl->B.tile0;
   }
-  bl->iter_kernels = A.pnew ? 6 : 5;
+  if (mbcg) {
+    // NEXT-4 (mBCG on A): apply 1 alone per iteration, q = A p for every column, its dots with the
+    // freshly formed p (Y2 := P_new by parity) -> alpha; no Q(A) second apply, no Pade tail
+    A.mbcg = true;
+    A.a1.out = e.Q; A.a1.epi = EPI_DOT; A.a1.Sout = nullptr; A.a1.use_par_p2 = 2; A.a1.P2 = nullptr;
+    A.a1.dots = e.dots; A.a1.fin = FIN_ALPHA;
+    for (int c = 0; c < MAXC; ++c) { A.a1.cA[c] = 1.0; A.a1.cV[c] = 0.0; A.a1.cP[c] = 0.0; }
+    if (A.pnew) A.t1.task0 = nullptr;
+  }
+  bl->pnew = A.pnew;
   A.st = e.st; A.R = e.R; A.Pb[0] = e.Pb[0]; A.Pb[1] = e.Pb[1]; A.n_pad = L.n_pad; A.ncol = ncol;
   return NUGPR_OK;
 }
@@ -1005,16 +1023,37 @@ static void launch_iteration(const IterArgs& A, bool useB, cudaStream_t s) {
   launch_lowrank(A.t1, A.ncp, s);
   if (A.pnew) launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s);
   launch_apply(A.a1, A.ncp, useB, s);
+  if (A.mbcg) { launch_update(A.ua, A.ncp, s); return; }
   launch_lowrank(A.t2, A.ncp, s);
   launch_apply(A.a2, A.ncp, useB, s);
   launch_update(A.ua, A.ncp, s);
 }
+// tail + final kernel; mBCG: quad = c^T x partials (no Pade trace applies)
+static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol,
+                              int logdet_mode, cudaStream_t s);
 static void launch_tail(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol, cudaStream_t s) {
   launch_spart(bl->Ld, bl->B.u, e.X, ncol, e.SX, s);
   launch_lowrank(A.t3, A.ncp, s);
   launch_apply(A.a3, A.ncp, useB, s);
   launch_lowrank(A.t4, A.ncp, s);
   launch_apply(A.a4, A.ncp, useB, s);
+}
+
+static int quad_nparts(const nugpr_blocks* bl) {
+  return quad_parts(bl->L.n_pad, static_cast<int>(bl->Ld.n_tiles) * MAXC);
+}
+static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol,
+                              int logdet_mode, cudaStream_t s) {
+  if (A.mbcg) {
+    const int np = quad_nparts(bl);
+    launch_quad_part(e.RHS, e.X, bl->L.n_pad, np, e.SX, s);
+    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n), ncol,
+                 logdet_mode, e.out, s, e.SX, np);
+    return;
+  }
+  launch_tail(bl, e, A, useB, ncol, s);
+  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n),
+               ncol, logdet_mode, e.out, s);
 }
 
 // Graph of one slot: while (any column active) { CG iteration }; spart; trace applies; final.
@@ -1028,8 +1067,8 @@ static std::string graph_key(const nugpr_blocks* bl, int slot, int ncol, int log
   const HostLayout& L = bl->L;
   uint64_t h = 1469598103934665603ull;    // FNV-1a over the offsets (pointers follow from them)
   for (int64_t v : L.off) { h ^= static_cast<uint64_t>(v); h *= 1099511628211ull; }
-  snprintf(buf, sizeof(buf), "%p|%zu|%d|%d|%d|%d|%llx|%d", static_cast<const void*>(bl->ws_base), bl->E.size(),
-           slot, ncol, logdet_mode, L.d, static_cast<unsigned long long>(h), L.n_c);
+  snprintf(buf, sizeof(buf), "%p|%zu|%d|%d|%d|%d|%llx|%d|%d", static_cast<const void*>(bl->ws_base), bl->E.size(),
+           slot, ncol, logdet_mode, L.d, static_cast<unsigned long long>(h), L.n_c, bl->f32 ? 1 : 0);
   return std::string(buf);
 }
 
@@ -1100,6 +1139,19 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     if (as != s) CK(cudaStreamWaitEvent(s, ctx->ev_aux[slot][1], 0));
     lam0_ptr = e.scal;
   }
+  bl->f32 = cfg->block_storage == NUGPR_BLOCKS_F32;
+  if (bl->f32) {
+    if (L.big) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs clusters <= %d points", LD_SMALL_MAX);
+    if (mode == NUGPR_MODE_GENERIC) {
+      float* g32 = reinterpret_cast<float*>(e.T);            // free after the G GEMMs
+      launch_d2f(e.G, g32, L.blk_total, s);
+      P.B32 = g32;
+    } else if (P.B) {
+      if (!bl->h32_ready) { launch_d2f(B.H, B.H32, L.blk_total, s); bl->h32_ready = true; }
+      P.B32 = B.H32;
+    }
+    CKL();
+  }
   P.mode = mode;
   P.lam0_src = lam0_ptr;
   if (mode_out) *mode_out = mode;
@@ -1133,12 +1185,12 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   }
   // direct launches (profiling / NUGPR_NO_GRAPH): host polls the activity flag every CH iterations
   IterArgs A;
-  RET(make_iter_args(bl, e, ncol, A));
+  RET(make_iter_args(bl, e, ncol, A, cfg->logdet_mode == NUGPR_LOGDET_MBCG));
   double sum_b2 = 0.0;
   for (int i = 0; i < L.n_c; ++i) { double b = static_cast<double>(L.off[i + 1] - L.off[i]); sum_b2 += b * b; }
   // algorithmic bytes of one apply: w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
   const double vec_bytes = 8.0 * (2.0 * L.n * ncol + L.n + static_cast<double>(L.n_c) * L.n_c);
-  const double apply_bytes = (useB ? 8.0 * sum_b2 : 0.0) + vec_bytes;
+  const double apply_bytes = (useB ? (bl->f32 ? 4.0 : 8.0) * sum_b2 : 0.0) + vec_bytes;   // B as stored
   const int apply_cls = useB ? PC_APPLY_B : PC_APPLY_LR;
   const int limit = cfg->replay_iters ? [&] { int mx = 0; for (int c = 0; c < ncol; ++c) mx = std::max(mx, P.replay_iters[c]); return mx; }()
                                       : max_iter;
@@ -1149,8 +1201,10 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
       PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
       if (A.pnew) PROF(ctx, PC_UPDATE, 0.0, s, launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s));
       PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
-      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+      if (!A.mbcg) {
+        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+      }
       PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
     }
     CKL();
@@ -1158,13 +1212,17 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     CK(cudaStreamSynchronize(s));
     if (!*ctx->h_flag) break;
   }
-  launch_spart(Ld, B.u, e.X, ncol, e.SX, s);
-  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
-  PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
-  PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
-  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(L.n),
-               ncol, cfg->logdet_mode, e.out, s);
+  if (A.mbcg) {
+    launch_tail_final(bl, e, A, useB, ncol, cfg->logdet_mode, s);
+  } else {
+    launch_spart(Ld, B.u, e.X, ncol, e.SX, s);
+    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
+    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
+    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(L.n),
+                 ncol, cfg->logdet_mode, e.out, s);
+  }
   CKL();
   return NUGPR_OK;
 }
@@ -1176,7 +1234,7 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   if (it != ctx->graphs.end()) { *out = it->second; return NUGPR_OK; }
   EvalDev& e = bl->E[slot];
   IterArgs A;
-  RET(make_iter_args(bl, e, ncol, A));
+  RET(make_iter_args(bl, e, ncol, A, logdet_mode == NUGPR_LOGDET_MBCG));
   // every kernel of the graph opts into its shared memory before capture
   cudaStream_t cs = ctx->capture_stream;
   cudaGraph_t g = nullptr;
@@ -1197,9 +1255,7 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   cudaError_t ce = cudaStreamEndCapture(cs, &body_out);
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph body capture: %s", cudaGetErrorString(ce)); }
   CK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  launch_tail(bl, e, A, true, ncol, cs);
-  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n),
-               ncol, logdet_mode, e.out, cs);
+  launch_tail_final(bl, e, A, true, ncol, logdet_mode, cs);
   cudaGraph_t g_out = nullptr;
   ce = cudaStreamEndCapture(cs, &g_out);
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph tail capture: %s", cudaGetErrorString(ce)); }
@@ -1318,7 +1374,7 @@ static nugpr_status check_cfg(const nugpr_solve_cfg* cfg) {
   if (cfg->cg_max_iter < 1 || cfg->cg_max_iter >= HIST)
     return fail(NUGPR_ERR_INVALID_ARG, "cg_max_iter must be in [1, %d)", HIST);
   if (!(cfg->cg_tol >= 0.0)) return fail(NUGPR_ERR_INVALID_ARG, "cg_tol must be >= 0");
-  if (cfg->logdet_mode != 0 && cfg->logdet_mode != 1) return fail(NUGPR_ERR_INVALID_ARG, "bad logdet_mode");
+  if (cfg->logdet_mode < 0 || cfg->logdet_mode > 2) return fail(NUGPR_ERR_INVALID_ARG, "bad logdet_mode");
   return NUGPR_OK;
 }
 
@@ -1330,15 +1386,17 @@ static nugpr_status stage_y(nugpr_blocks* bl, const double* y, cudaStream_t s, c
 }
 
 // Kernel launches a finished graph-mode evaluation made (host counter for gpu_launches).
-static void account_graph_launches(const nugpr_blocks* bl, const nugpr_mll_out& o) {
+static void account_graph_launches(const nugpr_blocks* bl, const nugpr_mll_out& o, int logdet_mode) {
   int k = o.iters_y;
   for (int j = 0; j < 16; ++j) k = std::max(k, o.iters_q[j]);
-  note_launch(static_cast<long long>(bl->iter_kernels) * std::max(1, k) + 6);
+  const bool mb = logdet_mode == NUGPR_LOGDET_MBCG;
+  const long long per_it = (mb ? 3 : 5) + (bl->pnew ? 1 : 0);
+  note_launch(per_it * std::max(1, k) + (mb ? 2 : 6));
 }
 
 static nugpr_status finish_record(nugpr_blocks* bl, const nugpr_solve_cfg* cfg, const nugpr_mll_out& o,
                                   bool graph) {
-  if (graph) account_graph_launches(bl, o);
+  if (graph) account_graph_launches(bl, o, cfg->logdet_mode);
   bl->last_m = cfg->num_probes;
   bl->last_seed = cfg->probe_seed;
   if (!(o.lambda0 > 0.0)) return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", o.lambda0);
@@ -1469,6 +1527,11 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
     for (int j = 0; j < nk; ++j) { cudaEventCreate(&tls[j]); cudaEventCreate(&tlp[j]); cudaEventCreate(&tle[j]); }
     cudaEventRecord(tl0, s0);
   }
+  if (cfg->block_storage == NUGPR_BLOCKS_F32 && !bl->h32_ready && !bl->L.big) {
+    launch_d2f(bl->B.H, bl->B.H32, bl->L.blk_total, s0);   // before the fork: every stream reads it
+    CKL();
+    bl->h32_ready = true;
+  }
   CK(cudaEventRecord(ctx->ev_fork, s0));
   int modes[16] = {0};
   // NEXT-3 batching: the noise- and scale-step evaluations (B = H for all of them) form one
@@ -1477,7 +1540,8 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   // opt-in (NUGPR_BATCH=1): at C3 the per-cluster phases of the apply dominate and a 4-group apply
   // is no faster than four separate ones; it pays where streaming dominates (large clusters)
   static const bool batch_on = [] { const char* v = getenv("NUGPR_BATCH"); return v && v[0] == '1'; }();
-  if (batch_on && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big) {
+  if (batch_on && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big &&
+      cfg->logdet_mode != NUGPR_LOGDET_MBCG) {
     const nugpr_theta t0 = bl->theta0;
     for (int j = 0; j < nk && batch.size() < 4; ++j) {
       const nugpr_theta& th = pts[ks[j]];
@@ -1632,13 +1696,48 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
 
 // ------------------------------------------------------------------------------------------
 // NEXT-1: posterior mean / variance (Eq. 4-5) with the exact structured K''^{-1} (predict_kernels.cu).
+// The capacitance matrix of Eq. (28)'s Woodbury form (reading P22): with c = R^{-T} y in B.cy,
+// zeta_i = u_i^T c_i / sqrt(d_i) -> e.Tbuf[0:n_c], sqrt(d_i) -> e.Tbuf[n_c:2n_c];
+// C = I + D^{1/2} M D^{1/2} (one ldc x ldc block in e.V), factorised in place to Linv_C with
+// log|C| -> e.scal[0]; lz = Linv_C zeta -> e.Tbuf[2n_c:3n_c].  Small (fused) or blocked big-block
+// factorisation by size.  Synchronises the stream (reads the SPD status).
+static nugpr_status factor_capacitance(nugpr_blocks* bl, EvalDev& e, const double* c, int ldc, cudaStream_t s) {
+  const HostLayout& L = bl->L;
+  BlocksDev& B = bl->B;
+  const int n_c = L.n_c;
+  const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
+  if (static_cast<size_t>(ldc) * ldc > vec || static_cast<size_t>(3) * n_c > static_cast<size_t>(n_c) * MAXC)
+    return fail(NUGPR_ERR_WORKSPACE, "capacitance matrix (%d x %d) exceeds the evaluation slot", ldc, ldc);
+  const bool big = ldc > LD_SMALL_MAX;
+  if (big && big_scratch_doubles(1, ldc) > vec) return fail(NUGPR_ERR_WORKSPACE, "capacitance scratch too small");
+  double* Cm = e.V;
+  double* zeta = e.Tbuf, *sd = e.Tbuf + n_c, *lz = e.Tbuf + 2 * n_c;
+  launch_pred_setup(bl->Ld, c, B.u, B.M, ldc, zeta, sd, Cm, s);
+  int64_t hm[16] = {0, n_c, 0, ldc, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // off[2], poff[2], boff[1]
+  int32_t* ldp = reinterpret_cast<int32_t*>(B.pmeta + 8);                     // ld[1]
+  int32_t ldh = ldc;
+  std::memcpy(&hm[8], &ldh, sizeof(int32_t));
+  CK(cudaMemcpyAsync(B.pmeta, hm, sizeof(hm), cudaMemcpyHostToDevice, s));
+  LayoutDev Lc = bl->Ld;
+  Lc.off = B.pmeta; Lc.poff = B.pmeta + 2; Lc.boff = B.pmeta + 4; Lc.ld = ldp; Lc.n_c = 1;
+  if (big) launch_big_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, e.Pb[0], s);
+  else launch_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, s);
+  CKL();
+  int32_t cst = 0;
+  CK(cudaMemcpyAsync(&cst, e.linfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+  launch_pred_lz(Cm, ldc, n_c, zeta, lz, s);
+  CKL();
+  CK(cudaStreamSynchronize(s));
+  if (cst) return fail(NUGPR_ERR_NOT_SPD, "I + M~ is not SPD (degenerate low-rank term)");
+  return NUGPR_OK;
+}
+
 extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, const double* X_test,
                                       int64_t n_test, int32_t add_noise, double* mean, double* var) {
   if (!ctx || !bl || !y_sorted || !X_test || !mean) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
   if (n_test < 0) return fail(NUGPR_ERR_INVALID_ARG, "n_test < 0");
   if (n_test == 0) return NUGPR_OK;
   const HostLayout& L = bl->L;
-  if (L.n_c > LD_SMALL_MAX) return fail(NUGPR_ERR_UNSUPPORTED, "predict supports n_c <= %d in this build", LD_SMALL_MAX);
   CK(cudaSetDevice(ctx->device));
   cudaGetLastError();
   cudaStream_t s = ctx->stream;
@@ -1661,32 +1760,17 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   double* p = ww + static_cast<int64_t>(n_c) * nt;
   double* pc = e.R;                       // ldc x nt
   double* lp = e.X;                       // ldc x nt
-  double* Cm = e.V;                       // ldc x ldc (C, then Linv_C)
-  double* zeta = e.Tbuf, *sd = e.Tbuf + n_c, *lz = e.Tbuf + 2 * n_c;
+  double* Cm = e.V;                       // ldc x ldc (C, then Linv_C): factor_capacitance
+  double* zeta = e.Tbuf, *lz = e.Tbuf + 2 * n_c;
   double* xt = e.Q;                       // nt x d staged test inputs
   double* ostage = e.dots;                // 2 * nt outputs when the user's buffers are host memory
   // c = R^{-T} y
   const double* y_dev = nullptr;
   RET(stage_y(bl, y_sorted, s, &y_dev));
   launch_cy(Ld, B.Linv, y_dev, L.ld_max, B.cy, s);
-  // C = I + D^{1/2} M D^{1/2}, its factor and inverse (one-block layout), lz = Linv_C zeta
-  launch_pred_setup(Ld, B.cy, B.u, B.M, ldc, zeta, sd, Cm, s);
-  int64_t hm[16] = {0, n_c, 0, ldc, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // off[2], poff[2], boff[1]
-  int32_t* ldp = reinterpret_cast<int32_t*>(B.pmeta + 8);                     // ld[1]
+  RET(factor_capacitance(bl, e, B.cy, ldc, s));
+  int32_t* ldp = reinterpret_cast<int32_t*>(B.pmeta + 8);                     // ld[1] of the one-block layout
   int64_t* zero64 = B.pmeta + 10;                                             // loff = goff = 0
-  int32_t ldh = ldc;
-  CK(cudaMemcpyAsync(B.pmeta, hm, sizeof(hm), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(ldp, &ldh, sizeof(int32_t), cudaMemcpyHostToDevice, s));
-  LayoutDev Lc = Ld;
-  Lc.off = B.pmeta; Lc.poff = B.pmeta + 2; Lc.boff = B.pmeta + 4; Lc.ld = ldp; Lc.n_c = 1;
-  launch_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, s);
-  CKL();
-  int32_t cst = 0;
-  CK(cudaMemcpyAsync(&cst, e.linfo, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-  launch_pred_lz(Cm, ldc, n_c, zeta, lz, s);
-  CKL();
-  CK(cudaStreamSynchronize(s));
-  if (cst) return fail(NUGPR_ERR_NOT_SPD, "I + M~ is not SPD (degenerate low-rank term)");
   const bool xdev = is_device_ptr(X_test), mdev = is_device_ptr(mean), vdev = var ? is_device_ptr(var) : true;
   const double noise_add = add_noise ? th.noise : 0.0;
   for (int64_t j0 = 0; j0 < n_test; j0 += nt) {
@@ -1714,6 +1798,34 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   return NUGPR_OK;
 }
 
+
+// ------------------------------------------------------------------------------------------
+// NEXT-2: the exact structured MLL at the blocks' theta_0 (Eq. (28)-(29)):
+// determinant lemma + Woodbury on the rank-n_c term, no probes / Pade / CG.
+extern "C" nugpr_status nugpr_mll_exact(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, double out[4]) {
+  if (!ctx || !bl || !y_sorted || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  CK(cudaSetDevice(ctx->device));
+  cudaGetLastError();
+  cudaStream_t s = ctx->stream;
+  const HostLayout& L = bl->L;
+  BlocksDev& B = bl->B;
+  EvalDev& e = bl->E[0];
+  const int ldc = (L.n_c + PAD - 1) / PAD * PAD;
+  const double* y_dev = nullptr;
+  RET(stage_y(bl, y_sorted, s, &y_dev));
+  launch_cy(bl->Ld, B.Linv, y_dev, L.ld_max, B.cy, s);
+  bl->cy_ready = false;                          // B.cy now holds this y's c (numgrad recomputes its own)
+  CKL();
+  RET(factor_capacitance(bl, e, B.cy, ldc, s));
+  double* ccblk = e.Tbuf + 3 * L.n_c;
+  double* dout = e.scal + 4;
+  launch_exact_final(bl->Ld, B.cy, e.Tbuf, e.Tbuf + 2 * L.n_c, B.scal, e.scal, ccblk, L.n, dout, s);
+  CKL();
+  CK(cudaMemcpyAsync(ctx->h_out, dout, 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  std::memcpy(out, ctx->h_out, 4 * sizeof(double));
+  return NUGPR_OK;
+}
 // ------------------------------------------------------------------------------------------
 extern "C" nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr) {
   if (!state || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");

@@ -394,7 +394,7 @@ __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
   const double* Bi = useB ? B + a.L.boff[i] : nullptr;
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   __shared__ double Bs[BNB * BLDS];          // Bs[k][r] = B_i[k0+k][r0+r]
   __shared__ double Ds[BNB * NCP];           // Ds[k][c] = D_i[k0+k][c]

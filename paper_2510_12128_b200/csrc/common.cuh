@@ -54,6 +54,7 @@ struct EvalParams {
   double a;
   double b0, b1;
   const double* B;       // H or G (block storage layout), NULL => no block term
+  const float* B32;      // FP32-stored copy of B (NUGPR_F32_BLOCKS storage), NULL in FP64 mode
   const double* Mp;      // n_c x n_c row-major
   double mscale;
   double tol;
@@ -125,6 +126,7 @@ struct ApplyArgs {
   int lds;                 // column-task kernel: padded column stride in shared memory
   int d_is_pnew;           // column-task kernel: D := P_new = Pbuf[par^1] (formed by pnew_kernel)
   int big;                 // big-block mode (ld_max > 512): row-tiled apply_big_kernel
+  int f32;                 // 1: the DMMA apply streams the FP32-stored block (P->B32)
 };
 
 struct ApplyPlan {

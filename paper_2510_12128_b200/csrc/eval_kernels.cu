@@ -285,7 +285,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
   const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   if (tid == 0) {
     for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWC); }
@@ -518,7 +518,7 @@ __device__ __forceinline__ void mma_sync_consumers() {
   asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
 }
 
-template <int MTMAX>   // m-tiles per warp: 4 (ld <= 224), 8 (ld <= 448), 10 (ld <= 560)
+template <int MTMAX, typename TB>   // m-tiles per warp: 4 (ld <= 224), 8, 10; TB: stored element of B
 __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   constexpr int EG = 2;                      // m-tiles per epilogue load group
   constexpr int NCPE = 10;                 // epilogue column slots (9 used)
@@ -536,8 +536,9 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   const int ncol = a.ncol;                 // == 9
   const EvalParams* P = a.prm;
   const int par = a.st->par;
-  const double* B = P->B;
-  const bool useB = (B != nullptr);
+  const TB* B = (sizeof(TB) == 4) ? reinterpret_cast<const TB*>(P->B32) : reinterpret_cast<const TB*>(P->B);
+  const bool useB = (P->B != nullptr);
+  constexpr int EPS = 8 / static_cast<int>(sizeof(TB));   // B elements per 8-byte slot unit
   const int slot = a.slot_doubles;
   const int nstage = a.nstage;
   const int G = gridDim.x;
@@ -546,7 +547,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   double* ys = Dp + a.ld_max * LDP;                          // ld_max
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   if (tid == 0) {
     for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWM); }
@@ -564,8 +565,8 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
       for (int t = blockIdx.x; t < n_tiles; t += G) {
         const int i = a.L.tiles[t].blk;
         const int ld = a.L.ld[i];
-        const int KC = max(4, (slot / ld) & ~3);
-        const double* Bi = B + a.L.boff[i];
+        const int KC = max(4, (EPS * slot / ld) & ~3);
+        const TB* Bi = B + a.L.boff[i];
         if (!(a.dbg & 32)) {
           // warm L2 with this cluster's epilogue inputs and the next cluster's D inputs, so the
           // consumers' plain loads there do not queue behind the B stream in DRAM
@@ -574,7 +575,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
           tma_prefetch_l2(a.u + p0, cb8);
           for (int c = 0; c < ncol; ++c) {
             if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cb8);
-            if (a.epi != EPI_S && Y2 != P2) tma_prefetch_l2(Y2 + c * n_pad + p0, cb8);
+            if (a.epi != EPI_S && Y2 != P2 && a.use_par_p2 != 2) tma_prefetch_l2(Y2 + c * n_pad + p0, cb8);
           }
           const int tn = t + G;
           if (tn < n_tiles) {
@@ -592,7 +593,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
           const uint32_t use = pseq / nstage;
           if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
           const int kc = min(KC, ld - ck0);
-          const uint32_t bytes = static_cast<uint32_t>(kc) * ld * 8u;
+          const uint32_t bytes = static_cast<uint32_t>(kc) * ld * static_cast<uint32_t>(sizeof(TB));
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[s_], bytes);
           tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
@@ -673,23 +674,23 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
 #pragma unroll
     for (int j = 0; j < MTMAX; ++j) { acc0[j] = 0.0; acc1[j] = 0.0; accy[j] = 0.0; }
     if (useB) {
-      const int KC = max(4, (slot / ld) & ~3);
+      const int KC = max(4, (EPS * slot / ld) & ~3);
       for (int k0 = 0; k0 < ld; k0 += KC, ++seq) {
         const int kc = min(KC, ld - k0);
         const int s_ = static_cast<int>(seq % nstage);
         mbar_wait(&full[s_], (seq / nstage) & 1u);
-        const double* cbuf = ring + s_ * slot;
+        const TB* cbuf = reinterpret_cast<const TB*>(ring + s_ * slot);
         if (!(a.dbg & 1)) {
           for (int kq = 0; kq < kc; kq += 4) {
             const int k = k0 + kq + qc;                      // this lane's k in the cluster
             const double bfr = Dp[k * LDP + qr];             // B fragment: D_p[k][n = qr]
             const double yv = ys[k];
-            const double* acol = cbuf + (kq + qc) * ld + qr; // A fragment base: B_i[r][k]
+            const TB* acol = cbuf + (kq + qc) * ld + qr;     // A fragment base: B_i[r][k]
 #pragma unroll
             for (int j = 0; j < MTMAX; ++j) {
               const int mt = wid + j * NWM;
               if (mt < mtt) {
-                const double afr = acol[mt * 8];
+                const double afr = static_cast<double>(acol[mt * 8]);
                 dmma884(acc0[j], acc1[j], afr, bfr);
                 accy[j] = fma(afr, yv, accy[j]);
               }
@@ -733,7 +734,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
             const int64_t gi = c * n_pad + p0 + r;
             const bool le = on && (e < 2 || qc == 0);
             p2v[jj][e] = (le && P2) ? P2[gi] : 0.0;
-            y2v[jj][e] = (le && a.epi != EPI_S) ? Y2[gi] : 0.0;
+            y2v[jj][e] = (le && a.epi != EPI_S && a.use_par_p2 != 2) ? Y2[gi] : 0.0;
           }
         }
 #pragma unroll
@@ -755,7 +756,8 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
               double o = a.cA[c] * val + a.cV[c] * d;
               if (P2) o += a.cP[c] * p2v[jj][e];
               a.out[gi] = o;
-              const double y2 = (a.epi == EPI_S) ? uu[jj] : y2v[jj][e];
+              // (mBCG: the dot partner is P_new = D_i itself, already in shared memory)
+              const double y2 = (a.epi == EPI_S) ? uu[jj] : (a.use_par_p2 == 2) ? d : y2v[jj][e];
               // ep[c] += o * y2 with a compile-time column index
 #pragma unroll
               for (int cc = 0; cc < 9; ++cc)
@@ -970,7 +972,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_multi_kernel(const __grid_consta
       const ApplyArgs& a = ma.g[g];
       const EvalParams* P = a.prm;
       const int par = s_par[g];
-      const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+      const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
       const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
       double ep[NCPE];
 #pragma unroll
@@ -1111,7 +1113,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_staged_kernel(ApplyArgs a) {
   const int nmine = (n_tiles - static_cast<int>(blockIdx.x) + G - 1) / G;
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   const bool eY2 = (a.epi != EPI_S) && (Y2 != P2);          // Y2 needs its own staging
   double* ring = sm;                                         // nstage * slot
@@ -1404,7 +1406,7 @@ __global__ void __launch_bounds__(NTM, 1) apply_col_kernel(ApplyArgs a) {
   const int t1 = static_cast<int>((static_cast<int64_t>(T) * (blockIdx.x + 1)) / G);
   const int nt = t1 - t0;
   const double* D = a.d_is_pnew ? a.Pbuf[par ^ 1] : a.D;
-  const double* P2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.P2;
+  const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   // slot layout (doubles): task slot = CTW columns of B_i at their natural stride ld (one bulk copy)
   const int tslot = CTW * a.ld_max;
@@ -1857,6 +1859,8 @@ struct FinalArgs {
   int ncol;
   int logdet_mode;
   nugpr_mll_out* out;
+  const double* quad_part;   // NEXT-4 (mBCG): partials of c^T x (column 0), summed in order
+  int n_quad_part;
 };
 
 __global__ void final_kernel(FinalArgs a) {
@@ -1876,7 +1880,10 @@ __global__ void final_kernel(FinalArgs a) {
       for (int q = 1; q < k; ++q) d[q] = 1.0 / al[q] + be[q - 1] / al[q - 1];
       for (int q = 0; q + 1 < k; ++q) e[q] = sqrt(be[q]) / al[q];
       tql_first(k, d, e, z);
-      for (int l = 0; l < k; ++l) val += z[l] * z[l] * log(-2.0 + sqrt(3.0 + d[l]));
+      if (a.logdet_mode == 2)            // mBCG on A: Ritz values of A itself, f = log
+        for (int l = 0; l < k; ++l) val += z[l] * z[l] * log(d[l]);
+      else                               // CG on Q(A): map mu -> lambda = -2 + sqrt(3 + mu)
+        for (int l = 0; l < k; ++l) val += z[l] * z[l] * log(-2.0 + sqrt(3.0 + d[l]));
       val *= st->rr0[j];
     }
     s_slq[j] = val;
@@ -1896,11 +1903,17 @@ __global__ void final_kernel(FinalArgs a) {
       o.iters_q[c - 1] = st->iters[c];
     }
     const double ldR = a.logdet_R[0];
-    o.quad = st->quad;
+    if (a.quad_part) {
+      double q = 0.0;
+      for (int b = 0; b < a.n_quad_part; ++b) q += a.quad_part[b];
+      o.quad = q;
+    } else {
+      o.quad = st->quad;
+    }
     o.logdet_R = ldR;
-    o.logdet_pade = ldR + tsum / m;
+    o.logdet_pade = (a.logdet_mode == 2) ? __longlong_as_double(0x7ff8000000000000ll) : ldR + tsum / m;
     o.logdet_slq = ldR + ssum / m;
-    o.logdet = (a.logdet_mode == 1) ? o.logdet_slq : o.logdet_pade;
+    o.logdet = (a.logdet_mode != 0) ? o.logdet_slq : o.logdet_pade;
     o.L = 0.5 * (o.quad + o.logdet + a.n * 1.8378770664093453);   // n log(2 pi)
     o.lambda0 = a.prm->lam0_src ? a.prm->lam0_src[0] : a.prm->lam0_val;
     o.resid_y = sqrt(st->rr[0]);
@@ -1910,6 +1923,23 @@ __global__ void final_kernel(FinalArgs a) {
     o.converged = st->hit_max ? 0 : 1;
     o.mode = a.prm->mode;
     *a.out = o;
+  }
+}
+
+// NEXT-4 (mBCG): quad = c^T x over column 0, per-CTA partials of contiguous ranges (fixed order)
+__global__ void __launch_bounds__(256) quad_part_kernel(const double* c, const double* x, int64_t n_pad,
+                                                        int64_t chunk, double* part) {
+  __shared__ double red[8];
+  const int64_t lo = blockIdx.x * chunk, hi = min(n_pad, lo + chunk);
+  double s = 0.0;
+  for (int64_t p = lo + threadIdx.x; p < hi; p += 256) s = fma(c[p], x[p], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    part[blockIdx.x] = t;
   }
 }
 
@@ -1943,6 +1973,18 @@ static int env_int(const char* name, int dflt) {
 }
 
 int num_sms_host() { return num_sms(); }
+
+// FP32-stored copy of a block array (NUGPR_F32_BLOCKS): round to nearest
+__global__ void d2f_kernel(const double* src, float* dst, int64_t n) {
+  for (int64_t k = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; k < n;
+       k += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    dst[k] = __double2float_rn(src[k]);
+}
+void launch_d2f(const double* src, float* dst, int64_t n, cudaStream_t s) {
+  const int grid = static_cast<int>(std::min<int64_t>((n + 255) / 256, 8 * num_sms()));
+  d2f_kernel<<<grid, 256, 0, s>>>(src, dst, n);
+  note_launch(); post_launch("d2f_kernel");
+}
 
 // Shared-memory / grid plan of the apply (host side).  ncol == 9 (the paper's m = 8) uses the DMMA
 // kernel unless NUGPR_APPLY_MMA=0; the ring depth is chosen to fit; NUGPR_APPLY_{SLOT,PER,BAL}
@@ -2059,16 +2101,19 @@ void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
   }
   if (a.mma) {
     size_t smem = useB ? a.smem_b : a.smem_nob;
+#define NUGPR_AMK(MT, TBT)                                                                  \
+  do {                                                                                      \
+    smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<MT, TBT>));                  \
+    apply_mma_kernel<MT, TBT><<<a.grid, NTM, smem, s>>>(a);                                \
+  } while (0)
     if (a.ld_max <= 4 * NWM * 8) {
-      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<4>));
-      apply_mma_kernel<4><<<a.grid, NTM, smem, s>>>(a);
+      if (a.f32) NUGPR_AMK(4, float); else NUGPR_AMK(4, double);
     } else if (a.ld_max <= 8 * NWM * 8) {
-      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<8>));
-      apply_mma_kernel<8><<<a.grid, NTM, smem, s>>>(a);
+      if (a.f32) NUGPR_AMK(8, float); else NUGPR_AMK(8, double);
     } else {
-      smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<10>));
-      apply_mma_kernel<10><<<a.grid, NTM, smem, s>>>(a);
+      if (a.f32) NUGPR_AMK(10, float); else NUGPR_AMK(10, double);
     }
+#undef NUGPR_AMK
     note_launch(); post_launch("apply_mma_kernel");
     return;
   }
@@ -2175,10 +2220,22 @@ void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol
   note_launch(); post_launch("spart_kernel");
 }
 
+int quad_parts(int64_t n_pad, int cap) {
+  const int64_t want = (n_pad + 4095) / 4096;
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>({want, static_cast<int64_t>(num_sms()), cap})));
+}
+
+void launch_quad_part(const double* c, const double* x, int64_t n_pad, int nparts, double* part, cudaStream_t s) {
+  const int64_t chunk = (n_pad + nparts - 1) / nparts;
+  quad_part_kernel<<<nparts, 256, 0, s>>>(c, x, n_pad, chunk, part);
+  note_launch(); post_launch("quad_part_kernel");
+}
+
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
                   int stride, double* slq_work, const double* logdet_R, double n,
-                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s) {
-  FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, n, ncol, logdet_mode, out};
+                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s,
+                  const double* quad_part, int n_quad_part) {
+  FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, n, ncol, logdet_mode, out, quad_part, n_quad_part};
   final_kernel<<<1, 32, 0, s>>>(a);
   note_launch(); post_launch("final_kernel");
 }

@@ -51,6 +51,7 @@ void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s);
 int num_sms_host();
+void launch_d2f(const double* src, float* dst, int64_t n, cudaStream_t s);
 void launch_apply_multi(const ApplyArgs* ga, int ng, cudaStream_t s);
 size_t apply_multi_smem(int ng, int ld_max, int slot_doubles, int nstage);
 void launch_cond_any(const CGState* const* sts, int ng, unsigned long long cond, cudaStream_t s);
@@ -59,7 +60,10 @@ void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol
                   cudaStream_t s);
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
                   int stride, double* slq_work, const double* logdet_R, double n,
-                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s);
+                  int ncol, int logdet_mode, nugpr_mll_out* out, cudaStream_t s,
+                  const double* quad_part = nullptr, int n_quad_part = 0);
+int quad_parts(int64_t n_pad, int cap);
+void launch_quad_part(const double* c, const double* x, int64_t n_pad, int nparts, double* part, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
 
 // big_kernels.cu (ld_max > 512)
@@ -75,6 +79,9 @@ void launch_pred_trmm(const double* Lm, const double* Bm, double* Cm, const int3
                       const int64_t* goff, int groups, int nt, int ld_max, cudaStream_t s);
 void launch_pred_reduce(const LayoutDev& L, const double* W, const double* c, const double* u, int nt, double* wc,
                         double* ww, double* p, cudaStream_t s);
+void launch_exact_final(const LayoutDev& L, const double* c, const double* zeta, const double* lz,
+                        const double* logdet_R, const double* logdet_C, double* ccblk, int64_t n, double* out,
+                        cudaStream_t s);
 void launch_pred_setup(const LayoutDev& L, const double* c, const double* u, const double* M, int ldc, double* zeta,
                        double* sd, double* Cm, cudaStream_t s);
 void launch_pred_lz(const double* Lc, int ldc, int n_c, const double* zeta, double* lz, cudaStream_t s);

@@ -216,6 +216,56 @@ __global__ void pred_pcol_kernel(const double* p, int n_c, int nt, int ldc, doub
   pc[idx] = (r < n_c) ? p[static_cast<int64_t>(r) * nt + j] : 0.0;
 }
 
+// NEXT-2 (exact structured evaluator): per-cluster c_i . c_i (one warp per cluster)
+__global__ void exact_cc_kernel(LayoutDev L, const double* c, double* ccblk) {
+  const int i = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (i >= L.n_c) return;
+  const int ld = L.ld[i];
+  const int64_t p0 = L.poff[i];
+  double s = 0.0;
+  for (int r = lane; r < ld; r += 32) s = fma(c[p0 + r], c[p0 + r], s);
+  s = warp_sum(s);
+  if (lane == 0) ccblk[i] = s;
+}
+
+// quad = c^T c - (zeta^T zeta - ||Linv_C zeta||^2), logdet = logdet_R + log|C|, L = (quad + logdet + n log 2 pi)/2
+// (one CTA; fixed-order strided partials then a fixed tree -> deterministic)
+__global__ void __launch_bounds__(256) exact_final_kernel(int n_c, int64_t n, const double* ccblk, const double* zeta,
+                                                          const double* lz, const double* logdet_R,
+                                                          const double* logdet_C, double* out) {
+  __shared__ double red[3][256];
+  double a = 0.0, b = 0.0, c = 0.0;
+  for (int i = threadIdx.x; i < n_c; i += 256) {
+    a += ccblk[i];
+    b = fma(zeta[i], zeta[i], b);
+    c = fma(lz[i], lz[i], c);
+  }
+  red[0][threadIdx.x] = a; red[1][threadIdx.x] = b; red[2][threadIdx.x] = c;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w)
+      for (int q = 0; q < 3; ++q) red[q][threadIdx.x] += red[q][threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    const double quad = red[0][0] - (red[1][0] - red[2][0]);
+    const double logdet = logdet_R[0] + logdet_C[0];
+    out[0] = 0.5 * (quad + logdet + static_cast<double>(n) * 1.8378770664093454836);   // log(2 pi)
+    out[1] = quad;
+    out[2] = logdet;
+    out[3] = logdet_C[0];
+  }
+}
+
+void launch_exact_final(const LayoutDev& L, const double* c, const double* zeta, const double* lz,
+                        const double* logdet_R, const double* logdet_C, double* ccblk, int64_t n, double* out,
+                        cudaStream_t s) {
+  exact_cc_kernel<<<(L.n_c + 7) / 8, 256, 0, s>>>(L, c, ccblk);
+  exact_final_kernel<<<1, 256, 0, s>>>(L.n_c, n, ccblk, zeta, lz, logdet_R, logdet_C, out);
+  note_launch(2); post_launch("exact_final");
+}
+
 // ------------------------------------------------------------------------------- launchers
 void launch_pred_ks(const double* X, const double* Xt, int d, const LayoutDev& L, int nt, int ld_max, int kind,
                     double lam, double alpha, double* Ks, cudaStream_t s) {

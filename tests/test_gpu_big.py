@@ -172,3 +172,10 @@ def test_C5_full_size_logdetR_and_quad_bound(P, ctx):
     xi = np.array([bo.u[i] @ c[bo.block(i)] for i in range(bo.n_c)]) / sd
     quad_exact = float(c @ c) - float(xi @ (Mt @ np.linalg.solve(np.eye(bo.n_c) + Mt, xi)))
     assert abs(rec["quad"] - quad_exact) <= tol * math.sqrt(float(c @ c)) * 1.0001 + 1e-9 * abs(quad_exact)
+    # NEXT-2 at full size (n_c = 2000 > 512: blocked capacitance factorisation) against O-EXACT's
+    # arithmetic on the same blocks
+    ex = P.mll_exact(ctx, bg, ds.y)
+    logdet = bo.logdet_R + float(np.sum(np.log1p(np.linalg.eigvalsh(Mt))))
+    assert rel(ex["quad"], quad_exact) < 1e-10
+    assert rel(ex["logdet"], logdet) < 1e-10
+    assert rel(ex["L"], 0.5 * (quad_exact + logdet + ds.n * math.log(2 * math.pi))) < 1e-10
