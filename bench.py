@@ -238,8 +238,20 @@ def run_ours(args):
     torch.cuda.set_device(local)
     import paper_2510_12128_b200 as P
     P._native.lib()
-    group = True if world > 1 else None
-    ctx = P.Context(local, group=group)
+    shard = args.shard == "clusters"
+    if shard and world == 1:
+        # PAR-2 on one GPU: a 1-rank NCCL group so the exchange path (NCCL all_reduce) is the same
+        import socket
+        import torch.distributed as dist
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local))
+    group = True if (world > 1 or shard) else None
+    ctx = P.Context(local, group=group, shard_clusters=shard)
+    if shard:
+        args.eval_slots = 1          # sharded evaluations run one after another, all ranks together
     ds = load_config(args.config, P, ctx)
     kernel = ds.meta.get("kernel", "rbf")
     seed = ds.meta["probe_seed"]
@@ -247,8 +259,8 @@ def run_ours(args):
     Xd = torch.tensor(ds.X, device=dev)
     yd = torch.tensor(ds.y, device=dev)
     rd = torch.tensor(ds.reps, device=dev)
-    ws = torch.empty(P.workspace_size(ds.offsets, ds.n_c, ds.d, args.eval_slots), dtype=torch.uint8,
-                     device=dev)
+    ws = torch.empty(P.workspace_size(ds.offsets, ds.n_c, ds.d, args.eval_slots, rank, world, shard=shard),
+                     dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream(local)
     state = np.zeros(10)
     state[:3] = ds.theta0
@@ -260,7 +272,7 @@ def run_ours(args):
         return st2, rec
 
     def barrier():
-        if world > 1:
+        if world > 1 or shard:
             import torch.distributed as dist
             dist.barrier()
 
@@ -376,7 +388,9 @@ def run_ours(args):
                         "(build preconditioner + 7-point central-difference gradient + Adam)",
             "n": ds.n, "n_c": ds.n_c, "b": int(ds.offsets[1]), "b_max": int(np.diff(ds.offsets).max()), "d": ds.d, "m": 8,
             "kernel": kernel, "logdet": args.logdet, "block_storage": args.blocks,
-            "parallelism": f"perturbation-sharded x{world}" if world > 1 else "single GPU",
+            "parallelism": (f"cluster-sharded x{world} (PAR-2: contiguous cluster ranges, 3 allreduces of "
+                            "per-cluster partials per CG iteration)") if shard else
+                           (f"perturbation-sharded x{world}" if world > 1 else "single GPU"),
             "l2": "inputs larger than L2: per step the preconditioner Linv + H + G(lambda+-) stream "
                   f"{3 * 8 * float(np.sum(np.diff(ds.offsets).astype(np.float64) ** 2)) / 1e6:.0f} MB (> 126 MB L2)",
             "train_time_50_epochs_s": 50 * ms / args.steps / 1e3,
@@ -421,6 +435,8 @@ def main():
     ap.add_argument("--logdet", default="pade", choices=["pade", "slq", "mbcg"],
                     help="log-det estimator (mbcg: NEXT-4, one CG on A, SLQ with f = log)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="perturbation", choices=["perturbation", "clusters"],
+                    help="multi-GPU split: PAR-1 by perturbation (default) or PAR-2 by cluster range")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -132,6 +132,16 @@ typedef struct nugpr_blocks nugpr_blocks;
  * (the Python binding routes it through torch.distributed, NCCL on GPU boxes). */
 typedef int (*nugpr_allgather_fn)(const void* send, size_t bytes, void* recv, void* user);
 
+/* PAR-2 ("at large n the clusters shard across GPUs as well, with an allreduce of
+ * CG dot products"): FP64 sum-allreduce of `count` doubles, recv[k] = sum over ranks of send[k].
+ * send / recv are DEVICE pointers into the workspace given to nugpr_build_blocks (never aliased),
+ * enqueued in order on `stream` (the context's cudaStream_t); the call may return before the
+ * data moved (NCCL) as long as later work on `stream` sees the result.  Returns 0 on success.
+ * The library only reduces zero-padded per-cluster partial arrays: every rank writes the slots
+ * of its own clusters and zeros elsewhere, so the sum is exact (x + 0 = x) and every rank gets
+ * the same partials a single GPU would have produced, in the same order. */
+typedef int (*nugpr_allreduce_fn)(const double* send, double* recv, size_t count, void* stream, void* user);
+
 const char* nugpr_version(void);
 const char* nugpr_last_error(void);
 
@@ -140,6 +150,16 @@ const char* nugpr_last_error(void);
  * the host helpers below (nugpr_numgrad_exchange). */
 nugpr_status nugpr_ctx_create(int device, void* cuda_stream, int rank, int world, nugpr_ctx** out);
 nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void* user);
+/* PAR-2 cluster sharding on this context (fn != NULL enables it, NULL disables).  Then
+ * nugpr_build_blocks keeps only this rank's contiguous cluster range (nugpr_shard_range) and every
+ * later call on those blocks (mll, numgrad, train) is COLLECTIVE: all ranks call it with identical
+ * arguments (global offsets, full X_sorted / reps / y_sorted) and receive identical results.
+ * Per CG iteration the ranks exchange three partial arrays through `fn` (S(A p) of the low-rank
+ * term, p^T q, and r^T r with S(r)); everything else (K_rep, lambda_0, M', the 3-scalar CG state)
+ * is replicated.  Small-block layouts only (clusters <= 512 points); mll_exact / predict /
+ * the mBCG log-det mode return NUGPR_ERR_UNSUPPORTED on sharded blocks.  world = 1 is allowed
+ * (exercises the exchange path on one GPU). */
+nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, void* user);
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
 
 /* Kernel-class profiler (bench.py's live roofline): when enabled, CUDA events are recorded on
@@ -183,6 +203,13 @@ nugpr_status nugpr_cluster(nugpr_ctx* ctx, const double* X, int64_t n, int32_t d
  * fit in the bytes it is given. */
 nugpr_status nugpr_workspace_size(const int64_t* offsets, int32_t n_c, int32_t d,
                                   int32_t eval_slots, size_t* bytes);
+/* PAR-2: the contiguous cluster range [range[0], range[1]) rank `rank` of `world` owns, balanced
+ * by the streamed block bytes sum_i ld_i^2 (ld_i = b_i rounded up to 8), at least one cluster per
+ * rank (n_c >= world, else NUGPR_ERR_SHAPE); and the workspace bytes of that rank's blocks
+ * (eval_slots as above; global offsets).  Host-only. */
+nugpr_status nugpr_shard_range(const int64_t* offsets, int32_t n_c, int32_t rank, int32_t world, int32_t range[2]);
+nugpr_status nugpr_workspace_size_shard(const int64_t* offsets, int32_t n_c, int32_t d, int32_t eval_slots,
+                                        int32_t rank, int32_t world, size_t* bytes);
 
 /* A1 — Alg. 1 line 264 at theta0: K_i assembled on the fly from X_sorted, R_i = chol(K_i)
  * with the jitter ladder, logdet_R, u_i = R_i^{-T} 1, H_i = R_i^{-T} R_i^{-1}, K_rep,

@@ -76,9 +76,12 @@ class Context:
     """nugpr_ctx on one device, enqueuing on torch's current stream of that device.
 
     group: an initialised torch.distributed process group (or True for the default group)
-    enables perturbation sharding in numgrad/train via the allgather callback."""
+    enables perturbation sharding in numgrad/train via the allgather callback (PAR-1).
+    shard_clusters=True additionally (PAR-2) keeps only this rank's cluster range in the blocks
+    and makes mll/numgrad/train collective over the group, with the library's partial-sum
+    exchanges routed through torch.distributed.all_reduce (NCCL on GPU boxes)."""
 
-    def __init__(self, device: int = 0, stream=None, group=None):
+    def __init__(self, device: int = 0, stream=None, group=None, shard_clusters: bool = False):
         """device < 0: host-only context (rank/world/allgather for the host helpers; no CUDA)."""
         self.device = int(device)
         self.rank, self.world = 0, 1
@@ -103,6 +106,53 @@ class Context:
         if self.world > 1:
             self._cb = N.ALLGATHER_FN(self._allgather)
             N.check(N.lib().nugpr_ctx_set_allgather(self.handle, self._cb, None))
+        self.shard_clusters = bool(shard_clusters)
+        self._buffers = {}          # data_ptr -> tensor: device memory the exchange may address
+        self._ar_cb = None
+        self.exchanges = 0
+        if self.shard_clusters:
+            if group is None:
+                raise ValueError("shard_clusters needs a torch.distributed process group")
+            self._ar_cb = N.ALLREDUCE_FN(self._allreduce)
+            N.check(N.lib().nugpr_ctx_set_cluster_shard(self.handle, self._ar_cb, None))
+
+    def register(self, buf):
+        """Make a tensor's memory addressable by the PAR-2 exchange (build_blocks does this for
+        its workspace)."""
+        self._buffers[buf.data_ptr()] = buf
+
+    def _view(self, ptr, count):
+        import torch
+        nb = 8 * count
+        for base, buf in self._buffers.items():
+            size = buf.numel() * buf.element_size()
+            if base <= ptr and ptr + nb <= base + size:
+                off = ptr - base
+                return buf.view(torch.uint8)[off:off + nb].view(torch.float64)
+        # host memory (host-only tests): wrap without copying
+        arr = np.ctypeslib.as_array(C.cast(ptr, C.POINTER(C.c_double)), shape=(count,))
+        return torch.from_numpy(arr)
+
+    def _allreduce(self, send, recv, count, stream, user):
+        """PAR-2 exchange: recv = sum over ranks of send, ordered on the context stream."""
+        try:
+            import torch
+            import torch.distributed as dist
+            s_t, r_t = self._view(send, count), self._view(recv, count)
+            if r_t.is_cuda and dist.get_backend(self.group) != "nccl":
+                # gloo (CPU tests, or several ranks sharing one GPU): through host memory
+                tmp = s_t.cpu()
+                dist.all_reduce(tmp, group=self.group)
+                r_t.copy_(tmp)
+            else:
+                r_t.copy_(s_t)
+                dist.all_reduce(r_t, group=self.group)
+            self.exchanges += 1
+            return 0
+        except Exception as exc:  # noqa: BLE001 — reported to C as a status
+            import sys
+            print(f"[nugpr] PAR-2 allreduce failed: {exc!r}", file=sys.stderr)
+            return 1
 
     def _allgather(self, send, nbytes, recv, user):
         try:
@@ -190,11 +240,32 @@ def numgrad_exchange(ctx: Context, theta, step, L_mine):
     return L0.value, g
 
 
-def workspace_size(offsets, n_c: int, d: int, eval_slots: int = 1) -> int:
+def workspace_size(offsets, n_c: int, d: int, eval_slots: int = 1, rank: int = 0, world: int = 1,
+                   shard: bool = False) -> int:
+    """Workspace bytes (shard=True: this rank's PAR-2 cluster range, nugpr_workspace_size_shard)."""
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     out = C.c_size_t()
-    N.check(N.lib().nugpr_workspace_size(off.ctypes.data, int(n_c), int(d), int(eval_slots), C.byref(out)))
+    if shard:
+        N.check(N.lib().nugpr_workspace_size_shard(off.ctypes.data, int(n_c), int(d), int(eval_slots), int(rank),
+                                                   int(world), C.byref(out)))
+    else:
+        N.check(N.lib().nugpr_workspace_size(off.ctypes.data, int(n_c), int(d), int(eval_slots), C.byref(out)))
     return int(out.value)
+
+
+def shard_range(offsets, rank: int, world: int):
+    """PAR-2: the cluster range [lo, hi) rank `rank` of `world` holds (balanced by sum ld_i^2)."""
+    off = np.ascontiguousarray(offsets, dtype=np.int64)
+    r = (C.c_int32 * 2)()
+    N.check(N.lib().nugpr_shard_range(off.ctypes.data, off.shape[0] - 1, int(rank), int(world), r))
+    return int(r[0]), int(r[1])
+
+
+def _ctx_workspace(ctx, off, n_c, d, eval_slots):
+    import torch
+    nbytes = workspace_size(off, n_c, d, eval_slots, ctx.rank, ctx.world, getattr(ctx, "shard_clusters", False))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", ctx.device))
+    return ws
 
 
 class Blocks:
@@ -268,9 +339,10 @@ def build_blocks(ctx: Context, X_sorted, offsets, reps, theta0, kernel: str = "r
     off = np.ascontiguousarray(offsets, dtype=np.int64)
     X = _f64(X_sorted)
     n_c, d = off.shape[0] - 1, int(X.shape[1])
-    nbytes = workspace_size(off, n_c, d, eval_slots)
     if workspace is None:
-        workspace = torch.empty(nbytes, dtype=torch.uint8, device=torch.device("cuda", ctx.device))
+        workspace = _ctx_workspace(ctx, off, n_c, d, eval_slots)
+    if getattr(ctx, "shard_clusters", False):
+        ctx.register(workspace)
     h = C.c_void_p()
     fb = C.c_int32(-1)
     jit = C.c_double(0.0)
@@ -381,8 +453,9 @@ def train(ctx: Context, X_sorted, offsets, reps, y_sorted, theta0, epochs=50, lr
     X = _f64(X_sorted)
     n_c, d = off.shape[0] - 1, int(X.shape[1])
     if workspace is None:
-        workspace = torch.empty(workspace_size(off, n_c, d, eval_slots), dtype=torch.uint8,
-                                device=torch.device("cuda", ctx.device))
+        workspace = _ctx_workspace(ctx, off, n_c, d, eval_slots)
+    if getattr(ctx, "shard_clusters", False):
+        ctx.register(workspace)
     scfg = _solve_cfg(keep=keep, **solve)
     gcfg = _grad_cfg(mode, step, threshold, threshold_relative, max_halvings)
     st = np.zeros(10)

@@ -56,6 +56,8 @@ class MllOut(C.Structure):
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
+# nugpr_allreduce_fn(send, recv, count, stream, user) — PAR-2 cluster sharding
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 
 _lib = None
 
@@ -75,6 +77,10 @@ def lib():
         "nugpr_last_error": (C.c_char_p, []),
         "nugpr_ctx_create": (C.c_int, [C.c_int, P, C.c_int, C.c_int, C.POINTER(P)]),
         "nugpr_ctx_set_allgather": (C.c_int, [P, ALLGATHER_FN, P]),
+        "nugpr_ctx_set_cluster_shard": (C.c_int, [P, ALLREDUCE_FN, P]),
+        "nugpr_shard_range": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.POINTER(C.c_int32)]),
+        "nugpr_workspace_size_shard": (C.c_int, [P, C.c_int32, C.c_int32, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.POINTER(C.c_size_t)]),
         "nugpr_ctx_destroy": (C.c_int, [P]),
         "nugpr_ctx_set_profiling": (C.c_int, [P, C.c_int32]),
         "nugpr_ctx_profile": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
@@ -124,4 +130,5 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_launch_count", "nugpr_workspace_size", "nugpr_build_blocks", "nugpr_blocks_destroy",
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
             "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster",
-            "nugpr_numgrad_exchange", "nugpr_predict", "nugpr_mll_exact"]
+            "nugpr_numgrad_exchange", "nugpr_predict", "nugpr_mll_exact", "nugpr_ctx_set_cluster_shard",
+            "nugpr_shard_range", "nugpr_workspace_size_shard"]

@@ -164,6 +164,7 @@ struct EvalDev {
   nugpr_mll_out* out = nullptr;
   double* ah = nullptr, *bh = nullptr, *slqw = nullptr;
   double* Tbuf = nullptr;     // n_c x MAXC
+  double* xs = nullptr, *xr = nullptr;   // PAR-2 exchange send / recv: [3][n_c_global][MAXC] each
 };
 
 struct BlocksDev {
@@ -184,11 +185,17 @@ struct BlocksDev {
   int64_t* pmeta = nullptr;   // predict: one-block layout of C = I + M~ (off, poff, boff, ld, loff, goff)
 };
 
-void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E) {
+// n_cg / n_glob: the global cluster / row counts (differ from L's only for PAR-2 sharded blocks,
+// where L is this rank's cluster range): the representatives, K_rep, M, lambda_0 scratch and the
+// staged y are global (replicated), everything per cluster / per row is local.
+void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vector<EvalDev>& E, int n_cg = -1,
+               int64_t n_glob = -1) {
   const int n_c = L.n_c;
+  if (n_cg < 0) n_cg = n_c;
+  if (n_glob < 0) n_glob = L.n;
   const int64_t nt = static_cast<int64_t>(L.tiles.size());
-  const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
-  const size_t lzs = lanczos_scratch_doubles(n_c, kmax);
+  const int kmax = std::min(n_cg, LANCZOS_KMAX_CAP);
+  const size_t lzs = lanczos_scratch_doubles(n_cg, kmax);
   B.off = c.take<int64_t>(n_c + 1);
   B.poff = c.take<int64_t>(n_c + 1);
   B.boff = c.take<int64_t>(n_c);
@@ -200,7 +207,7 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.ctasks = c.take<TileDesc>(L.ctasks.size());
   B.ctask0 = c.take<int32_t>(n_c + 1);
   B.X = c.take<double>(static_cast<size_t>(L.n) * L.d);
-  B.reps = c.take<double>(static_cast<size_t>(n_c) * L.d);
+  B.reps = c.take<double>(static_cast<size_t>(n_cg) * L.d);
   B.Linv = c.take<double>(L.blk_total);
   B.H = c.take<double>(L.blk_total);
   B.H32 = reinterpret_cast<float*>(c.take<double>((L.blk_total + 1) / 2));
@@ -208,14 +215,14 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.jitter = c.take<double>(n_c);
   B.logdet_blk = c.take<double>(n_c);
   B.scal = c.take<double>(8);
-  B.Krep = c.take<double>(static_cast<size_t>(n_c) * n_c);
-  B.M = c.take<double>(static_cast<size_t>(n_c) * n_c);
-  B.v0 = c.take<double>(n_c);
+  B.Krep = c.take<double>(static_cast<size_t>(n_cg) * n_cg);
+  B.M = c.take<double>(static_cast<size_t>(n_cg) * n_cg);
+  B.v0 = c.take<double>(n_cg);
   B.lz = c.take<double>(lzs);
   B.linfo = c.take<int32_t>(4);
   B.Zexport = c.take<double>(static_cast<size_t>(NUGPR_MAX_PROBES) * L.n);
   B.cy = c.take<double>(L.n_pad);
-  B.ystage = c.take<double>(L.n);
+  B.ystage = c.take<double>(n_glob);
   B.pmeta = c.take<int64_t>(16);
   if (L.big) B.bigscr = c.take<double>(big_scratch_doubles(n_c, L.ld_max));
   E.assign(slots, EvalDev());
@@ -224,9 +231,9 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     EvalDev& e = E[s];
     e.G = c.take<double>(L.blk_total);
     e.T = c.take<double>(L.blk_total);
-    e.Krep = c.take<double>(static_cast<size_t>(n_c) * n_c);
-    e.M = c.take<double>(static_cast<size_t>(n_c) * n_c);
-    e.v0 = c.take<double>(n_c);
+    e.Krep = c.take<double>(static_cast<size_t>(n_cg) * n_cg);
+    e.M = c.take<double>(static_cast<size_t>(n_cg) * n_cg);
+    e.v0 = c.take<double>(n_cg);
     e.lz = c.take<double>(lzs);
     e.linfo = c.take<int32_t>(4);
     e.scal = c.take<double>(8);
@@ -239,8 +246,8 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.Pb[0] = c.take<double>(vec);
     e.Pb[1] = c.take<double>(vec);
     e.SR = c.take<double>(nt * MAXC);
-    e.SPb[0] = c.take<double>(nt * MAXC);
-    e.SPb[1] = c.take<double>(nt * MAXC);
+    e.SPb[0] = c.take<double>(std::max<int64_t>(nt, n_cg) * MAXC);   // S(P): global under PAR-2
+    e.SPb[1] = c.take<double>(std::max<int64_t>(nt, n_cg) * MAXC);
     const int64_t npart = std::max<int64_t>(nt, static_cast<int64_t>(L.ctasks.size()));   // per tile or per column task
     e.SV = c.take<double>(npart * MAXC);
     e.SX = c.take<double>(nt * MAXC);
@@ -253,6 +260,8 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.bh = c.take<double>(static_cast<size_t>(MAXC) * HIST);
     e.slqw = c.take<double>(static_cast<size_t>(MAXC) * 3 * HIST);
     e.Tbuf = c.take<double>(static_cast<size_t>(n_c) * MAXC);
+    e.xs = c.take<double>(static_cast<size_t>(3) * n_cg * MAXC);
+    e.xr = c.take<double>(static_cast<size_t>(3) * n_cg * MAXC);
   }
 }
 
@@ -278,6 +287,8 @@ struct nugpr_ctx {
   int rank = 0, world = 1;
   nugpr_allgather_fn ag = nullptr;
   void* ag_user = nullptr;
+  nugpr_allreduce_fn ar = nullptr;       // PAR-2 cluster sharding (nugpr_ctx_set_cluster_shard)
+  void* ar_user = nullptr;
   int32_t* h_flag = nullptr;             // pinned
   nugpr_mll_out* h_out = nullptr;        // pinned
   bool prof = false;
@@ -378,6 +389,10 @@ struct nugpr_blocks {
   bool pnew = false;          // the CG iteration launches pnew_kernel (launch accounting)
   bool f32 = false;           // current evaluation streams FP32-stored blocks
   bool h32_ready = false;     // H32 holds the FP32 copy of H
+  // PAR-2: this rank's cluster range of the global problem (L is the local layout)
+  bool shard = false;
+  int c_lo = 0, c_hi = 0, n_cg = 0;
+  int64_t n_glob = 0, pos0 = 0;
 };
 
 extern "C" {
@@ -418,6 +433,13 @@ nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void
   if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
   ctx->ag = fn;
   ctx->ag_user = user;
+  return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, void* user) {
+  if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
+  ctx->ar = fn;
+  ctx->ar_user = user;
   return NUGPR_OK;
 }
 
@@ -477,6 +499,64 @@ static nugpr_status ws_size_slots(const int64_t* offsets, int32_t n_c, int32_t d
   return NUGPR_OK;
 }
 
+// PAR-2 partition: contiguous cluster ranges balanced by the streamed block bytes
+// sum ld_i^2, every rank at least one cluster.
+static nugpr_status shard_range_impl(const int64_t* off, int n_c, int rank, int world, int* lo, int* hi) {
+  if (!off || n_c < 1 || world < 1 || rank < 0 || rank >= world) return fail(NUGPR_ERR_INVALID_ARG, "bad shard range args");
+  if (n_c < world) return fail(NUGPR_ERR_SHAPE, "n_c = %d < world = %d: every rank needs a cluster", n_c, world);
+  std::vector<double> cum(n_c + 1, 0.0);
+  for (int i = 0; i < n_c; ++i) {
+    const int64_t b = off[i + 1] - off[i];
+    if (b <= 0) return fail(NUGPR_ERR_SHAPE, "offsets must be strictly increasing (cluster %d empty)", i);
+    const double ld = static_cast<double>((b + PAD - 1) / PAD * PAD);
+    cum[i + 1] = cum[i] + ld * ld;
+  }
+  std::vector<int> bd(world + 1, 0);
+  bd[world] = n_c;
+  for (int r = 1; r < world; ++r) {
+    const double target = cum[n_c] * r / world;
+    int k = static_cast<int>(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+    if (k > 0 && target - cum[k - 1] < cum[k] - target) k -= 1;
+    bd[r] = std::max(bd[r - 1] + 1, std::min(k, n_c - (world - r)));
+  }
+  *lo = bd[rank];
+  *hi = bd[rank + 1];
+  return NUGPR_OK;
+}
+
+extern "C" nugpr_status nugpr_shard_range(const int64_t* offsets, int32_t n_c, int32_t rank, int32_t world,
+                                          int32_t range[2]) {
+  if (!range) return fail(NUGPR_ERR_INVALID_ARG, "range is NULL");
+  int lo = 0, hi = 0;
+  RET(shard_range_impl(offsets, n_c, rank, world, &lo, &hi));
+  range[0] = lo;
+  range[1] = hi;
+  return NUGPR_OK;
+}
+
+static std::vector<int64_t> local_offsets(const int64_t* off, int lo, int hi) {
+  std::vector<int64_t> o(hi - lo + 1);
+  for (int i = lo; i <= hi; ++i) o[i - lo] = off[i] - off[lo];
+  return o;
+}
+
+extern "C" nugpr_status nugpr_workspace_size_shard(const int64_t* offsets, int32_t n_c, int32_t d, int32_t eval_slots,
+                                                   int32_t rank, int32_t world, size_t* bytes) {
+  if (!bytes) return fail(NUGPR_ERR_INVALID_ARG, "bytes is NULL");
+  if (eval_slots < 1 || eval_slots > NUGPR_NUM_EVALS) return fail(NUGPR_ERR_INVALID_ARG, "eval_slots must be in [1, 7]");
+  int lo = 0, hi = 0;
+  RET(shard_range_impl(offsets, n_c, rank, world, &lo, &hi));
+  const std::vector<int64_t> lo_off = local_offsets(offsets, lo, hi);
+  HostLayout L;
+  RET(make_layout(lo_off.data(), hi - lo, d, L));
+  Carver c(nullptr);
+  BlocksDev B;
+  std::vector<EvalDev> E;
+  carve_all(c, L, eval_slots, B, E, n_c, offsets[n_c]);
+  *bytes = c.pos + 256;
+  return NUGPR_OK;
+}
+
 extern "C" nugpr_status nugpr_workspace_size(const int64_t* offsets, int32_t n_c, int32_t d,
                                              int32_t eval_slots, size_t* bytes) {
   if (!bytes) return fail(NUGPR_ERR_INVALID_ARG, "bytes is NULL");
@@ -492,10 +572,47 @@ static bool theta_ok(const nugpr_theta& t) {
 // Lanczos lambda_0 of K (device n_c x n_c), warm start vinit (or NULL), writes lam0/v0/M.
 static nugpr_status enqueue_lambda0(nugpr_blocks* bl, const double* K, const double* vinit, double* lz,
                                     double* lam0, double* v0, double* M, int32_t* info, cudaStream_t s) {
-  const int n_c = bl->L.n_c;
+  const int n_c = bl->n_cg;   // K_rep is global (replicated under PAR-2)
   const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
   launch_lanczos(K, n_c, vinit, lz, kmax, 1e-11, lam0, v0, M, info, s);
   CKL();
+  return NUGPR_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// PAR-2 exchange helpers.  Every exchange is a sum-allreduce of a zero-padded
+// global array in which each rank filled only its own clusters' slots: exact, and every rank ends
+// with the partials a single GPU would hold, in the same order.
+static nugpr_status xchg(nugpr_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (!ctx->ar) return fail(NUGPR_ERR_COMM, "sharded blocks but no allreduce callback on the context");
+  if (ctx->ar(send, recv, count, static_cast<void*>(s), ctx->ar_user) != 0)
+    return fail(NUGPR_ERR_COMM, "allreduce callback failed (PAR-2 exchange)");
+  return NUGPR_OK;
+}
+
+// per-cluster local [n_loc][w] device array -> global [n_cg][w] (glob must not be slot 0's xs)
+static nugpr_status gather_clusters(nugpr_blocks* bl, const double* loc, int w, double* glob, cudaStream_t s) {
+  EvalDev& e = bl->E[0];
+  const size_t tot = static_cast<size_t>(bl->n_cg) * w;
+  CK(cudaMemsetAsync(e.xs, 0, sizeof(double) * tot, s));
+  CK(cudaMemcpyAsync(e.xs + static_cast<size_t>(bl->c_lo) * w, loc, sizeof(double) * bl->L.n_c * w,
+                     cudaMemcpyDeviceToDevice, s));
+  return xchg(bl->ctx, e.xs, glob, tot, s);
+}
+
+// k host doubles from every rank -> out[world][k] on every rank (synchronises s)
+static nugpr_status allgather_host(nugpr_blocks* bl, const double* mine, int k, std::vector<double>& out,
+                                   cudaStream_t s) {
+  nugpr_ctx* ctx = bl->ctx;
+  EvalDev& e = bl->E[0];
+  const size_t tot = static_cast<size_t>(ctx->world) * k;
+  if (tot > static_cast<size_t>(3) * bl->n_cg * MAXC) return fail(NUGPR_ERR_INTERNAL, "exchange buffer too small");
+  CK(cudaMemsetAsync(e.xs, 0, sizeof(double) * tot, s));
+  CK(cudaMemcpyAsync(e.xs + static_cast<size_t>(ctx->rank) * k, mine, sizeof(double) * k, cudaMemcpyHostToDevice, s));
+  RET(xchg(ctx, e.xs, e.xr, tot, s));
+  out.assign(tot, 0.0);
+  CK(cudaMemcpyAsync(out.data(), e.xr, sizeof(double) * tot, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
   return NUGPR_OK;
 }
 
@@ -511,24 +628,47 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   if (reinterpret_cast<uintptr_t>(workspace) % 256) return fail(NUGPR_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   CK(cudaSetDevice(ctx->device));
   cudaGetLastError();   // drop stale errors left by unrelated runtime calls
+  if (!offsets) return fail(NUGPR_ERR_INVALID_ARG, "offsets is NULL");
+  // PAR-2: this rank keeps the contiguous cluster range [c_lo, c_hi) (local layout, local blocks)
+  const bool shard = ctx->ar != nullptr;
+  int c_lo = 0, c_hi = n_c;
+  std::vector<int64_t> loff;
+  const int64_t* offs = offsets;
+  if (shard) {
+    RET(shard_range_impl(offsets, n_c, ctx->rank, ctx->world, &c_lo, &c_hi));
+    loff = local_offsets(offsets, c_lo, c_hi);
+    offs = loff.data();
+  }
+  const int nl = c_hi - c_lo;               // clusters held here (= n_c unless sharded)
   nugpr_blocks* bl = new nugpr_blocks();
-  nugpr_status st = make_layout(offsets, n_c, d, bl->L);
+  nugpr_status st = make_layout(offs, nl, d, bl->L);
   if (st != NUGPR_OK) { delete bl; return st; }
+  bl->shard = shard;
+  bl->c_lo = c_lo; bl->c_hi = c_hi; bl->n_cg = n_c;
+  bl->n_glob = offsets[n_c]; bl->pos0 = offsets[c_lo];
+  if (shard && bl->L.big) {
+    delete bl;
+    return fail(NUGPR_ERR_UNSUPPORTED, "cluster sharding needs clusters <= %d points", LD_SMALL_MAX);
+  }
   // number of eval slots that fit
+  auto need_bytes = [&](int sl) {
+    Carver cz(nullptr);
+    BlocksDev Bz;
+    std::vector<EvalDev> Ez;
+    carve_all(cz, bl->L, sl, Bz, Ez, n_c, offsets[n_c]);
+    return cz.pos + 256;
+  };
   int slots = 0;
   for (int s = NUGPR_NUM_EVALS; s >= 1; --s) {
-    size_t need = 0;
-    ws_size_slots(offsets, n_c, d, s, &need);
-    if (need <= ws_bytes) { slots = s; break; }
+    if (need_bytes(s) <= ws_bytes) { slots = s; break; }
   }
   if (slots == 0) {
-    size_t need = 0;
-    ws_size_slots(offsets, n_c, d, 1, &need);
+    const size_t need = need_bytes(1);
     delete bl;
     return fail(NUGPR_ERR_WORKSPACE, "workspace too small: %zu < %zu bytes", ws_bytes, need);
   }
   Carver c(workspace);
-  carve_all(c, bl->L, slots, bl->B, bl->E);
+  carve_all(c, bl->L, slots, bl->B, bl->E, n_c, offsets[n_c]);
   bl->ctx = ctx;
   bl->ws_base = workspace;
   {
@@ -542,22 +682,22 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   cudaStream_t s = ctx->stream;
   LayoutDev& Ld = bl->Ld;
   Ld.off = B.off; Ld.poff = B.poff; Ld.boff = B.boff; Ld.ld = B.ld; Ld.tiles = B.tiles;
-  Ld.tile0 = B.tile0; Ld.n_c = n_c; Ld.n_tiles = static_cast<int32_t>(L.tiles.size());
+  Ld.tile0 = B.tile0; Ld.n_c = nl; Ld.n_tiles = static_cast<int32_t>(L.tiles.size());
   Ld.ctasks = B.ctasks; Ld.ctask0 = B.ctask0; Ld.n_ctasks = static_cast<int32_t>(L.ctasks.size());
   Ld.n = L.n; Ld.n_pad = L.n_pad;
 #define CKB(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { delete bl; \
     return fail(NUGPR_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
-  CKB(cudaMemcpyAsync(B.off, L.off.data(), sizeof(int64_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.poff, L.poff.data(), sizeof(int64_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.boff, L.boff.data(), sizeof(int64_t) * n_c, cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * n_c, cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.off, L.off.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.poff, L.poff.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.boff, L.boff.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
   CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
   CKB(cudaMemcpyAsync(B.ctasks, L.ctasks.data(), sizeof(TileDesc) * L.ctasks.size(), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (n_c + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.X, X_sorted, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
+  CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+  CKB(cudaMemcpyAsync(B.X, X_sorted + static_cast<size_t>(bl->pos0) * d, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
   CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
-  CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * n_c, s));
+  CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * nl, s));
   for (EvalDev& ev : bl->E) {
     const size_t np = static_cast<size_t>(L.tiles.size()) * MAXC * sizeof(double);
     for (double* p : {ev.SR, ev.SPb[0], ev.SPb[1], ev.SV, ev.SX, ev.dots, ev.rrp}) CKB(cudaMemsetAsync(p, 0, np, s));
@@ -601,24 +741,19 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     PROF(ctx, PC_CHOL, 0.0, s, launch_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, s));
   }
   CKB(cudaGetLastError());
-  std::vector<int32_t> hstat(n_c);
-  CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
+  std::vector<int32_t> hstat(nl);
+  CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
-  bl->h_jitter.assign(n_c, 0.0);
+  bl->h_jitter.assign(nl, 0.0);
   const double base = 1e-8 * (theta0.outputscale + theta0.noise);   // 1e-8 * mean(diag K_i)
+  int fb = -1;                                                       // global index of a failed block
   for (int t = 0; t <= 5; ++t) {
     bl->h_list.clear();
-    for (int i = 0; i < n_c; ++i) if (hstat[i]) bl->h_list.push_back(i);
+    for (int i = 0; i < nl; ++i) if (hstat[i]) bl->h_list.push_back(i);
     if (bl->h_list.empty()) break;
-    if (t == 5) {
-      int fb = bl->h_list[0];
-      if (failed_block) *failed_block = fb;
-      cudaStreamSynchronize(bas);           // the side stream still writes into the workspace
-      delete bl;
-      return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
-    }
+    if (t == 5) { fb = c_lo + bl->h_list[0]; break; }
     for (int i : bl->h_list) bl->h_jitter[i] = base * std::pow(10.0, t);
-    CKB(cudaMemcpyAsync(B.jitter, bl->h_jitter.data(), sizeof(double) * n_c, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.jitter, bl->h_jitter.data(), sizeof(double) * nl, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(B.list, bl->h_list.data(), sizeof(int32_t) * bl->h_list.size(), cudaMemcpyHostToDevice, s));
     if (L.big) {
       launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
@@ -635,13 +770,40 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
                         B.logdet_blk, B.u, s);
     }
     CKB(cudaGetLastError());
-    CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * n_c, cudaMemcpyDeviceToHost, s));
+    CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, s));
     CKB(cudaStreamSynchronize(s));
   }
   for (double j : bl->h_jitter) bl->max_jitter = std::max(bl->max_jitter, j);
+  if (shard) {
+    // every rank learns the first failed block and the largest jitter (one host-level exchange)
+    const double mine[2] = {static_cast<double>(fb + 1), bl->max_jitter};
+    std::vector<double> all;
+    nugpr_status xs_ = allgather_host(bl, mine, 2, all, s);
+    if (xs_ != NUGPR_OK) { cudaStreamSynchronize(bas); delete bl; return xs_; }
+    for (int r = 0; r < ctx->world; ++r) {
+      const int f = static_cast<int>(all[2 * r]) - 1;
+      if (f >= 0 && (fb < 0 || f < fb)) fb = f;
+      bl->max_jitter = std::max(bl->max_jitter, all[2 * r + 1]);
+    }
+  }
+  if (fb >= 0) {
+    if (failed_block) *failed_block = fb;
+    cudaStreamSynchronize(bas);           // the side stream still writes into the workspace
+    delete bl;
+    return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
+  }
   // H_i = Linv_i Linv_i^T ; logdet_R (K_rep, lambda_0, M were launched on the side stream)
   PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
-  launch_sum(B.logdet_blk, n_c, B.scal + 0, s);
+  if (shard) {
+    // logdet_R = 2 sum_i sum_j log (R_i)_jj over ALL clusters: gather the per-cluster terms, then the
+    // same fixed-order sum as one GPU
+    double* lg = bl->E[0].xr;
+    nugpr_status gs_ = gather_clusters(bl, B.logdet_blk, 1, lg, s);
+    if (gs_ != NUGPR_OK) { cudaStreamSynchronize(bas); delete bl; return gs_; }
+    launch_sum(lg, n_c, B.scal + 0, s);
+  } else {
+    launch_sum(B.logdet_blk, n_c, B.scal + 0, s);
+  }
   CKB(cudaGetLastError());
   if (bas != s) CKB(cudaStreamWaitEvent(s, ctx->ev_aux[NUGPR_NUM_EVALS][1], 0));
   double hs[2];
@@ -702,7 +864,7 @@ extern "C" nugpr_status nugpr_blocks_export(const nugpr_blocks* bl, int32_t what
       break;
     }
     case 5: {
-      size_t n = sizeof(double) * L.n_c * L.n_c;
+      size_t n = sizeof(double) * bl->n_cg * bl->n_cg;
       if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
       CK(cudaMemcpyAsync(dst, bl->B.M, n, cudaMemcpyDeviceToHost, s));
       break;
@@ -970,6 +1132,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   t1.task0 = nullptr;
   t1.st = e.st; t1.prm = e.prm; t1.Mp = nullptr; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
   t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
+  t1.row0 = 0; t1.nrows = L.n_c;
   LowrankArgs& t2 = A.t2;
   t2 = t1;
   t2.S = e.SV; t2.fuse_p = 0;
@@ -1012,6 +1175,24 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     A.a1.dots = e.dots; A.a1.fin = FIN_ALPHA;
     for (int c = 0; c < MAXC; ++c) { A.a1.cA[c] = 1.0; A.a1.cV[c] = 0.0; A.a1.cP[c] = 0.0; }
     if (A.pnew) A.t1.task0 = nullptr;
+  }
+  if (bl->shard) {
+    // PAR-2: the partials of this rank's clusters go to their global slots of the zero-padded send
+    // array xs = [rr | S(r) | S(A p), p^T q, S(x), trace dots] ([3][n_cg][MAXC]); the exchange fills
+    // xr with every rank's; finalisers run as fin_kernel after it; T = M'S for the local rows only
+    if (A.pnew || mbcg || L.big)
+      return fail(NUGPR_ERR_UNSUPPORTED, "cluster sharding: column-task apply / mBCG / big blocks not supported");
+    const size_t G = static_cast<size_t>(bl->n_cg) * MAXC, o = static_cast<size_t>(bl->c_lo) * MAXC;
+    A.a1.Sout = e.xs + 2 * G + o;
+    A.a2.dots = e.xs + 2 * G + o; A.a2.fin = FIN_NONE;
+    A.a3.Sout = e.xs + 2 * G + o;
+    A.a4.dots = e.xs + 2 * G + o; A.a4.fin = FIN_NONE;
+    A.ua.rr_part = e.xs + o; A.ua.SR_part = e.xs + G + o; A.ua.nofin = 1;
+    A.t1.S = e.xr + G;
+    A.t2.S = e.xr + 2 * G;
+    A.t3.S = e.xr + 2 * G;
+    A.t4.S = e.xr + 2 * G;
+    for (LowrankArgs* t : {&A.t1, &A.t2, &A.t3, &A.t4}) { t->n_c = bl->n_cg; t->row0 = bl->c_lo; t->nrows = L.n_c; }
   }
   bl->pnew = A.pnew;
   A.st = e.st; A.R = e.R; A.Pb[0] = e.Pb[0]; A.Pb[1] = e.Pb[1]; A.n_pad = L.n_pad; A.ncol = ncol;
@@ -1124,7 +1305,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
       CK(cudaEventRecord(ctx->ev_aux[slot][0], s));
       CK(cudaStreamWaitEvent(as, ctx->ev_aux[slot][0], 0));
     }
-    launch_krep(B.reps, L.n_c, L.d, bl->kind, th.lengthscale, th.outputscale, e.Krep, as);
+    launch_krep(B.reps, bl->n_cg, L.d, bl->kind, th.lengthscale, th.outputscale, e.Krep, as);
     CKL();
     nugpr_status ls;
     PROF(ctx, PC_LANCZOS, 0.0, as, ls = enqueue_lambda0(bl, e.Krep, B.v0, e.lz, e.scal, e.v0, e.M, e.linfo, as));
@@ -1166,18 +1347,31 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   // self-resetting last-CTA tickets) and the S partials start from zero every evaluation
   CK(cudaMemsetAsync(e.st, 0, sizeof(CGState), s));
   // rhs + init
+  const size_t XG = static_cast<size_t>(bl->n_cg) * MAXC, XO = static_cast<size_t>(bl->c_lo) * MAXC;
+  if (bl->shard) CK(cudaMemsetAsync(e.xs, 0, sizeof(double) * 3 * XG, s));   // zero padding of the exchanges
   RhsArgs ra;
-  ra.L = Ld; ra.prm = e.prm; ra.st = e.st; ra.Linv = B.Linv; ra.y = y_dev;
+  ra.L = Ld; ra.prm = e.prm; ra.st = e.st; ra.Linv = B.Linv; ra.y = y_dev + bl->pos0;
   ra.probes = cfg->probes; ra.seed = cfg->probe_seed; ra.u = B.u; ra.RHS = e.RHS; ra.R = e.R;
   ra.X = e.X; ra.P0 = e.Pb[0]; ra.SP0 = e.SPb[0]; ra.SR_part = e.SR; ra.rr_part = e.rrp; ra.ncol = ncol;
   ra.cy = bl->cy_ready ? B.cy : nullptr;
   ra.cy_out = nullptr;
+  ra.pos0 = bl->pos0; ra.n_glob = bl->n_glob; ra.nofin = 0;
+  if (bl->shard) {
+    ra.rr_part = e.xs + XO; ra.SR_part = e.xs + XG + XO; ra.SP0 = e.xs + 2 * XG + XO; ra.nofin = 1;
+  }
   if (ctx->tl_pre) CK(cudaEventRecord(ctx->tl_pre, s));
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
+  if (bl->shard) {
+    // PAR-2: r^T r and S(r) of every rank -> CG state; S(p_0) = S(r_0) (global)
+    RET(xchg(ctx, e.xs, e.xr, 2 * XG, s));
+    launch_fin(FIN_INIT, e.st, e.prm, e.xr, bl->n_cg, ncol, nullptr, HIST, s);
+    CK(cudaMemcpyAsync(e.SPb[0], e.xr + XG, sizeof(double) * XG, cudaMemcpyDeviceToDevice, s));
+    CKL();
+  }
   if (prep_only) return NUGPR_OK;
   const bool useB = P.B != nullptr;
-  if (!ctx->prof && !bl->no_graph) {
+  if (!ctx->prof && !bl->no_graph && !bl->shard) {
     cudaGraphExec_t ex = nullptr;
     RET(get_graph(ctx, bl, slot, ncol, cfg->logdet_mode, &ex));
     CK(cudaGraphLaunch(ex, s));
@@ -1196,6 +1390,41 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
                                       : max_iter;
   const int CH = 4;
   int done = 0;
+  if (bl->shard) {
+    // PAR-2 CG: the same kernels on this rank's clusters, three exchanges per iteration
+    double* xs = e.xs, *xr = e.xr;
+    while (done < limit) {
+      for (int q = 0; q < CH && done < limit; ++q, ++done) {
+        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
+        RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // S(A p)
+        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+        RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // p^T q
+        launch_fin(FIN_ALPHA, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, e.ah, HIST, s);
+        PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
+        RET(xchg(ctx, xs, xr, 2 * XG, s));                                    // r^T r, S(r)
+        launch_fin(FIN_UPDATE, e.st, e.prm, xr, bl->n_cg, ncol, e.bh, HIST, s);
+      }
+      CKL();
+      CK(cudaMemcpyAsync(ctx->h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      if (!*ctx->h_flag) break;
+    }
+    launch_spart(Ld, B.u, e.X, ncol, xs + 2 * XG + XO, s);
+    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(x)
+    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
+    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(A x)
+    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
+    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // quad, trace dots
+    launch_fin(FIN_TRACE, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, nullptr, HIST, s);
+    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(bl->n_glob),
+                 ncol, cfg->logdet_mode, e.out, s);
+    CKL();
+    return NUGPR_OK;
+  }
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
       PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
@@ -1380,7 +1609,7 @@ static nugpr_status check_cfg(const nugpr_solve_cfg* cfg) {
 
 static nugpr_status stage_y(nugpr_blocks* bl, const double* y, cudaStream_t s, const double** y_dev) {
   if (is_device_ptr(y)) { *y_dev = y; return NUGPR_OK; }
-  CK(cudaMemcpyAsync(bl->B.ystage, y, sizeof(double) * bl->L.n, cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(bl->B.ystage, y, sizeof(double) * bl->n_glob, cudaMemcpyHostToDevice, s));
   *y_dev = bl->B.ystage;
   return NUGPR_OK;
 }
@@ -1459,9 +1688,9 @@ struct EvalRecord {
 // (Eq. 11 read as a central difference, reading X2).
 static nugpr_status central_exchange(nugpr_ctx* ctx, const int32_t* owner, const EvalRecord* mine,
                                      const double* h, double* L0, double* grad, nugpr_mll_out* evals,
-                                     nugpr_status* worst) {
+                                     nugpr_status* worst, int world) {
   EvalRecord all[NUGPR_NUM_EVALS];
-  if (ctx->world > 1) {
+  if (world > 1) {
     if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");
     std::vector<EvalRecord> recv(static_cast<size_t>(ctx->world) * NUGPR_NUM_EVALS);
     if (ctx->ag(mine, sizeof(EvalRecord) * NUGPR_NUM_EVALS, recv.data(), ctx->ag_user) != 0)
@@ -1497,7 +1726,7 @@ extern "C" nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta
   for (int k = 0; k < NUGPR_NUM_EVALS; ++k)
     if (owner[k] == ctx->rank) { mine[k].o.L = L_mine[k]; mine[k].valid = 1; mine[k].status = NUGPR_OK; }
   nugpr_status worst = NUGPR_OK;
-  return central_exchange(ctx, owner, mine, h, L0, grad, nullptr, &worst);
+  return central_exchange(ctx, owner, mine, h, L0, grad, nullptr, &worst, ctx->world);
 }
 
 // Evaluate the points `ks` (indices into pts) concurrently: evaluation j runs on slot j % slots,
@@ -1508,7 +1737,7 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   cudaStream_t s0 = ctx->stream;
   const int slots = static_cast<int>(bl->E.size());
   const bool graph = !ctx->prof && !bl->no_graph;
-  if (slots <= 1 || ctx->prof || ks.size() <= 1) {
+  if (slots <= 1 || ctx->prof || ks.size() <= 1 || bl->shard) {
     for (int k : ks) {
       nugpr_status st = run_eval(ctx, bl, y_dev, pts[k], cfg, &recs[k].o);
       recs[k].status = st;
@@ -1627,7 +1856,7 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   int ne = 0;
   // every evaluation of this call shares y and R: c = R^{-T} y is computed once and reused
   struct CyGuard { nugpr_blocks* b; ~CyGuard() { b->cy_ready = false; } } cyg{bl};
-  launch_cy(bl->Ld, bl->B.Linv, y_dev, bl->L.ld_max, bl->B.cy, ctx->stream);
+  launch_cy(bl->Ld, bl->B.Linv, y_dev + bl->pos0, bl->L.ld_max, bl->B.cy, ctx->stream);
   CKL();
   bl->cy_ready = true;
   if (gcfg->mode == NUGPR_GRAD_CENTRAL) {
@@ -1646,14 +1875,16 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
     // G precompute + Lanczos)
     const double cost[NUGPR_NUM_EVALS] = {1.0, 3.0, 3.0, 2.0, 2.0, 2.0, 2.0};
     int32_t owner[NUGPR_NUM_EVALS];
-    RET(nugpr_shard_plan(ctx->world, cost, NUGPR_NUM_EVALS, owner));
+    // (PAR-2 sharded blocks: every rank takes part in every evaluation, so no perturbation split)
+    const int pw = bl->shard ? 1 : ctx->world, pr = bl->shard ? 0 : ctx->rank;
+    RET(nugpr_shard_plan(pw, cost, NUGPR_NUM_EVALS, owner));
     EvalRecord mine[NUGPR_NUM_EVALS];
     memset(mine, 0, sizeof(mine));
     std::vector<int> ks;                       // this rank's evaluations, most expensive first
-    for (int k : {1, 2, 3, 4, 5, 6, 0}) if (owner[k] == ctx->rank) ks.push_back(k);
+    for (int k : {1, 2, 3, 4, 5, 6, 0}) if (owner[k] == pr) ks.push_back(k);
     RET(run_evals_concurrent(ctx, bl, y_dev, ks, tp, scfg, mine));
     nugpr_status worst = NUGPR_OK;
-    RET(central_exchange(ctx, owner, mine, h, L0, grad, evals, &worst));
+    RET(central_exchange(ctx, owner, mine, h, L0, grad, evals, &worst, pw));
     ne = NUGPR_NUM_EVALS;
     if (n_evals) *n_evals = ne;
     if (worst != NUGPR_OK) return fail(worst, "an evaluation did not converge");
@@ -1736,6 +1967,7 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
                                       int64_t n_test, int32_t add_noise, double* mean, double* var) {
   if (!ctx || !bl || !y_sorted || !X_test || !mean) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
   if (n_test < 0) return fail(NUGPR_ERR_INVALID_ARG, "n_test < 0");
+  if (bl->shard) return fail(NUGPR_ERR_UNSUPPORTED, "predict needs replicated (unsharded) blocks");
   if (n_test == 0) return NUGPR_OK;
   const HostLayout& L = bl->L;
   CK(cudaSetDevice(ctx->device));
@@ -1804,6 +2036,7 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
 // determinant lemma + Woodbury on the rank-n_c term, no probes / Pade / CG.
 extern "C" nugpr_status nugpr_mll_exact(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, double out[4]) {
   if (!ctx || !bl || !y_sorted || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  if (bl->shard) return fail(NUGPR_ERR_UNSUPPORTED, "mll_exact needs replicated (unsharded) blocks");
   CK(cudaSetDevice(ctx->device));
   cudaGetLastError();
   cudaStream_t s = ctx->stream;

@@ -143,10 +143,11 @@ struct LowrankArgs {
   const double* S;         // [n_tiles][16] S partials (tiles == clusters); fuse_p: S(R)
   double* SPbuf[2];        // fuse_p: S(P) ping-pong
   int fuse_p;
-  double* T;               // [n_c][16] out
-  int n_c;
+  double* T;               // [nrows][16] out: rows row0 .. row0+nrows-1 of M' S
+  int n_c;                 // S / M' extent (all clusters, also when the clusters are sharded)
   int ncol;
   int gate;
+  int row0, nrows;         // PAR-2: only this rank's clusters' rows of T (row0 = 0, nrows = n_c otherwise)
 };
 
 struct UpdateArgs {
@@ -164,6 +165,7 @@ struct UpdateArgs {
   int hist_stride;
   int ncol;
   unsigned long long cond; // cudaGraphConditionalHandle of the CG while-loop (0 = not in a graph)
+  int nofin;               // PAR-2: no last-CTA finaliser (fin_kernel runs after the partials exchange)
 };
 
 struct RhsArgs {
@@ -185,6 +187,9 @@ struct RhsArgs {
   int ncol;
   const double* cy;        // NULL, or the precomputed transformed RHS c = R^{-T} y (padded layout)
   double* cy_out;          // NULL, or where to store c (first evaluation of a numgrad)
+  int64_t pos0;            // PAR-2: global sorted position of this rank's first row (probe counter)
+  int64_t n_glob;          // row count of the caller's probe matrix (= n when not sharded)
+  int nofin;               // PAR-2: no last-CTA finaliser
 };
 
 __device__ __forceinline__ double warp_sum(double v) {

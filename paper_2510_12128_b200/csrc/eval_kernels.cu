@@ -72,6 +72,119 @@ __device__ __forceinline__ int is_active(const EvalParams* P, int c, int iters, 
   return 1;
 }
 
+// ---------------------------------------------------------------------------------------
+// CG finalisers.  Each runs in ONE CTA over the per-tile partials: in the last CTA of the
+// kernel that wrote them (one GPU), or in fin_kernel after the PAR-2 exchange made the partials
+// of every rank's clusters visible (same partial layout, same summation order => same bits).
+// Warps w = 0..nw-1 stride over the columns.
+__device__ void fin_init_body(CGState* st, const EvalParams* prm, const double* rr_part, int n_tiles, int ncol,
+                              int nw) {
+  __shared__ int act[MAXC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid < nw) {
+    for (int c = wid; c < MAXC; c += nw) {
+      if (c < ncol) {
+        const double tot = col_total(rr_part, n_tiles, c);
+        if (lane == 0) {
+          st->rr[c] = tot;
+          st->rr0[c] = tot;
+          st->alpha[c] = 0.0;
+          st->beta[c] = 0.0;
+          st->iters[c] = 0;
+          st->t[c] = 0.0;
+          act[c] = st->active[c] = is_active(prm, c, 0, tot);
+        }
+      } else if (lane == 0) {
+        st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0;
+        act[c] = 0;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int c = 0; c < ncol; ++c) any |= act[c];
+    st->any_active = any;
+    st->par = 0;
+    st->hit_max = 0;
+    st->quad = 0.0;
+  }
+}
+
+// FIN_ALPHA: alpha_c = r^T r / p^T q (active columns) + history; FIN_TRACE: quad (column 0) and the
+// Pade trace terms t_j.  No block barrier inside (the DMMA apply calls it from its consumer warps).
+__device__ __forceinline__ void fin_alpha_trace_body(int fin, CGState* st, const double* dots, int n_tiles,
+                                                     int ncol, double* alpha_hist, int hist_stride, int nw) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (wid >= nw) return;
+  for (int c = wid; c < ncol; c += nw) {
+    const double tot = col_total(dots, n_tiles, c);
+    if (lane == 0) {
+      if (fin == FIN_ALPHA) {
+        if (st->active[c]) {
+          const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
+          st->alpha[c] = al;
+          alpha_hist[c * hist_stride + st->iters[c]] = al;
+        }
+      } else {  // FIN_TRACE
+        if (c == 0) st->quad = tot; else st->t[c] = tot;
+      }
+    }
+  }
+}
+
+// FIN_UPDATE: beta = r'^T r' / r^T r, history, iteration counters, freezing (readings P3, P5).
+__device__ void fin_update_body(CGState* st, const EvalParams* P, const double* rr_part, int n_tiles, int ncol,
+                                double* beta_hist, int hist_stride, unsigned long long cond, int nw) {
+  __shared__ int act[MAXC];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int par = st->par;
+  if (wid < nw) {
+    for (int c = wid; c < ncol; c += nw) {
+      const bool was = st->active[c] != 0;
+      double tot = 0.0;
+      if (was) tot = col_total(rr_part, n_tiles, c);
+      if (lane == 0) {
+        if (was) {
+          const double be = tot / st->rr[c];
+          st->beta[c] = be;
+          beta_hist[c * hist_stride + st->iters[c]] = be;
+          st->rr[c] = tot;
+          st->iters[c] += 1;
+          const int na = is_active(P, c, st->iters[c], tot);
+          if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
+            st->hit_max = 1;
+          st->active[c] = na;
+        }
+        act[c] = st->active[c];
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int any = 0;
+    for (int c = 0; c < ncol; ++c) any |= act[c];
+    st->any_active = any;
+    st->par = par ^ 1;
+    if (cond) cudaGraphSetConditional(cond, any ? 1u : 0u);
+  }
+}
+
+// PAR-2 (cluster-sharded evaluation): the finaliser as its own single-CTA launch
+// after the exchange of the partials.  FIN_UPDATE skips when no column is active (as update does).
+__global__ void __launch_bounds__(NT) fin_kernel(int fin, CGState* st, const EvalParams* prm, const double* part,
+                                                 int n_tiles, int ncol, double* hist, int hist_stride) {
+  if (fin == FIN_INIT) {
+    fin_init_body(st, prm, part, n_tiles, ncol, NT / 32);
+  } else if (fin == FIN_UPDATE) {
+    if (!st->any_active) return;
+    fin_update_body(st, prm, part, n_tiles, ncol, hist, hist_stride, 0ull, NT / 32);
+  } else {
+    if (fin == FIN_ALPHA && !st->any_active) return;
+    fin_alpha_trace_body(fin, st, part, n_tiles, ncol, hist, hist_stride, NT / 32);
+  }
+}
+
 // Row r of the per-cluster lower triangular product c_i = Linv_i y_i (c = R^{-T} y):
 // one fixed summation order, shared by rhs_init and cy_kernel so both give the same bits.
 __device__ __forceinline__ double trmv_row(const double* Li, const double* ys, int ld, int r) {
@@ -146,7 +259,8 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
       double v;
       if (c == 0) v = cval;
       else if (r >= b) v = 0.0;
-      else v = a.probes ? a.probes[static_cast<int64_t>(c - 1) * n + o + r] : probe_value(a.seed, c - 1, o + r);
+      else v = a.probes ? a.probes[static_cast<int64_t>(c - 1) * a.n_glob + a.pos0 + o + r]
+                         : probe_value(a.seed, c - 1, a.pos0 + o + r);
       const int64_t gi = c * n_pad + g;
       a.RHS[gi] = v;
       a.R[gi] = v;
@@ -164,37 +278,9 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
     a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
     a.SP0[t * MAXC + threadIdx.x] = outv[threadIdx.x];
   }
-  if (last_cta(&a.st->ticket[FIN_INIT])) {
-    CGState* st = a.st;
-    __shared__ int act[MAXC];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int c = wid; c < MAXC; c += NT / 32) {
-      if (c < ncol) {
-        const double tot = col_total(a.rr_part, a.L.n_tiles, c);
-        if (lane == 0) {
-          st->rr[c] = tot;
-          st->rr0[c] = tot;
-          st->alpha[c] = 0.0;
-          st->beta[c] = 0.0;
-          st->iters[c] = 0;
-          st->t[c] = 0.0;
-          act[c] = st->active[c] = is_active(a.prm, c, 0, tot);
-        }
-      } else if (lane == 0) {
-        st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0;
-        act[c] = 0;
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int c = 0; c < ncol; ++c) any |= act[c];
-      st->any_active = any;
-      st->par = 0;
-      st->hit_max = 0;
-      st->quad = 0.0;
-      st->ticket[FIN_INIT] = 0;
-    }
+  if (!a.nofin && last_cta(&a.st->ticket[FIN_INIT])) {
+    fin_init_body(a.st, a.prm, a.rr_part, a.L.n_tiles, ncol, NT / 32);
+    if (threadIdx.x == 0) a.st->ticket[FIN_INIT] = 0;
   }
 }
 
@@ -473,20 +559,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
   if (a.fin != FIN_NONE) {
     if (last_cta(&a.st->ticket[a.fin])) {
       CGState* st = a.st;
-      for (int c = wid; c < ncol; c += NTA / 32) {
-        const double tot = col_total(a.dots, n_tiles, c);
-        if (lane == 0) {
-          if (a.fin == FIN_ALPHA) {
-            if (st->active[c]) {
-              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
-              st->alpha[c] = al;
-              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
-            }
-          } else {  // FIN_TRACE
-            if (c == 0) st->quad = tot; else st->t[c] = tot;
-          }
-        }
-      }
+      fin_alpha_trace_body(a.fin, st, a.dots, n_tiles, ncol, a.alpha_hist, a.hist_stride, NTA / 32);
       __syncthreads();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
@@ -803,20 +876,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
     if (s_last) {
       __threadfence();
       CGState* st = a.st;
-      for (int c = wid; c < ncol; c += NWM) {
-        const double tot = col_total(a.dots, n_tiles, c);
-        if (lane == 0) {
-          if (a.fin == FIN_ALPHA) {
-            if (st->active[c]) {
-              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
-              st->alpha[c] = al;
-              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
-            }
-          } else {  // FIN_TRACE
-            if (c == 0) st->quad = tot; else st->t[c] = tot;
-          }
-        }
-      }
+      fin_alpha_trace_body(a.fin, st, a.dots, n_tiles, ncol, a.alpha_hist, a.hist_stride, NWM);
       mma_sync_consumers();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
@@ -1341,20 +1401,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_staged_kernel(ApplyArgs a) {
     if (s_last) {
       __threadfence();
       CGState* st = a.st;
-      for (int c = wid; c < ncol; c += NWM) {
-        const double tot = col_total(a.dots, n_tiles, c);
-        if (lane == 0) {
-          if (a.fin == FIN_ALPHA) {
-            if (st->active[c]) {
-              const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
-              st->alpha[c] = al;
-              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
-            }
-          } else {  // FIN_TRACE
-            if (c == 0) st->quad = tot; else st->t[c] = tot;
-          }
-        }
-      }
+      fin_alpha_trace_body(a.fin, st, a.dots, n_tiles, ncol, a.alpha_hist, a.hist_stride, NWM);
       mma_sync_consumers();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
@@ -1704,8 +1751,9 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
     }
   }
   __syncthreads();
-  const int i = blockIdx.x * TROWS + wid;
-  if (i >= n_c) return;
+  const int il = blockIdx.x * TROWS + wid;          // row of T (local to this rank's clusters)
+  if (il >= a.nrows) return;
+  const int i = a.row0 + il;                         // row of M'
   const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
   double t[NCP];
 #pragma unroll
@@ -1725,7 +1773,7 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
   for (int c = 0; c < NCP; ++c) t[c] = warp_sum(t[c]);
   if (lane == 0) {
 #pragma unroll
-    for (int c = 0; c < NCP; ++c) a.T[i * MAXC + c] = t[c];
+    for (int c = 0; c < NCP; ++c) a.T[il * MAXC + c] = t[c];
   }
 }
 
@@ -1789,38 +1837,9 @@ __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
   __syncthreads();
   block_reduce_cols<NCP>(sr, sred, outv);
   if (threadIdx.x < ncol) a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
-  if (last_cta(&st->ticket[FIN_UPDATE])) {
-    const EvalParams* P = a.prm;
-    __shared__ int act[MAXC];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    for (int c = wid; c < ncol; c += NT / 32) {
-      const bool was = st->active[c] != 0;
-      double tot = 0.0;
-      if (was) tot = col_total(a.rr_part, a.L.n_tiles, c);
-      if (lane == 0) {
-        if (was) {
-          const double be = tot / st->rr[c];
-          st->beta[c] = be;
-          a.beta_hist[c * a.hist_stride + st->iters[c]] = be;
-          st->rr[c] = tot;
-          st->iters[c] += 1;
-          const int na = is_active(P, c, st->iters[c], tot);
-          if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
-            st->hit_max = 1;
-          st->active[c] = na;
-        }
-        act[c] = st->active[c];
-      }
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int any = 0;
-      for (int c = 0; c < ncol; ++c) any |= act[c];
-      st->any_active = any;
-      st->par = par ^ 1;
-      st->ticket[FIN_UPDATE] = 0;
-      if (a.cond) cudaGraphSetConditional(a.cond, any ? 1u : 0u);
-    }
+  if (!a.nofin && last_cta(&st->ticket[FIN_UPDATE])) {
+    fin_update_body(st, a.prm, a.rr_part, a.L.n_tiles, ncol, a.beta_hist, a.hist_stride, a.cond, NT / 32);
+    if (threadIdx.x == 0) st->ticket[FIN_UPDATE] = 0;
   }
 }
 
@@ -2133,7 +2152,7 @@ template <int NCP>
 static void lowrank_launch_t(const LowrankArgs& a, cudaStream_t s) {
   const size_t smem = sizeof(double) * static_cast<size_t>(a.n_c) * NCP;
   smem_optin(reinterpret_cast<const void*>(lowrank_kernel<NCP>));
-  lowrank_kernel<NCP><<<(a.n_c + TROWS - 1) / TROWS, NT, smem, s>>>(a);
+  lowrank_kernel<NCP><<<(a.nrows + TROWS - 1) / TROWS, NT, smem, s>>>(a);
   note_launch(); post_launch("lowrank_kernel");
 }
 
@@ -2238,6 +2257,12 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
   FinalArgs a{st, prm, ah, bh, stride, slq_work, logdet_R, n, ncol, logdet_mode, out, quad_part, n_quad_part};
   final_kernel<<<1, 32, 0, s>>>(a);
   note_launch(); post_launch("final_kernel");
+}
+
+void launch_fin(int fin, CGState* st, const EvalParams* prm, const double* part, int n_tiles, int ncol,
+                double* hist, int hist_stride, cudaStream_t s) {
+  fin_kernel<<<1, NT, 0, s>>>(fin, st, prm, part, n_tiles, ncol, hist, hist_stride);
+  note_launch(); post_launch("fin_kernel");
 }
 
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s) {
