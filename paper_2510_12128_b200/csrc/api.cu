@@ -9,6 +9,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <ctime>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -182,6 +183,8 @@ struct BlocksDev {
   double* cy = nullptr;       // n_pad: c = R^{-T} y cached across the evaluations of one numgrad
   double* ystage = nullptr;   // n: host y staged to the device
   double* bigscr = nullptr;   // big-block mode: diagonal-block inverses + inverse-step scratch
+  double* cap = nullptr;      // NEXT-1/2: capacitance C = I + M~ (ldc x ldc, ldc = n_c rounded up to 8)
+  double* capscr = nullptr;   // its blocked (big-block) factorisation scratch when ldc > 512
   int64_t* pmeta = nullptr;   // predict: one-block layout of C = I + M~ (off, poff, boff, ld, loff, goff)
 };
 
@@ -224,6 +227,11 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.cy = c.take<double>(L.n_pad);
   B.ystage = c.take<double>(n_glob);
   B.pmeta = c.take<int64_t>(16);
+  {
+    const int ldc = (n_cg + PAD - 1) / PAD * PAD;
+    B.cap = c.take<double>(static_cast<size_t>(ldc) * ldc);
+    if (ldc > LD_SMALL_MAX) B.capscr = c.take<double>(big_scratch_doubles(1, ldc));
+  }
   if (L.big) B.bigscr = c.take<double>(big_scratch_doubles(n_c, L.ld_max));
   E.assign(slots, EvalDev());
   const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
@@ -616,10 +624,55 @@ static nugpr_status allgather_host(nugpr_blocks* bl, const double* mine, int k, 
   return NUGPR_OK;
 }
 
+// reuse: the workspace still holds this layout, X, reps and zeroed slot partials from a previous
+// build on the same arguments (nugpr_train's later epochs: it owns the workspace between them), so
+// the uploads and memsets are skipped.
+static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
+                               int32_t d, const double* reps, int32_t kernel, nugpr_theta theta0, void* workspace,
+                               size_t ws_bytes, nugpr_blocks** out, int32_t* failed_block, double* max_jitter,
+                               bool reuse);
+
 extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets,
                                            int32_t n_c, int32_t d, const double* reps, int32_t kernel,
                                            nugpr_theta theta0, void* workspace, size_t ws_bytes,
                                            nugpr_blocks** out, int32_t* failed_block, double* max_jitter) {
+  return build_impl(ctx, X_sorted, offsets, n_c, d, reps, kernel, theta0, workspace, ws_bytes, out, failed_block,
+                    max_jitter, false);
+}
+
+// NUGPR_BUILD_TRACE=1: host wall-clock of the build phases on stderr (debugging the build's overhead)
+struct BuildTrace {
+  bool on = false;
+  std::vector<std::pair<const char*, double>> pts;
+  double t0 = 0;
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
+  }
+  BuildTrace() {
+    const char* v = getenv("NUGPR_BUILD_TRACE");
+    on = v && v[0] == '1';
+    t0 = now();
+  }
+  void mark(const char* what, cudaStream_t s, bool sync = false) {
+    if (!on) return;
+    if (sync) cudaStreamSynchronize(s);
+    pts.emplace_back(what, now() - t0);
+  }
+  ~BuildTrace() {
+    if (!on) return;
+    fprintf(stderr, "[nugpr build]");
+    for (auto& p : pts) fprintf(stderr, " %s=%.0f", p.first, p.second);
+    fprintf(stderr, " us\n");
+  }
+};
+
+static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
+                               int32_t d, const double* reps, int32_t kernel, nugpr_theta theta0, void* workspace,
+                               size_t ws_bytes, nugpr_blocks** out, int32_t* failed_block, double* max_jitter,
+                               bool reuse) {
+  BuildTrace tr;
   if (failed_block) *failed_block = -1;
   if (max_jitter) *max_jitter = 0.0;
   if (!ctx || !X_sorted || !reps || !workspace || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
@@ -687,22 +740,24 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   Ld.n = L.n; Ld.n_pad = L.n_pad;
 #define CKB(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { delete bl; \
     return fail(NUGPR_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
-  CKB(cudaMemcpyAsync(B.off, L.off.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.poff, L.poff.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.boff, L.boff.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.ctasks, L.ctasks.data(), sizeof(TileDesc) * L.ctasks.size(), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
-  CKB(cudaMemcpyAsync(B.X, X_sorted + static_cast<size_t>(bl->pos0) * d, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
-  CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
-  CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * nl, s));
-  for (EvalDev& ev : bl->E) {
-    const size_t np = static_cast<size_t>(L.tiles.size()) * MAXC * sizeof(double);
-    for (double* p : {ev.SR, ev.SPb[0], ev.SPb[1], ev.SV, ev.SX, ev.dots, ev.rrp}) CKB(cudaMemsetAsync(p, 0, np, s));
-    CKB(cudaMemsetAsync(ev.st, 0, sizeof(CGState), s));
+  if (!reuse) {
+    CKB(cudaMemcpyAsync(B.off, L.off.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.poff, L.poff.data(), sizeof(int64_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.boff, L.boff.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.ctasks, L.ctasks.data(), sizeof(TileDesc) * L.ctasks.size(), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.X, X_sorted + static_cast<size_t>(bl->pos0) * d, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
+    CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
+    for (EvalDev& ev : bl->E) {
+      const size_t np = static_cast<size_t>(L.tiles.size()) * MAXC * sizeof(double);
+      for (double* p : {ev.SR, ev.SPb[0], ev.SPb[1], ev.SV, ev.SX, ev.dots, ev.rrp}) CKB(cudaMemsetAsync(p, 0, np, s));
+      CKB(cudaMemsetAsync(ev.st, 0, sizeof(CGState), s));
+    }
   }
+  CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * nl, s));
   CKB(cudaMemsetAsync(B.u, 0, sizeof(double) * L.n_pad, s));
   // K_rep(theta0), lambda_0, v_0, M depend on the representatives only: side stream, overlapped
   // with the block factorisation below
@@ -723,6 +778,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   }
   if (bas != s) CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][1], bas));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
+  tr.mark("uploads", s, true);
   const bool fused_chol = !L.big && chol_fused_ok(L.ld_max);
   if (L.big) {
     PROF(ctx, PC_OTHER, 0.0, s,
@@ -744,6 +800,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   std::vector<int32_t> hstat(nl);
   CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
+  tr.mark("chol+status", s);
   bl->h_jitter.assign(nl, 0.0);
   const double base = 1e-8 * (theta0.outputscale + theta0.noise);   // 1e-8 * mean(diag K_i)
   int fb = -1;                                                       // global index of a failed block
@@ -793,7 +850,9 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
     return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
   }
   // H_i = Linv_i Linv_i^T ; logdet_R (K_rep, lambda_0, M were launched on the side stream)
+  tr.mark("ladder", s);
   PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
+  tr.mark("H", s, true);
   if (shard) {
     // logdet_R = 2 sum_i sum_j log (R_i)_jj over ALL clusters: gather the per-cluster terms, then the
     // same fixed-order sum as one GPU
@@ -810,6 +869,7 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
   CKB(cudaMemcpyAsync(hs, B.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
 #undef CKB
+  tr.mark("final", s);
   prof_harvest(ctx);
   bl->logdet_R = hs[0];
   bl->lam0 = hs[1];
@@ -1936,12 +1996,8 @@ static nugpr_status factor_capacitance(nugpr_blocks* bl, EvalDev& e, const doubl
   const HostLayout& L = bl->L;
   BlocksDev& B = bl->B;
   const int n_c = L.n_c;
-  const size_t vec = static_cast<size_t>(MAXC) * L.n_pad;
-  if (static_cast<size_t>(ldc) * ldc > vec || static_cast<size_t>(3) * n_c > static_cast<size_t>(n_c) * MAXC)
-    return fail(NUGPR_ERR_WORKSPACE, "capacitance matrix (%d x %d) exceeds the evaluation slot", ldc, ldc);
   const bool big = ldc > LD_SMALL_MAX;
-  if (big && big_scratch_doubles(1, ldc) > vec) return fail(NUGPR_ERR_WORKSPACE, "capacitance scratch too small");
-  double* Cm = e.V;
+  double* Cm = B.cap;                     // its own workspace region (any n_c)
   double* zeta = e.Tbuf, *sd = e.Tbuf + n_c, *lz = e.Tbuf + 2 * n_c;
   launch_pred_setup(bl->Ld, c, B.u, B.M, ldc, zeta, sd, Cm, s);
   int64_t hm[16] = {0, n_c, 0, ldc, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};   // off[2], poff[2], boff[1]
@@ -1951,7 +2007,7 @@ static nugpr_status factor_capacitance(nugpr_blocks* bl, EvalDev& e, const doubl
   CK(cudaMemcpyAsync(B.pmeta, hm, sizeof(hm), cudaMemcpyHostToDevice, s));
   LayoutDev Lc = bl->Ld;
   Lc.off = B.pmeta; Lc.poff = B.pmeta + 2; Lc.boff = B.pmeta + 4; Lc.ld = ldp; Lc.n_c = 1;
-  if (big) launch_big_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, e.Pb[0], s);
+  if (big) launch_big_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, B.capscr, s);
   else launch_chol_trtri(Cm, Lc, nullptr, 0, ldc, e.linfo, e.scal, e.U, s);
   CKL();
   int32_t cst = 0;
@@ -1992,7 +2048,7 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
   double* p = ww + static_cast<int64_t>(n_c) * nt;
   double* pc = e.R;                       // ldc x nt
   double* lp = e.X;                       // ldc x nt
-  double* Cm = e.V;                       // ldc x ldc (C, then Linv_C): factor_capacitance
+  double* Cm = B.cap;                     // ldc x ldc (C, then Linv_C): factor_capacitance
   double* zeta = e.Tbuf, *lz = e.Tbuf + 2 * n_c;
   double* xt = e.Q;                       // nt x d staged test inputs
   double* ostage = e.dots;                // 2 * nt outputs when the user's buffers are host memory
@@ -2090,7 +2146,7 @@ extern "C" nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, cons
     nugpr_blocks* bl = nullptr;
     int32_t fb = -1;
     double jit = 0.0;
-    RET(nugpr_build_blocks(ctx, X_sorted, offsets, n_c, d, reps, kernel, th, workspace, ws_bytes, &bl, &fb, &jit));
+    RET(build_impl(ctx, X_sorted, offsets, n_c, d, reps, kernel, th, workspace, ws_bytes, &bl, &fb, &jit, ep > 0));
     double L0 = 0.0, g[3] = {0, 0, 0};
     nugpr_mll_out ev[1 + 3 * 21];
     int32_t ne = 0;
