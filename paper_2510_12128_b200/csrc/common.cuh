@@ -127,10 +127,14 @@ struct ApplyArgs {
   int d_is_pnew;           // column-task kernel: D := P_new = Pbuf[par^1] (formed by pnew_kernel)
   int big;                 // big-block mode (ld_max > 512): row-tiled apply_big_kernel
   int f32;                 // 1: the DMMA apply streams the FP32-stored block (P->B32)
+  int nw;                  // DMMA apply: consumer warps per CTA (7: 2 CTAs/SM; 3: 4 CTAs/SM)
+  int dstride;             // DMMA apply: > 0 => D_i arrives per chunk with the TMA stream (stage row stride)
 };
 
 struct ApplyPlan {
   int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0, lds = 0;
+  int nw = 7;
+  int dstride = 0;
   size_t smem_b = 0, smem_nob = 0;
   bool ok = false;
 };

@@ -581,6 +581,7 @@ __global__ void __launch_bounds__(NTA, 2) apply_kernel(ApplyArgs a) {
 constexpr int NWM = 7;                    // consumer warps of the DMMA apply (2 CTAs x 8 warps / SM)
 constexpr int NTM = (NWM + 1) * 32;       // + 1 TMA producer warp
 constexpr int LDP = 12;                   // row stride of the probe block in shared memory
+constexpr int NW_SMALL = 3;               // consumer warps of the 4-CTA/SM DMMA apply (ld <= 9 * 3 * 8 = 216)
 
 __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
@@ -590,16 +591,23 @@ __device__ __forceinline__ void dmma884(double& d0, double& d1, double a, double
 __device__ __forceinline__ void mma_sync_consumers() {
   asm volatile("bar.sync 1, %0;" ::"r"(NWM * 32) : "memory");
 }
+template <int NW>
+__device__ __forceinline__ void bar_consumers() {
+  asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+}
 
-template <int MTMAX, typename TB>   // m-tiles per warp: 4 (ld <= 224), 8, 10; TB: stored element of B
-__global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
+// NW: consumer warps.  NW = NW (7): 2 CTAs per SM, persistent over clusters.  NW = 3 (128
+// threads, <= 128 registers): 4 CTAs per SM, so that at C3 every cluster has its own CTA and the
+// per-cluster phases (forming D_i, the epilogue) of co-resident CTAs overlap each other's streams.
+template <int MTMAX, typename TB, int NW>   // m-tiles per warp; TB: stored element of B
+__global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_kernel(ApplyArgs a) {
   constexpr int EG = 2;                      // m-tiles per epilogue load group
   constexpr int NCPE = 10;                 // epilogue column slots (9 used)
   if (a.gate && !a.st->any_active) return;
   extern __shared__ __align__(128) double sm[];
   __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
   __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
-  __shared__ double sred[NWM * NCPE];
+  __shared__ double sred[NW * NCPE];
   __shared__ double Esm[NCPE];
   __shared__ double cb[2 * NCPE];
   const int tid = threadIdx.x;
@@ -615,15 +623,21 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   const int slot = a.slot_doubles;
   const int nstage = a.nstage;
   const int G = gridDim.x;
+  // progressive D (dstride > 0, with a block term): the TMA producer also brings each chunk's k-rows
+  // of D (and of P_old for the fused first apply) into a per-stage area next to the B chunk, so the
+  // consumers start on the block stream at once instead of first loading all of D_i
+  const int pd = a.dstride;
+  const bool prog = useB && pd > 0;
   double* ring = sm;                                         // nstage * slot (useB only)
-  double* Dp = ring + (useB ? nstage * slot : 0);            // ld_max * LDP
+  double* Dst = ring + (useB ? nstage * slot : 0);           // prog: nstage * 18 * pd ([c][pd], R then P_old)
+  double* Dp = Dst + (prog ? nstage * 18 * pd : 0);          // ld_max * LDP
   double* ys = Dp + a.ld_max * LDP;                          // ld_max
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
   const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 ? a.Pbuf[par ^ 1] : a.Y2;
   if (tid == 0) {
-    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NWM); }
+    for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], NW); }
     fence_mbar_init();
   }
   if (tid < NCPE) {
@@ -631,7 +645,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
     cb[NCPE + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
   __syncthreads();
-  if (wid == NWM) {
+  if (wid == NW) {
     // ============================ TMA producer ============================
     if (lane == 0 && useB) {
       uint32_t pseq = 0;
@@ -667,9 +681,19 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
           if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
           const int kc = min(KC, ld - ck0);
           const uint32_t bytes = static_cast<uint32_t>(kc) * ld * static_cast<uint32_t>(sizeof(TB));
+          const uint32_t dseg = static_cast<uint32_t>(kc) * 8u;
+          const uint32_t dbytes = prog ? dseg * 9u * (a.fuse_p ? 2u : 1u) : 0u;
           fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&full[s_], bytes);
+          mbar_arrive_expect_tx(&full[s_], bytes + dbytes);
           tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
+          if (prog) {
+            const int64_t p0 = a.L.poff[i];
+            double* ds = Dst + s_ * 18 * pd;
+            for (int c = 0; c < 9; ++c) {
+              tma_load_1d(ds + c * pd, a.D + c * n_pad + p0 + ck0, dseg, &full[s_]);
+              if (a.fuse_p) tma_load_1d(ds + (9 + c) * pd, Pold + c * n_pad + p0 + ck0, dseg, &full[s_]);
+            }
+          }
         }
       }
     }
@@ -696,8 +720,10 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
     const int mtt = ld >> 3;                               // m-tiles of the cluster
     // 1. D_i -> shared (fused: D = R + beta o P_old for active columns, P_new written back);
     //    loads batched 4 deep per thread so one cluster costs ~one memory round trip
-    if (a.dbg & 4) {
-      for (int idx = tid; idx < ld * 9; idx += NWM * 32) {
+    if (prog) {
+      // (D_i arrives chunk by chunk with the block stream)
+    } else if (a.dbg & 4) {
+      for (int idx = tid; idx < ld * 9; idx += NW * 32) {
         const int c = idx / ld, k = idx - c * ld;
         const int64_t gi = c * n_pad + p0 + k;
         double v = a.D[gi];
@@ -711,12 +737,12 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
     } else {
       /* batched conversion below */
       const int tot = ld * 9;
-      constexpr int CU = 4;
-      for (int base = 0; base < tot; base += CU * NWM * 32) {
+      constexpr int CU = (NW < 5) ? 8 : 4;
+      for (int base = 0; base < tot; base += CU * NW * 32) {
         double v[CU], po[CU];
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-          const int idx = base + u * NWM * 32 + tid;
+          const int idx = base + u * NW * 32 + tid;
           v[u] = 0.0; po[u] = 0.0;
           if (idx < tot) {
             const int c = idx / ld, k = idx - c * ld;
@@ -727,7 +753,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         }
 #pragma unroll
         for (int u = 0; u < CU; ++u) {
-          const int idx = base + u * NWM * 32 + tid;
+          const int idx = base + u * NW * 32 + tid;
           if (idx < tot) {
             const int c = idx / ld, k = idx - c * ld;
             double x = v[u];
@@ -740,7 +766,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         }
       }
     }
-    mma_sync_consumers();
+    bar_consumers<NW>();
     stamp();
     // 2. block term: DMMA over the ring chunks
     double acc0[MTMAX], acc1[MTMAX], accy[MTMAX];
@@ -753,7 +779,42 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         const int s_ = static_cast<int>(seq % nstage);
         mbar_wait(&full[s_], (seq / nstage) & 1u);
         const TB* cbuf = reinterpret_cast<const TB*>(ring + s_ * slot);
-        if (!(a.dbg & 1)) {
+        if (prog) {
+          const double* ds = Dst + s_ * 18 * pd;
+          // the D value of column c at chunk row kk (fused: R + beta o P_old for active columns)
+          auto dval = [&](int c, int kk) -> double {
+            double v = ds[c * pd + kk];
+            if (a.fuse_p) {
+              const double po = ds[(9 + c) * pd + kk];
+              v = (cb[NCPE + c] != 0.0) ? v + cb[c] * po : po;
+            }
+            return v;
+          };
+          for (int kq = 0; kq < kc; kq += 4) {
+            const int kk = kq + qc;
+            const double bfr = dval(1 + qr, kk);             // B fragment: D_p[k][n = qr]
+            const double yv = dval(0, kk);
+            const TB* acol = cbuf + kk * ld + qr;            // A fragment base: B_i[r][k]
+#pragma unroll
+            for (int j = 0; j < MTMAX; ++j) {
+              const int mt = wid + j * NW;
+              if (mt < mtt) {
+                const double afr = static_cast<double>(acol[mt * 8]);
+                dmma884(acc0[j], acc1[j], afr, bfr);
+                accy[j] = fma(afr, yv, accy[j]);
+              }
+            }
+          }
+          // one warp per chunk keeps D_i for the epilogue (and writes P_new of the fused apply)
+          if (wid == static_cast<int>(seq % NW)) {
+            for (int idx = lane; idx < 9 * kc; idx += 32) {
+              const int c = idx / kc, kk = idx - c * kc;
+              const double v = dval(c, kk);
+              if (a.fuse_p) Pnew[c * n_pad + p0 + k0 + kk] = v;
+              if (c == 0) ys[k0 + kk] = v; else Dp[(k0 + kk) * LDP + (c - 1)] = v;
+            }
+          }
+        } else if (!(a.dbg & 1)) {
           for (int kq = 0; kq < kc; kq += 4) {
             const int k = k0 + kq + qc;                      // this lane's k in the cluster
             const double bfr = Dp[k * LDP + qr];             // B fragment: D_p[k][n = qr]
@@ -761,7 +822,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
             const TB* acol = cbuf + (kq + qc) * ld + qr;     // A fragment base: B_i[r][k]
 #pragma unroll
             for (int j = 0; j < MTMAX; ++j) {
-              const int mt = wid + j * NWM;
+              const int mt = wid + j * NW;
               if (mt < mtt) {
                 const double afr = static_cast<double>(acol[mt * 8]);
                 dmma884(acc0[j], acc1[j], afr, bfr);
@@ -774,6 +835,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         if (lane == 0) mbar_arrive(&empty[s_]);
       }
     }
+    if (prog) bar_consumers<NW>();            // D_i complete in shared memory for the epilogue
     stamp();
     // y column: reduce the 4 k-lanes of each row quad
 #pragma unroll
@@ -797,7 +859,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
         double uu[EG], p2v[EG][3], y2v[EG][3];
 #pragma unroll
         for (int jj = 0; jj < EG; ++jj) {
-          const int mt = wid + (jg + jj) * NWM;
+          const int mt = wid + (jg + jj) * NW;
           const bool on = mt < mtt;
           const int r = mt * 8 + qr;
           uu[jj] = on ? __ldg(a.u + p0 + r) : 0.0;
@@ -813,7 +875,7 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
 #pragma unroll
         for (int jj = 0; jj < EG; ++jj) {
           const int j = jg + jj;
-          const int mt = wid + j * NWM;
+          const int mt = wid + j * NW;
           if (mt < mtt) {
             const int r = mt * 8 + qr;
 #pragma unroll
@@ -847,14 +909,14 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
 #pragma unroll
       for (int c = 0; c < NCPE; ++c) sred[wid * NCPE + c] = ep[c];
     }
-    mma_sync_consumers();
+    bar_consumers<NW>();
     if (tid < ncol) {
       double s = 0.0;
-      for (int w = 0; w < NWM; ++w) s += sred[w * NCPE + tid];
+      for (int w = 0; w < NW; ++w) s += sred[w * NCPE + tid];
       if (a.epi == EPI_S) a.Sout[t * MAXC + tid] = s;
       else a.dots[t * MAXC + tid] = s;
     }
-    mma_sync_consumers();                                   // sred / Dp / ys reuse
+    bar_consumers<NW>();                                   // sred / Dp / ys reuse
     stamp();
   }
   if ((a.dbg & 16) && tid == 0) {
@@ -867,17 +929,17 @@ __global__ void __launch_bounds__(NTM, 2) apply_mma_kernel(ApplyArgs a) {
   if (a.fin != FIN_NONE) {
     __shared__ int s_last;
     __threadfence();
-    mma_sync_consumers();
+    bar_consumers<NW>();
     if (tid == 0) {
       const unsigned int tk = atomicAdd(&a.st->ticket[a.fin], 1u);
       s_last = (tk == gridDim.x - 1);
     }
-    mma_sync_consumers();
+    bar_consumers<NW>();
     if (s_last) {
       __threadfence();
       CGState* st = a.st;
-      fin_alpha_trace_body(a.fin, st, a.dots, n_tiles, ncol, a.alpha_hist, a.hist_stride, NWM);
-      mma_sync_consumers();
+      fin_alpha_trace_body(a.fin, st, a.dots, n_tiles, ncol, a.alpha_hist, a.hist_stride, NW);
+      bar_consumers<NW>();
       if (tid == 0) st->ticket[a.fin] = 0;
     }
   }
@@ -2009,7 +2071,6 @@ void launch_d2f(const double* src, float* dst, int64_t n, cudaStream_t s) {
 // kernel unless NUGPR_APPLY_MMA=0; the ring depth is chosen to fit; NUGPR_APPLY_{SLOT,PER,BAL}
 // are tuning knobs (slot doubles, max CTAs per SM, equal clusters per CTA).
 ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid_unused, int n_ctasks) {
-  (void)ld_min;
   (void)grid_unused;
   int dev = 0, optin = 0, per_sm = 0;
   cudaGetDevice(&dev);
@@ -2060,9 +2121,31 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
       if (p.ok) return p;
     }
   }
+  // experimental (NUGPR_APPLY_SMALL=1): 4 CTAs per SM of 3 consumer warps each, one cluster per
+  // CTA, ld <= 216.  Measured at C3: apply 57.3 us (ncu) vs 54.7 us for the 2-CTA/SM kernel, and
+  // numgrad 7.15 vs 6.65 ms — the per-cluster phases of co-resident CTAs run in lockstep, so more
+  // CTAs do not overlap them (profiles/r01i_apply_small_ab.txt)
+  if (mma && ld_max <= 9 * NW_SMALL * 8 && env_int("NUGPR_APPLY_SMALL", 0) != 0) {
+    ApplyPlan p;
+    p.mma = 1;
+    p.nw = NW_SMALL;
+    const int per = 4;
+    const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - static_smem;
+    p.ctas_per_sm = per;
+    p.grid = std::min(n_tiles, per * num_sms());
+    p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
+    p.slot_doubles = std::max(env_int("NUGPR_APPLY_SLOT_SMALL", 4 * ld_max), 4 * ld_max);
+    const long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
+    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+    p.smem_nob = fixed * sizeof(double);
+    p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
+    p.ok = p.nstage >= 2;
+    if (p.ok) return p;
+  }
   for (int per = per_max; per >= 1; --per) {
     ApplyPlan p;
     p.mma = mma ? 1 : 0;
+    p.nw = NWM;
     const size_t budget = std::min<size_t>(static_cast<size_t>(optin), static_cast<size_t>(per_sm) / per) - static_smem;
     p.red_doubles = 0;
     p.ctas_per_sm = per;
@@ -2070,14 +2153,21 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
     p.nmine_max = (n_tiles + p.grid - 1) / p.grid;
     if (balance) p.grid = (n_tiles + p.nmine_max - 1) / p.nmine_max;
     p.slot_doubles = std::max(slot_target, mma ? 4 * ld_max : ld_max);
+    // progressive D (DMMA apply): per stage also 18 rows-of-chunk of D / P_old, row stride dstride
+    // (the largest chunk width over the clusters for FP32 or FP64 blocks, + 2 against bank conflicts)
+    const bool prog = mma && env_int("NUGPR_APPLY_PROG", 0) != 0;   // experimental: slower at C3 (profiles/r01i_apply_prog_sweep.txt)
+    auto dstride_for = [&](int slot) { return prog ? std::max(4, (2 * slot / std::max(ld_min, 8)) & ~3) + 2 : 0; };
+    p.dstride = dstride_for(p.slot_doubles);
     long avail = static_cast<long>(budget / sizeof(double)) - static_cast<long>(fixed);
-    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+    p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / (p.slot_doubles + 18 * p.dstride)));
     if (p.nstage < 2) {
       p.slot_doubles = mma ? 4 * ld_max : ld_max;
-      p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / p.slot_doubles));
+      p.dstride = dstride_for(p.slot_doubles);
+      p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail / (p.slot_doubles + 18 * p.dstride)));
     }
     p.smem_nob = fixed * sizeof(double);
-    p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * p.slot_doubles) * sizeof(double);
+    p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * (p.slot_doubles + 18 * p.dstride)) *
+               sizeof(double);
     p.ok = p.nstage >= 2;
     if (p.ok) return p;
   }
@@ -2122,10 +2212,18 @@ void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s) {
     size_t smem = useB ? a.smem_b : a.smem_nob;
 #define NUGPR_AMK(MT, TBT)                                                                  \
   do {                                                                                      \
-    smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<MT, TBT>));                  \
-    apply_mma_kernel<MT, TBT><<<a.grid, NTM, smem, s>>>(a);                                \
+    smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<MT, TBT, NWM>));             \
+    apply_mma_kernel<MT, TBT, NWM><<<a.grid, NTM, smem, s>>>(a);                           \
   } while (0)
-    if (a.ld_max <= 4 * NWM * 8) {
+    if (a.nw == NW_SMALL) {
+      if (a.f32) {
+        smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<9, float, NW_SMALL>));
+        apply_mma_kernel<9, float, NW_SMALL><<<a.grid, (NW_SMALL + 1) * 32, smem, s>>>(a);
+      } else {
+        smem_optin(reinterpret_cast<const void*>(apply_mma_kernel<9, double, NW_SMALL>));
+        apply_mma_kernel<9, double, NW_SMALL><<<a.grid, (NW_SMALL + 1) * 32, smem, s>>>(a);
+      }
+    } else if (a.ld_max <= 4 * NWM * 8) {
       if (a.f32) NUGPR_AMK(4, float); else NUGPR_AMK(4, double);
     } else if (a.ld_max <= 8 * NWM * 8) {
       if (a.f32) NUGPR_AMK(8, float); else NUGPR_AMK(8, double);
