@@ -314,6 +314,10 @@ struct nugpr_ctx {
   cudaEvent_t ev_aux[NUGPR_NUM_EVALS + 1][2] = {{nullptr}};
   EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
   cudaEvent_t tl_pre = nullptr;          // NUGPR_TIMELINE: recorded before rhs_init of the next eval
+  // nugpr_train's deferred build: H_i = Linv_i Linv_i^T on its own stream, overlapping the
+  // evaluations that do not read H (baseline, lengthscale steps); ev_h1 marks it done
+  cudaStream_t h_stream = nullptr;
+  cudaEvent_t ev_h0 = nullptr, ev_h1 = nullptr;
   // instantiated CG graphs keyed by (workspace, layout, slot, ncol, logdet mode)
   std::unordered_map<std::string, cudaGraphExec_t> graphs;
   std::vector<cudaGraph_t> graph_defs;
@@ -397,6 +401,7 @@ struct nugpr_blocks {
   bool pnew = false;          // the CG iteration launches pnew_kernel (launch accounting)
   bool f32 = false;           // current evaluation streams FP32-stored blocks
   bool h32_ready = false;     // H32 holds the FP32 copy of H
+  bool h_pending = false;     // H is being formed on ctx->h_stream (wait on ctx->ev_h1 before reading it)
   // PAR-2: this rank's cluster range of the global problem (L is the local layout)
   bool shard = false;
   int c_lo = 0, c_hi = 0, n_cg = 0;
@@ -486,6 +491,9 @@ nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
     for (int e = 0; e < 2; ++e) if (ctx->ev_aux[k][e]) cudaEventDestroy(ctx->ev_aux[k][e]);
   }
   if (ctx->capture_stream) cudaStreamDestroy(ctx->capture_stream);
+  if (ctx->h_stream) cudaStreamDestroy(ctx->h_stream);
+  if (ctx->ev_h0) cudaEventDestroy(ctx->ev_h0);
+  if (ctx->ev_h1) cudaEventDestroy(ctx->ev_h1);
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
@@ -630,7 +638,7 @@ static nugpr_status allgather_host(nugpr_blocks* bl, const double* mine, int k, 
 static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
                                int32_t d, const double* reps, int32_t kernel, nugpr_theta theta0, void* workspace,
                                size_t ws_bytes, nugpr_blocks** out, int32_t* failed_block, double* max_jitter,
-                               bool reuse);
+                               bool reuse, bool defer = false);
 
 extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets,
                                            int32_t n_c, int32_t d, const double* reps, int32_t kernel,
@@ -671,7 +679,7 @@ struct BuildTrace {
 static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
                                int32_t d, const double* reps, int32_t kernel, nugpr_theta theta0, void* workspace,
                                size_t ws_bytes, nugpr_blocks** out, int32_t* failed_block, double* max_jitter,
-                               bool reuse) {
+                               bool reuse, bool defer) {
   BuildTrace tr;
   if (failed_block) *failed_block = -1;
   if (max_jitter) *max_jitter = 0.0;
@@ -851,7 +859,20 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   }
   // H_i = Linv_i Linv_i^T ; logdet_R (K_rep, lambda_0, M were launched on the side stream)
   tr.mark("ladder", s);
-  PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
+  defer = defer && !ctx->prof;
+  if (defer) {
+    // deferred (nugpr_train): H on its own stream; the evaluations that read it wait on ev_h1
+    if (!ctx->h_stream) CKB(cudaStreamCreateWithFlags(&ctx->h_stream, cudaStreamNonBlocking));
+    if (!ctx->ev_h0) CKB(cudaEventCreateWithFlags(&ctx->ev_h0, cudaEventDisableTiming));
+    if (!ctx->ev_h1) CKB(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
+    CKB(cudaEventRecord(ctx->ev_h0, s));
+    CKB(cudaStreamWaitEvent(ctx->h_stream, ctx->ev_h0, 0));
+    launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, ctx->h_stream);
+    CKB(cudaEventRecord(ctx->ev_h1, ctx->h_stream));
+    bl->h_pending = true;
+  } else {
+    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
+  }
   tr.mark("H", s, true);
   if (shard) {
     // logdet_R = 2 sum_i sum_j log (R_i)_jj over ALL clusters: gather the per-cluster terms, then the
@@ -865,6 +886,16 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   }
   CKB(cudaGetLastError());
   if (bas != s) CKB(cudaStreamWaitEvent(s, ctx->ev_aux[NUGPR_NUM_EVALS][1], 0));
+  if (defer) {
+    // no host read-back: logdet_R and lambda_0 stay on the device (the evaluations' records carry
+    // them and check lambda_0 > 0 themselves)
+    CKB(cudaGetLastError());
+    bl->logdet_R = NAN;
+    bl->lam0 = NAN;
+    if (max_jitter) *max_jitter = bl->max_jitter;
+    *out = bl;
+    return NUGPR_OK;
+  }
   double hs[2];
   CKB(cudaMemcpyAsync(hs, B.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
@@ -1382,6 +1413,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     if (as != s) CK(cudaStreamWaitEvent(s, ctx->ev_aux[slot][1], 0));
     lam0_ptr = e.scal;
   }
+  if (P.B == B.H && bl->h_pending) CK(cudaStreamWaitEvent(s, ctx->ev_h1, 0));   // deferred build's H
   bl->f32 = cfg->block_storage == NUGPR_BLOCKS_F32;
   if (bl->f32) {
     if (L.big) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs clusters <= %d points", LD_SMALL_MAX);
@@ -1397,12 +1429,14 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   }
   P.mode = mode;
   P.lam0_src = lam0_ptr;
+  P.lam0_mul = 1.0;
   if (mode_out) *mode_out = mode;
   if (mode == NUGPR_MODE_SCALE) {
     // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
     // build read back (reported in the record only)
-    P.lam0_val = bl->lam0 * P.mscale;
-    P.lam0_src = nullptr;
+    // (read on the device from the build's lambda_0: the build need not sync to the host first)
+    P.lam0_src = B.scal + 1;
+    P.lam0_mul = P.mscale;
   }
   CK(cudaMemcpyAsync(e.prm, &P, sizeof(P), cudaMemcpyHostToDevice, s));
   // the workspace is caller memory with arbitrary contents: the CG state (incl. the
@@ -1819,6 +1853,7 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
     cudaEventRecord(tl0, s0);
   }
   if (cfg->block_storage == NUGPR_BLOCKS_F32 && !bl->h32_ready && !bl->L.big) {
+    if (bl->h_pending) CK(cudaStreamWaitEvent(s0, ctx->ev_h1, 0));
     launch_d2f(bl->B.H, bl->B.H32, bl->L.blk_total, s0);   // before the fork: every stream reads it
     CKL();
     bl->h32_ready = true;
@@ -2148,11 +2183,13 @@ extern "C" nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, cons
     nugpr_blocks* bl = nullptr;
     int32_t fb = -1;
     double jit = 0.0;
-    RET(build_impl(ctx, X_sorted, offsets, n_c, d, reps, kernel, th, workspace, ws_bytes, &bl, &fb, &jit, ep > 0));
+    RET(build_impl(ctx, X_sorted, offsets, n_c, d, reps, kernel, th, workspace, ws_bytes, &bl, &fb, &jit, ep > 0,
+                   true));
     double L0 = 0.0, g[3] = {0, 0, 0};
     nugpr_mll_out ev[1 + 3 * 21];
     int32_t ne = 0;
     nugpr_status st = nugpr_numgrad(ctx, bl, y_sorted, th, gcfg, scfg, &L0, g, ev, &ne);
+    if (bl->h_pending) cudaStreamWaitEvent(ctx->stream, ctx->ev_h1, 0);   // H done before the next build
     nugpr_blocks_destroy(bl);
     if (st != NUGPR_OK) return st;
     if (records) {

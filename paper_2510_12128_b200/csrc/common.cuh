@@ -63,8 +63,9 @@ struct EvalParams {
   int32_t replay_iters[MAXC];
   int32_t ncol;
   int32_t mode;
-  const double* lam0_src;  // lambda_0(theta) for the record: device scalar, or NULL => lam0_val
+  const double* lam0_src;  // lambda_0(theta) for the record: device scalar (times lam0_mul), or NULL => lam0_val
   double lam0_val;
+  double lam0_mul;
 };
 
 // CG state for up to MAXC columns, updated only by "last CTA" finalisers.

@@ -1996,7 +1996,7 @@ __global__ void final_kernel(FinalArgs a) {
     o.logdet_slq = ldR + ssum / m;
     o.logdet = (a.logdet_mode != 0) ? o.logdet_slq : o.logdet_pade;
     o.L = 0.5 * (o.quad + o.logdet + a.n * 1.8378770664093453);   // n log(2 pi)
-    o.lambda0 = a.prm->lam0_src ? a.prm->lam0_src[0] : a.prm->lam0_val;
+    o.lambda0 = a.prm->lam0_src ? a.prm->lam0_src[0] * a.prm->lam0_mul : a.prm->lam0_val;
     o.resid_y = sqrt(st->rr[0]);
     o.resid_q_max = rq;
     o.iters_y = st->iters[0];

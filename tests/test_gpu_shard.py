@@ -35,6 +35,9 @@ def _free_port():
 
 
 def dataset(case):
+    if case == "C5":
+        ds = synth.make_config("C5")
+        return ds.X, ds.y, ds.offsets, ds.reps, tuple(ds.theta0)
     if case == "uneven":
         rng = np.random.default_rng(7)
         sizes = rng.integers(60, 400, size=13)
@@ -52,6 +55,13 @@ def run_all(P, ctx, case):
     X, y, off, reps, th0 = dataset(case)
     bg = P.build_blocks(ctx, X, off, reps, th0)
     out = {}
+    if case == "C5":                  # full size: one evaluation per operator mode family
+        out["pade"] = P.mll(ctx, bg, y, th0, probe_seed=205)
+        out["noise"] = P.mll(ctx, bg, y, (th0[0], th0[1] * 1.001, th0[2]), probe_seed=205)
+        out["lam"] = P.mll(ctx, bg, y, (th0[0] * 1.001, th0[1], th0[2]), probe_seed=205)
+        out["scalars"] = [float(v) for v in bg.export("scalars")]
+        bg.close()
+        return out
     out["pade"] = P.mll(ctx, bg, y, th0, probe_seed=5)
     out["slq"] = P.mll(ctx, bg, y, th0, probe_seed=5, logdet="slq")
     L0, g, ev = P.numgrad(ctx, bg, y, th0, probe_seed=5)
@@ -170,3 +180,22 @@ def test_cluster_shard_nccl_world1(P):
     outs = spawn(1, "nccl", "c3shape")
     assert outs[0]["exchanges"] > 0
     check_against_replicated(P, outs, "c3shape")
+
+
+def test_cluster_shard_C5_full_size_world4(P):
+    """C5 (n = 1M, 2000 clusters x 500) split over 4 ranks (500 clusters each; gloo, all on cuda:0):
+    baseline, noise-step and lengthscale-step evaluations equal the replicated one-GPU path."""
+    outs = spawn(4, "gloo", "C5")
+    assert [o["range"] for o in outs] == [(0, 500), (500, 1000), (1000, 1500), (1500, 2000)]
+    ctx = P.Context(0)
+    X, y, off, reps, th0 = dataset("C5")
+    bg = P.build_blocks(ctx, X, off, reps, th0)
+    ref = {"pade": P.mll(ctx, bg, y, th0, probe_seed=205),
+           "noise": P.mll(ctx, bg, y, (th0[0], th0[1] * 1.001, th0[2]), probe_seed=205),
+           "lam": P.mll(ctx, bg, y, (th0[0] * 1.001, th0[1], th0[2]), probe_seed=205)}
+    scal = [float(v) for v in bg.export("scalars")]
+    bg.close()
+    for out in outs:
+        for k in ("pade", "noise", "lam"):
+            same_rec(out[k], ref[k])
+        np.testing.assert_allclose(out["scalars"], scal, rtol=TIGHT)
