@@ -820,7 +820,7 @@ __device__ __forceinline__ void dmma884g(double& d0, double& d1, double a, doubl
 }
 
 template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM>
-__global__ void __launch_bounds__(256) gemm_dmma_kernel(GemmArgs g) {
+__global__ void __launch_bounds__(256, 3) gemm_dmma_kernel(GemmArgs g) {
   const int i = blockIdx.y;
   const int ld = g.ld[i];
   const int nt = (ld + 63) / 64;

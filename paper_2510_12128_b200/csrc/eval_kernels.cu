@@ -1952,9 +1952,12 @@ __global__ void final_kernel(FinalArgs a) {
     const int k = st->iters[j];
     double val = 0.0;
     if (k > 0) {
+      // the usual k (<= 64 CG iterations) in shared memory; long histories in the global scratch
+      __shared__ double sh_dez[MAXC][3][64];
       double* d = a.slq_work + static_cast<int64_t>(j) * 3 * a.hist_stride;
       double* e = d + a.hist_stride;
       double* z = e + a.hist_stride;
+      if (k <= 64) { d = sh_dez[j][0]; e = sh_dez[j][1]; z = sh_dez[j][2]; }
       const double* al = a.alpha_hist + j * a.hist_stride;
       const double* be = a.beta_hist + j * a.hist_stride;
       d[0] = 1.0 / al[0];

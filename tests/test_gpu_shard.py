@@ -51,7 +51,41 @@ def dataset(case):
     return ds.X, ds.y, ds.offsets, ds.reps, tuple(ds.theta0)
 
 
+def variants(P, ctx):
+    """Jitter ladder, NOT_SPD agreement, FP32 block storage and FORWARD_HALVING under the same
+    context (sharded or not)."""
+    from paper_2510_12128_b200 import _native as N
+    out = {}
+    rng = np.random.default_rng(2)
+    X = np.concatenate([rng.normal(size=(12, 2)), 5 + rng.normal(size=(12, 2)), np.zeros((12, 2)),
+                        -5 + rng.normal(size=(12, 2))])
+    y = rng.normal(size=48)
+    off = np.array([0, 12, 24, 36, 48], dtype=np.int64)
+    reps = np.array([[0.0, 0.0], [5.0, 5.0], [0.0, 0.0], [-5.0, -5.0]]) + np.array([[0, 0], [0, 0], [0.0, 9.0], [0, 0]])
+    th0 = (1.0, 1e-18, 1.0)
+    bg = P.build_blocks(ctx, X, off, reps, th0)          # cluster 2 (identical points) needs jitter
+    out["max_jitter"] = bg.max_jitter
+    out["jitter_mll"] = P.mll(ctx, bg, y, th0, probe_seed=9, tol=1e-6)
+    bg.close()
+    Xn = X.copy()
+    Xn[40] = np.nan                                        # cluster 3 cannot be factorised
+    try:
+        P.build_blocks(ctx, Xn, off, reps, (1.0, 0.1, 1.0))
+        out["not_spd"] = None
+    except N.NugprError as e:
+        out["not_spd"] = e.name
+    Xc, yc, offc, repsc, thc = dataset("c3shape")
+    bg = P.build_blocks(ctx, Xc, offc, repsc, thc)
+    out["f32"] = P.mll(ctx, bg, yc, (thc[0], thc[1] * 1.001, thc[2]), probe_seed=5, block_storage="f32")
+    L0, g, ev = P.numgrad(ctx, bg, yc, thc, probe_seed=5, mode="forward_halving")
+    out["halving"] = dict(L0=L0, g=g.tolist(), n=len(ev))
+    bg.close()
+    return out
+
+
 def run_all(P, ctx, case):
+    if case == "variants":
+        return variants(P, ctx)
     X, y, off, reps, th0 = dataset(case)
     bg = P.build_blocks(ctx, X, off, reps, th0)
     out = {}
@@ -89,9 +123,9 @@ def _worker(rank, world, port, backend, case, q):
     try:
         import paper_2510_12128_b200 as P
         ctx = P.Context(0, group=True, shard_clusters=True)
-        X, y, off, reps, th0 = dataset(case)
         out = run_all(P, ctx, case)
-        out["range"] = P.shard_range(off, rank, world)
+        if case != "variants":
+            out["range"] = P.shard_range(dataset(case)[2], rank, world)
         out["exchanges"] = ctx.exchanges
         q.put((rank, out, None))
     except Exception as e:  # noqa: BLE001
@@ -199,3 +233,21 @@ def test_cluster_shard_C5_full_size_world4(P):
         for k in ("pade", "noise", "lam"):
             same_rec(out[k], ref[k])
         np.testing.assert_allclose(out["scalars"], scal, rtol=TIGHT)
+
+
+def test_cluster_shard_variants_world2(P):
+    """Under PAR-2 (world 2): the jitter ladder's outcome is shared (rank 1 owns the singular
+    cluster, both report the same largest jitter), a block that cannot be factorised fails on
+    EVERY rank with NOT_SPD (no rank is left waiting in an exchange), FP32 block storage and the
+    FORWARD_HALVING gradient equal the replicated path."""
+    outs = spawn(2, "gloo", "variants")
+    ref = variants(P, P.Context(0))
+    assert ref["max_jitter"] > 0 and ref["not_spd"] == "NOT_SPD"
+    for out in outs:
+        assert out["max_jitter"] == ref["max_jitter"]
+        assert out["not_spd"] == "NOT_SPD"
+        same_rec(out["jitter_mll"], ref["jitter_mll"], tol=1e-10)
+        same_rec(out["f32"], ref["f32"])
+        assert out["halving"]["n"] == ref["halving"]["n"]
+        assert rel(out["halving"]["L0"], ref["halving"]["L0"]) <= TIGHT
+        np.testing.assert_allclose(out["halving"]["g"], ref["halving"]["g"], rtol=1e-9, atol=1e-12)
