@@ -649,32 +649,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
     // ============================ TMA producer ============================
     if (lane == 0 && useB) {
       uint32_t pseq = 0;
+      // cluster descriptors are loaded one cluster ahead, and the L2 prefetches are issued after the
+      // cluster's first chunk, so no chain of dependent descriptor loads sits between the last chunk
+      // of one cluster and the first chunk of the next (it drained the ring at every transition)
+      int i_nx = 0, ld_nx = 0;
+      int64_t bo_nx = 0, p0_nx = 0;
+      if (static_cast<int>(blockIdx.x) < n_tiles) {
+        i_nx = a.L.tiles[blockIdx.x].blk;
+        ld_nx = a.L.ld[i_nx];
+        bo_nx = a.L.boff[i_nx];
+        p0_nx = a.L.poff[i_nx];
+      }
       for (int t = blockIdx.x; t < n_tiles; t += G) {
-        const int i = a.L.tiles[t].blk;
-        const int ld = a.L.ld[i];
-        const int KC = max(4, (EPS * slot / ld) & ~3);
-        const TB* Bi = B + a.L.boff[i];
-        if (!(a.dbg & 32)) {
-          // warm L2 with this cluster's epilogue inputs and the next cluster's D inputs, so the
-          // consumers' plain loads there do not queue behind the B stream in DRAM
-          const int64_t p0 = a.L.poff[i];
-          const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
-          tma_prefetch_l2(a.u + p0, cb8);
-          for (int c = 0; c < ncol; ++c) {
-            if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cb8);
-            if (a.epi != EPI_S && Y2 != P2 && a.use_par_p2 != 2) tma_prefetch_l2(Y2 + c * n_pad + p0, cb8);
-          }
-          const int tn = t + G;
-          if (tn < n_tiles) {
-            const int in = a.L.tiles[tn].blk;
-            const int64_t pn = a.L.poff[in];
-            const uint32_t cbn = static_cast<uint32_t>(a.L.ld[in]) * 8u;
-            for (int c = 0; c < ncol; ++c) {
-              tma_prefetch_l2(a.D + c * n_pad + pn, cbn);
-              if (a.fuse_p) tma_prefetch_l2(Pold + c * n_pad + pn, cbn);
-            }
-          }
+        const int i = i_nx, ld = ld_nx;
+        const int64_t p0 = p0_nx;
+        const TB* Bi = B + bo_nx;
+        const int tn = t + G;
+        if (tn < n_tiles) {
+          i_nx = a.L.tiles[tn].blk;
+          ld_nx = a.L.ld[i_nx];
+          bo_nx = a.L.boff[i_nx];
+          p0_nx = a.L.poff[i_nx];
         }
+        const int KC = max(4, (EPS * slot / ld) & ~3);
         for (int ck0 = 0; ck0 < ld; ck0 += KC, ++pseq) {
           const int s_ = static_cast<int>(pseq % nstage);
           const uint32_t use = pseq / nstage;
@@ -687,11 +684,27 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
           mbar_arrive_expect_tx(&full[s_], bytes + dbytes);
           tma_load_1d(ring + s_ * slot, Bi + static_cast<int64_t>(ck0) * ld, bytes, &full[s_]);
           if (prog) {
-            const int64_t p0 = a.L.poff[i];
             double* ds = Dst + s_ * 18 * pd;
             for (int c = 0; c < 9; ++c) {
               tma_load_1d(ds + c * pd, a.D + c * n_pad + p0 + ck0, dseg, &full[s_]);
               if (a.fuse_p) tma_load_1d(ds + (9 + c) * pd, Pold + c * n_pad + p0 + ck0, dseg, &full[s_]);
+            }
+          }
+          if (ck0 == 0 && !(a.dbg & 32)) {
+            // warm L2 with this cluster's epilogue inputs and the next cluster's D inputs, so the
+            // consumers' plain loads there do not queue behind the B stream in DRAM
+            const uint32_t cb8 = static_cast<uint32_t>(ld) * 8u;
+            tma_prefetch_l2(a.u + p0, cb8);
+            for (int c = 0; c < ncol; ++c) {
+              if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cb8);
+              if (a.epi != EPI_S && Y2 != P2 && a.use_par_p2 != 2) tma_prefetch_l2(Y2 + c * n_pad + p0, cb8);
+            }
+            if (tn < n_tiles) {
+              const uint32_t cbn = static_cast<uint32_t>(ld_nx) * 8u;
+              for (int c = 0; c < ncol; ++c) {
+                tma_prefetch_l2(a.D + c * n_pad + p0_nx, cbn);
+                if (a.fuse_p) tma_prefetch_l2(Pold + c * n_pad + p0_nx, cbn);
+              }
             }
           }
         }
@@ -713,15 +726,29 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
     }
   };
   stamp();
+  // cluster descriptors one cluster ahead (their dependent loads overlap the previous cluster)
+  int ci_nx = 0, cld_nx = 0;
+  int64_t cp0_nx = 0;
+  if (static_cast<int>(blockIdx.x) < n_tiles) {
+    ci_nx = a.L.tiles[blockIdx.x].blk;
+    cld_nx = a.L.ld[ci_nx];
+    cp0_nx = a.L.poff[ci_nx];
+  }
   for (int t = blockIdx.x; t < n_tiles; t += G) {
-    const TileDesc td = a.L.tiles[t];
-    const int i = td.blk, ld = a.L.ld[i];
-    const int64_t p0 = a.L.poff[i];
+    const int i = ci_nx, ld = cld_nx;
+    const int64_t p0 = cp0_nx;
+    if (t + G < n_tiles) {
+      ci_nx = a.L.tiles[t + G].blk;
+      cld_nx = a.L.ld[ci_nx];
+      cp0_nx = a.L.poff[ci_nx];
+    }
     const int mtt = ld >> 3;                               // m-tiles of the cluster
     // 1. D_i -> shared (fused: D = R + beta o P_old for active columns, P_new written back);
     //    loads batched 4 deep per thread so one cluster costs ~one memory round trip
     if (prog) {
       // (D_i arrives chunk by chunk with the block stream)
+    } else if (a.dbg & 64) {
+      // timing experiment only: no D_i load (results invalid)
     } else if (a.dbg & 4) {
       for (int idx = tid; idx < ld * 9; idx += NW * 32) {
         const int c = idx / ld, k = idx - c * ld;

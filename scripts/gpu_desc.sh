@@ -1,0 +1,10 @@
+#!/bin/bash
+# descriptor-ahead producer/consumer: micro + bench + parity subset
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+for dbg in 0 67; do NUGPR_APPLY_DBG=$dbg timeout 120 python scripts/apply_micro.py C3 2>&1 | grep -v Warn; done
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_desc.json 2> gpurun_out/bench_desc.err
+python -c "
+import json; d = json.load(open('gpurun_out/bench_desc.json')); r = d['roofline']
+print('value', round(d['value'], 1), 'ms/step', round(d['ms_per_step'], 3), 'e2e', round(d['e2e']['value'], 1), 'apply us', round(r['avg_launch_us'], 2), 'frac', round(r['frac'], 3), 'phase', d['config']['phase_ms'])"
+timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "C3 or C2 or all_modes or f32 or graph or slots" > gpurun_out/pyt_desc.log 2>&1; echo "rc=$?" >> gpurun_out/pyt_desc.log; tail -3 gpurun_out/pyt_desc.log
