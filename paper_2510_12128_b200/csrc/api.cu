@@ -1195,6 +1195,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     a1.lds = pl.lds;
     a1.nw = pl.nw;
     a1.dstride = pl.dstride;
+    a1.dbuf = pl.dbuf;
     if (bl->f32) {
       if (pl.mma != 1) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs the m = 8 DMMA apply");
       a1.f32 = 1;

@@ -130,12 +130,14 @@ struct ApplyArgs {
   int f32;                 // 1: the DMMA apply streams the FP32-stored block (P->B32)
   int nw;                  // DMMA apply: consumer warps per CTA (7: 2 CTAs/SM; 3: 4 CTAs/SM)
   int dstride;             // DMMA apply: > 0 => D_i arrives per chunk with the TMA stream (stage row stride)
+  int dbuf;                // DMMA apply: second D_i buffer; unfused applies prefetch the next cluster's D_i
 };
 
 struct ApplyPlan {
   int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0, lds = 0;
   int nw = 7;
   int dstride = 0;
+  int dbuf = 0;
   size_t smem_b = 0, smem_nob = 0;
   bool ok = false;
 };

@@ -632,6 +632,13 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
   double* Dst = ring + (useB ? nstage * slot : 0);           // prog: nstage * 18 * pd ([c][pd], R then P_old)
   double* Dp = Dst + (prog ? nstage * 18 * pd : 0);          // ld_max * LDP
   double* ys = Dp + a.ld_max * LDP;                          // ld_max
+  // dbuf: a second D_i buffer.  An apply whose D is a plain vector (not the fused R + beta P_old)
+  // copies the NEXT cluster's D_i into it with cp.async while this cluster streams, so only a
+  // CTA's first cluster waits for its D_i
+  double* Dp1 = ys + a.ld_max;                               // dbuf: ld_max * LDP
+  double* ys1 = Dp1 + a.ld_max * LDP;                        // dbuf: ld_max
+  const bool dpre = a.dbuf && !a.fuse_p && !prog && !(a.dbg & 64);
+  bool have_next = false;                                    // D_i of this cluster already copied
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
   const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
@@ -747,6 +754,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
     //    loads batched 4 deep per thread so one cluster costs ~one memory round trip
     if (prog) {
       // (D_i arrives chunk by chunk with the block stream)
+    } else if (have_next) {
+      cp_async_wait_all();                                   // (made visible by the barrier below)
     } else if (a.dbg & 64) {
       // timing experiment only: no D_i load (results invalid)
     } else if (a.dbg & 4) {
@@ -794,6 +803,19 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
       }
     }
     bar_consumers<NW>();
+    have_next = false;
+    if (dpre && t + G < n_tiles) {
+      // the next cluster's D_i -> the other buffer, asynchronously (waited for at its start)
+      const int ldn = cld_nx;
+      const int64_t pn = cp0_nx;
+      for (int idx = tid; idx < ldn * 9; idx += NW * 32) {
+        const int c = idx / ldn, k = idx - c * ldn;
+        const double* src = a.D + c * n_pad + pn + k;
+        cp_async8((c == 0) ? ys1 + k : Dp1 + k * LDP + (c - 1), src);
+      }
+      cp_async_commit();
+      have_next = true;
+    }
     stamp();
     // 2. block term: DMMA over the ring chunks
     double acc0[MTMAX], acc1[MTMAX], accy[MTMAX];
@@ -944,6 +966,10 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
       else a.dots[t * MAXC + tid] = s;
     }
     bar_consumers<NW>();                                   // sred / Dp / ys reuse
+    if (dpre) {                                            // the prefetched buffer becomes current
+      double* tp = Dp; Dp = Dp1; Dp1 = tp;
+      tp = ys; ys = ys1; ys1 = tp;
+    }
     stamp();
   }
   if ((a.dbg & 16) && tid == 0) {
@@ -2198,6 +2224,16 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
     p.smem_nob = fixed * sizeof(double);
     p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * (p.slot_doubles + 18 * p.dstride)) *
                sizeof(double);
+    if (mma && env_int("NUGPR_APPLY_DBUF", 1) != 0) {
+      // second D_i buffer (next-cluster prefetch) if the ring keeps the same number of stages
+      const long avail2 = avail - static_cast<long>(fixed);
+      const int ns2 = static_cast<int>(std::min<long>(MAX_NSTAGE, avail2 / (p.slot_doubles + 18 * p.dstride)));
+      if (ns2 >= 2 && ns2 == p.nstage) {
+        p.dbuf = 1;
+        p.smem_nob = 2 * fixed * sizeof(double);
+        p.smem_b = (2 * fixed + static_cast<size_t>(ns2) * (p.slot_doubles + 18 * p.dstride)) * sizeof(double);
+      }
+    }
     p.ok = p.nstage >= 2;
     if (p.ok) return p;
   }

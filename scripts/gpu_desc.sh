@@ -7,4 +7,4 @@ timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out
 python -c "
 import json; d = json.load(open('gpurun_out/bench_desc.json')); r = d['roofline']
 print('value', round(d['value'], 1), 'ms/step', round(d['ms_per_step'], 3), 'e2e', round(d['e2e']['value'], 1), 'apply us', round(r['avg_launch_us'], 2), 'frac', round(r['frac'], 3), 'phase', d['config']['phase_ms'])"
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "C3 or C2 or all_modes or f32 or graph or slots" > gpurun_out/pyt_desc.log 2>&1; echo "rc=$?" >> gpurun_out/pyt_desc.log; tail -3 gpurun_out/pyt_desc.log
+timeout 1200 python -m pytest tests/test_gpu_parity.py tests/test_gpu_big.py tests/test_gpu_shard.py -q -x -k "C3 or C2 or all_modes or f32 or graph or slots or uneven or mbcg or nccl" > gpurun_out/pyt_desc.log 2>&1; echo "rc=$?" >> gpurun_out/pyt_desc.log; tail -3 gpurun_out/pyt_desc.log
