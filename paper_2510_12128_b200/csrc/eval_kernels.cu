@@ -637,7 +637,9 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
   // CTA's first cluster waits for its D_i
   double* Dp1 = ys + a.ld_max;                               // dbuf: ld_max * LDP
   double* ys1 = Dp1 + a.ld_max * LDP;                        // dbuf: ld_max
-  const bool dpre = a.dbuf && !a.fuse_p && !prog && !(a.dbg & 64);
+  double* Pst = ys1 + a.ld_max;                              // dbuf == 2: next cluster's P_old [9][ld]
+  // (dbuf == 2: the fused apply also prefetches R and P_old and forms R + beta o P_old at the start)
+  const bool dpre = a.dbuf && (!a.fuse_p || a.dbuf == 2) && !prog && !(a.dbg & 64);
   bool have_next = false;                                    // D_i of this cluster already copied
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
@@ -756,6 +758,17 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
       // (D_i arrives chunk by chunk with the block stream)
     } else if (have_next) {
       cp_async_wait_all();                                   // (made visible by the barrier below)
+      if (a.fuse_p) {
+        bar_consumers<NW>();
+        for (int idx = tid; idx < ld * 9; idx += NW * 32) {
+          const int c = idx / ld, k = idx - c * ld;
+          double* dst = (c == 0) ? ys + k : Dp + k * LDP + (c - 1);
+          const double po = Pst[c * ld + k];
+          const double x = (cb[NCPE + c] != 0.0) ? *dst + cb[c] * po : po;
+          Pnew[c * n_pad + p0 + k] = x;
+          *dst = x;
+        }
+      }
     } else if (a.dbg & 64) {
       // timing experiment only: no D_i load (results invalid)
     } else if (a.dbg & 4) {
@@ -812,6 +825,7 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
         const int c = idx / ldn, k = idx - c * ldn;
         const double* src = a.D + c * n_pad + pn + k;
         cp_async8((c == 0) ? ys1 + k : Dp1 + k * LDP + (c - 1), src);
+        if (a.fuse_p) cp_async8(Pst + c * ldn + k, Pold + c * n_pad + pn + k);
       }
       cp_async_commit();
       have_next = true;
@@ -2224,7 +2238,8 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
     p.smem_nob = fixed * sizeof(double);
     p.smem_b = (fixed + static_cast<size_t>(std::max(p.nstage, 0)) * (p.slot_doubles + 18 * p.dstride)) *
                sizeof(double);
-    if (mma && env_int("NUGPR_APPLY_DBUF", 1) != 0) {
+    const int dbuf_mode = env_int("NUGPR_APPLY_DBUF", 1);   // 2: measured slower at C3 (smaller ring slot)
+    if (mma && dbuf_mode >= 1) {
       // second D_i buffer (next-cluster prefetch) if the ring keeps the same number of stages
       const long avail2 = avail - static_cast<long>(fixed);
       const int ns2 = static_cast<int>(std::min<long>(MAX_NSTAGE, avail2 / (p.slot_doubles + 18 * p.dstride)));
@@ -2232,6 +2247,17 @@ ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int
         p.dbuf = 1;
         p.smem_nob = 2 * fixed * sizeof(double);
         p.smem_b = (2 * fixed + static_cast<size_t>(ns2) * (p.slot_doubles + 18 * p.dstride)) * sizeof(double);
+      }
+      // + a P_old staging area so the fused apply prefetches too, trading at most 1/4 of the ring slot
+      const long fixed3 = 2 * static_cast<long>(fixed) + 9L * ld_max;
+      const long avail3 = static_cast<long>(budget / sizeof(double)) - fixed3;
+      const int slot3 = std::min<int>(p.slot_doubles, static_cast<int>(avail3 / 2));
+      if (dbuf_mode >= 2 && p.dbuf && p.dstride == 0 && slot3 >= 4 * ld_max && 4 * slot3 >= 3 * p.slot_doubles) {
+        p.dbuf = 2;
+        p.slot_doubles = slot3;
+        p.nstage = static_cast<int>(std::min<long>(MAX_NSTAGE, avail3 / slot3));
+        p.smem_nob = fixed3 * sizeof(double);
+        p.smem_b = (fixed3 + static_cast<size_t>(p.nstage) * p.slot_doubles) * sizeof(double);
       }
     }
     p.ok = p.nstage >= 2;
