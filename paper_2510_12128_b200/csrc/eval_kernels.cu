@@ -932,7 +932,8 @@ __global__ void __launch_bounds__((NW + 1) * 32, (NW >= 7) ? 2 : 4) apply_mma_ke
             const int64_t gi = c * n_pad + p0 + r;
             const bool le = on && (e < 2 || qc == 0);
             p2v[jj][e] = (le && P2) ? P2[gi] : 0.0;
-            y2v[jj][e] = (le && a.epi != EPI_S && a.use_par_p2 != 2) ? Y2[gi] : 0.0;
+            // (the Q(A) apply's dot partner is its combine term P_new: one load serves both)
+            y2v[jj][e] = (le && a.epi != EPI_S && a.use_par_p2 != 2) ? ((Y2 == P2) ? p2v[jj][e] : Y2[gi]) : 0.0;
           }
         }
 #pragma unroll
@@ -1820,7 +1821,7 @@ __global__ void __launch_bounds__(NT) pnew_kernel(const CGState* st, const doubl
 // Low-rank coefficients T = M' S(D) (Eq. 19-21: block i of W M' W^T D is u_i T_i), one warp per
 // row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new) = S(R) +
 // beta o S(P_old) for the active columns (S is linear), and CTA 0 also stores S(P_new).
-constexpr int TROWS = 8;   // rows of T per CTA (one per warp)
+constexpr int TROWS = 8;   // rows of T per CTA (one per warp; 16 = two per warp measured slower at C3)
 
 template <int NCP>
 __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
@@ -1880,29 +1881,32 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
     }
   }
   __syncthreads();
-  const int il = blockIdx.x * TROWS + wid;          // row of T (local to this rank's clusters)
-  if (il >= a.nrows) return;
-  const int i = a.row0 + il;                         // row of M'
-  const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
-  double t[NCP];
+  // each warp forms TROWS / 8 rows of T (one S staging per CTA serves all of them)
+  for (int q = 0; q < TROWS / 8; ++q) {
+    const int il = blockIdx.x * TROWS + q * 8 + wid;   // row of T (local to this rank's clusters)
+    if (il >= a.nrows) return;
+    const int i = a.row0 + il;                         // row of M'
+    const double* Mrow = (a.prm ? a.prm->Mp : a.Mp) + static_cast<int64_t>(i) * n_c;
+    double t[NCP];
 #pragma unroll
-  for (int c = 0; c < NCP; ++c) t[c] = 0.0;
+    for (int c = 0; c < NCP; ++c) t[c] = 0.0;
 #pragma unroll 4
-  for (int j = lane; j < n_c; j += 32) {
-    const double m = Mrow[j];
-    const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
+    for (int j = lane; j < n_c; j += 32) {
+      const double m = Mrow[j];
+      const double2* sj = reinterpret_cast<const double2*>(Ss + j * NCP);
 #pragma unroll
-    for (int c2 = 0; c2 < NCP / 2; ++c2) {
-      const double2 v = sj[c2];
-      t[2 * c2] = fma(m, v.x, t[2 * c2]);
-      t[2 * c2 + 1] = fma(m, v.y, t[2 * c2 + 1]);
+      for (int c2 = 0; c2 < NCP / 2; ++c2) {
+        const double2 v = sj[c2];
+        t[2 * c2] = fma(m, v.x, t[2 * c2]);
+        t[2 * c2 + 1] = fma(m, v.y, t[2 * c2 + 1]);
+      }
     }
-  }
 #pragma unroll
-  for (int c = 0; c < NCP; ++c) t[c] = warp_sum(t[c]);
-  if (lane == 0) {
+    for (int c = 0; c < NCP; ++c) t[c] = warp_sum(t[c]);
+    if (lane == 0) {
 #pragma unroll
-    for (int c = 0; c < NCP; ++c) a.T[il * MAXC + c] = t[c];
+      for (int c = 0; c < NCP; ++c) a.T[il * MAXC + c] = t[c];
+    }
   }
 }
 
