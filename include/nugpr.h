@@ -158,7 +158,10 @@ nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void
  * term, p^T q, and r^T r with S(r)); everything else (K_rep, lambda_0, M', the 3-scalar CG state)
  * is replicated.  Small-block layouts only (clusters <= 512 points); mll_exact / predict /
  * the mBCG log-det mode return NUGPR_ERR_UNSUPPORTED on sharded blocks.  world = 1 is allowed
- * (exercises the exchange path on one GPU). */
+ * (exercises the exchange path on one GPU).  Errors: every decision that ends a call early is
+ * taken on replicated data (the CG state, lambda_0, the exchanged jitter-ladder outcome), so all
+ * ranks return the same status together; only a failing callback (NUGPR_ERR_COMM) can leave the
+ * other ranks inside an exchange — treat it as fatal for the process group. */
 nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, void* user);
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
 
