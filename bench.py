@@ -399,7 +399,7 @@ def run_ours(args):
         "clocks": clk,
         "gpu_launches": int(launches),
         "roofline": {
-            "kernel": "apply_kernel (fused multi-RHS block matvec + low-rank correction, mode with B)",
+            "kernel": "apply_mma_kernel (fused multi-RHS block matvec on the FP64 DMMA pipe + low-rank correction, modes with a block term)",
             "bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
             "frac": (achieved / peak) if achieved else None, "traffic": traffic,
             "launches": int(a_n), "avg_launch_us": 1e3 * a_ms / a_n if a_n else None,
