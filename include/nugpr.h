@@ -56,8 +56,10 @@ typedef enum {
   NUGPR_ERR_WORKSPACE = 6,        /* workspace too small */
   NUGPR_ERR_CUDA = 7,
   NUGPR_ERR_COMM = 8,             /* the allgather callback failed */
-  NUGPR_ERR_INTERNAL = 9,
-  NUGPR_ERR_UNSUPPORTED = 10
+  NUGPR_ERR_INTERNAL = 9,         /* e.g. the lambda_0 Lanczos did not converge within its iteration cap */
+  NUGPR_ERR_UNSUPPORTED = 10,
+  NUGPR_ERR_BREAKDOWN = 11        /* a CG quantity went non-finite or p^T q <= 0 (non-finite inputs, or the
+                                     operator is not SPD at this theta); the record holds the state reached */
 } nugpr_status;
 
 typedef enum {
@@ -120,8 +122,14 @@ typedef struct {
   int32_t iters_y;
   int32_t iters_q_max;
   int32_t iters_q[16];
-  int32_t converged;   /* 1 if every column met cg_tol (or replay ran) */
+  int32_t converged;   /* 1 if every column met cg_tol (or replay ran) and no breakdown occurred */
   int32_t mode;        /* nugpr_mode */
+  int32_t breakdown;   /* 1 if a column hit a non-finite / non-positive CG quantity (status NUGPR_ERR_BREAKDOWN) */
+  int32_t lanczos_iters;     /* Lanczos iterations of the lambda_0 this evaluation used (build's or its own) */
+  int32_t lanczos_converged; /* 1 if that Lanczos met its Ritz-residual bound (else NUGPR_ERR_INTERNAL) */
+  int32_t lambda0_degenerate;/* 1 if lambda_0 <= 1e-11 ||K_rep||_inf: not certifiably > 0 (DEGENERATE_REPS) */
+  double probe_t[16];  /* Pade trace term t_j = z_j^T P(A) Q(A)^{-1} z_j of probe j (Eq. 10; j < m) */
+  double probe_s[16];  /* SLQ term s_j ~ z_j^T log(A) z_j of probe j (from the CG coefficients; j < m) */
 } nugpr_mll_out;
 
 typedef struct nugpr_ctx nugpr_ctx;
@@ -164,6 +172,17 @@ nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void
  * other ranks inside an exchange — treat it as fatal for the process group. */
 nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, void* user);
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
+
+/* Execution options of a context (defaults in brackets).
+ *  NUGPR_OPT_GRAPHS [1]: each evaluation's CG loop runs as ONE CUDA graph whose conditional WHILE node
+ *    is driven by the device (no host round trip per iteration); 0: the same kernels launched directly
+ *    with a host poll of the activity flag every 4 iterations (profiling with ncu, which cannot see
+ *    kernels inside conditional graphs).  Both give bit-identical results.
+ *  NUGPR_OPT_BATCH [0]: NEXT-3 cross-perturbation batching — nugpr_numgrad runs its noise- and
+ *    scale-step evaluations (all four apply the same H, Eq. 24-25) in lockstep so every block apply
+ *    streams H once for all of them.  Same records as unbatched, to FP64 rounding. */
+typedef enum { NUGPR_OPT_GRAPHS = 0, NUGPR_OPT_BATCH = 1 } nugpr_option;
+nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value);
 
 /* Kernel-class profiler (bench.py's live roofline): when enabled, CUDA events are recorded on
  * the context stream around every launch of a class; accumulators reset on (re-)enable.
@@ -286,11 +305,15 @@ nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* blocks, const double* y
 /* Host-only helpers (no device work; usable without a GPU). */
 /* PAR-1 exchange of nugpr_numgrad CENTRAL: the 7 evaluations theta, theta +- h_i e_i
  * (h_i = step_i theta_i) are owned per nugpr_shard_plan(world, {1,3,3,2,2,2,2}); this rank passes
- * the losses of the evaluations it owns in L_mine[k] (others ignored); one allgather through the
- * context callback; every rank returns the same L0 = L(theta) and g_i = (L+ - L-)/(2 h_i)
- * (Eq. 11 as a central difference, reading X2).  nugpr_numgrad uses the same exchange. */
+ * the losses of the evaluations it owns in L_mine[k] (others ignored) and their statuses in
+ * status_mine[k] ([host] or NULL = all OK); one allgather through the context callback; every rank
+ * returns the same L0 = L(theta) and g_i = (L+ - L-)/(2 h_i) (Eq. 11 as a central difference,
+ * reading X2) and the same status: the first failed evaluation's (hard failures before
+ * NUGPR_ERR_CG_NOT_CONVERGED).  nugpr_numgrad uses the same exchange and ALWAYS reaches it, failed
+ * evaluations included, so one rank's failure never leaves the others waiting in the allgather. */
 nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta, const double step[3],
-                                    const double L_mine[7], double* L0, double grad[3]);
+                                    const double L_mine[7], const int32_t* status_mine, double* L0,
+                                    double grad[3]);
 /* One Adam step on state {theta[3], m[3], v[3], t}. */
 nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr);
 /* Longest-processing-time assignment of n tasks with costs to `world` ranks: owner[n]. */

@@ -24,12 +24,35 @@ Test infrastructure only (see oracle/__init__.py).
 """
 from __future__ import annotations
 
+import os
+from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass
 
 import numpy as np
 from scipy.linalg import solve_triangular
+from threadpoolctl import threadpool_limits
 
 from .kernels import kernel_matrix
+
+# Per-cluster loops run over a thread pool (SURVEY §8(d) "parallelising O-ALG's per-cluster loop
+# over a thread pool is allowed, and the thread count is stated").  Each cluster's step is the same
+# independent NumPy/SciPy call as in a plain loop, with BLAS held to ONE thread inside the pool, so
+# the result of every cluster — and therefore of the oracle — does not depend on ORACLE_THREADS.
+# (The per-apply triangular solves skip SciPy's input scan, check_finite=False: R is finite by
+# construction — a Cholesky factor that passed — and the scan held the GIL for most of an apply.)
+ORACLE_THREADS = max(1, int(os.environ.get("ORACLE_THREADS", os.cpu_count() or 1)))
+_POOL = None
+
+
+def cluster_map(fn, n):
+    """[fn(i) for i in range(n)], evaluated cluster-parallel (results in cluster order)."""
+    global _POOL
+    with threadpool_limits(limits=1):
+        if n < 32 or ORACLE_THREADS == 1:
+            return [fn(i) for i in range(n)]
+        if _POOL is None:
+            _POOL = ThreadPoolExecutor(ORACLE_THREADS)
+        return list(_POOL.map(fn, range(n)))
 
 
 class NotSPD(Exception):
@@ -128,16 +151,19 @@ def build_blocks(X, offsets, reps, theta0, kind="rbf") -> Blocks:
     n_c = offsets.shape[0] - 1
     if offsets[0] != 0 or offsets[-1] != X.shape[0] or np.any(np.diff(offsets) <= 0):
         raise ValueError("offsets must be strictly increasing from 0 to n")
-    R, jit, u = [], np.zeros(n_c), []
-    logdet_R = 0.0
-    for i in range(n_c):
+    def one(i):
         Xi = X[offsets[i]:offsets[i + 1]]
         Ki = kernel_matrix(kind, Xi, Xi, lam, alpha) + s2 * np.eye(Xi.shape[0])
         Ri, eps = chol_upper_with_jitter(Ki, i)
+        return Ri, eps, solve_triangular(Ri, np.ones(Xi.shape[0]), trans="T")   # Eq. (21)
+
+    R, jit, u = [], np.zeros(n_c), []
+    logdet_R = 0.0
+    for i, (Ri, eps, ui) in enumerate(cluster_map(one, n_c)):
         R.append(Ri)
         jit[i] = eps
         logdet_R += 2.0 * float(np.sum(np.log(np.diag(Ri))))          # Eq. (16)
-        u.append(solve_triangular(Ri, np.ones(Xi.shape[0]), trans="T"))  # Eq. (21)
+        u.append(ui)
     Krep, lam0, M = krep_and_M(kind, reps, theta0)
     return Blocks(X=X, offsets=offsets, reps=np.asarray(reps, dtype=np.float64), kind=kind,
                   theta0=(lam, s2, alpha), R=R, jitter=jit, logdet_R=logdet_R, u=u,
@@ -148,9 +174,9 @@ def solve_Rt(blocks: Blocks, y):
     """c = R^{-T} y, block by block (transformed right-hand side)."""
     y = np.asarray(y, dtype=np.float64)
     out = np.empty_like(y)
+    parts = cluster_map(lambda i: solve_triangular(blocks.R[i], y[blocks.block(i)], trans="T"), blocks.n_c)
     for i in range(blocks.n_c):
-        sl = blocks.block(i)
-        out[sl] = solve_triangular(blocks.R[i], y[sl], trans="T")
+        out[blocks.block(i)] = parts[i]
     return out
 
 
@@ -183,12 +209,12 @@ class Operator:
             self.Mp, self.lam0 = (1.0 + r) * blocks.M, (1.0 + r) * blocks.lam0
         else:
             _, self.lam0, self.Mp = krep_and_M(blocks.kind, blocks.reps, self.theta)
-            self.Kd = [blocks.K_block(i, self.theta) for i in range(blocks.n_c)]
+            self.Kd = cluster_map(lambda i: blocks.K_block(i, self.theta), blocks.n_c)
 
     def _H(self, i, Di):
         """H_i D_i = R_i^{-T} (R_i^{-1} D_i)  (NOT K_i^{-1})."""
         Ri = self.b.R[i]
-        return solve_triangular(Ri, solve_triangular(Ri, Di), trans="T")
+        return solve_triangular(Ri, solve_triangular(Ri, Di, check_finite=False), trans="T", check_finite=False)
 
     def F(self, i, Di):
         lam, s2, alpha = self.theta
@@ -201,7 +227,8 @@ class Operator:
             r = self.r
             return (1.0 + r) * Di - (s20 + self.b.jitter[i]) * r * self._H(i, Di)
         Ri = self.b.R[i]                                             # generic, Eq. (18)-(19)
-        return solve_triangular(Ri, self.Kd[i] @ solve_triangular(Ri, Di), trans="T")
+        return solve_triangular(Ri, self.Kd[i] @ solve_triangular(Ri, Di, check_finite=False), trans="T",
+                                check_finite=False)
 
     def apply(self, D):
         D = np.asarray(D, dtype=np.float64)
@@ -214,9 +241,9 @@ class Operator:
             S[j] = self.b.u[j] @ D[self.b.block(j)]
         T = self.Mp @ S                                              # T = M' S
         out = np.empty_like(D)
+        Fs = cluster_map(lambda i: self.F(i, D[self.b.block(i)]), nb)
         for i in range(nb):                                          # out_i = F_i + u_i T_i
-            sl = self.b.block(i)
-            out[sl] = self.F(i, D[sl]) + np.outer(self.b.u[i], T[i])
+            out[self.b.block(i)] = Fs[i] + np.outer(self.b.u[i], T[i])
         return out[:, 0] if vec else out
 
     def apply_Q(self, D):

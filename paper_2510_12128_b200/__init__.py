@@ -136,17 +136,23 @@ class Context:
     def _allreduce(self, send, recv, count, stream, user):
         """PAR-2 exchange: recv = sum over ranks of send, ordered on the context stream."""
         try:
+            import contextlib
             import torch
             import torch.distributed as dist
             s_t, r_t = self._view(send, count), self._view(recv, count)
-            if r_t.is_cuda and dist.get_backend(self.group) != "nccl":
-                # gloo (CPU tests, or several ranks sharing one GPU): through host memory
-                tmp = s_t.cpu()
-                dist.all_reduce(tmp, group=self.group)
-                r_t.copy_(tmp)
-            else:
-                r_t.copy_(s_t)
-                dist.all_reduce(r_t, group=self.group)
+            # order the copies / collective on the stream the library enqueued its partials on (the
+            # caller's current torch stream may be another one)
+            sc = (torch.cuda.stream(torch.cuda.ExternalStream(stream, device=torch.device("cuda", self.device)))
+                  if (r_t.is_cuda and stream) else contextlib.nullcontext())
+            with sc:
+                if r_t.is_cuda and dist.get_backend(self.group) != "nccl":
+                    # gloo (CPU tests, or several ranks sharing one GPU): through host memory
+                    tmp = s_t.cpu()
+                    dist.all_reduce(tmp, group=self.group)
+                    r_t.copy_(tmp)
+                else:
+                    r_t.copy_(s_t)
+                    dist.all_reduce(r_t, group=self.group)
             self.exchanges += 1
             return 0
         except Exception as exc:  # noqa: BLE001 — reported to C as a status
@@ -161,6 +167,11 @@ class Context:
             return 0
         except Exception:  # noqa: BLE001 — reported to C as a status
             return 1
+
+    def set_option(self, name: str, value):
+        """nugpr_ctx_set_option: 'graphs' (CG loop as a device-driven CUDA graph, default True) or
+        'batch' (NEXT-3 cross-perturbation batching in numgrad, default False)."""
+        N.check(N.lib().nugpr_ctx_set_option(self.handle, N.OPTIONS[name], int(value)))
 
     def set_profiling(self, enable: bool = True):
         N.check(N.lib().nugpr_ctx_set_profiling(self.handle, int(bool(enable))))
@@ -228,15 +239,18 @@ def allgather_bytes(data: bytes, world: int, group=None, device: int = -1) -> by
     return out.cpu().numpy().tobytes()
 
 
-def numgrad_exchange(ctx: Context, theta, step, L_mine):
-    """Host side of the perturbation-sharded CENTRAL gradient (nugpr_numgrad_exchange)."""
+def numgrad_exchange(ctx: Context, theta, step, L_mine, status_mine=None):
+    """Host side of the perturbation-sharded CENTRAL gradient (nugpr_numgrad_exchange).  Raises
+    NugprError with the exchanged worst status when any evaluation (of any rank) failed."""
     st = np.ascontiguousarray(step, dtype=np.float64)
     Lm = np.ascontiguousarray(L_mine, dtype=np.float64)
+    sm = None if status_mine is None else np.ascontiguousarray(status_mine, dtype=np.int32)
     L0 = C.c_double()
     g = np.zeros(3)
     P_ = C.POINTER(C.c_double)
     N.check(N.lib().nugpr_numgrad_exchange(ctx.handle, _theta(theta), st.ctypes.data_as(P_), Lm.ctypes.data_as(P_),
-                                           C.byref(L0), g.ctypes.data_as(P_)))
+                                           sm.ctypes.data if sm is not None else None, C.byref(L0),
+                                           g.ctypes.data_as(P_)))
     return L0.value, g
 
 
@@ -376,7 +390,10 @@ def _rec(o: N.MllOut, m: int) -> dict:
                 logdet_slq=o.logdet_slq, logdet_R=o.logdet_R, lambda0=o.lambda0,
                 resid_y=o.resid_y, resid_q_max=o.resid_q_max, iters_y=o.iters_y,
                 iters_q=[o.iters_q[j] for j in range(m)], iters_q_max=o.iters_q_max,
-                converged=bool(o.converged), mode=N.MODES.get(o.mode, o.mode))
+                converged=bool(o.converged), mode=N.MODES.get(o.mode, o.mode), breakdown=bool(o.breakdown),
+                lanczos_iters=o.lanczos_iters, lanczos_converged=bool(o.lanczos_converged),
+                lambda0_degenerate=bool(o.lambda0_degenerate),
+                probe_t=[o.probe_t[j] for j in range(m)], probe_s=[o.probe_s[j] for j in range(m)])
 
 
 def mll(ctx: Context, blocks: Blocks, y_sorted, theta, **solve) -> dict:

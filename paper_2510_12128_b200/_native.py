@@ -17,10 +17,11 @@ NUGPR_TRAIN_RECORD = 12
 
 STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "DEGENERATE_REPS",
           5: "CG_NOT_CONVERGED", 6: "WORKSPACE", 7: "CUDA", 8: "COMM", 9: "INTERNAL",
-          10: "UNSUPPORTED"}
+          10: "UNSUPPORTED", 11: "BREAKDOWN"}
 KERNELS = {"rbf": 0, "matern52": 1, "rbf_as_printed": 2}
 REP_MODES = {"given": 0, "centroid": 1, "medoid": 2}
 MODES = {0: "baseline", 1: "noise", 2: "scale", 3: "generic"}
+OPTIONS = {"graphs": 0, "batch": 1}
 PROF_CLASSES = {"apply_B": 0, "apply_lowrank": 1, "update": 2, "rhs": 3, "gemm": 4, "chol": 5,
                 "lanczos": 6, "other": 7}
 
@@ -52,7 +53,9 @@ class MllOut(C.Structure):
                 ("logdet_pade", C.c_double), ("logdet_slq", C.c_double), ("logdet_R", C.c_double),
                 ("lambda0", C.c_double), ("resid_y", C.c_double), ("resid_q_max", C.c_double),
                 ("iters_y", C.c_int32), ("iters_q_max", C.c_int32), ("iters_q", C.c_int32 * 16),
-                ("converged", C.c_int32), ("mode", C.c_int32)]
+                ("converged", C.c_int32), ("mode", C.c_int32), ("breakdown", C.c_int32),
+                ("lanczos_iters", C.c_int32), ("lanczos_converged", C.c_int32), ("lambda0_degenerate", C.c_int32),
+                ("probe_t", C.c_double * 16), ("probe_s", C.c_double * 16)]
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
@@ -83,6 +86,7 @@ def lib():
                                                  C.POINTER(C.c_size_t)]),
         "nugpr_ctx_destroy": (C.c_int, [P]),
         "nugpr_ctx_set_profiling": (C.c_int, [P, C.c_int32]),
+        "nugpr_ctx_set_option": (C.c_int, [P, C.c_int32, C.c_int32]),
         "nugpr_ctx_profile": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_int64)]),
         "nugpr_launch_count": (C.c_int64, []),
@@ -103,7 +107,7 @@ def lib():
         "nugpr_cluster": (C.c_int, [P, P, C.c_int64, C.c_int32, C.c_int32, P, C.c_uint64, C.c_int32,
                                     C.c_int32, C.c_int32, Theta, P, P, C.c_size_t, P, P, P, P, P,
                                     C.POINTER(C.c_int32)]),
-        "nugpr_numgrad_exchange": (C.c_int, [P, Theta, C.POINTER(C.c_double), C.POINTER(C.c_double),
+        "nugpr_numgrad_exchange": (C.c_int, [P, Theta, C.POINTER(C.c_double), C.POINTER(C.c_double), P,
                                              C.POINTER(C.c_double), C.POINTER(C.c_double)]),
         "nugpr_predict": (C.c_int, [P, P, P, P, C.c_int64, C.c_int32, P, P]),
         "nugpr_mll_exact": (C.c_int, [P, P, P, C.POINTER(C.c_double)]),
@@ -131,4 +135,4 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
             "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster",
             "nugpr_numgrad_exchange", "nugpr_predict", "nugpr_mll_exact", "nugpr_ctx_set_cluster_shard",
-            "nugpr_shard_range", "nugpr_workspace_size_shard"]
+            "nugpr_shard_range", "nugpr_workspace_size_shard", "nugpr_ctx_set_option"]

@@ -58,7 +58,9 @@ nugpr_status fail(nugpr_status st, const char* fmt, ...) {
 constexpr int HIST = 4096;          // max recorded CG iterations (cg_max_iter cap)
 constexpr int LD_MAX_SUPPORTED = 8192;
 constexpr int LD_SMALL_MAX = 512;     // above: big-block mode (blocked multi-launch factorisation, row-tiled apply)
-constexpr int LANCZOS_KMAX_CAP = 400;
+// Lanczos iteration cap for lambda_0: with full reorthogonalisation, k = n_c iterations reproduce the
+// whole spectrum, so the cap only binds (and the solve reports non-convergence) for n_c > 2048.
+constexpr int LANCZOS_KMAX_CAP = 2048;
 
 struct HostLayout {
   int n_c = 0, d = 0;
@@ -313,7 +315,8 @@ struct nugpr_ctx {
   cudaStream_t aux_stream[NUGPR_NUM_EVALS + 1] = {nullptr};
   cudaEvent_t ev_aux[NUGPR_NUM_EVALS + 1][2] = {{nullptr}};
   EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
-  cudaEvent_t tl_pre = nullptr;          // NUGPR_TIMELINE: recorded before rhs_init of the next eval
+  bool use_graphs = true;                // NUGPR_OPT_GRAPHS
+  bool batch = false;                    // NUGPR_OPT_BATCH (NEXT-3)
   // nugpr_train's deferred build: H_i = Linv_i Linv_i^T on its own stream, overlapping the
   // evaluations that do not read H (baseline, lengthscale steps); ev_h1 marks it done
   cudaStream_t h_stream = nullptr;
@@ -396,7 +399,6 @@ struct nugpr_blocks {
   uint64_t last_seed = 0;
   const double* last_probes = nullptr;
   bool cy_ready = false;      // B.cy holds c = R^{-T} y for the current numgrad call
-  bool no_graph = false;      // NUGPR_NO_GRAPH=1: direct launches with host polling
   const void* ws_base = nullptr;
   bool pnew = false;          // the CG iteration launches pnew_kernel (launch accounting)
   bool f32 = false;           // current evaluation streams FP32-stored blocks
@@ -454,6 +456,15 @@ nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, 
   ctx->ar = fn;
   ctx->ar_user = user;
   return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value) {
+  if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
+  switch (option) {
+    case NUGPR_OPT_GRAPHS: ctx->use_graphs = value != 0; return NUGPR_OK;
+    case NUGPR_OPT_BATCH: ctx->batch = value != 0; return NUGPR_OK;
+    default: return fail(NUGPR_ERR_INVALID_ARG, "unknown option %d", option);
+  }
 }
 
 nugpr_status nugpr_ctx_set_profiling(nugpr_ctx* ctx, int32_t enable) {
@@ -590,7 +601,8 @@ static nugpr_status enqueue_lambda0(nugpr_blocks* bl, const double* K, const dou
                                     double* lam0, double* v0, double* M, int32_t* info, cudaStream_t s) {
   const int n_c = bl->n_cg;   // K_rep is global (replicated under PAR-2)
   const int kmax = std::min(n_c, LANCZOS_KMAX_CAP);
-  launch_lanczos(K, n_c, vinit, lz, kmax, 1e-11, lam0, v0, M, info, s);
+  const cudaError_t e = launch_lanczos(K, n_c, vinit, lz, kmax, 1e-11, lam0, v0, M, info, s);
+  if (e != cudaSuccess) return fail(NUGPR_ERR_CUDA, "lambda_0 Lanczos launch: %s", cudaGetErrorString(e));
   CKL();
   return NUGPR_OK;
 }
@@ -648,39 +660,10 @@ extern "C" nugpr_status nugpr_build_blocks(nugpr_ctx* ctx, const double* X_sorte
                     max_jitter, false);
 }
 
-// NUGPR_BUILD_TRACE=1: host wall-clock of the build phases on stderr (debugging the build's overhead)
-struct BuildTrace {
-  bool on = false;
-  std::vector<std::pair<const char*, double>> pts;
-  double t0 = 0;
-  static double now() {
-    timespec ts;
-    clock_gettime(CLOCK_MONOTONIC, &ts);
-    return ts.tv_sec * 1e6 + ts.tv_nsec * 1e-3;
-  }
-  BuildTrace() {
-    const char* v = getenv("NUGPR_BUILD_TRACE");
-    on = v && v[0] == '1';
-    t0 = now();
-  }
-  void mark(const char* what, cudaStream_t s, bool sync = false) {
-    if (!on) return;
-    if (sync) cudaStreamSynchronize(s);
-    pts.emplace_back(what, now() - t0);
-  }
-  ~BuildTrace() {
-    if (!on) return;
-    fprintf(stderr, "[nugpr build]");
-    for (auto& p : pts) fprintf(stderr, " %s=%.0f", p.first, p.second);
-    fprintf(stderr, " us\n");
-  }
-};
-
 static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int64_t* offsets, int32_t n_c,
                                int32_t d, const double* reps, int32_t kernel, nugpr_theta theta0, void* workspace,
                                size_t ws_bytes, nugpr_blocks** out, int32_t* failed_block, double* max_jitter,
                                bool reuse, bool defer) {
-  BuildTrace tr;
   if (failed_block) *failed_block = -1;
   if (max_jitter) *max_jitter = 0.0;
   if (!ctx || !X_sorted || !reps || !workspace || !out) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
@@ -732,10 +715,6 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   carve_all(c, bl->L, slots, bl->B, bl->E, n_c, offsets[n_c]);
   bl->ctx = ctx;
   bl->ws_base = workspace;
-  {
-    const char* ng = getenv("NUGPR_NO_GRAPH");
-    bl->no_graph = ng && ng[0] == '1';
-  }
   bl->kind = kernel;
   bl->theta0 = theta0;
   HostLayout& L = bl->L;
@@ -786,18 +765,12 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   }
   if (bas != s) CKB(cudaEventRecord(ctx->ev_aux[NUGPR_NUM_EVALS][1], bas));
   // A1: K_i(theta0) assembled on the fly, Cholesky + inverse, jitter ladder
-  tr.mark("uploads", s, true);
-  const bool fused_chol = !L.big && chol_fused_ok(L.ld_max);
   if (L.big) {
     PROF(ctx, PC_OTHER, 0.0, s,
          launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
                          theta0.noise, theta0.outputscale, s));
     PROF(ctx, PC_CHOL, 0.0, s,
          launch_big_chol_trtri(B.Linv, Ld, nullptr, 0, L.ld_max, B.status, B.logdet_blk, B.u, B.bigscr, s));
-  } else if (fused_chol) {
-    PROF(ctx, PC_CHOL, 0.0, s,
-         launch_chol_fused(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
-                           theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s));
   } else {
     PROF(ctx, PC_OTHER, 0.0, s,
          launch_assemble(B.X, d, Ld, nullptr, 0, L.ld_max, B.jitter, B.Linv, kernel, theta0.lengthscale,
@@ -808,7 +781,6 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   std::vector<int32_t> hstat(nl);
   CKB(cudaMemcpyAsync(hstat.data(), B.status, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
-  tr.mark("chol+status", s);
   bl->h_jitter.assign(nl, 0.0);
   const double base = 1e-8 * (theta0.outputscale + theta0.noise);   // 1e-8 * mean(diag K_i)
   int fb = -1;                                                       // global index of a failed block
@@ -825,9 +797,6 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
                       kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
       launch_big_chol_trtri(B.Linv, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.status,
                             B.logdet_blk, B.u, B.bigscr, s);
-    } else if (fused_chol) {
-      launch_chol_fused(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
-                        kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, B.status, B.logdet_blk, B.u, s);
     } else {
       launch_assemble(B.X, d, Ld, B.list, static_cast<int>(bl->h_list.size()), L.ld_max, B.jitter, B.Linv,
                       kernel, theta0.lengthscale, theta0.noise, theta0.outputscale, s);
@@ -858,7 +827,6 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
     return fail(NUGPR_ERR_NOT_SPD, "cluster %d is not SPD after the jitter ladder", fb);
   }
   // H_i = Linv_i Linv_i^T ; logdet_R (K_rep, lambda_0, M were launched on the side stream)
-  tr.mark("ladder", s);
   defer = defer && !ctx->prof;
   if (defer) {
     // deferred (nugpr_train): H on its own stream; the evaluations that read it wait on ev_h1
@@ -873,7 +841,6 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   } else {
     PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
   }
-  tr.mark("H", s, true);
   if (shard) {
     // logdet_R = 2 sum_i sum_j log (R_i)_jj over ALL clusters: gather the per-cluster terms, then the
     // same fixed-order sum as one GPU
@@ -897,17 +864,23 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
     return NUGPR_OK;
   }
   double hs[2];
+  int32_t lzi[3] = {0, 0, 0};
   CKB(cudaMemcpyAsync(hs, B.scal, sizeof(double) * 2, cudaMemcpyDeviceToHost, s));
+  CKB(cudaMemcpyAsync(lzi, B.linfo, sizeof(int32_t) * 3, cudaMemcpyDeviceToHost, s));
   CKB(cudaStreamSynchronize(s));
 #undef CKB
-  tr.mark("final", s);
   prof_harvest(ctx);
   bl->logdet_R = hs[0];
   bl->lam0 = hs[1];
   if (max_jitter) *max_jitter = bl->max_jitter;
-  if (!(bl->lam0 > 0.0)) {
+  if (!lzi[1]) {
     delete bl;
-    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0 = %g <= 0 (degenerate representatives)", hs[1]);
+    return fail(NUGPR_ERR_INTERNAL, "lambda_0 Lanczos did not converge in %d iterations (n_c = %d)", lzi[0], n_c);
+  }
+  if (!(bl->lam0 > 0.0) || lzi[2]) {
+    delete bl;
+    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0 = %g is not certifiably > 0 (degenerate representatives)",
+                hs[1]);
   }
   *out = bl;
   return NUGPR_OK;
@@ -1431,6 +1404,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   P.mode = mode;
   P.lam0_src = lam0_ptr;
   P.lam0_mul = 1.0;
+  P.lz_info = (mode == NUGPR_MODE_GENERIC) ? e.linfo : B.linfo;
   if (mode_out) *mode_out = mode;
   if (mode == NUGPR_MODE_SCALE) {
     // lam0(theta') = (1+r) lam0(theta0): one scalar, computed on the host from the value the
@@ -1456,7 +1430,6 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   if (bl->shard) {
     ra.rr_part = e.xs + XO; ra.SR_part = e.xs + XG + XO; ra.SP0 = e.xs + 2 * XG + XO; ra.nofin = 1;
   }
-  if (ctx->tl_pre) CK(cudaEventRecord(ctx->tl_pre, s));
   PROF(ctx, PC_RHS, 0.0, s, launch_rhs_init(ra, L.ld_max, s));
   CKL();
   if (bl->shard) {
@@ -1468,13 +1441,13 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   }
   if (prep_only) return NUGPR_OK;
   const bool useB = P.B != nullptr;
-  if (!ctx->prof && !bl->no_graph && !bl->shard) {
+  if (!ctx->prof && ctx->use_graphs && !bl->shard) {
     cudaGraphExec_t ex = nullptr;
     RET(get_graph(ctx, bl, slot, ncol, cfg->logdet_mode, &ex));
     CK(cudaGraphLaunch(ex, s));
     return NUGPR_OK;
   }
-  // direct launches (profiling / NUGPR_NO_GRAPH): host polls the activity flag every CH iterations
+  // direct launches (profiling / NUGPR_OPT_GRAPHS = 0): host polls the activity flag every CH iterations
   IterArgs A;
   RET(make_iter_args(bl, e, ncol, A, cfg->logdet_mode == NUGPR_LOGDET_MBCG));
   double sum_b2 = 0.0;
@@ -1725,7 +1698,12 @@ static nugpr_status finish_record(nugpr_blocks* bl, const nugpr_solve_cfg* cfg, 
   if (graph) account_graph_launches(bl, o, cfg->logdet_mode);
   bl->last_m = cfg->num_probes;
   bl->last_seed = cfg->probe_seed;
-  if (!(o.lambda0 > 0.0)) return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g <= 0", o.lambda0);
+  if (!o.lanczos_converged)
+    return fail(NUGPR_ERR_INTERNAL, "lambda_0 Lanczos did not converge in %d iterations", o.lanczos_iters);
+  if (!(o.lambda0 > 0.0) || o.lambda0_degenerate)
+    return fail(NUGPR_ERR_DEGENERATE_REPS, "lambda_0(theta) = %g is not certifiably > 0", o.lambda0);
+  if (o.breakdown)
+    return fail(NUGPR_ERR_BREAKDOWN, "CG breakdown: non-finite r^T r or non-positive / non-finite p^T q");
   if (!o.converged) return fail(NUGPR_ERR_CG_NOT_CONVERGED, "CG reached cg_max_iter = %d", cfg->cg_max_iter);
   return NUGPR_OK;
 }
@@ -1741,7 +1719,7 @@ static nugpr_status run_eval(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_d
   CK(cudaStreamSynchronize(s));
   prof_harvest(ctx);
   *out = ctx->h_out[0];
-  return finish_record(bl, cfg, *out, !ctx->prof && !bl->no_graph);
+  return finish_record(bl, cfg, *out, !ctx->prof && ctx->use_graphs);
 }
 
 extern "C" nugpr_status nugpr_mll(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
@@ -1779,6 +1757,20 @@ struct EvalRecord {
   int32_t valid;
 };
 
+// Status of a set of evaluation records: the first hard failure (in evaluation order) wins over
+// CG non-convergence ("flag any instances"), which wins over OK.
+static nugpr_status worst_status(const EvalRecord* recs, int n, int* which) {
+  nugpr_status w = NUGPR_OK;
+  *which = -1;
+  for (int k = 0; k < n; ++k) {
+    const nugpr_status st = static_cast<nugpr_status>(recs[k].status);
+    if (st == NUGPR_OK) continue;
+    if (st != NUGPR_ERR_CG_NOT_CONVERGED) { *which = k; return st; }
+    if (w == NUGPR_OK) { w = st; *which = k; }
+  }
+  return w;
+}
+
 // PAR-1 exchange of the CENTRAL gradient: every rank holds the records of the
 // evaluations it owns (owner[k] == rank); one allgather of the 7-record arrays, then each record
 // is taken from its owner's copy, and every rank forms the same L0 and g_i = (L+ - L-)/(2 h_i)
@@ -1796,12 +1788,15 @@ static nugpr_status central_exchange(nugpr_ctx* ctx, const int32_t* owner, const
   } else {
     memcpy(all, mine, sizeof(all));
   }
-  *worst = NUGPR_OK;
   for (int k = 0; k < NUGPR_NUM_EVALS; ++k) {
     if (!all[k].valid) return fail(NUGPR_ERR_COMM, "evaluation %d missing after exchange", k);
-    if (all[k].status != NUGPR_OK) *worst = static_cast<nugpr_status>(all[k].status);
     if (evals) evals[k] = all[k].o;
   }
+  int which = -1;
+  *worst = worst_status(all, NUGPR_NUM_EVALS, &which);
+  if (*worst != NUGPR_OK)
+    fail(*worst, "central-difference evaluation %d (0 = theta, 1+2i / 2+2i = theta +- h_i e_i) ended with status %d "
+                 "(rank %d owned it)", which, static_cast<int>(*worst), owner[which]);
   *L0 = all[0].o.L;
   for (int i = 0; i < 3; ++i) grad[i] = (all[1 + 2 * i].o.L - all[2 + 2 * i].o.L) / (2.0 * h[i]);
   return NUGPR_OK;
@@ -1810,7 +1805,8 @@ static nugpr_status central_exchange(nugpr_ctx* ctx, const int32_t* owner, const
 // Host-only entry to the same exchange (tests of the sharded path without a GPU): this rank
 // passes L values for the evaluations nugpr_shard_plan gives it (others ignored).
 extern "C" nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta, const double step[3],
-                                               const double L_mine[7], double* L0, double grad[3]) {
+                                               const double L_mine[7], const int32_t* status_mine, double* L0,
+                                               double grad[3]) {
   if (!ctx || !step || !L_mine || !L0 || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
   const double th[3] = {theta.lengthscale, theta.noise, theta.outputscale};
   double h[3];
@@ -1821,9 +1817,14 @@ extern "C" nugpr_status nugpr_numgrad_exchange(nugpr_ctx* ctx, nugpr_theta theta
   EvalRecord mine[NUGPR_NUM_EVALS];
   memset(mine, 0, sizeof(mine));
   for (int k = 0; k < NUGPR_NUM_EVALS; ++k)
-    if (owner[k] == ctx->rank) { mine[k].o.L = L_mine[k]; mine[k].valid = 1; mine[k].status = NUGPR_OK; }
+    if (owner[k] == ctx->rank) {
+      mine[k].o.L = L_mine[k];
+      mine[k].valid = 1;
+      mine[k].status = status_mine ? status_mine[k] : NUGPR_OK;
+    }
   nugpr_status worst = NUGPR_OK;
-  return central_exchange(ctx, owner, mine, h, L0, grad, nullptr, &worst, ctx->world);
+  RET(central_exchange(ctx, owner, mine, h, L0, grad, nullptr, &worst, ctx->world));
+  return worst;
 }
 
 // Evaluate the points `ks` (indices into pts) concurrently: evaluation j runs on slot j % slots,
@@ -1833,26 +1834,26 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
                                          const nugpr_solve_cfg* cfg, EvalRecord* recs) {
   cudaStream_t s0 = ctx->stream;
   const int slots = static_cast<int>(bl->E.size());
-  const bool graph = !ctx->prof && !bl->no_graph;
+  const bool graph = !ctx->prof && ctx->use_graphs;
+  // Every evaluation gets a record and a status, whatever happens to the others: nugpr_numgrad
+  // always reaches the PAR-1 exchange afterwards, so no rank is left waiting in it (a rank that
+  // returned early would deadlock the others' allgather).
+  auto mark_rest = [&](size_t from, nugpr_status st) {
+    for (size_t q = from; q < ks.size(); ++q) { recs[ks[q]].status = st; recs[ks[q]].valid = 1; }
+  };
   if (slots <= 1 || ctx->prof || ks.size() <= 1 || bl->shard) {
     for (int k : ks) {
       nugpr_status st = run_eval(ctx, bl, y_dev, pts[k], cfg, &recs[k].o);
       recs[k].status = st;
       recs[k].valid = 1;
-      if (st != NUGPR_OK && st != NUGPR_ERR_CG_NOT_CONVERGED) return st;
     }
     return NUGPR_OK;
   }
-  RET(ensure_slot_streams(ctx, slots));
-  // NUGPR_TIMELINE=1: per-evaluation start / pre-work done / end times (debugging the overlap)
-  static const bool tl_on = [] { const char* v = getenv("NUGPR_TIMELINE"); return v && v[0] == '1'; }();
-  cudaEvent_t tl0 = nullptr, tls[16], tlp[16], tle[16];
-  const int nk = static_cast<int>(ks.size());
-  if (tl_on) {
-    cudaEventCreate(&tl0);
-    for (int j = 0; j < nk; ++j) { cudaEventCreate(&tls[j]); cudaEventCreate(&tlp[j]); cudaEventCreate(&tle[j]); }
-    cudaEventRecord(tl0, s0);
+  {
+    const nugpr_status ss_ = ensure_slot_streams(ctx, slots);
+    if (ss_ != NUGPR_OK) { mark_rest(0, ss_); return NUGPR_OK; }
   }
+  const int nk = static_cast<int>(ks.size());
   if (cfg->block_storage == NUGPR_BLOCKS_F32 && !bl->h32_ready && !bl->L.big) {
     if (bl->h_pending) CK(cudaStreamWaitEvent(s0, ctx->ev_h1, 0));
     launch_d2f(bl->B.H, bl->B.H32, bl->L.blk_total, s0);   // before the fork: every stream reads it
@@ -1864,10 +1865,7 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   // NEXT-3 batching: the noise- and scale-step evaluations (B = H for all of them) form one
   // lockstep batch whose applies read H once (m = 8 DMMA path, graphs, one slot per evaluation)
   std::vector<int> batch;
-  // opt-in (NUGPR_BATCH=1): at C3 the per-cluster phases of the apply dominate and a 4-group apply
-  // is no faster than four separate ones; it pays where streaming dominates (large clusters)
-  static const bool batch_on = [] { const char* v = getenv("NUGPR_BATCH"); return v && v[0] == '1'; }();
-  if (batch_on && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big &&
+  if (ctx->batch && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big &&
       cfg->logdet_mode != NUGPR_LOGDET_MBCG) {
     const nugpr_theta t0 = bl->theta0;
     for (int j = 0; j < nk && batch.size() < 4; ++j) {
@@ -1880,64 +1878,72 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   std::vector<char> in_batch(nk, 0);
   for (int j : batch) in_batch[j] = 1;
   int q = 0;                                         // stream index of the next job
-  for (int j = 0; j < nk; ++j) {
+  // an enqueue failure ends the launching (that job and the ones not yet launched carry its status);
+  // the jobs already in flight are still joined and read back
+  nugpr_status enq = NUGPR_OK;
+  int failed_at = nk;
+  auto note_enq = [&](nugpr_status st, int j) { if (st != NUGPR_OK && enq == NUGPR_OK) { enq = st; failed_at = j; } };
+  std::vector<char> launched(nk, 0);
+  for (int j = 0; j < nk && enq == NUGPR_OK; ++j) {
     if (in_batch[j]) continue;
     const int slot = j % slots;
     cudaStream_t ss = ctx->slot_stream[q % slots];
-    if (q < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    if (q < slots) note_enq(cudaStreamWaitEvent(ss, ctx->ev_fork, 0) == cudaSuccess ? NUGPR_OK
+                            : fail(NUGPR_ERR_CUDA, "stream fork failed"), j);
     ++q;
-    if (tl_on) { cudaEventRecord(tls[j], ss); ctx->tl_pre = tlp[j]; }
-    RET(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j]));
-    ctx->tl_pre = nullptr;
-    if (tl_on) cudaEventRecord(tle[j], ss);
-    CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
+    if (enq != NUGPR_OK) break;
+    note_enq(enqueue_eval(ctx, bl, slot, y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j]), j);
+    if (enq != NUGPR_OK) break;
+    note_enq(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss)
+                     == cudaSuccess ? NUGPR_OK : fail(NUGPR_ERR_CUDA, "record read-back failed"), j);
+    if (enq == NUGPR_OK) launched[j] = 1;
   }
-  if (!batch.empty()) {
+  if (!batch.empty() && enq == NUGPR_OK) {
     cudaStream_t ss = ctx->slot_stream[q % slots];
-    if (q < slots) CK(cudaStreamWaitEvent(ss, ctx->ev_fork, 0));
+    if (q < slots) cudaStreamWaitEvent(ss, ctx->ev_fork, 0);
     ++q;
     int bslots[4];
-    for (size_t g = 0; g < batch.size(); ++g) {
+    for (size_t g = 0; g < batch.size() && enq == NUGPR_OK; ++g) {
       const int j = batch[g];
       bslots[g] = j % slots;
-      if (tl_on) { cudaEventRecord(tls[j], ss); ctx->tl_pre = tlp[j]; }
-      RET(enqueue_eval(ctx, bl, bslots[g], y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j], true));
-      ctx->tl_pre = nullptr;
+      note_enq(enqueue_eval(ctx, bl, bslots[g], y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j], true), j);
     }
     cudaGraphExec_t ex = nullptr;
-    RET(get_batch_graph(ctx, bl, bslots, static_cast<int>(batch.size()), 1 + cfg->num_probes, cfg->logdet_mode, &ex));
-    CK(cudaGraphLaunch(ex, ss));
-    for (int j : batch) {
-      if (tl_on) cudaEventRecord(tle[j], ss);
-      CK(cudaMemcpyAsync(&ctx->h_out[j], bl->E[j % slots].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss));
+    if (enq == NUGPR_OK)
+      note_enq(get_batch_graph(ctx, bl, bslots, static_cast<int>(batch.size()), 1 + cfg->num_probes,
+                               cfg->logdet_mode, &ex), batch[0]);
+    if (enq == NUGPR_OK) {
+      cudaGraphLaunch(ex, ss);
+      for (int j : batch) {
+        cudaMemcpyAsync(&ctx->h_out[j], bl->E[j % slots].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss);
+        launched[j] = 1;
+      }
     }
   }
   for (int slot = 0; slot < std::min(slots, q); ++slot) {
-    CK(cudaEventRecord(ctx->ev_join[slot], ctx->slot_stream[slot]));
-    CK(cudaStreamWaitEvent(s0, ctx->ev_join[slot], 0));
+    cudaEventRecord(ctx->ev_join[slot], ctx->slot_stream[slot]);
+    cudaStreamWaitEvent(s0, ctx->ev_join[slot], 0);
   }
-  CK(cudaStreamSynchronize(s0));
-  if (tl_on) {
-    for (int j = 0; j < nk; ++j) {
-      float a0 = 0.f, a1 = 0.f, a2 = 0.f;
-      cudaEventElapsedTime(&a0, tl0, tls[j]);
-      cudaEventElapsedTime(&a1, tl0, tlp[j]);
-      cudaEventElapsedTime(&a2, tl0, tle[j]);
-      fprintf(stderr, "[nugpr timeline] eval %d mode %d start %.3f pre-done %.3f end %.3f ms (iters %d)\n", ks[j],
-              modes[j], a0, a1, a2, ctx->h_out[j].iters_q_max);
-      cudaEventDestroy(tls[j]); cudaEventDestroy(tlp[j]); cudaEventDestroy(tle[j]);
-    }
-    cudaEventDestroy(tl0);
+  const cudaError_t se = cudaStreamSynchronize(s0);
+  if (se != cudaSuccess) {
+    mark_rest(0, fail(NUGPR_ERR_CUDA, "evaluation streams: %s", cudaGetErrorString(se)));
+    return NUGPR_OK;
   }
   for (int j = 0; j < nk; ++j) {
     EvalRecord& r = recs[ks[j]];
-    r.o = ctx->h_out[j];
     r.valid = 1;
-    r.status = finish_record(bl, cfg, r.o, graph);
-    if (r.status != NUGPR_OK && r.status != NUGPR_ERR_CG_NOT_CONVERGED) return static_cast<nugpr_status>(r.status);
+    if (launched[j]) {
+      r.o = ctx->h_out[j];
+      r.status = finish_record(bl, cfg, r.o, graph);
+    } else {
+      memset(&r.o, 0, sizeof(r.o));
+      r.o.L = NAN;
+      r.status = (j >= failed_at) ? enq : NUGPR_ERR_INTERNAL;
+    }
   }
   return NUGPR_OK;
 }
+
 
 extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const double* y_sorted, nugpr_theta theta,
                                       const nugpr_grad_cfg* gcfg, const nugpr_solve_cfg* scfg, double* L0,
@@ -1980,12 +1986,13 @@ extern "C" nugpr_status nugpr_numgrad(nugpr_ctx* ctx, nugpr_blocks* bl, const do
     memset(mine, 0, sizeof(mine));
     std::vector<int> ks;                       // this rank's evaluations, most expensive first
     for (int k : {1, 2, 3, 4, 5, 6, 0}) if (owner[k] == pr) ks.push_back(k);
-    RET(run_evals_concurrent(ctx, bl, y_dev, ks, tp, scfg, mine));
+    RET(run_evals_concurrent(ctx, bl, y_dev, ks, tp, scfg, mine));   // statuses live in the records
+    // every rank exchanges, failed evaluations included (their status travels with the record)
     nugpr_status worst = NUGPR_OK;
     RET(central_exchange(ctx, owner, mine, h, L0, grad, evals, &worst, pw));
     ne = NUGPR_NUM_EVALS;
     if (n_evals) *n_evals = ne;
-    if (worst != NUGPR_OK) return fail(worst, "an evaluation did not converge");
+    if (worst != NUGPR_OK) return worst;     // central_exchange set the message
     return NUGPR_OK;
   } else if (gcfg->mode == NUGPR_GRAD_FORWARD_HALVING) {
     if (gcfg->max_halvings < 0 || gcfg->max_halvings > 20) return fail(NUGPR_ERR_INVALID_ARG, "max_halvings must be in [0, 20]");
@@ -2111,10 +2118,12 @@ extern "C" nugpr_status nugpr_predict(nugpr_ctx* ctx, nugpr_blocks* bl, const do
     launch_pred_reduce(Ld, W, B.cy, B.u, m, wc, ww, p, s);
     launch_pred_pcol(p, n_c, m, ldc, pc, s);
     launch_pred_trmm(Cm, pc, lp, ldp, zero64, zero64, 1, m, ldc, s);
+    // device outputs are written in place at offset j0; host outputs go through the staging area
+    // (mean at ostage[0..m), var at ostage[nt..nt+m)) and are copied out below — independently per output
     double* mo = mdev ? mean : ostage;
     double* vo = var ? (vdev ? var : ostage + nt) : nullptr;
     launch_pred_final(n_c, m, ldc, wc, ww, pc, lp, zeta, lz, th.outputscale, noise_add, mo, vo,
-                      mdev ? j0 : 0, s);
+                      mdev ? j0 : 0, vdev ? j0 : 0, s);
     CKL();
     if (!mdev) CK(cudaMemcpyAsync(mean + j0, ostage, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
     if (var && !vdev) CK(cudaMemcpyAsync(var + j0, ostage + nt, sizeof(double) * m, cudaMemcpyDeviceToHost, s));
@@ -2156,6 +2165,11 @@ extern "C" nugpr_status nugpr_mll_exact(nugpr_ctx* ctx, nugpr_blocks* bl, const 
 // ------------------------------------------------------------------------------------------
 extern "C" nugpr_status nugpr_adam_step(double state[10], const double grad[3], double lr) {
   if (!state || !grad) return fail(NUGPR_ERR_INVALID_ARG, "NULL argument");
+  for (int i = 0; i < 3; ++i)
+    if (!std::isfinite(grad[i]))    // (a NaN would otherwise pass the clamp below as 1e-8 and poison m, v)
+      return fail(NUGPR_ERR_INVALID_ARG, "non-finite gradient component %d (%g): Adam step refused", i, grad[i]);
+  for (int i = 0; i < 9; ++i)
+    if (!std::isfinite(state[i])) return fail(NUGPR_ERR_INVALID_ARG, "non-finite Adam state entry %d", i);
   const double b1 = 0.9, b2 = 0.999, eps = 1e-8;
   double t = state[9] + 1.0;
   for (int i = 0; i < 3; ++i) {
@@ -2193,6 +2207,7 @@ extern "C" nugpr_status nugpr_train(nugpr_ctx* ctx, const double* X_sorted, cons
     if (bl->h_pending) cudaStreamWaitEvent(ctx->stream, ctx->ev_h1, 0);   // H done before the next build
     nugpr_blocks_destroy(bl);
     if (st != NUGPR_OK) return st;
+    if (!std::isfinite(L0)) return fail(NUGPR_ERR_BREAKDOWN, "epoch %d: non-finite loss L0 = %g", ep, L0);
     if (records) {
       double* r = records + static_cast<size_t>(ep) * NUGPR_TRAIN_RECORD;
       int ky = 0, kq = 0;

@@ -158,9 +158,6 @@ struct CholArgs {
   double* u;             // [n_pad]
 };
 
-__device__ int g_chol_trace = 0;
-__device__ __forceinline__ bool getenv_flag_chol_trace() { return g_chol_trace != 0; }
-
 __device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
@@ -176,18 +173,12 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   __shared__ double red[8];
   const int tid = threadIdx.x;
   if (tid == 0) fail = 0;
-  unsigned long long tst[3];
-  const bool trace = getenv_flag_chol_trace();
-  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[0]));
   __syncthreads();
 
   // ---------------- Cholesky (right-looking, NB-column panels) ----------------
   // Panel Pn is column-major in smem with leading dimension pr (rows contiguous): every
   // per-row sweep is unit-stride across lanes (no bank conflicts).
   double* Pn = sm;
-  long long tph[4] = {0, 0, 0, 0};
-  long long tc0 = clock64();
-  auto tick = [&](int q) { if (tid == 0) { long long t = clock64(); tph[q] += t - tc0; tc0 = t; } };
   for (int k0 = 0; k0 < ld; k0 += NB) {
     const int nb = min(NB, ld - k0);
     const int pr = ld - k0;          // panel rows
@@ -201,7 +192,6 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
     // scaling first), and the scaling of the panel's columns is applied after the loop
     // ccol[j&1][c] mirrors the panel's column j at rows c < nb in a separate array (written by
     // the step before), so the broadcast reads of the update do not alias its stores
-    tick(0);
     __shared__ double pdg[NB], pinv[NB], ccol[2][NB];
     for (int r = tid; r < nb; r += NT) ccol[0][r] = Pn[r];
     __syncthreads();
@@ -238,12 +228,10 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       else if (r > c) Pn[c * pr + r] *= pinv[c];
     }
     __syncthreads();
-    tick(1);
     for (int idx = tid; idx < pr * nb; idx += NT) {
       const int c = idx / pr, r = idx % pr;
       A[static_cast<int64_t>(k0 + c) * ld + k0 + r] = (r >= c) ? Pn[c * pr + r] : 0.0;
     }
-    tick(2);
     // trailing update of the lower triangle: A[t+r][t+c] -= sum_j P[nb+r][j] P[nb+c][j], r >= c,
     // in 64x64 output tiles, 4x4 register tile per thread, coalesced read-modify-write of A.
     const int tr = pr - nb;
@@ -291,9 +279,7 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
       }
     }
     __syncthreads();
-    tick(3);
   }
-  if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[1]));
   // logdet partial (real rows only; padding diagonal is 1)
   double ls = 0.0;
   for (int r = tid; r < b; r += NT) ls += log(A[static_cast<int64_t>(r) * ld + r]);
@@ -425,264 +411,6 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
     }
     a.u[p0 + r] = (a0 + a1) + (a2 + a3);
   }
-  if (tid == 0) {
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[2]));
-    if (trace && blockIdx.x < 4)
-      printf("CHOLG blk %d chol %.1f inv %.1f us | cycles load %lld cols %lld store %lld trail %lld\n", blockIdx.x,
-             (tst[1] - tst[0]) * 1e-3, (tst[2] - tst[1]) * 1e-3, tph[0], tph[1], tph[2], tph[3]);
-  }
-}
-
-// ---------------------------------------------------------------------------------------
-// Shared-memory-resident variant for ld <= CS_LDMAX (C1-C3): the packed lower triangle of the
-// block lives in shared memory for the whole factorisation (ld = 200: 161 KB), K_i is
-// assembled straight into it from X (the same distance / kernel arithmetic as
-// assemble_kernel, so the blocks are bit-identical), then: blocked right-looking Cholesky
-// (16-column panels, column steps by all threads, 4x4 register-tiled trailing update),
-// logdet, in-place triangular inverse by 16-row panels, and one coalesced write of Linv
-// (zero upper triangle) plus u = Linv 1.  Global memory is touched once in and once out.
-constexpr int CS_NT = 512;
-constexpr int CS_NB = 16;
-constexpr int CS_YC = 32;
-constexpr int CS_LDMAX = 216;
-
-__device__ __forceinline__ int cofs(int c, int ld) { return c * ld - (c * (c - 1)) / 2; }
-
-
-struct CholSmemArgs {
-  CholArgs c;
-  const double* X;       // cluster-sorted inputs (fused assembly)
-  int d;
-  const double* jitter;
-  int kind;
-  double lam, noise, alpha;
-};
-
-__global__ void __launch_bounds__(CS_NT) chol_smem_kernel(CholSmemArgs g) {
-  const CholArgs& a = g.c;
-  const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
-  const int ld = a.ld[i];
-  const int64_t o = a.off[i];
-  const int b = static_cast<int>(a.off[i + 1] - o);
-  double* A = a.A + a.boff[i];
-  extern __shared__ double sm[];
-  const int np = ld * (ld + 1) / 2;
-  double* S = sm;                                    // packed lower: (r, c) at cofs(c) + r - c
-  double* XdT = S + ((np + 1) & ~1);                 // (NB+1) x NB
-  double* Yc = XdT + (CS_NB + 1) * CS_NB;            // NB x YC
-  __shared__ int fail;
-  __shared__ double red[CS_NT / 32];
-  __shared__ double s_inv;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  constexpr int NWP = CS_NT / 32;
-  if (tid == 0) fail = 0;
-  unsigned long long tst[6];
-  auto stamp = [&](int q) { if (tid == 0) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tst[q])); };
-  const bool trace = getenv_flag_chol_trace();
-  stamp(0);
-#define SP(r, c) S[cofs((c), ld) + (r) - (c)]
-  // ---- fused assembly of K_i = k(X_i, X_i) + (noise + jitter_i) I, padding = identity ----
-  {
-    const double diag_add = g.noise + (g.jitter ? g.jitter[i] : 0.0);
-    const double* Xi = g.X + o * g.d;
-    for (int c = wid; c < ld; c += NWP) {
-      for (int r = c + lane; r < ld; r += 32) {
-        double v;
-        if (r < b && c < b) {
-          double sq = 0.0;
-          for (int dd = 0; dd < g.d; ++dd) {
-            const double df = __dsub_rn(Xi[static_cast<int64_t>(r) * g.d + dd], Xi[static_cast<int64_t>(c) * g.d + dd]);
-            sq = __dadd_rn(sq, __dmul_rn(df, df));
-          }
-          v = kval(g.kind, sq, g.lam, g.alpha);
-          if (r == c) v += diag_add;
-        } else {
-          v = (r == c) ? 1.0 : 0.0;
-        }
-        SP(r, c) = v;
-      }
-    }
-  }
-  __syncthreads();
-  stamp(1);
-  // ---- Cholesky, 16-column panels ----
-  for (int k0 = 0; k0 < ld; k0 += CS_NB) {
-    const int nb = min(CS_NB, ld - k0);
-    for (int j = 0; j < nb; ++j) {
-      const int col = k0 + j;
-      if (tid == 0) {
-        double piv = SP(col, col);
-        if (!(piv > 0.0)) { fail = 1; piv = 1.0; }
-        const double dg = sqrt(piv);
-        SP(col, col) = dg;
-        s_inv = 1.0 / dg;
-      }
-      __syncthreads();
-      const double inv = s_inv;
-      for (int r = col + 1 + tid; r < ld; r += CS_NT) SP(r, col) *= inv;
-      __syncthreads();
-      const int ncols = k0 + nb - col - 1;          // remaining panel columns
-      if (ncols > 0) {
-        const int nrow = ld - col - 1;
-        for (int idx = tid; idx < ncols * nrow; idx += CS_NT) {
-          const int c2 = col + 1 + idx / nrow, r = col + 1 + idx % nrow;
-          if (r >= c2) SP(r, c2) -= SP(r, col) * SP(c2, col);
-        }
-        __syncthreads();
-      }
-    }
-    // trailing update of the lower triangle with the panel, 4x4 tiles
-    const int t0 = k0 + nb;
-    const int tr = ld - t0;
-    if (tr > 0) {
-      const int nt4 = (tr + 3) / 4;
-      const int ntl = nt4 * (nt4 + 1) / 2;
-      for (int tt = tid; tt < ntl; tt += CS_NT) {
-        int bi = static_cast<int>((sqrtf(8.0f * tt + 1.0f) - 1.0f) * 0.5f);
-        while (bi * (bi + 1) / 2 > tt) --bi;
-        while ((bi + 1) * (bi + 2) / 2 <= tt) ++bi;
-        const int bj = tt - bi * (bi + 1) / 2;
-        const int rb = t0 + bi * 4, cb = t0 + bj * 4;
-        double acc[4][4];
-#pragma unroll
-        for (int x = 0; x < 4; ++x)
-#pragma unroll
-          for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-        for (int jj = 0; jj < nb; ++jj) {
-          const double* pc = S + cofs(k0 + jj, ld) - (k0 + jj);   // column k0+jj, indexed by row
-          double av[4], bv[4];
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            av[x] = (rb + x < ld) ? pc[rb + x] : 0.0;
-            bv[x] = (cb + x < ld) ? pc[cb + x] : 0.0;
-          }
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-#pragma unroll
-            for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
-        }
-#pragma unroll
-        for (int y = 0; y < 4; ++y) {
-          const int c = cb + y;
-          if (c >= ld) continue;
-#pragma unroll
-          for (int x = 0; x < 4; ++x) {
-            const int r = rb + x;
-            if (r < ld && r >= c) SP(r, c) -= acc[x][y];
-          }
-        }
-      }
-    }
-    __syncthreads();
-  }
-  stamp(2);
-  // logdet partial (real rows only; padding diagonal is 1)
-  double ls = 0.0;
-  for (int r = tid; r < b; r += CS_NT) ls += log(SP(r, r));
-  ls = warp_sum(ls);
-  if (lane == 0) red[wid] = ls;
-  __syncthreads();
-  if (tid == 0) {
-    double s_ = 0.0;
-    for (int w = 0; w < NWP; ++w) s_ += red[w];
-    a.logdet_blk[i] = 2.0 * s_;
-    a.status[i] = fail;
-  }
-  __syncthreads();
-  if (fail) return;
-  // ---- triangular inverse in place, by 16-row panels ----
-  // Row panel I = rows [I0, I0+nb): X_II = L_II^{-1} (XdT, 16 threads), Y = L[I, 0:I0] X[0:I0, 0:I0]
-  // (thread pair per column c: 8 rows each, 8 independent accumulators over k = c..I0-1, with
-  // the L row segments broadcast), then X[I, 0:I0] = -X_II Y written over L[I, 0:I0].
-  constexpr int NBP = CS_NB + 1;
-  double* Yt = Yc;                                   // Y as [c][16]: 16 * I0 <= 16 * ld doubles
-  for (int I0 = 0; I0 < ld; I0 += CS_NB) {
-    const int nb = min(CS_NB, ld - I0);
-    if (tid < nb) {
-      const int j = tid;
-      for (int r = 0; r < nb; ++r) {
-        double v = 0.0;
-        if (r >= j) {
-          v = (r == j) ? 1.0 : 0.0;
-          for (int k = j; k < r; ++k) v -= SP(I0 + r, I0 + k) * XdT[j * NBP + k];
-          v /= SP(I0 + r, I0 + r);
-        }
-        XdT[j * NBP + r] = v;
-      }
-    }
-    for (int t = tid; t < 2 * I0; t += CS_NT) {
-      const int c = t >> 1, rh = (t & 1) * 8;
-      double acc[8];
-#pragma unroll
-      for (int q = 0; q < 8; ++q) acc[q] = 0.0;
-      const double* xc = S + cofs(c, ld) - c;          // X[k][c] = xc[k], k >= c
-      for (int k = c; k < I0; ++k) {
-        const double xv = xc[k];
-        const double* lk = S + cofs(k, ld) - k + I0 + rh;   // L[I0+rh+q][k] = lk[q]
-#pragma unroll
-        for (int q = 0; q < 8; ++q) acc[q] = fma((rh + q < nb) ? lk[q] : 0.0, xv, acc[q]);
-      }
-#pragma unroll
-      for (int q = 0; q < 8; ++q) Yt[c * CS_NB + rh + q] = acc[q];
-    }
-    __syncthreads();
-    for (int idx = tid; idx < nb * I0; idx += CS_NT) {
-      const int r = idx % nb, c = idx / nb;
-      double acc = 0.0;
-      for (int k = 0; k <= r; ++k) acc = fma(XdT[k * NBP + r], Yt[c * CS_NB + k], acc);
-      SP(I0 + r, c) = -acc;
-    }
-    for (int idx = tid; idx < nb * nb; idx += CS_NT) {
-      const int r = idx % nb, c = idx / nb;
-      if (r >= c) SP(I0 + r, I0 + c) = XdT[c * NBP + r];
-    }
-    __syncthreads();
-  }
-  stamp(3);
-  // ---- write Linv (zero upper triangle) and u = Linv 1_b ----
-  for (int c = wid; c < ld; c += NWP)
-    for (int r = lane; r < ld; r += 32) A[static_cast<int64_t>(c) * ld + r] = (r >= c) ? SP(r, c) : 0.0;
-  const int64_t p0 = a.poff[i];
-  for (int r = tid; r < ld; r += CS_NT) {
-    double acc = 0.0;
-    if (r < b)
-      for (int k = 0; k <= r; ++k) acc += SP(r, k);
-    a.u[p0 + r] = acc;
-  }
-  stamp(4);
-  if (trace && tid == 0 && blockIdx.x < 4)
-    printf("CHOL blk %d asm %.1f chol %.1f inv %.1f out %.1f us\n", blockIdx.x, (tst[1] - tst[0]) * 1e-3,
-           (tst[2] - tst[1]) * 1e-3, (tst[3] - tst[2]) * 1e-3, (tst[4] - tst[3]) * 1e-3);
-#undef SP
-}
-
-size_t chol_smem_bytes_fused(int ld_max) {
-  const size_t np = static_cast<size_t>(ld_max) * (ld_max + 1) / 2;
-  return sizeof(double) * (((np + 1) & ~static_cast<size_t>(1)) + (CS_NB + 1) * CS_NB + CS_NB * static_cast<size_t>(ld_max));
-}
-
-bool chol_fused_ok(int ld_max) {
-  const char* v = getenv("NUGPR_CHOL_SMEM");      // experimental: slower than the global-memory kernel so far
-  return ld_max <= CS_LDMAX && v && v[0] == '1';
-}
-
-void launch_chol_fused(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
-                       const double* jitter, double* A, int kind, double lam, double noise, double alpha,
-                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s) {
-  CholSmemArgs g;
-  g.c = CholArgs{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
-  g.X = X; g.d = d; g.jitter = jitter; g.kind = kind; g.lam = lam; g.noise = noise; g.alpha = alpha;
-  smem_optin(reinterpret_cast<const void*>(chol_smem_kernel));
-  {
-    static int traced = -1;
-    if (traced < 0) {
-      const char* v = getenv("NUGPR_CHOL_TRACE");
-      traced = (v && v[0] == '1') ? 1 : 0;
-      if (traced) cudaMemcpyToSymbol(g_chol_trace, &traced, sizeof(int));
-    }
-  }
-  chol_smem_kernel<<<list ? nlist : L.n_c, CS_NT, chol_smem_bytes_fused(ld_max), s>>>(g);
-  note_launch(); post_launch("chol_smem_kernel");
 }
 
 size_t chol_smem_bytes(int ld_max) {
@@ -696,14 +424,6 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
   CholArgs a{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
   size_t smem = chol_smem_bytes(ld_max);
   smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel));
-  {
-    static int traced = -1;
-    if (traced < 0) {
-      const char* v = getenv("NUGPR_CHOL_TRACE");
-      traced = (v && v[0] == '1') ? 1 : 0;
-      if (traced) cudaMemcpyToSymbol(g_chol_trace, &traced, sizeof(int));
-    }
-  }
   chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
   note_launch(); post_launch("chol_trtri_kernel");
 }
@@ -713,7 +433,6 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
 //   op(B)(k,c) = TRANSB ? B[k*ld + c] (= B^T) : B[c*ld + k]
 //   A_LOWER: A(r,k) = 0 for k > r;  B_LOWERT: op(B)(k,c) = 0 for k > c (B^T of a lower matrix)
 //   SYM: C symmetric — only tiles with tile_r >= tile_c are computed and mirrored.
-// 64x64 tiles, 256 threads, 4x4 register tile per thread, K step 16 in shared memory.
 struct GemmArgs {
   const double* A;
   const double* B;
@@ -723,92 +442,7 @@ struct GemmArgs {
   int ntile_max;         // tiles per dimension of the largest block
 };
 
-template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM>
-__global__ void __launch_bounds__(256) gemm_blocks_kernel(GemmArgs g) {
-  const int i = blockIdx.y;
-  const int ld = g.ld[i];
-  const int nt = (ld + 63) / 64;
-  int tr, tc;
-  if (SYM) {
-    int t = blockIdx.x;
-    if (t >= nt * (nt + 1) / 2) return;
-    tr = static_cast<int>((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
-    while (tr * (tr + 1) / 2 > t) --tr;
-    while ((tr + 1) * (tr + 2) / 2 <= t) ++tr;
-    tc = t - tr * (tr + 1) / 2;
-  } else {
-    if (static_cast<int>(blockIdx.x) >= nt * nt) return;
-    tr = blockIdx.x % nt;
-    tc = blockIdx.x / nt;
-  }
-  const int64_t bo = g.boff[i];
-  const double* A = g.A + bo;
-  const double* B = g.B + bo;
-  double* C = g.C + bo;
-  const int r0 = tr * 64, c0 = tc * 64;
-  int kend = ld;
-  if (A_LOWER) kend = min(kend, r0 + 64);
-  if (B_LOWERT) kend = min(kend, c0 + 64);
-  __shared__ double As[16][64 + 2];
-  __shared__ double Bs[16][64 + 2];
-  const int tid = threadIdx.x;
-  const int tx = tid & 15, ty = tid >> 4;
-  double acc[4][4];
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
-  for (int k0 = 0; k0 < kend; k0 += 16) {
-    // A tile: rows r0..r0+63, k0..k0+15 ; load coalesced over rows
-    for (int idx = tid; idx < 16 * 64; idx += 256) {
-      int kk = idx / 64, rr = idx % 64;
-      int r = r0 + rr, k = k0 + kk;
-      As[kk][rr] = (r < ld && k < ld) ? A[static_cast<int64_t>(k) * ld + r] : 0.0;
-    }
-    for (int idx = tid; idx < 16 * 64; idx += 256) {
-      int kk, cc;
-      if (TRANSB) { kk = idx / 64; cc = idx % 64; }
-      else        { cc = idx / 16; kk = idx % 16; }
-      int c = c0 + cc, k = k0 + kk;
-      double v = 0.0;
-      if (c < ld && k < ld) v = TRANSB ? B[static_cast<int64_t>(k) * ld + c] : B[static_cast<int64_t>(c) * ld + k];
-      Bs[kk][cc] = v;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) {
-      double a4[4], b4[4];
-#pragma unroll
-      for (int x = 0; x < 4; ++x) a4[x] = As[kk][ty + 16 * x];
-#pragma unroll
-      for (int y = 0; y < 4; ++y) b4[y] = Bs[kk][tx + 16 * y];
-#pragma unroll
-      for (int x = 0; x < 4; ++x)
-#pragma unroll
-        for (int y = 0; y < 4; ++y) acc[x][y] = fma(a4[x], b4[y], acc[x][y]);
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int x = 0; x < 4; ++x)
-#pragma unroll
-    for (int y = 0; y < 4; ++y) {
-      int r = r0 + ty + 16 * x, c = c0 + tx + 16 * y;
-      if (r < ld && c < ld) {
-        if (SYM) {
-          if (r >= c) {
-            C[static_cast<int64_t>(c) * ld + r] = acc[x][y];
-            C[static_cast<int64_t>(r) * ld + c] = acc[x][y];
-          }
-        } else {
-          C[static_cast<int64_t>(c) * ld + r] = acc[x][y];
-        }
-      }
-    }
-}
-
-// DMMA (mma.sync m8n8k4 f64) version of the batched block GEMM: same contract as
-// gemm_blocks_kernel.  64x64 CTA tile, 8 warps as 2 (rows) x 4 (cols), warp tile 32x16 =
+// Batched block GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64).  64x64 CTA tile, 8 warps as 2 (rows) x 4 (cols), warp tile 32x16 =
 // 4 x 2 m8n8 tiles; K staged 16 at a time in shared memory (k-major, row stride 68 = 4 mod 16
 // so the fragment loads are bank-conflict free), register double buffering of the next stage.
 // 8x8 sub-tiles entirely outside the block (ld is a multiple of 8) are skipped.
@@ -1029,7 +663,7 @@ struct LanczosArgs {
   double* lam0;          // [1]
   double* v0;            // [n_c] out
   double* M;             // n_c x n_c out (K - lam0 I)
-  int32_t* info;         // [2] {iterations, converged}
+  int32_t* info;         // [3] {iterations, converged, lambda_0 not certifiably > 0}
   int cacheK;
   int kcache;            // Lanczos vectors cached in shared memory
 };
@@ -1335,7 +969,14 @@ __global__ void __launch_bounds__(LZ_NT, 1) lanczos_cluster_kernel(LanczosArgs a
     const int64_t g = static_cast<int64_t>(r0) * n + idx;
     a.M[g] = Krow(r)[c] - ((r0 + r) == c ? theta : 0.0);
   }
-  if (q == 0 && tid == 0) { a.lam0[0] = theta; a.info[0] = k_final; a.info[1] = s_conv; }
+  // info[2]: lambda_0 is not certifiably positive — within the Ritz-residual bound tol_rel ||K||_inf of
+  // zero (|theta - lambda| <= that bound), e.g. duplicate representatives (reading P27)
+  if (q == 0 && tid == 0) {
+    a.lam0[0] = theta;
+    a.info[0] = k_final;
+    a.info[1] = s_conv;
+    a.info[2] = (theta > a.tol_rel * knorm) ? 0 : 1;
+  }
   cl.sync();   // keep shared memory alive until every CTA is done reading remote slots
 }
 
@@ -1382,9 +1023,9 @@ static cudaError_t lanczos_launch_cs(const LanczosArgs& a0, cudaStream_t s) {
   return cudaLaunchKernelEx(&cfg, kern, a);
 }
 
-void launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
-                    double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
-                    cudaStream_t s) {
+cudaError_t launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
+                           double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
+                           cudaStream_t s) {
   LanczosArgs a;
   a.K = K; a.n_c = n_c; a.vinit = vinit; a.V = scratch; a.kmax = kmax; a.tol_rel = tol_rel;
   a.lam0 = lam0; a.v0 = v0; a.M = M; a.info = info; a.cacheK = 0; a.kcache = 0;
@@ -1395,8 +1036,8 @@ void launch_lanczos(const double* K, int n_c, const double* vinit, double* scrat
   } else {
     e = lanczos_launch_cs<4>(a, s);
   }
-  (void)e;
   note_launch(); post_launch("lanczos_cluster_kernel");
+  return e;
 }
 
 }  // namespace nugpr

@@ -66,6 +66,7 @@ struct EvalParams {
   const double* lam0_src;  // lambda_0(theta) for the record: device scalar (times lam0_mul), or NULL => lam0_val
   double lam0_val;
   double lam0_mul;
+  const int32_t* lz_info;  // {iterations, converged} of the Lanczos that produced lambda_0 (NULL: none)
 };
 
 // CG state for up to MAXC columns, updated only by "last CTA" finalisers.
@@ -79,7 +80,7 @@ struct CGState {
   int32_t any_active;
   int32_t par;            // ping-pong parity of the P / S(P) buffers
   int32_t hit_max;        // some column stopped at max_iter unconverged
-  int32_t pad_;
+  int32_t breakdown;      // some column met a non-finite r^T r or a non-finite / non-positive p^T q
   double quad;
   double t[MAXC];         // Pade trace terms
   unsigned int ticket[8]; // last-CTA counters (self-resetting)

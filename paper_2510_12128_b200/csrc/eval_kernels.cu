@@ -79,7 +79,9 @@ __device__ __forceinline__ int is_active(const EvalParams* P, int c, int iters, 
 // Warps w = 0..nw-1 stride over the columns.
 __device__ void fin_init_body(CGState* st, const EvalParams* prm, const double* rr_part, int n_tiles, int ncol,
                               int nw) {
-  __shared__ int act[MAXC];
+  __shared__ int act[MAXC], bd[MAXC];
+  if (threadIdx.x < MAXC) bd[threadIdx.x] = 0;
+  __syncthreads();
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   if (wid < nw) {
     for (int c = wid; c < MAXC; c += nw) {
@@ -92,7 +94,8 @@ __device__ void fin_init_body(CGState* st, const EvalParams* prm, const double* 
           st->beta[c] = 0.0;
           st->iters[c] = 0;
           st->t[c] = 0.0;
-          act[c] = st->active[c] = is_active(prm, c, 0, tot);
+          act[c] = st->active[c] = isfinite(tot) ? is_active(prm, c, 0, tot) : 0;
+          if (!isfinite(tot)) bd[c] = 1;
         }
       } else if (lane == 0) {
         st->active[c] = 0; st->iters[c] = 0; st->beta[c] = 0.0; st->alpha[c] = 0.0;
@@ -102,11 +105,12 @@ __device__ void fin_init_body(CGState* st, const EvalParams* prm, const double* 
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    int any = 0;
-    for (int c = 0; c < ncol; ++c) any |= act[c];
+    int any = 0, b = 0;
+    for (int c = 0; c < ncol; ++c) { any |= act[c]; b |= bd[c]; }
     st->any_active = any;
     st->par = 0;
     st->hit_max = 0;
+    st->breakdown = b;
     st->quad = 0.0;
   }
 }
@@ -123,8 +127,16 @@ __device__ __forceinline__ void fin_alpha_trace_body(int fin, CGState* st, const
       if (fin == FIN_ALPHA) {
         if (st->active[c]) {
           const double al = st->rr[c] / tot;          // alpha = r^T r / p^T q
-          st->alpha[c] = al;
-          alpha_hist[c * hist_stride + st->iters[c]] = al;
+          if (!(tot > 0.0) || !isfinite(al)) {
+            // breakdown: A is SPD in exact arithmetic, so p^T q <= 0 or a non-finite value means the
+            // operator is not SPD at this theta or the inputs are not finite; freeze the column
+            st->active[c] = 0;
+            st->alpha[c] = 0.0;
+            st->breakdown = 1;
+          } else {
+            st->alpha[c] = al;
+            alpha_hist[c * hist_stride + st->iters[c]] = al;
+          }
         }
       } else {  // FIN_TRACE
         if (c == 0) st->quad = tot; else st->t[c] = tot;
@@ -151,7 +163,8 @@ __device__ void fin_update_body(CGState* st, const EvalParams* P, const double* 
           beta_hist[c * hist_stride + st->iters[c]] = be;
           st->rr[c] = tot;
           st->iters[c] += 1;
-          const int na = is_active(P, c, st->iters[c], tot);
+          int na = is_active(P, c, st->iters[c], tot);
+          if (!isfinite(tot)) { na = 0; st->breakdown = 1; }
           if (!na && !P->replay && st->iters[c] >= P->max_iter && !(sqrt(tot) < P->tol) && tot > 0.0)
             st->hit_max = 1;
           st->active[c] = na;
@@ -2049,13 +2062,15 @@ __global__ void final_kernel(FinalArgs a) {
     double tsum = 0.0, ssum = 0.0, rq = 0.0;
     int kq = 0;
     nugpr_mll_out o;
-    for (int q = 0; q < 16; ++q) o.iters_q[q] = 0;
+    for (int q = 0; q < 16; ++q) { o.iters_q[q] = 0; o.probe_t[q] = 0.0; o.probe_s[q] = 0.0; }
     for (int c = 1; c < a.ncol; ++c) {
       tsum += st->t[c];
       ssum += s_slq[c];
       rq = fmax(rq, sqrt(st->rr[c]));
       kq = max(kq, st->iters[c]);
       o.iters_q[c - 1] = st->iters[c];
+      o.probe_t[c - 1] = (a.logdet_mode == 2) ? __longlong_as_double(0x7ff8000000000000ll) : st->t[c];
+      o.probe_s[c - 1] = s_slq[c];
     }
     const double ldR = a.logdet_R[0];
     if (a.quad_part) {
@@ -2075,8 +2090,12 @@ __global__ void final_kernel(FinalArgs a) {
     o.resid_q_max = rq;
     o.iters_y = st->iters[0];
     o.iters_q_max = kq;
-    o.converged = st->hit_max ? 0 : 1;
+    o.converged = (st->hit_max || st->breakdown) ? 0 : 1;
     o.mode = a.prm->mode;
+    o.breakdown = st->breakdown;
+    o.lanczos_iters = a.prm->lz_info ? a.prm->lz_info[0] : 0;
+    o.lanczos_converged = a.prm->lz_info ? a.prm->lz_info[1] : 1;
+    o.lambda0_degenerate = a.prm->lz_info ? a.prm->lz_info[2] : 0;
     *a.out = o;
   }
 }

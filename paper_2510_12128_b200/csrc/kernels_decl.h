@@ -23,10 +23,6 @@ void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* 
                      int ld_max, const double* jitter, double* dst, int kind, double lam,
                      double noise, double alpha, cudaStream_t s);
 size_t chol_smem_bytes(int ld_max);
-bool chol_fused_ok(int ld_max);
-void launch_chol_fused(const double* X, int d, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
-                       const double* jitter, double* A, int kind, double lam, double noise, double alpha,
-                       int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
 void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
                        int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
 void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s);
@@ -38,9 +34,10 @@ void launch_sum(const double* v, int n, double* out, cudaStream_t s);
 void launch_krep(const double* reps, int n_c, int d, int kind, double lam, double alpha, double* K,
                  cudaStream_t s);
 size_t lanczos_scratch_doubles(int n_c, int kmax);
-void launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
-                    double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
-                    cudaStream_t s);
+// Returns the launch status (a cluster launch can fail for lack of shared memory / co-residency).
+cudaError_t launch_lanczos(const double* K, int n_c, const double* vinit, double* scratch, int kmax,
+                           double tol_rel, double* lam0, double* v0, double* M, int32_t* info,
+                           cudaStream_t s);
 
 // eval_kernels.cu
 ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid, int n_ctasks);
@@ -91,7 +88,7 @@ void launch_pred_lz(const double* Lc, int ldc, int n_c, const double* zeta, doub
 void launch_pred_pcol(const double* p, int n_c, int nt, int ldc, double* pc, cudaStream_t s);
 void launch_pred_final(int n_c, int nt, int ldc, const double* wc, const double* ww, const double* p, const double* lp,
                        const double* zeta, const double* lz, double alpha, double noise_add, double* mean, double* var,
-                       int64_t out_off, cudaStream_t s);
+                       int64_t mean_off, int64_t var_off, cudaStream_t s);
 
 // cluster_kernels.cu (row A0)
 void launch_km_absmax(const double* X, int64_t cnt, unsigned long long* out, cudaStream_t s);

@@ -190,7 +190,8 @@ __global__ void pred_lz_kernel(const double* Lc, int ldc, int n_c, const double*
 // final: mean/var per test point; p and lp stored [n_c][nt] (p padded to ldc rows for the trmm)
 __global__ void pred_final_kernel(int n_c, int nt, int ldc, const double* wc, const double* ww, const double* p,
                                   const double* lp, const double* zeta, const double* lz, double alpha,
-                                  double noise_add, double* mean, double* var, int64_t out_off) {
+                                  double noise_add, double* mean, double* var, int64_t mean_off,
+                                  int64_t var_off) {
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= nt) return;
   double swc = 0.0, sww = 0.0, spz = 0.0, slz = 0.0, spp = 0.0, sll = 0.0;
@@ -204,8 +205,8 @@ __global__ void pred_final_kernel(int n_c, int nt, int ldc, const double* wc, co
     spp = fma(pv, pv, spp);
     sll = fma(lv, lv, sll);
   }
-  mean[out_off + j] = swc - (spz - slz);
-  if (var) var[out_off + j] = alpha - (sww - (spp - sll)) + noise_add;
+  mean[mean_off + j] = swc - (spz - slz);
+  if (var) var[var_off + j] = alpha - (sww - (spp - sll)) + noise_add;
 }
 
 // p [n_c][nt] -> column-major ldc x nt (zero padding rows) for the Linv_C trmm
@@ -309,9 +310,9 @@ void launch_pred_pcol(const double* p, int n_c, int nt, int ldc, double* pc, cud
 
 void launch_pred_final(int n_c, int nt, int ldc, const double* wc, const double* ww, const double* p, const double* lp,
                        const double* zeta, const double* lz, double alpha, double noise_add, double* mean, double* var,
-                       int64_t out_off, cudaStream_t s) {
+                       int64_t mean_off, int64_t var_off, cudaStream_t s) {
   pred_final_kernel<<<(nt + 127) / 128, 128, 0, s>>>(n_c, nt, ldc, wc, ww, p, lp, zeta, lz, alpha, noise_add, mean, var,
-                                                   out_off);
+                                                   mean_off, var_off);
   note_launch(); post_launch("pred_final_kernel");
 }
 

@@ -56,7 +56,15 @@ def compare(rec, ds, bo, theta, Z, rtol=TIGHT, free_check=True, logdet_mode="pad
     else:
         assert rel(rec["logdet_pade"], ro.logdet_pade) < rtol
     assert rel(rec["logdet_slq"], ro.logdet_slq) < rtol
-    assert rel(rec["lambda0"], ro.lambda0) < 1e-10
+    # lambda_0: the Lanczos stops at Ritz residual <= 1e-11 ||K_rep||_inf, which bounds |theta - lambda|
+    # (DESIGN reading P27); that bound, not a fixed relative bar, is what the two must meet
+    Krep = OS.krep_and_M(bo.kind, bo.reps, theta)[0]
+    assert abs(rec["lambda0"] - ro.lambda0) <= 1e-11 * float(np.max(np.sum(np.abs(Krep), axis=1))) + \
+        1e-14 * abs(ro.lambda0)
+    # per-probe Pade / SLQ terms, element by element
+    if logdet_mode != "mbcg":
+        np.testing.assert_allclose(rec["probe_t"], ro.t, rtol=rtol, atol=rtol * np.max(np.abs(ro.t)))
+    np.testing.assert_allclose(rec["probe_s"], ro.s, rtol=rtol, atol=rtol * np.max(np.abs(ro.s)))
     if free_check:
         rf = oracle_mll(bo, ds.y, theta, Z, tol=tol, logdet_mode=logdet_mode)
         if [rf.iters_y] + rf.iters_q != replay:
@@ -131,7 +139,7 @@ def test_mll_parity_C3_full_size(P, ctx, which):
     th = perturbed(ds.theta0)[which]
     Z = synth.probes(203, 8, ds.n)
     rec = P.mll(ctx, bg, ds.y, th, probe_seed=203, num_probes=8)
-    compare(rec, ds, bo, th, Z, free_check=False)
+    compare(rec, ds, bo, th, Z)
 
 
 def test_given_probes_and_slq_mode(P, ctx):
@@ -272,17 +280,18 @@ def test_jitter_ladder_matches_oracle(P, ctx):
 
 
 # ----------------------------------------------------------------------------- execution modes
-def test_graph_mode_equals_direct_launches_bitwise(P, ctx, monkeypatch):
+def test_graph_mode_equals_direct_launches_bitwise(P, ctx):
     """The CUDA-graph CG loop (conditional while node) runs the same kernels in the same order
-    as the direct-launch path: records are bit-identical in every operator mode."""
+    as the direct-launch path (NUGPR_OPT_GRAPHS = 0): records are bit-identical in every operator
+    mode."""
     ds = synth.make_config("C2")
     bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
-    monkeypatch.setenv("NUGPR_NO_GRAPH", "1")
-    bd = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
-    monkeypatch.delenv("NUGPR_NO_GRAPH")
+    cd = P.Context(0)
+    cd.set_option("graphs", False)
+    bd = P.build_blocks(cd, ds.X, ds.offsets, ds.reps, ds.theta0)
     for which, th in perturbed(ds.theta0).items():
         r1 = P.mll(ctx, bg, ds.y, th, probe_seed=202)
-        r2 = P.mll(ctx, bd, ds.y, th, probe_seed=202)
+        r2 = P.mll(cd, bd, ds.y, th, probe_seed=202)
         assert r1 == r2, which
     rr = P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=202, replay=[3] * 9)
     assert rr["iters_y"] == 3 and rr["iters_q"] == [3] * 8
@@ -301,7 +310,7 @@ def test_concurrent_slots_equal_serial_bitwise_and_oracle(P, ctx):
     Z = synth.probes(202, 8, ds.n)
     from oracle.mll import central_perturbations
     for rec, th in zip(e7, central_perturbations(ds.theta0)[0]):
-        compare(rec, ds, bo, th, Z, free_check=False)
+        compare(rec, ds, bo, th, Z)
 
 
 def test_train_concurrent_C2_matches_oracle(P, ctx):
@@ -367,7 +376,7 @@ def test_mbcg_parity(P, ctx, cfg, which):
     Z = synth.probes(seed, 8, ds.n)
     rec = P.mll(ctx, bg, ds.y, th, probe_seed=seed, logdet="mbcg")
     assert rec["converged"]
-    compare(rec, ds, bo, th, Z, logdet_mode="mbcg", free_check=(cfg != "C3"))
+    compare(rec, ds, bo, th, Z, logdet_mode="mbcg")
 
 
 def test_mbcg_numgrad_concurrent_equals_serial(P, ctx):

@@ -1,0 +1,230 @@
+"""GPU parity on every BASELINE config (north_star: "oracle-matched MLL, gradients and trained
+hyperparameters on all five configs"), and the error paths of the C-ABI on the device.
+
+  C3  (n = 100,000): all 7 central-difference records and the gradient vs the oracle.
+  C4  (G-REAL, k-means, Matern-5/2, uneven clusters up to ~4.3k): all 7 records, the gradient and
+      2 epochs of Algorithm 1 vs the oracle.
+  C5  (n = 1,000,000): the baseline, noise-step and lengthscale-step records vs the oracle at full
+      size (the oracle's per-cluster loops run on a thread pool, ORACLE_THREADS = host cores).
+  Errors: DEGENERATE_REPS (identical representatives), CG_NOT_CONVERGED with
+      cg_max_iter = 1 ("flag any instances"), BREAKDOWN on non-finite y.
+
+Records are compared in replay mode (the GPU's per-column iteration counts) at the 1e-9 bar the
+identical FP64 algorithm reaches, and the free-run counts must agree unless a residual sits on the
+threshold (SURVEY §8(c) parity protocol, step 3)."""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import structured as OS
+from oracle.mll import central_perturbations, mll as oracle_mll, numgrad_central, train as oracle_train
+
+pytestmark = pytest.mark.gpu
+
+TIGHT = 1e-9
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_2510_12128_b200 as pkg
+    pkg._native.lib()
+    return pkg
+
+
+@pytest.fixture(scope="module")
+def ctx(P):
+    return P.Context(0)
+
+
+def rel(a, b):
+    return abs(a - b) / max(abs(b), 1e-300)
+
+
+def lam0_bound(bo, theta):
+    """|lambda_0(GPU) - lambda_0(LAPACK)| bound: the Lanczos stops when its Ritz residual
+    |beta_k s_k| <= 1e-11 ||K_rep||_inf, and for a symmetric matrix the Ritz value is within the
+    residual norm of an eigenvalue (DESIGN reading P27), plus FP64 rounding of eigvalsh."""
+    Krep = OS.krep_and_M(bo.kind, bo.reps, theta)[0]
+    kn = float(np.max(np.sum(np.abs(Krep), axis=1)))
+    return 1e-11 * kn
+
+
+def check_record(rec, ro, bo, theta, rtol=TIGHT):
+    assert rec["mode"] == ro.mode
+    for k in ("L", "quad", "logdet_pade", "logdet_slq", "logdet_R"):
+        assert rel(rec[k], getattr(ro, k)) < rtol, (k, rec[k], getattr(ro, k))
+    assert abs(rec["lambda0"] - ro.lambda0) <= lam0_bound(bo, theta) + 1e-14 * abs(ro.lambda0)
+    # per-probe terms element by element (errors in single probes cannot cancel in the mean)
+    np.testing.assert_allclose(rec["probe_t"], ro.t, rtol=rtol, atol=rtol * np.max(np.abs(ro.t)))
+    np.testing.assert_allclose(rec["probe_s"], ro.s, rtol=rtol, atol=rtol * np.max(np.abs(ro.s)))
+
+
+def free_run_agrees(rec, ro_free, tol=0.01):
+    """Free-run iteration counts equal the GPU's, unless a disagreeing column's residual sits within
+    1e-6 tol of the threshold (parity protocol step 3)."""
+    g = [rec["iters_y"]] + list(rec["iters_q"])
+    o = [ro_free.iters_y] + list(ro_free.iters_q)
+    if g == o:
+        return True
+    return abs(ro_free.resid_y - tol) < 1e-6 * tol or abs(ro_free.resid_q_max - tol) < 1e-6 * tol
+
+
+# ----------------------------------------------------------------------------- C3
+def test_numgrad_C3_all_records_and_gradient(P, ctx):
+    """C3 (n = 100k, the bench workload): the 7 concurrent evaluations of the central-difference
+    gradient, each record against the oracle in replay mode, the gradient against numgrad_central
+    over the replayed oracle, and a free run of the baseline and lengthscale evaluations."""
+    ds = synth.make_config("C3")
+    seed = ds.meta["probe_seed"]
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=7)
+    bo = OS.build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    Z = synth.probes(seed, 8, ds.n)
+    L0, g, evals = P.numgrad(ctx, bg, ds.y, ds.theta0, probe_seed=seed)
+    pts, _ = central_perturbations(ds.theta0)
+    reps = iter([[e["iters_y"]] + e["iters_q"] for e in evals])
+    ros = []
+
+    def loss(p):
+        r = oracle_mll(bo, ds.y, p, Z, replay=next(reps))
+        ros.append(r)
+        return r.L
+
+    L0o, go, _ = numgrad_central(loss, ds.theta0)
+    for k in range(7):
+        check_record(evals[k], ros[k], bo, pts[k])
+    assert rel(L0, L0o) < TIGHT
+    np.testing.assert_allclose(g, go, rtol=1e-5)
+    for k in (0, 1):
+        assert free_run_agrees(evals[k], oracle_mll(bo, ds.y, pts[k], Z))
+
+
+# ----------------------------------------------------------------------------- C4
+def c4_dataset():
+    from oracle import kmeans as KM
+    g = synth.g_real(N=40000, d=8, seed=104)
+    km = KM.kmeans(g["X"], 20, seed=104, rep_mode=KM.CENTROID)
+    X, y, off = g["X"][km["perm"]], g["y"][km["perm"]], km["offsets"]
+    rng = np.random.default_rng(0)
+    dists = []
+    for i in range(20):
+        Xi = X[off[i]:off[i + 1]]
+        a = rng.integers(0, Xi.shape[0], 200)
+        b = rng.integers(0, Xi.shape[0], 200)
+        dists.append(np.linalg.norm(Xi[a] - Xi[b], axis=1))
+    th0 = (float(np.median(np.concatenate(dists))), 0.16, float(np.var(y)))
+    return np.ascontiguousarray(X), np.ascontiguousarray(y), off, km["reps"], th0
+
+
+def test_numgrad_and_train_C4(P, ctx):
+    """C4 ('train + predict with variance'): the 7 records and the gradient at theta_0 against the
+    oracle, then 2 epochs of Algorithm 1 against the oracle's (free run, theta within 1e-6)."""
+    X, y, off, reps, th0 = c4_dataset()
+    seed = 204
+    bg = P.build_blocks(ctx, X, off, reps, th0, kernel="matern52", eval_slots=7)
+    bo = OS.build_blocks(X, off, reps, th0, kind="matern52")
+    Z = synth.probes(seed, 8, X.shape[0])
+    L0, g, evals = P.numgrad(ctx, bg, y, th0, probe_seed=seed)
+    pts, _ = central_perturbations(th0)
+    reps_it = iter([[e["iters_y"]] + e["iters_q"] for e in evals])
+    ros = []
+
+    def loss(p):
+        r = oracle_mll(bo, y, p, Z, replay=next(reps_it))
+        ros.append(r)
+        return r.L
+
+    L0o, go, _ = numgrad_central(loss, th0)
+    for k in range(7):
+        check_record(evals[k], ros[k], bo, pts[k])
+    np.testing.assert_allclose(g, go, rtol=1e-5)
+    E = 2
+    st, rec = P.train(ctx, X, off, reps, y, th0, epochs=E, kernel="matern52", probe_seed=seed, eval_slots=7)
+    sto, reco = oracle_train(X, off, reps, y, th0, Z, epochs=E, kind="matern52")
+    for e in range(E):
+        assert rel(rec[e, 0], reco[e]["L0"]) < TIGHT
+        np.testing.assert_allclose(rec[e, 4:7], reco[e]["theta"], rtol=1e-9)
+        np.testing.assert_allclose(rec[e, 1:4], reco[e]["grad"], rtol=1e-5)
+    np.testing.assert_allclose(st[:3], sto.theta, rtol=1e-6)       # north_star bar: 1e-3
+
+
+# ----------------------------------------------------------------------------- C5
+@pytest.mark.parametrize("which", ["baseline", "noise+", "lam-"])
+def test_mll_parity_C5_full_size(P, ctx, which):
+    """C5 (n = 1,000,000, 2000 clusters of 500) at full size: one record per operator family
+    against the oracle in replay mode."""
+    ds = synth.make_config("C5")
+    seed = ds.meta["probe_seed"]
+    l, s, a = ds.theta0
+    th = {"baseline": (l, s, a), "noise+": (l, s * 1.001, a), "lam-": (l * 0.999, s, a)}[which]
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=1)
+    rec = P.mll(ctx, bg, ds.y, th, probe_seed=seed)
+    bg.close()
+    bo = _c5_oracle_blocks(ds)
+    Z = synth.probes(seed, 8, ds.n)
+    ro = oracle_mll(bo, ds.y, th, Z, replay=[rec["iters_y"]] + rec["iters_q"])
+    check_record(rec, ro, bo, th)
+
+
+_C5 = {}
+
+
+def _c5_oracle_blocks(ds):
+    if "bo" not in _C5:
+        _C5["bo"] = OS.build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
+    return _C5["bo"]
+
+
+# ----------------------------------------------------------------------------- error paths
+def test_degenerate_reps_on_device(P, ctx):
+    """Identical representatives: K_rep = alpha 11^T has lambda_min = 0, so Eq. (26)'s
+    lambda_0 > 0 cannot hold: the build reports DEGENERATE_REPS (and the oracle's LAPACK value is
+    zero to rounding)."""
+    ds = synth.g_hyper(n_c=6, b=40, d=2, seed=21)
+    reps = np.repeat(ds.reps[:1], ds.n_c, axis=0)
+    with pytest.raises(P.NugprError) as e:
+        P.build_blocks(ctx, ds.X, ds.offsets, reps, ds.theta0)
+    assert e.value.name == "DEGENERATE_REPS"
+    lam = float(np.linalg.eigvalsh(np.full((ds.n_c, ds.n_c), ds.theta0[2]))[0])
+    assert abs(lam) < 1e-14 * ds.n_c
+
+
+def test_cg_not_converged_is_flagged(P, ctx):
+    """cg_max_iter = 1 on a case that needs more: nugpr_mll, the 7
+    concurrent numgrad evaluations and nugpr_train all return CG_NOT_CONVERGED; the record holds
+    the last iterate with converged = False and counts = 1."""
+    ds = synth.make_config("C1")
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0, eval_slots=7)
+    with pytest.raises(P.NugprError) as e:
+        P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=201, max_iter=1)
+    assert e.value.name == "CG_NOT_CONVERGED"
+    with pytest.raises(P.NugprError) as e:
+        P.numgrad(ctx, bg, ds.y, ds.theta0, probe_seed=201, max_iter=1)
+    assert e.value.name == "CG_NOT_CONVERGED"
+    with pytest.raises(P.NugprError) as e:
+        P.train(ctx, ds.X, ds.offsets, ds.reps, ds.y, ds.theta0, epochs=2, probe_seed=201, max_iter=1)
+    assert e.value.name == "CG_NOT_CONVERGED"
+    # the library still works afterwards (no stuck stream / graph state)
+    rec = P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=201)
+    assert rec["converged"]
+
+
+def test_breakdown_on_nonfinite_input(P, ctx):
+    """A NaN in y makes r^T r non-finite: the evaluation reports BREAKDOWN instead of a silently
+    'converged' NaN loss, and Adam refuses a non-finite gradient."""
+    ds = synth.make_config("C1")
+    bg = P.build_blocks(ctx, ds.X, ds.offsets, ds.reps, ds.theta0)
+    y = ds.y.copy()
+    y[17] = np.nan
+    with pytest.raises(P.NugprError) as e:
+        P.mll(ctx, bg, y, ds.theta0, probe_seed=201)
+    assert e.value.name == "BREAKDOWN"
+    with pytest.raises(P.NugprError) as e:
+        P.train(ctx, ds.X, ds.offsets, ds.reps, y, ds.theta0, epochs=1, probe_seed=201)
+    assert e.value.name == "BREAKDOWN"
+    rec = P.mll(ctx, bg, ds.y, ds.theta0, probe_seed=201)
+    assert rec["converged"] and not rec["breakdown"] and math.isfinite(rec["L"])

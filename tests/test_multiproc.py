@@ -100,3 +100,57 @@ def test_single_rank_exchange_needs_no_collective():
     L0, g = P.numgrad_exchange(ctx, THETA, STEP, [loss(p) for p in pts])
     assert L0 == loss(THETA)
     assert list(g) == [(loss(pts[1 + 2 * i]) - loss(pts[2 + 2 * i])) / (2.0 * h[i]) for i in range(3)]
+
+
+def _worker_fail(rank, world, port, q):
+    """Rank 1 reports a hard failure (NOT_SPD = 3) for the first evaluation it owns and
+    CG_NOT_CONVERGED (5) for another; every rank must return the same worst status together."""
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, root)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import paper_2510_12128_b200 as P
+        ctx = P.Context(-1, group=True)
+        owner = P.shard_plan(world, COSTS)
+        pts, _ = points()
+        L_mine = [loss(pts[k]) if owner[k] == rank else float("nan") for k in range(7)]
+        st = [0] * 7
+        mine = [k for k in range(7) if owner[k] == rank]
+        if rank == 1:
+            st[mine[-1]] = 5
+            st[mine[0]] = 3
+        try:
+            P.numgrad_exchange(ctx, THETA, STEP, L_mine, status_mine=st)
+            q.put((rank, None, "no error raised"))
+        except P.NugprError as e:
+            q.put((rank, e.name, None))
+    except Exception as e:  # noqa: BLE001
+        q.put((rank, None, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_failed_evaluation_fails_every_rank_together():
+    """a rank whose evaluation fails must not return before the PAR-1 exchange (the
+    others would wait forever in the allgather).  The statuses travel with the records, so every
+    rank returns the same error, the hard failure (NOT_SPD) winning over CG_NOT_CONVERGED."""
+    from paper_2510_12128_b200 import _native as N
+    if not os.path.exists(N.LIB_PATH):
+        from paper_2510_12128_b200 import build
+        build.build()
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_fail, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+    assert [r[2] for r in res] == [None, None], res
+    assert [r[1] for r in res] == ["NOT_SPD", "NOT_SPD"]

@@ -87,6 +87,54 @@ def test_cholesky_negative_definite_fails_and_singular_gets_jitter():
     np.testing.assert_allclose(R.T @ R, Ksing + eps * np.eye(4), atol=1e-12)
 
 
+def test_jitter_ladder_needs_exactly_t2():
+    """SPEC.md:125 ladder eps_t = 1e-8 mean(diag K) 10^t: a symmetric K whose smallest eigenvalue is
+    -10^1.5 base (base = 1e-8 mean diag) fails for t = 0, 1 (eps < |lambda_min|) and succeeds at
+    t = 2, so the returned jitter must be exactly base * 100 and R^T R = K + 100 base I."""
+    rng = np.random.default_rng(9)
+    n = 12
+    Q, _ = np.linalg.qr(rng.normal(size=(n, n)))
+    mu = np.linspace(1.0, 3.0, n)
+    base_guess = 1e-8 * np.mean(mu)
+    mu[0] = -(10 ** 1.5) * base_guess
+    K = (Q * mu) @ Q.T
+    K = 0.5 * (K + K.T)
+    base = 1e-8 * float(np.mean(np.diag(K)))            # = 1e-8 mean eig (trace invariance)
+    assert 10 * base < -mu[0] < 100 * base
+    with pytest.raises(np.linalg.LinAlgError):
+        np.linalg.cholesky(K + base * 10 * np.eye(n))     # t = 1 still fails
+    R, eps = chol_upper_with_jitter(K)
+    assert eps == base * 10.0 ** 2
+    np.testing.assert_allclose(R.T @ R, K + eps * np.eye(n), rtol=0, atol=1e-13)
+
+
+def test_scale_step_on_jittered_block_matches_dense():
+    """Eq. (25) scale step on a JITTERED block: the model's block is K_i + (sigma_0^2 + eps_i) I, so
+    the shortcut must use (sigma_0^2 + eps_i) r H (SURVEY §8(c) step 2 / DESIGN jitter reading).
+    Brute force: dense R^-T K''(theta') R^-1 with the jittered diagonal, entry by entry."""
+    rng = np.random.default_rng(12)
+    X = np.concatenate([np.zeros((6, 2)), rng.normal(size=(7, 2)) + 4.0, rng.normal(size=(5, 2)) - 4.0])
+    off = np.array([0, 6, 13, 18], dtype=np.int64)
+    reps = np.array([[0.0, 0.0], [4.0, 4.0], [-4.0, -4.0]])
+    th0 = (1.0, 1e-18, 1.0)                              # cluster 0: 6 identical points -> singular
+    b = build_blocks(X, off, reps, th0)
+    assert b.jitter[0] > 0 and b.jitter[1] == 0 and b.jitter[2] == 0
+    ds = synth.Dataset(X=X, y=np.zeros(18), offsets=off, reps=reps, theta0=th0)
+    V = rng.normal(size=(18, 3))
+    Rinv = np.linalg.inv(dense_R(b))
+    for r in (0.5, -0.3):
+        th = (th0[0], th0[1], th0[2] * (1 + r))
+        op = Operator(b, th)
+        assert op.mode == "scale"
+        A = Rinv.T @ _brute_K(ds, th, b) @ Rinv
+        # tolerance: the jittered block has cond ~ 6 alpha / eps_0 ~ 1e8, so both routes carry
+        # ~cond x 1e-16 = 1e-8 rounding; the eps-dropping mistake below is 1e6 times larger
+        np.testing.assert_allclose(op.apply(V), A @ V, rtol=1e-6, atol=1e-6 * np.abs(A @ V).max())
+        # dropping eps_i from the shortcut would be a gross error here (eps_i H ~ I on that block)
+        wrong = (1 + r) * V[:6] - th0[1] * r * np.linalg.solve(b.R[0], np.linalg.solve(b.R[0].T, V[:6]))
+        assert np.abs(wrong - op.apply(V)[:6]).max() > 0.01
+
+
 def test_build_blocks_invariants():
     ds = small(4, 15, 3)
     b = build_blocks(ds.X, ds.offsets, ds.reps, ds.theta0)
