@@ -177,11 +177,8 @@ nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
  *  NUGPR_OPT_GRAPHS [1]: each evaluation's CG loop runs as ONE CUDA graph whose conditional WHILE node
  *    is driven by the device (no host round trip per iteration); 0: the same kernels launched directly
  *    with a host poll of the activity flag every 4 iterations (profiling with ncu, which cannot see
- *    kernels inside conditional graphs).  Both give bit-identical results.
- *  NUGPR_OPT_BATCH [0]: NEXT-3 cross-perturbation batching — nugpr_numgrad runs its noise- and
- *    scale-step evaluations (all four apply the same H, Eq. 24-25) in lockstep so every block apply
- *    streams H once for all of them.  Same records as unbatched, to FP64 rounding. */
-typedef enum { NUGPR_OPT_GRAPHS = 0, NUGPR_OPT_BATCH = 1 } nugpr_option;
+ *    kernels inside conditional graphs).  Both give bit-identical results. */
+typedef enum { NUGPR_OPT_GRAPHS = 0 } nugpr_option;
 nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value);
 
 /* Kernel-class profiler (bench.py's live roofline): when enabled, CUDA events are recorded on

@@ -169,8 +169,7 @@ class Context:
             return 1
 
     def set_option(self, name: str, value):
-        """nugpr_ctx_set_option: 'graphs' (CG loop as a device-driven CUDA graph, default True) or
-        'batch' (NEXT-3 cross-perturbation batching in numgrad, default False)."""
+        """nugpr_ctx_set_option: 'graphs' (CG loop as a device-driven CUDA graph, default True)."""
         N.check(N.lib().nugpr_ctx_set_option(self.handle, N.OPTIONS[name], int(value)))
 
     def set_profiling(self, enable: bool = True):

@@ -21,7 +21,7 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "DEGENERATE_RE
 KERNELS = {"rbf": 0, "matern52": 1, "rbf_as_printed": 2}
 REP_MODES = {"given": 0, "centroid": 1, "medoid": 2}
 MODES = {0: "baseline", 1: "noise", 2: "scale", 3: "generic"}
-OPTIONS = {"graphs": 0, "batch": 1}
+OPTIONS = {"graphs": 0}
 PROF_CLASSES = {"apply_B": 0, "apply_lowrank": 1, "update": 2, "rhs": 3, "gemm": 4, "chol": 5,
                 "lanczos": 6, "other": 7}
 

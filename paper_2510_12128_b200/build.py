@@ -19,7 +19,8 @@ ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libnugpr.so")
-SOURCES = ["api.cu", "build_kernels.cu", "eval_kernels.cu", "cluster_kernels.cu", "big_kernels.cu", "predict_kernels.cu"]
+SOURCES = ["api.cu", "build_kernels.cu", "eval_kernels.cu", "apply_kernels.cu", "cluster_kernels.cu", "big_kernels.cu",
+           "predict_kernels.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
          "--expt-relaxed-constexpr", f"-I{INCLUDE}", f"-I{CSRC}"]

@@ -66,11 +66,79 @@ struct HostLayout {
   int n_c = 0, d = 0;
   bool big = false;
   int64_t n = 0, n_pad = 0, blk_total = 0;
+  int64_t pk_total = 0;           // packed symmetric storage of H / G (small layout): 64 sum tri(mt_i)
   int ld_max = 0;
-  std::vector<int64_t> off, poff, boff;
-  std::vector<int32_t> ld, tile0, ctask0;
-  std::vector<TileDesc> tiles, ctasks;
+  std::vector<int64_t> off, poff, boff, pboff;
+  std::vector<int32_t> ld, tile0;
+  std::vector<TileDesc> tiles;
+  // packed-apply partition (small layout): pieces of the packed stream per CTA, split scratch
+  std::vector<SegDesc> segs;
+  std::vector<int32_t> seg0;
+  int seg_max = 0, n_split = 0;
+  int64_t split_doubles = 0;
 };
+
+// Cut the packed tile stream of all clusters (blocks in storage order, cluster after cluster) into at
+// most PACK_CTAS pieces of (nearly) equal tile count at block boundaries; a block goes to the CTA
+// whose range holds its midpoint.  Clusters may span several CTAs (<= MAX_PARTS; the target
+// grows until that holds).  The partition depends only on the offsets (not on the device).
+static void make_partition(HostLayout& L) {
+  const int n_c = L.n_c;
+  int64_t total = 0;
+  for (int i = 0; i < n_c; ++i) total += tri_tiles(L.ld[i] / 8);
+  int G = static_cast<int>(std::min<int64_t>(PACK_CTAS, std::max<int64_t>(1, total / 64)));
+  for (;; G = std::max(1, G * 3 / 4)) {
+    L.segs.clear();
+    L.seg0.clear();
+    std::vector<int> parts(n_c, 0);
+    int64_t cum = 0;
+    int cur = -1;
+    for (int i = 0; i < n_c; ++i) {
+      const int mt = L.ld[i] / 8, ns = pk_ns(mt);
+      int bi = 0;
+      for (int sb = 0; sb < ns; ++sb)
+        for (int gb = sb; gb < ns; ++gb, ++bi) {
+          const int64_t len = pk_blk_size(gb, sb, mt);
+          const int cta = static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + len) * G / (2 * total)));
+          if (cta != cur) {                          // a new CTA starts here
+            L.seg0.push_back(static_cast<int32_t>(L.segs.size()));
+            cur = cta;
+            L.segs.push_back(SegDesc{i, bi, bi + 1, parts[i]++, 0, -1, 0});
+          } else if (L.segs.back().blk != i) {       // same CTA, next cluster
+            L.segs.push_back(SegDesc{i, bi, bi + 1, parts[i]++, 0, -1, 0});
+          } else {
+            L.segs.back().k1 = bi + 1;
+          }
+          cum += len;
+        }
+    }
+    L.seg0.push_back(static_cast<int32_t>(L.segs.size()));
+    int pmax = 0;
+    for (int i = 0; i < n_c; ++i) pmax = std::max(pmax, parts[i]);
+    if (pmax <= MAX_PARTS || G == 1) {
+      // split scratch: nparts_i x ld_i x 17 doubles per split cluster (17 = y + 16 probe slots)
+      L.n_split = 0;
+      L.split_doubles = 0;
+      std::vector<int> tick(n_c, -1);
+      std::vector<int64_t> sp(n_c, 0);
+      for (int i = 0; i < n_c; ++i) {
+        if (parts[i] > 1) {
+          tick[i] = L.n_split++;
+          sp[i] = L.split_doubles;
+          L.split_doubles += static_cast<int64_t>(parts[i]) * L.ld[i] * 17;
+        }
+      }
+      for (SegDesc& sd : L.segs) {
+        sd.nparts = parts[sd.blk];
+        sd.tick = tick[sd.blk];
+        sd.spoff = sp[sd.blk];
+      }
+      L.seg_max = 0;
+      for (size_t b = 0; b + 1 < L.seg0.size(); ++b) L.seg_max = std::max(L.seg_max, L.seg0[b + 1] - L.seg0[b]);
+      return;
+    }
+  }
+}
 
 nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) {
   if (!offsets) return fail(NUGPR_ERR_INVALID_ARG, "offsets is NULL");
@@ -87,9 +155,10 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
   const int tile_rows = L.big ? 64 : TILE_ROWS;
   L.poff.resize(n_c + 1);
   L.boff.resize(n_c);
+  L.pboff.resize(n_c);
   L.ld.resize(n_c);
   L.tile0.resize(n_c + 1);
-  int64_t pp = 0, bb = 0;
+  int64_t pp = 0, bb = 0, pk = 0;
   for (int i = 0; i < n_c; ++i) {
     int64_t b = offsets[i + 1] - offsets[i];
     if (b <= 0) return fail(NUGPR_ERR_SHAPE, "offsets must be strictly increasing (cluster %d empty)", i);
@@ -101,6 +170,7 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
     L.ld_max = std::max<int>(L.ld_max, static_cast<int>(ld));
     L.poff[i] = pp;
     L.boff[i] = bb;
+    L.pboff[i] = pk;
     L.tile0[i] = static_cast<int32_t>(L.tiles.size());
     for (int r0 = 0; r0 < ld; r0 += tile_rows) {
       TileDesc t;
@@ -112,26 +182,15 @@ nugpr_status make_layout(const int64_t* offsets, int n_c, int d, HostLayout& L) 
     }
     pp += ld;
     bb += ld * ld;
+    pk += 64 * tri_tiles(static_cast<int>(ld / 8));
   }
   L.poff[n_c] = pp;
   L.tile0[n_c] = static_cast<int32_t>(L.tiles.size());
-  // column tasks of the DMMA column apply: CTW columns (= rows of the symmetric block)
-  L.ctask0.resize(n_c + 1);
-  for (int i = 0; i < n_c; ++i) {
-    L.ctask0[i] = static_cast<int32_t>(L.ctasks.size());
-    for (int c0 = 0; c0 < L.ld[i]; c0 += CTW) {
-      TileDesc t;
-      t.blk = i;
-      t.row0 = c0;
-      t.nrows = std::min(CTW, L.ld[i] - c0);
-      t.pad_ = 0;
-      L.ctasks.push_back(t);
-    }
-  }
-  L.ctask0[n_c] = static_cast<int32_t>(L.ctasks.size());
   L.n = offsets[n_c];
   L.n_pad = pp;
   L.blk_total = bb;
+  L.pk_total = pk;
+  if (!L.big) make_partition(L);
   return NUGPR_OK;
 }
 
@@ -168,15 +227,20 @@ struct EvalDev {
   double* ah = nullptr, *bh = nullptr, *slqw = nullptr;
   double* Tbuf = nullptr;     // n_c x MAXC
   double* xs = nullptr, *xr = nullptr;   // PAR-2 exchange send / recv: [3][n_c_global][MAXC] each
+  double* split = nullptr;               // packed apply: partial products of split clusters
+  unsigned int* split_tick = nullptr;    // and their tickets (self-resetting)
 };
 
 struct BlocksDev {
   int64_t* off = nullptr, *poff = nullptr, *boff = nullptr;
-  int32_t* ld = nullptr, *tile0 = nullptr, *list = nullptr, *status = nullptr, *ctask0 = nullptr;
-  TileDesc* tiles = nullptr, *ctasks = nullptr;
+  int32_t* ld = nullptr, *tile0 = nullptr, *list = nullptr, *status = nullptr, *seg0 = nullptr;
+  int64_t* pboff = nullptr;
+  TileDesc* tiles = nullptr;
+  SegDesc* segs = nullptr;
   double* X = nullptr, *reps = nullptr;
-  double* Linv = nullptr, *H = nullptr;
-  float* H32 = nullptr;       // FP32-stored H (NUGPR_BLOCKS_F32)
+  double* Linv = nullptr;     // R_i^{-T}, full ld_i x ld_i (boff)
+  double* H = nullptr;        // H_i = Linv_i Linv_i^T: packed (pboff) in the small layout, full (boff) when big
+  float* H32 = nullptr;       // FP32-stored H (NUGPR_BLOCKS_F32), same layout as H
   double* u = nullptr, *jitter = nullptr, *logdet_blk = nullptr;
   double* scal = nullptr;     // [0] logdet_R, [1] lam0
   double* Krep = nullptr, *M = nullptr, *v0 = nullptr, *lz = nullptr;
@@ -209,13 +273,15 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
   B.list = c.take<int32_t>(n_c);
   B.status = c.take<int32_t>(n_c);
   B.tiles = c.take<TileDesc>(nt);
-  B.ctasks = c.take<TileDesc>(L.ctasks.size());
-  B.ctask0 = c.take<int32_t>(n_c + 1);
+  B.pboff = c.take<int64_t>(n_c);
+  B.segs = c.take<SegDesc>(std::max<size_t>(1, L.segs.size()));
+  B.seg0 = c.take<int32_t>(std::max<size_t>(1, L.seg0.size()));
   B.X = c.take<double>(static_cast<size_t>(L.n) * L.d);
   B.reps = c.take<double>(static_cast<size_t>(n_cg) * L.d);
   B.Linv = c.take<double>(L.blk_total);
-  B.H = c.take<double>(L.blk_total);
-  B.H32 = reinterpret_cast<float*>(c.take<double>((L.blk_total + 1) / 2));
+  const int64_t hsize = L.big ? L.blk_total : L.pk_total;     // stored H / G elements
+  B.H = c.take<double>(hsize);
+  B.H32 = reinterpret_cast<float*>(c.take<double>((hsize + 1) / 2));
   B.u = c.take<double>(L.n_pad);
   B.jitter = c.take<double>(n_c);
   B.logdet_blk = c.take<double>(n_c);
@@ -258,10 +324,9 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.SR = c.take<double>(nt * MAXC);
     e.SPb[0] = c.take<double>(std::max<int64_t>(nt, n_cg) * MAXC);   // S(P): global under PAR-2
     e.SPb[1] = c.take<double>(std::max<int64_t>(nt, n_cg) * MAXC);
-    const int64_t npart = std::max<int64_t>(nt, static_cast<int64_t>(L.ctasks.size()));   // per tile or per column task
-    e.SV = c.take<double>(npart * MAXC);
+    e.SV = c.take<double>(nt * MAXC);
     e.SX = c.take<double>(nt * MAXC);
-    e.dots = c.take<double>(npart * MAXC);
+    e.dots = c.take<double>(nt * MAXC);
     e.rrp = c.take<double>(nt * MAXC);
     e.prm = c.take<EvalParams>(1);
     e.st = c.take<CGState>(1);
@@ -272,6 +337,8 @@ void carve_all(Carver& c, const HostLayout& L, int slots, BlocksDev& B, std::vec
     e.Tbuf = c.take<double>(static_cast<size_t>(n_c) * MAXC);
     e.xs = c.take<double>(static_cast<size_t>(3) * n_cg * MAXC);
     e.xr = c.take<double>(static_cast<size_t>(3) * n_cg * MAXC);
+    e.split = c.take<double>(std::max<int64_t>(1, L.split_doubles));
+    e.split_tick = c.take<unsigned int>(std::max(1, L.n_split));
   }
 }
 
@@ -316,7 +383,6 @@ struct nugpr_ctx {
   cudaEvent_t ev_aux[NUGPR_NUM_EVALS + 1][2] = {{nullptr}};
   EvalParams* h_prm = nullptr;           // pinned [MAX_STAGE]
   bool use_graphs = true;                // NUGPR_OPT_GRAPHS
-  bool batch = false;                    // NUGPR_OPT_BATCH (NEXT-3)
   // nugpr_train's deferred build: H_i = Linv_i Linv_i^T on its own stream, overlapping the
   // evaluations that do not read H (baseline, lengthscale steps); ev_h1 marks it done
   cudaStream_t h_stream = nullptr;
@@ -400,7 +466,6 @@ struct nugpr_blocks {
   const double* last_probes = nullptr;
   bool cy_ready = false;      // B.cy holds c = R^{-T} y for the current numgrad call
   const void* ws_base = nullptr;
-  bool pnew = false;          // the CG iteration launches pnew_kernel (launch accounting)
   bool f32 = false;           // current evaluation streams FP32-stored blocks
   bool h32_ready = false;     // H32 holds the FP32 copy of H
   bool h_pending = false;     // H is being formed on ctx->h_stream (wait on ctx->ev_h1 before reading it)
@@ -462,7 +527,6 @@ nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value)
   if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
   switch (option) {
     case NUGPR_OPT_GRAPHS: ctx->use_graphs = value != 0; return NUGPR_OK;
-    case NUGPR_OPT_BATCH: ctx->batch = value != 0; return NUGPR_OK;
     default: return fail(NUGPR_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }
@@ -723,7 +787,8 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   LayoutDev& Ld = bl->Ld;
   Ld.off = B.off; Ld.poff = B.poff; Ld.boff = B.boff; Ld.ld = B.ld; Ld.tiles = B.tiles;
   Ld.tile0 = B.tile0; Ld.n_c = nl; Ld.n_tiles = static_cast<int32_t>(L.tiles.size());
-  Ld.ctasks = B.ctasks; Ld.ctask0 = B.ctask0; Ld.n_ctasks = static_cast<int32_t>(L.ctasks.size());
+  Ld.pboff = B.pboff; Ld.segs = B.segs; Ld.seg0 = B.seg0;
+  Ld.n_seg_ctas = L.seg0.empty() ? 0 : static_cast<int32_t>(L.seg0.size() - 1); Ld.seg_max = L.seg_max;
   Ld.n = L.n; Ld.n_pad = L.n_pad;
 #define CKB(call) do { cudaError_t e_ = (call); if (e_ != cudaSuccess) { delete bl; \
     return fail(NUGPR_ERR_CUDA, "%s: %s", #call, cudaGetErrorString(e_)); } } while (0)
@@ -734,14 +799,18 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
     CKB(cudaMemcpyAsync(B.ld, L.ld.data(), sizeof(int32_t) * nl, cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(B.tile0, L.tile0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
     CKB(cudaMemcpyAsync(B.tiles, L.tiles.data(), sizeof(TileDesc) * L.tiles.size(), cudaMemcpyHostToDevice, s));
-    CKB(cudaMemcpyAsync(B.ctasks, L.ctasks.data(), sizeof(TileDesc) * L.ctasks.size(), cudaMemcpyHostToDevice, s));
-    CKB(cudaMemcpyAsync(B.ctask0, L.ctask0.data(), sizeof(int32_t) * (nl + 1), cudaMemcpyHostToDevice, s));
+    CKB(cudaMemcpyAsync(B.pboff, L.pboff.data(), sizeof(int64_t) * nl, cudaMemcpyHostToDevice, s));
+    if (!L.segs.empty()) {
+      CKB(cudaMemcpyAsync(B.segs, L.segs.data(), sizeof(SegDesc) * L.segs.size(), cudaMemcpyHostToDevice, s));
+      CKB(cudaMemcpyAsync(B.seg0, L.seg0.data(), sizeof(int32_t) * L.seg0.size(), cudaMemcpyHostToDevice, s));
+    }
     CKB(cudaMemcpyAsync(B.X, X_sorted + static_cast<size_t>(bl->pos0) * d, sizeof(double) * L.n * d, cudaMemcpyDefault, s));
     CKB(cudaMemcpyAsync(B.reps, reps, sizeof(double) * n_c * d, cudaMemcpyDefault, s));
     for (EvalDev& ev : bl->E) {
       const size_t np = static_cast<size_t>(L.tiles.size()) * MAXC * sizeof(double);
       for (double* p : {ev.SR, ev.SPb[0], ev.SPb[1], ev.SV, ev.SX, ev.dots, ev.rrp}) CKB(cudaMemsetAsync(p, 0, np, s));
       CKB(cudaMemsetAsync(ev.st, 0, sizeof(CGState), s));
+      CKB(cudaMemsetAsync(ev.split_tick, 0, sizeof(unsigned int) * std::max(1, L.n_split), s));
     }
   }
   CKB(cudaMemsetAsync(B.jitter, 0, sizeof(double) * nl, s));
@@ -835,11 +904,11 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
     if (!ctx->ev_h1) CKB(cudaEventCreateWithFlags(&ctx->ev_h1, cudaEventDisableTiming));
     CKB(cudaEventRecord(ctx->ev_h0, s));
     CKB(cudaStreamWaitEvent(ctx->h_stream, ctx->ev_h0, 0));
-    launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, ctx->h_stream);
+    launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, !L.big, ctx->h_stream);
     CKB(cudaEventRecord(ctx->ev_h1, ctx->h_stream));
     bl->h_pending = true;
   } else {
-    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, s));
+    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_H(B.Linv, B.H, Ld, L.ld_max, !L.big, s));
   }
   if (shard) {
     // logdet_R = 2 sum_i sum_j log (R_i)_jj over ALL clusters: gather the per-cluster terms, then the
@@ -902,8 +971,27 @@ extern "C" nugpr_status nugpr_blocks_export(const nugpr_blocks* bl, int32_t what
     case 1: {
       size_t n = sizeof(double) * L.blk_total;
       if (!need(n)) return fail(NUGPR_ERR_INVALID_ARG, "need %zu bytes", n);
-      CK(cudaMemcpyAsync(dst, what == 0 ? bl->B.Linv : bl->B.H, n, cudaMemcpyDeviceToHost, s));
-      break;
+      if (what == 0 || L.big) {
+        CK(cudaMemcpyAsync(dst, what == 0 ? bl->B.Linv : bl->B.H, n, cudaMemcpyDeviceToHost, s));
+        break;
+      }
+      // H in the small layout is stored packed: expand to full ld_i x ld_i column-major blocks
+      std::vector<double> pk(L.pk_total);
+      CK(cudaMemcpyAsync(pk.data(), bl->B.H, sizeof(double) * L.pk_total, cudaMemcpyDeviceToHost, s));
+      CK(cudaStreamSynchronize(s));
+      double* o = static_cast<double*>(dst);
+      for (int i = 0; i < L.n_c; ++i) {
+        const int ld = L.ld[i], mt = ld / 8;
+        const double* bp = pk.data() + L.pboff[i];
+        double* ob = o + L.boff[i];
+        for (int c = 0; c < ld; ++c)
+          for (int r = 0; r < ld; ++r) {
+            const int rr = std::max(r, c), cc = std::min(r, c);
+            const int I = rr / 8, K = cc / 8;
+            ob[static_cast<int64_t>(c) * ld + r] = bp[static_cast<int64_t>(pk_tile(I, K, mt)) * 64 + swz(rr % 8, cc % 8)];
+          }
+      }
+      return NUGPR_OK;
     }
     case 2: {
       size_t n = sizeof(double) * L.n;
@@ -1123,94 +1211,67 @@ extern "C" nugpr_status nugpr_cluster(nugpr_ctx* ctx, const double* X, int64_t n
 
 struct IterArgs {
   ApplyArgs a1, a2, a3, a4;
-  LowrankArgs t1, t2, t3, t4;
+  LowrankArgs t1, t2, t3, t4;   // big-block layout only: T = M'S before each apply
   UpdateArgs ua;
   int ncp = 0;
-  bool pnew = false;       // launch pnew_kernel before apply 1
-  const CGState* st = nullptr;
-  const double* R = nullptr;
-  double* Pb[2] = {nullptr, nullptr};
-  int64_t n_pad = 0;
+  bool lowrank = false;         // separate low-rank launches (big-block layout)
   int ncol = 0;
-  bool mbcg = false;       // NEXT-4: one apply per iteration (CG on A for every column)
+  bool mbcg = false;            // NEXT-4: one apply per iteration (CG on A for every column)
 };
 
+// Launch arguments of one evaluation's CG iteration and trace tail (slot e, ncol RHS columns).
+//  apply 1: V = A p with p = r + beta p fused (P_new written), epilogue S(V)
+//  apply 2: q = A V + 4 V + p (probe columns: Q(A) p), q = V (y column); dots p^T q -> alpha
+//  update : x += alpha p, r -= alpha q; r^T r and S(r) -> beta, freezing, the graph's while condition
+//  trace  : V = A x (S(V)), U = 3 A V - 3 x (probe columns: P(A) x, Eq. 10) / x (y column), dotted with
+//           the right-hand sides -> t_j and quad (FIN_TRACE)
+// The packed apply forms the low-rank rows M'S(D) itself from the S rows its input's producer wrote
+// (S_D); the big-block layout keeps a lowrank_kernel launch before each apply.
 static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterArgs& A, bool mbcg = false) {
   const HostLayout& L = bl->L;
   const LayoutDev& Ld = bl->Ld;
   const BlocksDev& B = bl->B;
   A.ncp = (ncol + 1) & ~1;
+  A.ncol = ncol;
+  A.lowrank = L.big;
   ApplyArgs& a1 = A.a1;
   memset(&a1, 0, sizeof(a1));
   a1.L = Ld; a1.prm = e.prm; a1.st = e.st; a1.u = B.u; a1.jitter = B.jitter; a1.ncol = ncol;
   a1.Pbuf[0] = e.Pb[0]; a1.Pbuf[1] = e.Pb[1]; a1.SPbuf[0] = e.SPb[0]; a1.SPbuf[1] = e.SPb[1];
   a1.alpha_hist = e.ah; a1.hist_stride = HIST;
   a1.ld_max = L.ld_max;
+  a1.lr_row0 = 0; a1.lr_nc = L.n_c;
+  a1.Tbuf = e.Tbuf;
+  a1.split_part = e.split; a1.split_ticket = e.split_tick;
   if (L.big) {
     a1.big = 1;
     a1.grid = Ld.n_tiles;
-    a1.Tbuf = e.Tbuf;
   } else {
-    const int ld_min = *std::min_element(L.ld.begin(), L.ld.end());
-    const ApplyPlan pl = plan_apply(A.ncp, ncol, L.ld_max, ld_min, Ld.n_tiles, apply_grid(Ld.n_tiles), Ld.n_ctasks);
-    if (!pl.ok) return fail(NUGPR_ERR_SHAPE, "apply kernel does not fit shared memory (ld_max=%d, ncol=%d)", L.ld_max, ncol);
-    a1.slot_doubles = pl.slot_doubles;
-    a1.red_doubles = pl.red_doubles;
-    a1.nstage = pl.nstage;
-    a1.nmine_max = pl.nmine_max;
-    a1.Tbuf = e.Tbuf;
-    a1.smem_b = pl.smem_b;
-    a1.smem_nob = pl.smem_nob;
-    a1.grid = pl.grid;
-    const char* dbg = getenv("NUGPR_APPLY_DBG");
-    a1.dbg = dbg ? atoi(dbg) : 0;
-    a1.mma = pl.mma;
-    a1.lds = pl.lds;
-    a1.nw = pl.nw;
-    a1.dstride = pl.dstride;
-    a1.dbuf = pl.dbuf;
-    if (bl->f32) {
-      if (pl.mma != 1) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs the m = 8 DMMA apply");
-      a1.f32 = 1;
-    }
+    if (!plan_packed_apply(L.ld_max, ncol, bl->f32, L.seg_max, a1))
+      return fail(NUGPR_ERR_SHAPE, "packed apply does not fit shared memory (ld_max=%d, ncol=%d, pieces/CTA=%d)",
+                  L.ld_max, ncol, L.seg_max);
+    a1.grid = Ld.n_seg_ctas;
   }
   ApplyArgs& a2 = A.a2;
   a2 = a1;
-  // apply 1: V = A p, p = r + beta p (fused), epilogue S(V)
   a1.D = e.R; a1.S_D = e.SR; a1.fuse_p = 1; a1.out = e.V; a1.epi = EPI_S; a1.Sout = e.SV;
   a1.fin = FIN_NONE; a1.gate = 1;
   for (int c = 0; c < MAXC; ++c) { a1.cA[c] = 1.0; a1.cV[c] = 0.0; a1.cP[c] = 0.0; }
-  // apply 2: q = A V + 4 V + p (probe columns), q = V (y column); p^T q partials -> alpha
   a2.D = e.V; a2.S_D = e.SV; a2.fuse_p = 0; a2.out = e.Q; a2.use_par_p2 = 1; a2.epi = EPI_DOT;
   a2.dots = e.dots; a2.fin = FIN_ALPHA; a2.gate = 1;
   for (int c = 0; c < MAXC; ++c) {
     if (c == 0) { a2.cA[c] = 0.0; a2.cV[c] = 1.0; a2.cP[c] = 0.0; }
     else { a2.cA[c] = 1.0; a2.cV[c] = 4.0; a2.cP[c] = 1.0; }
   }
-  // (with use_par_p2 the kernel takes both the combine term P2 and the dot partner Y2 from
-  //  the parity-resolved current direction P[par^1])
   UpdateArgs& ua = A.ua;
   memset(&ua, 0, sizeof(ua));
   ua.L = Ld; ua.prm = e.prm; ua.st = e.st; ua.u = B.u; ua.X = e.X; ua.R = e.R; ua.Q = e.Q;
   ua.Pbuf[0] = e.Pb[0]; ua.Pbuf[1] = e.Pb[1]; ua.rr_part = e.rrp; ua.SR_part = e.SR;
   ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol; ua.cond = 0;
-  LowrankArgs& t1 = A.t1;
-  memset(&t1, 0, sizeof(t1));
-  t1.task0 = nullptr;
-  t1.st = e.st; t1.prm = e.prm; t1.Mp = nullptr; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
-  t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
-  t1.row0 = 0; t1.nrows = L.n_c;
-  LowrankArgs& t2 = A.t2;
-  t2 = t1;
-  t2.S = e.SV; t2.fuse_p = 0;
-  // trace: V = A X, U = 3 A V - 3 X (probe cols) / X (y col), dotted with RHS
   ApplyArgs& a3 = A.a3;
   a3 = a1;
   a3.D = e.X; a3.S_D = e.SX; a3.fuse_p = 0; a3.out = e.V; a3.epi = EPI_S; a3.Sout = e.SV;
   a3.fin = FIN_NONE; a3.gate = 0; a3.use_par_p2 = 0; a3.P2 = nullptr;
-  LowrankArgs& t3 = A.t3;
-  t3 = t2;
-  t3.S = e.SX; t3.gate = 0;
   ApplyArgs& a4 = A.a4;
   a4 = a3;
   a4.D = e.V; a4.S_D = e.SV; a4.out = e.U; a4.P2 = e.X; a4.epi = EPI_DOT; a4.Y2 = e.RHS; a4.dots = e.dots;
@@ -1219,79 +1280,67 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     if (c == 0) { a4.cA[c] = 0.0; a4.cV[c] = 0.0; a4.cP[c] = 1.0; }
     else { a4.cA[c] = 3.0; a4.cV[c] = 0.0; a4.cP[c] = -3.0; }
   }
-  LowrankArgs& t4 = A.t4;
-  t4 = t2;
-  t4.S = e.SV; t4.gate = 0;
-  if (a1.mma == 3) {
-    // column-task apply: P_new is formed by pnew_kernel before apply 1; the apply outputs'
-    // S / dot partials are per column task
-    A.pnew = true;
-    A.a1.fuse_p = 0;
-    A.a1.d_is_pnew = 1;
-    A.t2.task0 = bl->B.ctask0;
-    A.t4.task0 = bl->B.ctask0;
-  }
-  if (L.big) {                                   // S partials are per 64-row tile
-    A.t1.task0 = bl->B.tile0; A.t2.task0 = bl->B.tile0; A.t3.task0 = bl->B.tile0; A.t4.task0 = bl->B.tile0;
-  }
   if (mbcg) {
     // NEXT-4 (mBCG on A): apply 1 alone per iteration, q = A p for every column, its dots with the
-    // freshly formed p (Y2 := P_new by parity) -> alpha; no Q(A) second apply, no Pade tail
+    // freshly formed p (Y2 := D = P_new) -> alpha; no Q(A) second apply, no Pade tail
     A.mbcg = true;
-    A.a1.out = e.Q; A.a1.epi = EPI_DOT; A.a1.Sout = nullptr; A.a1.use_par_p2 = 2; A.a1.P2 = nullptr;
-    A.a1.dots = e.dots; A.a1.fin = FIN_ALPHA;
-    for (int c = 0; c < MAXC; ++c) { A.a1.cA[c] = 1.0; A.a1.cV[c] = 0.0; A.a1.cP[c] = 0.0; }
-    if (A.pnew) A.t1.task0 = nullptr;
+    a1.out = e.Q; a1.epi = EPI_DOT; a1.Sout = nullptr; a1.use_par_p2 = 2; a1.P2 = nullptr;
+    a1.dots = e.dots; a1.fin = FIN_ALPHA;
   }
+  // big-block layout: separate low-rank launches, S partials per 64-row tile (summed via tile0)
+  LowrankArgs& t1 = A.t1;
+  memset(&t1, 0, sizeof(t1));
+  t1.task0 = L.big ? B.tile0 : nullptr;
+  t1.st = e.st; t1.prm = e.prm; t1.Mp = nullptr; t1.S = e.SR; t1.SPbuf[0] = e.SPb[0]; t1.SPbuf[1] = e.SPb[1];
+  t1.fuse_p = 1; t1.T = e.Tbuf; t1.n_c = L.n_c; t1.ncol = ncol; t1.gate = 1;
+  t1.row0 = 0; t1.nrows = L.n_c;
+  A.t2 = t1; A.t2.S = e.SV; A.t2.fuse_p = 0;
+  A.t3 = A.t2; A.t3.S = e.SX; A.t3.gate = 0;
+  A.t4 = A.t2; A.t4.S = e.SV; A.t4.gate = 0;
   if (bl->shard) {
     // PAR-2: the partials of this rank's clusters go to their global slots of the zero-padded send
     // array xs = [rr | S(r) | S(A p), p^T q, S(x), trace dots] ([3][n_cg][MAXC]); the exchange fills
-    // xr with every rank's; finalisers run as fin_kernel after it; T = M'S for the local rows only
-    if (A.pnew || mbcg || L.big)
-      return fail(NUGPR_ERR_UNSUPPORTED, "cluster sharding: column-task apply / mBCG / big blocks not supported");
+    // xr with every rank's; finalisers run as fin_kernel after it; the apply reads the GLOBAL S rows
+    // and forms M'S for its local rows only (lr_row0 = c_lo)
+    if (mbcg || L.big)
+      return fail(NUGPR_ERR_UNSUPPORTED, "cluster sharding: mBCG / big blocks not supported");
     const size_t G = static_cast<size_t>(bl->n_cg) * MAXC, o = static_cast<size_t>(bl->c_lo) * MAXC;
-    A.a1.Sout = e.xs + 2 * G + o;
-    A.a2.dots = e.xs + 2 * G + o; A.a2.fin = FIN_NONE;
-    A.a3.Sout = e.xs + 2 * G + o;
-    A.a4.dots = e.xs + 2 * G + o; A.a4.fin = FIN_NONE;
-    A.ua.rr_part = e.xs + o; A.ua.SR_part = e.xs + G + o; A.ua.nofin = 1;
-    A.t1.S = e.xr + G;
-    A.t2.S = e.xr + 2 * G;
-    A.t3.S = e.xr + 2 * G;
-    A.t4.S = e.xr + 2 * G;
-    for (LowrankArgs* t : {&A.t1, &A.t2, &A.t3, &A.t4}) { t->n_c = bl->n_cg; t->row0 = bl->c_lo; t->nrows = L.n_c; }
+    a1.Sout = e.xs + 2 * G + o;
+    a2.dots = e.xs + 2 * G + o; a2.fin = FIN_NONE;
+    a3.Sout = e.xs + 2 * G + o;
+    a4.dots = e.xs + 2 * G + o; a4.fin = FIN_NONE;
+    ua.rr_part = e.xs + o; ua.SR_part = e.xs + G + o; ua.nofin = 1;
+    a1.S_D = e.xr + G;
+    a2.S_D = e.xr + 2 * G;
+    a3.S_D = e.xr + 2 * G;
+    a4.S_D = e.xr + 2 * G;
+    for (ApplyArgs* x : {&a1, &a2, &a3, &a4}) { x->lr_row0 = bl->c_lo; x->lr_nc = bl->n_cg; }
   }
-  bl->pnew = A.pnew;
-  A.st = e.st; A.R = e.R; A.Pb[0] = e.Pb[0]; A.Pb[1] = e.Pb[1]; A.n_pad = L.n_pad; A.ncol = ncol;
   return NUGPR_OK;
 }
 
-// Direct launches of one CG iteration / the tail (useB selects the apply's smem variant).
-static void launch_iteration(const IterArgs& A, bool useB, cudaStream_t s) {
-  launch_lowrank(A.t1, A.ncp, s);
-  if (A.pnew) launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s);
-  launch_apply(A.a1, A.ncp, useB, s);
+// Direct launches of one CG iteration / the trace tail.
+static void launch_iteration(const IterArgs& A, cudaStream_t s) {
+  if (A.lowrank) launch_lowrank(A.t1, A.ncp, s);
+  launch_apply(A.a1, A.ncp, s);
   if (A.mbcg) { launch_update(A.ua, A.ncp, s); return; }
-  launch_lowrank(A.t2, A.ncp, s);
-  launch_apply(A.a2, A.ncp, useB, s);
+  if (A.lowrank) launch_lowrank(A.t2, A.ncp, s);
+  launch_apply(A.a2, A.ncp, s);
   launch_update(A.ua, A.ncp, s);
 }
-// tail + final kernel; mBCG: quad = c^T x partials (no Pade trace applies)
-static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol,
-                              int logdet_mode, cudaStream_t s);
-static void launch_tail(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol, cudaStream_t s) {
+static void launch_tail(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, int ncol, cudaStream_t s) {
   launch_spart(bl->Ld, bl->B.u, e.X, ncol, e.SX, s);
-  launch_lowrank(A.t3, A.ncp, s);
-  launch_apply(A.a3, A.ncp, useB, s);
-  launch_lowrank(A.t4, A.ncp, s);
-  launch_apply(A.a4, A.ncp, useB, s);
+  if (A.lowrank) launch_lowrank(A.t3, A.ncp, s);
+  launch_apply(A.a3, A.ncp, s);
+  if (A.lowrank) launch_lowrank(A.t4, A.ncp, s);
+  launch_apply(A.a4, A.ncp, s);
 }
 
 static int quad_nparts(const nugpr_blocks* bl) {
   return quad_parts(bl->L.n_pad, static_cast<int>(bl->Ld.n_tiles) * MAXC);
 }
-static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, bool useB, int ncol,
-                              int logdet_mode, cudaStream_t s) {
+static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, int ncol, int logdet_mode,
+                              cudaStream_t s) {
   if (A.mbcg) {
     const int np = quad_nparts(bl);
     launch_quad_part(e.RHS, e.X, bl->L.n_pad, np, e.SX, s);
@@ -1299,17 +1348,12 @@ static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, b
                  logdet_mode, e.out, s, e.SX, np);
     return;
   }
-  launch_tail(bl, e, A, useB, ncol, s);
+  launch_tail(bl, e, A, ncol, s);
   launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n),
                ncol, logdet_mode, e.out, s);
 }
 
 // Graph of one slot: while (any column active) { CG iteration }; spart; trace applies; final.
-struct EvalGraph {
-  cudaGraph_t g = nullptr;
-  cudaGraphExec_t exec = nullptr;
-};
-
 static std::string graph_key(const nugpr_blocks* bl, int slot, int ncol, int logdet_mode) {
   char buf[160];
   const HostLayout& L = bl->L;
@@ -1382,7 +1426,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
          launch_assemble(B.X, L.d, Ld, nullptr, 0, L.ld_max, B.jitter, e.G, bl->kind, th.lengthscale,
                          th.noise, th.outputscale, s));
     PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_KLt(e.G, B.Linv, e.T, Ld, L.ld_max, s));
-    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_LT(B.Linv, e.T, e.G, Ld, L.ld_max, s));
+    PROF(ctx, PC_GEMM, 0.0, s, launch_gemm_LT(B.Linv, e.T, e.G, Ld, L.ld_max, !L.big, s));
     CKL();
     if (as != s) CK(cudaStreamWaitEvent(s, ctx->ev_aux[slot][1], 0));
     lam0_ptr = e.scal;
@@ -1393,10 +1437,10 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     if (L.big) return fail(NUGPR_ERR_UNSUPPORTED, "FP32 block storage needs clusters <= %d points", LD_SMALL_MAX);
     if (mode == NUGPR_MODE_GENERIC) {
       float* g32 = reinterpret_cast<float*>(e.T);            // free after the G GEMMs
-      launch_d2f(e.G, g32, L.blk_total, s);
+      launch_d2f(e.G, g32, L.pk_total, s);
       P.B32 = g32;
     } else if (P.B) {
-      if (!bl->h32_ready) { launch_d2f(B.H, B.H32, L.blk_total, s); bl->h32_ready = true; }
+      if (!bl->h32_ready) { launch_d2f(B.H, B.H32, L.pk_total, s); bl->h32_ready = true; }
       P.B32 = B.H32;
     }
     CKL();
@@ -1450,11 +1494,15 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   // direct launches (profiling / NUGPR_OPT_GRAPHS = 0): host polls the activity flag every CH iterations
   IterArgs A;
   RET(make_iter_args(bl, e, ncol, A, cfg->logdet_mode == NUGPR_LOGDET_MBCG));
-  double sum_b2 = 0.0;
-  for (int i = 0; i < L.n_c; ++i) { double b = static_cast<double>(L.off[i + 1] - L.off[i]); sum_b2 += b * b; }
-  // algorithmic bytes of one apply: w (sum b_i^2 [full B] + 2 n c + n + n_c^2)
+  // algorithmic bytes of one apply: w (P + 2 n c + n + n_c^2) with P = sum b_i (b_i + 1) / 2
+  // for the packed symmetric blocks of the small layout, sum b_i^2 for the full blocks of the big one
+  double sum_p = 0.0;
+  for (int i = 0; i < L.n_c; ++i) {
+    const double b = static_cast<double>(L.off[i + 1] - L.off[i]);
+    sum_p += L.big ? b * b : 0.5 * b * (b + 1.0);
+  }
   const double vec_bytes = 8.0 * (2.0 * L.n * ncol + L.n + static_cast<double>(L.n_c) * L.n_c);
-  const double apply_bytes = (useB ? (bl->f32 ? 4.0 : 8.0) * sum_b2 : 0.0) + vec_bytes;   // B as stored
+  const double apply_bytes = (useB ? (bl->f32 ? 4.0 : 8.0) * sum_p : 0.0) + vec_bytes;   // B as stored
   const int apply_cls = useB ? PC_APPLY_B : PC_APPLY_LR;
   const int limit = cfg->replay_iters ? [&] { int mx = 0; for (int c = 0; c < ncol; ++c) mx = std::max(mx, P.replay_iters[c]); return mx; }()
                                       : max_iter;
@@ -1465,11 +1513,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     double* xs = e.xs, *xr = e.xr;
     while (done < limit) {
       for (int q = 0; q < CH && done < limit; ++q, ++done) {
-        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
-        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, s));
         RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // S(A p)
-        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
-        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, s));
         RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // p^T q
         launch_fin(FIN_ALPHA, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, e.ah, HIST, s);
         PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
@@ -1483,11 +1529,9 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     }
     launch_spart(Ld, B.u, e.X, ncol, xs + 2 * XG + XO, s);
     RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(x)
-    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, s));
     RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(A x)
-    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, s));
     RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // quad, trace dots
     launch_fin(FIN_TRACE, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, nullptr, HIST, s);
     launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(bl->n_glob),
@@ -1497,12 +1541,11 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   }
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
-      PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
-      if (A.pnew) PROF(ctx, PC_UPDATE, 0.0, s, launch_pnew(A.st, A.R, A.Pb, A.n_pad, A.ncol, s));
-      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, useB, s));
+      if (A.lowrank) PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t1, A.ncp, s));
+      PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, s));
       if (!A.mbcg) {
-        PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
-        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, useB, s));
+        if (A.lowrank) PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t2, A.ncp, s));
+        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, s));
       }
       PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
     }
@@ -1512,13 +1555,13 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
     if (!*ctx->h_flag) break;
   }
   if (A.mbcg) {
-    launch_tail_final(bl, e, A, useB, ncol, cfg->logdet_mode, s);
+    launch_tail_final(bl, e, A, ncol, cfg->logdet_mode, s);
   } else {
     launch_spart(Ld, B.u, e.X, ncol, e.SX, s);
-    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, useB, s));
-    PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, useB, s));
+    if (A.lowrank) PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t3, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, s));
+    if (A.lowrank) PROF(ctx, PC_OTHER, 0.0, s, launch_lowrank(A.t4, A.ncp, s));
+    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, s));
     launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(L.n),
                  ncol, cfg->logdet_mode, e.out, s);
   }
@@ -1549,12 +1592,12 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   A.ua.cond = h;
   CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_iteration(A, true, cs);
+  launch_iteration(A, cs);
   cudaGraph_t body_out = nullptr;
   cudaError_t ce = cudaStreamEndCapture(cs, &body_out);
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph body capture: %s", cudaGetErrorString(ce)); }
   CK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  launch_tail_final(bl, e, A, true, ncol, logdet_mode, cs);
+  launch_tail_final(bl, e, A, ncol, logdet_mode, cs);
   cudaGraph_t g_out = nullptr;
   ce = cudaStreamEndCapture(cs, &g_out);
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph tail capture: %s", cudaGetErrorString(ce)); }
@@ -1563,105 +1606,6 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce)); }
   ctx->graphs[key] = ex;
   ctx->graph_defs.push_back(g);
-  *out = ex;
-  return NUGPR_OK;
-}
-
-// ------------------------------------------------------------------------------------------
-// NEXT-3: a batch of ng evaluations whose operators share the block term (noise and scale steps:
-// B = H) runs its CG in lockstep in ONE graph; every apply is one apply_multi_kernel launch that
-// streams H once for the batch.  The other kernels (lowrank, update, spart, final) stay per
-// evaluation; a tiny kernel ORs the groups' activity into the while-loop condition.
-static nugpr_status get_batch_graph(nugpr_ctx* ctx, nugpr_blocks* bl, const int* slots, int ng, int ncol,
-                                    int logdet_mode, cudaGraphExec_t* out) {
-  std::string key = "batch";
-  for (int g = 0; g < ng; ++g) key += ":" + std::to_string(slots[g]);
-  key += "|" + graph_key(bl, slots[0], ncol, logdet_mode);
-  auto it = ctx->graphs.find(key);
-  if (it != ctx->graphs.end()) { *out = it->second; return NUGPR_OK; }
-  std::vector<IterArgs> A(ng);
-  for (int g = 0; g < ng; ++g) RET(make_iter_args(bl, bl->E[slots[g]], ncol, A[g]));
-  // multi-apply launch plan: 2 CTAs per SM when the per-group D staging and a >= 2-deep ring fit
-  int dev = 0, optin = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-  cudaDeviceGetAttribute(&per_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const int ld_max = bl->L.ld_max;
-  int grid = 0, slot_d = 0, nstage = 0;
-  size_t smem = 0;
-  for (int per = 2; per >= 1 && !smem; --per) {
-    const size_t budget = std::min<size_t>(optin, per_sm / per) - 4096;
-    for (int sl : {4096, 2048}) {
-      const int sd = std::max(sl, 4 * ld_max);
-      const size_t fixed = apply_multi_smem(ng, ld_max, 0, 0);
-      if (fixed >= budget) continue;
-      const int ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed) / (sizeof(double) * sd)));
-      if (ns >= 2) {
-        slot_d = sd; nstage = ns; smem = apply_multi_smem(ng, ld_max, sd, ns);
-        const int nt = bl->Ld.n_tiles;
-        int gr = std::min(nt, per * num_sms_host());
-        const int nm = (nt + gr - 1) / gr;
-        grid = (nt + nm - 1) / nm;
-        break;
-      }
-    }
-  }
-  if (!smem) return fail(NUGPR_ERR_SHAPE, "batched apply does not fit shared memory (ld_max=%d)", ld_max);
-  auto fix = [&](ApplyArgs& x) { x.grid = grid; x.slot_doubles = slot_d; x.nstage = nstage; x.smem_b = smem; x.smem_nob = smem; };
-  ApplyArgs ga1[4], ga2[4], ga3[4], ga4[4];
-  const CGState* sts[4];
-  for (int g = 0; g < ng; ++g) {
-    fix(A[g].a1); fix(A[g].a2); fix(A[g].a3); fix(A[g].a4);
-    ga1[g] = A[g].a1; ga2[g] = A[g].a2; ga3[g] = A[g].a3; ga4[g] = A[g].a4;
-    sts[g] = bl->E[slots[g]].st;
-  }
-  cudaStream_t cs = ctx->capture_stream;
-  cudaGraph_t g0 = nullptr;
-  CK(cudaGraphCreate(&g0, 0));
-  cudaGraphConditionalHandle h;
-  CK(cudaGraphConditionalHandleCreate(&h, g0, 1u, cudaGraphCondAssignDefault));
-  cudaGraphNodeParams cp = {cudaGraphNodeTypeConditional};
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeWhile;
-  cp.conditional.size = 1;
-  cudaGraphNode_t wnode;
-  CK(cudaGraphAddNode(&wnode, g0, nullptr, 0, &cp));
-  cudaGraph_t body = cp.conditional.phGraph_out[0];
-  CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  for (int g = 0; g < ng; ++g) {
-    launch_lowrank(A[g].t1, A[g].ncp, cs);
-    if (A[g].pnew) launch_pnew(A[g].st, A[g].R, A[g].Pb, A[g].n_pad, A[g].ncol, cs);
-  }
-  launch_apply_multi(ga1, ng, cs);
-  for (int g = 0; g < ng; ++g) launch_lowrank(A[g].t2, A[g].ncp, cs);
-  launch_apply_multi(ga2, ng, cs);
-  for (int g = 0; g < ng; ++g) { UpdateArgs ua = A[g].ua; ua.cond = 0; launch_update(ua, A[g].ncp, cs); }
-  launch_cond_any(sts, ng, h, cs);
-  cudaGraph_t bo = nullptr;
-  cudaError_t ce = cudaStreamEndCapture(cs, &bo);
-  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch body capture: %s", cudaGetErrorString(ce)); }
-  CK(cudaStreamBeginCaptureToGraph(cs, g0, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  for (int g = 0; g < ng; ++g) {
-    EvalDev& e = bl->E[slots[g]];
-    launch_spart(bl->Ld, bl->B.u, e.X, ncol, e.SX, cs);
-    launch_lowrank(A[g].t3, A[g].ncp, cs);
-  }
-  launch_apply_multi(ga3, ng, cs);
-  for (int g = 0; g < ng; ++g) launch_lowrank(A[g].t4, A[g].ncp, cs);
-  launch_apply_multi(ga4, ng, cs);
-  for (int g = 0; g < ng; ++g) {
-    EvalDev& e = bl->E[slots[g]];
-    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->L.n), ncol,
-                 logdet_mode, e.out, cs);
-  }
-  cudaGraph_t go = nullptr;
-  ce = cudaStreamEndCapture(cs, &go);
-  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch tail capture: %s", cudaGetErrorString(ce)); }
-  cudaGraphExec_t ex = nullptr;
-  ce = cudaGraphInstantiate(&ex, g0, 0);
-  if (ce != cudaSuccess) { cudaGraphDestroy(g0); return fail(NUGPR_ERR_CUDA, "batch graph instantiate: %s", cudaGetErrorString(ce)); }
-  ctx->graphs[key] = ex;
-  ctx->graph_defs.push_back(g0);
   *out = ex;
   return NUGPR_OK;
 }
@@ -1689,8 +1633,11 @@ static void account_graph_launches(const nugpr_blocks* bl, const nugpr_mll_out& 
   int k = o.iters_y;
   for (int j = 0; j < 16; ++j) k = std::max(k, o.iters_q[j]);
   const bool mb = logdet_mode == NUGPR_LOGDET_MBCG;
-  const long long per_it = (mb ? 3 : 5) + (bl->pnew ? 1 : 0);
-  note_launch(per_it * std::max(1, k) + (mb ? 2 : 6));
+  // per iteration: apply (+ apply) + update, + a lowrank before each apply in the big-block layout;
+  // tail: spart + 2 applies (+ 2 lowrank) + final, or quad_part + final (mBCG)
+  const bool lr = bl->L.big;
+  const long long per_it = (mb ? 2 : 3) + (lr ? (mb ? 1 : 2) : 0);
+  note_launch(per_it * std::max(1, k) + (mb ? 2 : (lr ? 6 : 4)));
 }
 
 static nugpr_status finish_record(nugpr_blocks* bl, const nugpr_solve_cfg* cfg, const nugpr_mll_out& o,
@@ -1856,27 +1803,12 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   const int nk = static_cast<int>(ks.size());
   if (cfg->block_storage == NUGPR_BLOCKS_F32 && !bl->h32_ready && !bl->L.big) {
     if (bl->h_pending) CK(cudaStreamWaitEvent(s0, ctx->ev_h1, 0));
-    launch_d2f(bl->B.H, bl->B.H32, bl->L.blk_total, s0);   // before the fork: every stream reads it
+    launch_d2f(bl->B.H, bl->B.H32, bl->L.pk_total, s0);    // before the fork: every stream reads it
     CKL();
     bl->h32_ready = true;
   }
   CK(cudaEventRecord(ctx->ev_fork, s0));
   int modes[16] = {0};
-  // NEXT-3 batching: the noise- and scale-step evaluations (B = H for all of them) form one
-  // lockstep batch whose applies read H once (m = 8 DMMA path, graphs, one slot per evaluation)
-  std::vector<int> batch;
-  if (ctx->batch && graph && slots >= nk && cfg->num_probes == 8 && !bl->L.big &&
-      cfg->logdet_mode != NUGPR_LOGDET_MBCG) {
-    const nugpr_theta t0 = bl->theta0;
-    for (int j = 0; j < nk && batch.size() < 4; ++j) {
-      const nugpr_theta& th = pts[ks[j]];
-      const bool sl = th.lengthscale == t0.lengthscale, ss_ = th.noise == t0.noise, sa = th.outputscale == t0.outputscale;
-      if (sl && (ss_ != sa)) batch.push_back(j);      // exactly one of noise / scale differs
-    }
-    if (batch.size() < 2) batch.clear();
-  }
-  std::vector<char> in_batch(nk, 0);
-  for (int j : batch) in_batch[j] = 1;
   int q = 0;                                         // stream index of the next job
   // an enqueue failure ends the launching (that job and the ones not yet launched carry its status);
   // the jobs already in flight are still joined and read back
@@ -1885,7 +1817,6 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
   auto note_enq = [&](nugpr_status st, int j) { if (st != NUGPR_OK && enq == NUGPR_OK) { enq = st; failed_at = j; } };
   std::vector<char> launched(nk, 0);
   for (int j = 0; j < nk && enq == NUGPR_OK; ++j) {
-    if (in_batch[j]) continue;
     const int slot = j % slots;
     cudaStream_t ss = ctx->slot_stream[q % slots];
     if (q < slots) note_enq(cudaStreamWaitEvent(ss, ctx->ev_fork, 0) == cudaSuccess ? NUGPR_OK
@@ -1897,28 +1828,6 @@ static nugpr_status run_evals_concurrent(nugpr_ctx* ctx, nugpr_blocks* bl, const
     note_enq(cudaMemcpyAsync(&ctx->h_out[j], bl->E[slot].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss)
                      == cudaSuccess ? NUGPR_OK : fail(NUGPR_ERR_CUDA, "record read-back failed"), j);
     if (enq == NUGPR_OK) launched[j] = 1;
-  }
-  if (!batch.empty() && enq == NUGPR_OK) {
-    cudaStream_t ss = ctx->slot_stream[q % slots];
-    if (q < slots) cudaStreamWaitEvent(ss, ctx->ev_fork, 0);
-    ++q;
-    int bslots[4];
-    for (size_t g = 0; g < batch.size() && enq == NUGPR_OK; ++g) {
-      const int j = batch[g];
-      bslots[g] = j % slots;
-      note_enq(enqueue_eval(ctx, bl, bslots[g], y_dev, pts[ks[j]], cfg, ss, &modes[j], &ctx->h_prm[j], true), j);
-    }
-    cudaGraphExec_t ex = nullptr;
-    if (enq == NUGPR_OK)
-      note_enq(get_batch_graph(ctx, bl, bslots, static_cast<int>(batch.size()), 1 + cfg->num_probes,
-                               cfg->logdet_mode, &ex), batch[0]);
-    if (enq == NUGPR_OK) {
-      cudaGraphLaunch(ex, ss);
-      for (int j : batch) {
-        cudaMemcpyAsync(&ctx->h_out[j], bl->E[j % slots].out, sizeof(nugpr_mll_out), cudaMemcpyDeviceToHost, ss);
-        launched[j] = 1;
-      }
-    }
   }
   for (int slot = 0; slot < std::min(slots, q); ++slot) {
     cudaEventRecord(ctx->ev_join[slot], ctx->slot_stream[slot]);

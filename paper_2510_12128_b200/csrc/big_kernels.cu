@@ -17,6 +17,7 @@
 // epilogue contract as the other apply kernels and per-tile partial sums.
 #include <cstdint>
 
+#include "cg_fin.cuh"
 #include "common.cuh"
 #include "kernels_decl.h"
 
@@ -513,25 +514,9 @@ __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
     __syncthreads();
     if (s_last) {
       __threadfence();
-      CGState* st = a.st;
-      for (int c = wid; c < ncol; c += 8) {
-        double tot = 0.0;
-        for (int tt = lane; tt < a.L.n_tiles; tt += 32) tot += a.dots[tt * MAXC + c];
-        tot = warp_sum(tot);
-        if (lane == 0) {
-          if (a.fin == FIN_ALPHA) {
-            if (st->active[c]) {
-              const double al = st->rr[c] / tot;
-              st->alpha[c] = al;
-              a.alpha_hist[c * a.hist_stride + st->iters[c]] = al;
-            }
-          } else {
-            if (c == 0) st->quad = tot; else st->t[c] = tot;
-          }
-        }
-      }
+      fin_alpha_trace_body(a.fin, a.st, a.dots, a.L.n_tiles, ncol, a.alpha_hist, a.hist_stride, 8);
       __syncthreads();
-      if (tid == 0) st->ticket[a.fin] = 0;
+      if (tid == 0) a.st->ticket[a.fin] = 0;
     }
   }
 }

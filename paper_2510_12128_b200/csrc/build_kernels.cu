@@ -163,7 +163,8 @@ __device__ __forceinline__ void dmma_c(double& d0, double& d1, double a, double 
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-__global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
+template <int PR_T>   // panel rows per thread: ld <= PR_T * NT
+__global__ void __launch_bounds__(256, (PR_T == 1) ? 2 : 1) chol_trtri_kernel(CholArgs a) {
   const int i = a.list ? a.list[blockIdx.x] : blockIdx.x;
   const int ld = a.ld[i];
   const int b = static_cast<int>(a.off[i + 1] - a.off[i]);
@@ -182,50 +183,71 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   for (int k0 = 0; k0 < ld; k0 += NB) {
     const int nb = min(NB, ld - k0);
     const int pr = ld - k0;          // panel rows
-    for (int idx = tid; idx < pr * nb; idx += NT) {
-      const int c = idx / pr, r = idx % pr;
-      Pn[c * pr + r] = A[static_cast<int64_t>(k0 + c) * ld + k0 + r];
+    // Panel factorisation with the panel rows in REGISTERS: thread t owns panel rows t, t + NT, ...
+    // (PR_T rows of 32 columns).  Column step j costs ONE barrier: before it, the owner of row j
+    // publishes the pivot d_j = sqrt(a_jj) and every top-row owner (r < 32) its current a_rj; after
+    // it, each thread scales its own a_rj by 1/d_j and updates its row with the top rows' a_cj / d_j
+    // formed on the fly (the same roundings as scaling the column first).
+    double prow[PR_T][NB];
+#pragma unroll
+    for (int h = 0; h < PR_T; ++h) {
+      const int r = tid + h * NT;
+#pragma unroll
+      for (int c = 0; c < NB; ++c)
+        prow[h][c] = (r < pr && c < nb) ? A[static_cast<int64_t>(k0 + c) * ld + k0 + r] : 0.0;
+    }
+    __shared__ double lcol[2][NB], dpiv[NB];
+    if (tid < NB) {
+      lcol[0][tid] = prow[0][0];                          // column 0 of the top rows
+      if (tid == 0) {
+        const double piv = prow[0][0];
+        if (!(piv > 0.0)) fail = 1;
+        dpiv[0] = sqrt(piv > 0.0 ? piv : 1.0);
+      }
     }
     __syncthreads();
-    // one barrier per column: every thread forms the pivot, the rank-1 update of the remaining
-    // panel columns uses the scaled column j formed on the fly (x*inv, the same roundings as
-    // scaling first), and the scaling of the panel's columns is applied after the loop
-    // ccol[j&1][c] mirrors the panel's column j at rows c < nb in a separate array (written by
-    // the step before), so the broadcast reads of the update do not alias its stores
-    __shared__ double pdg[NB], pinv[NB], ccol[2][NB];
-    for (int r = tid; r < nb; r += NT) ccol[0][r] = Pn[r];
-    __syncthreads();
-    for (int j = 0; j < nb; ++j) {
-      double piv = Pn[j * pr + j];
-      if (!(piv > 0.0)) { if (tid == 0) fail = 1; piv = 1.0; }
-      const double dgv = sqrt(piv);
-      const double inv = 1.0 / dgv;
-      if (tid == 0) { pdg[j] = dgv; pinv[j] = inv; }
-      const int cmax_p = nb - 1;
-      const double* cc = ccol[j & 1];
-      double* cn = ccol[(j + 1) & 1];
-      for (int r = j + 1 + tid; r < pr; r += NT) {
-        const double lr = Pn[j * pr + r] * inv;
-        const int cmax = min(r, cmax_p);
-        // groups of 4 columns: all loads of a group are issued before its stores (ILP 4)
-        for (int c0 = j + 1; c0 <= cmax; c0 += 4) {
-          double v[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] = (c0 + q <= cmax) ? Pn[(c0 + q) * pr + r] : 0.0;
+    for (int j = 0; j < NB; ++j) {
+      if (j < nb) {
+        const double dgv = dpiv[j];
+        const double inv = 1.0 / dgv;
+        const double* uc = lcol[j & 1];
 #pragma unroll
-          for (int q = 0; q < 4; ++q) v[q] -= lr * (cc[min(c0 + q, NB - 1)] * inv);
+        for (int h = 0; h < PR_T; ++h) {
+          const int r = tid + h * NT;
+          if (r > j && r < pr) {
+            const double l = prow[h][j] * inv;
+            prow[h][j] = l;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (c0 + q <= cmax) Pn[(c0 + q) * pr + r] = v[q];
-          if (c0 == j + 1 && r < nb) cn[r] = v[0];
+            for (int c = j + 1; c < NB; ++c)
+              if (c <= r) prow[h][c] -= l * (uc[c] * inv);
+          } else if (r == j) {
+            prow[h][j] = dgv;
+          }
+        }
+        if (j + 1 < nb) {
+          // publish column j+1 of the top rows and its pivot for the next step
+#pragma unroll
+          for (int h = 0; h < PR_T; ++h) {
+            const int r = tid + h * NT;
+            if (r < NB) lcol[(j + 1) & 1][r] = prow[h][j + 1];
+            if (r == j + 1) {
+              const double piv = prow[h][j + 1];
+              if (!(piv > 0.0)) fail = 1;
+              dpiv[j + 1] = sqrt(piv > 0.0 ? piv : 1.0);
+            }
+          }
+          __syncthreads();
         }
       }
-      __syncthreads();
     }
-    for (int idx = tid; idx < pr * nb; idx += NT) {
-      const int c = idx / pr, r = idx % pr;
-      if (r == c) Pn[c * pr + r] = pdg[c];
-      else if (r > c) Pn[c * pr + r] *= pinv[c];
+    // the finished panel to shared memory (the trailing update reads it) and global
+#pragma unroll
+    for (int h = 0; h < PR_T; ++h) {
+      const int r = tid + h * NT;
+      if (r < pr)
+#pragma unroll
+        for (int c = 0; c < NB; ++c) Pn[c * pr + r] = (c < nb && r >= c) ? prow[h][c] : 0.0;
     }
     __syncthreads();
     for (int idx = tid; idx < pr * nb; idx += NT) {
@@ -266,6 +288,8 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 #pragma unroll
               for (int n = 0; n < 2; ++n) dmma_c(acc[m][n][0], acc[m][n][1], af[m], bf[n]);
           }
+          // read-modify-write of the trailing tile: all 16 loads in flight, then the stores
+          double old_[4][2][2];
 #pragma unroll
           for (int m = 0; m < 4; ++m)
 #pragma unroll
@@ -273,7 +297,16 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 #pragma unroll
               for (int e = 0; e < 2; ++e) {
                 const int r = rw + m * 8 + qr, c = cw + n * 8 + 2 * qc + e;
-                if (r < tr && c < tr && r >= c) A[static_cast<int64_t>(t0 + c) * ld + t0 + r] -= acc[m][n][e];
+                old_[m][n][e] = (r < tr && c < tr && r >= c) ? A[static_cast<int64_t>(t0 + c) * ld + t0 + r] : 0.0;
+              }
+#pragma unroll
+          for (int m = 0; m < 4; ++m)
+#pragma unroll
+            for (int n = 0; n < 2; ++n)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                const int r = rw + m * 8 + qr, c = cw + n * 8 + 2 * qc + e;
+                if (r < tr && c < tr && r >= c) A[static_cast<int64_t>(t0 + c) * ld + t0 + r] = old_[m][n][e] - acc[m][n][e];
               }
         }
       }
@@ -301,12 +334,14 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
   //   Yc[cl*NB + r] = (L[I,0:I0] * Xinv[0:I0, cc0+cl])[r].
   constexpr int YC = 64;
   constexpr int NBP = NB + 1;                 // padded stride: conflict-free column sweeps
+  constexpr int XKC = 32, XSP = YC + 4;       // staged X rows per chunk; row stride (conflict-free B fragments)
   double* LrT = sm;
   for (int I0 = 0; I0 < ld; I0 += NB) {
     const int nb = min(NB, ld - I0);
     const int ldr = I0 + nb;
     double* XdT = LrT + NBP * ldr;            // NB x NB (stride NBP)
     double* Yc = XdT + NBP * NB;              // NB x YC
+    double* Xs = Yc + NB * YC;                // XKC x XSP
     for (int idx = tid; idx < nb * ldr; idx += NT) {
       const int k = idx / nb, r = idx % nb;   // coalesced over r in global and smem
       LrT[k * NBP + r] = A[static_cast<int64_t>(k) * ld + I0 + r];
@@ -325,7 +360,7 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 #pragma unroll
           for (int k = 0; k < r; ++k)
             if (k >= j) v -= LrT[(I0 + k) * NBP + r] * x[k];
-          v /= LrT[(I0 + r) * NBP + r];
+          v *= 1.0 / LrT[(I0 + r) * NBP + r];
         }
         x[r] = v;
       }
@@ -344,17 +379,29 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
         double acc[4][2];
 #pragma unroll
         for (int m = 0; m < 4; ++m) { acc[m][0] = 0.0; acc[m][1] = 0.0; }
-        if (c8 < ncc) {
-          const double* xcol = A + static_cast<int64_t>(cc0 + c8 + qr) * ld;   // X[k][cc0+c8+qr]
-          for (int k4 = cc0 + c8; k4 < I0; k4 += 4) {
-            const double bf = xcol[k4 + qc];
+        // X[k][cc0 : cc0+64] staged through shared memory 32 rows at a time (coalesced column runs)
+        // instead of per-fragment global loads inside the tensor loop
+        for (int kc = cc0; kc < I0; kc += XKC) {
+          const int nk = min(XKC, I0 - kc);
+          for (int idx = tid; idx < nk * YC; idx += NT) {
+            const int cl = idx / nk, kl = idx - cl * nk;
+            Xs[kl * XSP + cl] = (cl < ncc) ? A[static_cast<int64_t>(cc0 + cl) * ld + kc + kl] : 0.0;
+          }
+          __syncthreads();
+          if (c8 < ncc) {
+            // X is lower triangular: rows k < cc0 + c8 of these columns are zero
+            const int kstart = max(kc, cc0 + c8);
+            for (int k4 = kstart; k4 < kc + nk; k4 += 4) {
+              const double bf = Xs[(k4 - kc + qc) * XSP + c8 + qr];
 #pragma unroll
-            for (int m = 0; m < 4; ++m) {
-              const int r = m * 8 + qr;
-              const double af = (r < nb) ? LrT[(k4 + qc) * NBP + r] : 0.0;
-              dmma_c(acc[m][0], acc[m][1], af, bf);
+              for (int m = 0; m < 4; ++m) {
+                const int r = m * 8 + qr;
+                const double af = (r < nb) ? LrT[(k4 + qc) * NBP + r] : 0.0;
+                dmma_c(acc[m][0], acc[m][1], af, bf);
+              }
             }
           }
+          __syncthreads();
         }
 #pragma unroll
         for (int m = 0; m < 4; ++m)
@@ -415,7 +462,7 @@ __global__ void __launch_bounds__(256) chol_trtri_kernel(CholArgs a) {
 
 size_t chol_smem_bytes(int ld_max) {
   size_t panel = static_cast<size_t>(ld_max) * NB;                         // Cholesky panel
-  size_t inv = static_cast<size_t>(NB + 1) * ld_max + (NB + 1) * NB + static_cast<size_t>(NB) * 64 + 64;
+  size_t inv = static_cast<size_t>(NB + 1) * ld_max + (NB + 1) * NB + static_cast<size_t>(NB) * 64 + 32 * 68 + 64;
   return sizeof(double) * (panel > inv ? panel : inv);
 }
 
@@ -423,8 +470,13 @@ void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int n
                        int32_t* status, double* logdet_blk, double* u, cudaStream_t s) {
   CholArgs a{A, L.off, L.poff, L.boff, L.ld, list, status, logdet_blk, u};
   size_t smem = chol_smem_bytes(ld_max);
-  smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel));
-  chol_trtri_kernel<<<list ? nlist : L.n_c, NT, smem, s>>>(a);
+  if (ld_max <= NT) {
+    smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel<1>));
+    chol_trtri_kernel<1><<<list ? nlist : L.n_c, NT, smem, s>>>(a);
+  } else {
+    smem_optin(reinterpret_cast<const void*>(chol_trtri_kernel<2>));
+    chol_trtri_kernel<2><<<list ? nlist : L.n_c, NT, smem, s>>>(a);
+  }
   note_launch(); post_launch("chol_trtri_kernel");
 }
 
@@ -440,6 +492,7 @@ struct GemmArgs {
   const int64_t* boff;
   const int32_t* ld;
   int ntile_max;         // tiles per dimension of the largest block
+  const int64_t* pboff;  // PACKED output: C_i's packed lower-tile storage at pboff[i] (else NULL)
 };
 
 // Batched block GEMM on the FP64 tensor pipe (mma.sync m8n8k4 f64).  64x64 CTA tile, 8 warps as 2 (rows) x 4 (cols), warp tile 32x16 =
@@ -453,7 +506,7 @@ __device__ __forceinline__ void dmma884g(double& d0, double& d1, double a, doubl
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
-template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM>
+template <bool TRANSB, bool A_LOWER, bool B_LOWERT, bool SYM, bool PACKED>
 __global__ void __launch_bounds__(256, 3) gemm_dmma_kernel(GemmArgs g) {
   const int i = blockIdx.y;
   const int ld = g.ld[i];
@@ -474,7 +527,7 @@ __global__ void __launch_bounds__(256, 3) gemm_dmma_kernel(GemmArgs g) {
   const int64_t bo = g.boff[i];
   const double* A = g.A + bo;
   const double* B = g.B + bo;
-  double* C = g.C + bo;
+  double* C = g.C + (PACKED ? g.pboff[i] : bo);
   const int r0 = tr * 64, c0 = tc * 64;
   int kend = ld;
   if (A_LOWER) kend = min(kend, r0 + 64);
@@ -566,7 +619,16 @@ __global__ void __launch_bounds__(256, 3) gemm_dmma_kernel(GemmArgs g) {
       for (int e = 0; e < 2; ++e) {
         const int c = wc + n * 8 + 2 * qc + e;
         const double v = acc[m][n][e];
-        if (SYM) {
+        if (PACKED) {
+          // lower tiles (r/8 >= c/8) in the packed block order, swizzled (common.cuh); the diagonal
+          // tiles are written from their lower half and mirrored, so they are exactly symmetric
+          const int I = r >> 3, K = c >> 3, mt = ld >> 3;
+          if (r >= c) {
+            double* tp = C + static_cast<int64_t>(pk_tile(I, K, mt)) * 64;
+            tp[swz(r & 7, c & 7)] = v;
+            if (I == K) tp[swz(c & 7, r & 7)] = v;
+          }
+        } else if (SYM) {
           if (r >= c) {
             C[static_cast<int64_t>(c) * ld + r] = v;
             C[static_cast<int64_t>(r) * ld + c] = v;
@@ -579,26 +641,28 @@ __global__ void __launch_bounds__(256, 3) gemm_dmma_kernel(GemmArgs g) {
 }
 
 // H = Linv * Linv^T (symmetric)
-void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s) {
+void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, bool packed, cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
-  GemmArgs g{Linv, Linv, H, L.boff, L.ld, nt};
-  gemm_dmma_kernel<true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  GemmArgs g{Linv, Linv, H, L.boff, L.ld, nt, L.pboff};
+  if (packed) gemm_dmma_kernel<true, true, true, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  else gemm_dmma_kernel<true, true, true, true, false><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_H");
 }
 // T = K * Linv^T
 void launch_gemm_KLt(const double* K, const double* Linv, double* T, const LayoutDev& L, int ld_max,
                      cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
-  GemmArgs g{K, Linv, T, L.boff, L.ld, nt};
-  gemm_dmma_kernel<true, false, true, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
+  GemmArgs g{K, Linv, T, L.boff, L.ld, nt, nullptr};
+  gemm_dmma_kernel<true, false, true, false, false><<<dim3(nt * nt, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_KLt");
 }
 // G = Linv * T (symmetric)
-void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max,
+void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max, bool packed,
                     cudaStream_t s) {
   int nt = (ld_max + 63) / 64;
-  GemmArgs g{Linv, T, G, L.boff, L.ld, nt};
-  gemm_dmma_kernel<false, true, false, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  GemmArgs g{Linv, T, G, L.boff, L.ld, nt, L.pboff};
+  if (packed) gemm_dmma_kernel<false, true, false, true, true><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
+  else gemm_dmma_kernel<false, true, false, true, false><<<dim3(nt * (nt + 1) / 2, L.n_c), 256, 0, s>>>(g);
   note_launch(); post_launch("gemm_LT");
 }
 
@@ -711,23 +775,20 @@ __device__ double block_tridiag_min_eig(int k, const double* a, const double* b,
     lohi[1] = hi;
   }
   __syncthreads();
+  double lo = lohi[0], hi = lohi[1];
+  (void)cnt_sm;
   for (int it = 0; it < 8; ++it) {
-    const double lo = lohi[0], hi = lohi[1];
-    if (!(hi - lo > 1e-16 * fabs(hi))) break;       // uniform: all threads read the same values
+    if (!(hi - lo > 1e-16 * fabs(hi))) break;       // uniform: all threads hold the same values
     const double x = lo + (hi - lo) * (tid + 1) / (LZ_NT + 1.0);
-    cnt_sm[tid] = (sturm_count_nodiv(k, a, b, x) >= 1) ? 1 : 0;
-    __syncthreads();
-    if (tid == 0) {
-      int f = LZ_NT;
-      for (int t = 0; t < LZ_NT; ++t) if (cnt_sm[t]) { f = t; break; }
-      lohi[0] = lo + (hi - lo) * f / (LZ_NT + 1.0);
-      lohi[1] = (f < LZ_NT) ? lo + (hi - lo) * (f + 1) / (LZ_NT + 1.0) : hi;
-    }
-    __syncthreads();
+    // the flags "some eigenvalue below x" are monotone in tid, so the first set one is at index f =
+    // the number of unset ones: one counting barrier instead of a serial scan
+    const int f = __syncthreads_count(sturm_count_nodiv(k, a, b, x) < 1);
+    const double nlo = lo + (hi - lo) * f / (LZ_NT + 1.0);
+    const double nhi = (f < LZ_NT) ? lo + (hi - lo) * (f + 1) / (LZ_NT + 1.0) : hi;
+    lo = nlo;
+    hi = nhi;
   }
-  const double r = 0.5 * (lohi[0] + lohi[1]);
-  __syncthreads();
-  return r;
+  return 0.5 * (lo + hi);
 }
 
 // eigenvector of T for eigenvalue th: two inverse-iteration steps (Thomas, one division per row)

@@ -6,8 +6,9 @@
 //    are exactly invisible to the method.
 //  * Vectors: column-major [NC][n_pad] FP64 (one contiguous length-n_pad column per RHS;
 //    column 0 = the y-solve, columns 1..m = the Hutchinson probes).
-//  * Block matrices (Linv_i, H_i, G_i): dense ld_i x ld_i column-major at boff[i];
-//    H and G are stored full (both triangles) so the apply streams them coalesced.
+//  * Block matrices: Linv_i dense ld_i x ld_i column-major at boff[i]; H_i and G_i (symmetric)
+//    packed lower triangle in swizzled 8x8 tiles at pboff[i] (small layout, see swz below), or
+//    full ld_i x ld_i at boff[i] in big-block mode (ld > 512).
 //  * Row tiles: a cluster is split into tiles of <= TILE_ROWS padded rows; each apply /
 //    update CTA owns one tile; per-tile partial sums (S = W^T D partials, dots) live in
 //    [n_tiles][16] arrays and are reduced in fixed tile order (deterministic).
@@ -25,6 +26,51 @@ constexpr int SLOT_TARGET_DOUBLES = 4096;  // ~32 KB per TMA chunk
 constexpr int PAD = 8;          // cluster padding granularity (rows)
 constexpr int CTW = 16;         // columns per task of the DMMA column apply
 
+// Packed symmetric block storage (small layout, ld <= 512; "only (K_diag, K_rep)
+// need be stored", SURVEY §8(d) P = sum b(b+1)/2): only the lower triangle of H_i / G_i, in 8x8 tiles
+// (I, K), I >= K (mt = ld/8 tiles per side), 64 elements per tile with element (r, c) at swz(r, c).
+// Tiles are grouped in BLOCKS of up to 8x8 tiles: block (g, s) holds tiles I = 8g+a, K = 8s+b
+// (a < h(g), b < h(s), h(x) = min(8, mt - 8x); a >= b when g == s), stored b-major; blocks are
+// ordered column-block-major (s = 0.., then g = s..).  One block is one TMA chunk of the apply,
+// and in it warp w does exactly the products of row a = w (out_I += T D_K) and column b = w
+// (out_K += T^T D_I): regular, balanced work with no per-tile index search.  Diagonal tiles are
+// stored full.  The swizzle makes the DMMA fragment loads of both T and T^T bank-conflict-free.
+__host__ __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (((r >> 1) & 1) << 2)); }
+__host__ __device__ __forceinline__ int64_t tri_tiles(int mt) { return static_cast<int64_t>(mt) * (mt + 1) / 2; }
+__host__ __device__ __forceinline__ int pk_ns(int mt) { return (mt + 7) >> 3; }                 // block rows
+__host__ __device__ __forceinline__ int pk_h(int x, int mt) { return (mt - 8 * x < 8) ? mt - 8 * x : 8; }
+__host__ __device__ __forceinline__ int pk_nblocks(int mt) { const int ns = pk_ns(mt); return ns * (ns + 1) / 2; }
+// first tile of block (g, s), g >= s: all column blocks before s are 8 tiles wide
+__host__ __device__ __forceinline__ int pk_blk_off(int g, int s, int mt) {
+  const int o = s * (8 * mt - 28) - 32 * s * (s - 1);
+  if (g == s) return o;
+  const int w = pk_h(s, mt);
+  return o + w * (w + 1) / 2 + w * 8 * (g - s - 1);
+}
+__host__ __device__ __forceinline__ int pk_blk_size(int g, int s, int mt) {
+  const int w = pk_h(s, mt);
+  return (g == s) ? w * (w + 1) / 2 : pk_h(g, mt) * w;
+}
+// index of tile (I, K), I >= K, in the cluster's packed storage
+__host__ __device__ __forceinline__ int pk_tile(int I, int K, int mt) {
+  const int g = I >> 3, s = K >> 3, a = I & 7, b = K & 7;
+  const int h = pk_h(g, mt);
+  const int pos = (g == s) ? b * h - b * (b - 1) / 2 + (a - b) : b * h + a;
+  return pk_blk_off(g, s, mt) + pos;
+}
+
+// One CTA's piece of the packed-block stream of an apply: blocks [k0, k1) (in storage order) of
+// cluster blk.  The stream of all clusters is cut into PACK_CTAS pieces of equal tile count at block
+// boundaries, so a cluster can be split over up to MAX_PARTS CTAs (part = its index); a split
+// cluster's partial products meet in split scratch at `spoff` (doubles) and the last CTA to arrive
+// (ticket `tick`) sums them in part order and runs the epilogue.
+constexpr int PACK_CTAS = 148;   // B200 SM count: the partition is fixed (independent of the device)
+constexpr int MAX_PARTS = 4;
+struct SegDesc {
+  int32_t blk, k0, k1, part, nparts, tick;
+  int64_t spoff;
+};
+
 struct TileDesc {
   int32_t blk;    // cluster index
   int32_t row0;   // first padded row within the cluster
@@ -35,15 +81,17 @@ struct TileDesc {
 struct LayoutDev {
   const int64_t* off;    // [n_c+1] original (unpadded) row offsets
   const int64_t* poff;   // [n_c+1] padded row offsets
-  const int64_t* boff;   // [n_c] element offset of block i in block storage
+  const int64_t* boff;   // [n_c] element offset of block i in full block storage (ld_i x ld_i)
   const int32_t* ld;     // [n_c] padded cluster size
   const TileDesc* tiles; // [n_tiles]
   const int32_t* tile0;  // [n_c+1] tile range of each cluster
-  const TileDesc* ctasks; // [n_ctasks] column tasks of the DMMA column apply: (cluster, col0, ncols)
-  const int32_t* ctask0; // [n_c+1] column-task range of each cluster
+  const int64_t* pboff;   // [n_c] element offset of block i in PACKED block storage (small layout)
+  const SegDesc* segs;    // packed-apply pieces, CTA b owns segs[seg0[b] .. seg0[b+1])
+  const int32_t* seg0;    // [n_seg_ctas + 1]
   int32_t n_c;
   int32_t n_tiles;
-  int32_t n_ctasks;
+  int32_t n_seg_ctas;
+  int32_t seg_max;        // max pieces per CTA
   int64_t n;             // unpadded rows
   int64_t n_pad;         // padded rows (vector column stride)
 };
@@ -97,50 +145,34 @@ struct ApplyArgs {
   const double* jitter;    // [n_c]
   // input D
   const double* D;         // [NC][n_pad]; with fuse_p this is R
-  const double* S_D;       // [n_tiles][16] partials of S(D) (fuse_p: S(R))
+  const double* S_D;       // [lr_nc][MAXC] per-cluster S rows of D (fuse_p: S(R)); global under PAR-2
   int fuse_p;              // D := R + beta o P_old (active columns), P_new written
   double* Pbuf[2];         // P ping-pong
-  double* SPbuf[2];        // S(P) ping-pong partials
-  int use_par_p2;          // P2 := Pbuf[par^1] (current search direction)
+  double* SPbuf[2];        // S(P) ping-pong rows [lr_nc][MAXC]
+  int use_par_p2;          // 1: P2 = Y2 := Pbuf[par^1]; 2: Y2 := D itself (mBCG)
+  int lr_row0, lr_nc;      // low-rank term: M' rows of local cluster 0 (PAR-2 offset), S / M' extent
   // output
   double* out;
   const double* P2;        // combine term (or NULL)
   double cA[MAXC], cV[MAXC], cP[MAXC];
   int epi;                 // EpiKind
-  double* Sout;            // EPI_S: partials of u^T out
+  double* Sout;            // EPI_S: per-cluster rows of u^T out
   const double* Y2;        // EPI_DOT: partner of the dot
-  double* dots;            // EPI_DOT: partials of out . Y2
+  double* dots;            // EPI_DOT: per-cluster rows of out . Y2
   int fin;                 // FinKind (FIN_ALPHA or FIN_TRACE)
   int gate;                // return immediately when !st->any_active
   int ncol;
   double* alpha_hist;      // [MAXC][hist_stride]
   int hist_stride;
+  // packed apply: split-cluster partial sums / tickets, launch plan
+  double* split_part;
+  unsigned int* split_ticket;
+  int grid, slot_tiles, nstage, mtmax, nt8, f32;
+  size_t smem;
   int ld_max;
-  int slot_doubles;        // TMA ring slot size (>= ld_max)
-  int red_doubles;         // cross-k-group reduction scratch
-  int nstage;              // TMA ring depth
-  double* Tbuf;            // [n_c][MAXC] low-rank coefficients M' S (phase 1 of the apply)
-  int nmine_max;           // max clusters per persistent CTA
-  size_t smem_b, smem_nob; // dynamic shared memory with / without the ring
-  int grid;                // persistent grid size
-  int dbg;                 // timing experiments (NUGPR_APPLY_DBG); 0 in production
-  int mma;                 // 3: DMMA column-task kernel, 2: staged DMMA, 1: DMMA, 0: DFMA
-  int lds;                 // column-task kernel: padded column stride in shared memory
-  int d_is_pnew;           // column-task kernel: D := P_new = Pbuf[par^1] (formed by pnew_kernel)
-  int big;                 // big-block mode (ld_max > 512): row-tiled apply_big_kernel
-  int f32;                 // 1: the DMMA apply streams the FP32-stored block (P->B32)
-  int nw;                  // DMMA apply: consumer warps per CTA (7: 2 CTAs/SM; 3: 4 CTAs/SM)
-  int dstride;             // DMMA apply: > 0 => D_i arrives per chunk with the TMA stream (stage row stride)
-  int dbuf;                // DMMA apply: second D_i buffer; unfused applies prefetch the next cluster's D_i
-};
-
-struct ApplyPlan {
-  int slot_doubles = 0, red_doubles = 0, nstage = 0, nmine_max = 0, grid = 0, ctas_per_sm = 0, mma = 0, lds = 0;
-  int nw = 7;
-  int dstride = 0;
-  int dbuf = 0;
-  size_t smem_b = 0, smem_nob = 0;
-  bool ok = false;
+  // big-block path (ld > 512, apply_big_kernel): low-rank rows T = M'S from lowrank_kernel
+  int big;
+  double* Tbuf;            // [n_c][MAXC]
 };
 
 struct LowrankArgs {

@@ -25,10 +25,12 @@ void launch_assemble(const double* X, int d, const LayoutDev& L, const int32_t* 
 size_t chol_smem_bytes(int ld_max);
 void launch_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, int nlist, int ld_max,
                        int32_t* status, double* logdet_blk, double* u, cudaStream_t s);
-void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, cudaStream_t s);
+// H = Linv Linv^T and G = Linv T: packed output (PACKED storage at L.pboff) for the small layout,
+// full ld x ld storage at L.boff for the big-block layout
+void launch_gemm_H(const double* Linv, double* H, const LayoutDev& L, int ld_max, bool packed, cudaStream_t s);
 void launch_gemm_KLt(const double* K, const double* Linv, double* T, const LayoutDev& L, int ld_max,
                      cudaStream_t s);
-void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max,
+void launch_gemm_LT(const double* Linv, const double* T, double* G, const LayoutDev& L, int ld_max, bool packed,
                     cudaStream_t s);
 void launch_sum(const double* v, int n, double* out, cudaStream_t s);
 void launch_krep(const double* reps, int n_c, int d, int kind, double lam, double alpha, double* K,
@@ -40,19 +42,13 @@ cudaError_t launch_lanczos(const double* K, int n_c, const double* vinit, double
                            cudaStream_t s);
 
 // eval_kernels.cu
-ApplyPlan plan_apply(int ncp, int ncol, int ld_max, int ld_min, int n_tiles, int grid, int n_ctasks);
-int apply_grid(int n_tiles);
-void launch_apply(const ApplyArgs& a, int ncp, bool useB, cudaStream_t s);
+void launch_apply(const ApplyArgs& a, int ncp, cudaStream_t s);
 void launch_update(const UpdateArgs& a, int ncp, cudaStream_t s);
 void launch_lowrank(const LowrankArgs& a, int ncp, cudaStream_t s);
 void launch_rhs_init(const RhsArgs& a, int ld_max, cudaStream_t s);
 void launch_cy(const LayoutDev& L, const double* Linv, const double* y, int ld_max, double* cy, cudaStream_t s);
 int num_sms_host();
 void launch_d2f(const double* src, float* dst, int64_t n, cudaStream_t s);
-void launch_apply_multi(const ApplyArgs* ga, int ng, cudaStream_t s);
-size_t apply_multi_smem(int ng, int ld_max, int slot_doubles, int nstage);
-void launch_cond_any(const CGState* const* sts, int ng, unsigned long long cond, cudaStream_t s);
-void launch_pnew(const CGState* st, const double* R, double* const* Pbuf, int64_t n_pad, int ncol, cudaStream_t s);
 void launch_spart(const LayoutDev& L, const double* u, const double* V, int ncol, double* part,
                   cudaStream_t s);
 void launch_final(const CGState* st, const EvalParams* prm, const double* ah, const double* bh,
@@ -65,6 +61,11 @@ void launch_fin(int fin, CGState* st, const EvalParams* prm, const double* part,
 int quad_parts(int64_t n_pad, int cap);
 void launch_quad_part(const double* c, const double* x, int64_t n_pad, int nparts, double* part, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);
+
+// apply_kernels.cu (packed symmetric blocks, ld_max <= 512)
+// Plans the launch (smem ring, m-tiles per warp, probe n-tiles) into a; false if it cannot run.
+bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a);
+void launch_apply_packed(const ApplyArgs& a, cudaStream_t s);
 
 // big_kernels.cu (ld_max > 512)
 size_t big_scratch_doubles(int n_c, int ld_max);

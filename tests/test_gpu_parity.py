@@ -386,8 +386,15 @@ def test_mbcg_numgrad_concurrent_equals_serial(P, ctx):
     L7, g7, e7 = P.numgrad(ctx, b7, ds.y, ds.theta0, probe_seed=202, logdet="mbcg")
     L1, g1, e1 = P.numgrad(ctx, b1, ds.y, ds.theta0, probe_seed=202, logdet="mbcg")
     # records are bitwise equal (logdet_pade is NaN in mBCG mode: compare its bits, not with ==)
+    def bits(v):
+        if isinstance(v, float):
+            return np.float64(v).tobytes()
+        if isinstance(v, list):
+            return [bits(x) for x in v]
+        return v
+
     def key(rs):
-        return [{k: (np.float64(v).tobytes() if isinstance(v, float) else v) for k, v in r.items()} for r in rs]
+        return [{k: bits(v) for k, v in r.items()} for r in rs]
     assert key(e7) == key(e1) and np.array_equal(g7, g1)
     # fewer iterations than the Q(A) solve (A is better conditioned than Q(A))
     _, _, ep = P.numgrad(ctx, b7, ds.y, ds.theta0, probe_seed=202)
