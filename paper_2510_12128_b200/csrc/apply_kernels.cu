@@ -36,55 +36,74 @@
 
 namespace nugpr {
 
-constexpr int PNM = 8;                 // MMA warps (warp w owns the output m-tiles w, w+8, ...)
-constexpr int PWE = PNM;               // first epilogue warp
+// NM MMA warps (8), warp w owning the output m-tiles w, w+NM, ...; a block's tile rows / columns
+// w + NM rr (rr < 8 / NM)
 constexpr int PNE_MAX = 7;             // epilogue / prologue warps: 7 (ld <= 256) or 4 (ld <= 512), register budget
-constexpr int PLDP = 12;               // Dp row: 8 probe columns (conflict-free B fragments), y at slot 8
+// split-k of the thin last block row (height <= ESPLIT_H tiles): per-warp partials, reduced in fixed
+// warp order through ESC at the end of the piece
+constexpr int ESPLIT_H = 2;
+__host__ __device__ constexpr int esc_bytes(int nm) { return nm == 8 ? 8 * ESPLIT_H * 32 * 3 * 8 : 0; }
 constexpr int TQ = 4;                  // pieces per reduction pass of the low-rank rows
-constexpr int MAX_SEG_T = 8;           // pieces whose low-rank rows are formed from the staged S chunks
+constexpr int MAX_SEG_T = 8;           // pieces per CTA whose low-rank rows are formed from staged S rows
 
+// (not volatile: a pure function of its operands, so the compiler may schedule it freely)
 __device__ __forceinline__ void dmma_pk(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 template <int PNE>
 __device__ __forceinline__ void bar_epi() { asm volatile("bar.sync 2, %0;" ::"r"(PNE * 32) : "memory"); }
 
 template <typename TB>
 __device__ __forceinline__ double ldA(const TB* p) { return static_cast<double>(*p); }
+__device__ __forceinline__ double2 ldA2(const double* p) { return *reinterpret_cast<const double2*>(p); }
+__device__ __forceinline__ double2 ldA2(const float* p) {
+  const float2 v = *reinterpret_cast<const float2*>(p);
+  return make_double2(v.x, v.y);
+}
 
-// Shared-memory plan (host and device agree): ring | Dp[2] | Acc | Tsm
+// D buffer: column-major [NCP columns][ldp], column 0 = y; ldp = 8 (mod 16) doubles so that the
+// 16-byte B-pair loads D[8t + 2qc + h][col qr] of a quarter warp (rows qr = 2t', 2t'+1) hit all banks
+__host__ __device__ __forceinline__ int pk_ldp(int ld_max) { return ((ld_max + 15) & ~15) + 8; }
+
+// The low-rank rows T_q = M'[row(q), :] S(D) of all the CTA's pieces are formed first, from the S rows
+// (and S(P_old) for the fused apply) and the CTA's M' row segments staged through the (still empty)
+// ring in rounds of JC rows — one round trip at C3 — before the block stream starts.  JC is the same
+// on every CTA of a launch (it depends on seg_max, not on the CTA) and a multiple of the epilogue's
+// row stride nj, so T has the same bits on every CTA and on the plain-load path (n_c odd or more than
+// MAX_SEG_T pieces per CTA).
+__host__ __device__ __forceinline__ bool lr_stage(int nc, int seg_max) { return nc > 0 && (nc % 2) == 0 && seg_max <= MAX_SEG_T; }
+__host__ __device__ __forceinline__ int lr_chunk_rows(int nc, int fuse, int seg_max, size_t ring_bytes, int nj) {
+  const size_t per_row = static_cast<size_t>(fuse ? 2 : 1) * MAXC * 8 + static_cast<size_t>(seg_max) * 8;
+  int jc = static_cast<int>(ring_bytes / per_row) / nj * nj;
+  const int need = (nc + nj - 1) / nj * nj;
+  return jc < need ? jc : need;
+}
+
+// Shared-memory plan (host and device agree): ring | Dp[2] | Acc | Tsm | Esc
 struct PackSmem {
-  size_t ring, dp, acc, tsm, total;
+  size_t ring, dp, acc, tsm, esc, total;
 };
-__host__ __device__ inline PackSmem pack_smem(int slot_tiles, int nstage, int esize, int ld_max, int nt8, int seg_max) {
+__host__ __device__ inline PackSmem pack_smem(int slot_tiles, int nstage, int esize, int ld_max, int nt8, int nm, int pne) {
+  // (T rows: MAX_SEG_T per CTA on the staged path; the plain-load path forms one piece's row at a time)
   PackSmem p;
   const size_t ncp = 1 + 8 * static_cast<size_t>(nt8);
   p.ring = 0;
   size_t o = static_cast<size_t>(nstage) * slot_tiles * 64 * esize;
   o = (o + 127) / 128 * 128;
   p.dp = o;
-  o += 2 * static_cast<size_t>(nt8) * ld_max * PLDP * sizeof(double);
-  p.acc = o;
+  o += 2 * ncp * pk_ldp(ld_max) * sizeof(double);
+  p.acc = o;                                      // block products [ld_max][NCP]; D staging [NCP][ld]
   o += static_cast<size_t>(ld_max) * ncp * sizeof(double);
   p.tsm = o;
-  o += (static_cast<size_t>(seg_max) * MAXC + (PNM + PNE_MAX) * TQ * 16) * sizeof(double);   // T rows + per-warp partials
+  o += static_cast<size_t>(MAX_SEG_T + pne * TQ) * MAXC * sizeof(double);   // T rows + per-warp partials
+  o = (o + 127) / 128 * 128;
+  p.esc = o;
+  o += esc_bytes(nm);
   p.total = o;
   return p;
 }
 
-// The low-rank rows T_q = M'[row(q), :] S(D) need, per CTA, all n_c S rows (128 B each; with S(P_old)
-// for the fused apply) and the CTA's M' rows.  They are staged through the still empty ring in chunks
-// of JC rows of S together with the matching JC-wide segments of the M' rows (TMA path: n_c even and
-// at most MAX_SEG_T pieces); JC is the same on every CTA of a launch.
-__device__ __forceinline__ bool lr_tma(const ApplyArgs& a, int nseg) {
-  return (a.lr_nc % 2) == 0 && nseg <= MAX_SEG_T;
-}
-__device__ __forceinline__ int lr_chunk_rows(const ApplyArgs& a, int esize) {
-  const long ring_bytes = static_cast<long>(a.nstage) * a.slot_tiles * 64 * esize;
-  const long per_row = (a.fuse_p ? 2 : 1) * MAXC * 8 + MAX_SEG_T * 8;   // S (+ S(P_old)) + M' segments
-  return static_cast<int>(ring_bytes / per_row) & ~1;
-}
 
 // Warp-specialised persistent apply: 8 MMA warps stream the CTA's tile blocks, 4 epilogue warps form
 // the next piece's D and run the previous piece's epilogue (and the split-cluster combine, the
@@ -93,8 +112,10 @@ __device__ __forceinline__ int lr_chunk_rows(const ApplyArgs& a, int esize) {
 //   dready[2]                  epilogue -> MMA (D of piece q formed in Dp[q&1])
 //   accready / accfree         MMA -> epilogue (block products of piece q in Acc; Dp[q&1] is free
 //                              again) / epilogue -> MMA (Acc consumed)
-template <int MTMAX, int NT8, typename TB, int PNE>
-__global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(const __grid_constant__ ApplyArgs a) {
+template <int NM, int MTMAX, int NT8, typename TB, int PNE>
+__global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kernel(const __grid_constant__ ApplyArgs a) {
+  constexpr int PNM = NM, PWE = NM;              // MMA warps; the first epilogue warp
+  constexpr int RR = 8 / NM;                     // tile rows / columns per MMA warp in a block
   constexpr int NCP = 1 + 8 * NT8;               // y + probe columns held per row
   constexpr int PWP = PNM + PNE;                 // the TMA producer warp
   if (a.gate && !a.st->any_active) return;
@@ -104,15 +125,22 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
   __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
-  __shared__ __align__(8) uint64_t dready[2], accready, accfree, tfull, tempty;
+  __shared__ __align__(8) uint64_t dready[2], dbar[2], accready, accfree, tfull, tempty;
   __shared__ double ered[PNE_MAX * MAXC];
   __shared__ double cb[2 * MAXC];
   __shared__ int s_last;
-  const PackSmem L_ = pack_smem(a.slot_tiles, a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, a.L.seg_max);
+  const PackSmem L_ = pack_smem(a.slot_tiles, a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, NM, PNE);
   TB* ring = reinterpret_cast<TB*>(smraw + L_.ring);
-  double* Dpb = reinterpret_cast<double*>(smraw + L_.dp);   // [2][NT8][ld_max][PLDP]
+  double* Dpb = reinterpret_cast<double*>(smraw + L_.dp);   // [2][NCP][ldp]
   double* Acc = reinterpret_cast<double*>(smraw + L_.acc);  // [ld_max][NCP] block products of a piece
-  double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // [seg_max][MAXC], then partials
+  double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // T rows [MAX_SEG_T][MAXC], then partials
+  const bool tstage = lr_stage(a.lr_nc, a.L.seg_max);
+  // the staging rounds of the low-rank rows go through the LAST ring slot while the block stream fills
+  // the others (its first block in that slot waits until the rounds are consumed)
+  const size_t slot_bytes = static_cast<size_t>(a.slot_tiles) * 64 * sizeof(TB);
+  const int JC = lr_chunk_rows(a.lr_nc, a.fuse_p, a.L.seg_max, slot_bytes, 2 * PNE);
+  unsigned char* stg_base = smraw + L_.ring + static_cast<size_t>(a.nstage - 1) * slot_bytes;
+  double* Esc = reinterpret_cast<double*>(smraw + L_.esc);  // [PNM][ESPLIT_H][32 lanes][3] thin-row partials
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_pad = a.L.n_pad;
   const int ncol = a.ncol;
@@ -121,16 +149,15 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
   const TB* B = (sizeof(TB) == 4) ? reinterpret_cast<const TB*>(P->B32) : reinterpret_cast<const TB*>(P->B);
   const bool useB = (P->B != nullptr);
   const int nstage = a.nstage, slot_tiles = a.slot_tiles;
-  const int dpstride = NT8 * a.ld_max * PLDP;                // one Dp buffer
-  const int ldD = a.ld_max * PLDP;                           // n8-tile stride within a buffer
+  const int ldp = pk_ldp(a.ld_max);
+  const int dpstride = NCP * ldp;                            // one D buffer
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
   const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.Y2;
-  const double* Dv = a.fuse_p ? Pnew : a.D;                  // the apply's input vector D (fused: P_new)
   if (tid == 0) {
     for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], PNM); }
-    for (int k = 0; k < 2; ++k) mbar_init(&dready[k], 1);
+    for (int k = 0; k < 2; ++k) { mbar_init(&dready[k], 1); mbar_init(&dbar[k], 1); }
     mbar_init(&accready, PNM);
     mbar_init(&accfree, 1);
     mbar_init(&tfull, 1);
@@ -146,57 +173,66 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
   if (wid == PWP) {
     // ================================ TMA producer ================================
     if (lane == 0) {
-      // first, ahead of the block stream: the M' rows of this CTA's pieces (the consumers' low-rank
-      // rows read them right away; behind the stream they would wait in the DRAM queues)
-      if ((a.lr_nc & 1) == 0)                        // (bulk prefetch: 16-byte aligned rows)
+      // first, ahead of the block stream: the M' rows of this CTA's pieces (the epilogue warps' low-rank
+      // rows read them early; behind the stream they would wait in the DRAM queues)
+      if (!tstage && (a.lr_nc & 1) == 0)             // (bulk prefetch: 16-byte aligned rows)
         for (int q = 0; q < nseg; ++q)
           tma_prefetch_l2(P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * a.lr_nc,
                           static_cast<uint32_t>(a.lr_nc) * 8u);
-      // the S rows of the low-rank term (and S(P_old) for the fused apply) and the M' row segments
-      // staged through the still empty ring in chunks of JC rows, before the block stream starts
-      if (lr_tma(a, nseg)) {
-        const int JC = lr_chunk_rows(a, static_cast<int>(sizeof(TB)));
-        double* ringd = reinterpret_cast<double*>(ring);
-        int k = 0;
-        for (int j0 = 0; j0 < a.lr_nc; j0 += JC, ++k) {
-          if (k > 0) mbar_wait(&tempty, static_cast<uint32_t>((k - 1) & 1));
-          const int jn = min(JC, a.lr_nc - j0);
-          const uint32_t bytes = static_cast<uint32_t>(jn) * (MAXC * 8u);
-          const uint32_t mbytes = static_cast<uint32_t>(jn) * 8u;
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&tfull, bytes * (a.fuse_p ? 2u : 1u) + mbytes * nseg);
-          tma_load_1d(ringd, a.S_D + static_cast<int64_t>(j0) * MAXC, bytes, &tfull);
-          if (a.fuse_p) tma_load_1d(ringd + JC * MAXC, a.SPbuf[par] + static_cast<int64_t>(j0) * MAXC, bytes, &tfull);
-          double* mseg = ringd + (a.fuse_p ? 2 : 1) * JC * MAXC;
-          for (int q = 0; q < nseg; ++q)
-            tma_load_1d(mseg + q * JC, P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * a.lr_nc + j0,
-                        mbytes, &tfull);
+      // low-rank staging rounds (JC rows of S (and S(P_old)), the matching M' row segments) into the
+      // last ring slot; issued as the epilogue warps free the slot, polled between tile blocks
+      const int nc = a.lr_nc;
+      const int nround = tstage ? (nc + JC - 1) / JC : 0;
+      int rnd = 0;
+      auto issue_round = [&]() {
+        double* stg = reinterpret_cast<double*>(stg_base);
+        double* mseg = stg + (a.fuse_p ? 2 : 1) * JC * MAXC;
+        const int j0 = rnd * JC, jn = min(JC, nc - j0);
+        const uint32_t sbytes = static_cast<uint32_t>(jn) * (MAXC * 8u), mbytes = static_cast<uint32_t>(jn) * 8u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&tfull, sbytes * (a.fuse_p ? 2u : 1u) + mbytes * static_cast<uint32_t>(nseg));
+        // (the S rows are read by every CTA: sub-copies in a CTA-rotated order spread the L2 load)
+        constexpr int NSUB = 4;
+        const int rows_sub = (jn + NSUB - 1) / NSUB;
+        for (int u = 0; u < NSUB; ++u) {
+          const int sub = (u + b) % NSUB;
+          const int r0 = sub * rows_sub, rn = min(rows_sub, jn - r0);
+          if (rn <= 0) continue;
+          const uint32_t bb = static_cast<uint32_t>(rn) * (MAXC * 8u);
+          tma_load_1d(stg + r0 * MAXC, a.S_D + static_cast<int64_t>(j0 + r0) * MAXC, bb, &tfull);
+          if (a.fuse_p)
+            tma_load_1d(stg + (JC + r0) * MAXC, a.SPbuf[par] + static_cast<int64_t>(j0 + r0) * MAXC, bb, &tfull);
         }
-        mbar_wait(&tempty, static_cast<uint32_t>((k - 1) & 1));   // ring free again
-      }
+        for (int q = 0; q < nseg; ++q)
+          tma_load_1d(mseg + q * JC, P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * nc + j0,
+                      mbytes, &tfull);
+        ++rnd;
+      };
+      auto round_free = [&]() { return mbar_test_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1)); };
+      bool staged_done = nround == 0;
+      auto finish_rounds = [&]() {                   // all rounds issued and consumed
+        if (staged_done) return;
+        while (rnd < nround) {
+          mbar_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1));
+          issue_round();
+        }
+        mbar_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1));
+        staged_done = true;
+      };
+      if (nround > 0) issue_round();
       uint32_t pseq = 0;
-      for (int q = 0; q < nseg; ++q) {
+      for (int q = 0; q < nseg && useB; ++q) {
         const SegDesc sd = a.L.segs[s_lo + q];
         const int i = sd.blk;
         const int ld = a.L.ld[i], mt = ld >> 3;
         const int64_t p0 = a.L.poff[i];
-        // warm L2 with this piece's epilogue inputs and the next piece's D inputs (plain loads later)
+        // warm L2 with this piece's epilogue inputs (plain loads in the epilogue)
         const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
         tma_prefetch_l2(a.u + p0, cbytes);
         for (int c = 0; c < ncol; ++c) {
           if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cbytes);
           if (a.epi == EPI_DOT && Y2 && Y2 != P2) tma_prefetch_l2(Y2 + c * n_pad + p0, cbytes);
         }
-        if (q + 1 < nseg) {
-          const int i1 = a.L.segs[s_lo + q + 1].blk;
-          const int64_t p1 = a.L.poff[i1];
-          const uint32_t cb1 = static_cast<uint32_t>(a.L.ld[i1]) * 8u;
-          for (int c = 0; c < ncol; ++c) {
-            tma_prefetch_l2(a.D + c * n_pad + p1, cb1);
-            if (a.fuse_p) tma_prefetch_l2(Pold + c * n_pad + p1, cb1);
-          }
-        }
-        if (!useB) continue;
         // one chunk per tile block of the piece, in storage order (s-major, g ascending)
         const TB* Bi = B + a.L.pboff[i];
         const int ns = pk_ns(mt);
@@ -205,7 +241,16 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
         for (int k = sd.k0; k < sd.k1; ++k, ++pseq) {
           const int s_ = static_cast<int>(pseq % nstage);
           const uint32_t use = pseq / nstage;
-          if (use > 0) mbar_wait(&empty[s_], (use - 1) & 1u);
+          if (use == 0 && s_ == nstage - 1) finish_rounds();   // the staging slot
+          if (use > 0) {
+            if (rnd < nround) {                      // poll both (neither probe may block)
+              while (!mbar_test_wait(&empty[s_], (use - 1) & 1u))
+                if (rnd < nround && round_free()) issue_round();
+            } else {
+              mbar_wait(&empty[s_], (use - 1) & 1u);
+            }
+          }
+          if (rnd < nround && round_free()) issue_round();
           const int nt = pk_blk_size(gb, sb, mt);
           const uint32_t bytes = static_cast<uint32_t>(nt) * 64u * static_cast<uint32_t>(sizeof(TB));
           fence_proxy_async_smem();
@@ -215,160 +260,19 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
           if (++gb == ns) { ++sb; gb = sb; }
         }
       }
+      finish_rounds();                               // (a short stream never reached the staging slot)
     }
     return;
   }
 
-  // ===================== consumer prologue (MMA + epilogue warps together) =====================
-  constexpr int NCW = PNM + PNE;                     // consumer warps
-  const int ct = tid;                                // 0 .. 32 NCW - 1
-  auto bar_cons_all = [&]() { asm volatile("bar.sync 1, %0;" ::"r"(NCW * 32) : "memory"); };
-  // form D of piece q in Dp[q&1] (fused: D = R + beta o P_old for the active columns, P_new written by
-  // part 0), coalesced over the rows of each column; nthr threads starting at thread t0
-  auto form_d = [&](int q, int t0, int nthr) {
-    const SegDesc sd = a.L.segs[s_lo + q];
-    const int i = sd.blk, ld = a.L.ld[i];
-    const int64_t p0 = a.L.poff[i];
-    double* Dp = Dpb + (q & 1) * dpstride;
-    constexpr int U = 4;                             // elements per thread in flight
-    const int tot = ld * ncol;
-    for (int base = t0; base < tot; base += U * nthr) {
-      double v[U], po[U];
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * nthr;
-        v[u] = 0.0;
-        po[u] = 0.0;
-        if (idx < tot) {
-          const int c = idx / ld, k = idx - c * ld;
-          const int64_t gi = c * n_pad + p0 + k;
-          v[u] = __ldg(a.D + gi);
-          if (a.fuse_p) po[u] = __ldg(Pold + gi);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * nthr;
-        if (idx < tot) {
-          const int c = idx / ld, k = idx - c * ld;
-          double x = v[u];
-          if (a.fuse_p) {
-            x = (cb[MAXC + c] != 0.0) ? x + cb[c] * po[u] : po[u];
-            if (sd.part == 0) Pnew[c * n_pad + p0 + k] = x;
-          }
-          if (useB) Dp[(c == 0) ? k * PLDP + 8 : ((c - 1) >> 3) * ldD + k * PLDP + ((c - 1) & 7)] = x;
-        }
-      }
-    }
-  };
-  // low-rank rows T_q = M'[row(q), :] S(D) for every piece q of this CTA, with S read once per CTA in
-  // coalesced rows: thread ct owns column c = ct % 16 of the S rows j = ct/16 + 2 NCW k (8 in flight),
-  // times M'[row(q), j] for TQ pieces per pass; the row-offsets of each column are summed in fixed
-  // order (lane pairs, then warps) — the same decomposition on every CTA, so a cluster's T has the
-  // same bits wherever it is formed.  All consumer warps take part, before the pipeline starts.
-  {
-    const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-    const double* Mp = P->Mp;
-    const int nc = a.lr_nc;
-    const int c = ct & 15, j0 = ct >> 4;
-    const bool cact = c < ncol;
-    const double bc = cb[c], ac = cb[MAXC + c];
-    double* Tpart = Tsm + a.L.seg_max * MAXC;       // [NCW][TQ][16]
-    // (TMA path: the S rows and the M' row segments arrive through the ring in chunks of JC rows —
-    //  the same chunking on every CTA of a launch; in each chunk a thread takes rows j0, j0 + NJ, ...)
-    constexpr int NJ = 2 * NCW;
-    double t[MAX_SEG_T];
-#pragma unroll
-    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] = 0.0;
-    const bool tma_path = lr_tma(a, nseg);
-    if (tma_path) {
-      const int JC = lr_chunk_rows(a, static_cast<int>(sizeof(TB)));
-      const double* ringd = reinterpret_cast<const double*>(ring);
-      const double* mseg = ringd + (a.fuse_p ? 2 : 1) * JC * MAXC;
-      int k = 0;
-      for (int jc = 0; jc < nc; jc += JC, ++k) {
-        const int jn = min(JC, nc - jc);
-        mbar_wait(&tfull, static_cast<uint32_t>(k & 1));
-        for (int jj = j0; jj < jn; jj += NJ) {
-          double x = 0.0;
-          if (cact) {
-            x = ringd[jj * MAXC + c];
-            if (a.fuse_p) {
-              const double y = ringd[(JC + jj) * MAXC + c];
-              x = (ac != 0.0) ? x + bc * y : y;
-            }
-          }
-#pragma unroll
-          for (int qq = 0; qq < MAX_SEG_T; ++qq)
-            if (qq < nseg) t[qq] = fma(mseg[qq * JC + jj], x, t[qq]);
-        }
-        bar_cons_all();
-        if (ct == 0) mbar_arrive(&tempty);
-      }
-    }
-    // (global path: n_c odd, or more than MAX_SEG_T pieces, e.g. C5's many clusters per CTA)
-    for (int qb = tma_path ? nseg : 0; qb < nseg; ++qb) {
-      const double* Mr = Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + qb].blk) * nc;
-      double tv = 0.0;
-      for (int j = j0; j < nc; j += NJ) {
-        double x = 0.0;
-        if (cact) {
-          x = a.S_D[static_cast<int64_t>(j) * MAXC + c];
-          if (a.fuse_p) {
-            const double y = SPo[static_cast<int64_t>(j) * MAXC + c];
-            x = (ac != 0.0) ? x + bc * y : y;
-          }
-        }
-        tv = fma(__ldg(Mr + j), x, tv);
-      }
-      tv += __shfl_xor_sync(0xffffffffu, tv, 16);
-      if (lane < 16) Tpart[wid * 16 + lane] = tv;
-      bar_cons_all();
-      if (ct < 16) {
-        double acc_ = 0.0;
-        for (int w = 0; w < NCW; ++w) acc_ += Tpart[w * 16 + ct];
-        Tsm[qb * MAXC + ct] = acc_;
-      }
-      bar_cons_all();
-    }
-#pragma unroll
-    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] += __shfl_xor_sync(0xffffffffu, t[qq], 16);
-#pragma unroll
-    for (int qb = 0; qb < MAX_SEG_T; qb += TQ) {
-      if (!tma_path || qb >= nseg) break;
-      if (lane < 16)
-#pragma unroll
-        for (int qq = 0; qq < TQ; ++qq) Tpart[(wid * TQ + qq) * 16 + lane] = t[qb + qq];
-      bar_cons_all();
-      const int nq = min(TQ, min(nseg, MAX_SEG_T) - qb);
-      if (ct < nq * 16) {
-        const int qq = ct >> 4, cc = ct & 15;
-        double acc_ = 0.0;
-        for (int w = 0; w < NCW; ++w) acc_ += Tpart[(w * TQ + qq) * 16 + cc];
-        Tsm[(qb + qq) * MAXC + cc] = acc_;
-      }
-      bar_cons_all();
-    }
-    if (a.fuse_p && b == 0) {
-      // S(P_new) = S(R) + beta o S(P_old) (active columns; S is linear) for the next iteration
-      for (int idx = ct; idx < nc * ncol; idx += NCW * 32) {
-        const int j = idx / ncol, cc = idx - j * ncol;
-        const double x = a.S_D[static_cast<int64_t>(j) * MAXC + cc], y = SPo[static_cast<int64_t>(j) * MAXC + cc];
-        a.SPbuf[par ^ 1][static_cast<int64_t>(j) * MAXC + cc] = (cb[MAXC + cc] != 0.0) ? x + cb[cc] * y : y;
-      }
-    }
-  }
-  if (useB) {                                       // D of the first two pieces (both Dp buffers)
-    for (int q = 0; q < min(2, nseg); ++q) form_d(q, ct, NCW * 32);
-    bar_cons_all();
-  }
 
   if (wid < PNM) {
     // ================================ MMA warps ================================
     if (!useB) return;                               // no block term: the epilogue warps do everything
     const int qr = lane >> 2, qc = lane & 3;
-    const int offD0 = swz(qr, qc), offD1 = swz(qr, 4 + qc);    // A = T:    T[qr][h4 + qc]
-    const int offT0 = swz(qc, qr), offT1 = swz(4 + qc, qr);    // A = T^T:  T[h4 + qc][qr]
+    // k = 2 qc + h: direct A pair T[qr][2qc + h] (one 16-byte load), transposed A T[2qc + h][qr]
+    const int offD = swz(qr, 2 * qc), offT0 = swz(2 * qc, qr), offT1 = swz(2 * qc + 1, qr);
+    const int bo = (1 + qr) * ldp + 2 * qc;          // B pair D[8t + 2qc + h][probe qr] at bo + 8t
     uint32_t seq = 0;
     for (int q = 0; q < nseg; ++q) {
       const SegDesc sd = a.L.segs[s_lo + q];
@@ -383,6 +287,19 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
         for (int n = 0; n < NT8; ++n) { acc[n][0][j] = 0.0; acc[n][1][j] = 0.0; }
       }
       const int ns = pk_ns(mt);
+      // the thin last block row (h <= ESPLIT_H tiles): its direct products are split over the warps by
+      // tile column (warp w: tile (a, w)) instead of all falling to warp a
+      const int hl = pk_h(ns - 1, mt);
+      const bool esplit = NM == 8 && NT8 == 1 && ns > 1 && hl <= ESPLIT_H;
+      double e0[ESPLIT_H][2][NT8], e1[ESPLIT_H][2][NT8], ey[ESPLIT_H];
+#pragma unroll
+      for (int a_ = 0; a_ < ESPLIT_H; ++a_) {
+        ey[a_] = 0.0;
+#pragma unroll
+        for (int e = 0; e < 2; ++e)
+#pragma unroll
+          for (int n = 0; n < NT8; ++n) { e0[a_][e][n] = 0.0; e1[a_][e][n] = 0.0; }
+      }
       int sb = 0, gb = 0;
       for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
       for (int k = sd.k0; k < sd.k1; ++k, ++seq) {
@@ -391,122 +308,129 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
         const int h = pk_h(gb, mt), w = pk_h(sb, mt);
         const bool diag = gb == sb;
         mbar_wait(&full[s_], (seq / nstage) & 1u);
-        // full 8x8-tile block: warp w does, for k = 0..7, the direct tile (w, k) (k <= w on the
-        // diagonal) and the transposed tile (k, w) (k > w on the diagonal) with four independent
-        // accumulator chains (direct / transposed x even / odd k)
-        auto full_block = [&](auto diag_c) {
-          constexpr bool DG = decltype(diag_c)::value;
-          double d0[2][NT8], d1[2][NT8], dy[2] = {0.0, 0.0};
-          double t0[2][NT8], t1[2][NT8], ty[2] = {0.0, 0.0};
+        // one k-tile step: x[hh] += A_hh D[k-tile kt] (hh = 0, 1 independent DMMA chains), and the y column
+        auto step = [&](double (&x0)[2][NT8], double (&x1)[2][NT8], double& xy, double a0, double a1, int kt) {
+          const double* db = Dp + bo + kt * 8;
+#pragma unroll
+          for (int n = 0; n < NT8; ++n) {
+            const double2 bv = *reinterpret_cast<const double2*>(db + n * 8 * ldp);
+            dmma_pk(x0[0][n], x1[0][n], a0, bv.x);
+            dmma_pk(x0[1][n], x1[1][n], a1, bv.y);
+          }
+          const double2 yv = *reinterpret_cast<const double2*>(Dp + kt * 8 + 2 * qc);
+          xy = fma(a1, yv.y, fma(a0, yv.x, xy));
+        };
+        auto fold = [&](double (&x0)[2][NT8], double (&x1)[2][NT8], double& xy, int jt) {
+#pragma unroll
+          for (int j = 0; j < MTMAX; ++j)
+            if (j == jt) {
+#pragma unroll
+              for (int n = 0; n < NT8; ++n) {
+                acc[n][0][j] += x0[0][n] + x0[1][n];
+                acc[n][1][j] += x1[0][n] + x1[1][n];
+              }
+              accy[j] += xy;
+            }
+        };
+        auto zero = [&](double (&x0)[2][NT8], double (&x1)[2][NT8], double& xy) {
 #pragma unroll
           for (int e = 0; e < 2; ++e)
 #pragma unroll
-            for (int n = 0; n < NT8; ++n) { d0[e][n] = 0.0; d1[e][n] = 0.0; t0[e][n] = 0.0; t1[e][n] = 0.0; }
-          const int rowK = 64 * sb, rowI = 64 * gb;          // first D row of the block's columns / rows
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const int e = kk & 1;
-            if (!DG || kk <= wid) {
-              const int pos = DG ? 8 * kk - kk * (kk - 1) / 2 + (wid - kk) : 8 * kk + wid;
-              const TB* tp = blk + pos * 64;
-              const double a0 = ldA(tp + offD0), a1 = ldA(tp + offD1);
-              const double* dr = Dp + (rowK + 8 * kk) * PLDP;
-#pragma unroll
-              for (int n = 0; n < NT8; ++n) {
-                dmma_pk(d0[e][n], d1[e][n], a0, dr[n * ldD + qc * PLDP + qr]);
-                dmma_pk(d0[e][n], d1[e][n], a1, dr[n * ldD + (4 + qc) * PLDP + qr]);
-              }
-              dy[e] = fma(a0, dr[qc * PLDP + 8], dy[e]);
-              dy[e] = fma(a1, dr[(4 + qc) * PLDP + 8], dy[e]);
-            }
-            if (!DG || kk > wid) {
-              const int pos = DG ? 8 * wid - wid * (wid - 1) / 2 + (kk - wid) : 8 * wid + kk;
-              const TB* tp = blk + pos * 64;
-              const double a0 = ldA(tp + offT0), a1 = ldA(tp + offT1);
-              const double* dr = Dp + (rowI + 8 * kk) * PLDP;
-#pragma unroll
-              for (int n = 0; n < NT8; ++n) {
-                dmma_pk(t0[e][n], t1[e][n], a0, dr[n * ldD + qc * PLDP + qr]);
-                dmma_pk(t0[e][n], t1[e][n], a1, dr[n * ldD + (4 + qc) * PLDP + qr]);
-              }
-              ty[e] = fma(a0, dr[qc * PLDP + 8], ty[e]);
-              ty[e] = fma(a1, dr[(4 + qc) * PLDP + 8], ty[e]);
-            }
-          }
-#pragma unroll
-          for (int j = 0; j < MTMAX; ++j) {
-            if (j == gb) {                                    // direct: rows I = 8g + w
-#pragma unroll
-              for (int n = 0; n < NT8; ++n) { acc[n][0][j] += d0[0][n] + d0[1][n]; acc[n][1][j] += d1[0][n] + d1[1][n]; }
-              accy[j] += dy[0] + dy[1];
-            }
-            if (j == sb) {                                    // transposed: columns K = 8s + w
-#pragma unroll
-              for (int n = 0; n < NT8; ++n) { acc[n][0][j] += t0[0][n] + t0[1][n]; acc[n][1][j] += t1[0][n] + t1[1][n]; }
-              accy[j] += ty[0] + ty[1];
-            }
-          }
+            for (int n = 0; n < NT8; ++n) { x0[e][n] = 0.0; x1[e][n] = 0.0; }
+          xy = 0.0;
         };
-        if (h == 8 && w == 8) {
-          if (diag) full_block(std::true_type());
-          else full_block(std::false_type());
-        } else {
-          // edge block (the last block row / column of a cluster whose ld is not a multiple of 64)
-          double x0[NT8], x1[NT8], xy = 0.0;
+        // warp wid does the tile rows / columns wa = wid + NM rr of the block (rr < 8 / NM)
 #pragma unroll
-          for (int n = 0; n < NT8; ++n) { x0[n] = 0.0; x1[n] = 0.0; }
-          if (wid < w) {                                      // transposed: column b = wid
-            const int bcol = wid;
-            const int cbase = diag ? bcol * h - bcol * (bcol - 1) / 2 - bcol : bcol * h;   // tile (a, b) at cbase + a
-            for (int aa = diag ? bcol + 1 : 0; aa < h; ++aa) {
-              const TB* tp = blk + (cbase + aa) * 64;
-              const double a0 = ldA(tp + offT0), a1 = ldA(tp + offT1);
-              const double* dr = Dp + (64 * gb + 8 * aa) * PLDP;
+        for (int rr = 0; rr < RR; ++rr) {
+          const int wa = wid + NM * rr;
+          double d0[2][NT8], d1[2][NT8], dy, t0[2][NT8], t1[2][NT8], ty;
+          zero(d0, d1, dy);
+          zero(t0, t1, ty);
+          if (h == 8 && w == 8) {
+            if (diag) {
+              // diagonal block: row wa of the lower triangle, the tiles (wa, kk) kk <= wa direct and
+              // (kk, wa) kk > wa transposed — both give rows 8g + wa from D rows 8kk (branch-free)
 #pragma unroll
-              for (int n = 0; n < NT8; ++n) {
-                dmma_pk(x0[n], x1[n], a0, dr[n * ldD + qc * PLDP + qr]);
-                dmma_pk(x0[n], x1[n], a1, dr[n * ldD + (4 + qc) * PLDP + qr]);
+              for (int kk = 0; kk < 8; ++kk) {
+                const bool dir = kk <= wa;
+                const int pos = dir ? 8 * kk - kk * (kk - 1) / 2 + (wa - kk) : 8 * wa - wa * (wa - 1) / 2 + (kk - wa);
+                const TB* tp = blk + pos * 64;
+                const double a0 = ldA(tp + (dir ? offD : offT0)), a1 = ldA(tp + (dir ? offD + 1 : offT1));
+                step(d0, d1, dy, a0, a1, 8 * sb + kk);
               }
-              xy = fma(a0, dr[qc * PLDP + 8], xy);
-              xy = fma(a1, dr[(4 + qc) * PLDP + 8], xy);
+              fold(d0, d1, dy, gb * RR + rr);
+            } else {
+              // off-diagonal block: direct tile (wa, kk) -> rows 8g + wa, transposed (kk, wa) -> rows 8s + wa
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                const TB* tpd = blk + (8 * kk + wa) * 64;
+                const double2 ad = ldA2(tpd + offD);
+                step(d0, d1, dy, ad.x, ad.y, 8 * sb + kk);
+                const TB* tpt = blk + (8 * wa + kk) * 64;
+                step(t0, t1, ty, ldA(tpt + offT0), ldA(tpt + offT1), 8 * gb + kk);
+              }
+              fold(d0, d1, dy, gb * RR + rr);
+              fold(t0, t1, ty, sb * RR + rr);
             }
-#pragma unroll
-            for (int j = 0; j < MTMAX; ++j)
-              if (j == sb) {
-#pragma unroll
-                for (int n = 0; n < NT8; ++n) { acc[n][0][j] += x0[n]; acc[n][1][j] += x1[n]; x0[n] = 0.0; x1[n] = 0.0; }
-                accy[j] += xy;
-                xy = 0.0;
+          } else {
+            // edge block (the last block row / column of a cluster whose ld is not a multiple of 64)
+            if (wa < w) {                                     // transposed: column b = wa
+              const int bcol = wa;
+              const int cbase = diag ? bcol * h - bcol * (bcol - 1) / 2 - bcol : bcol * h;   // tile (a, b) at cbase + a
+              for (int aa = diag ? bcol + 1 : 0; aa < h; ++aa) {
+                const TB* tp = blk + (cbase + aa) * 64;
+                step(t0, t1, ty, ldA(tp + offT0), ldA(tp + offT1), 8 * gb + aa);
               }
-          }
-          if (wid < h) {                                      // direct: row a = wid
-            const int arow = wid;
-            const int b_hi = diag ? arow : w - 1;
-            for (int bb = 0; bb <= b_hi; ++bb) {
-              const int pos = diag ? bb * h - bb * (bb - 1) / 2 + (arow - bb) : bb * h + arow;
-              const TB* tp = blk + pos * 64;
-              const double a0 = ldA(tp + offD0), a1 = ldA(tp + offD1);
-              const double* dr = Dp + (64 * sb + 8 * bb) * PLDP;
-#pragma unroll
-              for (int n = 0; n < NT8; ++n) {
-                dmma_pk(x0[n], x1[n], a0, dr[n * ldD + qc * PLDP + qr]);
-                dmma_pk(x0[n], x1[n], a1, dr[n * ldD + (4 + qc) * PLDP + qr]);
-              }
-              xy = fma(a0, dr[qc * PLDP + 8], xy);
-              xy = fma(a1, dr[(4 + qc) * PLDP + 8], xy);
+              fold(t0, t1, ty, sb * RR + rr);
             }
+            if (esplit && !diag) {                            // thin row, split: tiles (a, wa)
 #pragma unroll
-            for (int j = 0; j < MTMAX; ++j)
-              if (j == gb) {
-#pragma unroll
-                for (int n = 0; n < NT8; ++n) { acc[n][0][j] += x0[n]; acc[n][1][j] += x1[n]; }
-                accy[j] += xy;
+              for (int a_ = 0; a_ < ESPLIT_H; ++a_)
+                if (a_ < h) {
+                  const double2 ad = ldA2(blk + (wa * h + a_) * 64 + offD);
+                  step(e0[a_], e1[a_], ey[a_], ad.x, ad.y, 8 * sb + wa);
+                }
+            } else if (wa < h) {                              // direct: row a = wa
+              const int arow = wa;
+              const int b_hi = diag ? arow : w - 1;
+              for (int bb = 0; bb <= b_hi; ++bb) {
+                const int pos = diag ? bb * h - bb * (bb - 1) / 2 + (arow - bb) : bb * h + arow;
+                const double2 ad = ldA2(blk + pos * 64 + offD);
+                step(d0, d1, dy, ad.x, ad.y, 8 * sb + bb);
               }
+              fold(d0, d1, dy, gb * RR + rr);
+            }
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s_]);
         if (++gb == ns) { ++sb; gb = sb; }
+      }
+      if (esplit) {
+        // thin-row partials: every warp publishes, warp a sums them in warp order into its tile row
+        auto bar_mma = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(PNM * 32) : "memory"); };
+#pragma unroll
+        for (int a_ = 0; a_ < ESPLIT_H; ++a_)
+          if (a_ < hl) {
+            double* e = Esc + ((wid * ESPLIT_H + a_) * 32 + lane) * 3;
+            e[0] = e0[a_][0][0] + e0[a_][1][0];
+            e[1] = e1[a_][0][0] + e1[a_][1][0];
+            e[2] = ey[a_];
+          }
+        bar_mma();
+        if (wid < hl) {
+          double s0 = 0.0, s1 = 0.0, sy = 0.0;
+          for (int w2 = 0; w2 < PNM; ++w2) {
+            const double* e = Esc + ((w2 * ESPLIT_H + wid) * 32 + lane) * 3;
+            s0 += e[0];
+            s1 += e[1];
+            sy += e[2];
+          }
+#pragma unroll
+          for (int j = 0; j < MTMAX; ++j)
+            if (j == ns - 1) { acc[0][0][j] += s0; acc[0][1][j] += s1; accy[j] += sy; }
+        }
+        bar_mma();
       }
       // y column: sum the 4 k-lanes of each row quad
 #pragma unroll
@@ -514,7 +438,7 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 1);
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 2);
       }
-      if (q > 0) mbar_wait(&accfree, static_cast<uint32_t>((q - 1) & 1));
+      mbar_wait(&accfree, static_cast<uint32_t>(q & 1));
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
         const int mtj = wid + j * PNM;
@@ -537,91 +461,266 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
   // ================================ epilogue warps ================================
   const int et = tid - PWE * 32;                     // 0 .. 32 PNE - 1
   const int ew = wid - PWE;
-  if (useB && et == 0)
-    for (int q = 0; q < min(2, nseg); ++q) mbar_arrive(&dready[q]);
+  const int NET = PNE * 32;
+  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
+  if (a.fuse_p && b == 0) {
+    // S(P_new) = S(R) + beta o S(P_old) (active columns; S is linear) for the next iteration
+    const int nc = a.lr_nc;
+    for (int idx = et; idx < nc * ncol; idx += NET) {
+      const int j = idx / ncol, cc = idx - j * ncol;
+      const double x = a.S_D[static_cast<int64_t>(j) * MAXC + cc], y = SPo[static_cast<int64_t>(j) * MAXC + cc];
+      a.SPbuf[par ^ 1][static_cast<int64_t>(j) * MAXC + cc] = (cb[MAXC + cc] != 0.0) ? x + cb[cc] * y : y;
+    }
+  }
+  // D of piece q into Dp[q&1] by bulk copies, one per column (fused: R into Dp, P_old staged in Acc);
+  // issued by one thread, completing on dbar[q&1]
+  auto issue_d = [&](int q) {
+    const SegDesc sd = a.L.segs[s_lo + q];
+    const int ld = a.L.ld[sd.blk];
+    const int64_t p0 = a.L.poff[sd.blk];
+    double* Dp = Dpb + (q & 1) * dpstride;
+    const uint32_t bytes = static_cast<uint32_t>(ld) * 8u;
+    fence_proxy_async_smem();
+    mbar_arrive_expect_tx(&dbar[q & 1], bytes * static_cast<uint32_t>(ncol) * (a.fuse_p ? 2u : 1u));
+    for (int c = 0; c < ncol; ++c) {
+      tma_load_1d(Dp + c * ldp, a.D + c * n_pad + p0, bytes, &dbar[q & 1]);
+      if (a.fuse_p) tma_load_1d(Acc + c * ld, Pold + c * n_pad + p0, bytes, &dbar[q & 1]);
+    }
+  };
+  // fused apply: D = R + beta o P_old (active columns), P_old for inactive ones; P_new written by part 0
+  auto fuse_d = [&](int q) {
+    const SegDesc sd = a.L.segs[s_lo + q];
+    const int ld = a.L.ld[sd.blk];
+    const int64_t p0 = a.L.poff[sd.blk];
+    double* Dp = Dpb + (q & 1) * dpstride;
+    for (int idx = et; idx < ld * ncol; idx += NET) {
+      const int c = idx / ld, k = idx - c * ld;
+      const double po = Acc[c * ld + k];
+      const double x = (cb[MAXC + c] != 0.0) ? Dp[c * ldp + k] + cb[c] * po : po;
+      Dp[c * ldp + k] = x;
+      if (sd.part == 0) Pnew[c * n_pad + p0 + k] = x;
+    }
+  };
+  // form D of piece q in Dp[q&1] with plain loads (the apply without a block term)
+  auto form_d = [&](int q) {
+    const SegDesc sd = a.L.segs[s_lo + q];
+    const int ld = a.L.ld[sd.blk];
+    const int64_t p0 = a.L.poff[sd.blk];
+    double* Dp = Dpb + (q & 1) * dpstride;
+    for (int idx = et; idx < ld * ncol; idx += NET) {
+      const int c = idx / ld, k = idx - c * ld;
+      const int64_t gi = c * n_pad + p0 + k;
+      double x = __ldg(a.D + gi);
+      if (a.fuse_p) {
+        const double po = __ldg(Pold + gi);
+        x = (cb[MAXC + c] != 0.0) ? x + cb[c] * po : po;
+        if (sd.part == 0) Pnew[gi] = x;
+      }
+      Dp[c * ldp + k] = x;
+    }
+  };
+  // the D of piece q has landed (fused: combine it); then signal the MMA warps (and release Acc, which
+  // staged P_old: one accfree completion per piece, MMA piece q waits for completion q)
+  auto finish_d = [&](int q, bool rel) {
+    mbar_wait(&dbar[q & 1], static_cast<uint32_t>((q >> 1) & 1));
+    if (a.fuse_p) {
+      fuse_d(q);
+      bar_epi<PNE>();
+    }
+    if (et == 0) {
+      if (rel) mbar_arrive(&accfree);
+      mbar_arrive(&dready[q & 1]);
+    }
+  };
+  if (useB) {
+    // prologue: D of the first two pieces (fused: one at a time, P_old staged in Acc)
+    if (et == 0) {
+      issue_d(0);
+      if (!a.fuse_p && nseg > 1) issue_d(1);
+    }
+    if (a.fuse_p) {
+      finish_d(0, nseg == 1);
+      if (nseg > 1) {
+        if (et == 0) issue_d(1);
+        finish_d(1, true);
+      }
+    } else {
+      if (et == 0) mbar_arrive(&accfree);             // Acc was never a staging buffer
+      finish_d(0, false);
+      if (nseg > 1) finish_d(1, false);
+    }
+  }
+  double* Tpart = Tsm + MAX_SEG_T * MAXC;            // [PNE][TQ][MAXC] per-warp partials
+  // low-rank rows T of pieces [q0, q1) into Tsm[slot0 + ...] (slot0 = 0 on the staged path, q on the
+  // plain-load path).  Thread et owns column c = et % 16 of the S rows j = et/16 + 2 PNE k (fused:
+  // S(D) = S(R) + beta o S(P_old)); the row offsets of each column are summed in fixed order (lane
+  // pairs, then warps): the same decomposition on every CTA and on both paths.
+  auto lr_rows = [&](int slot0, int q0, int q1) {
+    const int nc = a.lr_nc;
+    const int c = et & 15, j0 = et >> 4, NJ = 2 * PNE;
+    const bool cact = c < ncol;
+    const double bc = cb[c], ac = cb[MAXC + c];
+    const int nq = q1 - q0;
+    double t[MAX_SEG_T];
+#pragma unroll
+    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] = 0.0;
+    if (tstage) {
+      const double* stg = reinterpret_cast<const double*>(stg_base);
+      const double* mseg = stg + (a.fuse_p ? 2 : 1) * JC * MAXC;
+      int r = 0;
+      for (int jc = 0; jc < nc; jc += JC, ++r) {
+        const int jn = min(JC, nc - jc);
+        mbar_wait(&tfull, static_cast<uint32_t>(r & 1));
+        for (int jj = j0; jj < jn; jj += NJ) {
+          double x = 0.0;
+          if (cact) {
+            x = stg[jj * MAXC + c];
+            if (a.fuse_p) {
+              const double y = stg[(JC + jj) * MAXC + c];
+              x = (ac != 0.0) ? x + bc * y : y;
+            }
+          }
+#pragma unroll
+          for (int qq = 0; qq < MAX_SEG_T; ++qq)
+            if (qq < nq) t[qq] = fma(mseg[qq * JC + jj], x, t[qq]);
+        }
+        bar_epi<PNE>();
+        if (et == 0) mbar_arrive(&tempty);
+      }
+    } else {
+      const double* Mr = P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q0].blk) * nc;
+      for (int j = j0; j < nc; j += NJ) {
+        double x = 0.0;
+        if (cact) {
+          x = a.S_D[static_cast<int64_t>(j) * MAXC + c];
+          if (a.fuse_p) {
+            const double y = SPo[static_cast<int64_t>(j) * MAXC + c];
+            x = (ac != 0.0) ? x + bc * y : y;
+          }
+        }
+        t[0] = fma(__ldg(Mr + j), x, t[0]);
+      }
+    }
+#pragma unroll
+    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] += __shfl_xor_sync(0xffffffffu, t[qq], 16);
+#pragma unroll
+    for (int qb = 0; qb < MAX_SEG_T; qb += TQ) {
+      if (qb >= nq) break;
+      if (lane < 16)
+#pragma unroll
+        for (int qq = 0; qq < TQ; ++qq) Tpart[(ew * TQ + qq) * MAXC + lane] = t[qb + qq];
+      bar_epi<PNE>();
+      const int nqq = min(TQ, nq - qb);
+      if (et < nqq * 16) {
+        const int qq = et >> 4, cc = et & 15;
+        double acc_ = 0.0;
+        for (int w = 0; w < PNE; ++w) acc_ += Tpart[(w * TQ + qq) * MAXC + cc];
+        Tsm[(slot0 + qb + qq) * MAXC + cc] = acc_;
+      }
+      bar_epi<PNE>();
+    }
+  };
+  if (tstage) lr_rows(0, 0, nseg);
+  int pend = -1;                                     // a piece whose D copy is in flight
   for (int q = 0; q < nseg; ++q) {
     const SegDesc sd = a.L.segs[s_lo + q];
     const int i = sd.blk, ld = a.L.ld[i];
     const int64_t p0 = a.L.poff[i];
+    const double* Dp = Dpb + (q & 1) * dpstride;      // D of this piece (kept until its epilogue)
     if (!useB) {
-      form_d(q, et, PNE * 32);                       // (fused apply without a block term: P_new only)
+      form_d(q);                                     // (no block term: the epilogue warps form D here)
       bar_epi<PNE>();
     }
+    // low-rank row (plain-load path: formed per piece, while the MMA warps stream it)
+    if (!tstage) lr_rows(0, q, q + 1);
+    if (pend >= 0) { finish_d(pend, a.fuse_p); pend = -1; }
+    // register prefetch of this piece's epilogue inputs for the first row of every thread (the
+    // latency hides behind the wait for the MMA warps)
+    const bool pf = et < ld;
+    double pf_u = 0.0, pf_p2[NCP], pf_y2[NCP];
+    if (pf) {
+      pf_u = __ldg(a.u + p0 + et);
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) {
+        const int64_t gi = c * n_pad + p0 + et;
+        const bool on = c < ncol;
+        pf_p2[c] = (on && P2) ? P2[gi] : 0.0;
+        pf_y2[c] = (on && a.epi == EPI_DOT && a.use_par_p2 == 0) ? Y2[gi] : 0.0;
+      }
+    }
+    bool run_epi = true;
     if (useB) {
       mbar_wait(&accready, static_cast<uint32_t>(q & 1));
-      // the MMA warps are done with Dp[q&1]: D of piece q+2 goes there while they stream piece q+1
-      if (q + 2 < nseg) {
-        form_d(q + 2, et, PNE * 32);
-        bar_epi<PNE>();
-        if (et == 0) mbar_arrive(&dready[q & 1]);
-      }
       // split cluster: publish this part's block products; the last part sums all parts in order
       if (sd.nparts > 1) {
         double* base = a.split_part + sd.spoff + static_cast<int64_t>(sd.part) * ld * NCP;
-        for (int idx = et; idx < ld * NCP; idx += PNE * 32) base[idx] = Acc[idx];
+        for (int idx = et; idx < ld * NCP; idx += NET) base[idx] = Acc[idx];
         __threadfence();
         bar_epi<PNE>();
         if (et == 0) s_last = (atomicAdd(&a.split_ticket[sd.tick], 1u) == static_cast<unsigned>(sd.nparts - 1));
         bar_epi<PNE>();
-        if (!s_last) {
-          if (et == 0) mbar_arrive(&accfree);
-          continue;
-        }
-        __threadfence();
-        const double* all = a.split_part + sd.spoff;
-        const int64_t pst = static_cast<int64_t>(ld) * NCP;
-        for (int base = et; base < ld * NCP; base += 2 * PNE * 32) {
-          double v[2][MAX_PARTS];
+        run_epi = s_last != 0;
+        if (run_epi) {
+          __threadfence();
+          const double* all = a.split_part + sd.spoff;
+          const int64_t pst = static_cast<int64_t>(ld) * NCP;
+          for (int base2 = et; base2 < ld * NCP; base2 += 2 * NET) {
+            double v[2][MAX_PARTS];
 #pragma unroll
-          for (int u = 0; u < 2; ++u)
+            for (int u = 0; u < 2; ++u)
 #pragma unroll
-            for (int pp = 0; pp < MAX_PARTS; ++pp) {
-              const int idx = base + u * PNE * 32;
-              v[u][pp] = (idx < ld * NCP && pp < sd.nparts) ? __ldcg(all + pp * pst + idx) : 0.0;
-            }
+              for (int pp = 0; pp < MAX_PARTS; ++pp) {
+                const int idx = base2 + u * NET;
+                v[u][pp] = (idx < ld * NCP && pp < sd.nparts) ? __ldcg(all + pp * pst + idx) : 0.0;
+              }
 #pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int idx = base + u * PNE * 32;
-            if (idx < ld * NCP) {
-              double acc_ = v[u][0];
-              for (int pp = 1; pp < sd.nparts; ++pp) acc_ += v[u][pp];
-              Acc[idx] = acc_;
+            for (int u = 0; u < 2; ++u) {
+              const int idx = base2 + u * NET;
+              if (idx < ld * NCP) {
+                double acc_ = v[u][0];
+                for (int pp = 1; pp < sd.nparts; ++pp) acc_ += v[u][pp];
+                Acc[idx] = acc_;
+              }
             }
           }
+          if (et == 0) a.split_ticket[sd.tick] = 0u;
         }
-        if (et == 0) a.split_ticket[sd.tick] = 0u;
-        bar_epi<PNE>();
       }
     } else if (sd.part != 0) {
-      continue;                                      // no block term: part 0 holds the whole result
+      run_epi = false;                               // no block term: part 0 holds the whole result
     }
-    // epilogue: thread et owns rows r = et, et + 128, ... (coalesced over r for every column c)
+    bar_epi<PNE>();                                  // T row (and the combined Acc) visible
+    // epilogue: thread et owns rows r = et, et + 32 PNE, ...; D from Dp (shared), the block products
+    // from Acc, the other inputs from global (coalesced over r for every column c)
     double ep[NCP];
 #pragma unroll
     for (int c = 0; c < NCP; ++c) ep[c] = 0.0;
-    {
+    if (run_epi) {
       const double bi = P->b0 + P->b1 * a.jitter[i];
       const double pa = P->a, ms = P->mscale;
-      const double* Tq = Tsm + q * MAXC;
-      // loads of a row first (all columns in flight), then the arithmetic
-      for (int r = et; r < ld; r += PNE * 32) {
-        const double uu = __ldg(a.u + p0 + r);
-        double dv[NCP], p2v[NCP], y2v[NCP];
+      for (int r = et; r < ld; r += NET) {
+        double uu, p2v[NCP], y2v[NCP];
+        if (r == et) {
+          uu = pf_u;
 #pragma unroll
-        for (int c = 0; c < NCP; ++c) {
-          const int64_t gi = c * n_pad + p0 + r;
-          const bool on = c < ncol;
-          dv[c] = on ? Dv[gi] : 0.0;
-          p2v[c] = (on && P2) ? P2[gi] : 0.0;
-          y2v[c] = (on && a.epi == EPI_DOT && a.use_par_p2 == 0) ? Y2[gi] : 0.0;
+          for (int c = 0; c < NCP; ++c) { p2v[c] = pf_p2[c]; y2v[c] = pf_y2[c]; }
+        } else {
+          uu = __ldg(a.u + p0 + r);
+#pragma unroll
+          for (int c = 0; c < NCP; ++c) {
+            const int64_t gi = c * n_pad + p0 + r;
+            const bool on = c < ncol;
+            p2v[c] = (on && P2) ? P2[gi] : 0.0;
+            y2v[c] = (on && a.epi == EPI_DOT && a.use_par_p2 == 0) ? Y2[gi] : 0.0;
+          }
         }
 #pragma unroll
         for (int c = 0; c < NCP; ++c) {
           if (c >= ncol) continue;
-          const double d = dv[c];
+          const double d = Dp[c * ldp + r];
           double val = pa * d;
           if (useB) val += bi * Acc[r * NCP + c];
-          val += uu * (ms * Tq[c]);
+          val += uu * (ms * Tsm[(tstage ? q : 0) * MAXC + c]);
           double o = a.cA[c] * val + a.cV[c] * d;
           if (P2) o += a.cP[c] * p2v[c];
           a.out[c * n_pad + p0 + r] = o;
@@ -631,10 +730,20 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
       }
     }
     if (useB) {
-      bar_epi<PNE>();                                     // all reads of Acc done
-      if (et == 0) mbar_arrive(&accfree);
+      bar_epi<PNE>();                                // all reads of Acc, Dp[q&1] and the T row done
+      // D of piece q+2 into Dp[q&1]: copies issued now, completed (and combined) after T_{q+1}
+      if (q + 2 < nseg) {
+        if (et == 0) {
+          issue_d(q + 2);
+          if (!a.fuse_p) mbar_arrive(&accfree);       // (fused: Acc stages P_old until finish_d)
+        }
+        pend = q + 2;
+      } else if (et == 0) {
+        mbar_arrive(&accfree);
+      }
     }
-    // per-cluster column sums: warp butterflies, then the 4 warps in fixed order
+    if (!run_epi) continue;
+    // per-cluster column sums: warp butterflies, then the warps in fixed order
 #pragma unroll
     for (int c = 0; c < NCP; ++c) ep[c] = warp_sum(ep[c]);
     if (lane == 0)
@@ -647,7 +756,7 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
       if (a.epi == EPI_S) a.Sout[static_cast<int64_t>(i) * MAXC + et] = s;
       else a.dots[static_cast<int64_t>(i) * MAXC + et] = s;
     }
-    bar_epi<PNE>();                                       // ered reuse
+    bar_epi<PNE>();                                  // ered reuse
   }
   // finaliser (last CTA; one epilogue warp per column)
   if (a.fin != FIN_NONE) {
@@ -666,7 +775,7 @@ __global__ void __launch_bounds__((PNM + PNE + 1) * 32, 1) apply_packed_kernel(c
 
 // --------------------------------------------------------------------------------------- host
 bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a) {
-  // the ring slot holds one tile block (<= 64 tiles); at least 2 slots
+  (void)seg_max;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
@@ -678,36 +787,35 @@ bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a
   a.f32 = f32 ? 1 : 0;
   a.ld_max = ld_max;
   const int es = f32 ? 4 : 8;
+  const int slot = 64;                                       // a ring slot holds one tile block
+  const int pne = (a.mtmax <= 4) ? 7 : 4;
   const size_t budget = static_cast<size_t>(optin) - 8192;   // static shared memory + margin
-  for (int slot : {64}) {
-    const PackSmem fixed = pack_smem(slot, 0, es, ld_max, a.nt8, seg_max);
-    if (fixed.total >= budget) continue;
-    const int ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(slot) * 64 * es)));
-    if (ns >= 2) {
-      a.slot_tiles = slot;
-      a.nstage = ns;
-      a.smem = pack_smem(slot, ns, es, ld_max, a.nt8, seg_max).total;
-      return true;
-    }
-  }
-  return false;
+  const PackSmem fixed = pack_smem(slot, 0, es, ld_max, a.nt8, 8, pne);
+  if (fixed.total >= budget) return false;
+  const int ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(slot) * 64 * es)));
+  if (ns < 2) return false;
+  a.slot_tiles = slot;
+  a.nstage = ns;
+  a.smem = pack_smem(slot, ns, es, ld_max, a.nt8, 8, pne).total;
+  return true;
 }
 
-template <int MT, int N8, typename TB>
+template <int NM, int MT, int N8, typename TB>
 static void launch_pk(const ApplyArgs& a, cudaStream_t s) {
-  constexpr int NE = (MT <= 4) ? 7 : 4;      // 16 or 13 warps: <= 4 per SM sub-partition (128 registers)
-  auto k = apply_packed_kernel<MT, N8, TB, NE>;
+  // 16 or 13 warps (<= 4 per SM sub-partition: 128 registers), one CTA per SM
+  constexpr int NE = (MT <= 4) ? 7 : 4;
+  auto k = apply_packed_kernel<NM, MT, N8, TB, NE>;
   smem_optin(reinterpret_cast<const void*>(k));
-  k<<<a.grid, (PNM + NE + 1) * 32, a.smem, s>>>(a);
+  k<<<a.grid, (NM + NE + 1) * 32, a.smem, s>>>(a);
 }
 
 void launch_apply_packed(const ApplyArgs& a, cudaStream_t s) {
 #define NUGPR_PK(MT)                                                        \
   do {                                                                      \
     if (a.nt8 == 1) {                                                       \
-      if (a.f32) launch_pk<MT, 1, float>(a, s); else launch_pk<MT, 1, double>(a, s); \
+      if (a.f32) launch_pk<8, MT, 1, float>(a, s); else launch_pk<8, MT, 1, double>(a, s); \
     } else {                                                                \
-      launch_pk<MT, 2, double>(a, s);                                       \
+      launch_pk<8, MT, 2, double>(a, s);                                    \
     }                                                                       \
   } while (0)
   if (a.mtmax == 2) NUGPR_PK(2);

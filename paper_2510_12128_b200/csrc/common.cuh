@@ -34,8 +34,14 @@ constexpr int CTW = 16;         // columns per task of the DMMA column apply
 // ordered column-block-major (s = 0.., then g = s..).  One block is one TMA chunk of the apply,
 // and in it warp w does exactly the products of row a = w (out_I += T D_K) and column b = w
 // (out_K += T^T D_I): regular, balanced work with no per-tile index search.  Diagonal tiles are
-// stored full.  The swizzle makes the DMMA fragment loads of both T and T^T bank-conflict-free.
-__host__ __device__ __forceinline__ int swz(int r, int c) { return 8 * r + (c ^ (((r >> 1) & 1) << 2)); }
+// stored full.  Within a tile, element (r, c) sits in 16-byte chunk pk_chunk(r, c/2) at half c&1:
+// the DMMA splits k = 8 into k = 2 qc + h (h = 0, 1), so lane (qr, qc) reads its direct A pair
+// T[qr][2qc..2qc+1] with one 16-byte load, and the chunk order (rows in pairs, columns XOR-rotated,
+// parity-interleaved) makes both that load and the transposed loads T[2qc+h][qr] bank-conflict-free.
+__host__ __device__ __forceinline__ int pk_chunk(int r, int j) {
+  return 8 * (r >> 1) + ((j ^ ((r >> 1) & 3)) + 4 * ((r + j) & 1));
+}
+__host__ __device__ __forceinline__ int swz(int r, int c) { return 2 * pk_chunk(r, c >> 1) + (c & 1); }
 __host__ __device__ __forceinline__ int64_t tri_tiles(int mt) { return static_cast<int64_t>(mt) * (mt + 1) / 2; }
 __host__ __device__ __forceinline__ int pk_ns(int mt) { return (mt + 7) >> 3; }                 // block rows
 __host__ __device__ __forceinline__ int pk_h(int x, int mt) { return (mt - 8 * x < 8) ? mt - 8 * x : 8; }
