@@ -46,18 +46,23 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(verbose: bool = False, ptxas_v: bool = False) -> str:
-    os.makedirs(BUILD, exist_ok=True)
+def build(verbose: bool = False, ptxas_v: bool = False, trace: bool = False) -> str:
+    """trace=True: the diagnostics variant libnugpr_trace.so (per-CTA globaltimer stamps of one
+    packed apply, tools/apply_trace.py); never loaded by the package itself."""
+    build_dir = BUILD + ("_trace" if trace else "")
+    lib_path = LIB.replace(".so", "_trace.so") if trace else LIB
+    extra = ["-DNUGPR_TRACE_APPLY"] if trace else []
+    os.makedirs(build_dir, exist_ok=True)
     nv = nvcc()
     hdrs = _headers()
     objs = []
     jobs = []
     for src in SOURCES:
         sp = os.path.join(CSRC, src)
-        obj = os.path.join(BUILD, src.replace(".cu", ".o"))
+        obj = os.path.join(build_dir, src.replace(".cu", ".o"))
         objs.append(obj)
         if _stale(obj, [sp] + hdrs):
-            cmd = [nv, *ARCH, *FLAGS, "-c", sp, "-o", obj]
+            cmd = [nv, *ARCH, *FLAGS, *extra, "-c", sp, "-o", obj]
             if ptxas_v:
                 cmd += ["-Xptxas", "-v"]
             jobs.append(cmd)
@@ -67,16 +72,15 @@ def build(verbose: bool = False, ptxas_v: bool = False) -> str:
                 sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
             if res.returncode != 0:
                 raise RuntimeError(f"nvcc failed for {cmd[-3]}")
-    if _stale(LIB, objs):
-        cmd = [nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", LIB, *objs, "-cudart", "static"]
+    if _stale(lib_path, objs):
+        cmd = [nv, *ARCH, "-shared", "-Xcompiler", "-fPIC", "-o", lib_path, *objs, "-cudart", "static"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if verbose or res.returncode != 0:
             sys.stderr.write(" ".join(cmd) + "\n" + res.stdout + res.stderr)
         if res.returncode != 0:
             raise RuntimeError("link failed")
-    return LIB
+    return lib_path
 
 
 if __name__ == "__main__":
-    build(verbose="--verbose" in sys.argv, ptxas_v="--ptxas" in sys.argv)
-    print(LIB)
+    print(build(verbose="--verbose" in sys.argv, ptxas_v="--ptxas" in sys.argv, trace="--trace" in sys.argv))

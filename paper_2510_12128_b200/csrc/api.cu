@@ -96,20 +96,26 @@ static void make_partition(HostLayout& L) {
     for (int i = 0; i < n_c; ++i) {
       const int mt = L.ld[i] / 8, ns = pk_ns(mt);
       int bi = 0;
+      int64_t loc = 0;                               // tiles of cluster i before block bi (storage order)
       for (int sb = 0; sb < ns; ++sb)
         for (int gb = sb; gb < ns; ++gb, ++bi) {
           const int64_t len = pk_blk_size(gb, sb, mt);
           const int cta = static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + len) * G / (2 * total)));
+          const SegDesc fresh{i, bi, bi + 1, 0, 0, -1, 0, L.pboff[i] / 64 + loc, static_cast<int32_t>(len), 0};
           if (cta != cur) {                          // a new CTA starts here
             L.seg0.push_back(static_cast<int32_t>(L.segs.size()));
             cur = cta;
-            L.segs.push_back(SegDesc{i, bi, bi + 1, parts[i]++, 0, -1, 0});
+            L.segs.push_back(fresh);
+            L.segs.back().part = parts[i]++;
           } else if (L.segs.back().blk != i) {       // same CTA, next cluster
-            L.segs.push_back(SegDesc{i, bi, bi + 1, parts[i]++, 0, -1, 0});
+            L.segs.push_back(fresh);
+            L.segs.back().part = parts[i]++;
           } else {
             L.segs.back().k1 = bi + 1;
+            L.segs.back().ntile += static_cast<int32_t>(len);
           }
           cum += len;
+          loc += len;
         }
     }
     L.seg0.push_back(static_cast<int32_t>(L.segs.size()));
@@ -1267,6 +1273,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
   memset(&ua, 0, sizeof(ua));
   ua.L = Ld; ua.prm = e.prm; ua.st = e.st; ua.u = B.u; ua.X = e.X; ua.R = e.R; ua.Q = e.Q;
   ua.Pbuf[0] = e.Pb[0]; ua.Pbuf[1] = e.Pb[1]; ua.rr_part = e.rrp; ua.SR_part = e.SR;
+  ua.SPbuf[0] = e.SPb[0]; ua.SPbuf[1] = e.SPb[1];
   ua.beta_hist = e.bh; ua.hist_stride = HIST; ua.ncol = ncol; ua.cond = 0;
   ApplyArgs& a3 = A.a3;
   a3 = a1;
@@ -1520,7 +1527,7 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
         launch_fin(FIN_ALPHA, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, e.ah, HIST, s);
         PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
         RET(xchg(ctx, xs, xr, 2 * XG, s));                                    // r^T r, S(r)
-        launch_fin(FIN_UPDATE, e.st, e.prm, xr, bl->n_cg, ncol, e.bh, HIST, s);
+        launch_fin(FIN_UPDATE, e.st, e.prm, xr, bl->n_cg, ncol, e.bh, HIST, s, xr + XG, e.SPb[0], e.SPb[1]);
       }
       CKL();
       CK(cudaMemcpyAsync(ctx->h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));

@@ -23,9 +23,11 @@
 //    (ticket) sums them in part order — deterministic — and runs the epilogue.
 //  * The low-rank coefficients T_i = M'[i,:] S(D) (Eq. 19-21) are formed by the consumer warps at
 //    kernel start from the previous kernel's per-cluster S rows, while the producer fills the ring:
-//    no separate low-rank launch (the fused first apply also forms S(P_new) = S(R) + beta S(P_old)).
+//    no separate low-rank launch (for the fused first apply the update finaliser has formed the rows
+//    S(P_new) = S(R) + beta S(P_old) already).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <type_traits>
 
@@ -36,15 +38,40 @@
 
 namespace nugpr {
 
+#ifdef NUGPR_TRACE_APPLY
+// diagnostics build only (build.py --trace): globaltimer stamps of one launch, per CTA
+constexpr int TRACE_W = 64;
+__device__ unsigned long long g_apply_trace[PACK_CTAS][TRACE_W];
+__device__ int g_apply_trace_on;
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define TR(idx) do { if (g_apply_trace_on && (idx) < TRACE_W) g_apply_trace[blockIdx.x][(idx)] = gtimer(); } while (0)
+#define TRV(idx, v) do { if (g_apply_trace_on) g_apply_trace[blockIdx.x][(idx)] = (v); } while (0)
+#define TCLK(v) (v) = clock64()
+#define TACC(idx, v) do { tacc_[(idx) - 48] += (v); } while (0)
+#define TACC_DECL long long tacc_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#define TACC_FLUSH do { if (g_apply_trace_on && wid == 0 && lane == 0) for (int i_ = 0; i_ < 8; ++i_) g_apply_trace[blockIdx.x][48 + i_] = tacc_[i_]; } while (0)
+#else
+#define TCLK(v) do {} while (0)
+#define TACC(idx, v) do {} while (0)
+#define TACC_DECL
+#define TACC_FLUSH do {} while (0)
+#define TR(idx) do {} while (0)
+#define TRV(idx, v) do {} while (0)
+#endif
+
 // NM MMA warps (8), warp w owning the output m-tiles w, w+NM, ...; a block's tile rows / columns
 // w + NM rr (rr < 8 / NM)
-constexpr int PNE_MAX = 7;             // epilogue / prologue warps: 7 (ld <= 256) or 4 (ld <= 512), register budget
+constexpr int PNE_MAX = 7;             // epilogue warps
 // split-k of the thin last block row (height <= ESPLIT_H tiles): per-warp partials, reduced in fixed
 // warp order through ESC at the end of the piece
 constexpr int ESPLIT_H = 2;
 __host__ __device__ constexpr int esc_bytes(int nm) { return nm == 8 ? 8 * ESPLIT_H * 32 * 3 * 8 : 0; }
-constexpr int TQ = 4;                  // pieces per reduction pass of the low-rank rows
-constexpr int MAX_SEG_T = 8;           // pieces per CTA whose low-rank rows are formed from staged S rows
+constexpr int LRG = 4;                 // pieces per pass of the low-rank rows (LRG x 4 accumulators per thread)
+constexpr int CHUNK = 64;              // tiles per ring chunk (32 KB FP64)
 
 // (not volatile: a pure function of its operands, so the compiler may schedule it freely)
 __device__ __forceinline__ void dmma_pk(double& d0, double& d1, double a, double b) {
@@ -66,37 +93,24 @@ __device__ __forceinline__ double2 ldA2(const float* p) {
 // 16-byte B-pair loads D[8t + 2qc + h][col qr] of a quarter warp (rows qr = 2t', 2t'+1) hit all banks
 __host__ __device__ __forceinline__ int pk_ldp(int ld_max) { return ((ld_max + 15) & ~15) + 8; }
 
-// The low-rank rows T_q = M'[row(q), :] S(D) of all the CTA's pieces are formed first, from the S rows
-// (and S(P_old) for the fused apply) and the CTA's M' row segments staged through the (still empty)
-// ring in rounds of JC rows — one round trip at C3 — before the block stream starts.  JC is the same
-// on every CTA of a launch (it depends on seg_max, not on the CTA) and a multiple of the epilogue's
-// row stride nj, so T has the same bits on every CTA and on the plain-load path (n_c odd or more than
-// MAX_SEG_T pieces per CTA).
-__host__ __device__ __forceinline__ bool lr_stage(int nc, int seg_max) { return nc > 0 && (nc % 2) == 0 && seg_max <= MAX_SEG_T; }
-__host__ __device__ __forceinline__ int lr_chunk_rows(int nc, int fuse, int seg_max, size_t ring_bytes, int nj) {
-  const size_t per_row = static_cast<size_t>(fuse ? 2 : 1) * MAXC * 8 + static_cast<size_t>(seg_max) * 8;
-  int jc = static_cast<int>(ring_bytes / per_row) / nj * nj;
-  const int need = (nc + nj - 1) / nj * nj;
-  return jc < need ? jc : need;
-}
-
-// Shared-memory plan (host and device agree): ring | Dp[2] | Acc | Tsm | Esc
+// Shared-memory plan (host and device agree): ring | Dp[2] | Acc | Tsm (T rows of every piece, then
+// the per-warp partials of one pass) | Esc
 struct PackSmem {
   size_t ring, dp, acc, tsm, esc, total;
 };
-__host__ __device__ inline PackSmem pack_smem(int slot_tiles, int nstage, int esize, int ld_max, int nt8, int nm, int pne) {
-  // (T rows: MAX_SEG_T per CTA on the staged path; the plain-load path forms one piece's row at a time)
+__host__ __device__ inline PackSmem pack_smem(int nstage, int esize, int ld_max, int nt8, int nm, int pne, int seg_max,
+                                              int nacc) {
   PackSmem p;
   const size_t ncp = 1 + 8 * static_cast<size_t>(nt8);
   p.ring = 0;
-  size_t o = static_cast<size_t>(nstage) * slot_tiles * 64 * esize;
+  size_t o = static_cast<size_t>(nstage) * CHUNK * 64 * esize;
   o = (o + 127) / 128 * 128;
   p.dp = o;
   o += 2 * ncp * pk_ldp(ld_max) * sizeof(double);
-  p.acc = o;                                      // block products [ld_max][NCP]; D staging [NCP][ld]
-  o += static_cast<size_t>(ld_max) * ncp * sizeof(double);
+  p.acc = o;                                      // nacc x block products [ld_max][NCP]; P_old staging [NCP][ld]
+  o += static_cast<size_t>(nacc) * ld_max * ncp * sizeof(double);
   p.tsm = o;
-  o += static_cast<size_t>(MAX_SEG_T + pne * TQ) * MAXC * sizeof(double);   // T rows + per-warp partials
+  o += static_cast<size_t>(seg_max + pne * LRG) * MAXC * sizeof(double);
   o = (o + 127) / 128 * 128;
   p.esc = o;
   o += esc_bytes(nm);
@@ -105,13 +119,15 @@ __host__ __device__ inline PackSmem pack_smem(int slot_tiles, int nstage, int es
 }
 
 
-// Warp-specialised persistent apply: 8 MMA warps stream the CTA's tile blocks, 4 epilogue warps form
-// the next piece's D and run the previous piece's epilogue (and the split-cluster combine, the
-// low-rank rows, the finaliser), 1 warp drives the TMA ring.  Handshakes (mbarriers):
-//   full / empty [ring]        producer <-> MMA warps (one tile block per slot)
+// Warp-specialised persistent apply: 8 MMA warps stream the CTA's tile blocks, the epilogue warps form
+// the next piece's D, the low-rank rows and the previous piece's epilogue (and the split-cluster
+// combine, the finaliser), 1 warp drives the TMA ring.  Handshakes (mbarriers):
+//   full / empty [nstage]      producer <-> MMA warps (one 64-tile chunk of the stream per slot)
 //   dready[2]                  epilogue -> MMA (D of piece q formed in Dp[q&1])
-//   accready / accfree         MMA -> epilogue (block products of piece q in Acc; Dp[q&1] is free
-//                              again) / epilogue -> MMA (Acc consumed)
+//   accready / accfree [2]     MMA -> epilogue (block products of piece q in Acc[q % nacc]; Dp[q&1]
+//                              is free again) / epilogue -> MMA (Acc[x] consumed).  With nacc = 2
+//                              the MMA warps run a piece ahead of the epilogue (whose first piece
+//                              waits for the low-rank rows)
 template <int NM, int MTMAX, int NT8, typename TB, int PNE>
 __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kernel(const __grid_constant__ ApplyArgs a) {
   constexpr int PNM = NM, PWE = NM;              // MMA warps; the first epilogue warp
@@ -125,21 +141,17 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
   __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
-  __shared__ __align__(8) uint64_t dready[2], dbar[2], accready, accfree, tfull, tempty;
+  __shared__ __align__(8) uint64_t dready[2], dbar[2], accready[2], accfree[2];
   __shared__ double ered[PNE_MAX * MAXC];
   __shared__ double cb[2 * MAXC];
   __shared__ int s_last;
-  const PackSmem L_ = pack_smem(a.slot_tiles, a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, NM, PNE);
+  const int nacc = a.nacc;
+  const PackSmem L_ = pack_smem(a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, NM, PNE, a.L.seg_max, nacc);
   TB* ring = reinterpret_cast<TB*>(smraw + L_.ring);
   double* Dpb = reinterpret_cast<double*>(smraw + L_.dp);   // [2][NCP][ldp]
-  double* Acc = reinterpret_cast<double*>(smraw + L_.acc);  // [ld_max][NCP] block products of a piece
-  double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // T rows [MAX_SEG_T][MAXC], then partials
-  const bool tstage = lr_stage(a.lr_nc, a.L.seg_max);
-  // the staging rounds of the low-rank rows go through the LAST ring slot while the block stream fills
-  // the others (its first block in that slot waits until the rounds are consumed)
-  const size_t slot_bytes = static_cast<size_t>(a.slot_tiles) * 64 * sizeof(TB);
-  const int JC = lr_chunk_rows(a.lr_nc, a.fuse_p, a.L.seg_max, slot_bytes, 2 * PNE);
-  unsigned char* stg_base = smraw + L_.ring + static_cast<size_t>(a.nstage - 1) * slot_bytes;
+  double* Accb = reinterpret_cast<double*>(smraw + L_.acc); // nacc x [ld_max][NCP] block products of a piece
+  const int accstride = a.ld_max * NCP;
+  double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // T rows [seg_max][MAXC], then partials
   double* Esc = reinterpret_cast<double*>(smraw + L_.esc);  // [PNM][ESPLIT_H][32 lanes][3] thin-row partials
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_pad = a.L.n_pad;
@@ -148,7 +160,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   const int par = a.st->par;
   const TB* B = (sizeof(TB) == 4) ? reinterpret_cast<const TB*>(P->B32) : reinterpret_cast<const TB*>(P->B);
   const bool useB = (P->B != nullptr);
-  const int nstage = a.nstage, slot_tiles = a.slot_tiles;
+  const int nstage = a.nstage;
   const int ldp = pk_ldp(a.ld_max);
   const int dpstride = NCP * ldp;                            // one D buffer
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
@@ -156,12 +168,11 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.Y2;
   if (tid == 0) {
+    TR(0);
+    TRV(46, nseg);
     for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], PNM); }
     for (int k = 0; k < 2; ++k) { mbar_init(&dready[k], 1); mbar_init(&dbar[k], 1); }
-    mbar_init(&accready, PNM);
-    mbar_init(&accfree, 1);
-    mbar_init(&tfull, 1);
-    mbar_init(&tempty, 1);
+    for (int k = 0; k < 2; ++k) { mbar_init(&accready[k], PNM); mbar_init(&accfree[k], 1); }
     fence_mbar_init();
   }
   if (tid < MAXC) {
@@ -170,97 +181,73 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   }
   __syncthreads();
 
+  // registers: the two MMA warpgroups take 168 per thread, the epilogue / producer warpgroup 88
+  // (entry: 128 x 16 warps = the whole register file); the MMA block loop needs the headroom to issue
+  // its shared-memory operand loads ahead of the DMMAs
+  static_assert(NM == 8 && PNE == 7, "setmaxnreg split assumes warpgroups {MMA, MMA, epilogue+producer}");
+  if (wid < PNM) asm volatile("setmaxnreg.inc.sync.aligned.u32 168;\n" ::: "memory");
+  else asm volatile("setmaxnreg.dec.sync.aligned.u32 88;\n" ::: "memory");
+
   if (wid == PWP) {
     // ================================ TMA producer ================================
-    if (lane == 0) {
-      // first, ahead of the block stream: the M' rows of this CTA's pieces (the epilogue warps' low-rank
-      // rows read them early; behind the stream they would wait in the DRAM queues)
-      if (!tstage && (a.lr_nc & 1) == 0)             // (bulk prefetch: 16-byte aligned rows)
+    if (lane == 0 && nseg > 0) {
+      // the M' rows of this CTA's pieces (the epilogue warps' low-rank rows read them early; behind
+      // the block stream they would wait in the DRAM queues)
+      if ((a.lr_nc & 1) == 0)                       // (bulk prefetch: 16-byte aligned rows)
         for (int q = 0; q < nseg; ++q)
           tma_prefetch_l2(P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * a.lr_nc,
                           static_cast<uint32_t>(a.lr_nc) * 8u);
-      // low-rank staging rounds (JC rows of S (and S(P_old)), the matching M' row segments) into the
-      // last ring slot; issued as the epilogue warps free the slot, polled between tile blocks
-      const int nc = a.lr_nc;
-      const int nround = tstage ? (nc + JC - 1) / JC : 0;
-      int rnd = 0;
-      auto issue_round = [&]() {
-        double* stg = reinterpret_cast<double*>(stg_base);
-        double* mseg = stg + (a.fuse_p ? 2 : 1) * JC * MAXC;
-        const int j0 = rnd * JC, jn = min(JC, nc - j0);
-        const uint32_t sbytes = static_cast<uint32_t>(jn) * (MAXC * 8u), mbytes = static_cast<uint32_t>(jn) * 8u;
-        fence_proxy_async_smem();
-        mbar_arrive_expect_tx(&tfull, sbytes * (a.fuse_p ? 2u : 1u) + mbytes * static_cast<uint32_t>(nseg));
-        // (the S rows are read by every CTA: sub-copies in a CTA-rotated order spread the L2 load)
-        constexpr int NSUB = 4;
-        const int rows_sub = (jn + NSUB - 1) / NSUB;
-        for (int u = 0; u < NSUB; ++u) {
-          const int sub = (u + b) % NSUB;
-          const int r0 = sub * rows_sub, rn = min(rows_sub, jn - r0);
-          if (rn <= 0) continue;
-          const uint32_t bb = static_cast<uint32_t>(rn) * (MAXC * 8u);
-          tma_load_1d(stg + r0 * MAXC, a.S_D + static_cast<int64_t>(j0 + r0) * MAXC, bb, &tfull);
-          if (a.fuse_p)
-            tma_load_1d(stg + (JC + r0) * MAXC, a.SPbuf[par] + static_cast<int64_t>(j0 + r0) * MAXC, bb, &tfull);
-        }
-        for (int q = 0; q < nseg; ++q)
-          tma_load_1d(mseg + q * JC, P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * nc + j0,
-                      mbytes, &tfull);
-        ++rnd;
-      };
-      auto round_free = [&]() { return mbar_test_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1)); };
-      bool staged_done = nround == 0;
-      auto finish_rounds = [&]() {                   // all rounds issued and consumed
-        if (staged_done) return;
-        while (rnd < nround) {
-          mbar_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1));
-          issue_round();
-        }
-        mbar_wait(&tempty, static_cast<uint32_t>((rnd - 1) & 1));
-        staged_done = true;
-      };
-      if (nround > 0) issue_round();
-      uint32_t pseq = 0;
-      for (int q = 0; q < nseg && useB; ++q) {
-        const SegDesc sd = a.L.segs[s_lo + q];
-        const int i = sd.blk;
-        const int ld = a.L.ld[i], mt = ld >> 3;
-        const int64_t p0 = a.L.poff[i];
-        // warm L2 with this piece's epilogue inputs (plain loads in the epilogue)
-        const uint32_t cbytes = static_cast<uint32_t>(ld) * 8u;
-        tma_prefetch_l2(a.u + p0, cbytes);
-        for (int c = 0; c < ncol; ++c) {
-          if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cbytes);
-          if (a.epi == EPI_DOT && Y2 && Y2 != P2) tma_prefetch_l2(Y2 + c * n_pad + p0, cbytes);
-        }
-        // one chunk per tile block of the piece, in storage order (s-major, g ascending)
-        const TB* Bi = B + a.L.pboff[i];
-        const int ns = pk_ns(mt);
-        int sb = 0, gb = 0;
-        for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
-        for (int k = sd.k0; k < sd.k1; ++k, ++pseq) {
-          const int s_ = static_cast<int>(pseq % nstage);
-          const uint32_t use = pseq / nstage;
-          if (use == 0 && s_ == nstage - 1) finish_rounds();   // the staging slot
-          if (use > 0) {
-            if (rnd < nround) {                      // poll both (neither probe may block)
-              while (!mbar_test_wait(&empty[s_], (use - 1) & 1u))
-                if (rnd < nround && round_free()) issue_round();
-            } else {
-              mbar_wait(&empty[s_], (use - 1) & 1u);
-            }
+      if (useB) {
+        // the CTA's stream: tiles [t0, t0 + ntot) of the packed buffer, in CHUNK-tile copies
+        const int64_t t0 = a.L.segs[s_lo].t0;
+        const SegDesc last = a.L.segs[s_hi - 1];
+        const int64_t ntot = last.t0 + last.ntile - t0;
+        const int nchunk = static_cast<int>((ntot + CHUNK - 1) / CHUNK);
+        // warm L2 with the epilogue inputs of every piece (plain loads in the epilogue)
+        for (int q = 0; q < nseg; ++q) {
+          const int i = a.L.segs[s_lo + q].blk;
+          const int64_t p0 = a.L.poff[i];
+          const uint32_t cbytes = static_cast<uint32_t>(a.L.ld[i]) * 8u;
+          tma_prefetch_l2(a.u + p0, cbytes);
+          for (int c = 0; c < ncol; ++c) {
+            if (P2) tma_prefetch_l2(P2 + c * n_pad + p0, cbytes);
+            if (a.epi == EPI_DOT && Y2 && Y2 != P2) tma_prefetch_l2(Y2 + c * n_pad + p0, cbytes);
           }
-          if (rnd < nround && round_free()) issue_round();
-          const int nt = pk_blk_size(gb, sb, mt);
-          const uint32_t bytes = static_cast<uint32_t>(nt) * 64u * static_cast<uint32_t>(sizeof(TB));
+        }
+        // chunks = runs of consecutive blocks of <= CHUNK tiles (a block never straddles two chunks, so
+        // the MMA warps address a block's tiles at constant offsets from its base)
+        int s_ = 0, c = 0;
+        uint32_t ph = 0;
+        int64_t cstart = t0;
+        int cfill = 0;
+        auto issue = [&]() {
+          if (c >= nstage) mbar_wait_sleep(&empty[s_], ph ^ 1u, 64);
+          const uint32_t bytes = static_cast<uint32_t>(cfill) * 64u * static_cast<uint32_t>(sizeof(TB));
           fence_proxy_async_smem();
           mbar_arrive_expect_tx(&full[s_], bytes);
-          tma_load_1d(ring + static_cast<int64_t>(s_) * slot_tiles * 64,
-                      Bi + static_cast<int64_t>(pk_blk_off(gb, sb, mt)) * 64, bytes, &full[s_]);
-          if (++gb == ns) { ++sb; gb = sb; }
+          tma_load_1d(ring + static_cast<int64_t>(s_) * CHUNK * 64, B + cstart * 64, bytes, &full[s_]);
+          if (++s_ == nstage) { s_ = 0; ph ^= 1u; }
+          ++c;
+          cstart += cfill;
+          cfill = 0;
+        };
+        for (int q = 0; q < nseg; ++q) {
+          const SegDesc sd = a.L.segs[s_lo + q];
+          const int mt = a.L.ld[sd.blk] >> 3, ns = pk_ns(mt);
+          int sb = 0, gb = 0;
+          for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
+          for (int k = sd.k0; k < sd.k1; ++k) {
+            const int nt = pk_blk_size(gb, sb, mt);
+            if (cfill + nt > CHUNK) issue();
+            cfill += nt;
+            if (++gb == ns) { ++sb; gb = sb; }
+          }
         }
+        if (cfill > 0) issue();
+        (void)ntot;
+        (void)nchunk;
       }
-      finish_rounds();                               // (a short stream never reached the staging slot)
+      TR(2);
     }
     return;
   }
@@ -273,12 +260,17 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     // k = 2 qc + h: direct A pair T[qr][2qc + h] (one 16-byte load), transposed A T[2qc + h][qr]
     const int offD = swz(qr, 2 * qc), offT0 = swz(2 * qc, qr), offT1 = swz(2 * qc + 1, qr);
     const int bo = (1 + qr) * ldp + 2 * qc;          // B pair D[8t + 2qc + h][probe qr] at bo + 8t
-    uint32_t seq = 0;
+    // chunk bookkeeping (the producer's walk): the current chunk sits in slot cs, filled up to cfill tiles
+    int ws = 0, cs = -1;
+    uint32_t wph = 0;
+    int cfill = CHUNK;
+    TACC_DECL
     for (int q = 0; q < nseg; ++q) {
       const SegDesc sd = a.L.segs[s_lo + q];
       const int mt = a.L.ld[sd.blk] >> 3;
       const double* Dp = Dpb + (q & 1) * dpstride;
-      mbar_wait(&dready[q & 1], static_cast<uint32_t>((q >> 1) & 1));
+      mbar_wait_sleep(&dready[q & 1], static_cast<uint32_t>((q >> 1) & 1), 128);
+      if (wid == 0 && lane == 0 && q < 8) TR(4 + q);
       double acc[NT8][2][MTMAX], accy[MTMAX];
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
@@ -302,12 +294,26 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       }
       int sb = 0, gb = 0;
       for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
-      for (int k = sd.k0; k < sd.k1; ++k, ++seq) {
-        const int s_ = static_cast<int>(seq % nstage);
-        const TB* blk = ring + static_cast<int64_t>(s_) * slot_tiles * 64;
+      for (int k = sd.k0; k < sd.k1; ++k) {
         const int h = pk_h(gb, mt), w = pk_h(sb, mt);
         const bool diag = gb == sb;
-        mbar_wait(&full[s_], (seq / nstage) & 1u);
+        const int nt = diag ? w * (w + 1) / 2 : h * w;
+        long long tw0 = 0, tw1 = 0;
+        TCLK(tw0);
+        if (cfill + nt > CHUNK) {                    // next chunk: hand back the current one, wait for it
+          if (cs >= 0) {
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[cs]);
+          }
+          cs = ws;
+          mbar_wait_sleep(&full[ws], wph, 32);
+          if (++ws == nstage) { ws = 0; wph ^= 1u; }
+          cfill = 0;
+        }
+        TCLK(tw1);
+        if (wid == 0 && lane == 0) TACC(48, tw1 - tw0);
+        const TB* blk = ring + (static_cast<int64_t>(cs) * CHUNK + cfill) * 64;
+        auto tile = [&](int pos) -> const TB* { return blk + pos * 64; };
         // one k-tile step: x[hh] += A_hh D[k-tile kt] (hh = 0, 1 independent DMMA chains), and the y column
         auto step = [&](double (&x0)[2][NT8], double (&x1)[2][NT8], double& xy, double a0, double a1, int kt) {
           const double* db = Dp + bo + kt * 8;
@@ -349,25 +355,35 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
           if (h == 8 && w == 8) {
             if (diag) {
               // diagonal block: row wa of the lower triangle, the tiles (wa, kk) kk <= wa direct and
-              // (kk, wa) kk > wa transposed — both give rows 8g + wa from D rows 8kk (branch-free)
+              // (kk, wa) kk > wa transposed — both give rows 8g + wa from D rows 8kk (branch-free).
+              // All A operands are loaded first (shared-memory latency overlaps the DMMA chains).
+              double A0[8], A1[8];
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {
                 const bool dir = kk <= wa;
                 const int pos = dir ? 8 * kk - kk * (kk - 1) / 2 + (wa - kk) : 8 * wa - wa * (wa - 1) / 2 + (kk - wa);
-                const TB* tp = blk + pos * 64;
-                const double a0 = ldA(tp + (dir ? offD : offT0)), a1 = ldA(tp + (dir ? offD + 1 : offT1));
-                step(d0, d1, dy, a0, a1, 8 * sb + kk);
+                const TB* tp = tile(pos);
+                A0[kk] = ldA(tp + (dir ? offD : offT0));
+                A1[kk] = ldA(tp + (dir ? offD + 1 : offT1));
               }
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) step(d0, d1, dy, A0[kk], A1[kk], 8 * sb + kk);
               fold(d0, d1, dy, gb * RR + rr);
             } else {
               // off-diagonal block: direct tile (wa, kk) -> rows 8g + wa, transposed (kk, wa) -> rows 8s + wa
+              double2 AD[8];
+              double AT0[8], AT1[8];
 #pragma unroll
               for (int kk = 0; kk < 8; ++kk) {
-                const TB* tpd = blk + (8 * kk + wa) * 64;
-                const double2 ad = ldA2(tpd + offD);
-                step(d0, d1, dy, ad.x, ad.y, 8 * sb + kk);
-                const TB* tpt = blk + (8 * wa + kk) * 64;
-                step(t0, t1, ty, ldA(tpt + offT0), ldA(tpt + offT1), 8 * gb + kk);
+                AD[kk] = ldA2(tile(8 * kk + wa) + offD);
+                const TB* tpt = tile(8 * wa + kk);
+                AT0[kk] = ldA(tpt + offT0);
+                AT1[kk] = ldA(tpt + offT1);
+              }
+#pragma unroll
+              for (int kk = 0; kk < 8; ++kk) {
+                step(d0, d1, dy, AD[kk].x, AD[kk].y, 8 * sb + kk);
+                step(t0, t1, ty, AT0[kk], AT1[kk], 8 * gb + kk);
               }
               fold(d0, d1, dy, gb * RR + rr);
               fold(t0, t1, ty, sb * RR + rr);
@@ -378,7 +394,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
               const int bcol = wa;
               const int cbase = diag ? bcol * h - bcol * (bcol - 1) / 2 - bcol : bcol * h;   // tile (a, b) at cbase + a
               for (int aa = diag ? bcol + 1 : 0; aa < h; ++aa) {
-                const TB* tp = blk + (cbase + aa) * 64;
+                const TB* tp = tile(cbase + aa);
                 step(t0, t1, ty, ldA(tp + offT0), ldA(tp + offT1), 8 * gb + aa);
               }
               fold(t0, t1, ty, sb * RR + rr);
@@ -387,7 +403,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
 #pragma unroll
               for (int a_ = 0; a_ < ESPLIT_H; ++a_)
                 if (a_ < h) {
-                  const double2 ad = ldA2(blk + (wa * h + a_) * 64 + offD);
+                  const double2 ad = ldA2(tile(wa * h + a_) + offD);
                   step(e0[a_], e1[a_], ey[a_], ad.x, ad.y, 8 * sb + wa);
                 }
             } else if (wa < h) {                              // direct: row a = wa
@@ -395,15 +411,22 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
               const int b_hi = diag ? arow : w - 1;
               for (int bb = 0; bb <= b_hi; ++bb) {
                 const int pos = diag ? bb * h - bb * (bb - 1) / 2 + (arow - bb) : bb * h + arow;
-                const double2 ad = ldA2(blk + pos * 64 + offD);
+                const double2 ad = ldA2(tile(pos) + offD);
                 step(d0, d1, dy, ad.x, ad.y, 8 * sb + bb);
               }
               fold(d0, d1, dy, gb * RR + rr);
             }
           }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s_]);
+        long long tw2 = 0;
+        TCLK(tw2);
+        if (wid == 0 && lane == 0) {
+          TACC(49, tw2 - tw1);
+          const int ty = (h == 8 && w == 8) ? (diag ? 0 : 1) : 2;   // full diagonal / full off-diagonal / edge
+          TACC(50 + 2 * ty, tw2 - tw1);
+          TACC(51 + 2 * ty, 1);
+        }
+        cfill += nt;
         if (++gb == ns) { ++sb; gb = sb; }
       }
       if (esplit) {
@@ -438,7 +461,11 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 1);
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 2);
       }
-      mbar_wait(&accfree, static_cast<uint32_t>(q & 1));
+      if (wid == 0 && lane == 0 && q < 8) TR(12 + q);
+      const int ax = q % nacc;
+      mbar_wait_sleep(&accfree[ax], static_cast<uint32_t>((q / nacc) & 1), 128);
+      double* Acc = Accb + ax * accstride;
+      if (wid == 0 && lane == 0 && q < 8) TR(20 + q);
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
         const int mtj = wid + j * PNM;
@@ -453,8 +480,9 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&accready);
+      if (lane == 0) mbar_arrive(&accready[ax]);
     }
+    TACC_FLUSH;
     return;
   }
 
@@ -462,19 +490,13 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   const int et = tid - PWE * 32;                     // 0 .. 32 PNE - 1
   const int ew = wid - PWE;
   const int NET = PNE * 32;
-  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
-  if (a.fuse_p && b == 0) {
-    // S(P_new) = S(R) + beta o S(P_old) (active columns; S is linear) for the next iteration
-    const int nc = a.lr_nc;
-    for (int idx = et; idx < nc * ncol; idx += NET) {
-      const int j = idx / ncol, cc = idx - j * ncol;
-      const double x = a.S_D[static_cast<int64_t>(j) * MAXC + cc], y = SPo[static_cast<int64_t>(j) * MAXC + cc];
-      a.SPbuf[par ^ 1][static_cast<int64_t>(j) * MAXC + cc] = (cb[MAXC + cc] != 0.0) ? x + cb[cc] * y : y;
-    }
-  }
-  // D of piece q into Dp[q&1] by bulk copies, one per column (fused: R into Dp, P_old staged in Acc);
-  // issued by one thread, completing on dbar[q&1]
+  // the low-rank coefficients' input rows: S(D) of the previous kernel, or for the fused apply the
+  // S(P_new) rows the update finaliser formed (cg_fin.cuh)
+  const double* SD = a.fuse_p ? a.SPbuf[par] : a.S_D;
+  // D of piece q into Dp[q&1] by bulk copies, one per column (fused: R into Dp, P_old staged in
+  // Acc[q % nacc]); issued by one thread, completing on dbar[q&1]
   auto issue_d = [&](int q) {
+    double* Acc = Accb + (q % nacc) * accstride;
     const SegDesc sd = a.L.segs[s_lo + q];
     const int ld = a.L.ld[sd.blk];
     const int64_t p0 = a.L.poff[sd.blk];
@@ -489,6 +511,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   };
   // fused apply: D = R + beta o P_old (active columns), P_old for inactive ones; P_new written by part 0
   auto fuse_d = [&](int q) {
+    const double* Acc = Accb + (q % nacc) * accstride;
     const SegDesc sd = a.L.segs[s_lo + q];
     const int ld = a.L.ld[sd.blk];
     const int64_t p0 = a.L.poff[sd.blk];
@@ -519,121 +542,111 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       Dp[c * ldp + k] = x;
     }
   };
-  // the D of piece q has landed (fused: combine it); then signal the MMA warps (and release Acc, which
-  // staged P_old: one accfree completion per piece, MMA piece q waits for completion q)
+  // the D of piece q has landed (fused: combine it); then signal the MMA warps (and release
+  // Acc[q % nacc], which staged P_old: it is next written by the MMA warps' piece q - 2 + nacc)
   auto finish_d = [&](int q, bool rel) {
-    mbar_wait(&dbar[q & 1], static_cast<uint32_t>((q >> 1) & 1));
+    mbar_wait_sleep(&dbar[q & 1], static_cast<uint32_t>((q >> 1) & 1), 64);
     if (a.fuse_p) {
       fuse_d(q);
       bar_epi<PNE>();
     }
     if (et == 0) {
-      if (rel) mbar_arrive(&accfree);
+      if (rel) mbar_arrive(&accfree[q % nacc]);
       mbar_arrive(&dready[q & 1]);
     }
   };
   if (useB) {
-    // prologue: D of the first two pieces (fused: one at a time, P_old staged in Acc)
+    // prologue: D of the first two pieces (fused with one Acc: one at a time, P_old staged in it)
     if (et == 0) {
       issue_d(0);
-      if (!a.fuse_p && nseg > 1) issue_d(1);
+      if ((!a.fuse_p || nacc == 2) && nseg > 1) issue_d(1);
     }
     if (a.fuse_p) {
-      finish_d(0, nseg == 1);
+      finish_d(0, nseg == 1 || nacc == 2);
       if (nseg > 1) {
-        if (et == 0) issue_d(1);
+        if (et == 0 && nacc == 1) issue_d(1);
         finish_d(1, true);
       }
     } else {
-      if (et == 0) mbar_arrive(&accfree);             // Acc was never a staging buffer
+      if (et == 0)                                   // Acc was never a staging buffer
+        for (int x = 0; x < nacc; ++x) mbar_arrive(&accfree[x]);
       finish_d(0, false);
       if (nseg > 1) finish_d(1, false);
     }
   }
-  double* Tpart = Tsm + MAX_SEG_T * MAXC;            // [PNE][TQ][MAXC] per-warp partials
-  // low-rank rows T of pieces [q0, q1) into Tsm[slot0 + ...] (slot0 = 0 on the staged path, q on the
-  // plain-load path).  Thread et owns column c = et % 16 of the S rows j = et/16 + 2 PNE k (fused:
-  // S(D) = S(R) + beta o S(P_old)); the row offsets of each column are summed in fixed order (lane
-  // pairs, then warps): the same decomposition on every CTA and on both paths.
-  auto lr_rows = [&](int slot0, int q0, int q1) {
+  double* Tpart = Tsm + a.L.seg_max * MAXC;          // [PNE][LRG][MAXC] per-warp partials
+  // low-rank rows T_q = M'[row(q), :] S(D) of pieces [q0, q0 + LRG) into Tsm[q].  Thread et owns
+  // columns 4 cg .. 4 cg + 3 (cg = et % 4) of the S rows j = et / 4 + (NET / 4) k; each (piece, column)
+  // sum runs over j in that fixed order, then over the 8 row lanes of a warp (butterfly) and the warps in
+  // order: the same bits on every CTA, for any set of pieces, whatever the partition.
+  auto lr_rows = [&](int q0) {
     const int nc = a.lr_nc;
-    const int c = et & 15, j0 = et >> 4, NJ = 2 * PNE;
-    const bool cact = c < ncol;
-    const double bc = cb[c], ac = cb[MAXC + c];
-    const int nq = q1 - q0;
-    double t[MAX_SEG_T];
+    const int cg = et & 3, jl = et >> 2, NJ = NET / 4;
+    const int nq = min(LRG, nseg - q0);
+    const bool cact = 4 * cg < ncol;
+    const double* Mr[LRG];
 #pragma unroll
-    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] = 0.0;
-    if (tstage) {
-      const double* stg = reinterpret_cast<const double*>(stg_base);
-      const double* mseg = stg + (a.fuse_p ? 2 : 1) * JC * MAXC;
-      int r = 0;
-      for (int jc = 0; jc < nc; jc += JC, ++r) {
-        const int jn = min(JC, nc - jc);
-        mbar_wait(&tfull, static_cast<uint32_t>(r & 1));
-        for (int jj = j0; jj < jn; jj += NJ) {
-          double x = 0.0;
-          if (cact) {
-            x = stg[jj * MAXC + c];
-            if (a.fuse_p) {
-              const double y = stg[(JC + jj) * MAXC + c];
-              x = (ac != 0.0) ? x + bc * y : y;
-            }
-          }
+    for (int g = 0; g < LRG; ++g)
+      Mr[g] = P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q0 + min(g, nq - 1)].blk) * nc;
+    double t[LRG][4];
 #pragma unroll
-          for (int qq = 0; qq < MAX_SEG_T; ++qq)
-            if (qq < nq) t[qq] = fma(mseg[qq * JC + jj], x, t[qq]);
-        }
-        bar_epi<PNE>();
-        if (et == 0) mbar_arrive(&tempty);
-      }
-    } else {
-      const double* Mr = P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q0].blk) * nc;
-      for (int j = j0; j < nc; j += NJ) {
-        double x = 0.0;
-        if (cact) {
-          x = a.S_D[static_cast<int64_t>(j) * MAXC + c];
-          if (a.fuse_p) {
-            const double y = SPo[static_cast<int64_t>(j) * MAXC + c];
-            x = (ac != 0.0) ? x + bc * y : y;
-          }
-        }
-        t[0] = fma(__ldg(Mr + j), x, t[0]);
+    for (int g = 0; g < LRG; ++g)
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[g][u] = 0.0;
+    if (cact) {
+#pragma unroll 4
+      for (int j = jl; j < nc; j += NJ) {
+        const double2* sr = reinterpret_cast<const double2*>(SD + static_cast<int64_t>(j) * MAXC + 4 * cg);
+        const double2 s01 = __ldcg(sr), s23 = __ldcg(sr + 1);
+        const double x[4] = {s01.x, s01.y, s23.x, s23.y};
+        double m[LRG];
+#pragma unroll
+        for (int g = 0; g < LRG; ++g) m[g] = __ldg(Mr[g] + j);
+#pragma unroll
+        for (int g = 0; g < LRG; ++g)
+#pragma unroll
+          for (int u = 0; u < 4; ++u) t[g][u] = fma(m[g], x[u], t[g][u]);
       }
     }
+    // the 8 row lanes of the warp (lane = 4 jl' + cg), butterfly in fixed order
 #pragma unroll
-    for (int qq = 0; qq < MAX_SEG_T; ++qq) t[qq] += __shfl_xor_sync(0xffffffffu, t[qq], 16);
+    for (int g = 0; g < LRG; ++g)
 #pragma unroll
-    for (int qb = 0; qb < MAX_SEG_T; qb += TQ) {
-      if (qb >= nq) break;
-      if (lane < 16)
-#pragma unroll
-        for (int qq = 0; qq < TQ; ++qq) Tpart[(ew * TQ + qq) * MAXC + lane] = t[qb + qq];
-      bar_epi<PNE>();
-      const int nqq = min(TQ, nq - qb);
-      if (et < nqq * 16) {
-        const int qq = et >> 4, cc = et & 15;
-        double acc_ = 0.0;
-        for (int w = 0; w < PNE; ++w) acc_ += Tpart[(w * TQ + qq) * MAXC + cc];
-        Tsm[(slot0 + qb + qq) * MAXC + cc] = acc_;
+      for (int u = 0; u < 4; ++u) {
+        double v = t[g][u];
+        v += __shfl_xor_sync(0xffffffffu, v, 4);
+        v += __shfl_xor_sync(0xffffffffu, v, 8);
+        v += __shfl_xor_sync(0xffffffffu, v, 16);
+        t[g][u] = v;
       }
-      bar_epi<PNE>();
+    if (lane < 4)
+#pragma unroll
+      for (int g = 0; g < LRG; ++g)
+#pragma unroll
+        for (int u = 0; u < 4; ++u) Tpart[(ew * LRG + g) * MAXC + 4 * lane + u] = t[g][u];
+    bar_epi<PNE>();
+    if (et < nq * MAXC) {
+      const int g = et >> 4, cc = et & 15;
+      double acc_ = 0.0;
+      for (int w = 0; w < PNE; ++w) acc_ += Tpart[(w * LRG + g) * MAXC + cc];
+      Tsm[(q0 + g) * MAXC + cc] = acc_;
     }
+    bar_epi<PNE>();
   };
-  if (tstage) lr_rows(0, 0, nseg);
   int pend = -1;                                     // a piece whose D copy is in flight
   for (int q = 0; q < nseg; ++q) {
     const SegDesc sd = a.L.segs[s_lo + q];
     const int i = sd.blk, ld = a.L.ld[i];
     const int64_t p0 = a.L.poff[i];
     const double* Dp = Dpb + (q & 1) * dpstride;      // D of this piece (kept until its epilogue)
+    double* Acc = Accb + (q % nacc) * accstride;      // its block products
     if (!useB) {
       form_d(q);                                     // (no block term: the epilogue warps form D here)
       bar_epi<PNE>();
     }
-    // low-rank row (plain-load path: formed per piece, while the MMA warps stream it)
-    if (!tstage) lr_rows(0, q, q + 1);
     if (pend >= 0) { finish_d(pend, a.fuse_p); pend = -1; }
+    if (q % LRG == 0) lr_rows(q);                    // low-rank rows of pieces q .. q + LRG - 1
+    if (et == 0 && q == 0) TR(28);
     // register prefetch of this piece's epilogue inputs for the first row of every thread (the
     // latency hides behind the wait for the MMA warps)
     const bool pf = et < ld;
@@ -650,7 +663,8 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     }
     bool run_epi = true;
     if (useB) {
-      mbar_wait(&accready, static_cast<uint32_t>(q & 1));
+      mbar_wait_sleep(&accready[q % nacc], static_cast<uint32_t>((q / nacc) & 1), 256);
+      if (et == 0 && q < 8) TR(29 + q);
       // split cluster: publish this part's block products; the last part sums all parts in order
       if (sd.nparts > 1) {
         double* base = a.split_part + sd.spoff + static_cast<int64_t>(sd.part) * ld * NCP;
@@ -720,7 +734,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
           const double d = Dp[c * ldp + r];
           double val = pa * d;
           if (useB) val += bi * Acc[r * NCP + c];
-          val += uu * (ms * Tsm[(tstage ? q : 0) * MAXC + c]);
+          val += uu * (ms * Tsm[q * MAXC + c]);
           double o = a.cA[c] * val + a.cV[c] * d;
           if (P2) o += a.cP[c] * p2v[c];
           a.out[c * n_pad + p0 + r] = o;
@@ -731,18 +745,21 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     }
     if (useB) {
       bar_epi<PNE>();                                // all reads of Acc, Dp[q&1] and the T row done
-      // D of piece q+2 into Dp[q&1]: copies issued now, completed (and combined) after T_{q+1}
+      // D of piece q+2 into Dp[q&1]: copies issued now, completed (and combined) at the next piece
       if (q + 2 < nseg) {
         if (et == 0) {
           issue_d(q + 2);
-          if (!a.fuse_p) mbar_arrive(&accfree);       // (fused: Acc stages P_old until finish_d)
+          if (!a.fuse_p) mbar_arrive(&accfree[q % nacc]);   // (fused: Acc stages P_old until finish_d)
         }
         pend = q + 2;
       } else if (et == 0) {
-        mbar_arrive(&accfree);
+        mbar_arrive(&accfree[q % nacc]);
       }
     }
-    if (!run_epi) continue;
+    if (!run_epi) {
+      if (et == 0 && q < 8) TR(37 + q);
+      continue;
+    }
     // per-cluster column sums: warp butterflies, then the warps in fixed order
 #pragma unroll
     for (int c = 0; c < NCP; ++c) ep[c] = warp_sum(ep[c]);
@@ -757,6 +774,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       else a.dots[static_cast<int64_t>(i) * MAXC + et] = s;
     }
     bar_epi<PNE>();                                  // ered reuse
+    if (et == 0 && q < 8) TR(37 + q);
   }
   // finaliser (last CTA; one epilogue warp per column)
   if (a.fin != FIN_NONE) {
@@ -771,11 +789,11 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       if (et == 0) a.st->ticket[a.fin] = 0;
     }
   }
+  if (et == 0) TR(45);
 }
 
 // --------------------------------------------------------------------------------------- host
 bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a) {
-  (void)seg_max;
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
@@ -787,29 +805,49 @@ bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a
   a.f32 = f32 ? 1 : 0;
   a.ld_max = ld_max;
   const int es = f32 ? 4 : 8;
-  const int slot = 64;                                       // a ring slot holds one tile block
-  const int pne = (a.mtmax <= 4) ? 7 : 4;
+  const int pne = 7;
   const size_t budget = static_cast<size_t>(optin) - 8192;   // static shared memory + margin
-  const PackSmem fixed = pack_smem(slot, 0, es, ld_max, a.nt8, 8, pne);
-  if (fixed.total >= budget) return false;
-  const int ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(slot) * 64 * es)));
-  if (ns < 2) return false;
-  a.slot_tiles = slot;
+  // a second Acc buffer (the MMA warps run a piece ahead of the epilogue) when the ring keeps >= 4 slots
+  int nacc = 2, ns = 0;
+  for (; nacc >= 1; --nacc) {
+    const PackSmem fixed = pack_smem(0, es, ld_max, a.nt8, 8, pne, seg_max, nacc);
+    if (fixed.total >= budget) continue;
+    ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(CHUNK) * 64 * es)));
+    if (ns >= 4 || (nacc == 1 && ns >= 2)) break;
+  }
+  if (nacc < 1 || ns < 2) return false;
+  a.nacc = nacc;
+  a.slot_tiles = CHUNK;
   a.nstage = ns;
-  a.smem = pack_smem(slot, ns, es, ld_max, a.nt8, 8, pne).total;
+  a.smem = pack_smem(ns, es, ld_max, a.nt8, 8, pne, seg_max, nacc).total;
   return true;
 }
 
 template <int NM, int MT, int N8, typename TB>
 static void launch_pk(const ApplyArgs& a, cudaStream_t s) {
   // 16 or 13 warps (<= 4 per SM sub-partition: 128 registers), one CTA per SM
-  constexpr int NE = (MT <= 4) ? 7 : 4;
+  constexpr int NE = 7;
   auto k = apply_packed_kernel<NM, MT, N8, TB, NE>;
   smem_optin(reinterpret_cast<const void*>(k));
   k<<<a.grid, (NM + NE + 1) * 32, a.smem, s>>>(a);
 }
 
+#ifdef NUGPR_TRACE_APPLY
+static long long g_trace_count = 0, g_trace_at = -1;
+#endif
+
 void launch_apply_packed(const ApplyArgs& a, cudaStream_t s) {
+#ifdef NUGPR_TRACE_APPLY
+  if (g_trace_at < 0) { const char* e = getenv("NUGPR_TRACE_AT"); g_trace_at = e ? atoll(e) : 1LL << 60; }
+  const bool tr = g_trace_count++ == g_trace_at;
+  if (tr) {
+    const int one = 1;
+    void* tp = nullptr;
+    cudaGetSymbolAddress(&tp, g_apply_trace);
+    cudaMemsetAsync(tp, 0, sizeof(g_apply_trace), s);
+    cudaMemcpyToSymbolAsync(g_apply_trace_on, &one, sizeof(int), 0, cudaMemcpyHostToDevice, s);
+  }
+#endif
 #define NUGPR_PK(MT)                                                        \
   do {                                                                      \
     if (a.nt8 == 1) {                                                       \
@@ -822,7 +860,16 @@ void launch_apply_packed(const ApplyArgs& a, cudaStream_t s) {
   else if (a.mtmax == 4) NUGPR_PK(4);
   else NUGPR_PK(8);
 #undef NUGPR_PK
+#ifdef NUGPR_TRACE_APPLY
+  if (tr) { const int zero = 0; cudaMemcpyToSymbolAsync(g_apply_trace_on, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, s); }
+#endif
   note_launch(); post_launch("apply_packed_kernel");
 }
+
+#ifdef NUGPR_TRACE_APPLY
+extern "C" __attribute__((visibility("default"))) int nugpr_debug_apply_trace(unsigned long long* dst) {
+  return cudaMemcpyFromSymbol(dst, g_apply_trace, sizeof(g_apply_trace)) == cudaSuccess ? 0 : 1;
+}
+#endif
 
 }  // namespace nugpr

@@ -138,9 +138,21 @@ __device__ __forceinline__ void fin_alpha_trace_body(int fin, CGState* st, const
   }
 }
 
+// S(P) rows of the next search direction, formed where beta is decided (so the next fused apply
+// reads them ready-made): S(P_{k+1}) = S(R_{k+1}) + beta o S(P_k) on active columns, S(P_k) on frozen
+// ones (S = W^T . is linear, Eq. 19-21).  SR: per-tile S(r) rows; tile0 (or NULL: one tile per cluster)
+// maps cluster j to its tiles, summed in tile order.
+struct SPUpdate {
+  const double* SR;
+  const int32_t* tile0;
+  int n_c;
+  double* SP[2];
+};
+
 // FIN_UPDATE: beta = r'^T r' / r^T r, history, iteration counters, freezing (readings P3, P5).
 static __device__ void fin_update_body(CGState* st, const EvalParams* P, const double* rr_part, int n_tiles, int ncol,
-                                double* beta_hist, int hist_stride, unsigned long long cond, int nw) {
+                                double* beta_hist, int hist_stride, unsigned long long cond, int nw,
+                                const SPUpdate& sp) {
   __shared__ int act[MAXC];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const int par = st->par;
@@ -167,6 +179,26 @@ static __device__ void fin_update_body(CGState* st, const EvalParams* P, const d
     }
   }
   __syncthreads();
+  if (sp.SR) {
+    const double* SPo = sp.SP[par];
+    double* SPn = sp.SP[par ^ 1];
+    for (int idx = threadIdx.x; idx < sp.n_c * ncol; idx += blockDim.x) {
+      const int j = idx / ncol, c = idx - j * ncol;
+      const double y = SPo[static_cast<int64_t>(j) * MAXC + c];
+      double v = y;
+      if (act[c]) {
+        double x;
+        if (sp.tile0) {
+          x = 0.0;
+          for (int t = sp.tile0[j]; t < sp.tile0[j + 1]; ++t) x += sp.SR[static_cast<int64_t>(t) * MAXC + c];
+        } else {
+          x = sp.SR[static_cast<int64_t>(j) * MAXC + c];
+        }
+        v = x + st->beta[c] * y;
+      }
+      SPn[static_cast<int64_t>(j) * MAXC + c] = v;
+    }
+  }
   if (threadIdx.x == 0) {
     int any = 0;
     for (int c = 0; c < ncol; ++c) any |= act[c];

@@ -75,6 +75,9 @@ constexpr int MAX_PARTS = 4;
 struct SegDesc {
   int32_t blk, k0, k1, part, nparts, tick;
   int64_t spoff;
+  int64_t t0;      // first tile of the piece in the packed buffer (a CTA's pieces are contiguous there)
+  int32_t ntile;   // tiles in the piece
+  int32_t pad_;
 };
 
 struct TileDesc {
@@ -173,7 +176,7 @@ struct ApplyArgs {
   // packed apply: split-cluster partial sums / tickets, launch plan
   double* split_part;
   unsigned int* split_ticket;
-  int grid, slot_tiles, nstage, mtmax, nt8, f32;
+  int grid, slot_tiles, nstage, mtmax, nt8, f32, nacc;
   size_t smem;
   int ld_max;
   // big-block path (ld > 512, apply_big_kernel): low-rank rows T = M'S from lowrank_kernel
@@ -207,6 +210,7 @@ struct UpdateArgs {
   double* Pbuf[2];
   double* rr_part;         // [n_tiles][16]
   double* SR_part;         // [n_tiles][16]
+  double* SPbuf[2];        // S(P) rows ping-pong [n_c][MAXC]: the finaliser forms S(P_{k+1}) (cg_fin.cuh)
   double* beta_hist;       // [MAXC][hist_stride]
   int hist_stride;
   int ncol;

@@ -24,12 +24,12 @@ namespace nugpr {
 // PAR-2 (cluster-sharded evaluation): the finaliser as its own single-CTA launch
 // after the exchange of the partials.  FIN_UPDATE skips when no column is active (as update does).
 __global__ void __launch_bounds__(NT) fin_kernel(int fin, CGState* st, const EvalParams* prm, const double* part,
-                                                 int n_tiles, int ncol, double* hist, int hist_stride) {
+                                                 int n_tiles, int ncol, double* hist, int hist_stride, SPUpdate sp) {
   if (fin == FIN_INIT) {
     fin_init_body(st, prm, part, n_tiles, ncol, NT / 32);
   } else if (fin == FIN_UPDATE) {
     if (!st->any_active) return;
-    fin_update_body(st, prm, part, n_tiles, ncol, hist, hist_stride, 0ull, NT / 32);
+    fin_update_body(st, prm, part, n_tiles, ncol, hist, hist_stride, 0ull, NT / 32, sp);
   } else {
     if (fin == FIN_ALPHA && !st->any_active) return;
     fin_alpha_trace_body(fin, st, part, n_tiles, ncol, hist, hist_stride, NT / 32);
@@ -125,12 +125,20 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
   if (threadIdx.x < MAXC) a.rr_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
   __syncthreads();
   block_reduce_cols<MAXC>(sr, sred, outv);
+  const bool per_cluster = a.L.n_tiles == a.L.n_c;   // (big layout: several tiles per cluster)
   if (threadIdx.x < MAXC) {
     a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
-    a.SP0[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+    if (per_cluster) a.SP0[t * MAXC + threadIdx.x] = outv[threadIdx.x];   // S(P_0) = S(R_0)
   }
   if (!a.nofin && last_cta(&a.st->ticket[FIN_INIT])) {
     fin_init_body(a.st, a.prm, a.rr_part, a.L.n_tiles, ncol, NT / 32);
+    if (!per_cluster)                                // S(P_0) rows: the cluster's tiles in tile order
+      for (int idx = threadIdx.x; idx < a.L.n_c * MAXC; idx += NT) {
+        const int j = idx / MAXC, c = idx - j * MAXC;
+        double x = 0.0;
+        for (int tt = a.L.tile0[j]; tt < a.L.tile0[j + 1]; ++tt) x += a.SR_part[tt * MAXC + c];
+        a.SP0[idx] = x;
+      }
     if (threadIdx.x == 0) a.st->ticket[FIN_INIT] = 0;
   }
 }
@@ -138,8 +146,8 @@ __global__ void __launch_bounds__(NT) rhs_init_kernel(RhsArgs a) {
 // ---------------------------------------------------------------------------------------
 // Low-rank coefficients T = M' S(D) (Eq. 19-21: block i of W M' W^T D is u_i T_i) for the
 // big-block layout's apply (the packed apply forms its rows in-kernel), one warp per
-// row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new) = S(R) +
-// beta o S(P_old) for the active columns (S is linear), and CTA 0 also stores S(P_new).
+// row i, S staged once per CTA in shared memory.  With fuse_p, S(D) = S(P_new), the rows the update
+// finaliser (or rhs_init) formed in SPbuf[par].
 constexpr int TROWS = 8;   // rows of T per CTA (one per warp; 16 = two per warp measured slower at C3)
 
 template <int NCP>
@@ -156,7 +164,6 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
     cb[NCP + tid] = (tid < ncol) ? static_cast<double>(a.st->active[tid]) : 0.0;
   }
   __syncthreads();
-  const double* SPo = a.fuse_p ? a.SPbuf[par] : nullptr;
   // stage S (n_c rows of NCP) with all loads of a thread in flight: thread -> rows j = tid + k*NT
   for (int j0 = 0; j0 < n_c; j0 += NT * 2) {
     double v[2][NCP];
@@ -167,7 +174,9 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
       for (int c2 = 0; c2 < NCP / 2; ++c2) {
         double2 x = make_double2(0.0, 0.0);
         if (j < n_c) {
-          if (a.task0) {         // per-column-task partials of the cluster, summed in task order
+          if (a.fuse_p) {        // S(P_new) rows, formed by the update finaliser
+            x = *reinterpret_cast<const double2*>(a.SPbuf[par] + j * MAXC + 2 * c2);
+          } else if (a.task0) {  // per-column-task partials of the cluster, summed in task order
             for (int tk = a.task0[j]; tk < a.task0[j + 1]; ++tk) {
               const double2 w = *reinterpret_cast<const double2*>(a.S + tk * MAXC + 2 * c2);
               x.x += w.x;
@@ -175,11 +184,6 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
             }
           } else {
             x = *reinterpret_cast<const double2*>(a.S + j * MAXC + 2 * c2);
-          }
-          if (a.fuse_p) {
-            const double2 y = *reinterpret_cast<const double2*>(SPo + j * MAXC + 2 * c2);
-            x.x = (cb[NCP + 2 * c2] != 0.0) ? x.x + cb[2 * c2] * y.x : y.x;
-            x.y = (cb[NCP + 2 * c2 + 1] != 0.0) ? x.y + cb[2 * c2 + 1] * y.y : y.y;
           }
         }
         v[u][2 * c2] = x.x;
@@ -192,10 +196,6 @@ __global__ void __launch_bounds__(NT, 2) lowrank_kernel(LowrankArgs a) {
       if (j < n_c) {
 #pragma unroll
         for (int c = 0; c < NCP; ++c) Ss[j * NCP + c] = v[u][c];
-        if (a.fuse_p && blockIdx.x == 0)
-#pragma unroll
-          for (int c = 0; c < NCP; ++c)
-            if (c < ncol) a.SPbuf[par ^ 1][j * MAXC + c] = v[u][c];
       }
     }
   }
@@ -290,7 +290,8 @@ __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
   block_reduce_cols<NCP>(sr, sred, outv);
   if (threadIdx.x < ncol) a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
   if (!a.nofin && last_cta(&st->ticket[FIN_UPDATE])) {
-    fin_update_body(st, a.prm, a.rr_part, a.L.n_tiles, ncol, a.beta_hist, a.hist_stride, a.cond, NT / 32);
+    SPUpdate sp{a.SR_part, a.L.n_tiles == a.L.n_c ? nullptr : a.L.tile0, a.L.n_c, {a.SPbuf[0], a.SPbuf[1]}};
+    fin_update_body(st, a.prm, a.rr_part, a.L.n_tiles, ncol, a.beta_hist, a.hist_stride, a.cond, NT / 32, sp);
     if (threadIdx.x == 0) st->ticket[FIN_UPDATE] = 0;
   }
 }
@@ -540,8 +541,9 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
 }
 
 void launch_fin(int fin, CGState* st, const EvalParams* prm, const double* part, int n_tiles, int ncol,
-                double* hist, int hist_stride, cudaStream_t s) {
-  fin_kernel<<<1, NT, 0, s>>>(fin, st, prm, part, n_tiles, ncol, hist, hist_stride);
+                double* hist, int hist_stride, cudaStream_t s, const double* SR, double* SP0, double* SP1) {
+  SPUpdate sp{SR, nullptr, n_tiles, {SP0, SP1}};
+  fin_kernel<<<1, NT, 0, s>>>(fin, st, prm, part, n_tiles, ncol, hist, hist_stride, sp);
   note_launch(); post_launch("fin_kernel");
 }
 

@@ -62,6 +62,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// wait with a sleep between probes: a spinning probe is a shared-memory (MIO) operation, and warps
+// that wait long (a warp-specialised kernel's idle roles) would otherwise take the MIO slots the
+// compute warps' shared-memory loads need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t ns) {
+  while (!mbar_try_wait(bar, parity)) __nanosleep(ns);
+}
+
 // global -> shared bulk copy of `bytes` (multiple of 16, both addresses 16-byte aligned),
 // completing `bytes` transactions on `bar`.
 __device__ __forceinline__ void tma_load_1d(void* dst_smem, const void* src_gmem, uint32_t bytes,
