@@ -1253,7 +1253,7 @@ static nugpr_status make_iter_args(nugpr_blocks* bl, EvalDev& e, int ncol, IterA
     a1.big = 1;
     a1.grid = Ld.n_tiles;
   } else {
-    if (!plan_packed_apply(L.ld_max, ncol, bl->f32, L.seg_max, a1))
+    if (!plan_packed_apply(L.ld_max, ncol, bl->f32, L.seg_max, bl->n_cg, a1))
       return fail(NUGPR_ERR_SHAPE, "packed apply does not fit shared memory (ld_max=%d, ncol=%d, pieces/CTA=%d)",
                   L.ld_max, ncol, L.seg_max);
     a1.grid = Ld.n_seg_ctas;

@@ -53,7 +53,8 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TCLK(v) (v) = clock64()
 #define TACC(idx, v) do { tacc_[(idx) - 48] += (v); } while (0)
 #define TACC_DECL long long tacc_[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-#define TACC_FLUSH do { if (g_apply_trace_on && wid == 0 && lane == 0) for (int i_ = 0; i_ < 8; ++i_) g_apply_trace[blockIdx.x][48 + i_] = tacc_[i_]; } while (0)
+#define TACC_FLUSH do { if (g_apply_trace_on && wid == 0 && lane == 0) for (int i_ = 0; i_ < 8; ++i_) g_apply_trace[blockIdx.x][48 + i_] = tacc_[i_]; \
+  if (g_apply_trace_on && lane == 0 && wid < 8) g_apply_trace[blockIdx.x][56 + wid] = tacc_[1] + tacc_[0]; } while (0)
 #else
 #define TCLK(v) do {} while (0)
 #define TACC(idx, v) do {} while (0)
@@ -66,10 +67,6 @@ __device__ __forceinline__ unsigned long long gtimer() {
 // NM MMA warps (8), warp w owning the output m-tiles w, w+NM, ...; a block's tile rows / columns
 // w + NM rr (rr < 8 / NM)
 constexpr int PNE_MAX = 7;             // epilogue warps
-// split-k of the thin last block row (height <= ESPLIT_H tiles): per-warp partials, reduced in fixed
-// warp order through ESC at the end of the piece
-constexpr int ESPLIT_H = 2;
-__host__ __device__ constexpr int esc_bytes(int nm) { return nm == 8 ? 8 * ESPLIT_H * 32 * 3 * 8 : 0; }
 constexpr int LRG = 4;                 // pieces per pass of the low-rank rows (LRG x 4 accumulators per thread)
 constexpr int CHUNK = 64;              // tiles per ring chunk (32 KB FP64)
 
@@ -93,13 +90,13 @@ __device__ __forceinline__ double2 ldA2(const float* p) {
 // 16-byte B-pair loads D[8t + 2qc + h][col qr] of a quarter warp (rows qr = 2t', 2t'+1) hit all banks
 __host__ __device__ __forceinline__ int pk_ldp(int ld_max) { return ((ld_max + 15) & ~15) + 8; }
 
-// Shared-memory plan (host and device agree): ring | Dp[2] | Acc | Tsm (T rows of every piece, then
-// the per-warp partials of one pass) | Esc
+// Shared-memory plan (host and device agree): ring | Dp[2] | Acc[nacc] | Tsm (T rows of every piece,
+// then the per-warp partials of one pass) | Mst (the M' rows of the CTA's pieces, when staged)
 struct PackSmem {
-  size_t ring, dp, acc, tsm, esc, total;
+  size_t ring, dp, acc, tsm, mst, total;
 };
-__host__ __device__ inline PackSmem pack_smem(int nstage, int esize, int ld_max, int nt8, int nm, int pne, int seg_max,
-                                              int nacc) {
+__host__ __device__ inline PackSmem pack_smem(int nstage, int esize, int ld_max, int nt8, int pne, int seg_max,
+                                              int nacc, int64_t mst_doubles) {
   PackSmem p;
   const size_t ncp = 1 + 8 * static_cast<size_t>(nt8);
   p.ring = 0;
@@ -107,13 +104,13 @@ __host__ __device__ inline PackSmem pack_smem(int nstage, int esize, int ld_max,
   o = (o + 127) / 128 * 128;
   p.dp = o;
   o += 2 * ncp * pk_ldp(ld_max) * sizeof(double);
-  p.acc = o;                                      // nacc x block products [ld_max][NCP]; P_old staging [NCP][ld]
+  p.acc = o;                                      // nacc x block products [ld_max][NCP]
   o += static_cast<size_t>(nacc) * ld_max * ncp * sizeof(double);
   p.tsm = o;
   o += static_cast<size_t>(seg_max + pne * LRG) * MAXC * sizeof(double);
   o = (o + 127) / 128 * 128;
-  p.esc = o;
-  o += esc_bytes(nm);
+  p.mst = o;
+  o += static_cast<size_t>(mst_doubles) * sizeof(double);
   p.total = o;
   return p;
 }
@@ -141,18 +138,19 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ __align__(8) uint64_t full[MAX_NSTAGE];
   __shared__ __align__(8) uint64_t empty[MAX_NSTAGE];
-  __shared__ __align__(8) uint64_t dready[2], dbar[2], accready[2], accfree[2];
+  __shared__ __align__(8) uint64_t dready[2], dbar[2], accready[2], accfree[2], mfull;
   __shared__ double ered[PNE_MAX * MAXC];
   __shared__ double cb[2 * MAXC];
   __shared__ int s_last;
   const int nacc = a.nacc;
-  const PackSmem L_ = pack_smem(a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, NM, PNE, a.L.seg_max, nacc);
+  const int64_t mst_doubles = a.mst ? static_cast<int64_t>(a.L.seg_max) * a.lr_nc : 0;
+  const PackSmem L_ = pack_smem(a.nstage, static_cast<int>(sizeof(TB)), a.ld_max, NT8, PNE, a.L.seg_max, nacc, mst_doubles);
   TB* ring = reinterpret_cast<TB*>(smraw + L_.ring);
   double* Dpb = reinterpret_cast<double*>(smraw + L_.dp);   // [2][NCP][ldp]
   double* Accb = reinterpret_cast<double*>(smraw + L_.acc); // nacc x [ld_max][NCP] block products of a piece
   const int accstride = a.ld_max * NCP;
   double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // T rows [seg_max][MAXC], then partials
-  double* Esc = reinterpret_cast<double*>(smraw + L_.esc);  // [PNM][ESPLIT_H][32 lanes][3] thin-row partials
+  double* Mst = reinterpret_cast<double*>(smraw + L_.mst);  // [seg][lr_nc] staged M' rows (a.mst)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const int64_t n_pad = a.L.n_pad;
   const int ncol = a.ncol;
@@ -165,14 +163,24 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   const int dpstride = NCP * ldp;                            // one D buffer
   const double* Pold = a.fuse_p ? a.Pbuf[par] : nullptr;
   double* Pnew = a.fuse_p ? a.Pbuf[par ^ 1] : nullptr;
+  // the low-rank coefficients' input rows S(D) ([lr_nc][MAXC], 128 B each) are staged by one bulk copy
+  // into the first lrk ring slots when they fit while >= 2 slots stay for the block stream; those
+  // slots join the stream once the low-rank rows of all pieces are formed (virtual chunks 0 .. lrk-1)
+  const size_t slot_bytes = static_cast<size_t>(CHUNK) * 64 * sizeof(TB);
+  const size_t s_bytes = static_cast<size_t>(a.lr_nc) * MAXC * sizeof(double);
+  const int lrk_need = static_cast<int>((s_bytes + slot_bytes - 1) / slot_bytes);
+  const int lrk = (a.lr_stage_s && a.lr_nc > 0 && lrk_need <= (useB ? nstage - 2 : nstage)) ? lrk_need : 0;
   const double* P2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.P2;
   const double* Y2 = a.use_par_p2 == 1 ? a.Pbuf[par ^ 1] : a.Y2;
+  long long clk_start = 0;
+  TCLK(clk_start);
   if (tid == 0) {
     TR(0);
     TRV(46, nseg);
     for (int s_ = 0; s_ < nstage; ++s_) { mbar_init(&full[s_], 1); mbar_init(&empty[s_], PNM); }
     for (int k = 0; k < 2; ++k) { mbar_init(&dready[k], 1); mbar_init(&dbar[k], 1); }
     for (int k = 0; k < 2; ++k) { mbar_init(&accready[k], PNM); mbar_init(&accfree[k], 1); }
+    mbar_init(&mfull, 1);
     fence_mbar_init();
   }
   if (tid < MAXC) {
@@ -191,9 +199,25 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   if (wid == PWP) {
     // ================================ TMA producer ================================
     if (lane == 0 && nseg > 0) {
-      // the M' rows of this CTA's pieces (the epilogue warps' low-rank rows read them early; behind
-      // the block stream they would wait in the DRAM queues)
-      if ((a.lr_nc & 1) == 0)                       // (bulk prefetch: 16-byte aligned rows)
+      if (a.mst) {
+        // the M' rows of this CTA's pieces first (HBM reads at the head of the queue)
+        const uint32_t rb = static_cast<uint32_t>(a.lr_nc) * 8u;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&mfull, rb * static_cast<uint32_t>(nseg));
+        for (int q = 0; q < nseg; ++q)
+          tma_load_1d(Mst + static_cast<int64_t>(q) * a.lr_nc,
+                      P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * a.lr_nc, rb, &mfull);
+      }
+      if (lrk > 0) {
+        const double* SDp = a.fuse_p ? a.SPbuf[par] : a.S_D;
+        fence_proxy_async_smem();
+        mbar_arrive_expect_tx(&full[0], static_cast<uint32_t>(s_bytes));
+        tma_load_1d(ring, SDp, static_cast<uint32_t>(s_bytes), &full[0]);
+        for (int k = 1; k < lrk; ++k) mbar_arrive(&full[k]);
+      }
+      // (not staged) the M' rows of this CTA's pieces into L2 (the epilogue warps' low-rank rows read
+      // them early; behind the block stream they would wait in the DRAM queues)
+      if (!a.mst && (a.lr_nc & 1) == 0)             // (bulk prefetch: 16-byte aligned rows)
         for (int q = 0; q < nseg; ++q)
           tma_prefetch_l2(P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q].blk) * a.lr_nc,
                           static_cast<uint32_t>(a.lr_nc) * 8u);
@@ -216,7 +240,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         }
         // chunks = runs of consecutive blocks of <= CHUNK tiles (a block never straddles two chunks, so
         // the MMA warps address a block's tiles at constant offsets from its base)
-        int s_ = 0, c = 0;
+        int s_ = lrk, c = lrk;                       // (virtual chunks 0 .. lrk-1: the S staging)
         uint32_t ph = 0;
         int64_t cstart = t0;
         int cfill = 0;
@@ -261,7 +285,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     const int offD = swz(qr, 2 * qc), offT0 = swz(2 * qc, qr), offT1 = swz(2 * qc + 1, qr);
     const int bo = (1 + qr) * ldp + 2 * qc;          // B pair D[8t + 2qc + h][probe qr] at bo + 8t
     // chunk bookkeeping (the producer's walk): the current chunk sits in slot cs, filled up to cfill tiles
-    int ws = 0, cs = -1;
+    int ws = lrk, cs = -1;
     uint32_t wph = 0;
     int cfill = CHUNK;
     TACC_DECL
@@ -269,7 +293,11 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       const SegDesc sd = a.L.segs[s_lo + q];
       const int mt = a.L.ld[sd.blk] >> 3;
       const double* Dp = Dpb + (q & 1) * dpstride;
+      long long tp0 = 0, tp1 = 0, tp2 = 0, tp3 = 0, tp4 = 0;
+      TCLK(tp0);
       mbar_wait_sleep(&dready[q & 1], static_cast<uint32_t>((q >> 1) & 1), 128);
+      TCLK(tp1);
+      if (lane == 0) TACC(50, tp1 - tp0);
       if (wid == 0 && lane == 0 && q < 8) TR(4 + q);
       double acc[NT8][2][MTMAX], accy[MTMAX];
 #pragma unroll
@@ -279,19 +307,6 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         for (int n = 0; n < NT8; ++n) { acc[n][0][j] = 0.0; acc[n][1][j] = 0.0; }
       }
       const int ns = pk_ns(mt);
-      // the thin last block row (h <= ESPLIT_H tiles): its direct products are split over the warps by
-      // tile column (warp w: tile (a, w)) instead of all falling to warp a
-      const int hl = pk_h(ns - 1, mt);
-      const bool esplit = NM == 8 && NT8 == 1 && ns > 1 && hl <= ESPLIT_H;
-      double e0[ESPLIT_H][2][NT8], e1[ESPLIT_H][2][NT8], ey[ESPLIT_H];
-#pragma unroll
-      for (int a_ = 0; a_ < ESPLIT_H; ++a_) {
-        ey[a_] = 0.0;
-#pragma unroll
-        for (int e = 0; e < 2; ++e)
-#pragma unroll
-          for (int n = 0; n < NT8; ++n) { e0[a_][e][n] = 0.0; e1[a_][e][n] = 0.0; }
-      }
       int sb = 0, gb = 0;
       for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
       for (int k = sd.k0; k < sd.k1; ++k) {
@@ -311,7 +326,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
           cfill = 0;
         }
         TCLK(tw1);
-        if (wid == 0 && lane == 0) TACC(48, tw1 - tw0);
+        if (lane == 0) TACC(48, tw1 - tw0);
         const TB* blk = ring + (static_cast<int64_t>(cs) * CHUNK + cfill) * 64;
         auto tile = [&](int pos) -> const TB* { return blk + pos * 64; };
         // one k-tile step: x[hh] += A_hh D[k-tile kt] (hh = 0, 1 independent DMMA chains), and the y column
@@ -399,14 +414,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
               }
               fold(t0, t1, ty, sb * RR + rr);
             }
-            if (esplit && !diag) {                            // thin row, split: tiles (a, wa)
-#pragma unroll
-              for (int a_ = 0; a_ < ESPLIT_H; ++a_)
-                if (a_ < h) {
-                  const double2 ad = ldA2(tile(wa * h + a_) + offD);
-                  step(e0[a_], e1[a_], ey[a_], ad.x, ad.y, 8 * sb + wa);
-                }
-            } else if (wa < h) {                              // direct: row a = wa
+            if (wa < h) {                                     // direct: row a = wa
               const int arow = wa;
               const int b_hi = diag ? arow : w - 1;
               for (int bb = 0; bb <= b_hi; ++bb) {
@@ -420,51 +428,27 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         }
         long long tw2 = 0;
         TCLK(tw2);
-        if (wid == 0 && lane == 0) {
+        if (lane == 0) {
           TACC(49, tw2 - tw1);
-          const int ty = (h == 8 && w == 8) ? (diag ? 0 : 1) : 2;   // full diagonal / full off-diagonal / edge
-          TACC(50 + 2 * ty, tw2 - tw1);
-          TACC(51 + 2 * ty, 1);
         }
         cfill += nt;
         if (++gb == ns) { ++sb; gb = sb; }
       }
-      if (esplit) {
-        // thin-row partials: every warp publishes, warp a sums them in warp order into its tile row
-        auto bar_mma = [&]() { asm volatile("bar.sync 3, %0;" ::"r"(PNM * 32) : "memory"); };
-#pragma unroll
-        for (int a_ = 0; a_ < ESPLIT_H; ++a_)
-          if (a_ < hl) {
-            double* e = Esc + ((wid * ESPLIT_H + a_) * 32 + lane) * 3;
-            e[0] = e0[a_][0][0] + e0[a_][1][0];
-            e[1] = e1[a_][0][0] + e1[a_][1][0];
-            e[2] = ey[a_];
-          }
-        bar_mma();
-        if (wid < hl) {
-          double s0 = 0.0, s1 = 0.0, sy = 0.0;
-          for (int w2 = 0; w2 < PNM; ++w2) {
-            const double* e = Esc + ((w2 * ESPLIT_H + wid) * 32 + lane) * 3;
-            s0 += e[0];
-            s1 += e[1];
-            sy += e[2];
-          }
-#pragma unroll
-          for (int j = 0; j < MTMAX; ++j)
-            if (j == ns - 1) { acc[0][0][j] += s0; acc[0][1][j] += s1; accy[j] += sy; }
-        }
-        bar_mma();
-      }
+      TCLK(tp2);
       // y column: sum the 4 k-lanes of each row quad
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 1);
         accy[j] += __shfl_xor_sync(0xffffffffu, accy[j], 2);
       }
+      TCLK(tp3);
+      if (lane == 0) { TACC(52, tp3 - tp2); TACC(53, tp3 - tp1); }
       if (wid == 0 && lane == 0 && q < 8) TR(12 + q);
       const int ax = q % nacc;
       mbar_wait_sleep(&accfree[ax], static_cast<uint32_t>((q / nacc) & 1), 128);
       double* Acc = Accb + ax * accstride;
+      TCLK(tp4);
+      if (lane == 0) TACC(51, tp4 - tp3);
       if (wid == 0 && lane == 0 && q < 8) TR(20 + q);
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
@@ -587,21 +571,31 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     const double* Mr[LRG];
 #pragma unroll
     for (int g = 0; g < LRG; ++g)
-      Mr[g] = P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q0 + min(g, nq - 1)].blk) * nc;
+      Mr[g] = a.mst ? Mst + static_cast<int64_t>(q0 + min(g, nq - 1)) * nc
+                    : P->Mp + static_cast<int64_t>(a.lr_row0 + a.L.segs[s_lo + q0 + min(g, nq - 1)].blk) * nc;
     double t[LRG][4];
 #pragma unroll
     for (int g = 0; g < LRG; ++g)
 #pragma unroll
       for (int u = 0; u < 4; ++u) t[g][u] = 0.0;
     if (cact) {
+      const double* Sst = reinterpret_cast<const double*>(smraw + L_.ring);
 #pragma unroll 4
       for (int j = jl; j < nc; j += NJ) {
-        const double2* sr = reinterpret_cast<const double2*>(SD + static_cast<int64_t>(j) * MAXC + 4 * cg);
-        const double2 s01 = __ldcg(sr), s23 = __ldcg(sr + 1);
+        double2 s01, s23;
+        if (lrk > 0) {
+          const double2* sr = reinterpret_cast<const double2*>(Sst + j * MAXC + 4 * cg);
+          s01 = sr[0];
+          s23 = sr[1];
+        } else {
+          const double2* sr = reinterpret_cast<const double2*>(SD + static_cast<int64_t>(j) * MAXC + 4 * cg);
+          s01 = __ldcg(sr);
+          s23 = __ldcg(sr + 1);
+        }
         const double x[4] = {s01.x, s01.y, s23.x, s23.y};
         double m[LRG];
 #pragma unroll
-        for (int g = 0; g < LRG; ++g) m[g] = __ldg(Mr[g] + j);
+        for (int g = 0; g < LRG; ++g) m[g] = a.mst ? Mr[g][j] : __ldg(Mr[g] + j);
 #pragma unroll
         for (int g = 0; g < LRG; ++g)
 #pragma unroll
@@ -645,7 +639,22 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       bar_epi<PNE>();
     }
     if (pend >= 0) { finish_d(pend, a.fuse_p); pend = -1; }
-    if (q % LRG == 0) lr_rows(q);                    // low-rank rows of pieces q .. q + LRG - 1
+    if (a.mst && q == 0) {
+      mbar_wait_sleep(&mfull, 0u, 64);
+      if (et == 0) TR(1);
+    }
+    if (lrk > 0) {
+      if (q == 0) {
+        // staged S: the low-rank rows of every piece now, then the staging slots go to the stream
+        mbar_wait_sleep(&full[0], 0u, 64);
+        if (et == 0) TR(3);
+        for (int q0 = 0; q0 < nseg; q0 += LRG) lr_rows(q0);
+        if (et == 0)
+          for (int k = 0; k < lrk; ++k) mbar_arrive_cnt(&empty[k], PNM);
+      }
+    } else if (q % LRG == 0) {
+      lr_rows(q);                                    // low-rank rows of pieces q .. q + LRG - 1
+    }
     if (et == 0 && q == 0) TR(28);
     // register prefetch of this piece's epilogue inputs for the first row of every thread (the
     // latency hides behind the wait for the MMA warps)
@@ -789,11 +798,16 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
       if (et == 0) a.st->ticket[a.fin] = 0;
     }
   }
-  if (et == 0) TR(45);
+  if (et == 0) {
+    TR(45);
+    long long clk_end = 0;
+    TCLK(clk_end);
+    TRV(47, clk_end - clk_start);
+  }
 }
 
 // --------------------------------------------------------------------------------------- host
-bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a) {
+bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, int lr_nc, ApplyArgs& a) {
   int dev = 0, optin = 0;
   cudaGetDevice(&dev);
   if (cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || optin <= 0)
@@ -807,19 +821,27 @@ bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a
   const int es = f32 ? 4 : 8;
   const int pne = 7;
   const size_t budget = static_cast<size_t>(optin) - 8192;   // static shared memory + margin
-  // a second Acc buffer (the MMA warps run a piece ahead of the epilogue) when the ring keeps >= 4 slots
-  int nacc = 2, ns = 0;
-  for (; nacc >= 1; --nacc) {
-    const PackSmem fixed = pack_smem(0, es, ld_max, a.nt8, 8, pne, seg_max, nacc);
+  // options in order of preference, the first that keeps >= 4 ring slots: a second Acc buffer (the
+  // MMA warps run a piece ahead of the epilogue) and the staged M' rows (bulk copies, 16-byte rows)
+  const int64_t mst_need = static_cast<int64_t>(seg_max) * lr_nc;
+  const bool mst_ok = (lr_nc % 2) == 0;
+  const int opts[4][2] = {{2, 1}, {1, 1}, {2, 0}, {1, 0}};
+  int ns = 0, nacc = 1, mst = 0;
+  for (int o = 0; o < 5; ++o) {
+    const int na = o < 4 ? opts[o][0] : 1, ms = o < 4 ? opts[o][1] : 0;
+    if (ms && !mst_ok) continue;
+    const PackSmem fixed = pack_smem(0, es, ld_max, a.nt8, pne, seg_max, na, ms ? mst_need : 0);
     if (fixed.total >= budget) continue;
-    ns = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(CHUNK) * 64 * es)));
-    if (ns >= 4 || (nacc == 1 && ns >= 2)) break;
+    const int n = static_cast<int>(std::min<size_t>(MAX_NSTAGE, (budget - fixed.total) / (static_cast<size_t>(CHUNK) * 64 * es)));
+    if (n >= 4 || (o == 4 && n >= 2)) { ns = n; nacc = na; mst = ms; break; }
   }
-  if (nacc < 1 || ns < 2) return false;
+  if (ns < 2) return false;
   a.nacc = nacc;
+  a.mst = mst;
+  a.lr_stage_s = 1;                                          // S rows staged (measured 63.7 vs 68.0 us at C3)
   a.slot_tiles = CHUNK;
   a.nstage = ns;
-  a.smem = pack_smem(ns, es, ld_max, a.nt8, 8, pne, seg_max, nacc).total;
+  a.smem = pack_smem(ns, es, ld_max, a.nt8, pne, seg_max, nacc, mst ? mst_need : 0).total;
   return true;
 }
 

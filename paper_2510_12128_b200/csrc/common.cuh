@@ -176,7 +176,8 @@ struct ApplyArgs {
   // packed apply: split-cluster partial sums / tickets, launch plan
   double* split_part;
   unsigned int* split_ticket;
-  int grid, slot_tiles, nstage, mtmax, nt8, f32, nacc;
+  int grid, slot_tiles, nstage, mtmax, nt8, f32, nacc, mst;
+  int lr_stage_s;          // stage the S rows of the low-rank term in the ring (set by plan_packed_apply)
   size_t smem;
   int ld_max;
   // big-block path (ld > 512, apply_big_kernel): low-rank rows T = M'S from lowrank_kernel

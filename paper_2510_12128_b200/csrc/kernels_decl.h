@@ -65,7 +65,7 @@ void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s
 
 // apply_kernels.cu (packed symmetric blocks, ld_max <= 512)
 // Plans the launch (smem ring, m-tiles per warp, probe n-tiles) into a; false if it cannot run.
-bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, ApplyArgs& a);
+bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, int lr_nc, ApplyArgs& a);
 void launch_apply_packed(const ApplyArgs& a, cudaStream_t s);
 
 // big_kernels.cu (ld_max > 512)

@@ -52,7 +52,7 @@ for b in range(148):
     r = T[b]
     nseg = int(r[46])
     ends.append(us(r[45]))
-    line = [f"cta {b:3d} nseg {nseg:2d} start {us(r[0]):6.1f} lr {us(r[28]):6.1f} stg {us(r[1]):6.1f} prod_end {us(r[2]):6.1f}"]
+    line = [f"cta {b:3d} nseg {nseg:2d} start {us(r[0]):6.1f} M' {us(r[1]):6.1f} S {us(r[3]):6.1f} lr {us(r[28]):6.1f} prod_end {us(r[2]):6.1f}"]
     for q in range(min(nseg, 8)):
         line.append(f" | q{q} mma {us(r[4+q]):6.1f}-{us(r[12+q]):6.1f} free {us(r[20+q]):6.1f} epi {us(r[29+q]):6.1f}-{us(r[37+q]):6.1f}")
     line.append(f" | end {us(r[45]):6.1f}")
@@ -61,13 +61,18 @@ e = np.array(ends)
 wt, ct = T[:, 48].astype(float), T[:, 49].astype(float)
 print(f"MMA warp 0 cycles: chunk waits median {np.median(wt):.0f}, block compute median {np.median(ct):.0f} "
       f"(sum median {np.median(wt + ct):.0f})")
-for ty, nm in enumerate(["diag full", "off-diag full", "edge"]):
-    cyc, cnt = T[:, 50 + 2 * ty].astype(float), T[:, 51 + 2 * ty].astype(float)
-    ok = cnt > 0
-    if ok.any():
-        print(f"  {nm:14s}: median {np.median(cyc[ok] / cnt[ok]):.0f} cycles per block, median count {np.median(cnt[ok]):.0f}")
+mhz = T[:, 47].astype(float) / np.maximum(1e-9, (T[:, 45] - T[:, 0]).astype(float)) * 1e3
+print(f"effective SM clock over the kernel: median {np.median(mhz):.0f} MHz")
+pw = T[:, 56:64].astype(float)
+print(f"MMA warps (blocks + chunk waits) cycles: per-CTA min over warps median {np.median(pw.min(1)):.0f}, "
+      f"max over warps median {np.median(pw.max(1)):.0f}; per warp median {np.median(pw, 0).astype(int).tolist()}")
+for k, nm in [(50, "dready waits"), (51, "accfree waits"), (52, "esplit + tail"), (53, "piece intervals")]:
+    print(f"  warp 0 {nm:16s}: median {np.median(T[:, k].astype(float)):.0f} cycles")
 print(f"kernel end: min {np.nanmin(e):.1f} median {np.nanmedian(e):.1f} max {np.nanmax(e):.1f} us")
 first_mma = np.array([us(T[b][4]) for b in range(148)])
 print(f"first MMA piece start: median {np.nanmedian(first_mma):.1f} max {np.nanmax(first_mma):.1f}")
+for k, nm in [(1, "M' rows staged"), (3, "S rows staged")]:
+    v = np.array([us(T[b][k]) for b in range(148)])
+    print(f"{nm}: median {np.nanmedian(v):.1f} max {np.nanmax(v):.1f}")
 lr = np.array([us(T[b][28]) for b in range(148)])
 print(f"low-rank rows done: median {np.nanmedian(lr):.1f} max {np.nanmax(lr):.1f}")
