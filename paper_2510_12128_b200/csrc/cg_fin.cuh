@@ -180,23 +180,52 @@ static __device__ void fin_update_body(CGState* st, const EvalParams* P, const d
   }
   __syncthreads();
   if (sp.SR) {
-    const double* SPo = sp.SP[par];
-    double* SPn = sp.SP[par ^ 1];
-    for (int idx = threadIdx.x; idx < sp.n_c * ncol; idx += blockDim.x) {
-      const int j = idx / ncol, c = idx - j * ncol;
-      const double y = SPo[static_cast<int64_t>(j) * MAXC + c];
-      double v = y;
-      if (act[c]) {
-        double x;
-        if (sp.tile0) {
-          x = 0.0;
-          for (int t = sp.tile0[j]; t < sp.tile0[j + 1]; ++t) x += sp.SR[static_cast<int64_t>(t) * MAXC + c];
-        } else {
-          x = sp.SR[static_cast<int64_t>(j) * MAXC + c];
+    // all CTA threads, 16-byte rows pairs, eight loads of each in flight before the stores
+    __shared__ double sbeta[MAXC];
+    __shared__ int sact[MAXC];
+    if (threadIdx.x < MAXC) {
+      const int c = threadIdx.x;
+      sact[c] = (c < ncol) ? act[c] : 0;
+      sbeta[c] = (c < ncol && act[c]) ? st->beta[c] : 0.0;
+    }
+    __syncthreads();
+    const double2* SPo2 = reinterpret_cast<const double2*>(sp.SP[par]);
+    double2* SPn2 = reinterpret_cast<double2*>(sp.SP[par ^ 1]);
+    const double2* SR2 = reinterpret_cast<const double2*>(sp.SR);
+    const int tot = sp.n_c * (MAXC / 2);
+    constexpr int U = 8;
+    for (int base = threadIdx.x; base < tot; base += U * blockDim.x) {
+      double2 y[U], x[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        y[u] = make_double2(0.0, 0.0);
+        x[u] = make_double2(0.0, 0.0);
+        if (idx < tot) {
+          y[u] = SPo2[idx];
+          if (sp.tile0) {
+            const int j = idx / (MAXC / 2), h = idx - j * (MAXC / 2);
+            for (int t = sp.tile0[j]; t < sp.tile0[j + 1]; ++t) {
+              const double2 w = SR2[static_cast<int64_t>(t) * (MAXC / 2) + h];
+              x[u].x += w.x;
+              x[u].y += w.y;
+            }
+          } else {
+            x[u] = SR2[idx];
+          }
         }
-        v = x + st->beta[c] * y;
       }
-      SPn[static_cast<int64_t>(j) * MAXC + c] = v;
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int idx = base + u * blockDim.x;
+        if (idx < tot) {
+          const int c0 = 2 * (idx % (MAXC / 2));
+          double2 v;
+          v.x = sact[c0] ? x[u].x + sbeta[c0] * y[u].x : y[u].x;
+          v.y = sact[c0 + 1] ? x[u].y + sbeta[c0 + 1] * y[u].y : y[u].y;
+          SPn2[idx] = v;
+        }
+      }
     }
   }
   if (threadIdx.x == 0) {
