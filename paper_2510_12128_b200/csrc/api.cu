@@ -16,6 +16,7 @@
 
 #include "../../include/nugpr.h"
 #include "common.cuh"
+#include "nccl_rt.h"
 #include "kernels_decl.h"
 #include "tridiag.h"
 
@@ -79,8 +80,9 @@ struct HostLayout {
 };
 
 // Cut the packed tile stream of all clusters (blocks in storage order, cluster after cluster) into at
-// most PACK_CTAS pieces of (nearly) equal tile count at block boundaries; a block goes to the CTA
-// whose range holds its midpoint.  Clusters may span several CTAs (<= MAX_PARTS; the target
+// most PACK_CTAS pieces of (nearly) equal tile count: whole clusters where a cluster fits one CTA's
+// share, else at block boundaries; a block (whole cluster) goes to the CTA whose range holds its
+// midpoint.  Clusters may span several CTAs (<= MAX_PARTS; the target
 // grows until that holds).  The partition depends only on the offsets (not on the device).
 static void make_partition(HostLayout& L) {
   const int n_c = L.n_c;
@@ -100,7 +102,13 @@ static void make_partition(HostLayout& L) {
       for (int sb = 0; sb < ns; ++sb)
         for (int gb = sb; gb < ns; ++gb, ++bi) {
           const int64_t len = pk_blk_size(gb, sb, mt);
-          const int cta = static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + len) * G / (2 * total)));
+          // a cluster that fits one CTA's share stays whole (its CTA is the one holding its midpoint):
+          // a split costs a global combine and a second epilogue chain (C3: 818 vs 748 evals/s whole);
+          // larger clusters are cut at block boundaries
+          const int64_t ctot = tri_tiles(mt);
+          const bool whole = ctot * G <= total;
+          const int cta = whole ? (bi == 0 ? static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + ctot) * G / (2 * total))) : cur)
+                                : static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + len) * G / (2 * total)));
           const SegDesc fresh{i, bi, bi + 1, 0, 0, -1, 0, L.pboff[i] / 64 + loc, static_cast<int32_t>(len), 0};
           if (cta != cur) {                          // a new CTA starts here
             L.seg0.push_back(static_cast<int32_t>(L.segs.size()));
@@ -372,6 +380,10 @@ struct nugpr_ctx {
   void* ag_user = nullptr;
   nugpr_allreduce_fn ar = nullptr;       // PAR-2 cluster sharding (nugpr_ctx_set_cluster_shard)
   void* ar_user = nullptr;
+  bool shard_on = false;                 // PAR-2 enabled (callback or in-library NCCL)
+  ncclComm_t nccl = nullptr;             // in-library communicator (nugpr_ctx_set_nccl)
+  bool shard_graph_ok = true;            // the sharded CG loop captures into a graph (NCCL)
+  void* nccl_scratch = nullptr;          // 64 KB device scratch for the host-record allgather
   int32_t* h_flag = nullptr;             // pinned
   nugpr_mll_out* h_out = nullptr;        // pinned
   bool prof = false;
@@ -526,6 +538,38 @@ nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, 
   if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
   ctx->ar = fn;
   ctx->ar_user = user;
+  ctx->shard_on = fn != nullptr;
+  return NUGPR_OK;
+}
+
+int32_t nugpr_ctx_sharded_graphs(const nugpr_ctx* ctx) {
+  return (ctx && ctx->nccl && ctx->shard_graph_ok && ctx->use_graphs) ? 1 : 0;
+}
+
+nugpr_status nugpr_nccl_unique_id(uint8_t* id) {
+  if (!id) return fail(NUGPR_ERR_INVALID_ARG, "id is NULL");
+  const NcclRT& rt = nccl_rt();
+  if (!rt.ok) return fail(NUGPR_ERR_UNSUPPORTED, "libnccl.so.2 not found in the process or on the loader path");
+  ncclUniqueId u;
+  const ncclResult_t r = rt.GetUniqueId(&u);
+  if (r != ncclSuccess) return fail(NUGPR_ERR_COMM, "ncclGetUniqueId: %s", rt.GetErrorString(r));
+  static_assert(sizeof(ncclUniqueId) == NUGPR_NCCL_ID_BYTES, "NCCL unique id size");
+  memcpy(id, &u, sizeof(u));
+  return NUGPR_OK;
+}
+
+nugpr_status nugpr_ctx_set_nccl(nugpr_ctx* ctx, const uint8_t* id) {
+  if (!ctx || !id) return fail(NUGPR_ERR_INVALID_ARG, "ctx / id is NULL");
+  if (ctx->device < 0) return fail(NUGPR_ERR_INVALID_ARG, "host-only context");
+  const NcclRT& rt = nccl_rt();
+  if (!rt.ok) return fail(NUGPR_ERR_UNSUPPORTED, "libnccl.so.2 not found in the process or on the loader path");
+  CK(cudaSetDevice(ctx->device));
+  if (ctx->nccl) { rt.CommDestroy(ctx->nccl); ctx->nccl = nullptr; }
+  ncclUniqueId u;
+  memcpy(&u, id, sizeof(u));
+  const ncclResult_t r = rt.CommInitRank(&ctx->nccl, ctx->world, u, ctx->rank);
+  if (r != ncclSuccess) { ctx->nccl = nullptr; return fail(NUGPR_ERR_COMM, "ncclCommInitRank: %s", rt.GetErrorString(r)); }
+  if (!ctx->nccl_scratch) CK(cudaMalloc(&ctx->nccl_scratch, 65536));
   return NUGPR_OK;
 }
 
@@ -533,6 +577,11 @@ nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value)
   if (!ctx) return fail(NUGPR_ERR_INVALID_ARG, "ctx is NULL");
   switch (option) {
     case NUGPR_OPT_GRAPHS: ctx->use_graphs = value != 0; return NUGPR_OK;
+    case NUGPR_OPT_SHARD_CLUSTERS:
+      if (value && !ctx->nccl && !ctx->ar)
+        return fail(NUGPR_ERR_INVALID_ARG, "cluster sharding needs nugpr_ctx_set_nccl or an allreduce callback");
+      ctx->shard_on = value != 0;
+      return NUGPR_OK;
     default: return fail(NUGPR_ERR_INVALID_ARG, "unknown option %d", option);
   }
 }
@@ -578,6 +627,8 @@ nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx) {
   if (ctx->h_flag) cudaFreeHost(ctx->h_flag);
   if (ctx->h_out) cudaFreeHost(ctx->h_out);
   if (ctx->h_prm) cudaFreeHost(ctx->h_prm);
+  if (ctx->nccl) nccl_rt().CommDestroy(ctx->nccl);
+  if (ctx->nccl_scratch) cudaFree(ctx->nccl_scratch);
   delete ctx;
   return NUGPR_OK;
 }
@@ -682,6 +733,12 @@ static nugpr_status enqueue_lambda0(nugpr_blocks* bl, const double* K, const dou
 // global array in which each rank filled only its own clusters' slots: exact, and every rank ends
 // with the partials a single GPU would hold, in the same order.
 static nugpr_status xchg(nugpr_ctx* ctx, const double* send, double* recv, size_t count, cudaStream_t s) {
+  if (ctx->nccl) {                        // in-library NCCL on the stream (capturable into the graph)
+    const NcclRT& rt = nccl_rt();
+    const ncclResult_t r = rt.AllReduce(send, recv, count, ncclFloat64, ncclSum, ctx->nccl, s);
+    if (r != ncclSuccess) return fail(NUGPR_ERR_COMM, "ncclAllReduce: %s", rt.GetErrorString(r));
+    return NUGPR_OK;
+  }
   if (!ctx->ar) return fail(NUGPR_ERR_COMM, "sharded blocks but no allreduce callback on the context");
   if (ctx->ar(send, recv, count, static_cast<void*>(s), ctx->ar_user) != 0)
     return fail(NUGPR_ERR_COMM, "allreduce callback failed (PAR-2 exchange)");
@@ -744,7 +801,7 @@ static nugpr_status build_impl(nugpr_ctx* ctx, const double* X_sorted, const int
   cudaGetLastError();   // drop stale errors left by unrelated runtime calls
   if (!offsets) return fail(NUGPR_ERR_INVALID_ARG, "offsets is NULL");
   // PAR-2: this rank keeps the contiguous cluster range [c_lo, c_hi) (local layout, local blocks)
-  const bool shard = ctx->ar != nullptr;
+  const bool shard = ctx->shard_on;
   int c_lo = 0, c_hi = n_c;
   std::vector<int64_t> loff;
   const int64_t* offs = offsets;
@@ -1360,6 +1417,42 @@ static void launch_tail_final(nugpr_blocks* bl, EvalDev& e, const IterArgs& A, i
                ncol, logdet_mode, e.out, s);
 }
 
+// PAR-2 (sharded) CG iteration / tail: the same kernels on this rank's clusters with the three
+// partial exchanges per iteration and the finalisers as fin_kernel launches after them; enqueued
+// directly (host-driven loop) or captured into the evaluation graph when the exchanges are the
+// library's own NCCL collectives (cond: the graph's while handle, set by FIN_UPDATE).
+static nugpr_status launch_iteration_shard(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, const IterArgs& A,
+                                           int ncol, cudaStream_t s, unsigned long long cond, double apply_bytes = 0.0) {
+  const size_t XG = static_cast<size_t>(bl->n_cg) * MAXC;
+  double* xs = e.xs, *xr = e.xr;
+  const int cls = PC_APPLY_B;
+  PROF(ctx, cls, apply_bytes, s, launch_apply(A.a1, A.ncp, s));
+  RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                        // S(A p)
+  PROF(ctx, cls, apply_bytes, s, launch_apply(A.a2, A.ncp, s));
+  RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                        // p^T q
+  launch_fin(FIN_ALPHA, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, e.ah, HIST, s);
+  PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
+  RET(xchg(ctx, xs, xr, 2 * XG, s));                                      // r^T r, S(r)
+  launch_fin(FIN_UPDATE, e.st, e.prm, xr, bl->n_cg, ncol, e.bh, HIST, s, xr + XG, e.SPb[0], e.SPb[1], cond);
+  return NUGPR_OK;
+}
+static nugpr_status launch_tail_shard(nugpr_ctx* ctx, nugpr_blocks* bl, EvalDev& e, const IterArgs& A, int ncol,
+                                      int logdet_mode, cudaStream_t s, double apply_bytes = 0.0) {
+  const size_t XG = static_cast<size_t>(bl->n_cg) * MAXC, XO = static_cast<size_t>(bl->c_lo) * MAXC;
+  double* xs = e.xs, *xr = e.xr;
+  launch_spart(bl->Ld, bl->B.u, e.X, ncol, xs + 2 * XG + XO, s);
+  RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                        // S(x)
+  PROF(ctx, PC_APPLY_B, apply_bytes, s, launch_apply(A.a3, A.ncp, s));
+  RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                        // S(A x)
+  PROF(ctx, PC_APPLY_B, apply_bytes, s, launch_apply(A.a4, A.ncp, s));
+  RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                        // quad, trace dots
+  launch_fin(FIN_TRACE, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, nullptr, HIST, s);
+  launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, bl->B.scal + 0, static_cast<double>(bl->n_glob),
+               ncol, logdet_mode, e.out, s);
+  CKL();
+  return NUGPR_OK;
+}
+
 // Graph of one slot: while (any column active) { CG iteration }; spart; trace applies; final.
 static std::string graph_key(const nugpr_blocks* bl, int slot, int ncol, int logdet_mode) {
   char buf[160];
@@ -1492,11 +1585,18 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   }
   if (prep_only) return NUGPR_OK;
   const bool useB = P.B != nullptr;
-  if (!ctx->prof && ctx->use_graphs && !bl->shard) {
+  if (!ctx->prof && ctx->use_graphs && (!bl->shard || (ctx->nccl && ctx->shard_graph_ok))) {
     cudaGraphExec_t ex = nullptr;
-    RET(get_graph(ctx, bl, slot, ncol, cfg->logdet_mode, &ex));
-    CK(cudaGraphLaunch(ex, s));
-    return NUGPR_OK;
+    const nugpr_status gs = get_graph(ctx, bl, slot, ncol, cfg->logdet_mode, &ex);
+    if (gs == NUGPR_OK) {
+      CK(cudaGraphLaunch(ex, s));
+      return NUGPR_OK;
+    }
+    if (!bl->shard) return gs;
+    // the NCCL collectives could not be captured into a conditional graph on this system: keep the
+    // host-driven sharded loop (same kernels, same exchanges)
+    cudaGetLastError();
+    ctx->shard_graph_ok = false;
   }
   // direct launches (profiling / NUGPR_OPT_GRAPHS = 0): host polls the activity flag every CH iterations
   IterArgs A;
@@ -1516,35 +1616,16 @@ static nugpr_status enqueue_eval(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, con
   const int CH = 4;
   int done = 0;
   if (bl->shard) {
-    // PAR-2 CG: the same kernels on this rank's clusters, three exchanges per iteration
-    double* xs = e.xs, *xr = e.xr;
+    // PAR-2 CG (callback exchanges or profiling): host-driven, the activity flag read every CH iterations
     while (done < limit) {
-      for (int q = 0; q < CH && done < limit; ++q, ++done) {
-        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a1, A.ncp, s));
-        RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // S(A p)
-        PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a2, A.ncp, s));
-        RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                      // p^T q
-        launch_fin(FIN_ALPHA, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, e.ah, HIST, s);
-        PROF(ctx, PC_UPDATE, 0.0, s, launch_update(A.ua, A.ncp, s));
-        RET(xchg(ctx, xs, xr, 2 * XG, s));                                    // r^T r, S(r)
-        launch_fin(FIN_UPDATE, e.st, e.prm, xr, bl->n_cg, ncol, e.bh, HIST, s, xr + XG, e.SPb[0], e.SPb[1]);
-      }
+      for (int q = 0; q < CH && done < limit; ++q, ++done)
+        RET(launch_iteration_shard(ctx, bl, e, A, ncol, s, 0ull, apply_bytes));
       CKL();
       CK(cudaMemcpyAsync(ctx->h_flag, &e.st->any_active, sizeof(int32_t), cudaMemcpyDeviceToHost, s));
       CK(cudaStreamSynchronize(s));
       if (!*ctx->h_flag) break;
     }
-    launch_spart(Ld, B.u, e.X, ncol, xs + 2 * XG + XO, s);
-    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(x)
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a3, A.ncp, s));
-    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // S(A x)
-    PROF(ctx, apply_cls, apply_bytes, s, launch_apply(A.a4, A.ncp, s));
-    RET(xchg(ctx, xs + 2 * XG, xr + 2 * XG, XG, s));                          // quad, trace dots
-    launch_fin(FIN_TRACE, e.st, e.prm, xr + 2 * XG, bl->n_cg, ncol, nullptr, HIST, s);
-    launch_final(e.st, e.prm, e.ah, e.bh, HIST, e.slqw, B.scal + 0, static_cast<double>(bl->n_glob),
-                 ncol, cfg->logdet_mode, e.out, s);
-    CKL();
-    return NUGPR_OK;
+    return launch_tail_shard(ctx, bl, e, A, ncol, cfg->logdet_mode, s, apply_bytes);
   }
   while (done < limit) {
     for (int q = 0; q < CH && done < limit; ++q, ++done) {
@@ -1599,14 +1680,23 @@ static nugpr_status get_graph(nugpr_ctx* ctx, nugpr_blocks* bl, int slot, int nc
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   A.ua.cond = h;
   CK(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
-  launch_iteration(A, cs);
+  nugpr_status cst = NUGPR_OK;
+  if (bl->shard) {
+    A.ua.cond = 0;                                 // (FIN_UPDATE after the exchange sets the condition)
+    cst = launch_iteration_shard(ctx, bl, e, A, ncol, cs, h);
+  } else {
+    launch_iteration(A, cs);
+  }
   cudaGraph_t body_out = nullptr;
   cudaError_t ce = cudaStreamEndCapture(cs, &body_out);
+  if (cst != NUGPR_OK) { cudaGraphDestroy(g); return cst; }
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph body capture: %s", cudaGetErrorString(ce)); }
   CK(cudaStreamBeginCaptureToGraph(cs, g, &wnode, nullptr, 1, cudaStreamCaptureModeRelaxed));
-  launch_tail_final(bl, e, A, ncol, logdet_mode, cs);
+  if (bl->shard) cst = launch_tail_shard(ctx, bl, e, A, ncol, logdet_mode, cs);
+  else launch_tail_final(bl, e, A, ncol, logdet_mode, cs);
   cudaGraph_t g_out = nullptr;
   ce = cudaStreamEndCapture(cs, &g_out);
+  if (cst != NUGPR_OK) { cudaGraphDestroy(g); return cst; }
   if (ce != cudaSuccess) { cudaGraphDestroy(g); return fail(NUGPR_ERR_CUDA, "graph tail capture: %s", cudaGetErrorString(ce)); }
   cudaGraphExec_t ex = nullptr;
   ce = cudaGraphInstantiate(&ex, g, 0);
@@ -1733,7 +1823,20 @@ static nugpr_status central_exchange(nugpr_ctx* ctx, const int32_t* owner, const
                                      const double* h, double* L0, double* grad, nugpr_mll_out* evals,
                                      nugpr_status* worst, int world) {
   EvalRecord all[NUGPR_NUM_EVALS];
-  if (world > 1) {
+  if (world > 1 && ctx->nccl) {
+    // in-library NCCL: the records through the context's device scratch (one host sync)
+    const size_t nb = sizeof(EvalRecord) * NUGPR_NUM_EVALS;
+    if (nb * static_cast<size_t>(world) > 65536) return fail(NUGPR_ERR_INTERNAL, "record exchange scratch too small");
+    char* d = static_cast<char*>(ctx->nccl_scratch);
+    std::vector<EvalRecord> recv(static_cast<size_t>(world) * NUGPR_NUM_EVALS);
+    CK(cudaMemcpyAsync(d, mine, nb, cudaMemcpyHostToDevice, ctx->stream));
+    const NcclRT& rt = nccl_rt();
+    const ncclResult_t r = rt.AllGather(d, d + nb, nb, ncclUint8, ctx->nccl, ctx->stream);
+    if (r != ncclSuccess) return fail(NUGPR_ERR_COMM, "ncclAllGather: %s", rt.GetErrorString(r));
+    CK(cudaMemcpyAsync(recv.data(), d + nb, nb * world, cudaMemcpyDeviceToHost, ctx->stream));
+    CK(cudaStreamSynchronize(ctx->stream));
+    for (int k = 0; k < NUGPR_NUM_EVALS; ++k) all[k] = recv[static_cast<size_t>(owner[k]) * NUGPR_NUM_EVALS + k];
+  } else if (world > 1) {
     if (!ctx->ag) return fail(NUGPR_ERR_COMM, "world > 1 but no allgather callback set");
     std::vector<EvalRecord> recv(static_cast<size_t>(ctx->world) * NUGPR_NUM_EVALS);
     if (ctx->ag(mine, sizeof(EvalRecord) * NUGPR_NUM_EVALS, recv.data(), ctx->ag_user) != 0)
