@@ -171,14 +171,35 @@ nugpr_status nugpr_ctx_set_allgather(nugpr_ctx* ctx, nugpr_allgather_fn fn, void
  * ranks return the same status together; only a failing callback (NUGPR_ERR_COMM) can leave the
  * other ranks inside an exchange — treat it as fatal for the process group. */
 nugpr_status nugpr_ctx_set_cluster_shard(nugpr_ctx* ctx, nugpr_allreduce_fn fn, void* user);
+
+/* In-library NCCL (the library owns its collectives; PyTorch only carries the id).
+ * nugpr_nccl_unique_id writes an ncclUniqueId (NUGPR_NCCL_ID_BYTES bytes, caller memory) on ONE
+ * rank; the caller broadcasts those bytes to every rank (any transport), and every rank calls
+ * nugpr_ctx_set_nccl(ctx, id) — collective over the context's (rank, world), blocking until all
+ * ranks joined.  From then on the context's exchanges run as NCCL collectives on the context
+ * stream instead of the callbacks: the PAR-1 record allgather (through a 64 KB device scratch the
+ * call allocates — the library's only own device allocation, freed by nugpr_ctx_destroy) and the
+ * PAR-2 partial allreduces (FP64 sum on workspace pointers), which are then captured into the
+ * evaluation's device-driven CUDA graph (no host round trip per CG iteration).  NCCL is resolved
+ * at run time from the libnccl.so.2 already mapped into the process (torch's), else the loader
+ * path.  Errors: UNSUPPORTED (no libnccl), COMM (NCCL error; fatal for the group), CUDA. */
+#define NUGPR_NCCL_ID_BYTES 128
+nugpr_status nugpr_nccl_unique_id(uint8_t* id);
+nugpr_status nugpr_ctx_set_nccl(nugpr_ctx* ctx, const uint8_t* id);
+/* 1 if the context's sharded evaluations run their CG loop as a captured graph with the NCCL
+ * exchanges inside (0: host-driven loop — callbacks, profiling, graphs off, or the capture of the
+ * collectives was refused by the driver, after which the library keeps the host-driven loop). */
+int32_t nugpr_ctx_sharded_graphs(const nugpr_ctx* ctx);
 nugpr_status nugpr_ctx_destroy(nugpr_ctx* ctx);
 
 /* Execution options of a context (defaults in brackets).
+ *  NUGPR_OPT_SHARD_CLUSTERS [0]: 1 enables PAR-2 cluster sharding (as nugpr_ctx_set_cluster_shard)
+ *    over the in-library NCCL communicator (or the allreduce callback if one is set).
  *  NUGPR_OPT_GRAPHS [1]: each evaluation's CG loop runs as ONE CUDA graph whose conditional WHILE node
  *    is driven by the device (no host round trip per iteration); 0: the same kernels launched directly
  *    with a host poll of the activity flag every 4 iterations (profiling with ncu, which cannot see
  *    kernels inside conditional graphs).  Both give bit-identical results. */
-typedef enum { NUGPR_OPT_GRAPHS = 0 } nugpr_option;
+typedef enum { NUGPR_OPT_GRAPHS = 0, NUGPR_OPT_SHARD_CLUSTERS = 1 } nugpr_option;
 nugpr_status nugpr_ctx_set_option(nugpr_ctx* ctx, int32_t option, int32_t value);
 
 /* Kernel-class profiler (bench.py's live roofline): when enabled, CUDA events are recorded on

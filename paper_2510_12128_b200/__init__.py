@@ -78,10 +78,15 @@ class Context:
     group: an initialised torch.distributed process group (or True for the default group)
     enables perturbation sharding in numgrad/train via the allgather callback (PAR-1).
     shard_clusters=True additionally (PAR-2) keeps only this rank's cluster range in the blocks
-    and makes mll/numgrad/train collective over the group, with the library's partial-sum
-    exchanges routed through torch.distributed.all_reduce (NCCL on GPU boxes)."""
+    and makes mll/numgrad/train collective over the group.
 
-    def __init__(self, device: int = 0, stream=None, group=None, shard_clusters: bool = False):
+    comm: "nccl" — the library creates its own NCCL communicator (nugpr_ctx_set_nccl; torch only
+    broadcasts the 128-byte id) and runs every exchange as an NCCL collective on the context
+    stream, captured into the evaluation graphs; "callback" — the exchanges go through
+    torch.distributed from Python callbacks (gloo groups: CPU tests, several ranks on one GPU).
+    Default: "nccl" when the group's backend is NCCL, else "callback"."""
+
+    def __init__(self, device: int = 0, stream=None, group=None, shard_clusters: bool = False, comm=None):
         """device < 0: host-only context (rank/world/allgather for the host helpers; no CUDA)."""
         self.device = int(device)
         self.rank, self.world = 0, 1
@@ -103,7 +108,26 @@ class Context:
         N.check(N.lib().nugpr_ctx_create(self.device, sp, self.rank, self.world, C.byref(h)))
         self.handle = h
         self._cb = None
-        if self.world > 1:
+        self.comm = None
+        if group is not None and self.device >= 0:
+            import torch.distributed as dist
+            if comm is None:
+                comm = "nccl" if dist.get_backend(self.group) == "nccl" else "callback"
+            self.comm = comm
+            if comm == "nccl":
+                import torch
+                # the library's own communicator: rank 0 creates the id, torch broadcasts its bytes
+                idb = (C.c_uint8 * N.NCCL_ID_BYTES)()
+                if self.rank == 0:
+                    N.check(N.lib().nugpr_nccl_unique_id(idb))
+                t = torch.tensor(list(bytes(idb)), dtype=torch.uint8, device=torch.device("cuda", self.device))
+                dist.broadcast(t, src=dist.get_global_rank(self.group, 0) if self.group is not None else 0,
+                               group=self.group)
+                idb = (C.c_uint8 * N.NCCL_ID_BYTES)(*t.cpu().tolist())
+                N.check(N.lib().nugpr_ctx_set_nccl(self.handle, idb))
+            elif comm != "callback":
+                raise ValueError(f"comm must be 'nccl' or 'callback', not {comm!r}")
+        if self.world > 1 and self.comm != "nccl":
             self._cb = N.ALLGATHER_FN(self._allgather)
             N.check(N.lib().nugpr_ctx_set_allgather(self.handle, self._cb, None))
         self.shard_clusters = bool(shard_clusters)
@@ -113,8 +137,16 @@ class Context:
         if self.shard_clusters:
             if group is None:
                 raise ValueError("shard_clusters needs a torch.distributed process group")
-            self._ar_cb = N.ALLREDUCE_FN(self._allreduce)
-            N.check(N.lib().nugpr_ctx_set_cluster_shard(self.handle, self._ar_cb, None))
+            if self.comm == "nccl":
+                N.check(N.lib().nugpr_ctx_set_option(self.handle, N.OPTIONS["shard_clusters"], 1))
+            else:
+                self._ar_cb = N.ALLREDUCE_FN(self._allreduce)
+                N.check(N.lib().nugpr_ctx_set_cluster_shard(self.handle, self._ar_cb, None))
+
+    def sharded_graphs(self) -> bool:
+        """True if sharded evaluations run their CG loop as one captured graph with the library's
+        NCCL exchanges inside (nugpr_ctx_sharded_graphs)."""
+        return bool(N.lib().nugpr_ctx_sharded_graphs(self.handle))
 
     def register(self, buf):
         """Make a tensor's memory addressable by the PAR-2 exchange (build_blocks does this for

@@ -21,7 +21,8 @@ STATUS = {0: "OK", 1: "INVALID_ARG", 2: "SHAPE", 3: "NOT_SPD", 4: "DEGENERATE_RE
 KERNELS = {"rbf": 0, "matern52": 1, "rbf_as_printed": 2}
 REP_MODES = {"given": 0, "centroid": 1, "medoid": 2}
 MODES = {0: "baseline", 1: "noise", 2: "scale", 3: "generic"}
-OPTIONS = {"graphs": 0}
+OPTIONS = {"graphs": 0, "shard_clusters": 1}
+NCCL_ID_BYTES = 128
 PROF_CLASSES = {"apply_B": 0, "apply_lowrank": 1, "update": 2, "rhs": 3, "gemm": 4, "chol": 5,
                 "lanczos": 6, "other": 7}
 
@@ -115,6 +116,9 @@ def lib():
         "nugpr_shard_plan": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.c_int32, C.POINTER(C.c_int32)]),
         "nugpr_tridiag_eig": (C.c_int, [C.c_int32, C.POINTER(C.c_double), C.POINTER(C.c_double),
                                         C.POINTER(C.c_double), C.POINTER(C.c_double)]),
+        "nugpr_nccl_unique_id": (C.c_int, [P]),
+        "nugpr_ctx_set_nccl": (C.c_int, [P, P]),
+        "nugpr_ctx_sharded_graphs": (C.c_int32, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -135,4 +139,5 @@ EXPORTED = ["nugpr_version", "nugpr_last_error", "nugpr_ctx_create", "nugpr_ctx_
             "nugpr_blocks_export", "nugpr_mll", "nugpr_numgrad", "nugpr_train", "nugpr_adam_step",
             "nugpr_shard_plan", "nugpr_tridiag_eig", "nugpr_cluster_workspace_size", "nugpr_cluster",
             "nugpr_numgrad_exchange", "nugpr_predict", "nugpr_mll_exact", "nugpr_ctx_set_cluster_shard",
-            "nugpr_shard_range", "nugpr_workspace_size_shard", "nugpr_ctx_set_option"]
+            "nugpr_shard_range", "nugpr_workspace_size_shard", "nugpr_ctx_set_option",
+            "nugpr_nccl_unique_id", "nugpr_ctx_set_nccl", "nugpr_ctx_sharded_graphs"]

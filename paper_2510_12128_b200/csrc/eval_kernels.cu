@@ -24,12 +24,16 @@ namespace nugpr {
 // PAR-2 (cluster-sharded evaluation): the finaliser as its own single-CTA launch
 // after the exchange of the partials.  FIN_UPDATE skips when no column is active (as update does).
 __global__ void __launch_bounds__(NT) fin_kernel(int fin, CGState* st, const EvalParams* prm, const double* part,
-                                                 int n_tiles, int ncol, double* hist, int hist_stride, SPUpdate sp) {
+                                                 int n_tiles, int ncol, double* hist, int hist_stride, SPUpdate sp,
+                                                 unsigned long long cond) {
   if (fin == FIN_INIT) {
     fin_init_body(st, prm, part, n_tiles, ncol, NT / 32);
   } else if (fin == FIN_UPDATE) {
-    if (!st->any_active) return;
-    fin_update_body(st, prm, part, n_tiles, ncol, hist, hist_stride, 0ull, NT / 32, sp);
+    if (!st->any_active) {                       // (graph mode: end the CG while-loop)
+      if (cond && threadIdx.x == 0) cudaGraphSetConditional(cond, 0u);
+      return;
+    }
+    fin_update_body(st, prm, part, n_tiles, ncol, hist, hist_stride, cond, NT / 32, sp);
   } else {
     if (fin == FIN_ALPHA && !st->any_active) return;
     fin_alpha_trace_body(fin, st, part, n_tiles, ncol, hist, hist_stride, NT / 32);
@@ -541,9 +545,10 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
 }
 
 void launch_fin(int fin, CGState* st, const EvalParams* prm, const double* part, int n_tiles, int ncol,
-                double* hist, int hist_stride, cudaStream_t s, const double* SR, double* SP0, double* SP1) {
+                double* hist, int hist_stride, cudaStream_t s, const double* SR, double* SP0, double* SP1,
+                unsigned long long cond) {
   SPUpdate sp{SR, nullptr, n_tiles, {SP0, SP1}};
-  fin_kernel<<<1, NT, 0, s>>>(fin, st, prm, part, n_tiles, ncol, hist, hist_stride, sp);
+  fin_kernel<<<1, NT, 0, s>>>(fin, st, prm, part, n_tiles, ncol, hist, hist_stride, sp, cond);
   note_launch(); post_launch("fin_kernel");
 }
 

@@ -58,7 +58,7 @@ void launch_final(const CGState* st, const EvalParams* prm, const double* ah, co
 // PAR-2: single-CTA CG finaliser (FIN_INIT / FIN_ALPHA / FIN_UPDATE / FIN_TRACE) over exchanged partials
 void launch_fin(int fin, CGState* st, const EvalParams* prm, const double* part, int n_tiles, int ncol,
                 double* hist, int hist_stride, cudaStream_t s, const double* SR = nullptr, double* SP0 = nullptr,
-                double* SP1 = nullptr);
+                double* SP1 = nullptr, unsigned long long cond = 0);
 int quad_parts(int64_t n_pad, int cap);
 void launch_quad_part(const double* c, const double* x, int64_t n_pad, int nparts, double* part, cudaStream_t s);
 void launch_probe_gen(uint64_t seed, int m, int64_t n, double* Z, cudaStream_t s);

@@ -107,7 +107,7 @@ def run_all(P, ctx, case):
     return out
 
 
-def _worker(rank, world, port, backend, case, q):
+def _worker(rank, world, port, backend, case, q, comm=None):
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     sys.path.insert(0, root)
@@ -122,8 +122,9 @@ def _worker(rank, world, port, backend, case, q):
         dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import paper_2510_12128_b200 as P
-        ctx = P.Context(0, group=True, shard_clusters=True)
+        ctx = P.Context(0, group=True, shard_clusters=True, comm=comm)
         out = run_all(P, ctx, case)
+        out["sharded_graphs"] = ctx.sharded_graphs()
         if case != "variants":
             out["range"] = P.shard_range(dataset(case)[2], rank, world)
         out["exchanges"] = ctx.exchanges
@@ -145,12 +146,12 @@ def P():
     return pkg
 
 
-def spawn(world, backend, case):
+def spawn(world, backend, case, comm=None):
     import torch.multiprocessing as mp
     mctx = mp.get_context("spawn")
     q = mctx.Queue()
     port = _free_port()
-    procs = [mctx.Process(target=_worker, args=(r, world, port, backend, case, q)) for r in range(world)]
+    procs = [mctx.Process(target=_worker, args=(r, world, port, backend, case, q, comm)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
@@ -211,8 +212,15 @@ def test_cluster_shard_gloo_matches_replicated(P, world, case):
 
 
 def test_cluster_shard_nccl_world1(P):
-    outs = spawn(1, "nccl", "c3shape")
-    assert outs[0]["exchanges"] > 0
+    """Real NCCL group at world 1: the library's own communicator (nugpr_ctx_set_nccl; no Python
+    exchange callback runs, the sharded CG loop is one captured graph with the NCCL collectives
+    inside) and the callback route through torch.distributed both equal the replicated path."""
+    outs = spawn(1, "nccl", "c3shape", comm="nccl")
+    assert outs[0]["exchanges"] == 0
+    assert outs[0]["sharded_graphs"], "the NCCL exchanges were not captured into the evaluation graph"
+    check_against_replicated(P, outs, "c3shape")
+    outs = spawn(1, "nccl", "c3shape", comm="callback")
+    assert outs[0]["exchanges"] > 0 and not outs[0]["sharded_graphs"]
     check_against_replicated(P, outs, "c3shape")
 
 
