@@ -348,6 +348,27 @@ def run_ours(args):
         e1p.record(stream)
         torch.cuda.synchronize()
         phase["numgrad_ms"] = e0p.elapsed_time(e1p) / reps_ph
+        # each of the 7 central-difference evaluations ALONE on the GPU (its latency: what one rank
+        # of the perturbation-sharded gradient waits for; input of DESIGN §7's scaling model)
+        if not shard and world == 1:
+            l_, s_, a_ = th0
+            pts = [th0]
+            for i_ in range(3):
+                for sg in (1, -1):
+                    p_ = [l_, s_, a_]
+                    p_[i_] = p_[i_] + sg * 1e-3 * p_[i_]
+                    pts.append(tuple(p_))
+            solo = []
+            for th in pts:
+                P.mll(ctx, blk, yd, th, probe_seed=seed, num_probes=8, block_storage=args.blocks, logdet=args.logdet)
+                e0p.record(stream)
+                for _ in range(reps_ph):
+                    P.mll(ctx, blk, yd, th, probe_seed=seed, num_probes=8, block_storage=args.blocks,
+                          logdet=args.logdet)
+                e1p.record(stream)
+                torch.cuda.synchronize()
+                solo.append(round(e0p.elapsed_time(e1p) / reps_ph, 4))
+            phase["solo_eval_ms"] = solo        # [theta, l+, l-, noise+, noise-, scale+, scale-]
         blk.close()
     except Exception as ex:  # noqa: BLE001
         phase["error"] = str(ex)[:200]
