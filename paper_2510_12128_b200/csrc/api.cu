@@ -102,11 +102,12 @@ static void make_partition(HostLayout& L) {
       for (int sb = 0; sb < ns; ++sb)
         for (int gb = sb; gb < ns; ++gb, ++bi) {
           const int64_t len = pk_blk_size(gb, sb, mt);
-          // a cluster that fits one CTA's share stays whole (its CTA is the one holding its midpoint):
-          // a split costs a global combine and a second epilogue chain (C3: 818 vs 748 evals/s whole);
-          // larger clusters are cut at block boundaries
+          // a cluster of up to two CTA shares stays whole (its CTA is the one holding its midpoint; CTAs
+          // left without work are not launched): a split costs a global combine and a second epilogue
+          // chain (C3: 818 vs 748 evals/s whole; C2, 1.5 shares per cluster: 2391 vs 1823); larger
+          // clusters are cut at block boundaries
           const int64_t ctot = tri_tiles(mt);
-          const bool whole = ctot * G <= total;
+          const bool whole = ctot * G <= 2 * total;        // <= 2 shares (C2: 2391 vs 1823 evals/s at 1)
           const int cta = whole ? (bi == 0 ? static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + ctot) * G / (2 * total))) : cur)
                                 : static_cast<int>(std::min<int64_t>(G - 1, (2 * cum + len) * G / (2 * total)));
           const SegDesc fresh{i, bi, bi + 1, 0, 0, -1, 0, L.pboff[i] / 64 + loc, static_cast<int32_t>(len), 0};
