@@ -377,6 +377,12 @@ void launch_big_chol_trtri(double* A, const LayoutDev& L, const int32_t* list, i
 // 64-deep chunks staged in shared memory with plain coalesced loads (each chunk: 64 column
 // segments of B and the c columns of D).  Epilogue and partial sums as in apply_kernel; the
 // S / dot partials are per tile (lowrank sums a cluster's tiles through tile0).
+// (not volatile: a pure function of its operands)
+__device__ __forceinline__ void dmma_big(double& d0, double& d1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+      : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
 template <int NCP>
 __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
   if (a.gate && !a.st->any_active) return;
@@ -422,6 +428,9 @@ __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
   double acc[CPT];
 #pragma unroll
   for (int q = 0; q < CPT; ++q) acc[q] = 0.0;
+  const int qr = lane >> 2, qc = lane & 3;
+  double m0[2] = {0.0, 0.0}, m1[2] = {0.0, 0.0}, my = 0.0;   // (NCP == 10) DMMA accumulators
+  __shared__ double Accs[(NCP == 10) ? BNB * NCP : 1];
   if (useB) {
     // register double buffering: chunk k0+64 is loaded while chunk k0 is multiplied
     constexpr int NBV = BNB * BNB / 256, NDV = (BNB * NCP + 255) / 256;
@@ -460,11 +469,38 @@ __global__ void __launch_bounds__(256) apply_big_kernel(ApplyArgs a) {
       sstore();
       __syncthreads();
       if (k0 + BNB < ld) gload(k0 + BNB);
-      for (int k = 0; k < kc; ++k) {
-        const double bv = Bs[k * BLDS + r];
+      if constexpr (NCP == 10) {
+        // y + 8 probe columns: the 8 probes on the FP64 tensor pipe (warp w: rows 8w..8w+7 as one m8
+        // tile, the probes as one n8 tile, two independent accumulator chains over k), the y column
+        // by DFMA on the same A fragment; each B element is read once per warp from shared memory
+#pragma unroll 4
+        for (int k4 = 0; k4 < kc; k4 += 8) {
+          const int ka = k4 + qc, kb = k4 + 4 + qc;
+          const double aa = Bs[ka * BLDS + 8 * wid + qr], ab = Bs[kb * BLDS + 8 * wid + qr];
+          const double ba = Ds[ka * NCP + 1 + qr], bb = Ds[kb * NCP + 1 + qr];
+          dmma_big(m0[0], m0[1], aa, ba);
+          dmma_big(m1[0], m1[1], ab, bb);
+          my = fma(ab, Ds[kb * NCP], fma(aa, Ds[ka * NCP], my));
+        }
+      } else {
+        for (int k = 0; k < kc; ++k) {
+          const double bv = Bs[k * BLDS + r];
 #pragma unroll
-        for (int q = 0; q < CPT; ++q) acc[q] = fma(bv, Ds[k * NCP + min(cg + 4 * q, NCP - 1)], acc[q]);
+          for (int q = 0; q < CPT; ++q) acc[q] = fma(bv, Ds[k * NCP + min(cg + 4 * q, NCP - 1)], acc[q]);
+        }
       }
+    }
+    if constexpr (NCP == 10) {
+      // fragments -> (row, column) layout of the epilogue through shared memory
+      my += __shfl_xor_sync(0xffffffffu, my, 1);
+      my += __shfl_xor_sync(0xffffffffu, my, 2);
+      const int row = 8 * wid + qr;
+      if (qc == 0) Accs[row * NCP] = my;
+      Accs[row * NCP + 1 + 2 * qc] = m0[0] + m1[0];
+      Accs[row * NCP + 2 + 2 * qc] = m0[1] + m1[1];
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) acc[q] = Accs[r * NCP + min(cg + 4 * q, NCP - 1)];
     }
   }
   // epilogue for (row r, columns cg + 4q)
