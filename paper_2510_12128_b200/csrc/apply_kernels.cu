@@ -89,6 +89,9 @@ __device__ __forceinline__ double2 ldA2(const float* p) {
 // D buffer: column-major [NCP columns][ldp], column 0 = y; ldp = 8 (mod 16) doubles so that the
 // 16-byte B-pair loads D[8t + 2qc + h][col qr] of a quarter warp (rows qr = 2t', 2t'+1) hit all banks
 __host__ __device__ __forceinline__ int pk_ldp(int ld_max) { return ((ld_max + 15) & ~15) + 8; }
+// rows of one Acc buffer: whole 8 x 8-tile block rows, so a cluster whose last block row is one tile
+// high ("thin") can keep the other warps' partial products of that row in the tile rows past ld
+__host__ __device__ __forceinline__ int pk_acc_rows(int ld_max) { return ((ld_max / 8 + 7) / 8) * 64; }
 
 // Shared-memory plan (host and device agree): ring | Dp[2] | Acc[nacc] | Tsm (T rows of every piece,
 // then the per-warp partials of one pass) | Mst (the M' rows of the CTA's pieces, when staged)
@@ -105,7 +108,7 @@ __host__ __device__ inline PackSmem pack_smem(int nstage, int esize, int ld_max,
   p.dp = o;
   o += 2 * ncp * pk_ldp(ld_max) * sizeof(double);
   p.acc = o;                                      // nacc x block products [ld_max][NCP]
-  o += static_cast<size_t>(nacc) * ld_max * ncp * sizeof(double);
+  o += static_cast<size_t>(nacc) * pk_acc_rows(ld_max) * ncp * sizeof(double);
   p.tsm = o;
   o += static_cast<size_t>(seg_max + pne * LRG) * MAXC * sizeof(double);
   o = (o + 127) / 128 * 128;
@@ -148,7 +151,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
   TB* ring = reinterpret_cast<TB*>(smraw + L_.ring);
   double* Dpb = reinterpret_cast<double*>(smraw + L_.dp);   // [2][NCP][ldp]
   double* Accb = reinterpret_cast<double*>(smraw + L_.acc); // nacc x [ld_max][NCP] block products of a piece
-  const int accstride = a.ld_max * NCP;
+  const int accstride = pk_acc_rows(a.ld_max) * NCP;
   double* Tsm = reinterpret_cast<double*>(smraw + L_.tsm);  // T rows [seg_max][MAXC], then partials
   double* Mst = reinterpret_cast<double*>(smraw + L_.mst);  // [seg][lr_nc] staged M' rows (a.mst)
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -307,6 +310,10 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
         for (int n = 0; n < NT8; ++n) { acc[n][0][j] = 0.0; acc[n][1][j] = 0.0; }
       }
       const int ns = pk_ns(mt);
+      // thin last block row (one tile high): its direct products go to the warp owning the tile
+      // COLUMN (warp b: tile (last, 8s + b)), each into its unused accumulator slot of that block row;
+      // the epilogue sums the eight partial rows in warp order
+      const bool thin = NM == 8 && ns > 1 && pk_h(ns - 1, mt) == 1;
       int sb = 0, gb = 0;
       for (int k = 0; k < sd.k0; ++k) { if (++gb == ns) { ++sb; gb = sb; } }
       for (int k = sd.k0; k < sd.k1; ++k) {
@@ -414,7 +421,13 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
               }
               fold(t0, t1, ty, sb * RR + rr);
             }
-            if (wa < h) {                                     // direct: row a = wa
+            if (thin && h == 1 && !diag) {                    // thin row, split by tile column
+              if (wa < w) {
+                const double2 ad = ldA2(tile(wa) + offD);
+                step(d0, d1, dy, ad.x, ad.y, 8 * sb + wa);
+                fold(d0, d1, dy, gb * RR + rr);
+              }
+            } else if (wa < h) {                              // direct: row a = wa
               const int arow = wa;
               const int b_hi = diag ? arow : w - 1;
               for (int bb = 0; bb <= b_hi; ++bb) {
@@ -453,7 +466,7 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
 #pragma unroll
       for (int j = 0; j < MTMAX; ++j) {
         const int mtj = wid + j * PNM;
-        if (mtj < mt) {
+        if (mtj < mt || (thin && mtj < 8 * ns)) {
           double* row = Acc + (8 * mtj + qr) * NCP;
           if (qc == 0) row[0] = accy[j];
 #pragma unroll
@@ -674,6 +687,21 @@ __global__ void __launch_bounds__((NM + PNE + 1) * 32, 8 / NM) apply_packed_kern
     if (useB) {
       mbar_wait_sleep(&accready[q % nacc], static_cast<uint32_t>((q / nacc) & 1), 256);
       if (et == 0 && q < 8) TR(29 + q);
+      {
+        // thin last block row: its rows' products are split over eight partial tile rows
+        const int mtq = ld >> 3, nsq = pk_ns(mtq);
+        if (nsq > 1 && pk_h(nsq - 1, mtq) == 1) {
+          const int r0 = ld - 8;
+          for (int idx = et; idx < 8 * NCP; idx += NET) {
+            const int rr = idx / NCP, c = idx - rr * NCP;
+            double v = Acc[(r0 + rr) * NCP + c];
+#pragma unroll
+            for (int bb = 1; bb < 8; ++bb) v += Acc[(r0 + 8 * bb + rr) * NCP + c];
+            Acc[(r0 + rr) * NCP + c] = v;
+          }
+          bar_epi<PNE>();
+        }
+      }
       // split cluster: publish this part's block products; the last part sums all parts in order
       if (sd.nparts > 1) {
         double* base = a.split_part + sd.spoff + static_cast<int64_t>(sd.part) * ld * NCP;
