@@ -866,7 +866,9 @@ bool plan_packed_apply(int ld_max, int ncol, bool f32, int seg_max, int lr_nc, A
   if (ns < 2) return false;
   a.nacc = nacc;
   a.mst = mst;
-  a.lr_stage_s = 1;                                          // S rows staged (measured 63.7 vs 68.0 us at C3)
+  // S rows through the ring: off — with the thin-row split the stream needs all ring slots from the
+  // start (C3, 3 A/B pairs: 814 vs 798 evals/s, 57.5 vs 58.9 us per apply without the staging)
+  a.lr_stage_s = 0;
   a.slot_tiles = CHUNK;
   a.nstage = ns;
   a.smem = pack_smem(ns, es, ld_max, a.nt8, pne, seg_max, nacc, mst ? mst_need : 0).total;
