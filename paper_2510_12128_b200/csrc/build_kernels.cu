@@ -501,8 +501,9 @@ struct GemmArgs {
 // 8x8 sub-tiles entirely outside the block (ld is a multiple of 8) are skipped.
 constexpr int GLD = 68;
 
+// (not volatile: a pure function of its operands, so the compiler may interleave it with the loads)
 __device__ __forceinline__ void dmma884g(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
                : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
