@@ -244,8 +244,7 @@ __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
     if (a.cond && blockIdx.x == 0 && threadIdx.x == 0) cudaGraphSetConditional(a.cond, 0u);
     return;
   }
-  __shared__ double sred[(NT / 32) * MAXC];
-  __shared__ double outv[MAXC];
+  __shared__ double sred2[(NT / 32) * 2 * NCP];
   __shared__ double cal[NCP], cact[NCP];
   const int t = blockIdx.x;
   const TileDesc td = a.L.tiles[t];
@@ -288,11 +287,24 @@ __global__ void __launch_bounds__(NT, 2) update_kernel(UpdateArgs a) {
       }
     }
   }
-  block_reduce_cols<NCP>(rr, sred, outv);
-  if (threadIdx.x < ncol) a.rr_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
-  __syncthreads();
-  block_reduce_cols<NCP>(sr, sred, outv);
-  if (threadIdx.x < ncol) a.SR_part[t * MAXC + threadIdx.x] = outv[threadIdx.x];
+  // both per-tile partial rows (r^T r and S(r)) in one pass: warp butterflies, one barrier, then the
+  // warps in fixed order (the same sums as two block_reduce_cols passes)
+  {
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+    for (int c = 0; c < NCP; ++c) { rr[c] = warp_sum(rr[c]); sr[c] = warp_sum(sr[c]); }
+    if (lane == 0) {
+#pragma unroll
+      for (int c = 0; c < NCP; ++c) { sred2[wid * 2 * NCP + c] = rr[c]; sred2[wid * 2 * NCP + NCP + c] = sr[c]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < 2 * NCP) {
+      const int v = threadIdx.x, c = v % NCP;
+      double s = 0.0;
+      for (int w = 0; w < NT / 32; ++w) s += sred2[w * 2 * NCP + v];
+      if (c < ncol) (v < NCP ? a.rr_part : a.SR_part)[t * MAXC + c] = s;
+    }
+  }
   if (!a.nofin && last_cta(&st->ticket[FIN_UPDATE])) {
     SPUpdate sp{a.SR_part, a.L.n_tiles == a.L.n_c ? nullptr : a.L.tile0, a.L.n_c, {a.SPbuf[0], a.SPbuf[1]}};
     fin_update_body(st, a.prm, a.rr_part, a.L.n_tiles, ncol, a.beta_hist, a.hist_stride, a.cond, NT / 32, sp);
