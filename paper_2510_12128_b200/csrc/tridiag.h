@@ -7,6 +7,9 @@
 // only part of the eigenvectors Gauss quadrature needs (tau_l in SURVEY §8(a) row A6).
 // Each Givens rotation G acting on rows (i, i+1) of the eigenvector matrix only needs to
 // be applied to row 0, so the cost is O(k^2) instead of O(k^3).
+// Attribution: this is the textbook implicit-shift QL algorithm for symmetric tridiagonal
+// matrices (EISPACK tql1/tql2, Bowdler, Martin, Reinsch & Wilkinson 1968; the same iteration as
+// "tqli" in Numerical Recipes), restated here with the eigenvector update reduced to row 0.
 #pragma once
 #include <cmath>
 
